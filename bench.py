@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Throughput benchmark of the batched simulator step (BASELINE.json metric).
+
+One "step" = one fused step+observe launch over the whole scenario batch
+(Env::step then Env::observe of the stepped state, simcore.cpp:590-609).
+Episodes are 91 steps long (T_log = 92); the state is re-initialised (reset
+kernel, included in the timed region) every 91 steps.  Throughput runs use
+`disable_dones = true` like the reference bench (simcore.cpp:669).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL); each rank simulates
+its own shard of scenarios (weak scaling), no data-path collective; the only
+collective is the all-reduce of the int64 episode-stats vector.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "simulated agent-steps/sec (device-timed) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "agent-steps/s"
+EPISODE = 91  # steps per episode (92 logged states)
+
+# BASELINE.json configs; per-GPU shapes.
+CONFIGS = {
+    "C0": dict(scenarios=64, agents=32, road_points=2048,
+               workload="C0: 64 scenarios x 32 agents, 2k roadgraph points, 91-step rollouts (CPU reference case)"),
+    "C1": dict(scenarios=4096, agents=32, road_points=2048,
+               workload="C1: 1xB200, 4096 scenarios x 32 agents, 2k roadgraph points, top-k 16 agents / 128 "
+                        "polyline pts"),
+    "C3": dict(scenarios=8192, agents=64, road_points=4096,
+               workload="C3 per-GPU shard: 8192 scenarios x 64 agents, 4k roadgraph points"),
+    "C4": dict(scenarios=16384, agents=128, road_points=8192,
+               workload="C4 per-GPU shard at 8 GPUs: 16384 scenarios x 128 agents, 8k roadgraph points"),
+}
+LANES, LANE_VERTICES = 4, 64
+
+
+def scenario_step_bytes(A: int, P: int, R: int = 2 * LANES * LANE_VERTICES, L: int = LANES,
+                        C: int = LANE_VERTICES) -> int:
+    """Algorithmic HBM bytes per scenario-step of the fused step+observe
+    (SURVEY.md §8d): reads state 80, actions 8, agent slices 38(A-1), road
+    10P, route 10R, lane centerlines 32LC, lights/stops/goal 64; writes state
+    80, StepOut 21, observation 7852."""
+    return 80 + 8 + 38 * (A - 1) + 10 * P + 10 * R + 32 * L * C + 64 + 80 + 21 + 7852
+
+
+def hbm_peak() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(cfg_name: str, seed: int) -> dict | None:
+    """Reference simulator (oracle/_ref) timed on this host's cores over a
+    bounded sample of the same workload (rank 0, N=1 only)."""
+    try:
+        from oracle import refpy
+    except Exception:
+        return None
+    if not refpy.available():
+        return None
+    import paper_2312_15122_b200 as z
+    c = CONFIGS[cfg_name]
+    rows = min(1024, c["scenarios"])
+    zsim = z.stress_scenarios(z.StressConfig(count=rows, agents=c["agents"], road_points=c["road_points"]), seed)
+    A, S = z.random_actions(EPISODE, rows, seed=123)
+    threads = os.cpu_count() or 1
+    secs = refpy.bench(zsim, rows, 92, z.SimConfig(disable_dones=True), threads, 0, EPISODE, A, S)
+    return {"value": rows * c["agents"] * EPISODE / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{rows} of the {c['scenarios']} {cfg_name} scenarios x {EPISODE} steps (observe+step), "
+                      f"{threads} per-thread Env shards, oracle/_ref (-O2 -ffp-contract=off)",
+            "seconds": secs}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    import paper_2312_15122_b200 as z
+    from oracle import refpy
+    c = CONFIGS[args.config]
+    B = c["scenarios"]
+    if not refpy.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libzsim_ref.so not built"}))
+        return
+    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=c["agents"], road_points=c["road_points"]), 7)
+    A, S = z.random_actions(EPISODE, B, seed=123)
+    threads = os.cpu_count() or 1
+    secs = refpy.bench(zsim, B, 92, z.SimConfig(disable_dones=True), threads, args.warmup, args.steps, A, S)
+    value = B * c["agents"] * args.steps / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (stress generator seed 7)",
+        "config": {"workload": c["workload"], "scenarios": B, "agents": c["agents"],
+                   "road_points": c["road_points"], "steps_per_episode": EPISODE, "disable_dones": True},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"all {B} scenarios, {args.steps} observe+step iterations, {threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args) -> None:
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2312_15122_b200 as z
+
+    c = CONFIGS[args.config]
+    B, A_, P = c["scenarios"], c["agents"], c["road_points"]
+    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=A_, road_points=P), 7 + rank)
+    env = z.Env(zsim, config=z.SimConfig(disable_dones=True), device=local)
+    del zsim
+    accel, steer = z.random_actions(EPISODE, B, seed=123 + rank)
+    dA = torch.from_numpy(accel).cuda()
+    dS = torch.from_numpy(steer).cuda()
+    s0, s1 = env.device_state(), env.device_state()
+    so, ob = env.device_stepout(), env.device_obs()
+    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    k_state = {"k": 0}
+
+    def one_step(cur, nxt, events=None):
+        k = k_state["k"]
+        t = k % EPISODE
+        if t == 0:
+            env.reset_device(42, cur, stream)
+        if events is not None:
+            events[0].record(stream)
+        env.step_observe_device(cur, dA[t].data_ptr(), dS[t].data_ptr(), nxt, so, ob, stream)
+        if events is not None:
+            events[1].record(stream)
+        k_state["k"] = k + 1
+        return nxt, cur
+
+    cur, nxt = s0, s1
+    for _ in range(args.warmup):
+        cur, nxt = one_step(cur, nxt)
+    env.check_errors(stream)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)  # let the sampler start before the timed region
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    resets = 0
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(args.steps):
+        resets += 1 if k_state["k"] % EPISODE == 0 else 0
+        cur, nxt = one_step(cur, nxt, ev[i])
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if dist:
+        dist.barrier()
+    elapsed_ms = start.elapsed_time(end)
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    env.check_errors(stream)
+    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    env.episode_stats(cur, stats.data_ptr(), stream)
+    if dist:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM)  # the one NCCL collective
+    elapsed_ms = float(t_max.item())
+    agent_steps = B * A_ * args.steps * world
+    value = agent_steps / (elapsed_ms / 1e3)
+
+    # ---- e2e through the host-vector API (the drop-in overloads) ----
+    e2e = None
+    if not args.no_e2e:
+        st_h, nx_h = env.new_state(pinned=True), env.new_state(pinned=True)
+        so_h, ob_h = env.new_stepout(pinned=True), env.new_obs(pinned=True)
+        env.init_state(42, out=st_h)
+        ke = min(args.steps, EPISODE)
+        for t in range(min(3, ke)):
+            env.step(st_h, accel[t], steer[t], nx_h, so_h)
+            env.observe(nx_h, ob_h)
+        env.init_state(42, out=st_h)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for t in range(ke):
+            env.step(st_h, accel[t], steer[t], nx_h, so_h)
+            env.observe(nx_h, ob_h)
+            st_h, nx_h = nx_h, st_h
+        t1 = time.perf_counter()
+        e_s = torch.tensor([t1 - t0], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(e_s, op=dist.ReduceOp.MAX)
+        sb, sob, obb = env.layout
+        h2d = 2 * sb + 8 * B  # step uploads state + actions, observe uploads state
+        d2h = sb + sob + obb
+        e2e = {"value": B * A_ * ke * world / float(e_s.item()), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": ke,
+               "path": "Env.step + Env.observe host-vector API (zsim_step_host / zsim_observe_host), pinned buffers"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    per_scen = scenario_step_bytes(A_, P)
+    peak, peak_src = hbm_peak()
+    achieved = per_scen * B / (kern_ms / 1e3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():
+        try:
+            tj = json.loads(tp.read_text())
+            if tj.get("config") == args.config:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: stress generator (seed 7+rank), random actions (splitmix64 seed 123+rank)",
+        "config": {"workload": c["workload"], "scenarios_per_gpu": B, "agents": A_, "road_points": P,
+                   "route_points": 2 * LANES * LANE_VERTICES, "lanes": LANES, "lane_vertices": LANE_VERTICES,
+                   "steps_per_episode": EPISODE, "disable_dones": True,
+                   "l2": f"inputs larger than L2 (static pack {env.info.static_bytes / 1e6:.0f} MB per GPU)",
+                   "parallelism": f"scenario-sharded x{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "bytes_per_scenario_step": per_scen,
+                     "kernel": "k_step_observe<true,true>", "kernel_ms": kern_ms, "peak_source": peak_src},
+        "gpu_launches": args.steps + resets,
+        "scenario_steps_per_s": B * args.steps * world / (elapsed_ms / 1e3),
+        "episode_stats": stats.cpu().tolist(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if clk:
+        line["clocks"] = clk
+    if world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(args.config, 7)
+        if cb:
+            line["cpu_baseline"] = cb
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5 * EPISODE)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

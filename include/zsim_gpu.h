@@ -1,0 +1,280 @@
+/*
+ * zsim_gpu.h -- C-ABI of the B200-native batched driving-simulator step.
+ *
+ * This is the drop-in boundary for the reference's `zsim::sim::Env`
+ * (/root/reference/proj/src/core/simcore.hpp:191-245).  The reference builds a
+ * hidden-visibility C-API shared library `zsim` from capi/zsim_capi.cpp
+ * (proj/src/CMakeLists.txt:24-27) whose sources are not shipped, so the entry
+ * points below are designed fresh: plain pointers and sizes, no C++ or torch
+ * types, CUDA streams passed as `void*` (a `cudaStream_t`).  Every entry point
+ * cites the reference interface it replaces.
+ *
+ * Layouts:
+ *   - state   : SoA over the batch (SimStateBatch, simcore.hpp:107-121); the
+ *               reference's AoS EgoState (dynamics.hpp:10-16) is split into
+ *               x/y/heading/v/steering arrays.
+ *   - stepout : SoA (StepOut, simcore.hpp:123-131); `event` is DoneReason u8.
+ *   - obs     : row-major [B][slot][feat] f32 per modality, byte-identical to
+ *               ObservationBatch (simcore.hpp:76-103).
+ *   - actions : int32 [B] accel / steer bin indices (Env::step,
+ *               simcore.hpp:215-216).
+ *
+ * Errors: every function returns a status.  Codes 1..4 follow the order of
+ * zsim::ErrorKind (common.hpp:13); 5 is a CUDA failure.  zsim_last_error()
+ * returns a thread-local message for the last failing call on this thread.
+ */
+#ifndef ZSIM_GPU_H_
+#define ZSIM_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define ZSIM_API __attribute__((visibility("default")))
+#else
+#define ZSIM_API
+#endif
+
+#define ZSIM_ABI_VERSION 1
+
+enum zsim_status {
+    ZSIM_OK = 0,
+    ZSIM_INVALID_ARGUMENT = 1, /* ErrorKind::invalid_argument */
+    ZSIM_CONFIG = 2,           /* ErrorKind::config */
+    ZSIM_IO = 3,               /* ErrorKind::io */
+    ZSIM_RUNTIME = 4,          /* ErrorKind::runtime */
+    ZSIM_CUDA = 5
+};
+
+/* DoneReason (simcore.hpp:47-54). */
+enum zsim_done_reason {
+    ZSIM_REASON_NONE = 0,
+    ZSIM_REASON_COLLISION = 1,
+    ZSIM_REASON_OFF_ROUTE = 2,
+    ZSIM_REASON_RED_LIGHT = 3,
+    ZSIM_REASON_STOP_LINE = 4,
+    ZSIM_REASON_GOAL_REACHED = 5
+};
+
+/* SimConfig (simcore.hpp:14-45) + dyn::Limits (dynamics.hpp:18-21). */
+typedef struct zsim_sim_config {
+    double wheelbase;
+    double ego_length;
+    double ego_width;
+    double ego_center_offset;
+    double delta_max;
+    double v_min;
+    double goal_radius;
+    double footprint_margin;
+    double stop_cross_speed;
+    double stop_zone;
+    double stop_slow_speed;
+    int32_t disable_dones;
+    int32_t n_agents;
+    int32_t n_road;
+    int32_t n_route;
+    double w_progress;
+    double w_speed;
+    double w_lat;
+    double w_lon;
+    double terminal_penalty;
+    double feature_radius;
+    int32_t threads; /* accepted for API parity; the device ignores it */
+    int32_t reserved;
+} zsim_sim_config;
+
+/* SimStateBatch (simcore.hpp:107-121), SoA.  The same struct describes host
+ * buffers and device buffers; `stopped_flags` has env->total_stop_lines
+ * entries, every other array has `batch` entries. */
+typedef struct zsim_state_view {
+    double* x;
+    double* y;
+    double* heading;
+    double* v;
+    double* steering;
+    int32_t* t;
+    uint8_t* done;
+    uint8_t* reason;
+    uint64_t* rng;
+    double* proj_s;
+    double* proj_d;
+    uint8_t* proj_in_corridor;
+    uint8_t* events;
+    uint8_t* stopped_flags;
+} zsim_state_view;
+
+/* StepOut (simcore.hpp:123-131). */
+typedef struct zsim_stepout_view {
+    float* reward;
+    uint8_t* event;
+    float* s;
+    float* a_lat;
+    float* a_lon;
+    float* v;
+} zsim_stepout_view;
+
+/* ObservationBatch (simcore.hpp:76-103): active [B][9], agents [B][n_agents][6],
+ * road [B][n_road][12], route [B][n_route][5], value_only [B][2]. */
+typedef struct zsim_obs_view {
+    float* active;
+    float* agents;
+    float* road;
+    float* route;
+    float* value_only;
+} zsim_obs_view;
+
+/* Shape summary of an environment (Env accessors, simcore.hpp:200-209). */
+typedef struct zsim_env_info {
+    int32_t batch;            /* B = ScenarioBatch::batch */
+    int32_t horizon;          /* ScenarioBatch::horizon (padded T) */
+    double dt;                /* ScenarioBatch::dt */
+    int32_t total_stop_lines; /* length of stopped_flags */
+    int32_t zero_accel_idx;   /* ActionTable::nearest_accel(0) */
+    int32_t zero_steer_idx;   /* ActionTable::nearest_steer(0) */
+    int32_t num_accel;
+    int32_t num_steer;
+    /* per-batch padded capacities of the device pack */
+    int32_t cap_steps, cap_agents, cap_road, cap_route, cap_lanes, cap_vertices, cap_lights, cap_stops;
+    int32_t device;
+    uint64_t static_bytes; /* device bytes of the immutable scenario pack */
+} zsim_env_info;
+
+typedef struct zsim_env zsim_env;
+
+ZSIM_API int zsim_abi_version(void);
+ZSIM_API const char* zsim_last_error(void);
+
+/* SimConfig{} defaults (simcore.hpp:14-45). */
+ZSIM_API int zsim_sim_config_defaults(zsim_sim_config* cfg);
+
+/* Env::Env(shared_ptr<const ScenarioBatch>, SimConfig, ActionTable)
+ * (simcore.hpp:193-194, simcore.cpp:203-233), with the batch given the way the
+ * reference builds it: load_batch(Dataset(path), indices, horizon)
+ * (scenario_io.cpp:439-445) over an in-memory ZSIM container image
+ * (scenario.hpp:97-104, scenario_io.cpp:319-394).  `indices` may be NULL to
+ * take every record in order.  Bins NULL => ActionTable::defaults()
+ * (dynamics.cpp:21-26).  Route frames, stop/light s, goal_s, initial_s,
+ * logged_progress and route border points are staged on the host in fp64 with
+ * the reference's operation order, then uploaded once. */
+ZSIM_API int zsim_env_create(const uint8_t* zsim_file, size_t nbytes, const int64_t* indices, int32_t n_indices,
+                             int32_t horizon, const zsim_sim_config* cfg, const double* accel_bins, int32_t n_accel,
+                             const double* steer_bins, int32_t n_steer, int32_t device, zsim_env** out);
+ZSIM_API int zsim_env_destroy(zsim_env* env);
+ZSIM_API int zsim_env_get_info(const zsim_env* env, zsim_env_info* out);
+/* Env::goal_s / initial_s / logged_progress (simcore.hpp:207-209): host arrays of B doubles (any may be NULL). */
+ZSIM_API int zsim_env_get_scalars(const zsim_env* env, double* goal_s, double* initial_s, double* logged_progress);
+
+/* Device buffers (caller-owned; one contiguous allocation per call). */
+ZSIM_API int zsim_state_alloc(zsim_env* env, zsim_state_view* dev_out);
+ZSIM_API int zsim_state_free(zsim_env* env, zsim_state_view* dev);
+ZSIM_API int zsim_stepout_alloc(zsim_env* env, zsim_stepout_view* dev_out);
+ZSIM_API int zsim_stepout_free(zsim_env* env, zsim_stepout_view* dev);
+ZSIM_API int zsim_obs_alloc(zsim_env* env, zsim_obs_view* dev_out);
+ZSIM_API int zsim_obs_free(zsim_env* env, zsim_obs_view* dev);
+
+/* Blob layouts: every view the library allocates is carved from one
+ * contiguous block.  Carving caller memory (e.g. pinned host memory from
+ * zsim_host_alloc) with the same layout lets a copy between the two move as a
+ * single DMA. */
+ZSIM_API int zsim_layout_bytes(const zsim_env* env, size_t* state_bytes, size_t* stepout_bytes, size_t* obs_bytes);
+ZSIM_API int zsim_state_carve(const zsim_env* env, void* base, zsim_state_view* out);
+ZSIM_API int zsim_stepout_carve(const zsim_env* env, void* base, zsim_stepout_view* out);
+ZSIM_API int zsim_obs_carve(const zsim_env* env, void* base, zsim_obs_view* out);
+/* Page-locked host memory (cudaHostAlloc) for the host-vector path. */
+ZSIM_API int zsim_host_alloc(size_t bytes, void** out);
+ZSIM_API int zsim_host_free(void* p);
+
+/* Copies between views; `dir` 0 = host->device, 1 = device->host,
+ * 2 = device->device.  Asynchronous on `stream` (host buffers should be pinned
+ * for overlap). */
+ZSIM_API int zsim_state_copy(zsim_env* env, const zsim_state_view* dst, const zsim_state_view* src, int32_t dir,
+                             void* stream);
+ZSIM_API int zsim_stepout_copy(zsim_env* env, const zsim_stepout_view* dst, const zsim_stepout_view* src,
+                               int32_t dir, void* stream);
+ZSIM_API int zsim_obs_copy(zsim_env* env, const zsim_obs_view* dst, const zsim_obs_view* src, int32_t dir,
+                           void* stream);
+
+/* ---- device fast path (all pointers device pointers, stream-ordered) ---- */
+
+/* Env::init_state(seed) (simcore.cpp:237-276). */
+ZSIM_API int zsim_reset(zsim_env* env, uint64_t seed, const zsim_state_view* out, void* stream);
+
+/* Env::step(state, accel_idx, steer_idx, next, out) (simcore.cpp:406-421).
+ * `out` may alias `in`.  Out-of-range action indices (dynamics.cpp:66-71) set
+ * the env's device error word and leave that row unchanged; the error is
+ * reported by zsim_check_errors(). */
+ZSIM_API int zsim_step(zsim_env* env, const zsim_state_view* in, const int32_t* accel_idx, const int32_t* steer_idx,
+                       const zsim_state_view* out, const zsim_stepout_view* so, void* stream);
+
+/* Env::observe(state, obs) (simcore.cpp:540-552). */
+ZSIM_API int zsim_observe(zsim_env* env, const zsim_state_view* in, const zsim_obs_view* obs, void* stream);
+
+/* Fused Env::step followed by Env::observe of the stepped state, one kernel
+ * (the rollout loop body, simcore.cpp:590-609). */
+ZSIM_API int zsim_step_observe(zsim_env* env, const zsim_state_view* in, const int32_t* accel_idx,
+                               const int32_t* steer_idx, const zsim_state_view* out, const zsim_stepout_view* so,
+                               const zsim_obs_view* obs, void* stream);
+
+/* Optional device buffer of int32 [B][n_agents + n_road + n_route] that the
+ * observe kernels fill with the selected candidate indices (agent index into
+ * Scenario::agents, flat road-feature point index in nearest_features order
+ * (roads.cpp:220-229), route border point index (simcore.cpp:181-200)); -1 for
+ * empty slots.  NULL disables.  Used by the parity suite. */
+ZSIM_API int zsim_set_debug_topk(zsim_env* env, int32_t* dev_idx);
+
+/* Synchronises `stream`, reads and clears the device error word.  Returns
+ * ZSIM_INVALID_ARGUMENT ("action index out of range") if any step since the
+ * last check saw a bad action index. */
+ZSIM_API int zsim_check_errors(zsim_env* env, void* stream);
+
+/* Episode-stats vector of a state (the counts behind
+ * metrics::Aggregate, metrics.hpp:56-69): int64[8] = {rows, done rows,
+ * rows with latched collision, off_route, red_light, stop_line, goal_reached
+ * event bits, sum over rows of (proj_s - initial_s) in micrometres}.  Integer
+ * so a cross-GPU ncclAllReduce(sum) is exact.  `out_dev` is device memory. */
+#define ZSIM_STATS_LEN 8
+ZSIM_API int zsim_episode_stats(zsim_env* env, const zsim_state_view* state, int64_t* out_dev, void* stream);
+
+/* ---- host-vector path (the drop-in overloads; synchronous) ---- */
+
+/* Env::init_state(seed) into host buffers. */
+ZSIM_API int zsim_reset_host(zsim_env* env, uint64_t seed, const zsim_state_view* out_host);
+/* Env::step with host vectors: validates shapes/indices first (throws
+ * invalid_argument like simcore.cpp:409-411 / dynamics.cpp:67-69), copies
+ * state and actions in, runs the step kernel, copies next state and StepOut out. */
+ZSIM_API int zsim_step_host(zsim_env* env, const zsim_state_view* in_host, const int32_t* accel_idx,
+                            const int32_t* steer_idx, const zsim_state_view* out_host,
+                            const zsim_stepout_view* so_host);
+/* Env::observe with host vectors. */
+ZSIM_API int zsim_observe_host(zsim_env* env, const zsim_state_view* in_host, const zsim_obs_view* obs_host);
+
+/* ---- synthetic stress scenarios ---- */
+
+typedef struct zsim_stress_config {
+    int32_t count;          /* scenarios */
+    int32_t num_steps;      /* logged states per scenario (92) */
+    int32_t agents;         /* A: total agents incl. the ego => A-1 logged agents */
+    int32_t road_points;    /* P: total road-feature points */
+    int32_t lanes;          /* route lanes (4) */
+    int32_t lane_vertices;  /* vertices per lane border (64) */
+    double dt;              /* 0.1 */
+    double speed_limit;     /* 10 m/s */
+    double lane_width;      /* 3.5 m */
+} zsim_stress_config;
+
+ZSIM_API int zsim_stress_config_defaults(zsim_stress_config* cfg);
+/* Generates `cfg->count` scenarios deterministically from `seed`
+ * (per-scenario streams Rng(seed).split(i), common.hpp:47-50) and returns a
+ * ZSIM container image in a malloc'd buffer (free with zsim_free_buffer). */
+ZSIM_API int zsim_stress_generate(const zsim_stress_config* cfg, uint64_t seed, uint8_t** out_buf, size_t* out_len);
+ZSIM_API void zsim_free_buffer(void* buf);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ZSIM_GPU_H_ */

@@ -1,0 +1,93 @@
+"""Build recipe for the parity oracles (TEST INFRASTRUCTURE).
+
+* ``oracle/_ref/libzsim_ref.so`` -- the reference simulator compiled IN PLACE
+  from ``/root/reference/proj/src/core/*.cpp`` (never copied) plus our
+  ``ref_shim.cpp``.  Flags ``-std=c++20 -O2 -ffp-contract=off``: the
+  reference's own default ``-march=native`` build contracts FMAs and changes
+  output bits, so the oracle pins the uncontracted arithmetic
+  that the device (``-fmad=false``) reproduces.  Only built where
+  ``/root/reference`` exists; the built ``.so`` travels to the GPU box with the
+  repo snapshot (``oracle/_ref/`` is git-ignored, not gpurun-ignored).
+* ``oracle/_build/libzsim_oracle.so`` -- the plain-C restatement
+  ``oracle/zsim_oracle.c`` (always buildable, needs only gcc).
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+REF_ROOT = Path(os.environ.get("ZSIM_REFERENCE_DIR", "/root/reference"))
+REF_SRC = REF_ROOT / "proj" / "src"
+REF_OUT = HERE / "_ref" / "libzsim_ref.so"
+PORT_OUT = HERE / "_build" / "libzsim_oracle.so"
+NLOHMANN = Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
+
+REF_UNITS = ["common", "config", "geometry", "dynamics", "roads", "scenario_io", "scenario_gen", "simcore",
+             "metrics"]
+CXX = os.environ.get("CXX", "g++")
+
+
+def _run(cmd: list[str]) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+
+
+def reference_available() -> bool:
+    return (REF_SRC / "core" / "simcore.cpp").exists()
+
+
+def build_ref(force: bool = False) -> Path | None:
+    """Compile the reference + shim into oracle/_ref (None if the reference is absent)."""
+    if not reference_available():
+        return REF_OUT if REF_OUT.exists() else None
+    srcs = [REF_SRC / "core" / f"{u}.cpp" for u in REF_UNITS] + [HERE / "ref_shim.cpp"]
+    if not force and REF_OUT.exists():
+        t = REF_OUT.stat().st_mtime
+        if all(s.stat().st_mtime <= t for s in srcs):
+            return REF_OUT
+    objdir = HERE / "_ref" / "obj"
+    objdir.mkdir(parents=True, exist_ok=True)
+    flags = ["-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-I", str(REF_SRC), "-I", str(NLOHMANN),
+             "-I", str(HERE.parent / "include")]
+    jobs, objs = [], []
+    for s in srcs:
+        o = objdir / (s.stem + ".o")
+        objs.append(str(o))
+        jobs.append([CXX, *flags, "-c", str(s), "-o", str(o)])
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 2) as ex:
+        list(ex.map(_run, jobs))
+    tmp = REF_OUT.with_suffix(".tmp")
+    _run([CXX, "-shared", "-o", str(tmp), *objs, "-lpthread"])
+    os.replace(tmp, REF_OUT)
+    return REF_OUT
+
+
+def build_port(force: bool = False) -> Path | None:
+    """Compile the plain-C restatement (None if its source is not present yet)."""
+    src = HERE / "zsim_oracle.c"
+    if not src.exists():
+        return None
+    if not force and PORT_OUT.exists() and src.stat().st_mtime <= PORT_OUT.stat().st_mtime and \
+            (HERE / "zsim_oracle.h").stat().st_mtime <= PORT_OUT.stat().st_mtime:
+        return PORT_OUT
+    PORT_OUT.parent.mkdir(exist_ok=True)
+    tmp = PORT_OUT.with_suffix(".tmp")
+    _run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-I", str(HERE.parent / "include"),
+          "-o", str(tmp), str(src), "-lm"])
+    os.replace(tmp, PORT_OUT)
+    return PORT_OUT
+
+
+def build(force: bool = False) -> None:
+    build_port(force)
+    build_ref(force)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)
+    print(REF_OUT if REF_OUT.exists() else "(no reference)", PORT_OUT if PORT_OUT.exists() else "(no port)")

@@ -1,0 +1,217 @@
+"""TEST INFRASTRUCTURE: Python handle on the reference simulator compiled in
+place (oracle/_ref/libzsim_ref.so, built by oracle/build_oracle.py from
+/root/reference/proj/src/core without copying).  Mirrors the product's
+host API so parity tests read the same on both sides.  Never imported by the
+product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+from paper_2312_15122_b200._abi import ObsView, SimConfigC, StateView, StepOutView
+from paper_2312_15122_b200.env import ObservationBatch, SimConfig, SimStateBatch, StepOut, _ptr
+
+HERE = Path(__file__).resolve().parent
+REF_LIB = HERE / "_ref" / "libzsim_ref.so"
+
+_P = C.c_void_p
+_SIGS = {
+    "zref_last_error": (C.c_char_p, []),
+    "zref_env_create": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.POINTER(SimConfigC),
+                                  C.POINTER(_P)]),
+    "zref_env_destroy": (None, [_P]),
+    "zref_env_info": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "zref_scalars": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "zref_init_state": (C.c_int, [_P, C.c_uint64, C.POINTER(StateView)]),
+    "zref_step": (C.c_int, [_P, C.POINTER(StateView), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                            C.POINTER(StateView), C.POINTER(StepOutView)]),
+    "zref_observe": (C.c_int, [_P, C.POINTER(StateView), C.POINTER(ObsView)]),
+    "zref_validate": (C.c_int, [C.c_char_p, C.c_int64, C.c_char_p, C.c_int32]),
+    "zref_generate": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_char_p]),
+    "zref_recover_actions": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                       C.c_int32, C.POINTER(C.c_int32)]),
+    "zref_aggregate": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                 C.POINTER(C.c_float), C.POINTER(C.c_uint8), C.POINTER(C.c_uint8),
+                                 C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_double)]),
+    "zref_bench": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(SimConfigC), C.c_int32, C.c_int32,
+                             C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_uint64,
+                             C.POINTER(C.c_double)]),
+}
+
+_lib = None
+
+
+def available() -> bool:
+    return REF_LIB.exists()
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not REF_LIB.exists():
+            raise FileNotFoundError(f"{REF_LIB} not built (needs /root/reference; run oracle/build_oracle.py)")
+        _lib = C.CDLL(str(REF_LIB))
+        for n, (r, a) in _SIGS.items():
+            f = getattr(_lib, n)
+            f.restype = r
+            f.argtypes = a
+    return _lib
+
+
+class RefError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def _check(code: int) -> None:
+    if code != 0:
+        raise RefError(code, lib().zref_last_error().decode(errors="replace"))
+
+
+def _as_path(zsim) -> tuple[str, object]:
+    """Reference Dataset reads files; spill in-memory images to a temp file."""
+    if isinstance(zsim, (str, os.PathLike)):
+        return str(zsim), None
+    tf = tempfile.NamedTemporaryFile(suffix=".zsim", delete=False)
+    tf.write(bytes(zsim))
+    tf.close()
+    return tf.name, tf
+
+
+class RefEnv:
+    """The reference zsim::sim::Env (simcore.hpp:191-245) over the same inputs."""
+
+    def __init__(self, zsim, indices=None, horizon: int = 0, config: SimConfig | None = None):
+        self._path, self._tmp = _as_path(zsim)
+        self._config = config or SimConfig()
+        cfg = self._config.to_c()
+        idx, n = None, 0
+        if indices is not None:
+            self._idx = np.ascontiguousarray(np.asarray(indices, dtype=np.int64))
+            idx, n = self._idx.ctypes.data_as(C.POINTER(C.c_int64)), int(self._idx.size)
+        h = C.c_void_p()
+        _check(lib().zref_env_create(self._path.encode(), idx, n, int(horizon), C.byref(cfg), C.byref(h)))
+        self.handle = h.value
+        b, hz, ts = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().zref_env_info(self.handle, C.byref(b), C.byref(hz), C.byref(ts)))
+        self.batch, self.horizon, self.total_stop_lines = b.value, hz.value, ts.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                lib().zref_env_destroy(self.handle)
+                self.handle = None
+            if getattr(self, "_tmp", None) is not None:
+                os.unlink(self._path)
+                self._tmp = None
+        except Exception:
+            pass
+
+    def batch_size(self) -> int:
+        return self.batch
+
+    def scalars(self):
+        g, i, l = np.zeros(self.batch), np.zeros(self.batch), np.zeros(self.batch)
+        _check(lib().zref_scalars(self.handle, _ptr(g, C.c_double), _ptr(i, C.c_double), _ptr(l, C.c_double)))
+        return g, i, l
+
+    def new_state(self) -> SimStateBatch:
+        return SimStateBatch(self.batch, self.total_stop_lines)
+
+    def init_state(self, seed: int) -> SimStateBatch:
+        st = self.new_state()
+        v = st.view()
+        _check(lib().zref_init_state(self.handle, C.c_uint64(seed), C.byref(v)))
+        return st
+
+    def step(self, state: SimStateBatch, accel, steer):
+        a = np.ascontiguousarray(accel, dtype=np.int32)
+        s = np.ascontiguousarray(steer, dtype=np.int32)
+        nxt, so = self.new_state(), StepOut(self.batch)
+        vi, vo, vs = state.view(), nxt.view(), so.view()
+        _check(lib().zref_step(self.handle, C.byref(vi), _ptr(a, C.c_int32), _ptr(s, C.c_int32), C.byref(vo),
+                               C.byref(vs)))
+        return nxt, so
+
+    def observe(self, state: SimStateBatch) -> ObservationBatch:
+        c = self._config
+        ob = ObservationBatch(self.batch, c.n_agents, c.n_road, c.n_route)
+        vi, vo = state.view(), ob.view()
+        _check(lib().zref_observe(self.handle, C.byref(vi), C.byref(vo)))
+        return ob
+
+
+def validate(zsim, index: int) -> str:
+    path, tmp = _as_path(zsim)
+    try:
+        buf = C.create_string_buffer(1024)
+        _check(lib().zref_validate(path.encode(), int(index), buf, 1024))
+        return buf.value.decode()
+    finally:
+        if tmp is not None:
+            os.unlink(path)
+
+
+def generate(count: int, seed: int, num_steps: int = 92, density: float = 0.5) -> bytes:
+    """Reference generate_synthetic + write_file -> ZSIM bytes."""
+    with tempfile.TemporaryDirectory() as d:
+        p = Path(d) / "gen.zsim"
+        _check(lib().zref_generate(int(count), int(num_steps), float(density), C.c_uint64(seed), str(p).encode()))
+        return p.read_bytes()
+
+
+def recover_actions(zsim, index: int):
+    path, tmp = _as_path(zsim)
+    try:
+        cap = 4096
+        a = np.zeros(cap, np.int32)
+        s = np.zeros(cap, np.int32)
+        n = C.c_int32()
+        _check(lib().zref_recover_actions(path.encode(), int(index), _ptr(a, C.c_int32), _ptr(s, C.c_int32), cap,
+                                          C.byref(n)))
+        return a[:n.value].copy(), s[:n.value].copy()
+    finally:
+        if tmp is not None:
+            os.unlink(path)
+
+
+def aggregate(s, a_lat, a_lon, mask, events, initial_s, logged_progress, dt: float) -> np.ndarray:
+    """metrics::score_episode + aggregate over recorded [B][T] traces (12 doubles)."""
+    B, T = s.shape
+    out = np.zeros(12)
+    arrs = [np.ascontiguousarray(x, dtype=np.float32) for x in (s, a_lat, a_lon)]
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    ev = np.ascontiguousarray(events, dtype=np.uint8)
+    i0 = np.ascontiguousarray(initial_s, dtype=np.float32)
+    lp = np.ascontiguousarray(logged_progress, dtype=np.float32)
+    _check(lib().zref_aggregate(B, T, float(dt), *[_ptr(x, C.c_float) for x in arrs], _ptr(m, C.c_uint8),
+                                _ptr(ev, C.c_uint8), _ptr(i0, C.c_float), _ptr(lp, C.c_float),
+                                _ptr(out, C.c_double)))
+    return out
+
+
+def bench(zsim, n_rows: int, horizon: int, config: SimConfig, threads: int, warmup: int, steps: int, accel,
+          steer, seed: int = 42) -> float:
+    """Wall seconds of `steps` timed observe+step iterations over `n_rows` rows
+    on `threads` shards; `accel`/`steer` are [episode_len][n_rows] and the
+    state is re-initialised every episode_len steps."""
+    path, tmp = _as_path(zsim)
+    try:
+        a = np.ascontiguousarray(accel, dtype=np.int32)
+        s = np.ascontiguousarray(steer, dtype=np.int32)
+        assert a.shape[1] == n_rows
+        cfg = config.to_c()
+        out = C.c_double()
+        _check(lib().zref_bench(path.encode(), int(n_rows), int(horizon), C.byref(cfg), int(threads), int(warmup),
+                                int(steps), int(a.shape[0]), _ptr(a, C.c_int32), _ptr(s, C.c_int32),
+                                C.c_uint64(seed), C.byref(out)))
+        return out.value
+    finally:
+        if tmp is not None:
+            os.unlink(path)

@@ -1,0 +1,14 @@
+"""B200-native batched driving-simulator step (arXiv 2312.15122 reference path).
+
+The product is the native library ``libzsim_gpu.so`` (sm_100a kernels behind
+the C-ABI of ``include/zsim_gpu.h``); this package is its host-side mirror of
+the reference's ``zsim::sim::Env`` API.  Importing it loads the native library
+and fails loudly when it is missing -- there is no CPU fallback.
+"""
+from ._abi import ZsimError, lib  # noqa: F401
+from .env import (DONE_REASONS, DeviceObs, DeviceState, DeviceStepOut, Env, ObservationBatch,  # noqa: F401
+                  SimConfig, SimStateBatch, StepOut, StressConfig, event_bit, random_actions, stress_scenarios)
+
+__all__ = ["Env", "SimConfig", "SimStateBatch", "StepOut", "ObservationBatch", "DeviceState", "DeviceStepOut",
+           "DeviceObs", "StressConfig", "stress_scenarios", "random_actions", "ZsimError", "DONE_REASONS",
+           "event_bit", "lib"]

@@ -1,0 +1,81 @@
+"""Build the native library ``libzsim_gpu.so`` in-tree for sm_100a.
+
+Host C++ (ZSIM codec, staging, stress generator) is compiled with
+``-ffp-contract=off`` and every CUDA translation unit with ``-fmad=false`` so
+the fp64 arithmetic rounds exactly like the reference built without FMA
+contraction.  The CUDA runtime is linked statically so the
+library does not depend on which libcudart torch happens to ship.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+OUT = PKG / "libzsim_gpu.so"
+BUILD = PKG / "_build"
+
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",
+              "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden", *ARCH]
+CXX = os.environ.get("CXX", "g++")
+CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-fvisibility=hidden", "-Wall"]
+
+CU_SOURCES = ["zsim_kernels.cu", "zsim_capi.cu"]
+CXX_SOURCES = ["zsim_scenario.cpp", "zsim_stressgen.cpp"]
+
+
+def _sources() -> list[Path]:
+    return [CSRC / s for s in CU_SOURCES + CXX_SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + [
+        PKG.parent / "include" / "zsim_gpu.h"]
+
+
+def _stale() -> bool:
+    if not OUT.exists():
+        return True
+    t = OUT.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in _sources())
+
+
+def _run(cmd: list[str]) -> str:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return r.stdout + r.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile libzsim_gpu.so (no-op when up to date)."""
+    if not force and not _stale():
+        return OUT
+    BUILD.mkdir(exist_ok=True)
+    jobs = []
+    for s in CU_SOURCES:
+        o = BUILD / (s + ".o")
+        extra = ["-Xptxas", "-v"] if verbose else []
+        jobs.append([NVCC, *CUDA_FLAGS, *extra, "-I", str(PKG.parent / "include"), "-c", str(CSRC / s), "-o", str(o)])
+    for s in CXX_SOURCES:
+        o = BUILD / (s + ".o")
+        jobs.append([CXX, *CXX_FLAGS, "-I", str(PKG.parent / "include"), "-c", str(CSRC / s), "-o", str(o)])
+    logs = []
+    with cf.ThreadPoolExecutor(max_workers=min(4, os.cpu_count() or 1)) as ex:
+        for log in ex.map(_run, jobs):
+            logs.append(log)
+    objs = [str(BUILD / (s + ".o")) for s in CU_SOURCES + CXX_SOURCES]
+    tmp = OUT.with_suffix(".so.tmp")
+    _run([NVCC, "-shared", *ARCH, "-Xcompiler", "-fPIC", "-o", str(tmp), *objs, "-lpthread"])
+    os.replace(tmp, OUT)
+    if verbose:
+        sys.stderr.write("\n".join(l for l in logs if l.strip()) + "\n")
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(OUT)

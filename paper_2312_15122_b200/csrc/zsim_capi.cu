@@ -1,0 +1,1046 @@
+// zsim_capi.cu -- the extern "C" boundary (include/zsim_gpu.h): environment
+// staging, device buffers, copies and kernel launches.  Host C++.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/zsim_gpu.h"
+#include "zsim_geom.cuh"
+#include "zsim_kernels.cuh"
+#include "zsim_pack.cuh"
+#include "zsim_scenario.hpp"
+
+namespace zs {
+std::string stress_generate(const zsim_stress_config& cfg, uint64_t seed);
+}
+
+using zs::Err;
+using zs::Error;
+using zs::raise;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise(Err::cuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return ZSIM_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return int(e.kind);
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return ZSIM_RUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return ZSIM_RUNTIME;
+    }
+}
+
+size_t al(size_t v) { return (v + 255) / 256 * 256; }
+
+// Layout of a SoA block carved from one allocation.
+struct StateLayout {
+    size_t off[14];
+    size_t bytes;
+};
+
+StateLayout state_layout(int B, int S) {
+    const size_t sz[14] = {8, 8, 8, 8, 8, 4, 1, 1, 8, 8, 8, 1, 1, 1};
+    StateLayout L;
+    size_t o = 0;
+    for (int i = 0; i < 14; ++i) {
+        L.off[i] = o;
+        o += al(sz[i] * size_t(i == 13 ? std::max(S, 1) : B));
+    }
+    L.bytes = o;
+    return L;
+}
+
+void carve_state(unsigned char* base, const StateLayout& L, zsim_state_view* v) {
+    v->x = reinterpret_cast<double*>(base + L.off[0]);
+    v->y = reinterpret_cast<double*>(base + L.off[1]);
+    v->heading = reinterpret_cast<double*>(base + L.off[2]);
+    v->v = reinterpret_cast<double*>(base + L.off[3]);
+    v->steering = reinterpret_cast<double*>(base + L.off[4]);
+    v->t = reinterpret_cast<int32_t*>(base + L.off[5]);
+    v->done = base + L.off[6];
+    v->reason = base + L.off[7];
+    v->rng = reinterpret_cast<uint64_t*>(base + L.off[8]);
+    v->proj_s = reinterpret_cast<double*>(base + L.off[9]);
+    v->proj_d = reinterpret_cast<double*>(base + L.off[10]);
+    v->proj_in_corridor = base + L.off[11];
+    v->events = base + L.off[12];
+    v->stopped_flags = base + L.off[13];
+}
+
+struct StepoutLayout {
+    size_t off[6];
+    size_t bytes;
+};
+StepoutLayout stepout_layout(int B) {
+    const size_t sz[6] = {4, 1, 4, 4, 4, 4};
+    StepoutLayout L;
+    size_t o = 0;
+    for (int i = 0; i < 6; ++i) {
+        L.off[i] = o;
+        o += al(sz[i] * size_t(B));
+    }
+    L.bytes = o;
+    return L;
+}
+void carve_stepout(unsigned char* base, const StepoutLayout& L, zsim_stepout_view* v) {
+    v->reward = reinterpret_cast<float*>(base + L.off[0]);
+    v->event = base + L.off[1];
+    v->s = reinterpret_cast<float*>(base + L.off[2]);
+    v->a_lat = reinterpret_cast<float*>(base + L.off[3]);
+    v->a_lon = reinterpret_cast<float*>(base + L.off[4]);
+    v->v = reinterpret_cast<float*>(base + L.off[5]);
+}
+
+struct ObsLayout {
+    size_t off[5];
+    size_t n[5];  // floats per array
+    size_t bytes;
+};
+ObsLayout obs_layout(int B, int Ka, int Kr, int Kl) {
+    ObsLayout L;
+    L.n[0] = size_t(B) * 9;
+    L.n[1] = size_t(B) * Ka * 6;
+    L.n[2] = size_t(B) * Kr * 12;
+    L.n[3] = size_t(B) * Kl * 5;
+    L.n[4] = size_t(B) * 2;
+    size_t o = 0;
+    for (int i = 0; i < 5; ++i) {
+        L.off[i] = o;
+        o += al(L.n[i] * 4);
+    }
+    L.bytes = o;
+    return L;
+}
+void carve_obs(unsigned char* base, const ObsLayout& L, zsim_obs_view* v) {
+    v->active = reinterpret_cast<float*>(base + L.off[0]);
+    v->agents = reinterpret_cast<float*>(base + L.off[1]);
+    v->road = reinterpret_cast<float*>(base + L.off[2]);
+    v->route = reinterpret_cast<float*>(base + L.off[3]);
+    v->value_only = reinterpret_cast<float*>(base + L.off[4]);
+}
+
+// Host image of the pack: offsets into one buffer, then a single upload.
+struct PackBuilder {
+    std::vector<unsigned char> host;
+    size_t cursor = 0;
+    template <class T>
+    size_t reserve(size_t n) {
+        size_t o = cursor;
+        cursor += al(sizeof(T) * std::max<size_t>(n, 1));
+        return o;
+    }
+    template <class T>
+    T* at(size_t off) {
+        return reinterpret_cast<T*>(host.data() + off);
+    }
+};
+
+}  // namespace
+
+struct zsim_env {
+    int device = 0;
+    zs::KernelArgs base{};
+    void* d_pack = nullptr;
+    size_t pack_bytes = 0;
+    int32_t* d_err = nullptr;
+    int B = 0, horizon = 0, total_stop = 0;
+    double dt = 0.0;
+    int zero_accel = 0, zero_steer = 0;
+    std::vector<double> accel_bins, steer_bins;
+    std::vector<double> goal_s, initial_s, logged_progress;
+    zsim_sim_config cfg{};
+    StateLayout sl{};
+    StepoutLayout sol{};
+    ObsLayout ol{};
+    // host-vector path scratch (lazily allocated)
+    void* h_dev = nullptr;
+    zsim_state_view h_in{}, h_out{};
+    zsim_stepout_view h_so{};
+    zsim_obs_view h_obs{};
+    int32_t* h_act = nullptr;
+    cudaStream_t h_stream = nullptr;
+    double* d_initial_s = nullptr;
+    int grid = 0;
+};
+
+namespace {
+
+void set_device(const zsim_env* env) { cuda_check(cudaSetDevice(env->device), "cudaSetDevice"); }
+
+bool is_carved_state(const zsim_state_view* v, const StateLayout& L) {
+    unsigned char* base = reinterpret_cast<unsigned char*>(v->x);
+    zsim_state_view c;
+    carve_state(base, L, &c);
+    return std::memcmp(&c, v, sizeof(c)) == 0;
+}
+bool is_carved_stepout(const zsim_stepout_view* v, const StepoutLayout& L) {
+    unsigned char* base = reinterpret_cast<unsigned char*>(v->reward);
+    zsim_stepout_view c;
+    carve_stepout(base, L, &c);
+    return std::memcmp(&c, v, sizeof(c)) == 0;
+}
+bool is_carved_obs(const zsim_obs_view* v, const ObsLayout& L) {
+    unsigned char* base = reinterpret_cast<unsigned char*>(v->active);
+    zsim_obs_view c;
+    carve_obs(base, L, &c);
+    return std::memcmp(&c, v, sizeof(c)) == 0;
+}
+
+cudaMemcpyKind kind_of(int dir) {
+    switch (dir) {
+        case 0: return cudaMemcpyHostToDevice;
+        case 1: return cudaMemcpyDeviceToHost;
+        case 2: return cudaMemcpyDeviceToDevice;
+        default: raise(Err::invalid_argument, "copy direction must be 0 (h2d), 1 (d2h) or 2 (d2d)");
+    }
+}
+
+void copy_state(zsim_env* env, const zsim_state_view* dst, const zsim_state_view* src, int dir, cudaStream_t s) {
+    cudaMemcpyKind k = kind_of(dir);
+    if (is_carved_state(dst, env->sl) && is_carved_state(src, env->sl)) {
+        cuda_check(cudaMemcpyAsync(dst->x, src->x, env->sl.bytes, k, s), "state copy");
+        return;
+    }
+    const size_t B = size_t(env->B);
+    cuda_check(cudaMemcpyAsync(dst->x, src->x, 8 * B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->y, src->y, 8 * B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->heading, src->heading, 8 * B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->v, src->v, 8 * B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->steering, src->steering, 8 * B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->t, src->t, 4 * B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->done, src->done, B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->reason, src->reason, B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->rng, src->rng, 8 * B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->proj_s, src->proj_s, 8 * B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->proj_d, src->proj_d, 8 * B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->proj_in_corridor, src->proj_in_corridor, B, k, s), "state copy");
+    cuda_check(cudaMemcpyAsync(dst->events, src->events, B, k, s), "state copy");
+    if (env->total_stop > 0) {
+        cuda_check(cudaMemcpyAsync(dst->stopped_flags, src->stopped_flags, size_t(env->total_stop), k, s),
+                   "state copy");
+    }
+}
+
+void copy_stepout(zsim_env* env, const zsim_stepout_view* dst, const zsim_stepout_view* src, int dir,
+                  cudaStream_t s) {
+    cudaMemcpyKind k = kind_of(dir);
+    if (is_carved_stepout(dst, env->sol) && is_carved_stepout(src, env->sol)) {
+        cuda_check(cudaMemcpyAsync(dst->reward, src->reward, env->sol.bytes, k, s), "stepout copy");
+        return;
+    }
+    const size_t B = size_t(env->B);
+    cuda_check(cudaMemcpyAsync(dst->reward, src->reward, 4 * B, k, s), "stepout copy");
+    cuda_check(cudaMemcpyAsync(dst->event, src->event, B, k, s), "stepout copy");
+    cuda_check(cudaMemcpyAsync(dst->s, src->s, 4 * B, k, s), "stepout copy");
+    cuda_check(cudaMemcpyAsync(dst->a_lat, src->a_lat, 4 * B, k, s), "stepout copy");
+    cuda_check(cudaMemcpyAsync(dst->a_lon, src->a_lon, 4 * B, k, s), "stepout copy");
+    cuda_check(cudaMemcpyAsync(dst->v, src->v, 4 * B, k, s), "stepout copy");
+}
+
+void copy_obs(zsim_env* env, const zsim_obs_view* dst, const zsim_obs_view* src, int dir, cudaStream_t s) {
+    cudaMemcpyKind k = kind_of(dir);
+    if (is_carved_obs(dst, env->ol) && is_carved_obs(src, env->ol)) {
+        cuda_check(cudaMemcpyAsync(dst->active, src->active, env->ol.bytes, k, s), "obs copy");
+        return;
+    }
+    const ObsLayout& L = env->ol;
+    cuda_check(cudaMemcpyAsync(dst->active, src->active, 4 * L.n[0], k, s), "obs copy");
+    cuda_check(cudaMemcpyAsync(dst->agents, src->agents, 4 * L.n[1], k, s), "obs copy");
+    cuda_check(cudaMemcpyAsync(dst->road, src->road, 4 * L.n[2], k, s), "obs copy");
+    cuda_check(cudaMemcpyAsync(dst->route, src->route, 4 * L.n[3], k, s), "obs copy");
+    cuda_check(cudaMemcpyAsync(dst->value_only, src->value_only, 4 * L.n[4], k, s), "obs copy");
+}
+
+void check_view(const void* p, const char* what) {
+    if (!p) raise(Err::invalid_argument, std::string(what) + ": null view pointer");
+}
+
+zs::DevCfg make_dev_cfg(const zsim_sim_config& c, const std::vector<double>& ab, const std::vector<double>& sb) {
+    zs::DevCfg d{};
+    d.wheelbase = c.wheelbase;
+    d.ego_length = c.ego_length;
+    d.ego_width = c.ego_width;
+    d.ego_center_offset = c.ego_center_offset;
+    d.delta_max = c.delta_max;
+    d.v_min = c.v_min;
+    d.goal_radius = c.goal_radius;
+    d.footprint_margin = c.footprint_margin;
+    d.stop_cross_speed = c.stop_cross_speed;
+    d.stop_zone = c.stop_zone;
+    d.stop_slow_speed = c.stop_slow_speed;
+    d.w_progress = c.w_progress;
+    d.w_speed = c.w_speed;
+    d.w_lat = c.w_lat;
+    d.w_lon = c.w_lon;
+    d.terminal_penalty = c.terminal_penalty;
+    d.feature_radius = c.feature_radius;
+    d.disable_dones = c.disable_dones;
+    d.n_agents = c.n_agents;
+    d.n_road = c.n_road;
+    d.n_route = c.n_route;
+    d.n_accel = int32_t(ab.size());
+    d.n_steer = int32_t(sb.size());
+    for (size_t i = 0; i < ab.size(); ++i) d.accel_bins[i] = ab[i];
+    for (size_t i = 0; i < sb.size(); ++i) d.steer_bins[i] = sb[i];
+    return d;
+}
+
+int next_pow2(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+// Env::Env (simcore.cpp:203-233) over make_batch (scenario_io.cpp:404-437).
+void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon) {
+    using namespace zs;
+    if (scenes.empty()) raise(Err::invalid_argument, "make_batch: empty scenario list");
+    const int B = int(scenes.size());
+    const double dt = scenes[0].dt;
+    for (const auto& s : scenes) {
+        if (int(s.num_steps) > horizon) {
+            raise(Err::invalid_argument, "scenario `" + s.id + "` has " + std::to_string(s.num_steps) +
+                                             " steps > T=" + std::to_string(horizon));
+        }
+        if (s.dt != dt) raise(Err::invalid_argument, "mixed dt within batch");
+    }
+    // Route contexts and route border points (host fp64, reference op order).
+    std::vector<RouteCtx> ctx(static_cast<size_t>(B));
+    std::vector<std::vector<RoutePt>> rpts(static_cast<size_t>(B));
+    PackDims d{};
+    d.B = B;
+    d.T = 1;
+    d.A = 1;
+    d.P = 1;
+    d.R = 1;
+    d.L = 1;
+    d.C = 2;
+    d.NL = 1;
+    d.NS = 1;
+    for (int b = 0; b < B; ++b) {
+        const Scene& s = scenes[size_t(b)];
+        ctx[size_t(b)] = build_context(s);
+        rpts[size_t(b)] = build_route_points(s);
+        d.T = std::max(d.T, int(s.num_steps));
+        d.A = std::max(d.A, int(s.agents.size()));
+        size_t np = 0;
+        for (const auto& f : s.features) np += f.xy.size() / 2;
+        d.P = std::max(d.P, int(np));
+        d.R = std::max(d.R, int(rpts[size_t(b)].size()));
+        d.L = std::max(d.L, int(ctx[size_t(b)].lanes.size()));
+        for (const auto& lf : ctx[size_t(b)].lanes) d.C = std::max(d.C, int(lf.x.size()));
+        d.NL = std::max(d.NL, int(ctx[size_t(b)].lights.size()));
+        d.NS = std::max(d.NS, int(ctx[size_t(b)].stops.size()));
+        for (const auto& a : s.agents) {
+            if (a.x.size() < s.num_steps || a.y.size() < s.num_steps || a.heading.size() < s.num_steps ||
+                a.speed.size() < s.num_steps || a.valid.size() < s.num_steps)
+                raise(Err::invalid_argument, "scenario `" + s.id + "`: agent arrays shorter than num_steps");
+        }
+        for (const auto& lt : s.lights) {
+            if (lt.state.size() < s.num_steps)
+                raise(Err::invalid_argument, "scenario `" + s.id + "`: light state shorter than num_steps");
+        }
+        if (s.ego_x.size() < 2 || s.ego_v.size() < 2 || s.ego_h.size() < 2 || s.ego_y.size() < 2) {
+            if (s.ego_x.empty()) raise(Err::invalid_argument, "scenario `" + s.id + "`: empty ego log");
+        }
+    }
+    if (d.L > kMaxLanes) {
+        raise(Err::invalid_argument, "route has " + std::to_string(d.L) + " lanes; the device path supports " +
+                                         std::to_string(kMaxLanes));
+    }
+
+    PackBuilder pb;
+    size_t o_num_steps = pb.reserve<int32_t>(B), o_na = pb.reserve<int32_t>(B), o_nr = pb.reserve<int32_t>(B),
+           o_nrt = pb.reserve<int32_t>(B), o_nl = pb.reserve<int32_t>(B), o_nlt = pb.reserve<int32_t>(B),
+           o_ns = pb.reserve<int32_t>(B), o_soff = pb.reserve<int32_t>(B);
+    size_t o_sl = pb.reserve<float>(B), o_gx = pb.reserve<float>(B), o_gy = pb.reserve<float>(B);
+    size_t o_gs = pb.reserve<double>(B), o_rl = pb.reserve<double>(B);
+    size_t o_ix = pb.reserve<double>(B), o_iy = pb.reserve<double>(B), o_ih = pb.reserve<double>(B),
+           o_iv = pb.reserve<double>(B), o_ist = pb.reserve<double>(B);
+    const size_t nag = size_t(B) * d.T * d.A;
+    size_t o_agx = pb.reserve<float>(nag), o_agy = pb.reserve<float>(nag), o_agh = pb.reserve<float>(nag),
+           o_ags = pb.reserve<float>(nag), o_agv = pb.reserve<uint8_t>(nag);
+    size_t o_agl = pb.reserve<float>(size_t(B) * d.A), o_agw = pb.reserve<float>(size_t(B) * d.A);
+    size_t o_rxy = pb.reserve<float>(size_t(B) * d.P * 2), o_rkd = pb.reserve<uint8_t>(size_t(B) * d.P);
+    size_t o_txy = pb.reserve<float>(size_t(B) * d.R * 2), o_tfl = pb.reserve<uint8_t>(size_t(B) * d.R);
+    const size_t nln = size_t(B) * d.L * d.C;
+    size_t o_lx = pb.reserve<double>(nln), o_ly = pb.reserve<double>(nln), o_ls = pb.reserve<double>(nln),
+           o_lhw = pb.reserve<double>(nln);
+    size_t o_ln = pb.reserve<int32_t>(size_t(B) * d.L), o_lid = pb.reserve<uint32_t>(size_t(B) * d.L);
+    size_t o_lts = pb.reserve<double>(size_t(B) * d.NL), o_ltst = pb.reserve<uint8_t>(size_t(B) * d.NL * d.T);
+    size_t o_sts = pb.reserve<double>(size_t(B) * d.NS);
+    pb.host.assign(pb.cursor, 0);
+
+    env->goal_s.assign(size_t(B), 0.0);
+    env->initial_s.assign(size_t(B), 0.0);
+    env->logged_progress.assign(size_t(B), 0.0);
+    int total_stop = 0;
+    for (int b = 0; b < B; ++b) {
+        const Scene& s = scenes[size_t(b)];
+        const RouteCtx& c = ctx[size_t(b)];
+        const int T = d.T, A = d.A;
+        pb.at<int32_t>(o_num_steps)[b] = int32_t(s.num_steps);
+        pb.at<int32_t>(o_na)[b] = int32_t(s.agents.size());
+        size_t np = 0;
+        for (const auto& f : s.features) np += f.xy.size() / 2;
+        pb.at<int32_t>(o_nr)[b] = int32_t(np);
+        pb.at<int32_t>(o_nrt)[b] = int32_t(rpts[size_t(b)].size());
+        pb.at<int32_t>(o_nl)[b] = int32_t(c.lanes.size());
+        pb.at<int32_t>(o_nlt)[b] = int32_t(c.lights.size());
+        pb.at<int32_t>(o_ns)[b] = int32_t(c.stops.size());
+        pb.at<int32_t>(o_soff)[b] = total_stop;
+        total_stop += int(c.stops.size());
+        pb.at<float>(o_sl)[b] = s.speed_limit;
+        pb.at<float>(o_gx)[b] = s.goal_x;
+        pb.at<float>(o_gy)[b] = s.goal_y;
+        // simcore.cpp:217-223
+        double gs = project_host(double(s.goal_x), double(s.goal_y), c).s;
+        double s0 = project_host(double(s.ego_x.front()), double(s.ego_y.front()), c).s;
+        double s1 = project_host(double(s.ego_x[s.num_steps - 1]), double(s.ego_y[s.num_steps - 1]), c).s;
+        env->goal_s[size_t(b)] = gs;
+        env->initial_s[size_t(b)] = s0;
+        env->logged_progress[size_t(b)] = s1 - s0;
+        pb.at<double>(o_gs)[b] = gs;
+        pb.at<double>(o_rl)[b] = c.route_length;
+        pb.at<double>(o_ix)[b] = double(s.ego_x[0]);
+        pb.at<double>(o_iy)[b] = double(s.ego_y[0]);
+        pb.at<double>(o_ih)[b] = double(s.ego_h[0]);
+        pb.at<double>(o_iv)[b] = double(s.ego_v[0]);
+        pb.at<double>(o_ist)[b] = initial_steering(s, env->cfg.wheelbase, env->cfg.delta_max);
+        for (size_t j = 0; j < s.agents.size(); ++j) {
+            const AgentLog& ag = s.agents[j];
+            pb.at<float>(o_agl)[size_t(b) * A + j] = ag.length;
+            pb.at<float>(o_agw)[size_t(b) * A + j] = ag.width;
+            for (uint32_t t = 0; t < s.num_steps; ++t) {
+                size_t k = (size_t(b) * T + t) * A + j;
+                pb.at<float>(o_agx)[k] = ag.x[t];
+                pb.at<float>(o_agy)[k] = ag.y[t];
+                pb.at<float>(o_agh)[k] = ag.heading[t];
+                pb.at<float>(o_ags)[k] = ag.speed[t];
+                pb.at<uint8_t>(o_agv)[k] = ag.valid[t];
+            }
+        }
+        size_t p = 0;
+        for (const auto& f : s.features) {
+            for (size_t i = 0; i + 1 < f.xy.size(); i += 2, ++p) {
+                size_t k = size_t(b) * d.P + p;
+                pb.at<float>(o_rxy)[2 * k] = f.xy[i];
+                pb.at<float>(o_rxy)[2 * k + 1] = f.xy[i + 1];
+                pb.at<uint8_t>(o_rkd)[k] = uint8_t((f.kind & 15) | (f.dir << 4));
+            }
+        }
+        const auto& rp = rpts[size_t(b)];
+        for (size_t i = 0; i < rp.size(); ++i) {
+            size_t k = size_t(b) * d.R + i;
+            pb.at<float>(o_txy)[2 * k] = rp[i].x;
+            pb.at<float>(o_txy)[2 * k + 1] = rp[i].y;
+            pb.at<uint8_t>(o_tfl)[k] = uint8_t((rp[i].is_left ? 1 : 0) | (rp[i].lane_valid ? 2 : 0));
+        }
+        for (size_t l = 0; l < c.lanes.size(); ++l) {
+            const LaneFrame& lf = c.lanes[l];
+            pb.at<int32_t>(o_ln)[size_t(b) * d.L + l] = int32_t(lf.x.size());
+            pb.at<uint32_t>(o_lid)[size_t(b) * d.L + l] = lf.lane_id;
+            for (size_t i = 0; i < lf.x.size(); ++i) {
+                size_t k = (size_t(b) * d.L + l) * d.C + i;
+                pb.at<double>(o_lx)[k] = lf.x[i];
+                pb.at<double>(o_ly)[k] = lf.y[i];
+                pb.at<double>(o_ls)[k] = lf.s[i];
+                pb.at<double>(o_lhw)[k] = lf.hw[i];
+            }
+        }
+        for (size_t k = 0; k < c.lights.size(); ++k) {
+            pb.at<double>(o_lts)[size_t(b) * d.NL + k] = c.lights[k].second;
+            const auto& st = s.lights[size_t(c.lights[k].first)].state;
+            for (uint32_t t = 0; t < s.num_steps; ++t)
+                pb.at<uint8_t>(o_ltst)[(size_t(b) * d.NL + k) * d.T + t] = st[t];
+        }
+        for (size_t j = 0; j < c.stops.size(); ++j) pb.at<double>(o_sts)[size_t(b) * d.NS + j] = c.stops[j].second;
+    }
+
+    cuda_check(cudaMalloc(&env->d_pack, pb.cursor), "cudaMalloc(pack)");
+    env->pack_bytes = pb.cursor;
+    cuda_check(cudaMemcpy(env->d_pack, pb.host.data(), pb.cursor, cudaMemcpyHostToDevice), "upload pack");
+    unsigned char* D = static_cast<unsigned char*>(env->d_pack);
+    DevPack& pk = env->base.pk;
+    pk.d = d;
+    pk.dt = dt;
+    pk.horizon = horizon;
+    pk.total_stop_lines = total_stop;
+    pk.num_steps = reinterpret_cast<const int32_t*>(D + o_num_steps);
+    pk.n_agents = reinterpret_cast<const int32_t*>(D + o_na);
+    pk.n_road = reinterpret_cast<const int32_t*>(D + o_nr);
+    pk.n_route = reinterpret_cast<const int32_t*>(D + o_nrt);
+    pk.n_lanes = reinterpret_cast<const int32_t*>(D + o_nl);
+    pk.n_lights = reinterpret_cast<const int32_t*>(D + o_nlt);
+    pk.n_stops = reinterpret_cast<const int32_t*>(D + o_ns);
+    pk.stop_off = reinterpret_cast<const int32_t*>(D + o_soff);
+    pk.speed_limit = reinterpret_cast<const float*>(D + o_sl);
+    pk.goal_x = reinterpret_cast<const float*>(D + o_gx);
+    pk.goal_y = reinterpret_cast<const float*>(D + o_gy);
+    pk.goal_s = reinterpret_cast<const double*>(D + o_gs);
+    pk.route_len = reinterpret_cast<const double*>(D + o_rl);
+    pk.init_x = reinterpret_cast<const double*>(D + o_ix);
+    pk.init_y = reinterpret_cast<const double*>(D + o_iy);
+    pk.init_h = reinterpret_cast<const double*>(D + o_ih);
+    pk.init_v = reinterpret_cast<const double*>(D + o_iv);
+    pk.init_steer = reinterpret_cast<const double*>(D + o_ist);
+    pk.ag_x = reinterpret_cast<const float*>(D + o_agx);
+    pk.ag_y = reinterpret_cast<const float*>(D + o_agy);
+    pk.ag_h = reinterpret_cast<const float*>(D + o_agh);
+    pk.ag_sp = reinterpret_cast<const float*>(D + o_ags);
+    pk.ag_valid = D + o_agv;
+    pk.ag_len = reinterpret_cast<const float*>(D + o_agl);
+    pk.ag_wid = reinterpret_cast<const float*>(D + o_agw);
+    pk.road_xy = reinterpret_cast<const float2*>(D + o_rxy);
+    pk.road_kd = D + o_rkd;
+    pk.route_xy = reinterpret_cast<const float2*>(D + o_txy);
+    pk.route_fl = D + o_tfl;
+    pk.ln_x = reinterpret_cast<const double*>(D + o_lx);
+    pk.ln_y = reinterpret_cast<const double*>(D + o_ly);
+    pk.ln_s = reinterpret_cast<const double*>(D + o_ls);
+    pk.ln_hw = reinterpret_cast<const double*>(D + o_lhw);
+    pk.ln_n = reinterpret_cast<const int32_t*>(D + o_ln);
+    pk.ln_id = reinterpret_cast<const uint32_t*>(D + o_lid);
+    pk.lt_s = reinterpret_cast<const double*>(D + o_lts);
+    pk.lt_state = D + o_ltst;
+    pk.st_s = reinterpret_cast<const double*>(D + o_sts);
+
+    env->B = B;
+    env->horizon = horizon;
+    env->dt = dt;
+    env->total_stop = total_stop;
+    env->base.key_cap = std::max(d.P, d.R);
+    env->base.cand_cap = std::max(256, next_pow2(4 * std::max(env->cfg.n_road, env->cfg.n_route)));
+    env->sl = state_layout(B, total_stop);
+    env->sol = stepout_layout(B);
+    env->ol = obs_layout(B, env->cfg.n_agents, env->cfg.n_road, env->cfg.n_route);
+    env->grid = B;
+    size_t smem = zs::smem_bytes(env->base);
+    if (smem > 200 * 1024) raise(Err::invalid_argument, "scenario shapes exceed the kernel's shared-memory budget");
+}
+
+zs::KernelArgs args_for(zsim_env* env) { return env->base; }
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void ensure_host_scratch(zsim_env* env) {
+    if (env->h_dev) return;
+    size_t bytes = 2 * env->sl.bytes + env->sol.bytes + env->ol.bytes + al(size_t(env->B) * 8);
+    cuda_check(cudaMalloc(&env->h_dev, bytes), "cudaMalloc(host-path scratch)");
+    unsigned char* p = static_cast<unsigned char*>(env->h_dev);
+    carve_state(p, env->sl, &env->h_in);
+    p += env->sl.bytes;
+    carve_state(p, env->sl, &env->h_out);
+    p += env->sl.bytes;
+    carve_stepout(p, env->sol, &env->h_so);
+    p += env->sol.bytes;
+    carve_obs(p, env->ol, &env->h_obs);
+    p += env->ol.bytes;
+    env->h_act = reinterpret_cast<int32_t*>(p);
+    cuda_check(cudaStreamCreateWithFlags(&env->h_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+}
+
+void check_actions_host(zsim_env* env, const int32_t* accel, const int32_t* steer) {
+    if (!accel || !steer) raise(Err::invalid_argument, "env_step: action/state shape mismatch");
+    const int na = int(env->accel_bins.size()), ns = int(env->steer_bins.size());
+    for (int b = 0; b < env->B; ++b) {
+        if (accel[b] < 0 || accel[b] >= na || steer[b] < 0 || steer[b] >= ns)
+            raise(Err::invalid_argument, "action index out of range");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+ZSIM_API int zsim_abi_version(void) { return ZSIM_ABI_VERSION; }
+
+ZSIM_API const char* zsim_last_error(void) { return g_last_error.c_str(); }
+
+ZSIM_API int zsim_sim_config_defaults(zsim_sim_config* c) {
+    return guarded([&] {
+        if (!c) raise(Err::invalid_argument, "null config");
+        std::memset(c, 0, sizeof(*c));
+        c->wheelbase = 3.0;
+        c->ego_length = 4.7;
+        c->ego_width = 1.9;
+        c->ego_center_offset = 1.5;
+        c->delta_max = 0.55;
+        c->v_min = 0.0;
+        c->goal_radius = 2.0;
+        c->footprint_margin = 0.1;
+        c->stop_cross_speed = 0.5;
+        c->stop_zone = 2.0;
+        c->stop_slow_speed = 0.1;
+        c->disable_dones = 0;
+        c->n_agents = 16;
+        c->n_road = 128;
+        c->n_route = 64;
+        c->w_progress = 1.0;
+        c->w_speed = 0.1;
+        c->w_lat = 0.02;
+        c->w_lon = 0.02;
+        c->terminal_penalty = 10.0;
+        c->feature_radius = 100.0;
+        c->threads = 1;
+    });
+}
+
+ZSIM_API int zsim_env_create(const uint8_t* file, size_t nbytes, const int64_t* indices, int32_t n_indices,
+                             int32_t horizon, const zsim_sim_config* cfg, const double* accel_bins, int32_t n_accel,
+                             const double* steer_bins, int32_t n_steer, int32_t device, zsim_env** out) {
+    return guarded([&] {
+        if (!out) raise(Err::invalid_argument, "null output pointer");
+        *out = nullptr;
+        if (!file) raise(Err::invalid_argument, "null ZSIM buffer");
+        std::unique_ptr<zsim_env> env(new zsim_env());
+        env->device = device;
+        if (cfg) {
+            env->cfg = *cfg;
+        } else {
+            zsim_sim_config_defaults(&env->cfg);
+        }
+        if (env->cfg.n_agents <= 0 || env->cfg.n_road <= 0 || env->cfg.n_route <= 0)
+            raise(Err::invalid_argument, "nearest_features: k must be > 0");
+        if (accel_bins && n_accel > 0)
+            env->accel_bins.assign(accel_bins, accel_bins + n_accel);
+        else
+            env->accel_bins = {-4.0, -2.0, -0.5, 0.0, 0.5, 2.0, 4.0};
+        if (steer_bins && n_steer > 0)
+            env->steer_bins.assign(steer_bins, steer_bins + n_steer);
+        else
+            env->steer_bins = {-0.4, -0.1, 0.0, 0.1, 0.4};
+        zs::check_bins(env->accel_bins, "accel_bins");
+        zs::check_bins(env->steer_bins, "steer_rate_bins");
+        if (env->accel_bins.size() > 16 || env->steer_bins.size() > 16)
+            raise(Err::invalid_argument, "at most 16 bins per action head on the device path");
+        env->zero_accel = zs::nearest_bin(env->accel_bins, 0.0);
+        env->zero_steer = zs::nearest_bin(env->steer_bins, 0.0);
+
+        zs::ZsimIndex idx = zs::zsim_index(file, nbytes);
+        std::vector<int64_t> rows;
+        if (indices) {
+            if (n_indices <= 0) raise(Err::invalid_argument, "load_batch: empty index list");
+            rows.assign(indices, indices + n_indices);
+        } else {
+            for (int64_t i = 0; i < int64_t(idx.records.size()); ++i) rows.push_back(i);
+        }
+        std::vector<zs::Scene> scenes;
+        scenes.reserve(rows.size());
+        int maxsteps = 2;
+        for (int64_t r : rows) {
+            scenes.push_back(zs::zsim_decode(file, nbytes, idx, r));
+            maxsteps = std::max(maxsteps, int(scenes.back().num_steps));
+        }
+        if (horizon <= 0) horizon = maxsteps;
+        set_device(env.get());
+        env->base.cfg = make_dev_cfg(env->cfg, env->accel_bins, env->steer_bins);
+        stage_env(env.get(), scenes, horizon);
+        cuda_check(cudaMalloc(&env->d_err, 4), "cudaMalloc(err)");
+        cuda_check(cudaMemset(env->d_err, 0, 4), "cudaMemset(err)");
+        env->base.err = env->d_err;
+        *out = env.release();
+    });
+}
+
+ZSIM_API int zsim_env_destroy(zsim_env* env) {
+    return guarded([&] {
+        if (!env) return;
+        cudaSetDevice(env->device);
+        if (env->h_stream) cudaStreamDestroy(env->h_stream);
+        cudaFree(env->h_dev);
+        cudaFree(env->d_pack);
+        cudaFree(env->d_err);
+        cudaFree(env->d_initial_s);
+        delete env;
+    });
+}
+
+ZSIM_API int zsim_env_get_info(const zsim_env* env, zsim_env_info* out) {
+    return guarded([&] {
+        if (!env || !out) raise(Err::invalid_argument, "null env/info");
+        std::memset(out, 0, sizeof(*out));
+        out->batch = env->B;
+        out->horizon = env->horizon;
+        out->dt = env->dt;
+        out->total_stop_lines = env->total_stop;
+        out->zero_accel_idx = env->zero_accel;
+        out->zero_steer_idx = env->zero_steer;
+        out->num_accel = int32_t(env->accel_bins.size());
+        out->num_steer = int32_t(env->steer_bins.size());
+        const zs::PackDims& d = env->base.pk.d;
+        out->cap_steps = d.T;
+        out->cap_agents = d.A;
+        out->cap_road = d.P;
+        out->cap_route = d.R;
+        out->cap_lanes = d.L;
+        out->cap_vertices = d.C;
+        out->cap_lights = d.NL;
+        out->cap_stops = d.NS;
+        out->device = env->device;
+        out->static_bytes = env->pack_bytes;
+    });
+}
+
+ZSIM_API int zsim_env_get_scalars(const zsim_env* env, double* goal_s, double* initial_s, double* logged_progress) {
+    return guarded([&] {
+        if (!env) raise(Err::invalid_argument, "null env");
+        if (goal_s) std::copy(env->goal_s.begin(), env->goal_s.end(), goal_s);
+        if (initial_s) std::copy(env->initial_s.begin(), env->initial_s.end(), initial_s);
+        if (logged_progress) std::copy(env->logged_progress.begin(), env->logged_progress.end(), logged_progress);
+    });
+}
+
+ZSIM_API int zsim_state_alloc(zsim_env* env, zsim_state_view* v) {
+    return guarded([&] {
+        check_view(env, "state_alloc");
+        check_view(v, "state_alloc");
+        set_device(env);
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, env->sl.bytes), "cudaMalloc(state)");
+        cuda_check(cudaMemset(p, 0, env->sl.bytes), "cudaMemset(state)");
+        carve_state(static_cast<unsigned char*>(p), env->sl, v);
+    });
+}
+ZSIM_API int zsim_state_free(zsim_env* env, zsim_state_view* v) {
+    return guarded([&] {
+        if (!env || !v) return;
+        set_device(env);
+        cudaFree(v->x);
+        std::memset(v, 0, sizeof(*v));
+    });
+}
+ZSIM_API int zsim_stepout_alloc(zsim_env* env, zsim_stepout_view* v) {
+    return guarded([&] {
+        check_view(env, "stepout_alloc");
+        check_view(v, "stepout_alloc");
+        set_device(env);
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, env->sol.bytes), "cudaMalloc(stepout)");
+        cuda_check(cudaMemset(p, 0, env->sol.bytes), "cudaMemset(stepout)");
+        carve_stepout(static_cast<unsigned char*>(p), env->sol, v);
+    });
+}
+ZSIM_API int zsim_stepout_free(zsim_env* env, zsim_stepout_view* v) {
+    return guarded([&] {
+        if (!env || !v) return;
+        set_device(env);
+        cudaFree(v->reward);
+        std::memset(v, 0, sizeof(*v));
+    });
+}
+ZSIM_API int zsim_obs_alloc(zsim_env* env, zsim_obs_view* v) {
+    return guarded([&] {
+        check_view(env, "obs_alloc");
+        check_view(v, "obs_alloc");
+        set_device(env);
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, env->ol.bytes), "cudaMalloc(obs)");
+        cuda_check(cudaMemset(p, 0, env->ol.bytes), "cudaMemset(obs)");
+        carve_obs(static_cast<unsigned char*>(p), env->ol, v);
+    });
+}
+ZSIM_API int zsim_obs_free(zsim_env* env, zsim_obs_view* v) {
+    return guarded([&] {
+        if (!env || !v) return;
+        set_device(env);
+        cudaFree(v->active);
+        std::memset(v, 0, sizeof(*v));
+    });
+}
+
+ZSIM_API int zsim_layout_bytes(const zsim_env* env, size_t* state_bytes, size_t* stepout_bytes, size_t* obs_bytes) {
+    return guarded([&] {
+        check_view(env, "layout_bytes");
+        if (state_bytes) *state_bytes = env->sl.bytes;
+        if (stepout_bytes) *stepout_bytes = env->sol.bytes;
+        if (obs_bytes) *obs_bytes = env->ol.bytes;
+    });
+}
+ZSIM_API int zsim_state_carve(const zsim_env* env, void* base, zsim_state_view* out) {
+    return guarded([&] {
+        check_view(env, "state_carve");
+        check_view(base, "state_carve");
+        check_view(out, "state_carve");
+        carve_state(static_cast<unsigned char*>(base), env->sl, out);
+    });
+}
+ZSIM_API int zsim_stepout_carve(const zsim_env* env, void* base, zsim_stepout_view* out) {
+    return guarded([&] {
+        check_view(env, "stepout_carve");
+        check_view(base, "stepout_carve");
+        check_view(out, "stepout_carve");
+        carve_stepout(static_cast<unsigned char*>(base), env->sol, out);
+    });
+}
+ZSIM_API int zsim_obs_carve(const zsim_env* env, void* base, zsim_obs_view* out) {
+    return guarded([&] {
+        check_view(env, "obs_carve");
+        check_view(base, "obs_carve");
+        check_view(out, "obs_carve");
+        carve_obs(static_cast<unsigned char*>(base), env->ol, out);
+    });
+}
+ZSIM_API int zsim_host_alloc(size_t bytes, void** out) {
+    return guarded([&] {
+        check_view(out, "host_alloc");
+        *out = nullptr;
+        cuda_check(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable), "cudaHostAlloc");
+    });
+}
+ZSIM_API int zsim_host_free(void* p) {
+    return guarded([&] {
+        if (p) cuda_check(cudaFreeHost(p), "cudaFreeHost");
+    });
+}
+
+ZSIM_API int zsim_state_copy(zsim_env* env, const zsim_state_view* dst, const zsim_state_view* src, int32_t dir,
+                             void* stream) {
+    return guarded([&] {
+        check_view(env, "state_copy");
+        check_view(dst, "state_copy");
+        check_view(src, "state_copy");
+        set_device(env);
+        copy_state(env, dst, src, dir, as_stream(stream));
+    });
+}
+ZSIM_API int zsim_stepout_copy(zsim_env* env, const zsim_stepout_view* dst, const zsim_stepout_view* src,
+                               int32_t dir, void* stream) {
+    return guarded([&] {
+        check_view(env, "stepout_copy");
+        check_view(dst, "stepout_copy");
+        check_view(src, "stepout_copy");
+        set_device(env);
+        copy_stepout(env, dst, src, dir, as_stream(stream));
+    });
+}
+ZSIM_API int zsim_obs_copy(zsim_env* env, const zsim_obs_view* dst, const zsim_obs_view* src, int32_t dir,
+                           void* stream) {
+    return guarded([&] {
+        check_view(env, "obs_copy");
+        check_view(dst, "obs_copy");
+        check_view(src, "obs_copy");
+        set_device(env);
+        copy_obs(env, dst, src, dir, as_stream(stream));
+    });
+}
+
+ZSIM_API int zsim_reset(zsim_env* env, uint64_t seed, const zsim_state_view* out, void* stream) {
+    return guarded([&] {
+        check_view(env, "reset");
+        check_view(out, "reset");
+        set_device(env);
+        zs::KernelArgs a = args_for(env);
+        a.out = *out;
+        a.seed = seed;
+        cuda_check(zs::launch_reset(a, env->grid, as_stream(stream)), "reset kernel");
+    });
+}
+
+ZSIM_API int zsim_step(zsim_env* env, const zsim_state_view* in, const int32_t* accel, const int32_t* steer,
+                       const zsim_state_view* out, const zsim_stepout_view* so, void* stream) {
+    return guarded([&] {
+        check_view(env, "step");
+        check_view(in, "step");
+        check_view(out, "step");
+        check_view(so, "step");
+        if (!accel || !steer) raise(Err::invalid_argument, "env_step: action/state shape mismatch");
+        set_device(env);
+        zs::KernelArgs a = args_for(env);
+        a.in = *in;
+        a.out = *out;
+        a.accel = accel;
+        a.steer = steer;
+        a.so = *so;
+        cuda_check(zs::launch_step_observe(a, zs::kModeStep, env->grid, as_stream(stream)), "step kernel");
+    });
+}
+
+ZSIM_API int zsim_observe(zsim_env* env, const zsim_state_view* in, const zsim_obs_view* obs, void* stream) {
+    return guarded([&] {
+        check_view(env, "observe");
+        check_view(in, "observe");
+        check_view(obs, "observe");
+        set_device(env);
+        zs::KernelArgs a = args_for(env);
+        a.in = *in;
+        a.obs = *obs;
+        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->grid, as_stream(stream)), "observe kernel");
+    });
+}
+
+ZSIM_API int zsim_step_observe(zsim_env* env, const zsim_state_view* in, const int32_t* accel, const int32_t* steer,
+                               const zsim_state_view* out, const zsim_stepout_view* so, const zsim_obs_view* obs,
+                               void* stream) {
+    return guarded([&] {
+        check_view(env, "step_observe");
+        check_view(in, "step_observe");
+        check_view(out, "step_observe");
+        check_view(so, "step_observe");
+        check_view(obs, "step_observe");
+        if (!accel || !steer) raise(Err::invalid_argument, "env_step: action/state shape mismatch");
+        set_device(env);
+        zs::KernelArgs a = args_for(env);
+        a.in = *in;
+        a.out = *out;
+        a.accel = accel;
+        a.steer = steer;
+        a.so = *so;
+        a.obs = *obs;
+        cuda_check(zs::launch_step_observe(a, zs::kModeStepObserve, env->grid, as_stream(stream)),
+                   "step_observe kernel");
+    });
+}
+
+ZSIM_API int zsim_episode_stats(zsim_env* env, const zsim_state_view* state, int64_t* out_dev, void* stream) {
+    return guarded([&] {
+        check_view(env, "episode_stats");
+        check_view(state, "episode_stats");
+        check_view(out_dev, "episode_stats");
+        set_device(env);
+        if (!env->d_initial_s) {
+            cuda_check(cudaMalloc(&env->d_initial_s, sizeof(double) * size_t(env->B)), "cudaMalloc(initial_s)");
+            cuda_check(cudaMemcpy(env->d_initial_s, env->initial_s.data(), sizeof(double) * size_t(env->B),
+                                  cudaMemcpyHostToDevice),
+                       "upload initial_s");
+        }
+        zs::KernelArgs a = args_for(env);
+        a.in = *state;
+        cuda_check(zs::launch_episode_stats(a, env->d_initial_s, reinterpret_cast<long long*>(out_dev),
+                                            as_stream(stream)),
+                   "episode_stats kernel");
+    });
+}
+
+ZSIM_API int zsim_set_debug_topk(zsim_env* env, int32_t* dev_idx) {
+    return guarded([&] {
+        check_view(env, "set_debug_topk");
+        env->base.dbg = dev_idx;
+    });
+}
+
+ZSIM_API int zsim_check_errors(zsim_env* env, void* stream) {
+    return guarded([&] {
+        check_view(env, "check_errors");
+        set_device(env);
+        int32_t h = 0;
+        cuda_check(cudaMemcpyAsync(&h, env->d_err, 4, cudaMemcpyDeviceToHost, as_stream(stream)), "read error word");
+        cuda_check(cudaStreamSynchronize(as_stream(stream)), "stream sync");
+        if (h) {
+            cuda_check(cudaMemsetAsync(env->d_err, 0, 4, as_stream(stream)), "clear error word");
+            cuda_check(cudaStreamSynchronize(as_stream(stream)), "stream sync");
+            raise(Err::invalid_argument, "action index out of range");
+        }
+    });
+}
+
+ZSIM_API int zsim_reset_host(zsim_env* env, uint64_t seed, const zsim_state_view* out_host) {
+    return guarded([&] {
+        check_view(env, "reset_host");
+        check_view(out_host, "reset_host");
+        set_device(env);
+        ensure_host_scratch(env);
+        zs::KernelArgs a = args_for(env);
+        a.out = env->h_out;
+        a.seed = seed;
+        cuda_check(zs::launch_reset(a, env->grid, env->h_stream), "reset kernel");
+        copy_state(env, out_host, &env->h_out, 1, env->h_stream);
+        cuda_check(cudaStreamSynchronize(env->h_stream), "stream sync");
+    });
+}
+
+ZSIM_API int zsim_step_host(zsim_env* env, const zsim_state_view* in_host, const int32_t* accel,
+                            const int32_t* steer, const zsim_state_view* out_host, const zsim_stepout_view* so_host) {
+    return guarded([&] {
+        check_view(env, "step_host");
+        check_view(in_host, "step_host");
+        check_view(out_host, "step_host");
+        check_view(so_host, "step_host");
+        check_actions_host(env, accel, steer);
+        set_device(env);
+        ensure_host_scratch(env);
+        cudaStream_t s = env->h_stream;
+        copy_state(env, &env->h_in, in_host, 0, s);
+        const size_t B = size_t(env->B);
+        cuda_check(cudaMemcpyAsync(env->h_act, accel, 4 * B, cudaMemcpyHostToDevice, s), "action upload");
+        cuda_check(cudaMemcpyAsync(env->h_act + B, steer, 4 * B, cudaMemcpyHostToDevice, s), "action upload");
+        zs::KernelArgs a = args_for(env);
+        a.in = env->h_in;
+        a.out = env->h_out;
+        a.accel = env->h_act;
+        a.steer = env->h_act + B;
+        a.so = env->h_so;
+        cuda_check(zs::launch_step_observe(a, zs::kModeStep, env->grid, s), "step kernel");
+        copy_state(env, out_host, &env->h_out, 1, s);
+        copy_stepout(env, so_host, &env->h_so, 1, s);
+        cuda_check(cudaStreamSynchronize(s), "stream sync");
+    });
+}
+
+ZSIM_API int zsim_observe_host(zsim_env* env, const zsim_state_view* in_host, const zsim_obs_view* obs_host) {
+    return guarded([&] {
+        check_view(env, "observe_host");
+        check_view(in_host, "observe_host");
+        check_view(obs_host, "observe_host");
+        set_device(env);
+        ensure_host_scratch(env);
+        cudaStream_t s = env->h_stream;
+        copy_state(env, &env->h_in, in_host, 0, s);
+        zs::KernelArgs a = args_for(env);
+        a.in = env->h_in;
+        a.obs = env->h_obs;
+        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->grid, s), "observe kernel");
+        copy_obs(env, obs_host, &env->h_obs, 1, s);
+        cuda_check(cudaStreamSynchronize(s), "stream sync");
+    });
+}
+
+ZSIM_API int zsim_stress_config_defaults(zsim_stress_config* c) {
+    return guarded([&] {
+        if (!c) raise(Err::invalid_argument, "null config");
+        c->count = 64;
+        c->num_steps = 92;
+        c->agents = 32;
+        c->road_points = 2048;
+        c->lanes = 4;
+        c->lane_vertices = 64;
+        c->dt = 0.1;
+        c->speed_limit = 10.0;
+        c->lane_width = 3.5;
+    });
+}
+
+ZSIM_API int zsim_stress_generate(const zsim_stress_config* cfg, uint64_t seed, uint8_t** out_buf, size_t* out_len) {
+    return guarded([&] {
+        if (!cfg || !out_buf || !out_len) raise(Err::invalid_argument, "null argument");
+        std::string img = zs::stress_generate(*cfg, seed);
+        uint8_t* p = static_cast<uint8_t*>(std::malloc(img.size()));
+        if (!p) raise(Err::runtime, "out of host memory");
+        std::memcpy(p, img.data(), img.size());
+        *out_buf = p;
+        *out_len = img.size();
+    });
+}
+
+ZSIM_API void zsim_free_buffer(void* buf) { std::free(buf); }
+
+}  // extern "C"

@@ -1,0 +1,39 @@
+// zsim_kernels.cuh -- launch interface between the C-ABI host code and the
+// sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "zsim_pack.cuh"
+
+namespace zs {
+
+constexpr int kThreads = 128;  // threads per CTA (4 warps); one CTA per scenario row at a time
+constexpr int kMaxLanes = 16;  // route lanes per scenario supported by the projection scratch
+
+constexpr int kStatsLen = 8;  // episode-stats vector length
+
+enum { kModeStep = 0, kModeObserve = 1, kModeStepObserve = 2 };
+
+struct KernelArgs {
+    DevPack pk;
+    DevCfg cfg;
+    zsim_state_view in;
+    zsim_state_view out;
+    const int32_t* accel;
+    const int32_t* steer;
+    zsim_stepout_view so;
+    zsim_obs_view obs;
+    int32_t* dbg;
+    int32_t* err;
+    uint64_t seed;
+    int32_t key_cap;   // >= max(P, R)
+    int32_t cand_cap;  // power of two >= 2 * max(n_road, n_route)
+};
+
+size_t smem_bytes(const KernelArgs& a);
+cudaError_t launch_step_observe(const KernelArgs& a, int mode, int grid, cudaStream_t stream);
+cudaError_t launch_reset(const KernelArgs& a, int grid, cudaStream_t stream);
+cudaError_t launch_episode_stats(const KernelArgs& a, const double* initial_s, long long* out, cudaStream_t stream);
+
+}  // namespace zs

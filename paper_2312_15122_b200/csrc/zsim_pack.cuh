@@ -1,0 +1,91 @@
+// zsim_pack.cuh -- HBM layout of the immutable per-batch scenario pack and the
+// device-side SimConfig.  One contiguous allocation, every array 256-B
+// aligned, padded to per-batch capacities with per-scenario counts.
+//
+// Per scenario b (reference types in /root/reference/proj/src/core/):
+//   agents  [B][T][A]  x, y, heading, speed f32 + valid u8   (LoggedAgent, scenario.hpp:37-44)
+//   dims    [B][A]     length, width f32
+//   road    [B][P]     float2 xy + u8 kind|dir<<4 in nearest_features' flat
+//                      (feature, point) order (roads.cpp:220-229)
+//   route   [B][R]     float2 xy + u8 is_left|lane_valid<<1 (simcore.cpp:181-200)
+//   lanes   [B][L][C]  centerline x, y, s, half_width f64 after RouteFrame::build
+//                      clipping (roads.cpp:43-103); n vertices + lane_id per lane
+//   lights  [B][NL]    route s f64 + state u8[T] for lights kept by
+//                      RouteContext::build (roads.cpp:245-249)
+//   stops   [B][NS]    route s f64 for stop lines kept by RouteContext::build
+//   scalars [B]        counts, goal, goal_s, route_length, initial ego (+ steering
+//                      recovered on the host, simcore.cpp:620-627)
+#pragma once
+
+#include <stdint.h>
+
+#include "../../include/zsim_gpu.h"
+
+namespace zs {
+
+struct PackDims {
+    int32_t B, T, A, P, R, L, C, NL, NS;
+};
+
+struct DevPack {
+    PackDims d;
+    double dt;
+    int32_t horizon;
+    int32_t total_stop_lines;
+    // [B]
+    const int32_t* num_steps;
+    const int32_t* n_agents;
+    const int32_t* n_road;
+    const int32_t* n_route;
+    const int32_t* n_lanes;
+    const int32_t* n_lights;
+    const int32_t* n_stops;
+    const int32_t* stop_off;
+    const float* speed_limit;
+    const float* goal_x;
+    const float* goal_y;
+    const double* goal_s;
+    const double* route_len;
+    const double* init_x;
+    const double* init_y;
+    const double* init_h;
+    const double* init_v;
+    const double* init_steer;
+    // agents
+    const float* ag_x;
+    const float* ag_y;
+    const float* ag_h;
+    const float* ag_sp;
+    const uint8_t* ag_valid;
+    const float* ag_len;
+    const float* ag_wid;
+    // road / route points
+    const float2* road_xy;
+    const uint8_t* road_kd;
+    const float2* route_xy;
+    const uint8_t* route_fl;
+    // lanes
+    const double* ln_x;
+    const double* ln_y;
+    const double* ln_s;
+    const double* ln_hw;
+    const int32_t* ln_n;
+    const uint32_t* ln_id;
+    // lights / stops
+    const double* lt_s;
+    const uint8_t* lt_state;  // [B][NL][T]
+    const double* st_s;
+};
+
+// SimConfig + ActionTable as the kernels see them.
+struct DevCfg {
+    double wheelbase, ego_length, ego_width, ego_center_offset, delta_max, v_min;
+    double goal_radius, footprint_margin, stop_cross_speed, stop_zone, stop_slow_speed;
+    double w_progress, w_speed, w_lat, w_lon, terminal_penalty, feature_radius;
+    int32_t disable_dones, n_agents, n_road, n_route;
+    int32_t n_accel, n_steer;
+    double accel_bins[16];
+    double steer_bins[16];
+};
+
+}  // namespace zs

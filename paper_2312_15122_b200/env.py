@@ -1,0 +1,484 @@
+"""Host-side mirror of the reference's ``zsim::sim::Env`` over the C-ABI.
+
+Same method names, argument meaning and error behaviour as
+``/root/reference/proj/src/core/simcore.hpp:191-245``:
+
+* ``Env(batch, config, table)``      -> ``Env(zsim, indices, horizon, config, accel_bins, steer_bins)``
+* ``init_state(seed)``                -> ``SimStateBatch``            (simcore.cpp:237-276)
+* ``step(state, accel, steer, next, out)``                           (simcore.cpp:406-421)
+* ``observe(state, obs)``                                             (simcore.cpp:540-552)
+* accessors ``batch_size / horizon / dt / config / goal_s / initial_s / logged_progress``
+
+plus a device fast path (``DeviceState`` / ``DeviceStepOut`` / ``DeviceObs``
+and ``reset_device / step_device / observe_device / step_observe_device``)
+whose buffers stay resident in HBM and whose launches are stream-ordered.
+Errors raise ``ZsimError`` with the reference's ErrorKind.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, fields
+from pathlib import Path
+
+import numpy as np
+
+from ._abi import (EnvInfo, ObsView, SimConfigC, StateView, StepOutView, StressConfigC, ZsimError, check, lib)
+
+DONE_REASONS = ("none", "collision", "off_route", "red_light", "stop_line", "goal_reached")
+ACTIVE_FEAT, AGENT_FEAT, ROAD_FEAT, ROUTE_FEAT, VALUE_FEAT = 9, 6, 12, 5, 2  # ObsSpec (simcore.hpp:60-72)
+
+
+def event_bit(reason: int) -> int:
+    """simcore.hpp:58."""
+    return 1 << (reason - 1)
+
+
+@dataclass
+class SimConfig:
+    """SimConfig (simcore.hpp:14-45) with dyn::Limits (dynamics.hpp:18-21) flattened."""
+    wheelbase: float = 3.0
+    ego_length: float = 4.7
+    ego_width: float = 1.9
+    ego_center_offset: float = 1.5
+    delta_max: float = 0.55
+    v_min: float = 0.0
+    goal_radius: float = 2.0
+    footprint_margin: float = 0.1
+    stop_cross_speed: float = 0.5
+    stop_zone: float = 2.0
+    stop_slow_speed: float = 0.1
+    disable_dones: bool = False
+    w_progress: float = 1.0
+    w_speed: float = 0.1
+    w_lat: float = 0.02
+    w_lon: float = 0.02
+    terminal_penalty: float = 10.0
+    n_agents: int = 16
+    n_road: int = 128
+    n_route: int = 64
+    feature_radius: float = 100.0
+    threads: int = 1
+
+    def to_c(self) -> SimConfigC:
+        c = SimConfigC()
+        check(lib.zsim_sim_config_defaults(C.byref(c)))
+        for f in fields(self):
+            setattr(c, f.name, int(getattr(self, f.name)) if f.name in (
+                "disable_dones", "n_agents", "n_road", "n_route", "threads") else float(getattr(self, f.name)))
+        return c
+
+
+def _ptr(a: np.ndarray, ctype):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def _addr(p) -> int:
+    return C.cast(p, C.c_void_p).value or 0
+
+
+def _np_at(addr: int, dtype, n: int) -> np.ndarray:
+    dt = np.dtype(dtype)
+    buf = (C.c_char * max(1, n * dt.itemsize)).from_address(addr)
+    return np.frombuffer(buf, dtype=dt, count=n)
+
+
+_STATE_FIELDS = (("x", np.float64, C.c_double), ("y", np.float64, C.c_double),
+                 ("heading", np.float64, C.c_double), ("v", np.float64, C.c_double),
+                 ("steering", np.float64, C.c_double), ("t", np.int32, C.c_int32), ("done", np.uint8, C.c_uint8),
+                 ("reason", np.uint8, C.c_uint8), ("rng", np.uint64, C.c_uint64),
+                 ("proj_s", np.float64, C.c_double), ("proj_d", np.float64, C.c_double),
+                 ("proj_in_corridor", np.uint8, C.c_uint8), ("events", np.uint8, C.c_uint8),
+                 ("stopped_flags", np.uint8, C.c_uint8))
+_STEPOUT_FIELDS = (("reward", np.float32, C.c_float), ("event", np.uint8, C.c_uint8), ("s", np.float32, C.c_float),
+                   ("a_lat", np.float32, C.c_float), ("a_lon", np.float32, C.c_float), ("v", np.float32, C.c_float))
+_OBS_FIELDS = ("active", "agents", "road", "route", "value_only")
+
+
+class _Pinned:
+    """Page-locked host block from zsim_host_alloc, freed on collection."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        check(lib.zsim_host_alloc(C.c_size_t(nbytes), C.byref(p)))
+        self.addr = p.value
+        self.nbytes = nbytes
+
+    def __del__(self):
+        if getattr(self, "addr", None):
+            lib.zsim_host_free(C.c_void_p(self.addr))
+            self.addr = None
+
+
+class SimStateBatch:
+    """SimStateBatch (simcore.hpp:107-121) as SoA numpy arrays."""
+
+    def __init__(self, batch: int, total_stop_lines: int, arrays: dict | None = None, owner=None):
+        self.batch = batch
+        self.total_stop_lines = total_stop_lines
+        self._owner = owner
+        for name, dt, _ in _STATE_FIELDS:
+            n = total_stop_lines if name == "stopped_flags" else batch
+            a = arrays[name] if arrays is not None else np.zeros(max(n, 1), dtype=dt)
+            setattr(self, name, a)
+
+    @classmethod
+    def pinned(cls, env: "Env") -> "SimStateBatch":
+        blk = _Pinned(env.layout[0])
+        v = StateView()
+        check(lib.zsim_state_carve(env.handle, C.c_void_p(blk.addr), C.byref(v)))
+        arrays = {}
+        for name, dt, _ in _STATE_FIELDS:
+            n = env.total_stop_lines if name == "stopped_flags" else env.batch_size()
+            arrays[name] = _np_at(_addr(getattr(v, name)), dt, max(n, 1))
+        return cls(env.batch_size(), env.total_stop_lines, arrays, owner=blk)
+
+    def view(self) -> StateView:
+        v = StateView()
+        for name, _, ct in _STATE_FIELDS:
+            setattr(v, name, _ptr(getattr(self, name), ct))
+        return v
+
+    def copy(self) -> "SimStateBatch":
+        s = SimStateBatch(self.batch, self.total_stop_lines)
+        for name, _, _ in _STATE_FIELDS:
+            getattr(s, name)[...] = getattr(self, name)
+        return s
+
+    def copy_from(self, other: "SimStateBatch") -> None:
+        for name, _, _ in _STATE_FIELDS:
+            getattr(self, name)[...] = getattr(other, name)
+
+
+class StepOut:
+    """StepOut (simcore.hpp:123-131)."""
+
+    def __init__(self, batch: int, arrays: dict | None = None, owner=None):
+        self.batch = batch
+        self._owner = owner
+        for name, dt, _ in _STEPOUT_FIELDS:
+            setattr(self, name, arrays[name] if arrays is not None else np.zeros(batch, dtype=dt))
+
+    @classmethod
+    def pinned(cls, env: "Env") -> "StepOut":
+        blk = _Pinned(env.layout[1])
+        v = StepOutView()
+        check(lib.zsim_stepout_carve(env.handle, C.c_void_p(blk.addr), C.byref(v)))
+        arrays = {name: _np_at(_addr(getattr(v, name)), dt, env.batch_size()) for name, dt, _ in _STEPOUT_FIELDS}
+        return cls(env.batch_size(), arrays, owner=blk)
+
+    def view(self) -> StepOutView:
+        v = StepOutView()
+        for name, _, ct in _STEPOUT_FIELDS:
+            setattr(v, name, _ptr(getattr(self, name), ct))
+        return v
+
+
+class ObservationBatch:
+    """ObservationBatch (simcore.hpp:76-103): [B][slot][feat] f32 per modality."""
+
+    def __init__(self, batch: int, n_agents: int, n_road: int, n_route: int, arrays: dict | None = None,
+                 owner=None):
+        self.batch = batch
+        self.n_agents, self.n_road, self.n_route = n_agents, n_road, n_route
+        self._owner = owner
+        shapes = self.shapes()
+        for name in _OBS_FIELDS:
+            a = arrays[name] if arrays is not None else np.zeros(int(np.prod(shapes[name])), dtype=np.float32)
+            setattr(self, name, a.reshape(shapes[name]))
+
+    def shapes(self) -> dict:
+        B = self.batch
+        return {"active": (B, ACTIVE_FEAT), "agents": (B, self.n_agents, AGENT_FEAT),
+                "road": (B, self.n_road, ROAD_FEAT), "route": (B, self.n_route, ROUTE_FEAT),
+                "value_only": (B, VALUE_FEAT)}
+
+    @classmethod
+    def pinned(cls, env: "Env") -> "ObservationBatch":
+        blk = _Pinned(env.layout[2])
+        v = ObsView()
+        check(lib.zsim_obs_carve(env.handle, C.c_void_p(blk.addr), C.byref(v)))
+        cfg = env.config()
+        tmp = cls(env.batch_size(), cfg.n_agents, cfg.n_road, cfg.n_route)
+        arrays = {name: _np_at(_addr(getattr(v, name)), np.float32, getattr(tmp, name).size) for name in _OBS_FIELDS}
+        return cls(env.batch_size(), cfg.n_agents, cfg.n_road, cfg.n_route, arrays, owner=blk)
+
+    def view(self) -> ObsView:
+        v = ObsView()
+        for name in _OBS_FIELDS:
+            setattr(v, name, _ptr(getattr(self, name), C.c_float))
+        return v
+
+    @property
+    def nbytes(self) -> int:
+        return sum(getattr(self, n).nbytes for n in _OBS_FIELDS)
+
+
+class _DeviceBuf:
+    def __init__(self, env: "Env", view, free_fn):
+        self.env = env
+        self.v = view
+        self._free = free_fn
+
+    def close(self):
+        if self._free is not None and self.env.handle:
+            self._free(self.env.handle, C.byref(self.v))
+        self._free = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceState(_DeviceBuf):
+    pass
+
+
+class DeviceStepOut(_DeviceBuf):
+    pass
+
+
+class DeviceObs(_DeviceBuf):
+    pass
+
+
+def _stream(s) -> C.c_void_p:
+    if s is None:
+        return C.c_void_p(0)
+    if hasattr(s, "cuda_stream"):
+        return C.c_void_p(s.cuda_stream)
+    return C.c_void_p(int(s))
+
+
+class Env:
+    """The batched log-replay environment on one B200 (simcore.hpp:188-245)."""
+
+    def __init__(self, zsim, indices=None, horizon: int = 0, config: SimConfig | None = None,
+                 accel_bins=None, steer_bins=None, device: int = 0):
+        if isinstance(zsim, (str, os.PathLike)):
+            zsim = Path(zsim).read_bytes()
+        self._bytes = bytes(zsim)
+        self._config = config or SimConfig()
+        cfg = self._config.to_c()
+        idx = None
+        n_idx = 0
+        if indices is not None:
+            arr = np.ascontiguousarray(np.asarray(indices, dtype=np.int64))
+            idx, n_idx = arr.ctypes.data_as(C.POINTER(C.c_int64)), int(arr.size)
+            self._idx_keep = arr
+        ab = np.ascontiguousarray(accel_bins, dtype=np.float64) if accel_bins is not None else None
+        sb = np.ascontiguousarray(steer_bins, dtype=np.float64) if steer_bins is not None else None
+        h = C.c_void_p()
+        buf = C.create_string_buffer(self._bytes, len(self._bytes))
+        check(lib.zsim_env_create(C.cast(buf, C.c_void_p), C.c_size_t(len(self._bytes)), idx, n_idx, int(horizon),
+                                  C.byref(cfg), None if ab is None else _ptr(ab, C.c_double),
+                                  0 if ab is None else int(ab.size), None if sb is None else _ptr(sb, C.c_double),
+                                  0 if sb is None else int(sb.size), int(device), C.byref(h)))
+        self.handle = h.value
+        info = EnvInfo()
+        check(lib.zsim_env_get_info(self.handle, C.byref(info)))
+        self.info = info
+        self.total_stop_lines = info.total_stop_lines
+        B = info.batch
+        self._goal_s = np.zeros(B)
+        self._initial_s = np.zeros(B)
+        self._logged = np.zeros(B)
+        check(lib.zsim_env_get_scalars(self.handle, _ptr(self._goal_s, C.c_double), _ptr(self._initial_s, C.c_double),
+                                       _ptr(self._logged, C.c_double)))
+        sb_, so_, ob_ = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        check(lib.zsim_layout_bytes(self.handle, C.byref(sb_), C.byref(so_), C.byref(ob_)))
+        self.layout = (sb_.value, so_.value, ob_.value)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.zsim_env_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --- accessors (simcore.hpp:200-209) ---
+    def batch_size(self) -> int:
+        return self.info.batch
+
+    def horizon(self) -> int:
+        return self.info.horizon
+
+    def dt(self) -> float:
+        return self.info.dt
+
+    def config(self) -> SimConfig:
+        return self._config
+
+    def goal_s(self, b: int) -> float:
+        return float(self._goal_s[b])
+
+    def initial_s(self, b: int) -> float:
+        return float(self._initial_s[b])
+
+    def logged_progress(self, b: int) -> float:
+        return float(self._logged[b])
+
+    @property
+    def zero_accel_idx(self) -> int:
+        return self.info.zero_accel_idx
+
+    @property
+    def zero_steer_idx(self) -> int:
+        return self.info.zero_steer_idx
+
+    # --- host-vector path (the drop-in overloads) ---
+    def new_state(self, pinned: bool = False) -> SimStateBatch:
+        return SimStateBatch.pinned(self) if pinned else SimStateBatch(self.batch_size(), self.total_stop_lines)
+
+    def new_stepout(self, pinned: bool = False) -> StepOut:
+        return StepOut.pinned(self) if pinned else StepOut(self.batch_size())
+
+    def new_obs(self, pinned: bool = False) -> ObservationBatch:
+        c = self._config
+        return ObservationBatch.pinned(self) if pinned else ObservationBatch(self.batch_size(), c.n_agents, c.n_road,
+                                                                             c.n_route)
+
+    def init_state(self, seed: int, out: SimStateBatch | None = None) -> SimStateBatch:
+        st = out or self.new_state()
+        v = st.view()
+        check(lib.zsim_reset_host(self.handle, C.c_uint64(seed), C.byref(v)))
+        return st
+
+    def step(self, state: SimStateBatch, accel_idx, steer_idx, next: SimStateBatch | None = None,
+             out: StepOut | None = None):
+        B = self.batch_size()
+        a = np.ascontiguousarray(accel_idx, dtype=np.int32)
+        s = np.ascontiguousarray(steer_idx, dtype=np.int32)
+        if a.size != B or s.size != B or state.batch != B:
+            raise ZsimError(1, "env_step: action/state shape mismatch")
+        nxt = next if next is not None else self.new_state()
+        so = out if out is not None else self.new_stepout()
+        vin, vout, vso = state.view(), nxt.view(), so.view()
+        check(lib.zsim_step_host(self.handle, C.byref(vin), _ptr(a, C.c_int32), _ptr(s, C.c_int32), C.byref(vout),
+                                 C.byref(vso)))
+        return nxt, so
+
+    def observe(self, state: SimStateBatch, obs: ObservationBatch | None = None) -> ObservationBatch:
+        ob = obs if obs is not None else self.new_obs()
+        vin, vo = state.view(), ob.view()
+        check(lib.zsim_observe_host(self.handle, C.byref(vin), C.byref(vo)))
+        return ob
+
+    # --- device fast path ---
+    def device_state(self) -> DeviceState:
+        v = StateView()
+        check(lib.zsim_state_alloc(self.handle, C.byref(v)))
+        return DeviceState(self, v, lib.zsim_state_free)
+
+    def device_stepout(self) -> DeviceStepOut:
+        v = StepOutView()
+        check(lib.zsim_stepout_alloc(self.handle, C.byref(v)))
+        return DeviceStepOut(self, v, lib.zsim_stepout_free)
+
+    def device_obs(self) -> DeviceObs:
+        v = ObsView()
+        check(lib.zsim_obs_alloc(self.handle, C.byref(v)))
+        return DeviceObs(self, v, lib.zsim_obs_free)
+
+    def reset_device(self, seed: int, out: DeviceState, stream=None) -> None:
+        check(lib.zsim_reset(self.handle, C.c_uint64(seed), C.byref(out.v), _stream(stream)))
+
+    def step_device(self, state: DeviceState, accel_ptr: int, steer_ptr: int, next: DeviceState,
+                    out: DeviceStepOut, stream=None) -> None:
+        check(lib.zsim_step(self.handle, C.byref(state.v), C.cast(C.c_void_p(accel_ptr), C.POINTER(C.c_int32)),
+                            C.cast(C.c_void_p(steer_ptr), C.POINTER(C.c_int32)), C.byref(next.v), C.byref(out.v),
+                            _stream(stream)))
+
+    def observe_device(self, state: DeviceState, obs: DeviceObs, stream=None) -> None:
+        check(lib.zsim_observe(self.handle, C.byref(state.v), C.byref(obs.v), _stream(stream)))
+
+    def step_observe_device(self, state: DeviceState, accel_ptr: int, steer_ptr: int, next: DeviceState,
+                            out: DeviceStepOut, obs: DeviceObs, stream=None) -> None:
+        check(lib.zsim_step_observe(self.handle, C.byref(state.v),
+                                    C.cast(C.c_void_p(accel_ptr), C.POINTER(C.c_int32)),
+                                    C.cast(C.c_void_p(steer_ptr), C.POINTER(C.c_int32)), C.byref(next.v),
+                                    C.byref(out.v), C.byref(obs.v), _stream(stream)))
+
+    def episode_stats(self, state: DeviceState, out_ptr: int, stream=None) -> None:
+        """int64[8] episode-stats vector of `state` into device memory `out_ptr`."""
+        check(lib.zsim_episode_stats(self.handle, C.byref(state.v), C.cast(C.c_void_p(out_ptr),
+                                                                           C.POINTER(C.c_int64)), _stream(stream)))
+
+    def set_debug_topk(self, dev_ptr: int | None) -> None:
+        check(lib.zsim_set_debug_topk(self.handle, C.cast(C.c_void_p(dev_ptr or 0), C.POINTER(C.c_int32))))
+
+    def check_errors(self, stream=None) -> None:
+        check(lib.zsim_check_errors(self.handle, _stream(stream)))
+
+    def download_state(self, dev: DeviceState, host: SimStateBatch | None = None, stream=None) -> SimStateBatch:
+        st = host or self.new_state()
+        v = st.view()
+        check(lib.zsim_state_copy(self.handle, C.byref(v), C.byref(dev.v), 1, _stream(stream)))
+        return st
+
+    def upload_state(self, host: SimStateBatch, dev: DeviceState, stream=None) -> None:
+        v = host.view()
+        check(lib.zsim_state_copy(self.handle, C.byref(dev.v), C.byref(v), 0, _stream(stream)))
+
+    def download_stepout(self, dev: DeviceStepOut, host: StepOut | None = None, stream=None) -> StepOut:
+        so = host or self.new_stepout()
+        v = so.view()
+        check(lib.zsim_stepout_copy(self.handle, C.byref(v), C.byref(dev.v), 1, _stream(stream)))
+        return so
+
+    def download_obs(self, dev: DeviceObs, host: ObservationBatch | None = None, stream=None) -> ObservationBatch:
+        ob = host or self.new_obs()
+        v = ob.view()
+        check(lib.zsim_obs_copy(self.handle, C.byref(v), C.byref(dev.v), 1, _stream(stream)))
+        return ob
+
+
+@dataclass
+class StressConfig:
+    """Synthetic stress-scenario shape; see include/zsim_gpu.h."""
+    count: int = 64
+    num_steps: int = 92
+    agents: int = 32
+    road_points: int = 2048
+    lanes: int = 4
+    lane_vertices: int = 64
+    dt: float = 0.1
+    speed_limit: float = 10.0
+    lane_width: float = 3.5
+
+
+def stress_scenarios(cfg: StressConfig, seed: int = 7) -> bytes:
+    """ZSIM container image of `cfg.count` stress scenarios (host-only call)."""
+    c = StressConfigC(**{f.name: getattr(cfg, f.name) for f in fields(cfg)})
+    p = C.c_void_p()
+    n = C.c_size_t()
+    check(lib.zsim_stress_generate(C.byref(c), C.c_uint64(seed), C.byref(p), C.byref(n)))
+    try:
+        return C.string_at(p.value, n.value)
+    finally:
+        lib.zsim_free_buffer(p)
+
+
+def random_actions(steps: int, batch: int, seed: int = 123, num_accel: int = 7, num_steer: int = 5):
+    """Fixed [steps][batch] int32 action tensors, uniform over the bins from a
+    splitmix64 stream (common.hpp:28-44), as the BASELINE plan prescribes."""
+    n = steps * batch * 2
+    g = 0x9E3779B97F4A7C15
+    state = (seed + g) & 0xFFFFFFFFFFFFFFFF
+    idx = np.arange(1, n + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(state) + idx * np.uint64(g)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    z = z.reshape(steps, batch, 2)
+    accel = (z[..., 0] % np.uint64(num_accel)).astype(np.int32)
+    steer = (z[..., 1] % np.uint64(num_steer)).astype(np.int32)
+    return np.ascontiguousarray(accel), np.ascontiguousarray(steer)

@@ -1,0 +1,91 @@
+"""CPU tests of the boundary: the C-ABI library loads and exports every symbol
+include/zsim_gpu.h declares; host-only entry points (stress generator, config
+defaults) behave; no kernel is launched."""
+from __future__ import annotations
+
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2312_15122_b200 as z
+from paper_2312_15122_b200 import _abi
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _declared_symbols() -> list[str]:
+    text = (ROOT / "include" / "zsim_gpu.h").read_text()
+    return re.findall(r"ZSIM_API\s+[\w\s\*]+?\b(zsim_\w+)\s*\(", text)
+
+
+def test_header_declares_entry_points():
+    names = _declared_symbols()
+    assert len(names) >= 30
+    for must in ("zsim_env_create", "zsim_reset", "zsim_step", "zsim_observe", "zsim_step_observe",
+                 "zsim_step_host", "zsim_observe_host", "zsim_check_errors", "zsim_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(str(_abi.LIB_PATH))
+    missing = [n for n in _declared_symbols() if not hasattr(lib, n)]
+    assert not missing, missing
+    # and the ctypes table covers the whole header
+    assert set(_declared_symbols()) == set(_abi.SIGNATURES)
+
+
+def test_library_hides_internal_symbols():
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_abi.LIB_PATH)], capture_output=True, text=True).stdout
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    assert all(n.startswith("zsim_") for n in exported), sorted(n for n in exported if not n.startswith("zsim_"))
+
+
+def test_abi_version_and_defaults():
+    assert z.lib.zsim_abi_version() == 1
+    c = _abi.SimConfigC()
+    assert z.lib.zsim_sim_config_defaults(C.byref(c)) == 0
+    # SimConfig defaults (simcore.hpp:14-45)
+    assert (c.wheelbase, c.ego_length, c.ego_width, c.ego_center_offset) == (3.0, 4.7, 1.9, 1.5)
+    assert (c.n_agents, c.n_road, c.n_route, c.feature_radius) == (16, 128, 64, 100.0)
+    assert (c.w_progress, c.w_speed, c.w_lat, c.w_lon, c.terminal_penalty) == (1.0, 0.1, 0.02, 0.02, 10.0)
+    assert c.delta_max == 0.55 and c.disable_dones == 0
+    py = z.SimConfig().to_c()
+    assert bytes(py) == bytes(c)
+
+
+def test_error_reporting_without_device():
+    # a malformed container is rejected on the host before any device work
+    with pytest.raises(z.ZsimError) as ei:
+        z.Env(b"NOPE" + b"\0" * 20)
+    assert ei.value.kind == "io" and "not a ZSIM" in str(ei.value)
+
+
+def test_stress_generator_is_deterministic_and_shaped():
+    cfg = z.StressConfig(count=4, agents=8, road_points=300, lanes=3, lane_vertices=20)
+    a = z.stress_scenarios(cfg, seed=3)
+    b = z.stress_scenarios(cfg, seed=3)
+    c = z.stress_scenarios(cfg, seed=4)
+    assert a == b and a != c
+    assert a[:4] == b"ZSIM"
+    from tests.zsim_py import read_zsim
+    scen = read_zsim(a)
+    assert len(scen) == 4
+    for s in scen:
+        assert len(s["agents"]) == 7
+        assert sum(len(f["xy"]) // 2 for f in s["features"]) == 300
+        assert len(s["lanes"]) == 3 and all(len(l["left"]) == 40 for l in s["lanes"])
+        assert len(s["lights"]) == 1 and len(s["stops"]) == 1
+
+
+def test_random_actions_are_in_range_and_seeded():
+    A, S = z.random_actions(91, 64, seed=123)
+    assert A.shape == (91, 64) and A.dtype == np.int32
+    assert A.min() >= 0 and A.max() <= 6 and S.min() >= 0 and S.max() <= 4
+    A2, _ = z.random_actions(91, 64, seed=123)
+    assert np.array_equal(A, A2)
+    # roughly uniform
+    assert len(np.unique(A)) == 7 and len(np.unique(S)) == 5
