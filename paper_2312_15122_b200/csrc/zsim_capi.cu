@@ -385,7 +385,9 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     const size_t nln = size_t(B) * d.L * d.C;
     size_t o_lx = pb.reserve<double>(nln), o_ly = pb.reserve<double>(nln), o_ls = pb.reserve<double>(nln),
            o_lhw = pb.reserve<double>(nln);
+    size_t o_labx = pb.reserve<double>(nln), o_laby = pb.reserve<double>(nln), o_llen2 = pb.reserve<double>(nln);
     size_t o_ln = pb.reserve<int32_t>(size_t(B) * d.L), o_lid = pb.reserve<uint32_t>(size_t(B) * d.L);
+    size_t o_rbox = pb.reserve<float>(size_t(B) * 4), o_tbox = pb.reserve<float>(size_t(B) * 4);
     size_t o_lts = pb.reserve<double>(size_t(B) * d.NL), o_ltst = pb.reserve<uint8_t>(size_t(B) * d.NL * d.T);
     size_t o_sts = pb.reserve<double>(size_t(B) * d.NS);
     pb.host.assign(pb.cursor, 0);
@@ -448,6 +450,27 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
                 pb.at<uint8_t>(o_rkd)[k] = uint8_t((f.kind & 15) | (f.dir << 4));
             }
         }
+        {
+            float bx0 = 3e38f, by0 = 3e38f, bx1 = -3e38f, by1 = -3e38f;
+            for (const auto& f : s.features)
+                for (size_t i = 0; i + 1 < f.xy.size(); i += 2) {
+                    bx0 = std::min(bx0, f.xy[i]);
+                    by0 = std::min(by0, f.xy[i + 1]);
+                    bx1 = std::max(bx1, f.xy[i]);
+                    by1 = std::max(by1, f.xy[i + 1]);
+                }
+            float* bb = pb.at<float>(o_rbox) + 4 * size_t(b);
+            bb[0] = bx0, bb[1] = by0, bb[2] = bx1, bb[3] = by1;
+            float tx0 = 3e38f, ty0 = 3e38f, tx1 = -3e38f, ty1 = -3e38f;
+            for (const auto& q : rpts[size_t(b)]) {
+                tx0 = std::min(tx0, q.x);
+                ty0 = std::min(ty0, q.y);
+                tx1 = std::max(tx1, q.x);
+                ty1 = std::max(ty1, q.y);
+            }
+            float* tb = pb.at<float>(o_tbox) + 4 * size_t(b);
+            tb[0] = tx0, tb[1] = ty0, tb[2] = tx1, tb[3] = ty1;
+        }
         const auto& rp = rpts[size_t(b)];
         for (size_t i = 0; i < rp.size(); ++i) {
             size_t k = size_t(b) * d.R + i;
@@ -465,6 +488,13 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
                 pb.at<double>(o_ly)[k] = lf.y[i];
                 pb.at<double>(o_ls)[k] = lf.s[i];
                 pb.at<double>(o_lhw)[k] = lf.hw[i];
+                if (i + 1 < lf.x.size()) {
+                    // point_segment_dist2's ab = b - a and len2 = ab.norm2() (geometry.cpp:18-19)
+                    double abx = lf.x[i + 1] - lf.x[i], aby = lf.y[i + 1] - lf.y[i];
+                    pb.at<double>(o_labx)[k] = abx;
+                    pb.at<double>(o_laby)[k] = aby;
+                    pb.at<double>(o_llen2)[k] = abx * abx + aby * aby;
+                }
             }
         }
         for (size_t k = 0; k < c.lights.size(); ++k) {
@@ -518,6 +548,11 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.ln_y = reinterpret_cast<const double*>(D + o_ly);
     pk.ln_s = reinterpret_cast<const double*>(D + o_ls);
     pk.ln_hw = reinterpret_cast<const double*>(D + o_lhw);
+    pk.ln_abx = reinterpret_cast<const double*>(D + o_labx);
+    pk.ln_aby = reinterpret_cast<const double*>(D + o_laby);
+    pk.ln_len2 = reinterpret_cast<const double*>(D + o_llen2);
+    pk.road_box = reinterpret_cast<const float4*>(D + o_rbox);
+    pk.route_box = reinterpret_cast<const float4*>(D + o_tbox);
     pk.ln_n = reinterpret_cast<const int32_t*>(D + o_ln);
     pk.ln_id = reinterpret_cast<const uint32_t*>(D + o_lid);
     pk.lt_s = reinterpret_cast<const double*>(D + o_lts);
@@ -529,7 +564,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     env->dt = dt;
     env->total_stop = total_stop;
     env->base.key_cap = std::max(d.P, d.R);
-    env->base.cand_cap = std::max(256, next_pow2(4 * std::max(env->cfg.n_road, env->cfg.n_route)));
+    env->base.cand_cap = std::max(256, next_pow2(2 * std::max(env->cfg.n_road, env->cfg.n_route)));
     env->sl = state_layout(B, total_stop);
     env->sol = stepout_layout(B);
     env->ol = obs_layout(B, env->cfg.n_agents, env->cfg.n_road, env->cfg.n_route);

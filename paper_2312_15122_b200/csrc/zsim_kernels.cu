@@ -1,17 +1,31 @@
 // zsim_kernels.cu -- sm_100a kernels for the batched simulator step.
 //
-// One CTA (128 threads, 4 warps) per scenario row.  Within a CTA:
-//   * route projection: warps own lanes, lanes own segments; per-query argmin
-//     by (d2, segment) with warp shuffles (roads.cpp:125-166);
-//   * collision / agent features: threads own agents, 16-lane groups own the
-//     16 edge pairs of obb_distance (geometry.cpp:65-88);
-//   * top-k (road 128-of-P, route 64-of-R): fp32 keys in shared memory,
-//     packed-counter histograms to find a threshold, compaction of the few
-//     candidates that can make the cut, exact fp64 keys for those only, and a
-//     shared-memory bitonic sort by (d2, index) -- the exact reference order
-//     (roads.cpp:210-236, simcore.cpp:503-529).
-// Everything compiles with -fmad=false so every fp64 expression rounds like
-// the reference built with -ffp-contract=off.
+// Execution model: ONE WARP PER SCENARIO ROW.  A CTA holds kThreads/32
+// independent warps; each walks scenario rows in a grid-stride loop and never
+// waits on another warp (no __syncthreads on the hot path).  Per row, in one
+// launch:
+//
+//   step     bicycle_step -> route projection of the ego and of the four
+//            inflated footprint corners (lane-of-route x segment across the 32
+//            lanes, per-query argmin by (d2, segment) with REDUX) -> collision
+//            SAT against the agents valid at t+1 (one agent per lane) ->
+//            lights, stop lines, goal, done priority, reward
+//            (roads.cpp:125-208, simcore.cpp:278-404)
+//   observe  active/value features; agent boxes reused from the collision
+//            test when fused; obb_distance only for agents whose distance
+//            bounds can reach the top n_agents; road / route top-k
+//            (simcore.cpp:423-538)
+//
+// Top-k (road 128-of-P within 100 m, route 64-of-R): one pass computes fp32
+// squared distances and a 32-bucket pseudo-log histogram (lane-private smem
+// counters, bank-conflict-free) which yields a threshold with >= k points
+// under it; a second pass compacts, with ballots, the points that can make
+// the cut (fp32 error bound included); only those get exact fp64 keys, and a
+// counting sort on the exact keys (+ rank inside a bucket) emits the
+// reference's exact (d2, index) order.
+//
+// Every translation unit on the path builds with -fmad=false: each fp64
+// expression rounds like the reference compiled with -ffp-contract=off.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -24,210 +38,284 @@ namespace zs {
 
 namespace {
 
-constexpr int NT = kThreads;
-constexpr int NW = NT / 32;
-constexpr int NQ = 5;  // projection queries per step: ego position + 4 inflated corners
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NQ = 5;     // projection queries per step: ego position + 4 inflated corners
+constexpr int NB2 = 256;  // counting-sort buckets over the exact keys
+constexpr int kUnroll = 8;  // independent point loads in flight per lane in the key passes
 
-struct LaneRes {
-    double s, d, hw;
-    int set;
-};
-
-struct Smem {
-    // row state (pre-step, then post-step)
-    double x, y, h, v, steer, proj_s, proj_d;
-    uint64_t rng;
-    int t, done, reason, events, in_corr;
-    int skip;  // 1 = done pass-through, 2 = bad action
-    // step scratch
-    double accel, rate;
-    double nx, ny, nh, nv, nsteer;
-    double qx[NQ], qy[NQ];
-    Box ebox;
-    double ebx[4], eby[4];
-    LaneRes lres[kMaxLanes][NQ];
-    double p1s, p1d;
-    int p1_in;
-    // observe scratch
-    double oc, os;
-    int n_sel;
-    // top-k scratch
-    unsigned long long hist[NW][4];
-    float lo, hi, tcand;
-    int below, round_done, ccount, overflow, nvalid;
-    double red_key[NW];
-    int red_idx[NW];
-};
-
-__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_in_block() { return threadIdx.x >> 5; }
+__device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
 
-// Dynamic shared-memory carve-up (host mirror: smem_bytes()).
-struct Dyn {
-    float* akey;   // [key_cap] fp32 approximate keys
-    int* cidx;     // [cand_cap] candidate indices
-    double* ckey;  // [cand_cap] exact fp64 keys
-    double* agx;   // [A*4] agent corners
+// TMA-unit bulk prefetch of a byte range into L2 (cp.async.bulk.prefetch,
+// sm_90+): one instruction per array, no registers or smem held.
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+    uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    uintptr_t a0 = a & ~uintptr_t(15);
+    size_t n = (bytes + (a - a0) + 15) & ~size_t(15);
+    while (n > 0) {
+        unsigned chunk = unsigned(n > (1u << 20) ? (1u << 20) : n);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(chunk) : "memory");
+        a0 += chunk;
+        n -= chunk;
+    }
+}
+
+// Lexicographic warp argmin by (d2, idx) for d2 >= 0 (or +inf): the bit
+// pattern of a non-negative double is monotone, so three 32-bit REDUX ops.
+__device__ __forceinline__ void warp_argmin(double d2, int idx, double& out_d2, int& out_idx) {
+    unsigned hi = unsigned(__double2hiint(d2)), lo = unsigned(__double2loint(d2));
+    unsigned mhi = __reduce_min_sync(FULL, hi);
+    unsigned mlo = __reduce_min_sync(FULL, hi == mhi ? lo : 0xffffffffu);
+    bool eq = hi == mhi && lo == mlo;
+    unsigned mi = __reduce_min_sync(FULL, eq ? unsigned(idx) : 0xffffffffu);
+    out_d2 = __hiloint2double(int(mhi), int(mlo));
+    out_idx = int(mi);
+}
+
+template <class T>
+__device__ __forceinline__ T pick5(int k, T a0, T a1, T a2, T a3, T a4) {
+    return k == 0 ? a0 : k == 1 ? a1 : k == 2 ? a2 : k == 3 ? a3 : a4;
+}
+
+// Per-warp shared-memory carve-up (host mirror: smem_bytes()).
+struct WarpBuf {
+    double* agx;           // [A*4] agent corners
     double* agy;
-    double* agd;   // [A] agent bbox distance (or +inf if invalid)
-    int* agov;     // [A] -1 invalid, 0 separate, 1 overlap
-    int* sel;      // [Ka + Kr + Kl] selected indices
+    double* agd;           // [A] bbox distance
+    int* agf;              // [A] -1 invalid, 0 separate, 1 overlap
+    int* surv;             // [A] agents whose bounds can reach the top n_agents
+    unsigned* hist;        // [32*32] lane-private histogram; reused as counting-sort counts [NB2]
+    int* cidx;             // [cap] candidate indices
+    double* ckey;          // [cap] exact keys
+    int* cinfo;            // [cap] bucket << 16 | slot
+    int* order;            // [cap] candidates grouped by bucket
+    int* sel;              // [Ka + Kr + Kl] selected indices
     unsigned char* sflag;  // [NS] pre-step stopped flags
 };
 
+__host__ __device__ inline size_t al16(size_t v) { return (v + 15) / 16 * 16; }
 
-__device__ Dyn carve(unsigned char* base, const KernelArgs& a) {
-    Dyn d;
-    size_t off = 0;
-    d.ckey = reinterpret_cast<double*>(base + off);
-    off += size_t(a.cand_cap) * 8;
-    d.agx = reinterpret_cast<double*>(base + off);
-    off += size_t(a.pk.d.A) * 4 * 8;
-    d.agy = reinterpret_cast<double*>(base + off);
-    off += size_t(a.pk.d.A) * 4 * 8;
-    d.agd = reinterpret_cast<double*>(base + off);
-    off += size_t(a.pk.d.A) * 8;
-    d.akey = reinterpret_cast<float*>(base + off);
-    off += size_t(a.key_cap) * 4;
-    d.cidx = reinterpret_cast<int*>(base + off);
-    off += size_t(a.cand_cap) * 4;
-    d.agov = reinterpret_cast<int*>(base + off);
-    off += size_t(a.pk.d.A) * 4;
-    d.sel = reinterpret_cast<int*>(base + off);
-    off += size_t(a.cfg.n_agents + a.cfg.n_road + a.cfg.n_route) * 4;
-    d.sflag = base + off;
-    return d;
+__host__ __device__ inline size_t warp_smem_bytes(int A, int cap, int ksum, int ns) {
+    size_t o = 0;
+    o += al16(size_t(A) * 4 * 8) * 2;
+    o += al16(size_t(A) * 8);
+    o += al16(size_t(A) * 4) * 2;
+    o += 32 * 32 * 4;
+    o += al16(size_t(cap) * 4);
+    o += al16(size_t(cap) * 8);
+    o += al16(size_t(cap) * 4) * 2;
+    o += al16(size_t(ksum) * 4);
+    o += al16(size_t(ns) + 1);
+    return al16(o);
 }
 
-// ---------------------------------------------------------------------------
-// route projection of NQ query points (roads.cpp:125-166 / 192-198)
-// ---------------------------------------------------------------------------
-template <int Q>
-__device__ void project_queries(const DevPack& pk, int b, Smem& sm) {
+__device__ WarpBuf carve(unsigned char* base, const KernelArgs& a) {
+    const int A = a.pk.d.A, cap = a.cand_cap;
+    const int ksum = a.cfg.n_agents + a.cfg.n_road + a.cfg.n_route;
+    unsigned char* p = base + warp_smem_bytes(A, cap, ksum, a.pk.d.NS) * size_t(warp_in_block());
+    WarpBuf w;
+    size_t o = 0;
+    w.agx = reinterpret_cast<double*>(p + o);
+    o += al16(size_t(A) * 4 * 8);
+    w.agy = reinterpret_cast<double*>(p + o);
+    o += al16(size_t(A) * 4 * 8);
+    w.agd = reinterpret_cast<double*>(p + o);
+    o += al16(size_t(A) * 8);
+    w.agf = reinterpret_cast<int*>(p + o);
+    o += al16(size_t(A) * 4);
+    w.surv = reinterpret_cast<int*>(p + o);
+    o += al16(size_t(A) * 4);
+    w.hist = reinterpret_cast<unsigned*>(p + o);
+    o += 32 * 32 * 4;
+    w.cidx = reinterpret_cast<int*>(p + o);
+    o += al16(size_t(cap) * 4);
+    w.ckey = reinterpret_cast<double*>(p + o);
+    o += al16(size_t(cap) * 8);
+    w.cinfo = reinterpret_cast<int*>(p + o);
+    o += al16(size_t(cap) * 4);
+    w.order = reinterpret_cast<int*>(p + o);
+    o += al16(size_t(cap) * 4);
+    w.sel = reinterpret_cast<int*>(p + o);
+    o += al16(size_t(ksum) * 4);
+    w.sflag = p + o;
+    return w;
+}
+
+// Row state, uniform across the warp (every lane holds the same values).
+struct Row {
+    double x, y, h, v, steer, proj_s, proj_d;
+    unsigned long long rng;
+    int t, done, reason, events, in_corr;
+};
+
+__device__ __forceinline__ Row load_row(const zsim_state_view& in, int b) {
+    Row r;
+    r.x = in.x[b];
+    r.y = in.y[b];
+    r.h = in.heading[b];
+    r.v = in.v[b];
+    r.steer = in.steering[b];
+    r.t = in.t[b];
+    r.done = in.done[b];
+    r.reason = in.reason[b];
+    r.rng = in.rng[b];
+    r.proj_s = in.proj_s[b];
+    r.proj_d = in.proj_d[b];
+    r.in_corr = in.proj_in_corridor[b];
+    r.events = in.events[b];
+    return r;
+}
+
+__device__ __forceinline__ void store_row(const zsim_state_view& out, int b, const Row& r) {
+    out.x[b] = r.x;
+    out.y[b] = r.y;
+    out.heading[b] = r.h;
+    out.v[b] = r.v;
+    out.steering[b] = r.steer;
+    out.t[b] = r.t;
+    out.done[b] = uint8_t(r.done);
+    out.reason[b] = uint8_t(r.reason);
+    out.rng[b] = r.rng;
+    out.proj_s[b] = r.proj_s;
+    out.proj_d[b] = r.proj_d;
+    out.proj_in_corridor[b] = uint8_t(r.in_corr);
+    out.events[b] = uint8_t(r.events);
+}
+
+// point_segment_dist2 (geometry.cpp:17-25) with ab / len2 precomputed on the
+// host by the same expressions.  When the clamp decides t (dot <= 0 or
+// dot >= len2) the division is skipped: clamp(dot/len2, 0, 1) is then exactly
+// 0 (up to the sign of a zero, which changes no result) or exactly 1.
+__device__ __forceinline__ double seg_d2_pre(double px, double py, double ax, double ay, double abx, double aby,
+                                             double len2, double& t_out) {
+    double t = 0.0;
+    if (len2 > 0.0) {
+        double dot = (px - ax) * abx + (py - ay) * aby;
+        if (dot >= len2)
+            t = 1.0;
+        else if (dot > 0.0)
+            t = dot / len2;
+    }
+    double qx = ax + abx * t, qy = ay + aby * t;
+    double ex = px - qx, ey = py - qy;
+    t_out = t;
+    return ex * ex + ey * ey;
+}
+
+struct Proj {
+    double s, d;
+    int in_corr;   // query 0 lies in some lane corridor (roads.cpp:154)
+    int on_route;  // all four inflated corners lie in some corridor (roads.cpp:192-208)
+};
+
+// roads::project for NQU queries (q0 = the point; q1..4 = footprint corners
+// when NQU == 5): per route lane the first strictly smaller d2 segment
+// (roads.cpp:125-143), across lanes min |d| then lane_id (roads.cpp:147-166).
+// Uniform result.
+template <int NQU>
+__device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const double* qy) {
     const int L = pk.d.L, C = pk.d.C;
     const int nl = pk.n_lanes[b];
-    for (int l = warp_id(); l < nl; l += NW) {
+    const int lane = lane_id();
+    bool have = false;
+    double best_abs = 0.0, best_s = 0.0, best_d = 0.0;
+    uint32_t best_id = 0;
+    unsigned in_bits = 0;
+    for (int l = 0; l < nl; ++l) {
         const size_t base = (size_t(b) * L + l) * C;
-        const double* X = pk.ln_x + base;
-        const double* Y = pk.ln_y + base;
         const int nv = pk.ln_n[size_t(b) * L + l];
-        double bd2[Q];
-        int bi[Q];
+        double bd2[NQU];
+        int bi[NQU];
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
+        for (int q = 0; q < NQU; ++q) {
             bd2[q] = 1e300;
             bi[q] = INT_MAX;
         }
-        for (int i = lane_id(); i + 1 < nv; i += 32) {
-            double ax = X[i], ay = Y[i], bx = X[i + 1], by = Y[i + 1];
+        for (int i = lane; i + 1 < nv; i += 32) {
+            const double ax = pk.ln_x[base + i], ay = pk.ln_y[base + i];
+            const double abx = pk.ln_abx[base + i], aby = pk.ln_aby[base + i], len2 = pk.ln_len2[base + i];
 #pragma unroll
-            for (int q = 0; q < Q; ++q) {
+            for (int q = 0; q < NQU; ++q) {
                 double t;
-                double d2 = seg_dist2(sm.qx[q], sm.qy[q], ax, ay, bx, by, &t);
+                double d2 = seg_d2_pre(qx[q], qy[q], ax, ay, abx, aby, len2, t);
                 if (d2 < bd2[q]) {
                     bd2[q] = d2;
                     bi[q] = i;
                 }
             }
         }
+        double wd2[NQU];
+        int wi[NQU];
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                double od = __shfl_xor_sync(0xffffffffu, bd2[q], off);
-                int oi = __shfl_xor_sync(0xffffffffu, bi[q], off);
-                if (od < bd2[q] || (od == bd2[q] && oi < bi[q])) {
-                    bd2[q] = od;
-                    bi[q] = oi;
-                }
+        for (int q = 0; q < NQU; ++q) warp_argmin(bd2[q], bi[q], wd2[q], wi[q]);
+        // lane q evaluates query q's winning segment: s, signed d, half-width (roads.cpp:130-139)
+        bool ok = false;
+        double hs = 0.0, hd = 0.0;
+        if (lane < NQU) {
+            int i;
+            double px, py;
+            if constexpr (NQU == 1) {
+                i = wi[0];
+                px = qx[0];
+                py = qy[0];
+            } else {
+                i = pick5(lane, wi[0], wi[1], wi[2], wi[3], wi[4]);
+                px = pick5(lane, qx[0], qx[1], qx[2], qx[3], qx[4]);
+                py = pick5(lane, qy[0], qy[1], qy[2], qy[3], qy[4]);
+            }
+            if (i != INT_MAX) {
+                double t;
+                double d2 = seg_d2_pre(px, py, pk.ln_x[base + i], pk.ln_y[base + i], pk.ln_abx[base + i],
+                                       pk.ln_aby[base + i], pk.ln_len2[base + i], t);
+                LaneHit h =
+                    lane_hit(px, py, pk.ln_x + base, pk.ln_y + base, pk.ln_s + base, pk.ln_hw + base, i, d2, t);
+                hs = h.s;
+                hd = h.d;
+                ok = fabs(h.d) <= h.hw;
             }
         }
-        if (lane_id() == 0) {
-#pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                LaneRes r;
-                r.set = bi[q] != INT_MAX;
-                r.s = r.d = r.hw = 0.0;
-                if (r.set) {
-                    int i = bi[q];
-                    double t;
-                    double d2 = seg_dist2(sm.qx[q], sm.qy[q], X[i], Y[i], X[i + 1], Y[i + 1], &t);
-                    LaneHit h = lane_hit(sm.qx[q], sm.qy[q], X, Y, pk.ln_s + base, pk.ln_hw + base, i, d2, t);
-                    r.s = h.s;
-                    r.d = h.d;
-                    r.hw = h.hw;
-                }
-                sm.lres[l][q] = r;
+        in_bits |= __ballot_sync(FULL, ok);
+        if (wi[0] != INT_MAX) {
+            double s0 = __shfl_sync(FULL, hs, 0), d0 = __shfl_sync(FULL, hd, 0);
+            uint32_t id = pk.ln_id[size_t(b) * L + l];
+            if (!have || fabs(d0) < best_abs || (fabs(d0) == best_abs && id < best_id)) {
+                have = true;
+                best_abs = fabs(d0);
+                best_s = s0;
+                best_d = d0;
+                best_id = id;
             }
         }
     }
+    Proj p;
+    p.s = clampd(best_s, 0.0, pk.route_len[b]);
+    p.d = best_d;
+    p.in_corr = int(in_bits & 1u);
+    p.on_route = NQU == 5 ? int((in_bits & 0x1Eu) == 0x1Eu) : 1;
+    return p;
 }
 
-// roads::project combination across lanes for query q (roads.cpp:147-166).
-__device__ void combine_projection(const DevPack& pk, int b, const Smem& sm, int q, double& s, double& d,
-                                   int& in_corr) {
-    const int nl = pk.n_lanes[b];
-    bool have = false;
-    in_corr = 0;
-    double bs = 0.0, bdd = 0.0;
-    uint32_t bid = 0;
-    for (int l = 0; l < nl; ++l) {
-        const LaneRes& r = sm.lres[l][q];
-        if (!r.set) continue;
-        if (fabs(r.d) <= r.hw) in_corr = 1;
-        uint32_t id = pk.ln_id[size_t(b) * pk.d.L + l];
-        if (!have || fabs(r.d) < fabs(bdd) || (fabs(r.d) == fabs(bdd) && id < bid)) {
-            bs = r.s;
-            bdd = r.d;
-            bid = id;
-            have = true;
-        }
-    }
-    s = clampd(bs, 0.0, pk.route_len[b]);
-    d = bdd;
-}
-
-// ---------------------------------------------------------------------------
-// block reductions
-// ---------------------------------------------------------------------------
-__device__ float block_max_f(float v, Smem& sm) {
+// Agent box at log slice `slice` (agent_box, simcore.cpp:162-165): corners
+// into smem and the SAT overlap with the ego box (geometry.cpp:65-75).
+__device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int b, size_t slice, int j, const Box& eb,
+                                                 const double* EX, const double* EY, const WarpBuf& w) {
+    const int A = pk.d.A;
+    double h = double(pk.ag_h[slice + j]);
+    Box ab;
+    ab.cx = double(pk.ag_x[slice + j]);
+    ab.cy = double(pk.ag_y[slice + j]);
+    ab.hl = double(pk.ag_len[size_t(b) * A + j]) * 0.5;
+    ab.hw = double(pk.ag_wid[size_t(b) * A + j]) * 0.5;
+    sincos(h, &ab.s, &ab.c);
+    double X[4], Y[4];
+    box_corners(ab, X, Y);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-    __syncthreads();
-    if (lane_id() == 0) sm.red_key[warp_id()] = double(v);
-    __syncthreads();
-    float m = float(sm.red_key[0]);
-    for (int w = 1; w < NW; ++w) m = fmaxf(m, float(sm.red_key[w]));
-    __syncthreads();
-    return m;
-}
-
-// (key, idx) lexicographic argmin across the block; result broadcast.
-__device__ void block_argmin(double& key, int& idx, Smem& sm) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        double ok = __shfl_xor_sync(0xffffffffu, key, off);
-        int oi = __shfl_xor_sync(0xffffffffu, idx, off);
-        if (ok < key || (ok == key && oi < idx)) {
-            key = ok;
-            idx = oi;
-        }
+    for (int k = 0; k < 4; ++k) {
+        w.agx[4 * j + k] = X[k];
+        w.agy[4 * j + k] = Y[k];
     }
-    __syncthreads();
-    if (lane_id() == 0) {
-        sm.red_key[warp_id()] = key;
-        sm.red_idx[warp_id()] = idx;
-    }
-    __syncthreads();
-    key = sm.red_key[0];
-    idx = sm.red_idx[0];
-    for (int w = 1; w < NW; ++w) {
-        if (sm.red_key[w] < key || (sm.red_key[w] == key && sm.red_idx[w] < idx)) {
-            key = sm.red_key[w];
-            idx = sm.red_idx[w];
-        }
-    }
-    __syncthreads();
+    return boxes_overlap(eb, EX, EY, ab, X, Y) ? 1 : 0;
 }
 
 // Upper bound on |fp32 key - fp64 key| for points within sqrt(T)+1 of the
@@ -240,239 +328,261 @@ __device__ __forceinline__ double key_margin(double T, double ep) {
     return m * 1.25 + 1e-30;
 }
 
-// Threshold k of the current histogram round: lo + (k+1)*w, capped at hi.
-__device__ __forceinline__ float round_th(float lo, float w, float hi, int k) {
-    return k >= 15 ? hi : fminf(hi, lo + float(k + 1) * w);
+__device__ __forceinline__ float approx_key(float2 p, float pxf, float pyf) {
+    float dx = p.x - pxf, dy = p.y - pyf;
+    return __fmaf_rn(dx, dx, __fmul_rn(dy, dy));
+}
+
+// Squared distance from (px, py) to the farthest corner of a point set's
+// bounding box: an upper bound on every key of the set.
+__device__ __forceinline__ double box_far_d2(float4 bb, double px, double py) {
+    double dx = fmax(fabs(double(bb.x) - px), fabs(double(bb.z) - px));
+    double dy = fmax(fabs(double(bb.y) - py), fabs(double(bb.w) - py));
+    return dx * dx + dy * dy;
+}
+
+// Warp-wide bucket counts: lane k returns bucket k's count; clears the histogram.
+__device__ __forceinline__ unsigned hist_reduce(unsigned* hist) {
+    const int lane = lane_id();
+    unsigned mine = 0;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+        unsigned v = hist[k * 32 + lane];
+        hist[k * 32 + lane] = 0;
+        unsigned s = __reduce_add_sync(FULL, v);
+        if (lane == k) mine = s;
+    }
+    return mine;
+}
+
+__device__ __forceinline__ unsigned warp_incl_scan(unsigned v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        unsigned o = __shfl_up_sync(FULL, v, off);
+        if (lane >= off) v += o;
+    }
+    return v;
+}
+
+// Ballot compaction of the points with approx key <= tc; returns the count
+// (may exceed cap; only the first cap indices are stored).
+__device__ __forceinline__ int compact(const float2* __restrict__ pts, int n, float pxf, float pyf, float tc, int cap,
+                                       int* cidx) {
+    const int lane = lane_id();
+    int C = 0;
+    for (int i0 = 0; i0 < n; i0 += 32 * kUnroll) {
+        float2 pb[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            int i = i0 + u * 32 + lane;
+            pb[u] = i < n ? pts[i] : make_float2(INFINITY, INFINITY);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            int i = i0 + u * 32 + lane;
+            bool take = i < n && approx_key(pb[u], pxf, pyf) <= tc;
+            unsigned m = __ballot_sync(FULL, take);
+            if (m) {
+                int pos = C + __popc(m & lanemask_lt());
+                if (take && pos < cap) cidx[pos] = i;
+                C += __popc(m);
+            }
+        }
+    }
+    __syncwarp();
+    return C;
 }
 
 // ---------------------------------------------------------------------------
-// block top-k by (exact fp64 d2, index) over n points given by `pts`
-// (float2).  With `use_radius`, only points with exact d2 <= r2 qualify
-// (roads.cpp:219-229).  Writes up to K indices to `sel` in order; returns the
-// count.  All threads must call.
+// Warp top-k by (exact fp64 d2, index) over n points `pts` (float2).  With
+// use_r only points with exact d2 <= r2 qualify (roads.cpp:219-229).  Writes
+// the selected indices in order to sel[0..ret).
 // ---------------------------------------------------------------------------
-__device__ int block_topk(const float2* __restrict__ pts, int n, int K, double px, double py, bool use_radius,
-                          double r2, const Dyn& ws, int key_cap, int cand_cap, int* sel, Smem& sm) {
-    const int tid = threadIdx.x;
+__device__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px, double py, bool use_r, double r2,
+                         float4 bbox, int cap, const WarpBuf& w, int* sel) {
+    const int lane = lane_id();
+    if (n <= 0) return 0;
     const float pxf = float(px), pyf = float(py);
     const double ep = fmax(fabs(double(pxf) - px), fabs(double(pyf) - py));
+    double hi_d = box_far_d2(bbox, px, py);
+    hi_d += key_margin(hi_d, ep);
+    if (use_r) hi_d = fmin(hi_d, r2 + key_margin(r2, ep));
+    const float hi = __double2float_ru(hi_d);
+    // pseudo-log buckets: 2 per octave of the key; the top bucket holds hi
+    const int top = int(__float_as_uint(hi) >> 22);
+    const int base = max(top - 31, 0);
 
-    // 1. fp32 keys
-    float kmax = 0.f;
-    for (int i = tid; i < n; i += NT) {
-        float2 p = pts[i];
-        float dx = p.x - pxf, dy = p.y - pyf;
-        float a = dx * dx + dy * dy;
-        ws.akey[i] = a;
-        kmax = fmaxf(kmax, a);
+    // pass 1: histogram of the fp32 keys <= hi (loads batched for MLP)
+    for (int i0 = 0; i0 < n; i0 += 32 * kUnroll) {
+        float2 pb[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            int i = i0 + u * 32 + lane;
+            pb[u] = i < n ? pts[i] : make_float2(INFINITY, INFINITY);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            float a = approx_key(pb[u], pxf, pyf);
+            if (a <= hi) {
+                int bk = min(31, max(0, int(__float_as_uint(a) >> 22) - base));
+                w.hist[bk * 32 + lane] += 1;
+            }
+        }
     }
-    float hi;
-    if (use_radius) {
-        hi = __double2float_ru(r2 + key_margin(r2, ep));
+    __syncwarp();
+    unsigned cnt = hist_reduce(w.hist);
+    unsigned incl = warp_incl_scan(cnt);
+    const unsigned total = __shfl_sync(FULL, incl, 31);
+    double tcand, tsel = double(hi);
+    int kstar = 31;
+    if (total <= unsigned(K)) {
+        tcand = double(hi);  // every qualifying point is a candidate
     } else {
-        hi = block_max_f(kmax, sm);  // also orders the akey writes
+        kstar = __ffs(__ballot_sync(FULL, incl >= unsigned(K))) - 1;
+        tsel = kstar == 31 ? double(hi) : double(__uint_as_float(unsigned(kstar + base + 1) << 22));
+        double mg = key_margin(tsel, ep);
+        tcand = tsel + 2.0 * mg;
+        if (use_r && !(tsel + mg <= r2)) tcand = double(hi);
     }
-    __syncthreads();
+    float tc = fminf(__double2float_ru(tcand), hi);
 
-    // 2. histogram rounds over (lo, hi]: 16 buckets, packed 8-bit counters
-    if (tid == 0) {
-        sm.lo = -1.0f;
-        sm.hi = hi;
-        sm.below = 0;
-        sm.round_done = 0;
-    }
-    __syncthreads();
-    for (int round = 0; round < 3; ++round) {
-        const float lo = sm.lo, rhi = sm.hi;
-        const float w = (rhi - lo) * (1.0f / 16.0f);
-        const float inv_w = w > 0.f ? 1.0f / w : 0.f;
-        unsigned long long c0 = 0ull, c1 = 0ull;
-        for (int i = tid; i < n; i += NT) {
-            float a = ws.akey[i];
-            if (a > lo && a <= rhi) {
-                int bk = min(15, max(0, int((a - lo) * inv_w)));
-                while (bk > 0 && a <= round_th(lo, w, rhi, bk - 1)) --bk;
-                while (bk < 15 && a > round_th(lo, w, rhi, bk)) ++bk;
-                unsigned long long one = 1ull << ((bk & 7) * 8);
-                if (bk < 8)
-                    c0 += one;
-                else
-                    c1 += one;
+    // pass 2: ballot compaction of the candidates
+    int C = compact(pts, n, pxf, pyf, tc, cap, w.cidx);
+    if (C > cap && total > unsigned(K)) {
+        // refine inside bucket kstar with 32 linear sub-buckets
+        const float lo = kstar == 0 ? 0.f : __uint_as_float(unsigned(kstar + base) << 22);
+        const float hi2 = float(tsel);
+        const unsigned below = __shfl_sync(FULL, incl - cnt, kstar);
+        const float w2 = (hi2 - lo) * (1.0f / 32.0f);
+        const float inv2 = w2 > 0.f ? 1.0f / w2 : 0.f;
+        for (int i = lane; i < n; i += 32) {
+            float a = approx_key(pts[i], pxf, pyf);
+            if (a >= lo && a < hi2) {
+                int bk = min(31, max(0, int((a - lo) * inv2)));
+                w.hist[bk * 32 + lane] += 1;
             }
         }
-        // widen to 16-bit lanes: even/odd buckets
-        unsigned long long h[4];
-        h[0] = c0 & 0x00FF00FF00FF00FFull;         // buckets 0,2,4,6
-        h[1] = (c0 >> 8) & 0x00FF00FF00FF00FFull;  // 1,3,5,7
-        h[2] = c1 & 0x00FF00FF00FF00FFull;         // 8,10,12,14
-        h[3] = (c1 >> 8) & 0x00FF00FF00FF00FFull;  // 9,11,13,15
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) h[k] += __shfl_xor_sync(0xffffffffu, h[k], off);
-        }
-        if (lane_id() == 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) sm.hist[warp_id()][k] = h[k];
-        }
-        __syncthreads();
-        if (tid == 0) {
-            int cnt[16];
-            for (int k = 0; k < 16; ++k) cnt[k] = 0;
-            for (int wi = 0; wi < NW; ++wi) {
-                for (int k = 0; k < 4; ++k) {
-                    unsigned long long v = sm.hist[wi][k];
-                    for (int f = 0; f < 4; ++f) {
-                        int bucket = (k >> 1) * 8 + f * 2 + (k & 1);
-                        cnt[bucket] += int((v >> (16 * f)) & 0xFFFFull);
-                    }
-                }
-            }
-            int cum = sm.below;
-            int kstar = -1;
-            for (int k = 0; k < 16; ++k) {
-                if (cum + cnt[k] >= K) {
-                    kstar = k;
-                    break;
-                }
-                cum += cnt[k];
-            }
-            if (kstar < 0) {
-                // fewer than K points in (lo, hi] plus below: take everything up to hi
-                sm.round_done = 2;
-            } else {
-                float nlo = kstar == 0 ? lo : round_th(lo, w, rhi, kstar - 1);
-                float nhi = round_th(lo, w, rhi, kstar);
-                sm.below = cum;
-                sm.lo = nlo;
-                sm.hi = nhi;
-                // stop refining once the threshold bucket is small
-                if (cnt[kstar] <= 24 || !(nhi > nlo)) sm.round_done = 1;
+        __syncwarp();
+        cnt = hist_reduce(w.hist);
+        incl = warp_incl_scan(cnt) + below;
+        int k2 = __ffs(__ballot_sync(FULL, incl >= unsigned(K))) - 1;
+        if (k2 >= 0) {
+            double t2 = (double(lo) + double(k2 + 1) * double(w2)) * (1.0 + 1e-6) + 1e-30;
+            double mg = key_margin(t2, ep);
+            double tc2 = t2 + 2.0 * mg;
+            if (!(use_r && !(t2 + mg <= r2))) {
+                tc = fminf(__double2float_ru(tc2), tc);
+                C = compact(pts, n, pxf, pyf, tc, cap, w.cidx);
             }
         }
-        __syncthreads();
-        if (sm.round_done) break;
     }
-
-    // 3. candidate bound
-    if (tid == 0) {
-        double tsel = double(sm.hi);
-        double tc;
-        if (sm.round_done == 2) {
-            tc = double(hi);
-        } else {
-            double m = key_margin(tsel, ep);
-            tc = tsel + 2.0 * m;
-            if (use_radius && !(tsel + m <= r2)) tc = double(hi);
-        }
-        sm.tcand = __double2float_ru(tc);
-        sm.ccount = 0;
-        sm.overflow = 0;
-        sm.nvalid = 0;
-    }
-    __syncthreads();
-
-    // 4. compaction of candidates (warp ballot)
-    const float tcand = sm.tcand;
-    for (int base = 0; base < n; base += NT) {
-        int i = base + tid;
-        bool take = i < n && ws.akey[i] <= tcand;
-        unsigned m = __ballot_sync(0xffffffffu, take);
-        int wbase = 0;
-        if (lane_id() == 0 && m) wbase = atomicAdd(&sm.ccount, __popc(m));
-        wbase = __shfl_sync(0xffffffffu, wbase, 0);
-        if (take) {
-            int pos = wbase + __popc(m & ((1u << lane_id()) - 1u));
-            if (pos < cand_cap) ws.cidx[pos] = i;
-        }
-    }
-    __syncthreads();
-    const int C = sm.ccount;
-    if (C > cand_cap) {
+    if (C > cap) {
         // Pathological crowding at the threshold: exact iterative selection.
-        double pk = -1.0;
-        int pi = -1;
-        int nsel = 0;
+        double pk_ = -1.0;
+        int pi = -1, nsel = 0;
         for (int k = 0; k < K; ++k) {
             double best = INFINITY;
             int bi = INT_MAX;
-            for (int i = tid; i < n; i += NT) {
+            for (int i = lane; i < n; i += 32) {
                 float2 p = pts[i];
-                double dx = double(p.x) - px, dy2 = double(p.y) - py;
-                double e = dx * dx + dy2 * dy2;
-                if (use_radius && !(e <= r2)) continue;
-                bool after = e > pk || (e == pk && i > pi);
+                double dx = double(p.x) - px, dy = double(p.y) - py;
+                double e = dx * dx + dy * dy;
+                if (use_r && !(e <= r2)) continue;
+                bool after = e > pk_ || (e == pk_ && i > pi);
                 if (after && (e < best || (e == best && i < bi))) {
                     best = e;
                     bi = i;
                 }
             }
-            block_argmin(best, bi, sm);
-            if (bi == INT_MAX) break;
-            if (tid == 0) sel[k] = bi;
-            pk = best;
-            pi = bi;
+            double bd;
+            int bidx;
+            warp_argmin(best, bi, bd, bidx);
+            if (bidx == INT_MAX || !(bd < INFINITY)) break;
+            if (lane == 0) sel[k] = bidx;
+            pk_ = bd;
+            pi = bidx;
             ++nsel;
         }
-        __syncthreads();
+        __syncwarp();
         return nsel;
     }
 
-    // 5. exact keys for the candidates, padded to a power of two
-    int N2 = 1;
-    while (N2 < C) N2 <<= 1;
-    for (int c = tid; c < N2; c += NT) {
-        double e = INFINITY;
-        int idx = INT_MAX;
-        if (c < C) {
-            idx = ws.cidx[c];
-            float2 p = pts[idx];
-            double dx = double(p.x) - px, dyy = double(p.y) - py;
-            e = dx * dx + dyy * dyy;
-            if (use_radius && !(e <= r2)) e = INFINITY;
-            if (e < INFINITY) atomicAdd(&sm.nvalid, 1);
+    // exact fp64 keys (the reference's op order) + counting sort on them
+    unsigned* cntb = w.hist;  // NB2 counters in the (cleared) histogram area
+    const double sc2 = double(NB2) / (double(tc) > 0.0 ? double(tc) : 1.0);
+    int nvalid_local = 0;
+    for (int c = lane; c < C; c += 32) {
+        int i = w.cidx[c];
+        float2 p = pts[i];
+        double dx = double(p.x) - px, dy = double(p.y) - py;
+        double e = dx * dx + dy * dy;
+        int info = -1;
+        if (!use_r || e <= r2) {
+            int bk = min(NB2 - 1, int(e * sc2));
+            int slot = int(atomicAdd(&cntb[bk], 1u));
+            info = (bk << 16) | slot;
+            ++nvalid_local;
         }
-        ws.ckey[c] = e;
-        ws.cidx[c] = idx;
+        w.ckey[c] = e;
+        w.cinfo[c] = info;
     }
-    __syncthreads();
-
-    // 6. bitonic sort by (key, idx)
-    for (int k = 2; k <= N2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = tid; i < N2; i += NT) {
-                int ixj = i ^ j;
-                if (ixj > i) {
-                    double ka = ws.ckey[i], kb = ws.ckey[ixj];
-                    int ia = ws.cidx[i], ib = ws.cidx[ixj];
-                    bool a_gt = ka > kb || (ka == kb && ia > ib);
-                    bool up = (i & k) == 0;
-                    if (a_gt == up) {
-                        ws.ckey[i] = kb;
-                        ws.ckey[ixj] = ka;
-                        ws.cidx[i] = ib;
-                        ws.cidx[ixj] = ia;
-                    }
-                }
-            }
-            __syncthreads();
+    const int nvalid = int(__reduce_add_sync(FULL, unsigned(nvalid_local)));
+    __syncwarp();
+    {
+        unsigned v[NB2 / 32];
+        unsigned s = 0;
+#pragma unroll
+        for (int k = 0; k < NB2 / 32; ++k) {
+            v[k] = cntb[lane * (NB2 / 32) + k];
+            s += v[k];
+        }
+        unsigned run = warp_incl_scan(s) - s;
+#pragma unroll
+        for (int k = 0; k < NB2 / 32; ++k) {
+            cntb[lane * (NB2 / 32) + k] = run;  // bucket start
+            run += v[k];
         }
     }
-
-    // 7. emit (keys are sorted; non-qualifying candidates carry +inf and sort last)
-    const int nsel = min(K, sm.nvalid);
-    for (int c = tid; c < nsel; c += NT) sel[c] = ws.cidx[c];
-    __syncthreads();
-    return nsel;
+    __syncwarp();
+    for (int c = lane; c < C; c += 32) {
+        int info = w.cinfo[c];
+        if (info >= 0) w.order[cntb[info >> 16] + (info & 0xFFFF)] = c;
+    }
+    __syncwarp();
+    for (int c = lane; c < C; c += 32) {
+        int info = w.cinfo[c];
+        if (info < 0) continue;
+        int bk = info >> 16;
+        unsigned start = cntb[bk];
+        unsigned end = bk + 1 < NB2 ? cntb[bk + 1] : unsigned(nvalid);
+        double e = w.ckey[c];
+        int i = w.cidx[c];
+        unsigned rank = start;
+        for (unsigned q = start; q < end; ++q) {
+            int o = w.order[q];
+            double eo = w.ckey[o];
+            int io = w.cidx[o];
+            rank += (eo < e || (eo == e && io < i)) ? 1u : 0u;
+        }
+        if (rank < unsigned(K)) sel[rank] = i;
+    }
+    __syncwarp();
+    for (int k = lane; k < NB2; k += 32) cntb[k] = 0;
+    __syncwarp();
+    return min(K, nvalid);
 }
 
 // ---------------------------------------------------------------------------
-// observe one row (simcore.cpp:423-538) from the state held in `sm`
+// observe one row (simcore.cpp:423-538).  When `boxes_ready`, the agent boxes
+// at r.t and their overlap with the ego box `eb_in` are already in
+// w.agx/agy/agf (fused step+observe).
 // ---------------------------------------------------------------------------
-__device__ void observe_row(const KernelArgs& a, int b, Smem& sm, const Dyn& dy) {
+__device__ void observe_row(const KernelArgs& a, int b, const Row& r, const WarpBuf& w, bool boxes_ready,
+                            const Box& eb_in, const double* EX_in, const double* EY_in) {
     const DevPack& pk = a.pk;
     const DevCfg& cfg = a.cfg;
-    const int tid = threadIdx.x;
+    const int lane = lane_id();
     const int Ka = cfg.n_agents, Kr = cfg.n_road, Kl = cfg.n_route;
     float* act = a.obs.active + size_t(b) * 9;
     float* agt = a.obs.agents + size_t(b) * Ka * 6;
@@ -481,45 +591,56 @@ __device__ void observe_row(const KernelArgs& a, int b, Smem& sm, const Dyn& dy)
     float* val = a.obs.value_only + size_t(b) * 2;
     int32_t* dbg = a.dbg ? a.dbg + size_t(b) * (Ka + Kr + Kl) : nullptr;
 
-    if (sm.done) {
+    if (r.done) {
         // ObservationBatch::zero_row (simcore.cpp:37-43)
-        for (int i = tid; i < 9; i += NT) act[i] = 0.f;
-        for (int i = tid; i < Ka * 6; i += NT) agt[i] = 0.f;
-        for (int i = tid; i < Kr * 12; i += NT) rd[i] = 0.f;
-        for (int i = tid; i < Kl * 5; i += NT) rt[i] = 0.f;
-        if (tid < 2) val[tid] = 0.f;
+        for (int i = lane; i < 9; i += 32) act[i] = 0.f;
+        for (int i = lane; i < Ka * 6; i += 32) agt[i] = 0.f;
+        float4* rd4 = reinterpret_cast<float4*>(rd);
+        for (int i = lane; i < Kr * 3; i += 32) rd4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = lane; i < Kl * 5; i += 32) rt[i] = 0.f;
+        if (lane < 2) val[lane] = 0.f;
         if (dbg)
-            for (int i = tid; i < Ka + Kr + Kl; i += NT) dbg[i] = -1;
+            for (int i = lane; i < Ka + Kr + Kl; i += 32) dbg[i] = -1;
         return;
     }
 
-    const int t = sm.t;
-    if (tid == 0) {
-        sm.oc = cos(-sm.h);
-        sm.os = sin(-sm.h);
-        double c = cos(sm.h), s = sin(sm.h);
-        Box eb;
-        eb.cx = sm.x + c * cfg.ego_center_offset;
-        eb.cy = sm.y + s * cfg.ego_center_offset;
+    const int t = r.t;
+    double oc, os;
+    sincos(-r.h, &os, &oc);
+    Box eb;
+    double EX[4], EY[4];
+    if (boxes_ready) {
+        eb = eb_in;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            EX[k] = EX_in[k];
+            EY[k] = EY_in[k];
+        }
+    } else {
+        double c, s;
+        sincos(r.h, &s, &c);
+        eb.cx = r.x + c * cfg.ego_center_offset;
+        eb.cy = r.y + s * cfg.ego_center_offset;
         eb.hl = cfg.ego_length * 0.5;
         eb.hw = cfg.ego_width * 0.5;
         eb.c = c;
         eb.s = s;
-        sm.ebox = eb;
-        box_corners(eb, sm.ebx, sm.eby);
+        box_corners(eb, EX, EY);
+    }
 
-        // active features: roads::stop_info (roads.cpp:253-277), fill simcore.cpp:440-455
+    // ---- active features: roads::stop_info (roads.cpp:253-277), simcore.cpp:440-455 ----
+    {
         double best_stop = 1e300;
         const int ns = pk.n_stops[b];
         for (int j = 0; j < ns; ++j) {
-            double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - sm.proj_s;
+            double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - r.proj_s;
             if (ahead > 0.0 && ahead < best_stop) best_stop = ahead;
         }
         double best_light = 1e300;
         int best_k = -1;
         const int nlt = pk.n_lights[b];
         for (int k = 0; k < nlt; ++k) {
-            double ahead = pk.lt_s[size_t(b) * pk.d.NL + k] - sm.proj_s;
+            double ahead = pk.lt_s[size_t(b) * pk.d.NL + k] - r.proj_s;
             if (ahead > 0.0 && ahead < best_light) {
                 best_light = ahead;
                 best_k = k;
@@ -533,89 +654,136 @@ __device__ void observe_row(const KernelArgs& a, int b, Smem& sm, const Dyn& dy)
             light = pk.lt_state[(size_t(b) * pk.d.NL + best_k) * pk.d.T + step];
         }
         const double R = cfg.feature_radius;
-        float f[9];
-        for (int i = 0; i < 9; ++i) f[i] = 0.f;
-        f[0] = float(sm.v);
-        f[1] = float(sm.steer);
-        f[2] = float(best_stop < 1e300 ? mind(best_stop, R) : R);
-        f[3 + light] = 1.f;
-        f[7] = float(best_k >= 0 ? mind(best_light, R) : R);
-        f[8] = pk.speed_limit[b];
-        for (int i = 0; i < 9; ++i) act[i] = f[i];
-        // value-only (simcore.cpp:531-537)
-        double gx = double(pk.goal_x[b]) - sm.x, gy = double(pk.goal_y[b]) - sm.y;
-        val[0] = float(sqrt(gx * gx + gy * gy));
-        val[1] = float(pk.horizon - t);
-        sm.n_sel = 0;
+        if (lane < 9) {
+            float f = 0.f;
+            if (lane == 0) f = float(r.v);
+            if (lane == 1) f = float(r.steer);
+            if (lane == 2) f = float(best_stop < 1e300 ? mind(best_stop, R) : R);
+            if (lane >= 3 && lane <= 6) f = (lane - 3 == light) ? 1.f : 0.f;
+            if (lane == 7) f = float(best_k >= 0 ? mind(best_light, R) : R);
+            if (lane == 8) f = pk.speed_limit[b];
+            act[lane] = f;
+        }
+        // value-only features (simcore.cpp:531-537)
+        if (lane == 0) {
+            double gx = double(pk.goal_x[b]) - r.x, gy = double(pk.goal_y[b]) - r.y;
+            val[0] = float(sqrt(gx * gx + gy * gy));
+            val[1] = float(pk.horizon - t);
+        }
     }
-    __syncthreads();
 
-    // ---- agents: obb_distance to every valid agent, sort by (dist, idx) ----
-    const int A = pk.d.A, T = pk.d.T;
+    // ---- other agents: obb_distance, sorted by (dist, idx) (simcore.cpp:457-486) ----
+    const int A = pk.d.A;
     const int na = pk.n_agents[b];
     const bool t_ok = t < pk.num_steps[b];
-    const size_t aslice = (size_t(b) * T + (t_ok ? t : 0)) * A;
-    for (int j = tid; j < na; j += NT) {
-        int ov = -1;
-        if (t_ok && pk.ag_valid[aslice + j]) {
-            double h = double(pk.ag_h[aslice + j]);
-            Box ab;
-            ab.cx = double(pk.ag_x[aslice + j]);
-            ab.cy = double(pk.ag_y[aslice + j]);
-            ab.hl = double(pk.ag_len[size_t(b) * A + j]) * 0.5;
-            ab.hw = double(pk.ag_wid[size_t(b) * A + j]) * 0.5;
-            ab.c = cos(h);
-            ab.s = sin(h);
-            double* X = dy.agx + 4 * j;
-            double* Y = dy.agy + 4 * j;
-            box_corners(ab, X, Y);
-            ov = boxes_overlap(sm.ebox, sm.ebx, sm.eby, ab, X, Y) ? 1 : 0;
-            atomicAdd(&sm.n_sel, 1);
+    const size_t aslice = (size_t(b) * pk.d.T + (t_ok ? t : 0)) * A;
+    if (!boxes_ready) {
+        for (int j = lane; j < na; j += 32) {
+            int f = -1;
+            if (t_ok && pk.ag_valid[aslice + j]) f = agent_box_overlap(pk, b, aslice, j, eb, EX, EY, w);
+            w.agf[j] = f;
         }
-        dy.agov[j] = ov;
+        __syncwarp();
     }
-    __syncthreads();
-    for (int base = 0; base < na * 16; base += NT) {
-        int it = base + tid;
-        int j = it >> 4, p = it & 15;
-        double d2 = INFINITY;
-        if (j < na && dy.agov[j] == 0) {
-            d2 = box_edge_pair_dist2(sm.ebx, sm.eby, dy.agx + 4 * j, dy.agy + 4 * j, p >> 2, p & 3);
-        }
-#pragma unroll
-        for (int off = 8; off > 0; off >>= 1) d2 = mind(d2, __shfl_xor_sync(0xffffffffu, d2, off));
-        if (p == 0 && j < na) {
-            int ov = dy.agov[j];
-            dy.agd[j] = ov < 0 ? INFINITY : (ov == 1 ? 0.0 : sqrt(d2));
-        }
+    // Distance bounds: d <= |c_e - c_a| (both centres lie inside their boxes)
+    // and d >= |c_e - c_a| - r_e - r_a (circumradii).  An agent whose lower
+    // bound exceeds U, with >= Ka agents at upper bound <= U, cannot rank.
+    const float re = float(sqrt(eb.hl * eb.hl + eb.hw * eb.hw));
+    float my_min_ub = INFINITY;
+    for (int j = lane; j < na; j += 32) {
+        if (w.agf[j] < 0) continue;
+        float cx = 0.5f * float(w.agx[4 * j] + w.agx[4 * j + 2]);
+        float cy = 0.5f * float(w.agy[4 * j] + w.agy[4 * j + 2]);
+        float dx = cx - float(eb.cx), dy = cy - float(eb.cy);
+        float ub = sqrtf(dx * dx + dy * dy) * 1.0001f + 1e-3f;
+        my_min_ub = fminf(my_min_ub, ub);
     }
-    __syncthreads();
-    for (int j = tid; j < na; j += NT) {
-        if (dy.agov[j] < 0) continue;
-        double dj = dy.agd[j];
+    float U = INFINITY;
+    {
+        // Ka-th smallest per-lane minimum: >= Ka distinct agents lie at or under it
         int rank = 0;
-        for (int k = 0; k < na; ++k) {
-            if (dy.agov[k] < 0) continue;
-            double dk = dy.agd[k];
-            rank += (dk < dj || (dk == dj && k < j)) ? 1 : 0;
+        for (int k = 0; k < 32; ++k) {
+            float o = __shfl_sync(FULL, my_min_ub, k);
+            rank += (o < my_min_ub || (o == my_min_ub && k < lane)) ? 1 : 0;
         }
-        if (rank < Ka) dy.sel[rank] = j;
+        unsigned m = __ballot_sync(FULL, rank == Ka - 1 && my_min_ub < INFINITY);
+        if (Ka <= 32 && m) U = __shfl_sync(FULL, my_min_ub, __ffs(m) - 1);
     }
-    __syncthreads();
-    const int nvalid_ag = sm.n_sel;
-    const int nsel_ag = min(Ka, nvalid_ag);
-    const double oc = sm.oc, os = sm.os, ex = sm.x, ey = sm.y, eh = sm.h;
-    for (int k = tid; k < Ka; k += NT) {
+    int nsurv = 0;
+    for (int j0 = 0; j0 < na; j0 += 32) {
+        int j = j0 + lane;
+        bool keep = false;
+        if (j < na && w.agf[j] >= 0) {
+            float cx = 0.5f * float(w.agx[4 * j] + w.agx[4 * j + 2]);
+            float cy = 0.5f * float(w.agy[4 * j] + w.agy[4 * j + 2]);
+            float dx = cx - float(eb.cx), dy = cy - float(eb.cy);
+            double L2 = double(pk.ag_len[size_t(b) * A + j]), W2 = double(pk.ag_wid[size_t(b) * A + j]);
+            float ra = float(sqrt(L2 * L2 * 0.25 + W2 * W2 * 0.25));
+            float lb = sqrtf(dx * dx + dy * dy) * 0.9999f - re - ra - 1e-3f;
+            keep = lb <= U;
+        }
+        unsigned m = __ballot_sync(FULL, keep);
+        if (keep) w.surv[nsurv + __popc(m & lanemask_lt())] = j;
+        nsurv += __popc(m);
+    }
+    __syncwarp();
+    // Exact distance of each survivor: the 32 distinct point-to-edge d2 of
+    // obb_distance's 16 edge pairs (geometry.cpp:77-88), one per lane.
+    for (int s = 0; s < nsurv; ++s) {
+        const int j = w.surv[s];
+        if (w.agf[j] == 1) {
+            if (lane == 0) w.agd[j] = 0.0;
+            continue;
+        }
+        const double* AX = w.agx + 4 * j;
+        const double* AY = w.agy + 4 * j;
+        const int e = lane & 15, pi = e >> 2, sj = e & 3, sj1 = (sj + 1) & 3;
+        double d2;
+        if (lane < 16) {  // ego corner pi vs agent edge sj
+            d2 = seg_dist2(EX[pi], EY[pi], AX[sj], AY[sj], AX[sj1], AY[sj1]);
+        } else {  // agent corner pi vs ego edge sj
+            d2 = seg_dist2(AX[pi], AY[pi], EX[sj], EY[sj], EX[sj1], EY[sj1]);
+        }
+        double md2;
+        int dummy;
+        warp_argmin(d2, 0, md2, dummy);
+        if (md2 < 1e-18) {
+            // (near-)contact: a strict edge crossing is possible, so take the
+            // reference's full segment_segment_distance over the 16 pairs.
+            double v = INFINITY;
+            if (lane < 16) v = box_edge_pair_dist2(EX, EY, AX, AY, lane >> 2, lane & 3);
+            warp_argmin(v, 0, md2, dummy);
+        }
+        if (lane == 0) w.agd[j] = sqrt(md2);
+    }
+    __syncwarp();
+    for (int s0 = 0; s0 < nsurv; s0 += 32) {
+        int s = s0 + lane;
+        if (s < nsurv) {
+            int j = w.surv[s];
+            double dj = w.agd[j];
+            int rank = 0;
+            for (int q = 0; q < nsurv; ++q) {
+                int k = w.surv[q];
+                double dk = w.agd[k];
+                rank += (dk < dj || (dk == dj && k < j)) ? 1 : 0;
+            }
+            if (rank < Ka) w.sel[rank] = j;
+        }
+    }
+    const int nsel_ag = min(Ka, nsurv);
+    __syncwarp();
+    for (int k = lane; k < Ka; k += 32) {
         float f[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         int j = -1;
         if (k < nsel_ag) {
-            j = dy.sel[k];
-            double wx = double(pk.ag_x[aslice + j]) - ex, wy = double(pk.ag_y[aslice + j]) - ey;
+            j = w.sel[k];
+            double wx = double(pk.ag_x[aslice + j]) - r.x, wy = double(pk.ag_y[aslice + j]) - r.y;
             f[0] = float(oc * wx - os * wy);
             f[1] = float(os * wx + oc * wy);
-            f[2] = float(wrap_angle(double(pk.ag_h[aslice + j]) - eh));
+            f[2] = float(wrap_angle(double(pk.ag_h[aslice + j]) - r.h));
             f[3] = pk.ag_sp[aslice + j];
-            f[4] = float(dy.agd[j]);
+            f[4] = float(w.agd[j]);
             f[5] = 1.f;
         }
         float2* o = reinterpret_cast<float2*>(agt + k * 6);
@@ -624,17 +792,16 @@ __device__ void observe_row(const KernelArgs& a, int b, Smem& sm, const Dyn& dy)
         o[2] = make_float2(f[4], f[5]);
         if (dbg) dbg[k] = j;
     }
-    __syncthreads();
 
     // ---- road network points: nearest_features (roads.cpp:210-236) ----
     {
         const int n = pk.n_road[b];
         const float2* pts = pk.road_xy + size_t(b) * pk.d.P;
         const double R = cfg.feature_radius;
-        int* sel = dy.sel + Ka;
-        int nsel = block_topk(pts, n, Kr, ex, ey, true, R * R, dy, a.key_cap, a.cand_cap, sel, sm);
+        int* sel = w.sel + Ka;
+        const int nsel = warp_topk(pts, n, Kr, r.x, r.y, true, R * R, pk.road_box[b], a.cand_cap, w, sel);
         const uint8_t* kd = pk.road_kd + size_t(b) * pk.d.P;
-        for (int k = tid; k < Kr; k += NT) {
+        for (int k = lane; k < Kr; k += 32) {
             float f[12];
 #pragma unroll
             for (int i = 0; i < 12; ++i) f[i] = 0.f;
@@ -642,12 +809,14 @@ __device__ void observe_row(const KernelArgs& a, int b, Smem& sm, const Dyn& dy)
             if (k < nsel) {
                 i = sel[k];
                 float2 p = pts[i];
-                double wx = double(p.x) - ex, wy = double(p.y) - ey;
+                double wx = double(p.x) - r.x, wy = double(p.y) - r.y;
                 f[0] = float(oc * wx - os * wy);
                 f[1] = float(os * wx + oc * wy);
                 int kk = kd[i];
-                f[2 + (kk & 15)] = 1.f;
-                f[7 + (kk >> 4)] = 1.f;
+#pragma unroll
+                for (int q = 0; q < 5; ++q) f[2 + q] = (kk & 15) == q ? 1.f : 0.f;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) f[7 + q] = (kk >> 4) == q ? 1.f : 0.f;
                 f[11] = 1.f;
             }
             float4* o = reinterpret_cast<float4*>(rd + k * 12);
@@ -657,22 +826,21 @@ __device__ void observe_row(const KernelArgs& a, int b, Smem& sm, const Dyn& dy)
             if (dbg) dbg[Ka + k] = i;
         }
     }
-    __syncthreads();
 
     // ---- route border points: top n_route by (d2, idx), no radius (simcore.cpp:503-529) ----
     {
         const int n = pk.n_route[b];
         const float2* pts = pk.route_xy + size_t(b) * pk.d.R;
-        int* sel = dy.sel + Ka + Kr;
-        int nsel = block_topk(pts, n, Kl, ex, ey, false, 0.0, dy, a.key_cap, a.cand_cap, sel, sm);
+        int* sel = w.sel + Ka + Kr;
+        const int nsel = warp_topk(pts, n, Kl, r.x, r.y, false, 0.0, pk.route_box[b], a.cand_cap, w, sel);
         const uint8_t* fl = pk.route_fl + size_t(b) * pk.d.R;
-        for (int k = tid; k < Kl; k += NT) {
+        for (int k = lane; k < Kl; k += 32) {
             float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
             int i = -1;
             if (k < nsel) {
                 i = sel[k];
                 float2 p = pts[i];
-                double wx = double(p.x) - ex, wy = double(p.y) - ey;
+                double wx = double(p.x) - r.x, wy = double(p.y) - r.y;
                 f[0] = float(oc * wx - os * wy);
                 f[1] = float(os * wx + oc * wy);
                 f[2] = (fl[i] & 1) ? 1.f : 0.f;
@@ -680,6 +848,7 @@ __device__ void observe_row(const KernelArgs& a, int b, Smem& sm, const Dyn& dy)
                 f[4] = 1.f;
             }
             float* o = rt + k * 5;
+#pragma unroll
             for (int q = 0; q < 5; ++q) o[q] = f[q];
             if (dbg) dbg[Ka + Kr + k] = i;
         }
@@ -687,277 +856,221 @@ __device__ void observe_row(const KernelArgs& a, int b, Smem& sm, const Dyn& dy)
 }
 
 // ---------------------------------------------------------------------------
-// step one row (simcore.cpp:278-404); leaves the post-step state in `sm`
+// step one row (simcore.cpp:278-404).  Returns the post-step row; when the
+// row was simulated (not passed through) the agent boxes at t+1 and their
+// overlap with the new ego box stay in smem for a fused observe.
 // ---------------------------------------------------------------------------
-__device__ void step_row(const KernelArgs& a, int b, Smem& sm, const Dyn& dy) {
+__device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf& w, bool& boxes_ready, Box& eb,
+                        double* EX, double* EY) {
     const DevPack& pk = a.pk;
     const DevCfg& cfg = a.cfg;
-    const int tid = threadIdx.x;
+    const int lane = lane_id();
     const int ns = pk.n_stops[b];
     const int soff = pk.stop_off[b];
+    boxes_ready = false;
+    for (int j = lane; j < ns; j += 32) w.sflag[j] = a.in.stopped_flags[soff + j];
+    __syncwarp();
 
-    if (tid == 0) {
-        sm.skip = sm.done ? 1 : 0;
-        if (!sm.done) {
-            int ai = a.accel[b], si = a.steer[b];
-            if (ai < 0 || ai >= cfg.n_accel || si < 0 || si >= cfg.n_steer) {
-                atomicOr(a.err, 1);
-                sm.skip = 2;
-            } else {
-                sm.accel = cfg.accel_bins[ai];
-                sm.rate = cfg.steer_bins[si];
-                // dyn::bicycle_step (dynamics.cpp:10-19)
-                const double dt = pk.dt;
-                double c = cos(sm.h), s = sin(sm.h);
-                sm.nx = sm.x + sm.v * c * dt;
-                sm.ny = sm.y + sm.v * s * dt;
-                sm.nh = wrap_angle(sm.h + sm.v / cfg.wheelbase * tan(sm.steer) * dt);
-                sm.nv = maxd(sm.v + sm.accel * dt, cfg.v_min);
-                sm.nsteer = clampd(sm.steer + sm.rate * dt, -cfg.delta_max, cfg.delta_max);
-                // ego_box(e1) (simcore.cpp:156-160) and its inflated corners (roads.cpp:202-208)
-                double c1 = cos(sm.nh), s1 = sin(sm.nh);
-                Box eb;
-                eb.cx = sm.nx + c1 * cfg.ego_center_offset;
-                eb.cy = sm.ny + s1 * cfg.ego_center_offset;
-                eb.hl = cfg.ego_length * 0.5;
-                eb.hw = cfg.ego_width * 0.5;
-                eb.c = c1;
-                eb.s = s1;
-                sm.ebox = eb;
-                box_corners(eb, sm.ebx, sm.eby);
-                Box inf = eb;
-                inf.hl = eb.hl + cfg.footprint_margin;
-                inf.hw = eb.hw + cfg.footprint_margin;
-                double X[4], Y[4];
-                box_corners(inf, X, Y);
-                sm.qx[0] = sm.nx;
-                sm.qy[0] = sm.ny;
-                for (int k = 0; k < 4; ++k) {
-                    sm.qx[k + 1] = X[k];
-                    sm.qy[k + 1] = Y[k];
-                }
-            }
+    bool skip = r0.done != 0;
+    int ai = 0, si = 0;
+    if (!skip) {
+        ai = a.accel[b];
+        si = a.steer[b];
+        if (ai < 0 || ai >= cfg.n_accel || si < 0 || si >= cfg.n_steer) {
+            if (lane == 0) atomicOr(a.err, 1);
+            skip = true;
         }
     }
-    for (int j = tid; j < ns; j += NT) dy.sflag[j] = a.in.stopped_flags[soff + j];
-    __syncthreads();
-
-    if (sm.skip) {
+    if (skip) {
         // absorbing pass-through (simcore.cpp:281-299); bad-action rows are left unchanged
-        if (tid == 0) {
-            a.out.x[b] = sm.x;
-            a.out.y[b] = sm.y;
-            a.out.heading[b] = sm.h;
-            a.out.v[b] = sm.v;
-            a.out.steering[b] = sm.steer;
-            a.out.t[b] = sm.t;
-            a.out.done[b] = uint8_t(sm.done);
-            a.out.reason[b] = uint8_t(sm.reason);
-            a.out.rng[b] = sm.rng;
-            a.out.proj_s[b] = sm.proj_s;
-            a.out.proj_d[b] = sm.proj_d;
-            a.out.proj_in_corridor[b] = uint8_t(sm.in_corr);
-            a.out.events[b] = uint8_t(sm.events);
+        if (lane == 0) {
+            store_row(a.out, b, r0);
             a.so.reward[b] = 0.f;
             a.so.event[b] = 0;
-            a.so.s[b] = float(sm.proj_s);
+            a.so.s[b] = float(r0.proj_s);
             a.so.a_lat[b] = 0.f;
             a.so.a_lon[b] = 0.f;
-            a.so.v[b] = float(sm.v);
+            a.so.v[b] = float(r0.v);
         }
-        for (int j = tid; j < ns; j += NT) a.out.stopped_flags[soff + j] = dy.sflag[j];
-        __syncthreads();
-        return;
+        for (int j = lane; j < ns; j += 32) a.out.stopped_flags[soff + j] = w.sflag[j];
+        __syncwarp();
+        return r0;
     }
 
-    // projection of e1 and of the 4 inflated footprint corners
-    project_queries<NQ>(pk, b, sm);
+    const double accel = cfg.accel_bins[ai], rate = cfg.steer_bins[si];
+    const double dt = pk.dt;
+    // dyn::bicycle_step (dynamics.cpp:10-19)
+    double c0, s0;
+    sincos(r0.h, &s0, &c0);
+    Row r = r0;
+    r.x = r0.x + r0.v * c0 * dt;
+    r.y = r0.y + r0.v * s0 * dt;
+    r.h = wrap_angle(r0.h + r0.v / cfg.wheelbase * tan(r0.steer) * dt);
+    r.v = maxd(r0.v + accel * dt, cfg.v_min);
+    r.steer = clampd(r0.steer + rate * dt, -cfg.delta_max, cfg.delta_max);
+    r.t = r0.t + 1;
+    // ego_box(e1) (simcore.cpp:156-160) and its margin-inflated corners (roads.cpp:202-204)
+    double c1, s1;
+    sincos(r.h, &s1, &c1);
+    eb.cx = r.x + c1 * cfg.ego_center_offset;
+    eb.cy = r.y + s1 * cfg.ego_center_offset;
+    eb.hl = cfg.ego_length * 0.5;
+    eb.hw = cfg.ego_width * 0.5;
+    eb.c = c1;
+    eb.s = s1;
+    box_corners(eb, EX, EY);
+    double qx[NQ], qy[NQ];
+    {
+        Box inf = eb;
+        inf.hl = eb.hl + cfg.footprint_margin;
+        inf.hw = eb.hw + cfg.footprint_margin;
+        qx[0] = r.x;
+        qy[0] = r.y;
+        box_corners(inf, qx + 1, qy + 1);
+    }
+    const Proj p1 = warp_project<NQ>(pk, b, qx, qy);
 
-    // collision against agents valid at t+1 (simcore.cpp:323-331)
+    // collision with the agents valid at t+1 (simcore.cpp:323-331); boxes kept for observe(t+1)
     int hit = 0;
     {
-        const int t1 = sm.t + 1;
         const int na = pk.n_agents[b];
-        if (t1 < pk.num_steps[b]) {
-            const int A = pk.d.A;
-            const size_t slice = (size_t(b) * pk.d.T + t1) * A;
-            for (int j = tid; j < na; j += NT) {
-                if (!pk.ag_valid[slice + j]) continue;
-                double h = double(pk.ag_h[slice + j]);
-                Box ab;
-                ab.cx = double(pk.ag_x[slice + j]);
-                ab.cy = double(pk.ag_y[slice + j]);
-                ab.hl = double(pk.ag_len[size_t(b) * A + j]) * 0.5;
-                ab.hw = double(pk.ag_wid[size_t(b) * A + j]) * 0.5;
-                ab.c = cos(h);
-                ab.s = sin(h);
-                double X[4], Y[4];
-                box_corners(ab, X, Y);
-                if (boxes_overlap(sm.ebox, sm.ebx, sm.eby, ab, X, Y)) hit = 1;
-            }
+        const bool t_ok = r.t < pk.num_steps[b];
+        const size_t slice = (size_t(b) * pk.d.T + (t_ok ? r.t : 0)) * pk.d.A;
+        for (int j = lane; j < na; j += 32) {
+            int f = -1;
+            if (t_ok && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, b, slice, j, eb, EX, EY, w);
+            w.agf[j] = f;
+            hit |= f == 1;
+        }
+        hit = __any_sync(FULL, hit);
+        __syncwarp();
+        boxes_ready = true;
+    }
+
+    const bool hit_off_route = !p1.on_route;
+    bool hit_red = false;
+    {
+        const int nsteps = pk.num_steps[b];
+        const int t_light = r0.t < nsteps - 1 ? r0.t : nsteps - 1;
+        const int nlt = pk.n_lights[b];
+        for (int k = 0; k < nlt; ++k) {
+            double ls = pk.lt_s[size_t(b) * pk.d.NL + k];
+            if (r0.proj_s < ls && ls <= p1.s && pk.lt_state[(size_t(b) * pk.d.NL + k) * pk.d.T + t_light] == 0)
+                hit_red = true;
         }
     }
-    hit = __syncthreads_or(hit);
-
-    if (tid == 0) {
-        double p1s, p1d;
-        int p1_in;
-        combine_projection(pk, b, sm, 0, p1s, p1d, p1_in);
-        // footprint_on_route (roads.cpp:192-208)
-        bool on_route = true;
-        const int nl = pk.n_lanes[b];
-        for (int q = 1; q < NQ; ++q) {
-            bool any = false;
-            for (int l = 0; l < nl; ++l) {
-                const LaneRes& r = sm.lres[l][q];
-                if (r.set && fabs(r.d) <= r.hw) any = true;
-            }
-            if (!any) on_route = false;
-        }
-        const double dt = pk.dt;
-        const double progress = p1s - sm.proj_s;
-        const double a_lat = sm.v * sm.v * tan(sm.steer) / cfg.wheelbase;
-        const double a_lon = sm.accel;
-        double reward = cfg.w_progress * progress -
-                        cfg.w_speed * maxd(0.0, sm.nv - double(pk.speed_limit[b])) * dt -
-                        cfg.w_lat * a_lat * a_lat * dt - cfg.w_lon * a_lon * a_lon * dt;
-        const bool hit_collision = hit != 0;
-        const bool hit_off_route = !on_route;
-        bool hit_red = false;
-        {
-            int nsteps = pk.num_steps[b];
-            int t_light = sm.t < nsteps - 1 ? sm.t : nsteps - 1;
-            const int nlt = pk.n_lights[b];
-            for (int k = 0; k < nlt; ++k) {
-                double ls = pk.lt_s[size_t(b) * pk.d.NL + k];
-                if (sm.proj_s < ls && ls <= p1s) {
-                    if (pk.lt_state[(size_t(b) * pk.d.NL + k) * pk.d.T + t_light] == 0) hit_red = true;
-                }
-            }
-        }
-        bool hit_stop = false;
-        for (int j = 0; j < ns; ++j) {
-            double ss = pk.st_s[size_t(b) * pk.d.NS + j];
-            if (sm.proj_s < ss && ss <= p1s) {
-                if (sm.v > cfg.stop_cross_speed && !dy.sflag[j]) hit_stop = true;
-            }
-        }
-        const bool hit_goal = fabs(p1s - pk.goal_s[b]) <= cfg.goal_radius;
-        int reason = 0;
-        if (hit_collision)
-            reason = 1;
-        else if (hit_off_route)
-            reason = 2;
-        else if (hit_red)
-            reason = 3;
-        else if (hit_stop)
-            reason = 4;
-        else if (hit_goal)
-            reason = 5;
-        int events = sm.events;
-        if (cfg.disable_dones) {
-            if (hit_collision) events |= 1;
-            if (hit_off_route) events |= 2;
-            if (hit_red) events |= 4;
-            if (hit_stop) events |= 8;
-            if (hit_goal) events |= 16;
-        } else if (reason != 0) {
-            events |= 1 << (reason - 1);
-            if (reason != 5) reward -= cfg.terminal_penalty;
-        }
-        const int done = (!cfg.disable_dones && reason != 0) ? 1 : 0;
-        a.out.x[b] = sm.nx;
-        a.out.y[b] = sm.ny;
-        a.out.heading[b] = sm.nh;
-        a.out.v[b] = sm.nv;
-        a.out.steering[b] = sm.nsteer;
-        a.out.t[b] = sm.t + 1;
-        a.out.done[b] = uint8_t(done);
-        a.out.reason[b] = uint8_t(done ? reason : 0);
-        a.out.rng[b] = sm.rng;
-        a.out.proj_s[b] = p1s;
-        a.out.proj_d[b] = p1d;
-        a.out.proj_in_corridor[b] = uint8_t(p1_in);
-        a.out.events[b] = uint8_t(events);
+    bool hit_stop = false;
+    for (int j = 0; j < ns; ++j) {
+        double ss = pk.st_s[size_t(b) * pk.d.NS + j];
+        if (r0.proj_s < ss && ss <= p1.s && r0.v > cfg.stop_cross_speed && !w.sflag[j]) hit_stop = true;
+    }
+    const bool hit_goal = fabs(p1.s - pk.goal_s[b]) <= cfg.goal_radius;
+    const double progress = p1.s - r0.proj_s;
+    const double a_lat = r0.v * r0.v * tan(r0.steer) / cfg.wheelbase;
+    const double a_lon = accel;
+    double reward = cfg.w_progress * progress - cfg.w_speed * maxd(0.0, r.v - double(pk.speed_limit[b])) * dt -
+                    cfg.w_lat * a_lat * a_lat * dt - cfg.w_lon * a_lon * a_lon * dt;
+    const int reason = hit ? 1 : hit_off_route ? 2 : hit_red ? 3 : hit_stop ? 4 : hit_goal ? 5 : 0;
+    int events = r0.events;
+    if (cfg.disable_dones) {
+        events |= (hit ? 1 : 0) | (hit_off_route ? 2 : 0) | (hit_red ? 4 : 0) | (hit_stop ? 8 : 0) |
+                  (hit_goal ? 16 : 0);
+    } else if (reason != 0) {
+        events |= 1 << (reason - 1);
+        if (reason != 5) reward -= cfg.terminal_penalty;
+    }
+    r.done = (!cfg.disable_dones && reason != 0) ? 1 : 0;
+    r.reason = r.done ? reason : 0;
+    r.proj_s = p1.s;
+    r.proj_d = p1.d;
+    r.in_corr = p1.in_corr;
+    r.events = events;
+    if (lane == 0) {
+        store_row(a.out, b, r);
         a.so.reward[b] = float(reward);
         a.so.event[b] = uint8_t(reason);
-        a.so.s[b] = float(p1s);
+        a.so.s[b] = float(p1.s);
         a.so.a_lat[b] = float(a_lat);
         a.so.a_lon[b] = float(a_lon);
-        a.so.v[b] = float(sm.nv);
-        // the row state becomes the post-step state for a fused observe
-        sm.x = sm.nx;
-        sm.y = sm.ny;
-        sm.h = sm.nh;
-        sm.v = sm.nv;
-        sm.steer = sm.nsteer;
-        sm.t = sm.t + 1;
-        sm.done = done;
-        sm.reason = done ? reason : 0;
-        sm.proj_s = p1s;
-        sm.proj_d = p1d;
-        sm.in_corr = p1_in;
-        sm.events = events;
+        a.so.v[b] = float(r.v);
     }
-    __syncthreads();
     // stopped-flag update with the post-step state (simcore.cpp:390-396)
-    for (int j = tid; j < ns; j += NT) {
-        double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - sm.proj_s;
-        uint8_t f = dy.sflag[j];
-        if (ahead >= 0.0 && ahead <= cfg.stop_zone && sm.v < cfg.stop_slow_speed) f = 1;
-        a.out.stopped_flags[soff + j] = f;
+    for (int j = lane; j < ns; j += 32) {
+        double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - r.proj_s;
+        uint8_t fl = w.sflag[j];
+        if (ahead >= 0.0 && ahead <= cfg.stop_zone && r.v < cfg.stop_slow_speed) fl = 1;
+        a.out.stopped_flags[soff + j] = fl;
     }
-    __syncthreads();
+    __syncwarp();
+    return r;
 }
 
-__device__ void load_row(const zsim_state_view& in, int b, Smem& sm) {
-    sm.x = in.x[b];
-    sm.y = in.y[b];
-    sm.h = in.heading[b];
-    sm.v = in.v[b];
-    sm.steer = in.steering[b];
-    sm.t = in.t[b];
-    sm.done = in.done[b];
-    sm.reason = in.reason[b];
-    sm.rng = in.rng[b];
-    sm.proj_s = in.proj_s[b];
-    sm.proj_d = in.proj_d[b];
-    sm.in_corr = in.proj_in_corridor[b];
-    sm.events = in.events[b];
+// Prefetch row b's static scenario data (the arrays one step touches) into L2.
+// `t` is the log index of the agent slice the step will read (t+1 of the row).
+template <bool STEP, bool OBS>
+__device__ __forceinline__ void prefetch_row(const KernelArgs& a, int b, int t) {
+    const DevPack& pk = a.pk;
+    const int lane = lane_id();
+    const size_t LC = size_t(pk.d.L) * pk.d.C;
+    const size_t lb = size_t(b) * LC;
+    const int T = pk.d.T, A = pk.d.A;
+    const int ts = t < T ? (t >= 0 ? t : 0) : T - 1;
+    const size_t as = (size_t(b) * T + ts) * A;
+    switch (lane) {
+        case 0: if (STEP) prefetch_l2(pk.ln_x + lb, LC * 8); break;
+        case 1: if (STEP) prefetch_l2(pk.ln_y + lb, LC * 8); break;
+        case 2: if (STEP) prefetch_l2(pk.ln_abx + lb, LC * 8); break;
+        case 3: if (STEP) prefetch_l2(pk.ln_aby + lb, LC * 8); break;
+        case 4: if (STEP) prefetch_l2(pk.ln_len2 + lb, LC * 8); break;
+        case 5: if (STEP) prefetch_l2(pk.ln_s + lb, LC * 8); break;
+        case 6: if (STEP) prefetch_l2(pk.ln_hw + lb, LC * 8); break;
+        case 7: if (OBS) prefetch_l2(pk.road_xy + size_t(b) * pk.d.P, size_t(pk.d.P) * 8); break;
+        case 8: if (OBS) prefetch_l2(pk.road_kd + size_t(b) * pk.d.P, size_t(pk.d.P)); break;
+        case 9: if (OBS) prefetch_l2(pk.route_xy + size_t(b) * pk.d.R, size_t(pk.d.R) * 8); break;
+        case 10: if (OBS) prefetch_l2(pk.route_fl + size_t(b) * pk.d.R, size_t(pk.d.R)); break;
+        case 11: prefetch_l2(pk.ag_x + as, size_t(A) * 4); break;
+        case 12: prefetch_l2(pk.ag_y + as, size_t(A) * 4); break;
+        case 13: prefetch_l2(pk.ag_h + as, size_t(A) * 4); break;
+        case 14: prefetch_l2(pk.ag_sp + as, size_t(A) * 4); break;
+        case 15: prefetch_l2(pk.ag_valid + as, size_t(A)); break;
+        case 16: prefetch_l2(pk.ag_len + size_t(b) * A, size_t(A) * 4); break;
+        case 17: prefetch_l2(pk.ag_wid + size_t(b) * A, size_t(A) * 4); break;
+        default: break;
+    }
 }
 
 template <bool STEP, bool OBS>
-__global__ void __launch_bounds__(NT) k_step_observe(const KernelArgs a) {
+__global__ void __launch_bounds__(kThreads) k_step_observe(const KernelArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ Smem sm;
-    const Dyn dy = carve(dsm, a);
-    for (int b = blockIdx.x; b < a.pk.d.B; b += gridDim.x) {
-        if (threadIdx.x == 0) load_row(a.in, b, sm);
-        __syncthreads();
-        if (STEP) step_row(a, b, sm, dy);
-        if (OBS) observe_row(a, b, sm, dy);
-        __syncthreads();
+    const WarpBuf w = carve(dsm, a);
+    for (int k = lane_id(); k < 32 * 32; k += 32) w.hist[k] = 0;  // warp_topk leaves it cleared
+    __syncwarp();
+    const int wpb = kThreads / 32;
+    const int stride = gridDim.x * wpb;
+    int b = blockIdx.x * wpb + warp_in_block();
+    if (b < a.pk.d.B) prefetch_row<STEP, OBS>(a, b, a.in.t[b] + (STEP ? 1 : 0));
+    for (; b < a.pk.d.B; b += stride) {
+        Row r = load_row(a.in, b);
+        // the warp's next row: its static data streams into L2 while this row computes
+        if (b + stride < a.pk.d.B) prefetch_row<STEP, OBS>(a, b + stride, r.t + (STEP ? 1 : 0));
+        bool boxes_ready = false;
+        Box eb{};
+        double EX[4] = {0, 0, 0, 0}, EY[4] = {0, 0, 0, 0};
+        if (STEP) r = step_row(a, b, r, w, boxes_ready, eb, EX, EY);
+        if (OBS) observe_row(a, b, r, w, boxes_ready && !r.done, eb, EX, EY);
     }
 }
 
-// Env::init_state (simcore.cpp:237-276).
-__global__ void __launch_bounds__(NT) k_reset(const KernelArgs a) {
-    __shared__ Smem sm;
+// Env::init_state (simcore.cpp:237-276), one warp per row.
+__global__ void __launch_bounds__(kThreads) k_reset(const KernelArgs a) {
     const DevPack& pk = a.pk;
     const DevCfg& cfg = a.cfg;
-    for (int b = blockIdx.x; b < pk.d.B; b += gridDim.x) {
-        if (threadIdx.x == 0) {
-            sm.qx[0] = pk.init_x[b];
-            sm.qy[0] = pk.init_y[b];
-        }
-        __syncthreads();
-        project_queries<1>(pk, b, sm);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double s, d;
-            int in;
-            combine_projection(pk, b, sm, 0, s, d, in);
-            sm.proj_s = s;
+    const int lane = lane_id();
+    const int wpb = kThreads / 32;
+    for (int b = blockIdx.x * wpb + warp_in_block(); b < pk.d.B; b += gridDim.x * wpb) {
+        double qx[1] = {pk.init_x[b]}, qy[1] = {pk.init_y[b]};
+        const Proj p = warp_project<1>(pk, b, qx, qy);
+        if (lane == 0) {
             a.out.x[b] = pk.init_x[b];
             a.out.y[b] = pk.init_y[b];
             a.out.heading[b] = pk.init_h[b];
@@ -967,20 +1080,18 @@ __global__ void __launch_bounds__(NT) k_reset(const KernelArgs a) {
             a.out.done[b] = 0;
             a.out.reason[b] = 0;
             a.out.rng[b] = reset_rng_state(a.seed, uint64_t(b));
-            a.out.proj_s[b] = s;
-            a.out.proj_d[b] = d;
-            a.out.proj_in_corridor[b] = uint8_t(in);
+            a.out.proj_s[b] = p.s;
+            a.out.proj_d[b] = p.d;
+            a.out.proj_in_corridor[b] = uint8_t(p.in_corr);
             a.out.events[b] = 0;
         }
-        __syncthreads();
         const int ns = pk.n_stops[b];
         const int soff = pk.stop_off[b];
-        for (int j = threadIdx.x; j < ns; j += NT) {
-            double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - sm.proj_s;
+        for (int j = lane; j < ns; j += 32) {
+            double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - p.s;
             bool st = ahead >= 0.0 && ahead <= cfg.stop_zone && pk.init_v[b] < cfg.stop_slow_speed;
             a.out.stopped_flags[soff + j] = st ? 1 : 0;
         }
-        __syncthreads();
     }
 }
 
@@ -1004,7 +1115,7 @@ __global__ void __launch_bounds__(256) k_episode_stats(const KernelArgs a, const
     }
     for (int k = 0; k < kStatsLen; ++k) {
         long long v = loc[k];
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
         if ((threadIdx.x & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&acc[k]), (unsigned long long)v);
     }
     __syncthreads();
@@ -1014,49 +1125,59 @@ __global__ void __launch_bounds__(256) k_episode_stats(const KernelArgs a, const
 
 }  // namespace
 
+size_t smem_bytes(const KernelArgs& a) {
+    return warp_smem_bytes(a.pk.d.A, a.cand_cap, a.cfg.n_agents + a.cfg.n_road + a.cfg.n_route, a.pk.d.NS) *
+           size_t(kThreads / 32);
+}
+
+static int grid_for(const KernelArgs& a) {
+    const int wpb = kThreads / 32;
+    return (a.pk.d.B + wpb - 1) / wpb;
+}
+
+// Persistent grid: as many CTAs as fit on the device at once (each warp then
+// walks rows with a stride and prefetches its next row), capped by the work.
+template <class K>
+static int persistent_grid(K kern, const KernelArgs& a, size_t smem) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    int g = sms * per_sm;
+    int need = grid_for(a);
+    return g < need ? g : need;
+}
+
+cudaError_t launch_step_observe(const KernelArgs& a, int mode, int grid, cudaStream_t stream) {
+    (void)grid;
+    const size_t smem = smem_bytes(a);
+    auto launch = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        const int g = persistent_grid(kern, a, smem);
+        kern<<<g, kThreads, smem, stream>>>(a);
+        return cudaGetLastError();
+    };
+    switch (mode) {
+        case kModeStep: return launch(k_step_observe<true, false>);
+        case kModeObserve: return launch(k_step_observe<false, true>);
+        default: return launch(k_step_observe<true, true>);
+    }
+}
+
+cudaError_t launch_reset(const KernelArgs& a, int grid, cudaStream_t stream) {
+    (void)grid;
+    k_reset<<<grid_for(a), kThreads, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_episode_stats(const KernelArgs& a, const double* initial_s, long long* out, cudaStream_t stream) {
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(long long) * kStatsLen, stream);
     if (e != cudaSuccess) return e;
     int grid = (a.pk.d.B + 255) / 256;
     if (grid > 148 * 4) grid = 148 * 4;
     k_episode_stats<<<grid, 256, 0, stream>>>(a, initial_s, out);
-    return cudaGetLastError();
-}
-
-size_t smem_bytes(const KernelArgs& a) {
-    size_t off = 0;
-    off += size_t(a.cand_cap) * 8;
-    off += size_t(a.pk.d.A) * 4 * 8 * 2;
-    off += size_t(a.pk.d.A) * 8;
-    off += size_t(a.key_cap) * 4;
-    off += size_t(a.cand_cap) * 4;
-    off += size_t(a.pk.d.A) * 4;
-    off += size_t(a.cfg.n_agents + a.cfg.n_road + a.cfg.n_route) * 4;
-    off += size_t(a.pk.d.NS) + 16;
-    return (off + 15) / 16 * 16;
-}
-
-cudaError_t launch_step_observe(const KernelArgs& a, int mode, int grid, cudaStream_t stream) {
-    size_t smem = smem_bytes(a);
-    static bool attr_set[3] = {false, false, false};
-    auto launch = [&](auto kern, int m) -> cudaError_t {
-        if (!attr_set[m] || smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            if (e != cudaSuccess) return e;
-            attr_set[m] = true;
-        }
-        kern<<<grid, NT, smem, stream>>>(a);
-        return cudaGetLastError();
-    };
-    switch (mode) {
-        case kModeStep: return launch(k_step_observe<true, false>, 0);
-        case kModeObserve: return launch(k_step_observe<false, true>, 1);
-        default: return launch(k_step_observe<true, true>, 2);
-    }
-}
-
-cudaError_t launch_reset(const KernelArgs& a, int grid, cudaStream_t stream) {
-    k_reset<<<grid, NT, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

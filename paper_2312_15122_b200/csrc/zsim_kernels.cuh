@@ -9,7 +9,7 @@
 namespace zs {
 
 constexpr int kThreads = 128;  // threads per CTA (4 warps); one CTA per scenario row at a time
-constexpr int kMaxLanes = 16;  // route lanes per scenario supported by the projection scratch
+constexpr int kMaxLanes = 64;  // route lanes per scenario (projection walks lanes sequentially)
 
 constexpr int kStatsLen = 8;  // episode-stats vector length
 

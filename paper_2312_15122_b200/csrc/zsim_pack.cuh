@@ -9,7 +9,8 @@
 //                      (feature, point) order (roads.cpp:220-229)
 //   route   [B][R]     float2 xy + u8 is_left|lane_valid<<1 (simcore.cpp:181-200)
 //   lanes   [B][L][C]  centerline x, y, s, half_width f64 after RouteFrame::build
-//                      clipping (roads.cpp:43-103); n vertices + lane_id per lane
+//                      clipping (roads.cpp:43-103) + per-segment b-a and |b-a|^2;
+//                      n vertices + lane_id per lane
 //   lights  [B][NL]    route s f64 + state u8[T] for lights kept by
 //                      RouteContext::build (roads.cpp:245-249)
 //   stops   [B][NS]    route s f64 for stop lines kept by RouteContext::build
@@ -69,8 +70,13 @@ struct DevPack {
     const double* ln_y;
     const double* ln_s;
     const double* ln_hw;
+    const double* ln_abx;   // [B][L][C] segment vectors b - a (geometry.cpp:18), last slot unused
+    const double* ln_aby;
+    const double* ln_len2;  // |b - a|^2 with the reference's op order
     const int32_t* ln_n;
     const uint32_t* ln_id;
+    const float4* road_box;   // [B] (min x, min y, max x, max y) of the road points
+    const float4* route_box;  // [B] same for the route border points
     // lights / stops
     const double* lt_s;
     const uint8_t* lt_state;  // [B][NL][T]
