@@ -564,7 +564,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     env->dt = dt;
     env->total_stop = total_stop;
     env->base.key_cap = std::max(d.P, d.R);
-    env->base.cand_cap = std::max(256, next_pow2(2 * std::max(env->cfg.n_road, env->cfg.n_route)));
+    env->base.cand_cap = 256;  // = 32 lanes x kMaxCandPerLane in the top-k kernel
     env->sl = state_layout(B, total_stop);
     env->sol = stepout_layout(B);
     env->ol = obs_layout(B, env->cfg.n_agents, env->cfg.n_road, env->cfg.n_route);

@@ -42,6 +42,7 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int NQ = 5;     // projection queries per step: ego position + 4 inflated corners
 constexpr int NB2 = 256;  // counting-sort buckets over the exact keys
 constexpr int kUnroll = 8;  // independent point loads in flight per lane in the key passes
+constexpr int kMaxCandPerLane = 8;  // candidate cap / 32 (KernelArgs::cand_cap <= 256)
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int warp_in_block() { return threadIdx.x >> 5; }
@@ -49,17 +50,22 @@ __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1
 
 // TMA-unit bulk prefetch of a byte range into L2 (cp.async.bulk.prefetch,
 // sm_90+): one instruction per array, no registers or smem held.
-__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
     uintptr_t a = reinterpret_cast<uintptr_t>(p);
     uintptr_t a0 = a & ~uintptr_t(15);
-    size_t n = (bytes + (a - a0) + 15) & ~size_t(15);
-    while (n > 0) {
-        unsigned chunk = unsigned(n > (1u << 20) ? (1u << 20) : n);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(chunk) : "memory");
-        a0 += chunk;
-        n -= chunk;
-    }
+    unsigned n = (bytes + unsigned(a - a0) + 15u) & ~15u;
+    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(n) : "memory");
 }
+
+// One out-of-line copy of each fp64 libm routine (the inlined versions
+// multiply the kernel's code size past the instruction cache).
+__device__ __noinline__ double2 sincos2(double x) {
+    double s, c;
+    sincos(x, &s, &c);
+    return make_double2(s, c);
+}
+__device__ __noinline__ double tan1(double x) { return tan(x); }
+__device__ __noinline__ double wrap1(double a) { return wrap_angle(a); }
 
 // Lexicographic warp argmin by (d2, idx) for d2 >= 0 (or +inf): the bit
 // pattern of a non-negative double is monotone, so three 32-bit REDUX ops.
@@ -80,28 +86,30 @@ __device__ __forceinline__ T pick5(int k, T a0, T a1, T a2, T a3, T a4) {
 
 // Per-warp shared-memory carve-up (host mirror: smem_bytes()).
 struct WarpBuf {
+    double* egx;           // [4] ego box corners (lane-indexed reads)
+    double* egy;
     double* agx;           // [A*4] agent corners
     double* agy;
     double* agd;           // [A] bbox distance
     int* agf;              // [A] -1 invalid, 0 separate, 1 overlap
     int* surv;             // [A] agents whose bounds can reach the top n_agents
-    unsigned* hist;        // [32*32] lane-private histogram; reused as counting-sort counts [NB2]
+    unsigned short* hist;  // [32*32] lane-private u16 histogram; reused as counting-sort counts u32[NB2]
     int* cidx;             // [cap] candidate indices
     double* ckey;          // [cap] exact keys
     int* cinfo;            // [cap] bucket << 16 | slot
     int* order;            // [cap] candidates grouped by bucket
-    int* sel;              // [Ka + Kr + Kl] selected indices
+    int* sel;              // [Ka] selected agents (road/route selections land in `order`)
     unsigned char* sflag;  // [NS] pre-step stopped flags
 };
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) / 16 * 16; }
 
 __host__ __device__ inline size_t warp_smem_bytes(int A, int cap, int ksum, int ns) {
-    size_t o = 0;
+    size_t o = 64;
     o += al16(size_t(A) * 4 * 8) * 2;
     o += al16(size_t(A) * 8);
     o += al16(size_t(A) * 4) * 2;
-    o += 32 * 32 * 4;
+    o += 32 * 32 * 2;
     o += al16(size_t(cap) * 4);
     o += al16(size_t(cap) * 8);
     o += al16(size_t(cap) * 4) * 2;
@@ -112,10 +120,12 @@ __host__ __device__ inline size_t warp_smem_bytes(int A, int cap, int ksum, int 
 
 __device__ WarpBuf carve(unsigned char* base, const KernelArgs& a) {
     const int A = a.pk.d.A, cap = a.cand_cap;
-    const int ksum = a.cfg.n_agents + a.cfg.n_road + a.cfg.n_route;
+    const int ksum = a.cfg.n_agents;
     unsigned char* p = base + warp_smem_bytes(A, cap, ksum, a.pk.d.NS) * size_t(warp_in_block());
     WarpBuf w;
-    size_t o = 0;
+    w.egx = reinterpret_cast<double*>(p);
+    w.egy = reinterpret_cast<double*>(p + 32);
+    size_t o = 64;
     w.agx = reinterpret_cast<double*>(p + o);
     o += al16(size_t(A) * 4 * 8);
     w.agy = reinterpret_cast<double*>(p + o);
@@ -126,8 +136,8 @@ __device__ WarpBuf carve(unsigned char* base, const KernelArgs& a) {
     o += al16(size_t(A) * 4);
     w.surv = reinterpret_cast<int*>(p + o);
     o += al16(size_t(A) * 4);
-    w.hist = reinterpret_cast<unsigned*>(p + o);
-    o += 32 * 32 * 4;
+    w.hist = reinterpret_cast<unsigned short*>(p + o);
+    o += 32 * 32 * 2;
     w.cidx = reinterpret_cast<int*>(p + o);
     o += al16(size_t(cap) * 4);
     w.ckey = reinterpret_cast<double*>(p + o);
@@ -307,7 +317,9 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int b, size_
     ab.cy = double(pk.ag_y[slice + j]);
     ab.hl = double(pk.ag_len[size_t(b) * A + j]) * 0.5;
     ab.hw = double(pk.ag_wid[size_t(b) * A + j]) * 0.5;
-    sincos(h, &ab.s, &ab.c);
+    const double2 sc = sincos2(h);
+    ab.s = sc.x;
+    ab.c = sc.y;
     double X[4], Y[4];
     box_corners(ab, X, Y);
 #pragma unroll
@@ -342,13 +354,13 @@ __device__ __forceinline__ double box_far_d2(float4 bb, double px, double py) {
 }
 
 // Warp-wide bucket counts: lane k returns bucket k's count; clears the histogram.
-__device__ __forceinline__ unsigned hist_reduce(unsigned* hist) {
+__device__ __forceinline__ unsigned hist_reduce(unsigned short* hist) {
     const int lane = lane_id();
     unsigned mine = 0;
 #pragma unroll 8
     for (int k = 0; k < 32; ++k) {
         unsigned v = hist[k * 32 + lane];
-        hist[k * 32 + lane] = 0;
+        hist[k * 32 + lane] = 0;  // u16 lane-private counters
         unsigned s = __reduce_add_sync(FULL, v);
         if (lane == k) mine = s;
     }
@@ -399,8 +411,11 @@ __device__ __forceinline__ int compact(const float2* __restrict__ pts, int n, fl
 // use_r only points with exact d2 <= r2 qualify (roads.cpp:219-229).  Writes
 // the selected indices in order to sel[0..ret).
 // ---------------------------------------------------------------------------
-__device__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px, double py, bool use_r, double r2,
-                         float4 bbox, int cap, const WarpBuf& w, int* sel) {
+__device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px, double py, bool use_r,
+                                      double r2, float4 bbox, int cap, unsigned short* __restrict__ hist,
+                                      int* __restrict__ cidx, double* __restrict__ ckey, int* __restrict__ cinfo,
+                                      int* __restrict__ order) {
+    int* sel = order;
     const int lane = lane_id();
     if (n <= 0) return 0;
     const float pxf = float(px), pyf = float(py);
@@ -426,12 +441,12 @@ __device__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px
             float a = approx_key(pb[u], pxf, pyf);
             if (a <= hi) {
                 int bk = min(31, max(0, int(__float_as_uint(a) >> 22) - base));
-                w.hist[bk * 32 + lane] += 1;
+                hist[bk * 32 + lane] += 1;
             }
         }
     }
     __syncwarp();
-    unsigned cnt = hist_reduce(w.hist);
+    unsigned cnt = hist_reduce(hist);
     unsigned incl = warp_incl_scan(cnt);
     const unsigned total = __shfl_sync(FULL, incl, 31);
     double tcand, tsel = double(hi);
@@ -448,7 +463,7 @@ __device__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px
     float tc = fminf(__double2float_ru(tcand), hi);
 
     // pass 2: ballot compaction of the candidates
-    int C = compact(pts, n, pxf, pyf, tc, cap, w.cidx);
+    int C = compact(pts, n, pxf, pyf, tc, cap, cidx);
     if (C > cap && total > unsigned(K)) {
         // refine inside bucket kstar with 32 linear sub-buckets
         const float lo = kstar == 0 ? 0.f : __uint_as_float(unsigned(kstar + base) << 22);
@@ -460,11 +475,11 @@ __device__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px
             float a = approx_key(pts[i], pxf, pyf);
             if (a >= lo && a < hi2) {
                 int bk = min(31, max(0, int((a - lo) * inv2)));
-                w.hist[bk * 32 + lane] += 1;
+                hist[bk * 32 + lane] += 1;
             }
         }
         __syncwarp();
-        cnt = hist_reduce(w.hist);
+        cnt = hist_reduce(hist);
         incl = warp_incl_scan(cnt) + below;
         int k2 = __ffs(__ballot_sync(FULL, incl >= unsigned(K))) - 1;
         if (k2 >= 0) {
@@ -473,7 +488,7 @@ __device__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px
             double tc2 = t2 + 2.0 * mg;
             if (!(use_r && !(t2 + mg <= r2))) {
                 tc = fminf(__double2float_ru(tc2), tc);
-                C = compact(pts, n, pxf, pyf, tc, cap, w.cidx);
+                C = compact(pts, n, pxf, pyf, tc, cap, cidx);
             }
         }
     }
@@ -509,11 +524,11 @@ __device__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px
     }
 
     // exact fp64 keys (the reference's op order) + counting sort on them
-    unsigned* cntb = w.hist;  // NB2 counters in the (cleared) histogram area
+    unsigned* cntb = reinterpret_cast<unsigned*>(hist);  // NB2 u32 counters in the (cleared) histogram area
     const double sc2 = double(NB2) / (double(tc) > 0.0 ? double(tc) : 1.0);
     int nvalid_local = 0;
     for (int c = lane; c < C; c += 32) {
-        int i = w.cidx[c];
+        int i = cidx[c];
         float2 p = pts[i];
         double dx = double(p.x) - px, dy = double(p.y) - py;
         double e = dx * dx + dy * dy;
@@ -524,8 +539,8 @@ __device__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px
             info = (bk << 16) | slot;
             ++nvalid_local;
         }
-        w.ckey[c] = e;
-        w.cinfo[c] = info;
+        ckey[c] = e;
+        cinfo[c] = info;
     }
     const int nvalid = int(__reduce_add_sync(FULL, unsigned(nvalid_local)));
     __syncwarp();
@@ -546,27 +561,41 @@ __device__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px
     }
     __syncwarp();
     for (int c = lane; c < C; c += 32) {
-        int info = w.cinfo[c];
-        if (info >= 0) w.order[cntb[info >> 16] + (info & 0xFFFF)] = c;
+        int info = cinfo[c];
+        if (info >= 0) order[cntb[info >> 16] + (info & 0xFFFF)] = c;
     }
     __syncwarp();
-    for (int c = lane; c < C; c += 32) {
-        int info = w.cinfo[c];
+    // rank inside the bucket; ranks held in registers until every lane is
+    // done reading `order`, which then receives the selection
+    int rk[kMaxCandPerLane], ri[kMaxCandPerLane];
+#pragma unroll
+    for (int u = 0; u < kMaxCandPerLane; ++u) {
+        rk[u] = INT_MAX;
+        ri[u] = 0;
+        int c = lane + 32 * u;
+        if (c >= C) continue;
+        int info = cinfo[c];
         if (info < 0) continue;
         int bk = info >> 16;
         unsigned start = cntb[bk];
         unsigned end = bk + 1 < NB2 ? cntb[bk + 1] : unsigned(nvalid);
-        double e = w.ckey[c];
-        int i = w.cidx[c];
+        double e = ckey[c];
+        int i = cidx[c];
         unsigned rank = start;
+#pragma unroll 1
         for (unsigned q = start; q < end; ++q) {
-            int o = w.order[q];
-            double eo = w.ckey[o];
-            int io = w.cidx[o];
+            int o = order[q];
+            double eo = ckey[o];
+            int io = cidx[o];
             rank += (eo < e || (eo == e && io < i)) ? 1u : 0u;
         }
-        if (rank < unsigned(K)) sel[rank] = i;
+        rk[u] = int(rank);
+        ri[u] = i;
     }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kMaxCandPerLane; ++u)
+        if (rk[u] < K) sel[rk[u]] = ri[u];
     __syncwarp();
     for (int k = lane; k < NB2; k += 32) cntb[k] = 0;
     __syncwarp();
@@ -605,8 +634,6 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     }
 
     const int t = r.t;
-    double oc, os;
-    sincos(-r.h, &os, &oc);
     Box eb;
     double EX[4], EY[4];
     if (boxes_ready) {
@@ -617,8 +644,8 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
             EY[k] = EY_in[k];
         }
     } else {
-        double c, s;
-        sincos(r.h, &s, &c);
+        const double2 sc = sincos2(r.h);
+        const double c = sc.y, s = sc.x;
         eb.cx = r.x + c * cfg.ego_center_offset;
         eb.cy = r.y + s * cfg.ego_center_offset;
         eb.hl = cfg.ego_length * 0.5;
@@ -627,11 +654,14 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         eb.s = s;
         box_corners(eb, EX, EY);
     }
+    // ego-frame rotation by -heading (simcore.cpp:432): cos(-h) = cos h, sin(-h) = -sin h
+    const double oc = eb.c, os = -eb.s;
 
     // ---- active features: roads::stop_info (roads.cpp:253-277), simcore.cpp:440-455 ----
     {
         double best_stop = 1e300;
         const int ns = pk.n_stops[b];
+#pragma unroll 1
         for (int j = 0; j < ns; ++j) {
             double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - r.proj_s;
             if (ahead > 0.0 && ahead < best_stop) best_stop = ahead;
@@ -639,6 +669,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         double best_light = 1e300;
         int best_k = -1;
         const int nlt = pk.n_lights[b];
+#pragma unroll 1
         for (int k = 0; k < nlt; ++k) {
             double ahead = pk.lt_s[size_t(b) * pk.d.NL + k] - r.proj_s;
             if (ahead > 0.0 && ahead < best_light) {
@@ -702,6 +733,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     {
         // Ka-th smallest per-lane minimum: >= Ka distinct agents lie at or under it
         int rank = 0;
+#pragma unroll 4
         for (int k = 0; k < 32; ++k) {
             float o = __shfl_sync(FULL, my_min_ub, k);
             rank += (o < my_min_ub || (o == my_min_ub && k < lane)) ? 1 : 0;
@@ -729,6 +761,13 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     __syncwarp();
     // Exact distance of each survivor: the 32 distinct point-to-edge d2 of
     // obb_distance's 16 edge pairs (geometry.cpp:77-88), one per lane.
+    if (lane < 4) {
+        w.egx[lane] = pick5(lane, EX[0], EX[1], EX[2], EX[3], EX[3]);
+        w.egy[lane] = pick5(lane, EY[0], EY[1], EY[2], EY[3], EY[3]);
+    }
+    __syncwarp();
+    const double* GX = w.egx;
+    const double* GY = w.egy;
     for (int s = 0; s < nsurv; ++s) {
         const int j = w.surv[s];
         if (w.agf[j] == 1) {
@@ -740,9 +779,9 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         const int e = lane & 15, pi = e >> 2, sj = e & 3, sj1 = (sj + 1) & 3;
         double d2;
         if (lane < 16) {  // ego corner pi vs agent edge sj
-            d2 = seg_dist2(EX[pi], EY[pi], AX[sj], AY[sj], AX[sj1], AY[sj1]);
+            d2 = seg_dist2(GX[pi], GY[pi], AX[sj], AY[sj], AX[sj1], AY[sj1]);
         } else {  // agent corner pi vs ego edge sj
-            d2 = seg_dist2(AX[pi], AY[pi], EX[sj], EY[sj], EX[sj1], EY[sj1]);
+            d2 = seg_dist2(AX[pi], AY[pi], GX[sj], GY[sj], GX[sj1], GY[sj1]);
         }
         double md2;
         int dummy;
@@ -751,7 +790,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
             // (near-)contact: a strict edge crossing is possible, so take the
             // reference's full segment_segment_distance over the 16 pairs.
             double v = INFINITY;
-            if (lane < 16) v = box_edge_pair_dist2(EX, EY, AX, AY, lane >> 2, lane & 3);
+            if (lane < 16) v = box_edge_pair_dist2(GX, GY, AX, AY, lane >> 2, lane & 3);
             warp_argmin(v, 0, md2, dummy);
         }
         if (lane == 0) w.agd[j] = sqrt(md2);
@@ -763,6 +802,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
             int j = w.surv[s];
             double dj = w.agd[j];
             int rank = 0;
+#pragma unroll 1
             for (int q = 0; q < nsurv; ++q) {
                 int k = w.surv[q];
                 double dk = w.agd[k];
@@ -781,7 +821,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
             double wx = double(pk.ag_x[aslice + j]) - r.x, wy = double(pk.ag_y[aslice + j]) - r.y;
             f[0] = float(oc * wx - os * wy);
             f[1] = float(os * wx + oc * wy);
-            f[2] = float(wrap_angle(double(pk.ag_h[aslice + j]) - r.h));
+            f[2] = float(wrap1(double(pk.ag_h[aslice + j]) - r.h));
             f[3] = pk.ag_sp[aslice + j];
             f[4] = float(w.agd[j]);
             f[5] = 1.f;
@@ -798,8 +838,9 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         const int n = pk.n_road[b];
         const float2* pts = pk.road_xy + size_t(b) * pk.d.P;
         const double R = cfg.feature_radius;
-        int* sel = w.sel + Ka;
-        const int nsel = warp_topk(pts, n, Kr, r.x, r.y, true, R * R, pk.road_box[b], a.cand_cap, w, sel);
+        const int* sel = w.order;
+        const int nsel = warp_topk(pts, n, Kr, r.x, r.y, true, R * R, pk.road_box[b], a.cand_cap, w.hist, w.cidx,
+                                   w.ckey, w.cinfo, w.order);
         const uint8_t* kd = pk.road_kd + size_t(b) * pk.d.P;
         for (int k = lane; k < Kr; k += 32) {
             float f[12];
@@ -831,8 +872,9 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     {
         const int n = pk.n_route[b];
         const float2* pts = pk.route_xy + size_t(b) * pk.d.R;
-        int* sel = w.sel + Ka + Kr;
-        const int nsel = warp_topk(pts, n, Kl, r.x, r.y, false, 0.0, pk.route_box[b], a.cand_cap, w, sel);
+        const int* sel = w.order;
+        const int nsel = warp_topk(pts, n, Kl, r.x, r.y, false, 0.0, pk.route_box[b], a.cand_cap, w.hist, w.cidx,
+                                   w.ckey, w.cinfo, w.order);
         const uint8_t* fl = pk.route_fl + size_t(b) * pk.d.R;
         for (int k = lane; k < Kl; k += 32) {
             float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
@@ -900,24 +942,23 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
     const double accel = cfg.accel_bins[ai], rate = cfg.steer_bins[si];
     const double dt = pk.dt;
     // dyn::bicycle_step (dynamics.cpp:10-19)
-    double c0, s0;
-    sincos(r0.h, &s0, &c0);
+    const double2 sc0 = sincos2(r0.h);
+    const double tan_steer = tan1(r0.steer);
     Row r = r0;
-    r.x = r0.x + r0.v * c0 * dt;
-    r.y = r0.y + r0.v * s0 * dt;
-    r.h = wrap_angle(r0.h + r0.v / cfg.wheelbase * tan(r0.steer) * dt);
+    r.x = r0.x + r0.v * sc0.y * dt;
+    r.y = r0.y + r0.v * sc0.x * dt;
+    r.h = wrap1(r0.h + r0.v / cfg.wheelbase * tan_steer * dt);
     r.v = maxd(r0.v + accel * dt, cfg.v_min);
     r.steer = clampd(r0.steer + rate * dt, -cfg.delta_max, cfg.delta_max);
     r.t = r0.t + 1;
     // ego_box(e1) (simcore.cpp:156-160) and its margin-inflated corners (roads.cpp:202-204)
-    double c1, s1;
-    sincos(r.h, &s1, &c1);
-    eb.cx = r.x + c1 * cfg.ego_center_offset;
-    eb.cy = r.y + s1 * cfg.ego_center_offset;
+    const double2 sc1 = sincos2(r.h);
+    eb.cx = r.x + sc1.y * cfg.ego_center_offset;
+    eb.cy = r.y + sc1.x * cfg.ego_center_offset;
     eb.hl = cfg.ego_length * 0.5;
     eb.hw = cfg.ego_width * 0.5;
-    eb.c = c1;
-    eb.s = s1;
+    eb.c = sc1.y;
+    eb.s = sc1.x;
     box_corners(eb, EX, EY);
     double qx[NQ], qy[NQ];
     {
@@ -953,6 +994,7 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
         const int nsteps = pk.num_steps[b];
         const int t_light = r0.t < nsteps - 1 ? r0.t : nsteps - 1;
         const int nlt = pk.n_lights[b];
+#pragma unroll 1
         for (int k = 0; k < nlt; ++k) {
             double ls = pk.lt_s[size_t(b) * pk.d.NL + k];
             if (r0.proj_s < ls && ls <= p1.s && pk.lt_state[(size_t(b) * pk.d.NL + k) * pk.d.T + t_light] == 0)
@@ -960,13 +1002,14 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
         }
     }
     bool hit_stop = false;
+#pragma unroll 1
     for (int j = 0; j < ns; ++j) {
         double ss = pk.st_s[size_t(b) * pk.d.NS + j];
         if (r0.proj_s < ss && ss <= p1.s && r0.v > cfg.stop_cross_speed && !w.sflag[j]) hit_stop = true;
     }
     const bool hit_goal = fabs(p1.s - pk.goal_s[b]) <= cfg.goal_radius;
     const double progress = p1.s - r0.proj_s;
-    const double a_lat = r0.v * r0.v * tan(r0.steer) / cfg.wheelbase;
+    const double a_lat = r0.v * r0.v * tan_steer / cfg.wheelbase;
     const double a_lon = accel;
     double reward = cfg.w_progress * progress - cfg.w_speed * maxd(0.0, r.v - double(pk.speed_limit[b])) * dt -
                     cfg.w_lat * a_lat * a_lat * dt - cfg.w_lon * a_lon * a_lon * dt;
@@ -1016,34 +1059,37 @@ __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int b, int t) 
     const int T = pk.d.T, A = pk.d.A;
     const int ts = t < T ? (t >= 0 ? t : 0) : T - 1;
     const size_t as = (size_t(b) * T + ts) * A;
+    const void* ptr = nullptr;
+    size_t bytes = 0;
     switch (lane) {
-        case 0: if (STEP) prefetch_l2(pk.ln_x + lb, LC * 8); break;
-        case 1: if (STEP) prefetch_l2(pk.ln_y + lb, LC * 8); break;
-        case 2: if (STEP) prefetch_l2(pk.ln_abx + lb, LC * 8); break;
-        case 3: if (STEP) prefetch_l2(pk.ln_aby + lb, LC * 8); break;
-        case 4: if (STEP) prefetch_l2(pk.ln_len2 + lb, LC * 8); break;
-        case 5: if (STEP) prefetch_l2(pk.ln_s + lb, LC * 8); break;
-        case 6: if (STEP) prefetch_l2(pk.ln_hw + lb, LC * 8); break;
-        case 7: if (OBS) prefetch_l2(pk.road_xy + size_t(b) * pk.d.P, size_t(pk.d.P) * 8); break;
-        case 8: if (OBS) prefetch_l2(pk.road_kd + size_t(b) * pk.d.P, size_t(pk.d.P)); break;
-        case 9: if (OBS) prefetch_l2(pk.route_xy + size_t(b) * pk.d.R, size_t(pk.d.R) * 8); break;
-        case 10: if (OBS) prefetch_l2(pk.route_fl + size_t(b) * pk.d.R, size_t(pk.d.R)); break;
-        case 11: prefetch_l2(pk.ag_x + as, size_t(A) * 4); break;
-        case 12: prefetch_l2(pk.ag_y + as, size_t(A) * 4); break;
-        case 13: prefetch_l2(pk.ag_h + as, size_t(A) * 4); break;
-        case 14: prefetch_l2(pk.ag_sp + as, size_t(A) * 4); break;
-        case 15: prefetch_l2(pk.ag_valid + as, size_t(A)); break;
-        case 16: prefetch_l2(pk.ag_len + size_t(b) * A, size_t(A) * 4); break;
-        case 17: prefetch_l2(pk.ag_wid + size_t(b) * A, size_t(A) * 4); break;
+        case 0: ptr = STEP ? pk.ln_x + lb : nullptr; bytes = LC * 8; break;
+        case 1: ptr = STEP ? pk.ln_y + lb : nullptr; bytes = LC * 8; break;
+        case 2: ptr = STEP ? pk.ln_abx + lb : nullptr; bytes = LC * 8; break;
+        case 3: ptr = STEP ? pk.ln_aby + lb : nullptr; bytes = LC * 8; break;
+        case 4: ptr = STEP ? pk.ln_len2 + lb : nullptr; bytes = LC * 8; break;
+        case 5: ptr = STEP ? pk.ln_s + lb : nullptr; bytes = LC * 8; break;
+        case 6: ptr = STEP ? pk.ln_hw + lb : nullptr; bytes = LC * 8; break;
+        case 7: ptr = OBS ? pk.road_xy + size_t(b) * pk.d.P : nullptr; bytes = size_t(pk.d.P) * 8; break;
+        case 8: ptr = OBS ? pk.road_kd + size_t(b) * pk.d.P : nullptr; bytes = size_t(pk.d.P); break;
+        case 9: ptr = OBS ? pk.route_xy + size_t(b) * pk.d.R : nullptr; bytes = size_t(pk.d.R) * 8; break;
+        case 10: ptr = OBS ? pk.route_fl + size_t(b) * pk.d.R : nullptr; bytes = size_t(pk.d.R); break;
+        case 11: ptr = pk.ag_x + as; bytes = size_t(A) * 4; break;
+        case 12: ptr = pk.ag_y + as; bytes = size_t(A) * 4; break;
+        case 13: ptr = pk.ag_h + as; bytes = size_t(A) * 4; break;
+        case 14: ptr = pk.ag_sp + as; bytes = size_t(A) * 4; break;
+        case 15: ptr = pk.ag_valid + as; bytes = size_t(A); break;
+        case 16: ptr = pk.ag_len + size_t(b) * A; bytes = size_t(A) * 4; break;
+        case 17: ptr = pk.ag_wid + size_t(b) * A; bytes = size_t(A) * 4; break;
         default: break;
     }
+    if (ptr) prefetch_l2(ptr, unsigned(bytes < (1u << 24) ? bytes : (1u << 24)));
 }
 
 template <bool STEP, bool OBS>
-__global__ void __launch_bounds__(kThreads) k_step_observe(const KernelArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_step_observe(const KernelArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const WarpBuf w = carve(dsm, a);
-    for (int k = lane_id(); k < 32 * 32; k += 32) w.hist[k] = 0;  // warp_topk leaves it cleared
+    for (int k = lane_id(); k < 32 * 32; k += 32) w.hist[k] = 0;  // warp_topk leaves it cleared (u16)
     __syncwarp();
     const int wpb = kThreads / 32;
     const int stride = gridDim.x * wpb;
@@ -1126,7 +1172,7 @@ __global__ void __launch_bounds__(256) k_episode_stats(const KernelArgs a, const
 }  // namespace
 
 size_t smem_bytes(const KernelArgs& a) {
-    return warp_smem_bytes(a.pk.d.A, a.cand_cap, a.cfg.n_agents + a.cfg.n_road + a.cfg.n_route, a.pk.d.NS) *
+    return warp_smem_bytes(a.pk.d.A, a.cand_cap, a.cfg.n_agents, a.pk.d.NS) *
            size_t(kThreads / 32);
 }
 
