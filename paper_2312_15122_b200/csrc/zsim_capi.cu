@@ -179,6 +179,7 @@ struct zsim_env {
     int32_t* h_act = nullptr;
     cudaStream_t h_stream = nullptr;
     double* d_initial_s = nullptr;
+    float4* d_hint = nullptr;
     int grid = 0;
 };
 
@@ -385,7 +386,8 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     const size_t nln = size_t(B) * d.L * d.C;
     size_t o_lx = pb.reserve<double>(nln), o_ly = pb.reserve<double>(nln), o_ls = pb.reserve<double>(nln),
            o_lhw = pb.reserve<double>(nln);
-    size_t o_labx = pb.reserve<double>(nln), o_laby = pb.reserve<double>(nln), o_llen2 = pb.reserve<double>(nln);
+    size_t o_labx = pb.reserve<double>(nln), o_laby = pb.reserve<double>(nln), o_llen2 = pb.reserve<double>(nln),
+           o_linv2 = pb.reserve<double>(nln);
     size_t o_ln = pb.reserve<int32_t>(size_t(B) * d.L), o_lid = pb.reserve<uint32_t>(size_t(B) * d.L);
     size_t o_rbox = pb.reserve<float>(size_t(B) * 4), o_tbox = pb.reserve<float>(size_t(B) * 4);
     size_t o_lts = pb.reserve<double>(size_t(B) * d.NL), o_ltst = pb.reserve<uint8_t>(size_t(B) * d.NL * d.T);
@@ -493,7 +495,9 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
                     double abx = lf.x[i + 1] - lf.x[i], aby = lf.y[i + 1] - lf.y[i];
                     pb.at<double>(o_labx)[k] = abx;
                     pb.at<double>(o_laby)[k] = aby;
-                    pb.at<double>(o_llen2)[k] = abx * abx + aby * aby;
+                    double len2 = abx * abx + aby * aby;
+                    pb.at<double>(o_llen2)[k] = len2;
+                    pb.at<double>(o_linv2)[k] = len2 > 0.0 ? 1.0 / len2 : 0.0;
                 }
             }
         }
@@ -551,6 +555,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.ln_abx = reinterpret_cast<const double*>(D + o_labx);
     pk.ln_aby = reinterpret_cast<const double*>(D + o_laby);
     pk.ln_len2 = reinterpret_cast<const double*>(D + o_llen2);
+    pk.ln_inv2 = reinterpret_cast<const double*>(D + o_linv2);
     pk.road_box = reinterpret_cast<const float4*>(D + o_rbox);
     pk.route_box = reinterpret_cast<const float4*>(D + o_tbox);
     pk.ln_n = reinterpret_cast<const int32_t*>(D + o_ln);
@@ -690,6 +695,9 @@ ZSIM_API int zsim_env_create(const uint8_t* file, size_t nbytes, const int64_t* 
         set_device(env.get());
         env->base.cfg = make_dev_cfg(env->cfg, env->accel_bins, env->steer_bins);
         stage_env(env.get(), scenes, horizon);
+        cuda_check(cudaMalloc(&env->d_hint, sizeof(float4) * size_t(env->B)), "cudaMalloc(hint)");
+        cuda_check(cudaMemset(env->d_hint, 0xFF, sizeof(float4) * size_t(env->B)), "cudaMemset(hint)");  // NaN: no hint
+        env->base.hint = env->d_hint;
         cuda_check(cudaMalloc(&env->d_err, 4), "cudaMalloc(err)");
         cuda_check(cudaMemset(env->d_err, 0, 4), "cudaMemset(err)");
         env->base.err = env->d_err;
@@ -706,6 +714,7 @@ ZSIM_API int zsim_env_destroy(zsim_env* env) {
         cudaFree(env->d_pack);
         cudaFree(env->d_err);
         cudaFree(env->d_initial_s);
+        cudaFree(env->d_hint);
         delete env;
     });
 }

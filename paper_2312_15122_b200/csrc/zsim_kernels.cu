@@ -88,6 +88,7 @@ __device__ __forceinline__ T pick5(int k, T a0, T a1, T a2, T a3, T a4) {
 struct WarpBuf {
     double* egx;           // [4] ego box corners (lane-indexed reads)
     double* egy;
+    int* plist;            // [64] projection candidate list
     double* agx;           // [A*4] agent corners
     double* agy;
     double* agd;           // [A] bbox distance
@@ -105,7 +106,7 @@ struct WarpBuf {
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) / 16 * 16; }
 
 __host__ __device__ inline size_t warp_smem_bytes(int A, int cap, int ksum, int ns) {
-    size_t o = 64;
+    size_t o = 64 + 256;
     o += al16(size_t(A) * 4 * 8) * 2;
     o += al16(size_t(A) * 8);
     o += al16(size_t(A) * 4) * 2;
@@ -125,7 +126,8 @@ __device__ WarpBuf carve(unsigned char* base, const KernelArgs& a) {
     WarpBuf w;
     w.egx = reinterpret_cast<double*>(p);
     w.egy = reinterpret_cast<double*>(p + 32);
-    size_t o = 64;
+    w.plist = reinterpret_cast<int*>(p + 64);
+    size_t o = 64 + 256;
     w.agx = reinterpret_cast<double*>(p + o);
     o += al16(size_t(A) * 4 * 8);
     w.agy = reinterpret_cast<double*>(p + o);
@@ -219,81 +221,154 @@ struct Proj {
     int on_route;  // all four inflated corners lie in some corridor (roads.cpp:192-208)
 };
 
+// Division-free screening value of point_segment_dist2: t = dot * (1/len2)
+// instead of dot / len2.  Differs from the exact value by far less than the
+// screening margin used by warp_project.
+__device__ __forceinline__ double seg_d2_screen(double px, double py, double ax, double ay, double abx, double aby,
+                                                double inv2) {
+    double dot = (px - ax) * abx + (py - ay) * aby;
+    double t = dot * inv2;
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    double qx = ax + abx * t, qy = ay + aby * t;
+    double ex = px - qx, ey = py - qy;
+    return ex * ex + ey * ey;
+}
+
+__device__ __forceinline__ double warp_min_d(double v) {  // v >= 0 or +inf
+    unsigned hi = unsigned(__double2hiint(v)), lo = unsigned(__double2loint(v));
+    unsigned mhi = __reduce_min_sync(FULL, hi);
+    unsigned mlo = __reduce_min_sync(FULL, hi == mhi ? lo : 0xffffffffu);
+    return __hiloint2double(int(mhi), int(mlo));
+}
+
 // roads::project for NQU queries (q0 = the point; q1..4 = footprint corners
 // when NQU == 5): per route lane the first strictly smaller d2 segment
 // (roads.cpp:125-143), across lanes min |d| then lane_id (roads.cpp:147-166).
+// Each lane of the warp screens its segments with the division-free value;
+// only segments within the screening margin of the per-query minimum are
+// evaluated exactly (IEEE division, reference op order), one per lane, and
+// the exact (d2, segment) argmin decides.  `list` is 64 ints of warp smem.
 // Uniform result.
 template <int NQU>
-__device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const double* qy) {
+__device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const double* qy, int* list) {
     const int L = pk.d.L, C = pk.d.C;
     const int nl = pk.n_lanes[b];
     const int lane = lane_id();
+    double mag = 1e4;
+#pragma unroll
+    for (int q = 0; q < NQU; ++q) mag = fmax(mag, qx[q] * qx[q] + qy[q] * qy[q]);
     bool have = false;
     double best_abs = 0.0, best_s = 0.0, best_d = 0.0;
     uint32_t best_id = 0;
     unsigned in_bits = 0;
     for (int l = 0; l < nl; ++l) {
         const size_t base = (size_t(b) * L + l) * C;
-        const int nv = pk.ln_n[size_t(b) * L + l];
-        double bd2[NQU];
+        const double* X = pk.ln_x + base;
+        const double* Y = pk.ln_y + base;
+        const double* ABX = pk.ln_abx + base;
+        const double* ABY = pk.ln_aby + base;
+        const double* INV = pk.ln_inv2 + base;
+        const double* LEN2 = pk.ln_len2 + base;
+        const int nseg = pk.ln_n[size_t(b) * L + l] - 1;
+        // running exact best per query: (d2, segment) and the winner's s / d / hw
+        double bd2[NQU], bs[NQU], bd[NQU], bhw[NQU];
         int bi[NQU];
 #pragma unroll
         for (int q = 0; q < NQU; ++q) {
             bd2[q] = 1e300;
             bi[q] = INT_MAX;
+            bs[q] = bd[q] = bhw[q] = 0.0;
         }
-        for (int i = lane; i + 1 < nv; i += 32) {
-            const double ax = pk.ln_x[base + i], ay = pk.ln_y[base + i];
-            const double abx = pk.ln_abx[base + i], aby = pk.ln_aby[base + i], len2 = pk.ln_len2[base + i];
+        for (int c0 = 0; c0 < nseg; c0 += 64) {
+            // screening: two segments per lane
+            double sc[2][NQU];
+            double lmax = 0.0;
 #pragma unroll
-            for (int q = 0; q < NQU; ++q) {
-                double t;
-                double d2 = seg_d2_pre(qx[q], qy[q], ax, ay, abx, aby, len2, t);
-                if (d2 < bd2[q]) {
-                    bd2[q] = d2;
-                    bi[q] = i;
+            for (int u = 0; u < 2; ++u) {
+                const int i = c0 + lane + 32 * u;
+                if (i < nseg) {
+                    const double ax = X[i], ay = Y[i], abx = ABX[i], aby = ABY[i], inv2 = INV[i];
+                    lmax = fmax(lmax, abx * abx + aby * aby);
+#pragma unroll
+                    for (int q = 0; q < NQU; ++q) sc[u][q] = seg_d2_screen(qx[q], qy[q], ax, ay, abx, aby, inv2);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NQU; ++q) sc[u][q] = INFINITY;
                 }
             }
-        }
-        double wd2[NQU];
-        int wi[NQU];
+            // margin >= 2 x |screen - exact| (t differs by a few ulp)
+            const double lw = __hiloint2double(int(__reduce_max_sync(FULL, unsigned(__double2hiint(lmax)))), -1);
+            const double eta0 = 1e-12 * (mag + lw + 1.0);
+            // per-query screening threshold
+            int n = 0;
 #pragma unroll
-        for (int q = 0; q < NQU; ++q) warp_argmin(bd2[q], bi[q], wd2[q], wi[q]);
-        // lane q evaluates query q's winning segment: s, signed d, half-width (roads.cpp:130-139)
-        bool ok = false;
-        double hs = 0.0, hd = 0.0;
-        if (lane < NQU) {
-            int i;
-            double px, py;
-            if constexpr (NQU == 1) {
-                i = wi[0];
-                px = qx[0];
-                py = qy[0];
-            } else {
-                i = pick5(lane, wi[0], wi[1], wi[2], wi[3], wi[4]);
-                px = pick5(lane, qx[0], qx[1], qx[2], qx[3], qx[4]);
-                py = pick5(lane, qy[0], qy[1], qy[2], qy[3], qy[4]);
+            for (int q = 0; q < NQU; ++q) {
+                double m = warp_min_d(fmin(sc[0][q], sc[1][q]));
+                double thr = m + 1e-12 * m + eta0;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    bool cand = sc[u][q] <= thr;
+                    unsigned bal = __ballot_sync(FULL, cand);
+                    if (cand) {
+                        int pos = n + __popc(bal & lanemask_lt());
+                        if (pos < 64) list[pos] = (q << 16) | (c0 + lane + 32 * u);
+                    }
+                    n += __popc(bal);
+                }
             }
-            if (i != INT_MAX) {
-                double t;
-                double d2 = seg_d2_pre(px, py, pk.ln_x[base + i], pk.ln_y[base + i], pk.ln_abx[base + i],
-                                       pk.ln_aby[base + i], pk.ln_len2[base + i], t);
-                LaneHit h =
-                    lane_hit(px, py, pk.ln_x + base, pk.ln_y + base, pk.ln_s + base, pk.ln_hw + base, i, d2, t);
-                hs = h.s;
-                hd = h.d;
-                ok = fabs(h.d) <= h.hw;
+            __syncwarp();
+            if (n > 64) n = 64;  // cannot happen: >64 segments within 1e-12 relative of the minimum
+            // exact evaluation of the candidates, one per lane
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + lane;
+                int q = -1, i = INT_MAX;
+                double d2 = 1e300, hs = 0.0, hd = 0.0, hhw = 0.0;
+                if (k < n) {
+                    const int e = list[k];
+                    q = e >> 16;
+                    i = e & 0xFFFF;
+                    double px, py;
+                    if constexpr (NQU == 1) {
+                        px = qx[0];
+                        py = qy[0];
+                    } else {
+                        px = pick5(q, qx[0], qx[1], qx[2], qx[3], qx[4]);
+                        py = pick5(q, qy[0], qy[1], qy[2], qy[3], qy[4]);
+                    }
+                    double t;
+                    d2 = seg_d2_pre(px, py, X[i], Y[i], ABX[i], ABY[i], LEN2[i], t);
+                    LaneHit h = lane_hit(px, py, X, Y, pk.ln_s + base, pk.ln_hw + base, i, d2, t);
+                    hs = h.s;
+                    hd = h.d;
+                    hhw = h.hw;
+                }
+#pragma unroll
+                for (int q2 = 0; q2 < NQU; ++q2) {
+                    double wd2;
+                    int wi;
+                    warp_argmin(q == q2 ? d2 : 1e300, q == q2 ? i : INT_MAX, wd2, wi);
+                    if (wi != INT_MAX && (wd2 < bd2[q2] || (wd2 == bd2[q2] && wi < bi[q2]))) {
+                        const int src = __ffs(__ballot_sync(FULL, q == q2 && i == wi)) - 1;
+                        bd2[q2] = wd2;
+                        bi[q2] = wi;
+                        bs[q2] = __shfl_sync(FULL, hs, src);
+                        bd[q2] = __shfl_sync(FULL, hd, src);
+                        bhw[q2] = __shfl_sync(FULL, hhw, src);
+                    }
+                }
             }
+            __syncwarp();
         }
-        in_bits |= __ballot_sync(FULL, ok);
-        if (wi[0] != INT_MAX) {
-            double s0 = __shfl_sync(FULL, hs, 0), d0 = __shfl_sync(FULL, hd, 0);
+#pragma unroll
+        for (int q = 0; q < NQU; ++q)
+            if (bi[q] != INT_MAX && fabs(bd[q]) <= bhw[q]) in_bits |= 1u << q;
+        if (bi[0] != INT_MAX) {
             uint32_t id = pk.ln_id[size_t(b) * L + l];
-            if (!have || fabs(d0) < best_abs || (fabs(d0) == best_abs && id < best_id)) {
+            if (!have || fabs(bd[0]) < best_abs || (fabs(bd[0]) == best_abs && id < best_id)) {
                 have = true;
-                best_abs = fabs(d0);
-                best_s = s0;
-                best_d = d0;
+                best_abs = fabs(bd[0]);
+                best_s = bs[0];
+                best_d = bd[0];
                 best_id = id;
             }
         }
@@ -385,10 +460,15 @@ __device__ __forceinline__ int compact(const float2* __restrict__ pts, int n, fl
     int C = 0;
     for (int i0 = 0; i0 < n; i0 += 32 * kUnroll) {
         float2 pb[kUnroll];
+        if (i0 + 32 * kUnroll <= n) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            int i = i0 + u * 32 + lane;
-            pb[u] = i < n ? pts[i] : make_float2(INFINITY, INFINITY);
+            for (int u = 0; u < kUnroll; ++u) pb[u] = pts[i0 + u * 32 + lane];
+        } else {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                int i = i0 + u * 32 + lane;
+                pb[u] = i < n ? pts[i] : make_float2(INFINITY, INFINITY);
+            }
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -414,7 +494,7 @@ __device__ __forceinline__ int compact(const float2* __restrict__ pts, int n, fl
 __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px, double py, bool use_r,
                                       double r2, float4 bbox, int cap, unsigned short* __restrict__ hist,
                                       int* __restrict__ cidx, double* __restrict__ ckey, int* __restrict__ cinfo,
-                                      int* __restrict__ order) {
+                                      int* __restrict__ order, float4* hint, int which) {
     int* sel = order;
     const int lane = lane_id();
     if (n <= 0) return 0;
@@ -424,6 +504,27 @@ __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int
     hi_d += key_margin(hi_d, ep);
     if (use_r) hi_d = fmin(hi_d, r2 + key_margin(r2, ep));
     const float hi = __double2float_ru(hi_d);
+    int C = cap + 1;
+    float tc = hi;
+    // Fast path (speed only, never changes the result): the previous call's
+    // k-th exact key kth at position h bounds the new k-th key by the triangle
+    // inequality, E_k(p) <= (sqrt(kth) + |p - h|)^2 =: Ts, so every point that
+    // can make the cut has fp32 key <= Ts + margin: one compaction pass.
+    if (hint != nullptr) {
+        const float4 h = *hint;
+        const float kth = which == 0 ? h.z : h.w;
+        if (isfinite(h.x) && isfinite(h.y) && kth >= 0.f && isfinite(kth)) {
+            const double ddx = px - double(h.x), ddy = py - double(h.y);
+            const double dp = sqrt(ddx * ddx + ddy * ddy) + 1e-3 + 1e-6 * (fabs(px) + fabs(py));
+            const double rr = sqrt(double(kth)) + dp;
+            const double Ts = rr * rr * (1.0 + 1e-9);
+            if (!use_r || Ts <= r2) {
+                tc = fminf(__double2float_ru(Ts + key_margin(Ts, ep)), hi);
+                C = compact(pts, n, pxf, pyf, tc, cap, cidx);
+            }
+        }
+    }
+    if (C > cap) {
     // pseudo-log buckets: 2 per octave of the key; the top bucket holds hi
     const int top = int(__float_as_uint(hi) >> 22);
     const int base = max(top - 31, 0);
@@ -431,10 +532,15 @@ __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int
     // pass 1: histogram of the fp32 keys <= hi (loads batched for MLP)
     for (int i0 = 0; i0 < n; i0 += 32 * kUnroll) {
         float2 pb[kUnroll];
+        if (i0 + 32 * kUnroll <= n) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            int i = i0 + u * 32 + lane;
-            pb[u] = i < n ? pts[i] : make_float2(INFINITY, INFINITY);
+            for (int u = 0; u < kUnroll; ++u) pb[u] = pts[i0 + u * 32 + lane];
+        } else {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                int i = i0 + u * 32 + lane;
+                pb[u] = i < n ? pts[i] : make_float2(INFINITY, INFINITY);
+            }
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -460,10 +566,10 @@ __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int
         tcand = tsel + 2.0 * mg;
         if (use_r && !(tsel + mg <= r2)) tcand = double(hi);
     }
-    float tc = fminf(__double2float_ru(tcand), hi);
+    tc = fminf(__double2float_ru(tcand), hi);
 
     // pass 2: ballot compaction of the candidates
-    int C = compact(pts, n, pxf, pyf, tc, cap, cidx);
+    C = compact(pts, n, pxf, pyf, tc, cap, cidx);
     if (C > cap && total > unsigned(K)) {
         // refine inside bucket kstar with 32 linear sub-buckets
         const float lo = kstar == 0 ? 0.f : __uint_as_float(unsigned(kstar + base) << 22);
@@ -491,6 +597,7 @@ __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int
                 C = compact(pts, n, pxf, pyf, tc, cap, cidx);
             }
         }
+    }
     }
     if (C > cap) {
         // Pathological crowding at the threshold: exact iterative selection.
@@ -594,8 +701,20 @@ __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int
     }
     __syncwarp();
 #pragma unroll
-    for (int u = 0; u < kMaxCandPerLane; ++u)
+    for (int u = 0; u < kMaxCandPerLane; ++u) {
         if (rk[u] < K) sel[rk[u]] = ri[u];
+        if (hint != nullptr && rk[u] == K - 1) {
+            float* hk = which == 0 ? &hint->z : &hint->w;
+            *hk = __double2float_ru(ckey[lane + 32 * u]);
+        }
+    }
+    if (hint != nullptr && lane == 0) {
+        if (nvalid < K) (which == 0 ? hint->z : hint->w) = INFINITY;  // fewer than k qualify: no bound
+        if (which == 1) {  // both keys now refer to this position (road is selected first)
+            hint->x = float(px);
+            hint->y = float(py);
+        }
+    }
     __syncwarp();
     for (int k = lane; k < NB2; k += 32) cntb[k] = 0;
     __syncwarp();
@@ -771,7 +890,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     for (int s = 0; s < nsurv; ++s) {
         const int j = w.surv[s];
         if (w.agf[j] == 1) {
-            if (lane == 0) w.agd[j] = 0.0;
+            if (lane == 0) w.agd[j] = 0.0;  // obb_overlap => distance 0
             continue;
         }
         const double* AX = w.agx + 4 * j;
@@ -793,7 +912,12 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
             if (lane < 16) v = box_edge_pair_dist2(GX, GY, AX, AY, lane >> 2, lane & 3);
             warp_argmin(v, 0, md2, dummy);
         }
-        if (lane == 0) w.agd[j] = sqrt(md2);
+        if (lane == 0) w.agd[j] = md2;
+    }
+    __syncwarp();
+    for (int s = lane; s < nsurv; s += 32) {
+        const int j = w.surv[s];
+        w.agd[j] = sqrt(w.agd[j]);  // obb_distance returns sqrt of the min d2 (0 on overlap)
     }
     __syncwarp();
     for (int s0 = 0; s0 < nsurv; s0 += 32) {
@@ -840,7 +964,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         const double R = cfg.feature_radius;
         const int* sel = w.order;
         const int nsel = warp_topk(pts, n, Kr, r.x, r.y, true, R * R, pk.road_box[b], a.cand_cap, w.hist, w.cidx,
-                                   w.ckey, w.cinfo, w.order);
+                                   w.ckey, w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 0);
         const uint8_t* kd = pk.road_kd + size_t(b) * pk.d.P;
         for (int k = lane; k < Kr; k += 32) {
             float f[12];
@@ -874,7 +998,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         const float2* pts = pk.route_xy + size_t(b) * pk.d.R;
         const int* sel = w.order;
         const int nsel = warp_topk(pts, n, Kl, r.x, r.y, false, 0.0, pk.route_box[b], a.cand_cap, w.hist, w.cidx,
-                                   w.ckey, w.cinfo, w.order);
+                                   w.ckey, w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 1);
         const uint8_t* fl = pk.route_fl + size_t(b) * pk.d.R;
         for (int k = lane; k < Kl; k += 32) {
             float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
@@ -969,7 +1093,7 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
         qy[0] = r.y;
         box_corners(inf, qx + 1, qy + 1);
     }
-    const Proj p1 = warp_project<NQ>(pk, b, qx, qy);
+    const Proj p1 = warp_project<NQ>(pk, b, qx, qy, w.plist);
 
     // collision with the agents valid at t+1 (simcore.cpp:323-331); boxes kept for observe(t+1)
     int hit = 0;
@@ -1113,9 +1237,10 @@ __global__ void __launch_bounds__(kThreads) k_reset(const KernelArgs a) {
     const DevCfg& cfg = a.cfg;
     const int lane = lane_id();
     const int wpb = kThreads / 32;
+    __shared__ int lists[kThreads / 32][64];
     for (int b = blockIdx.x * wpb + warp_in_block(); b < pk.d.B; b += gridDim.x * wpb) {
         double qx[1] = {pk.init_x[b]}, qy[1] = {pk.init_y[b]};
-        const Proj p = warp_project<1>(pk, b, qx, qy);
+        const Proj p = warp_project<1>(pk, b, qx, qy, lists[warp_in_block()]);
         if (lane == 0) {
             a.out.x[b] = pk.init_x[b];
             a.out.y[b] = pk.init_y[b];

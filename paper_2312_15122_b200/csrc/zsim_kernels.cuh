@@ -27,8 +27,9 @@ struct KernelArgs {
     int32_t* dbg;
     int32_t* err;
     uint64_t seed;
+    float4* hint;      // [B] per-row top-k threshold hints (speed only; see warp_topk), may be null
     int32_t key_cap;   // >= max(P, R)
-    int32_t cand_cap;  // power of two >= 2 * max(n_road, n_route)
+    int32_t cand_cap;  // top-k candidate capacity per warp (= 32 x kMaxCandPerLane)
 };
 
 size_t smem_bytes(const KernelArgs& a);

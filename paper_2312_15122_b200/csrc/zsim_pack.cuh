@@ -73,6 +73,7 @@ struct DevPack {
     const double* ln_abx;   // [B][L][C] segment vectors b - a (geometry.cpp:18), last slot unused
     const double* ln_aby;
     const double* ln_len2;  // |b - a|^2 with the reference's op order
+    const double* ln_inv2;  // 1 / len2 (0 for a degenerate segment): division-free candidate screening
     const int32_t* ln_n;
     const uint32_t* ln_id;
     const float4* road_box;   // [B] (min x, min y, max x, max y) of the road points
