@@ -191,12 +191,18 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2312_15122_b200 as z
 
+    from paper_2312_15122_b200.shard import allreduce_stats, shard_rows
     c = CONFIGS[args.config]
-    B, A_, P = c["scenarios"], c["agents"], c["road_points"]
-    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=A_, road_points=P), 7 + rank)
+    A_, P = c["agents"], c["road_points"]
+    # weak scaling: the global set holds world x scenarios; rank r owns one contiguous shard
+    lo, hi = shard_rows(c["scenarios"] * world, world, rank)
+    B = hi - lo
+    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=A_, road_points=P, first_index=lo), 7)
     env = z.Env(zsim, config=z.SimConfig(disable_dones=True), device=local)
     del zsim
-    accel, steer = z.random_actions(EPISODE, B, seed=123 + rank)
+    accel_all, steer_all = z.random_actions(EPISODE, c["scenarios"] * world, seed=123)
+    accel = np.ascontiguousarray(accel_all[:, lo:hi])
+    steer = np.ascontiguousarray(steer_all[:, lo:hi])
     dA = torch.from_numpy(accel).cuda()
     dS = torch.from_numpy(steer).cuda()
     s0, s1 = env.device_state(), env.device_state()
@@ -248,7 +254,7 @@ def run_ours(args) -> None:
     env.episode_stats(cur, stats.data_ptr(), stream)
     if dist:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM)  # the one NCCL collective
+    allreduce_stats(stats)  # the one data collective: int64 episode stats over NCCL
     elapsed_ms = float(t_max.item())
     agent_steps = B * A_ * args.steps * world
     value = agent_steps / (elapsed_ms / 1e3)
@@ -303,7 +309,8 @@ def run_ours(args) -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: stress generator (seed 7+rank), random actions (splitmix64 seed 123+rank)",
+        "data": "synthetic: stress generator (seed 7; rank r owns global rows [r*B, (r+1)*B)), random actions "
+                "(splitmix64 seed 123)",
         "config": {"workload": c["workload"], "scenarios_per_gpu": B, "agents": A_, "road_points": P,
                    "route_points": 2 * LANES * LANE_VERTICES, "lanes": LANES, "lane_vertices": LANE_VERTICES,
                    "steps_per_episode": EPISODE, "disable_dones": True,

@@ -264,11 +264,14 @@ typedef struct zsim_stress_config {
     double dt;              /* 0.1 */
     double speed_limit;     /* 10 m/s */
     double lane_width;      /* 3.5 m */
+    int32_t first_index;    /* global index of the first scenario (shards of one global set) */
+    int32_t reserved;
 } zsim_stress_config;
 
 ZSIM_API int zsim_stress_config_defaults(zsim_stress_config* cfg);
-/* Generates `cfg->count` scenarios deterministically from `seed`
- * (per-scenario streams Rng(seed).split(i), common.hpp:47-50) and returns a
+/* Generates scenarios first_index .. first_index+count-1 of the global set
+ * deterministically from `seed` (scenario i draws from the stream
+ * Rng(seed).split(i), common.hpp:47-50, in closed form) and returns a
  * ZSIM container image in a malloc'd buffer (free with zsim_free_buffer). */
 ZSIM_API int zsim_stress_generate(const zsim_stress_config* cfg, uint64_t seed, uint8_t** out_buf, size_t* out_len);
 ZSIM_API void zsim_free_buffer(void* buf);

@@ -65,7 +65,8 @@ class EnvInfo(C.Structure):
 class StressConfigC(C.Structure):
     _fields_ = [("count", C.c_int32), ("num_steps", C.c_int32), ("agents", C.c_int32),
                 ("road_points", C.c_int32), ("lanes", C.c_int32), ("lane_vertices", C.c_int32),
-                ("dt", C.c_double), ("speed_limit", C.c_double), ("lane_width", C.c_double)]
+                ("dt", C.c_double), ("speed_limit", C.c_double), ("lane_width", C.c_double),
+                ("first_index", C.c_int32), ("reserved", C.c_int32)]
 
 
 # name -> (restype, argtypes); every symbol include/zsim_gpu.h declares.

@@ -1070,6 +1070,8 @@ ZSIM_API int zsim_stress_config_defaults(zsim_stress_config* c) {
         c->dt = 0.1;
         c->speed_limit = 10.0;
         c->lane_width = 3.5;
+        c->first_index = 0;
+        c->reserved = 0;
     });
 }
 

@@ -275,11 +275,14 @@ std::string stress_generate(const zsim_stress_config& cfg, uint64_t seed) {
     if (cfg.lanes < 1 || cfg.lane_vertices < 2) raise(Err::config, "stress: need >= 1 lane of >= 2 vertices");
     if (cfg.road_points < 2) raise(Err::config, "stress: road_points must be >= 2");
     if (!(cfg.dt > 0.0)) raise(Err::config, "stress: dt must be > 0");
+    if (cfg.first_index < 0) raise(Err::config, "stress: first_index must be >= 0");
     std::string out = zsim_header(cfg.dt);
-    Stream root(seed);
-    for (int i = 0; i < cfg.count; ++i) {
-        Stream s = root.split(uint64_t(i));
-        zsim_encode_append(out, make_scene(cfg, s, i));
+    for (int k = 0; k < cfg.count; ++k) {
+        const uint64_t i = uint64_t(cfg.first_index) + uint64_t(k);
+        // Rng(seed).split(i): the root has advanced i+1 times (reset_rng_state's closed form)
+        Stream s(0);
+        s.state = reset_rng_state(seed, i);
+        zsim_encode_append(out, make_scene(cfg, s, int(i)));
     }
     return out;
 }

@@ -452,11 +452,12 @@ class StressConfig:
     dt: float = 0.1
     speed_limit: float = 10.0
     lane_width: float = 3.5
+    first_index: int = 0
 
 
 def stress_scenarios(cfg: StressConfig, seed: int = 7) -> bytes:
     """ZSIM container image of `cfg.count` stress scenarios (host-only call)."""
-    c = StressConfigC(**{f.name: getattr(cfg, f.name) for f in fields(cfg)})
+    c = StressConfigC(**{f.name: getattr(cfg, f.name) for f in fields(cfg)}, reserved=0)
     p = C.c_void_p()
     n = C.c_size_t()
     check(lib.zsim_stress_generate(C.byref(c), C.c_uint64(seed), C.byref(p), C.byref(n)))

@@ -84,3 +84,82 @@ def read_zsim(b: bytes) -> list[dict]:
         out.append(sc)
         off += 4 + n
     return out
+
+
+def _p_str(o: bytearray, s: str) -> None:
+    b = s.encode()
+    o += struct.pack("<I", len(b)) + b
+
+
+def _p_f32s(o: bytearray, a) -> None:
+    a = np.asarray(a, dtype="<f4")
+    o += struct.pack("<I", a.size) + a.tobytes()
+
+
+def _p_u8s(o: bytearray, a) -> None:
+    a = np.asarray(a, dtype=np.uint8)
+    o += struct.pack("<I", a.size) + a.tobytes()
+
+
+def write_zsim(scenarios: list[dict], dt: float = 0.1) -> bytes:
+    """Inverse of read_zsim (encode_record, scenario_io.cpp:80-130)."""
+    out = bytearray(b"ZSIM" + struct.pack("<HHd", 1, 0, dt))
+    for sc in scenarios:
+        r = bytearray()
+        _p_str(r, sc.get("id", "s"))
+        r += struct.pack("<I", sc["num_steps"])
+        for k in ("x", "y", "heading", "v"):
+            _p_f32s(r, sc["ego"][k])
+        r += struct.pack("<I", len(sc["agents"]))
+        for a in sc["agents"]:
+            _p_str(r, a.get("id", "a"))
+            r += struct.pack("<ff", a["length"], a["width"])
+            for k in ("x", "y", "heading", "speed"):
+                _p_f32s(r, a[k])
+            _p_u8s(r, a["valid"])
+        r += struct.pack("<I", len(sc["lanes"]))
+        for l in sc["lanes"]:
+            r += struct.pack("<I", l["lane_id"])
+            _p_f32s(r, l["left"])
+            _p_f32s(r, l["right"])
+            r += struct.pack("<ff", l["s_start"], l["s_end"])
+        r += struct.pack("<I", len(sc["features"]))
+        for f in sc["features"]:
+            r += struct.pack("<BB", f["kind"], f["dir"])
+            _p_f32s(r, f["xy"])
+        r += struct.pack("<I", len(sc["lights"]))
+        for t in sc["lights"]:
+            r += struct.pack("<Iff", t.get("signal_id", 1), t["stop_x"], t["stop_y"])
+            _p_u8s(r, t["state"])
+        r += struct.pack("<I", len(sc["stops"]))
+        for s_ in sc["stops"]:
+            _p_f32s(r, s_["xy"])
+            r += struct.pack("<ff", s_["pos_x"], s_["pos_y"])
+        r += struct.pack("<fff", sc["speed_limit"], sc["goal_x"], sc["goal_y"])
+        out += struct.pack("<I", len(r)) + r
+    return bytes(out)
+
+
+def straight_scenario(n: int = 20, v: float = 10.0, heading: float = 0.0, length: float = 200.0, agents=(),
+                      lights=(), stops=(), goal=None, features=None, limit: float = 10.0) -> dict:
+    """A straight single-lane route along +x (lane width 3.5 m) with the ego
+    logged at constant speed from the origin; helpers for SPEC known-answer
+    tests.  `agents` are dicts with x/y/heading/length/width (static)."""
+    xs = np.arange(0.0, length + 1e-9, 2.0)
+    ego_x = np.array([v * 0.1 * t * np.cos(heading) for t in range(n)])
+    ego_y = np.array([v * 0.1 * t * np.sin(heading) for t in range(n)])
+    sc = {"id": "kat", "num_steps": n,
+          "ego": {"x": ego_x, "y": ego_y, "heading": np.full(n, heading), "v": np.full(n, v)},
+          "agents": [], "lanes": [{"lane_id": 0, "left": np.stack([xs, np.full_like(xs, 1.75)], 1).ravel(),
+                                    "right": np.stack([xs, np.full_like(xs, -1.75)], 1).ravel(),
+                                    "s_start": 0.0, "s_end": float(length)}],
+          "features": features if features is not None else [
+              {"kind": 0, "dir": 1, "xy": np.stack([xs, np.full_like(xs, 1.75)], 1).ravel()}],
+          "lights": list(lights), "stops": list(stops), "speed_limit": limit,
+          "goal_x": float(goal[0]) if goal else float(length - 10), "goal_y": float(goal[1]) if goal else 0.0}
+    for a in agents:
+        sc["agents"].append({"id": "a", "length": a.get("length", 4.0), "width": a.get("width", 2.0),
+                             "x": np.full(n, a["x"]), "y": np.full(n, a["y"]),
+                             "heading": np.full(n, a.get("heading", 0.0)), "speed": np.full(n, a.get("speed", 0.0)),
+                             "valid": np.ones(n, np.uint8)})
+    return sc
