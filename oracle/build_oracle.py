@@ -83,9 +83,32 @@ def build_port(force: bool = False) -> Path | None:
     return PORT_OUT
 
 
+DROPIN_OUT = HERE / "_ref" / "dropin_check"
+
+
+def build_dropin(force: bool = False) -> Path | None:
+    """The drop-in demonstration binary: dropin_check.cpp + the reference
+    objects + libzsim_gpu.so (needs the reference and the built library)."""
+    lib = HERE.parent / "paper_2312_15122_b200" / "libzsim_gpu.so"
+    if not reference_available() or not lib.exists() or build_ref(force) is None:
+        return DROPIN_OUT if DROPIN_OUT.exists() else None
+    src = HERE / "dropin_check.cpp"
+    deps = [src, lib, HERE.parent / "include" / "zsim_gpu.hpp", HERE.parent / "include" / "zsim_gpu.h"]
+    if not force and DROPIN_OUT.exists() and all(d.stat().st_mtime <= DROPIN_OUT.stat().st_mtime for d in deps):
+        return DROPIN_OUT
+    objs = [str(HERE / "_ref" / "obj" / f"{u}.o") for u in REF_UNITS]
+    tmp = DROPIN_OUT.with_suffix(".tmp")
+    _run([CXX, "-std=c++20", "-O2", "-ffp-contract=off", "-I", str(REF_SRC), "-I", str(NLOHMANN), "-I",
+          str(HERE.parent / "include"), "-o", str(tmp), str(src), *objs, str(lib),
+          "-Wl,-rpath,$ORIGIN/../../paper_2312_15122_b200", "-lpthread"])
+    os.replace(tmp, DROPIN_OUT)
+    return DROPIN_OUT
+
+
 def build(force: bool = False) -> None:
     build_port(force)
     build_ref(force)
+    build_dropin(force)
 
 
 if __name__ == "__main__":
