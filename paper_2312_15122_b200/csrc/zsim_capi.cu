@@ -311,6 +311,64 @@ int next_pow2(int v) {
     return p;
 }
 
+// Spatial order of a point set: stable sort by the Morton code of (x, y)
+// quantised over the set's bounding box.  Chunks of 32 consecutive points then
+// cover compact regions; the reference index rides along for tie-breaks.
+std::vector<int> morton_order(const std::vector<float>& xs, const std::vector<float>& ys) {
+    const size_t n = xs.size();
+    std::vector<int> perm(n);
+    for (size_t i = 0; i < n; ++i) perm[i] = int(i);
+    if (n < 2) return perm;
+    float x0 = xs[0], x1 = xs[0], y0 = ys[0], y1 = ys[0];
+    for (size_t i = 1; i < n; ++i) {
+        x0 = std::min(x0, xs[i]), x1 = std::max(x1, xs[i]);
+        y0 = std::min(y0, ys[i]), y1 = std::max(y1, ys[i]);
+    }
+    const double ext = std::max(double(x1) - x0, double(y1) - y0) + 1e-6;
+    auto spread = [](uint32_t v) {
+        uint64_t x = v & 0xFFFFu;
+        x = (x | (x << 8)) & 0x00FF00FFu;
+        x = (x | (x << 4)) & 0x0F0F0F0Fu;
+        x = (x | (x << 2)) & 0x33333333u;
+        x = (x | (x << 1)) & 0x55555555u;
+        return uint32_t(x);
+    };
+    std::vector<uint32_t> code(n);
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t qx = uint32_t((double(xs[i]) - x0) / ext * 65535.0);
+        uint32_t qy = uint32_t((double(ys[i]) - y0) / ext * 65535.0);
+        code[i] = spread(qx) | (spread(qy) << 1);
+    }
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return code[size_t(a)] < code[size_t(b)]; });
+    return perm;
+}
+
+// Writes one point set of scenario b in chunked spatial order.
+void write_points(unsigned char* host, size_t o_xy, size_t o_attr, size_t o_oi, size_t o_cb, int b, int cap, int ccap,
+                  const std::vector<float>& xs, const std::vector<float>& ys, const std::vector<uint8_t>& attr) {
+    const std::vector<int> perm = morton_order(xs, ys);
+    float* xy = reinterpret_cast<float*>(host + o_xy) + size_t(b) * cap * 2;
+    uint8_t* at = host + o_attr + size_t(b) * cap;
+    int32_t* oi = reinterpret_cast<int32_t*>(host + o_oi) + size_t(b) * cap;
+    float* cb = reinterpret_cast<float*>(host + o_cb) + size_t(b) * ccap * 4;
+    for (size_t k = 0; k < perm.size(); ++k) {
+        const int i = perm[k];
+        xy[2 * k] = xs[size_t(i)];
+        xy[2 * k + 1] = ys[size_t(i)];
+        at[k] = attr[size_t(i)];
+        oi[k] = i;
+    }
+    const int n = int(perm.size());
+    for (int c = 0; c * zs::kChunk < n; ++c) {
+        float bx0 = 3e38f, by0 = 3e38f, bx1 = -3e38f, by1 = -3e38f;
+        for (int k = c * zs::kChunk; k < std::min(n, (c + 1) * zs::kChunk); ++k) {
+            bx0 = std::min(bx0, xy[2 * k]), bx1 = std::max(bx1, xy[2 * k]);
+            by0 = std::min(by0, xy[2 * k + 1]), by1 = std::max(by1, xy[2 * k + 1]);
+        }
+        cb[4 * c] = bx0, cb[4 * c + 1] = by0, cb[4 * c + 2] = bx1, cb[4 * c + 3] = by1;
+    }
+}
+
 // Env::Env (simcore.cpp:203-233) over make_batch (scenario_io.cpp:404-437).
 void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon) {
     using namespace zs;
@@ -364,6 +422,8 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
             if (s.ego_x.empty()) raise(Err::invalid_argument, "scenario `" + s.id + "`: empty ego log");
         }
     }
+    d.PC = (d.P + kChunk - 1) / kChunk;
+    d.RC = (d.R + kChunk - 1) / kChunk;
     if (d.L > kMaxLanes) {
         raise(Err::invalid_argument, "route has " + std::to_string(d.L) + " lanes; the device path supports " +
                                          std::to_string(kMaxLanes));
@@ -382,7 +442,9 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
            o_ags = pb.reserve<float>(nag), o_agv = pb.reserve<uint8_t>(nag);
     size_t o_agl = pb.reserve<float>(size_t(B) * d.A), o_agw = pb.reserve<float>(size_t(B) * d.A);
     size_t o_rxy = pb.reserve<float>(size_t(B) * d.P * 2), o_rkd = pb.reserve<uint8_t>(size_t(B) * d.P);
+    size_t o_roi = pb.reserve<int32_t>(size_t(B) * d.P), o_rcb = pb.reserve<float>(size_t(B) * d.PC * 4);
     size_t o_txy = pb.reserve<float>(size_t(B) * d.R * 2), o_tfl = pb.reserve<uint8_t>(size_t(B) * d.R);
+    size_t o_toi = pb.reserve<int32_t>(size_t(B) * d.R), o_tcb = pb.reserve<float>(size_t(B) * d.RC * 4);
     const size_t nln = size_t(B) * d.L * d.C;
     size_t o_lx = pb.reserve<double>(nln), o_ly = pb.reserve<double>(nln), o_ls = pb.reserve<double>(nln),
            o_lhw = pb.reserve<double>(nln);
@@ -443,14 +505,24 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
                 pb.at<uint8_t>(o_agv)[k] = ag.valid[t];
             }
         }
-        size_t p = 0;
-        for (const auto& f : s.features) {
-            for (size_t i = 0; i + 1 < f.xy.size(); i += 2, ++p) {
-                size_t k = size_t(b) * d.P + p;
-                pb.at<float>(o_rxy)[2 * k] = f.xy[i];
-                pb.at<float>(o_rxy)[2 * k + 1] = f.xy[i + 1];
-                pb.at<uint8_t>(o_rkd)[k] = uint8_t((f.kind & 15) | (f.dir << 4));
+        {
+            std::vector<float> xs, ys;
+            std::vector<uint8_t> kd;
+            for (const auto& f : s.features) {
+                for (size_t i = 0; i + 1 < f.xy.size(); i += 2) {
+                    xs.push_back(f.xy[i]);
+                    ys.push_back(f.xy[i + 1]);
+                    kd.push_back(uint8_t((f.kind & 15) | (f.dir << 4)));
+                }
             }
+            write_points(pb.host.data(), o_rxy, o_rkd, o_roi, o_rcb, b, d.P, d.PC, xs, ys, kd);
+            xs.clear(), ys.clear(), kd.clear();
+            for (const auto& q : rpts[size_t(b)]) {
+                xs.push_back(q.x);
+                ys.push_back(q.y);
+                kd.push_back(uint8_t((q.is_left ? 1 : 0) | (q.lane_valid ? 2 : 0)));
+            }
+            write_points(pb.host.data(), o_txy, o_tfl, o_toi, o_tcb, b, d.R, d.RC, xs, ys, kd);
         }
         {
             float bx0 = 3e38f, by0 = 3e38f, bx1 = -3e38f, by1 = -3e38f;
@@ -473,13 +545,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
             float* tb = pb.at<float>(o_tbox) + 4 * size_t(b);
             tb[0] = tx0, tb[1] = ty0, tb[2] = tx1, tb[3] = ty1;
         }
-        const auto& rp = rpts[size_t(b)];
-        for (size_t i = 0; i < rp.size(); ++i) {
-            size_t k = size_t(b) * d.R + i;
-            pb.at<float>(o_txy)[2 * k] = rp[i].x;
-            pb.at<float>(o_txy)[2 * k + 1] = rp[i].y;
-            pb.at<uint8_t>(o_tfl)[k] = uint8_t((rp[i].is_left ? 1 : 0) | (rp[i].lane_valid ? 2 : 0));
-        }
+
         for (size_t l = 0; l < c.lanes.size(); ++l) {
             const LaneFrame& lf = c.lanes[l];
             pb.at<int32_t>(o_ln)[size_t(b) * d.L + l] = int32_t(lf.x.size());
@@ -546,8 +612,12 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.ag_wid = reinterpret_cast<const float*>(D + o_agw);
     pk.road_xy = reinterpret_cast<const float2*>(D + o_rxy);
     pk.road_kd = D + o_rkd;
+    pk.road_oi = reinterpret_cast<const int32_t*>(D + o_roi);
+    pk.road_cb = reinterpret_cast<const float4*>(D + o_rcb);
     pk.route_xy = reinterpret_cast<const float2*>(D + o_txy);
     pk.route_fl = D + o_tfl;
+    pk.route_oi = reinterpret_cast<const int32_t*>(D + o_toi);
+    pk.route_cb = reinterpret_cast<const float4*>(D + o_tcb);
     pk.ln_x = reinterpret_cast<const double*>(D + o_lx);
     pk.ln_y = reinterpret_cast<const double*>(D + o_ly);
     pk.ln_s = reinterpret_cast<const double*>(D + o_ls);

@@ -280,37 +280,39 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
             bs[q] = bd[q] = bhw[q] = 0.0;
         }
         for (int c0 = 0; c0 < nseg; c0 += 64) {
-            // screening: two segments per lane
-            double sc[2][NQU];
+            // screening: two segments per lane, one query at a time
+            double sx[2], sy[2], sbx[2], sby[2], sinv[2];
             double lmax = 0.0;
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int i = c0 + lane + 32 * u;
-                if (i < nseg) {
-                    const double ax = X[i], ay = Y[i], abx = ABX[i], aby = ABY[i], inv2 = INV[i];
-                    lmax = fmax(lmax, abx * abx + aby * aby);
-#pragma unroll
-                    for (int q = 0; q < NQU; ++q) sc[u][q] = seg_d2_screen(qx[q], qy[q], ax, ay, abx, aby, inv2);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < NQU; ++q) sc[u][q] = INFINITY;
-                }
+                const bool ok = i < nseg;
+                sx[u] = ok ? X[i] : 0.0;
+                sy[u] = ok ? Y[i] : 0.0;
+                sbx[u] = ok ? ABX[i] : 0.0;
+                sby[u] = ok ? ABY[i] : 0.0;
+                sinv[u] = ok ? INV[i] : 0.0;
+                if (ok) lmax = fmax(lmax, sbx[u] * sbx[u] + sby[u] * sby[u]);
             }
             // margin >= 2 x |screen - exact| (t differs by a few ulp)
             const double lw = __hiloint2double(int(__reduce_max_sync(FULL, unsigned(__double2hiint(lmax)))), -1);
             const double eta0 = 1e-12 * (mag + lw + 1.0);
-            // per-query screening threshold
             int n = 0;
 #pragma unroll
             for (int q = 0; q < NQU; ++q) {
-                double m = warp_min_d(fmin(sc[0][q], sc[1][q]));
-                double thr = m + 1e-12 * m + eta0;
+                double sc0 = c0 + lane < nseg ? seg_d2_screen(qx[q], qy[q], sx[0], sy[0], sbx[0], sby[0], sinv[0])
+                                               : INFINITY;
+                double sc1 = c0 + lane + 32 < nseg
+                                 ? seg_d2_screen(qx[q], qy[q], sx[1], sy[1], sbx[1], sby[1], sinv[1])
+                                 : INFINITY;
+                const double m = warp_min_d(fmin(sc0, sc1));
+                const double thr = m + 1e-12 * m + eta0;
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                    bool cand = sc[u][q] <= thr;
-                    unsigned bal = __ballot_sync(FULL, cand);
+                    const bool cand = (u == 0 ? sc0 : sc1) <= thr;
+                    const unsigned bal = __ballot_sync(FULL, cand);
                     if (cand) {
-                        int pos = n + __popc(bal & lanemask_lt());
+                        const int pos = n + __popc(bal & lanemask_lt());
                         if (pos < 64) list[pos] = (q << 16) | (c0 + lane + 32 * u);
                     }
                     n += __popc(bal);
@@ -452,51 +454,77 @@ __device__ __forceinline__ unsigned warp_incl_scan(unsigned v) {
     return v;
 }
 
-// Ballot compaction of the points with approx key <= tc; returns the count
-// (may exceed cap; only the first cap indices are stored).
-__device__ __forceinline__ int compact(const float2* __restrict__ pts, int n, float pxf, float pyf, float tc, int cap,
-                                       int* cidx) {
+// A point set in chunked spatial order (zsim_pack.cuh).
+struct PointSet {
+    const float2* xy;
+    const int32_t* oi;  // index in the reference order (tie-break key)
+    const float4* cb;   // chunk bounding boxes
+    int n, nch;
+};
+
+// Squared distances from (px, py) to a chunk box: a lower bound (nearest
+// point of the box) and an upper bound (farthest corner) on the exact fp64
+// key of every point inside, with slack for rounding.
+__device__ __forceinline__ void chunk_bounds(float4 bb, double px, double py, double& lo, double& hi) {
+    double x0 = double(bb.x) - px, x1 = double(bb.z) - px, y0 = double(bb.y) - py, y1 = double(bb.w) - py;
+    double nx = x0 > 0.0 ? x0 : (x1 < 0.0 ? -x1 : 0.0);
+    double ny = y0 > 0.0 ? y0 : (y1 < 0.0 ? -y1 : 0.0);
+    double fx = fmax(fabs(x0), fabs(x1)), fy = fmax(fabs(y0), fabs(y1));
+    lo = (nx * nx + ny * ny) * (1.0 - 1e-12);
+    hi = (fx * fx + fy * fy) * (1.0 + 1e-12) + 1e-300;
+}
+
+// One warp pass over the listed chunks (32 points each, one per lane), loads
+// batched for memory-level parallelism; calls f(position, approx_key) for
+// every existing point.
+template <class F>
+__device__ __forceinline__ void over_chunks(const PointSet& ps, const int* list, int nlist, float pxf, float pyf,
+                                            F&& f) {
     const int lane = lane_id();
-    int C = 0;
-    for (int i0 = 0; i0 < n; i0 += 32 * kUnroll) {
+    for (int j0 = 0; j0 < nlist; j0 += kUnroll) {
         float2 pb[kUnroll];
-        if (i0 + 32 * kUnroll <= n) {
+        int pos[kUnroll];
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) pb[u] = pts[i0 + u * 32 + lane];
-        } else {
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
-                int i = i0 + u * 32 + lane;
-                pb[u] = i < n ? pts[i] : make_float2(INFINITY, INFINITY);
+        for (int u = 0; u < kUnroll; ++u) {
+            pos[u] = -1;
+            pb[u] = make_float2(INFINITY, INFINITY);
+            if (j0 + u < nlist) {
+                const int p = list[j0 + u] * kChunk + lane;
+                if (p < ps.n) {
+                    pos[u] = p;
+                    pb[u] = ps.xy[p];
+                }
             }
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            int i = i0 + u * 32 + lane;
-            bool take = i < n && approx_key(pb[u], pxf, pyf) <= tc;
-            unsigned m = __ballot_sync(FULL, take);
-            if (m) {
-                int pos = C + __popc(m & lanemask_lt());
-                if (take && pos < cap) cidx[pos] = i;
-                C += __popc(m);
-            }
+            if (j0 + u < nlist) f(pos[u], approx_key(pb[u], pxf, pyf));
         }
     }
-    __syncwarp();
-    return C;
 }
 
 // ---------------------------------------------------------------------------
-// Warp top-k by (exact fp64 d2, index) over n points `pts` (float2).  With
-// use_r only points with exact d2 <= r2 qualify (roads.cpp:219-229).  Writes
-// the selected indices in order to sel[0..ret).
+// Warp top-k by (exact fp64 d2, reference index) over a chunked point set.
+// With use_r only points with exact d2 <= r2 qualify (roads.cpp:219-229).
+// Writes the selected POSITIONS (into ps.xy) in order to order[0..ret).
+//
+//  1. Upper bound T on the k-th exact key: the per-row hint (previous k-th key
+//     + displacement, triangle inequality) and/or the smallest chunk far-corner
+//     distance that covers >= k points.
+//  2. Only chunks whose nearest box point can hold a key <= T are read; their
+//     points with fp32 key <= T + margin are compacted (ballot).
+//  3. If that overflows the candidate capacity, a pseudo-log histogram over
+//     the same chunks tightens T (then a linear one, then an exact iterative
+//     fallback).
+//  4. Exact fp64 keys for the candidates, counting sort + in-bucket rank by
+//     (key, reference index).
 // ---------------------------------------------------------------------------
-__device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int K, double px, double py, bool use_r,
-                                      double r2, float4 bbox, int cap, unsigned short* __restrict__ hist,
-                                      int* __restrict__ cidx, double* __restrict__ ckey, int* __restrict__ cinfo,
-                                      int* __restrict__ order, float4* hint, int which) {
-    int* sel = order;
+__device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, bool use_r, double r2, float4 bbox,
+                                      int cap, unsigned short* __restrict__ hist, int* __restrict__ cidx,
+                                      double* __restrict__ ckey, int* __restrict__ cinfo, int* __restrict__ order,
+                                      float4* hint, int which) {
     const int lane = lane_id();
+    const int n = ps.n;
     if (n <= 0) return 0;
     const float pxf = float(px), pyf = float(py);
     const double ep = fmax(fabs(double(pxf) - px), fabs(double(pyf) - py));
@@ -504,12 +532,9 @@ __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int
     hi_d += key_margin(hi_d, ep);
     if (use_r) hi_d = fmin(hi_d, r2 + key_margin(r2, ep));
     const float hi = __double2float_ru(hi_d);
-    int C = cap + 1;
-    float tc = hi;
-    // Fast path (speed only, never changes the result): the previous call's
-    // k-th exact key kth at position h bounds the new k-th key by the triangle
-    // inequality, E_k(p) <= (sqrt(kth) + |p - h|)^2 =: Ts, so every point that
-    // can make the cut has fp32 key <= Ts + margin: one compaction pass.
+
+    // ---- 1. upper bound on the k-th exact key ----
+    double T = INFINITY;
     if (hint != nullptr) {
         const float4 h = *hint;
         const float kth = which == 0 ? h.z : h.w;
@@ -517,137 +542,166 @@ __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int
             const double ddx = px - double(h.x), ddy = py - double(h.y);
             const double dp = sqrt(ddx * ddx + ddy * ddy) + 1e-3 + 1e-6 * (fabs(px) + fabs(py));
             const double rr = sqrt(double(kth)) + dp;
-            const double Ts = rr * rr * (1.0 + 1e-9);
-            if (!use_r || Ts <= r2) {
-                tc = fminf(__double2float_ru(Ts + key_margin(Ts, ep)), hi);
-                C = compact(pts, n, pxf, pyf, tc, cap, cidx);
-            }
+            T = rr * rr * (1.0 + 1e-9);
         }
     }
-    if (C > cap) {
-    // pseudo-log buckets: 2 per octave of the key; the top bucket holds hi
-    const int top = int(__float_as_uint(hi) >> 22);
-    const int base = max(top - 31, 0);
-
-    // pass 1: histogram of the fp32 keys <= hi (loads batched for MLP)
-    for (int i0 = 0; i0 < n; i0 += 32 * kUnroll) {
-        float2 pb[kUnroll];
-        if (i0 + 32 * kUnroll <= n) {
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u) pb[u] = pts[i0 + u * 32 + lane];
-        } else {
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
-                int i = i0 + u * 32 + lane;
-                pb[u] = i < n ? pts[i] : make_float2(INFINITY, INFINITY);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            float a = approx_key(pb[u], pxf, pyf);
-            if (a <= hi) {
-                int bk = min(31, max(0, int(__float_as_uint(a) >> 22) - base));
-                hist[bk * 32 + lane] += 1;
-            }
-        }
-    }
-    __syncwarp();
-    unsigned cnt = hist_reduce(hist);
-    unsigned incl = warp_incl_scan(cnt);
-    const unsigned total = __shfl_sync(FULL, incl, 31);
-    double tcand, tsel = double(hi);
-    int kstar = 31;
-    if (total <= unsigned(K)) {
-        tcand = double(hi);  // every qualifying point is a candidate
-    } else {
-        kstar = __ffs(__ballot_sync(FULL, incl >= unsigned(K))) - 1;
-        tsel = kstar == 31 ? double(hi) : double(__uint_as_float(unsigned(kstar + base + 1) << 22));
-        double mg = key_margin(tsel, ep);
-        tcand = tsel + 2.0 * mg;
-        if (use_r && !(tsel + mg <= r2)) tcand = double(hi);
-    }
-    tc = fminf(__double2float_ru(tcand), hi);
-
-    // pass 2: ballot compaction of the candidates
-    C = compact(pts, n, pxf, pyf, tc, cap, cidx);
-    if (C > cap && total > unsigned(K)) {
-        // refine inside bucket kstar with 32 linear sub-buckets
-        const float lo = kstar == 0 ? 0.f : __uint_as_float(unsigned(kstar + base) << 22);
-        const float hi2 = float(tsel);
-        const unsigned below = __shfl_sync(FULL, incl - cnt, kstar);
-        const float w2 = (hi2 - lo) * (1.0f / 32.0f);
-        const float inv2 = w2 > 0.f ? 1.0f / w2 : 0.f;
-        for (int i = lane; i < n; i += 32) {
-            float a = approx_key(pts[i], pxf, pyf);
-            if (a >= lo && a < hi2) {
-                int bk = min(31, max(0, int((a - lo) * inv2)));
-                hist[bk * 32 + lane] += 1;
-            }
+    if (!(T < INFINITY) && ps.nch <= cap) {
+        // smallest far bound covering >= K points: chunk far bounds staged in
+        // ckey (free until the candidates), extracted in increasing order
+        for (int c = lane; c < ps.nch; c += 32) {
+            double lo_b, hi_b;
+            chunk_bounds(ps.cb[c], px, py, lo_b, hi_b);
+            ckey[c] = hi_b;
         }
         __syncwarp();
-        cnt = hist_reduce(hist);
-        incl = warp_incl_scan(cnt) + below;
-        int k2 = __ffs(__ballot_sync(FULL, incl >= unsigned(K))) - 1;
-        if (k2 >= 0) {
-            double t2 = (double(lo) + double(k2 + 1) * double(w2)) * (1.0 + 1e-6) + 1e-30;
-            double mg = key_margin(t2, ep);
-            double tc2 = t2 + 2.0 * mg;
-            if (!(use_r && !(t2 + mg <= r2))) {
-                tc = fminf(__double2float_ru(tc2), tc);
-                C = compact(pts, n, pxf, pyf, tc, cap, cidx);
-            }
+        int acc = 0;
+        for (int it = 0; it < ps.nch && acc < K; ++it) {
+            double mloc = INFINITY;
+            int mi = INT_MAX;
+            for (int c = lane; c < ps.nch; c += 32)
+                if (ckey[c] < mloc) mloc = ckey[c], mi = c;
+            double md;
+            int mc;
+            warp_argmin(mloc, mi, md, mc);
+            if (mc == INT_MAX || !(md < INFINITY)) break;
+            if (lane == 0) ckey[mc] = INFINITY;
+            __syncwarp();
+            acc += min(kChunk, n - mc * kChunk);
+            if (acc >= K) T = md;
         }
     }
+    if (use_r && T < INFINITY && !(T <= r2)) T = INFINITY;  // the k points might not all qualify
+    float tc = T < INFINITY ? fminf(__double2float_ru(T + key_margin(T, ep)), hi) : hi;
+
+    // ---- 2. needed chunks + candidate compaction ----
+    int* list = order;  // chunk list (order is free until the final sort)
+    int nlist = 0;
+    auto build_list = [&](float t) {
+        nlist = 0;
+        const double lim = double(t) + key_margin(double(t), ep);
+        for (int c0 = 0; c0 < ps.nch; c0 += 32) {
+            const int c = c0 + lane;
+            double lo_b = 0.0, hi_b = INFINITY;
+            if (c < ps.nch) chunk_bounds(ps.cb[c], px, py, lo_b, hi_b);
+            const bool need = c < ps.nch && lo_b <= lim;
+            const unsigned bal = __ballot_sync(FULL, need);
+            if (need) list[nlist + __popc(bal & lanemask_lt())] = c;
+            nlist += __popc(bal);
+        }
+        __syncwarp();
+    };
+    auto compact_chunks = [&](float t) {
+        int C = 0;
+        over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a) {
+            const bool take = pos >= 0 && a <= t;
+            const unsigned bal = __ballot_sync(FULL, take);
+            if (take) {
+                const int q = C + __popc(bal & lanemask_lt());
+                if (q < cap) cidx[q] = pos;
+            }
+            C += __popc(bal);
+        });
+        __syncwarp();
+        return C;
+    };
+    build_list(tc);
+    int C = compact_chunks(tc);
+
+    // ---- 3. tighten the bound when the candidates overflow ----
+    if (C > cap) {
+        const int top = int(__float_as_uint(tc) >> 22);
+        const int base = max(top - 31, 0);
+        over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a) {
+            if (pos >= 0 && a <= tc) hist[min(31, max(0, int(__float_as_uint(a) >> 22) - base)) * 32 + lane] += 1;
+        });
+        __syncwarp();
+        unsigned cnt = hist_reduce(hist);
+        unsigned incl = warp_incl_scan(cnt);
+        const unsigned total = __shfl_sync(FULL, incl, 31);
+        if (total > unsigned(K)) {
+            const int kstar = __ffs(__ballot_sync(FULL, incl >= unsigned(K))) - 1;
+            const double tsel =
+                kstar == 31 ? double(tc) : double(__uint_as_float(unsigned(kstar + base + 1) << 22));
+            const double mg = key_margin(tsel, ep);
+            if (!(use_r && !(tsel + mg <= r2))) {
+                tc = fminf(__double2float_ru(tsel + 2.0 * mg), tc);
+                C = compact_chunks(tc);
+            }
+            if (C > cap) {
+                // linear sub-buckets inside bucket kstar
+                const float lo = kstar == 0 ? 0.f : __uint_as_float(unsigned(kstar + base) << 22);
+                const float hi2 = float(tsel);
+                const unsigned below = __shfl_sync(FULL, incl - cnt, kstar);
+                const float w2 = (hi2 - lo) * (1.0f / 32.0f);
+                const float inv2 = w2 > 0.f ? 1.0f / w2 : 0.f;
+                over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a) {
+                    if (pos >= 0 && a >= lo && a < hi2) hist[min(31, max(0, int((a - lo) * inv2))) * 32 + lane] += 1;
+                });
+                __syncwarp();
+                cnt = hist_reduce(hist);
+                incl = warp_incl_scan(cnt) + below;
+                const int k2 = __ffs(__ballot_sync(FULL, incl >= unsigned(K))) - 1;
+                if (k2 >= 0) {
+                    const double t2 = (double(lo) + double(k2 + 1) * double(w2)) * (1.0 + 1e-6) + 1e-30;
+                    const double mg2 = key_margin(t2, ep);
+                    if (!(use_r && !(t2 + mg2 <= r2))) {
+                        tc = fminf(__double2float_ru(t2 + 2.0 * mg2), tc);
+                        C = compact_chunks(tc);
+                    }
+                }
+            }
+        }
     }
     if (C > cap) {
         // Pathological crowding at the threshold: exact iterative selection.
         double pk_ = -1.0;
-        int pi = -1, nsel = 0;
+        int po = -1, nsel = 0;
         for (int k = 0; k < K; ++k) {
             double best = INFINITY;
-            int bi = INT_MAX;
+            int bo = INT_MAX, bp = -1;
             for (int i = lane; i < n; i += 32) {
-                float2 p = pts[i];
-                double dx = double(p.x) - px, dy = double(p.y) - py;
-                double e = dx * dx + dy * dy;
+                const float2 p = ps.xy[i];
+                const double dx = double(p.x) - px, dy = double(p.y) - py;
+                const double e = dx * dx + dy * dy;
                 if (use_r && !(e <= r2)) continue;
-                bool after = e > pk_ || (e == pk_ && i > pi);
-                if (after && (e < best || (e == best && i < bi))) {
-                    best = e;
-                    bi = i;
-                }
+                const int o = ps.oi[i];
+                const bool after = e > pk_ || (e == pk_ && o > po);
+                if (after && (e < best || (e == best && o < bo))) best = e, bo = o, bp = i;
             }
             double bd;
             int bidx;
-            warp_argmin(best, bi, bd, bidx);
+            warp_argmin(best, bo, bd, bidx);
             if (bidx == INT_MAX || !(bd < INFINITY)) break;
-            if (lane == 0) sel[k] = bidx;
+            const int src = __ffs(__ballot_sync(FULL, bo == bidx && best == bd)) - 1;
+            const int bpos = __shfl_sync(FULL, bp, src);
+            if (lane == 0) order[k] = bpos;
             pk_ = bd;
-            pi = bidx;
+            po = bidx;
             ++nsel;
         }
         __syncwarp();
         return nsel;
     }
 
-    // exact fp64 keys (the reference's op order) + counting sort on them
-    unsigned* cntb = reinterpret_cast<unsigned*>(hist);  // NB2 u32 counters in the (cleared) histogram area
+    // ---- 4. exact fp64 keys (reference op order), counting sort, in-bucket rank ----
+    // cidx: candidate position, ckey: exact key, cinfo: reference index; the
+    // counting-sort counters / cursors live in the (clear) histogram area and
+    // the selection is written to `order` after the ranking is complete.
+    unsigned* cntb = reinterpret_cast<unsigned*>(hist);  // NB2 u32 counters
     const double sc2 = double(NB2) / (double(tc) > 0.0 ? double(tc) : 1.0);
     int nvalid_local = 0;
     for (int c = lane; c < C; c += 32) {
-        int i = cidx[c];
-        float2 p = pts[i];
-        double dx = double(p.x) - px, dy = double(p.y) - py;
-        double e = dx * dx + dy * dy;
-        int info = -1;
-        if (!use_r || e <= r2) {
-            int bk = min(NB2 - 1, int(e * sc2));
-            int slot = int(atomicAdd(&cntb[bk], 1u));
-            info = (bk << 16) | slot;
+        const int pos = cidx[c];
+        const float2 p = ps.xy[pos];
+        const double dx = double(p.x) - px, dy = double(p.y) - py;
+        const double e = dx * dx + dy * dy;
+        const bool ok = !use_r || e <= r2;
+        ckey[c] = ok ? e : INFINITY;
+        cinfo[c] = ps.oi[pos];
+        if (ok) {
+            atomicAdd(&cntb[min(NB2 - 1, int(e * sc2))], 1u);
             ++nvalid_local;
         }
-        ckey[c] = e;
-        cinfo[c] = info;
     }
     const int nvalid = int(__reduce_add_sync(FULL, unsigned(nvalid_local)));
     __syncwarp();
@@ -662,52 +716,44 @@ __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int
         unsigned run = warp_incl_scan(s) - s;
 #pragma unroll
         for (int k = 0; k < NB2 / 32; ++k) {
-            cntb[lane * (NB2 / 32) + k] = run;  // bucket start
+            cntb[lane * (NB2 / 32) + k] = run;            // bucket start
+            cntb[NB2 + lane * (NB2 / 32) + k] = run;      // scatter cursor
             run += v[k];
         }
     }
     __syncwarp();
     for (int c = lane; c < C; c += 32) {
-        int info = cinfo[c];
-        if (info >= 0) order[cntb[info >> 16] + (info & 0xFFFF)] = c;
+        const double e = ckey[c];
+        if (e < INFINITY) order[atomicAdd(&cntb[NB2 + min(NB2 - 1, int(e * sc2))], 1u)] = c;
     }
     __syncwarp();
-    // rank inside the bucket; ranks held in registers until every lane is
-    // done reading `order`, which then receives the selection
-    int rk[kMaxCandPerLane], ri[kMaxCandPerLane];
-#pragma unroll
-    for (int u = 0; u < kMaxCandPerLane; ++u) {
-        rk[u] = INT_MAX;
-        ri[u] = 0;
-        int c = lane + 32 * u;
-        if (c >= C) continue;
-        int info = cinfo[c];
-        if (info < 0) continue;
-        int bk = info >> 16;
-        unsigned start = cntb[bk];
-        unsigned end = bk + 1 < NB2 ? cntb[bk + 1] : unsigned(nvalid);
-        double e = ckey[c];
-        int i = cidx[c];
+    int* sel_tmp = reinterpret_cast<int*>(cntb + NB2);  // cursors are done: reuse as the selection
+    __syncwarp();
+    for (int c = lane; c < C; c += 32) {
+        const double e = ckey[c];
+        if (!(e < INFINITY)) continue;
+        const int bk = min(NB2 - 1, int(e * sc2));
+        const int o_self = cinfo[c];
+        const unsigned start = cntb[bk];
+        const unsigned end = bk + 1 < NB2 ? cntb[bk + 1] : unsigned(nvalid);
         unsigned rank = start;
 #pragma unroll 1
         for (unsigned q = start; q < end; ++q) {
-            int o = order[q];
-            double eo = ckey[o];
-            int io = cidx[o];
-            rank += (eo < e || (eo == e && io < i)) ? 1u : 0u;
+            const int o = order[q];
+            const double eo = ckey[o];
+            const int io = cinfo[o];
+            rank += (eo < e || (eo == e && io < o_self)) ? 1u : 0u;
         }
-        rk[u] = int(rank);
-        ri[u] = i;
+        if (rank < unsigned(K)) sel_tmp[rank] = cidx[c];
+        if (hint != nullptr && rank == unsigned(K - 1)) {
+            float* hk = which == 0 ? &hint->z : &hint->w;
+            *hk = __double2float_ru(e);
+        }
     }
     __syncwarp();
-#pragma unroll
-    for (int u = 0; u < kMaxCandPerLane; ++u) {
-        if (rk[u] < K) sel[rk[u]] = ri[u];
-        if (hint != nullptr && rk[u] == K - 1) {
-            float* hk = which == 0 ? &hint->z : &hint->w;
-            *hk = __double2float_ru(ckey[lane + 32 * u]);
-        }
-    }
+    const int nsel_out = min(K, nvalid);
+    for (int k = lane; k < nsel_out; k += 32) order[k] = sel_tmp[k];
+    __syncwarp();
     if (hint != nullptr && lane == 0) {
         if (nvalid < K) (which == 0 ? hint->z : hint->w) = INFINITY;  // fewer than k qualify: no bound
         if (which == 1) {  // both keys now refer to this position (road is selected first)
@@ -716,9 +762,9 @@ __device__ __noinline__ int warp_topk(const float2* __restrict__ pts, int n, int
         }
     }
     __syncwarp();
-    for (int k = lane; k < NB2; k += 32) cntb[k] = 0;
+    for (int k = lane; k < 2 * NB2; k += 32) cntb[k] = 0;
     __syncwarp();
-    return min(K, nvalid);
+    return nsel_out;
 }
 
 // ---------------------------------------------------------------------------
@@ -961,10 +1007,12 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     {
         const int n = pk.n_road[b];
         const float2* pts = pk.road_xy + size_t(b) * pk.d.P;
+        const int32_t* oidx = pk.road_oi + size_t(b) * pk.d.P;
         const double R = cfg.feature_radius;
         const int* sel = w.order;
-        const int nsel = warp_topk(pts, n, Kr, r.x, r.y, true, R * R, pk.road_box[b], a.cand_cap, w.hist, w.cidx,
-                                   w.ckey, w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 0);
+        const PointSet ps{pts, oidx, pk.road_cb + size_t(b) * pk.d.PC, n, (n + kChunk - 1) / kChunk};
+        const int nsel = warp_topk(ps, Kr, r.x, r.y, true, R * R, pk.road_box[b], a.cand_cap, w.hist, w.cidx, w.ckey,
+                                   w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 0);
         const uint8_t* kd = pk.road_kd + size_t(b) * pk.d.P;
         for (int k = lane; k < Kr; k += 32) {
             float f[12];
@@ -988,7 +1036,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
             o[0] = make_float4(f[0], f[1], f[2], f[3]);
             o[1] = make_float4(f[4], f[5], f[6], f[7]);
             o[2] = make_float4(f[8], f[9], f[10], f[11]);
-            if (dbg) dbg[Ka + k] = i;
+            if (dbg) dbg[Ka + k] = i < 0 ? -1 : oidx[i];
         }
     }
 
@@ -996,9 +1044,11 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     {
         const int n = pk.n_route[b];
         const float2* pts = pk.route_xy + size_t(b) * pk.d.R;
+        const int32_t* oidx = pk.route_oi + size_t(b) * pk.d.R;
         const int* sel = w.order;
-        const int nsel = warp_topk(pts, n, Kl, r.x, r.y, false, 0.0, pk.route_box[b], a.cand_cap, w.hist, w.cidx,
-                                   w.ckey, w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 1);
+        const PointSet ps{pts, oidx, pk.route_cb + size_t(b) * pk.d.RC, n, (n + kChunk - 1) / kChunk};
+        const int nsel = warp_topk(ps, Kl, r.x, r.y, false, 0.0, pk.route_box[b], a.cand_cap, w.hist, w.cidx, w.ckey,
+                                   w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 1);
         const uint8_t* fl = pk.route_fl + size_t(b) * pk.d.R;
         for (int k = lane; k < Kl; k += 32) {
             float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
@@ -1016,7 +1066,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
             float* o = rt + k * 5;
 #pragma unroll
             for (int q = 0; q < 5; ++q) o[q] = f[q];
-            if (dbg) dbg[Ka + Kr + k] = i;
+            if (dbg) dbg[Ka + Kr + k] = i < 0 ? -1 : oidx[i];
         }
     }
 }
@@ -1193,10 +1243,10 @@ __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int b, int t) 
         case 4: ptr = STEP ? pk.ln_len2 + lb : nullptr; bytes = LC * 8; break;
         case 5: ptr = STEP ? pk.ln_s + lb : nullptr; bytes = LC * 8; break;
         case 6: ptr = STEP ? pk.ln_hw + lb : nullptr; bytes = LC * 8; break;
-        case 7: ptr = OBS ? pk.road_xy + size_t(b) * pk.d.P : nullptr; bytes = size_t(pk.d.P) * 8; break;
-        case 8: ptr = OBS ? pk.road_kd + size_t(b) * pk.d.P : nullptr; bytes = size_t(pk.d.P); break;
+        case 7: ptr = OBS ? pk.road_cb + size_t(b) * pk.d.PC : nullptr; bytes = size_t(pk.d.PC) * 16; break;
+        case 8: ptr = OBS ? pk.route_cb + size_t(b) * pk.d.RC : nullptr; bytes = size_t(pk.d.RC) * 16; break;
         case 9: ptr = OBS ? pk.route_xy + size_t(b) * pk.d.R : nullptr; bytes = size_t(pk.d.R) * 8; break;
-        case 10: ptr = OBS ? pk.route_fl + size_t(b) * pk.d.R : nullptr; bytes = size_t(pk.d.R); break;
+        case 10: ptr = OBS ? pk.route_oi + size_t(b) * pk.d.R : nullptr; bytes = size_t(pk.d.R) * 4; break;
         case 11: ptr = pk.ag_x + as; bytes = size_t(A) * 4; break;
         case 12: ptr = pk.ag_y + as; bytes = size_t(A) * 4; break;
         case 13: ptr = pk.ag_h + as; bytes = size_t(A) * 4; break;

@@ -5,9 +5,11 @@
 // Per scenario b (reference types in /root/reference/proj/src/core/):
 //   agents  [B][T][A]  x, y, heading, speed f32 + valid u8   (LoggedAgent, scenario.hpp:37-44)
 //   dims    [B][A]     length, width f32
-//   road    [B][P]     float2 xy + u8 kind|dir<<4 in nearest_features' flat
-//                      (feature, point) order (roads.cpp:220-229)
-//   route   [B][R]     float2 xy + u8 is_left|lane_valid<<1 (simcore.cpp:181-200)
+//   road    [B][P]     float2 xy + u8 kind|dir<<4 + i32 index in nearest_features'
+//                      flat (feature, point) order (roads.cpp:220-229), stored in
+//                      Morton order as 32-point chunks with bounding boxes [B][PC]
+//   route   [B][R]     float2 xy + u8 is_left|lane_valid<<1 + i32 index in
+//                      build_route_points order (simcore.cpp:181-200), chunked likewise
 //   lanes   [B][L][C]  centerline x, y, s, half_width f64 after RouteFrame::build
 //                      clipping (roads.cpp:43-103) + per-segment b-a and |b-a|^2;
 //                      n vertices + lane_id per lane
@@ -26,7 +28,10 @@ namespace zs {
 
 struct PackDims {
     int32_t B, T, A, P, R, L, C, NL, NS;
+    int32_t PC, RC;  // 32-point chunks of the road / route point sets
 };
+
+constexpr int kChunk = 32;  // points per spatial chunk (one warp-wide load)
 
 struct DevPack {
     PackDims d;
@@ -61,10 +66,16 @@ struct DevPack {
     const float* ag_len;
     const float* ag_wid;
     // road / route points
+    // point sets in spatial (Morton) order, 32-point chunks with bounding boxes;
+    // *_oi is each point's index in the reference order (the tie-break key)
     const float2* road_xy;
     const uint8_t* road_kd;
+    const int32_t* road_oi;
+    const float4* road_cb;   // [B][PC] chunk boxes (min x, min y, max x, max y)
     const float2* route_xy;
     const uint8_t* route_fl;
+    const int32_t* route_oi;
+    const float4* route_cb;  // [B][RC]
     // lanes
     const double* ln_x;
     const double* ln_y;
