@@ -422,6 +422,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
             if (s.ego_x.empty()) raise(Err::invalid_argument, "scenario `" + s.id + "`: empty ego log");
         }
     }
+    d.GC = (d.C - 1 + kSegGroup - 1) / kSegGroup;
     d.PC = (d.P + kChunk - 1) / kChunk;
     d.RC = (d.R + kChunk - 1) / kChunk;
     if (d.L > kMaxLanes) {
@@ -450,6 +451,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
            o_lhw = pb.reserve<double>(nln);
     size_t o_labx = pb.reserve<double>(nln), o_laby = pb.reserve<double>(nln), o_llen2 = pb.reserve<double>(nln),
            o_linv2 = pb.reserve<double>(nln);
+    size_t o_lgb = pb.reserve<float>(size_t(B) * d.L * d.GC * 4);
     size_t o_ln = pb.reserve<int32_t>(size_t(B) * d.L), o_lid = pb.reserve<uint32_t>(size_t(B) * d.L);
     size_t o_rbox = pb.reserve<float>(size_t(B) * 4), o_tbox = pb.reserve<float>(size_t(B) * 4);
     size_t o_lts = pb.reserve<double>(size_t(B) * d.NL), o_ltst = pb.reserve<uint8_t>(size_t(B) * d.NL * d.T);
@@ -548,6 +550,20 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
 
         for (size_t l = 0; l < c.lanes.size(); ++l) {
             const LaneFrame& lf = c.lanes[l];
+            // group boxes: segments [g*8, g*8+8) touch vertices [g*8, g*8+8]
+            const int nseg = int(lf.x.size()) - 1;
+            for (int g = 0; g * kSegGroup < nseg; ++g) {
+                double x0 = 1e300, y0 = 1e300, x1 = -1e300, y1 = -1e300;
+                for (int v = g * kSegGroup; v <= std::min(nseg, (g + 1) * kSegGroup); ++v) {
+                    x0 = std::min(x0, lf.x[size_t(v)]), x1 = std::max(x1, lf.x[size_t(v)]);
+                    y0 = std::min(y0, lf.y[size_t(v)]), y1 = std::max(y1, lf.y[size_t(v)]);
+                }
+                float* gb = pb.at<float>(o_lgb) + ((size_t(b) * d.L + l) * d.GC + size_t(g)) * 4;
+                gb[0] = std::nextafter(float(x0), -3e38f);
+                gb[1] = std::nextafter(float(y0), -3e38f);
+                gb[2] = std::nextafter(float(x1), 3e38f);
+                gb[3] = std::nextafter(float(y1), 3e38f);
+            }
             pb.at<int32_t>(o_ln)[size_t(b) * d.L + l] = int32_t(lf.x.size());
             pb.at<uint32_t>(o_lid)[size_t(b) * d.L + l] = lf.lane_id;
             for (size_t i = 0; i < lf.x.size(); ++i) {
@@ -626,6 +642,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.ln_aby = reinterpret_cast<const double*>(D + o_laby);
     pk.ln_len2 = reinterpret_cast<const double*>(D + o_llen2);
     pk.ln_inv2 = reinterpret_cast<const double*>(D + o_linv2);
+    pk.ln_gb = reinterpret_cast<const float4*>(D + o_lgb);
     pk.road_box = reinterpret_cast<const float4*>(D + o_rbox);
     pk.route_box = reinterpret_cast<const float4*>(D + o_tbox);
     pk.ln_n = reinterpret_cast<const int32_t*>(D + o_ln);

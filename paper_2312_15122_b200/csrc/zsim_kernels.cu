@@ -42,7 +42,6 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int NQ = 5;     // projection queries per step: ego position + 4 inflated corners
 constexpr int NB2 = 256;  // counting-sort buckets over the exact keys
 constexpr int kUnroll = 8;  // independent point loads in flight per lane in the key passes
-constexpr int kMaxCandPerLane = 8;  // candidate cap / 32 (KernelArgs::cand_cap <= 256)
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int warp_in_block() { return threadIdx.x >> 5; }
@@ -88,9 +87,13 @@ __device__ __forceinline__ T pick5(int k, T a0, T a1, T a2, T a3, T a4) {
 struct WarpBuf {
     double* egx;           // [4] ego box corners (lane-indexed reads)
     double* egy;
-    int* plist;            // [64] projection candidate list
+    int* plist;            // unused
+    double* qx;            // [5] projection queries (ego position + inflated corners)
+    double* qy;
     double* agx;           // [A*4] agent corners
     double* agy;
+    float* agxf;           // [A*4] the same corners rounded to fp32 (distance screening)
+    float* agyf;
     double* agd;           // [A] bbox distance
     int* agf;              // [A] -1 invalid, 0 separate, 1 overlap
     int* surv;             // [A] agents whose bounds can reach the top n_agents
@@ -100,57 +103,76 @@ struct WarpBuf {
     int* cinfo;            // [cap] bucket << 16 | slot
     int* order;            // [cap] candidates grouped by bucket
     int* sel;              // [Ka] selected agents (road/route selections land in `order`)
+    int* acand;            // [cap] agent distance candidates (shares the top-k region)
     unsigned char* sflag;  // [NS] pre-step stopped flags
 };
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) / 16 * 16; }
 
-__host__ __device__ inline size_t warp_smem_bytes(int A, int cap, int ksum, int ns) {
-    size_t o = 64 + 256;
-    o += al16(size_t(A) * 4 * 8) * 2;
-    o += al16(size_t(A) * 8);
-    o += al16(size_t(A) * 4) * 2;
-    o += 32 * 32 * 2;
-    o += al16(size_t(cap) * 4);
-    o += al16(size_t(cap) * 8);
-    o += al16(size_t(cap) * 4) * 2;
-    o += al16(size_t(ksum) * 4);
-    o += al16(size_t(ns) + 1);
-    return al16(o);
+// Per-warp layout: [ego corners 64 B][union: agent phase | top-k phase][stop flags].
+// The agent buffers (boxes at t+1 from the step, distances, selection) are
+// dead once the agent features are written, before the road/route top-k, so
+// both phases share one region.
+struct WarpLayout {
+    size_t agx, agy, agxf, agyf, agd, agf, surv, sel, acand;  // agent phase
+    size_t hist, cidx, ckey, cinfo, order;                    // top-k phase
+    size_t sflag, total;
+};
+
+__host__ __device__ inline WarpLayout warp_layout(int A, int cap, int ka, int ns) {
+    WarpLayout L;
+    size_t o = 64 + 80 + 16;  // ego corners (64 B), projection queries (80 B), pad
+    const size_t u0 = o;
+    L.agx = o, o += al16(size_t(A) * 4 * 8);
+    L.agy = o, o += al16(size_t(A) * 4 * 8);
+    L.agxf = o, o += al16(size_t(A) * 4 * 4);
+    L.agyf = o, o += al16(size_t(A) * 4 * 4);
+    L.agd = o, o += al16(size_t(A) * 8);
+    L.agf = o, o += al16(size_t(A) * 4);
+    L.surv = o, o += al16(size_t(A) * 4);
+    L.sel = o, o += al16(size_t(ka) * 4);
+    L.acand = o, o += al16(size_t(cap > 0 ? cap : 0) * 4);  // agent screening candidates
+    const size_t agents_end = o;
+    o = u0;
+    L.hist = o, o += cap > 0 ? 32 * 32 * 2 : 0;  // no top-k buffers in the step-only kernel (cap = 0)
+    L.cidx = o, o += al16(size_t(cap) * 4);
+    L.ckey = o, o += al16(size_t(cap) * 8);
+    L.cinfo = o, o += al16(size_t(cap) * 4);
+    L.order = o, o += al16(size_t(cap) * 4);
+    o = o > agents_end ? o : agents_end;
+    L.sflag = o, o += al16(size_t(ns) + 1);
+    L.total = al16(o);
+    return L;
+}
+
+__host__ __device__ inline size_t warp_smem_bytes(int A, int cap, int ka, int ns) {
+    return warp_layout(A, cap, ka, ns).total;
 }
 
 __device__ WarpBuf carve(unsigned char* base, const KernelArgs& a) {
-    const int A = a.pk.d.A, cap = a.cand_cap;
-    const int ksum = a.cfg.n_agents;
-    unsigned char* p = base + warp_smem_bytes(A, cap, ksum, a.pk.d.NS) * size_t(warp_in_block());
+    const WarpLayout L = warp_layout(a.pk.d.A, a.cand_cap, a.cfg.n_agents, a.pk.d.NS);
+    unsigned char* p = base + L.total * size_t(warp_in_block());
     WarpBuf w;
     w.egx = reinterpret_cast<double*>(p);
     w.egy = reinterpret_cast<double*>(p + 32);
-    w.plist = reinterpret_cast<int*>(p + 64);
-    size_t o = 64 + 256;
-    w.agx = reinterpret_cast<double*>(p + o);
-    o += al16(size_t(A) * 4 * 8);
-    w.agy = reinterpret_cast<double*>(p + o);
-    o += al16(size_t(A) * 4 * 8);
-    w.agd = reinterpret_cast<double*>(p + o);
-    o += al16(size_t(A) * 8);
-    w.agf = reinterpret_cast<int*>(p + o);
-    o += al16(size_t(A) * 4);
-    w.surv = reinterpret_cast<int*>(p + o);
-    o += al16(size_t(A) * 4);
-    w.hist = reinterpret_cast<unsigned short*>(p + o);
-    o += 32 * 32 * 2;
-    w.cidx = reinterpret_cast<int*>(p + o);
-    o += al16(size_t(cap) * 4);
-    w.ckey = reinterpret_cast<double*>(p + o);
-    o += al16(size_t(cap) * 8);
-    w.cinfo = reinterpret_cast<int*>(p + o);
-    o += al16(size_t(cap) * 4);
-    w.order = reinterpret_cast<int*>(p + o);
-    o += al16(size_t(cap) * 4);
-    w.sel = reinterpret_cast<int*>(p + o);
-    o += al16(size_t(ksum) * 4);
-    w.sflag = p + o;
+    w.plist = nullptr;
+    w.qx = reinterpret_cast<double*>(p + 64);
+    w.qy = reinterpret_cast<double*>(p + 104);
+    w.agx = reinterpret_cast<double*>(p + L.agx);
+    w.agy = reinterpret_cast<double*>(p + L.agy);
+    w.agxf = reinterpret_cast<float*>(p + L.agxf);
+    w.agyf = reinterpret_cast<float*>(p + L.agyf);
+    w.agd = reinterpret_cast<double*>(p + L.agd);
+    w.agf = reinterpret_cast<int*>(p + L.agf);
+    w.surv = reinterpret_cast<int*>(p + L.surv);
+    w.sel = reinterpret_cast<int*>(p + L.sel);
+    w.acand = reinterpret_cast<int*>(p + L.acand);
+    w.hist = reinterpret_cast<unsigned short*>(p + L.hist);
+    w.cidx = reinterpret_cast<int*>(p + L.cidx);
+    w.ckey = reinterpret_cast<double*>(p + L.ckey);
+    w.cinfo = reinterpret_cast<int*>(p + L.cinfo);
+    w.order = reinterpret_cast<int*>(p + L.order);
+    w.sflag = p + L.sflag;
     return w;
 }
 
@@ -221,157 +243,132 @@ struct Proj {
     int on_route;  // all four inflated corners lie in some corridor (roads.cpp:192-208)
 };
 
-// Division-free screening value of point_segment_dist2: t = dot * (1/len2)
-// instead of dot / len2.  Differs from the exact value by far less than the
-// screening margin used by warp_project.
-__device__ __forceinline__ double seg_d2_screen(double px, double py, double ax, double ay, double abx, double aby,
-                                                double inv2) {
-    double dot = (px - ax) * abx + (py - ay) * aby;
-    double t = dot * inv2;
-    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
-    double qx = ax + abx * t, qy = ay + aby * t;
-    double ex = px - qx, ey = py - qy;
-    return ex * ex + ey * ey;
+// Lexicographic (d2, idx) min within aligned groups of 8 lanes.
+__device__ __forceinline__ void seg8_argmin(double& d2, int& idx) {
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) {
+        const double od = __shfl_xor_sync(FULL, d2, off);
+        const int oi = __shfl_xor_sync(FULL, idx, off);
+        if (od < d2 || (od == d2 && oi < idx)) {
+            d2 = od;
+            idx = oi;
+        }
+    }
 }
 
-__device__ __forceinline__ double warp_min_d(double v) {  // v >= 0 or +inf
-    unsigned hi = unsigned(__double2hiint(v)), lo = unsigned(__double2loint(v));
-    unsigned mhi = __reduce_min_sync(FULL, hi);
-    unsigned mlo = __reduce_min_sync(FULL, hi == mhi ? lo : 0xffffffffu);
-    return __hiloint2double(int(mhi), int(mlo));
+// Squared distance from a query to a (outward-rounded) box: a lower bound on
+// the exact fp64 point_segment_dist2 of every segment inside the box.
+__device__ __forceinline__ double box_lb(double qx, double qy, float4 bb) {
+    const double dx = fmax(fmax(double(bb.x) - qx, qx - double(bb.z)), 0.0);
+    const double dy = fmax(fmax(double(bb.y) - qy, qy - double(bb.w)), 0.0);
+    return (dx * dx + dy * dy) * (1.0 - 1e-12);
 }
 
 // roads::project for NQU queries (q0 = the point; q1..4 = footprint corners
 // when NQU == 5): per route lane the first strictly smaller d2 segment
 // (roads.cpp:125-143), across lanes min |d| then lane_id (roads.cpp:147-166).
-// Each lane of the warp screens its segments with the division-free value;
-// only segments within the screening margin of the per-query minimum are
-// evaluated exactly (IEEE division, reference op order), one per lane, and
-// the exact (d2, segment) argmin decides.  `list` is 64 ints of warp smem.
-// Uniform result.
+//
+// Blocks of 4 route lanes x 64 segments map onto the warp as lane =
+// (route lane, 8-segment group).  Per query and route lane, the group with the
+// smallest box lower bound is evaluated exactly (8 lanes, one segment each);
+// every other group whose bound does not exceed that exact minimum is
+// evaluated too; the exact lexicographic (d2, segment) minimum is the
+// reference's argmin.  Uniform result.
 template <int NQU>
-__device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const double* qy, int* list) {
-    const int L = pk.d.L, C = pk.d.C;
+__device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const double* qy, int* /*list*/) {
+    const int L = pk.d.L, C = pk.d.C, GC = pk.d.GC;
     const int nl = pk.n_lanes[b];
     const int lane = lane_id();
-    double mag = 1e4;
-#pragma unroll
-    for (int q = 0; q < NQU; ++q) mag = fmax(mag, qx[q] * qx[q] + qy[q] * qy[q]);
+    const int gl = lane >> 3, gg = lane & 7;
     bool have = false;
     double best_abs = 0.0, best_s = 0.0, best_d = 0.0;
     uint32_t best_id = 0;
     unsigned in_bits = 0;
-    for (int l = 0; l < nl; ++l) {
-        const size_t base = (size_t(b) * L + l) * C;
-        const double* X = pk.ln_x + base;
-        const double* Y = pk.ln_y + base;
-        const double* ABX = pk.ln_abx + base;
-        const double* ABY = pk.ln_aby + base;
-        const double* INV = pk.ln_inv2 + base;
-        const double* LEN2 = pk.ln_len2 + base;
-        const int nseg = pk.ln_n[size_t(b) * L + l] - 1;
-        // running exact best per query: (d2, segment) and the winner's s / d / hw
-        double bd2[NQU], bs[NQU], bd[NQU], bhw[NQU];
-        int bi[NQU];
-#pragma unroll
+    for (int l0 = 0; l0 < nl; l0 += 4) {
+        const int l = l0 + gl;
+        const bool lane_ok = l < nl;
+        const size_t lrow = size_t(b) * L + (lane_ok ? l : 0);
+        const size_t base = lrow * C;
+        const int nseg = lane_ok ? pk.ln_n[lrow] - 1 : 0;
+#pragma unroll 1
         for (int q = 0; q < NQU; ++q) {
-            bd2[q] = 1e300;
-            bi[q] = INT_MAX;
-            bs[q] = bd[q] = bhw[q] = 0.0;
-        }
-        for (int c0 = 0; c0 < nseg; c0 += 64) {
-            // screening: two segments per lane, one query at a time
-            double sx[2], sy[2], sbx[2], sby[2], sinv[2];
-            double lmax = 0.0;
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int i = c0 + lane + 32 * u;
-                const bool ok = i < nseg;
-                sx[u] = ok ? X[i] : 0.0;
-                sy[u] = ok ? Y[i] : 0.0;
-                sbx[u] = ok ? ABX[i] : 0.0;
-                sby[u] = ok ? ABY[i] : 0.0;
-                sinv[u] = ok ? INV[i] : 0.0;
-                if (ok) lmax = fmax(lmax, sbx[u] * sbx[u] + sby[u] * sby[u]);
-            }
-            // margin >= 2 x |screen - exact| (t differs by a few ulp)
-            const double lw = __hiloint2double(int(__reduce_max_sync(FULL, unsigned(__double2hiint(lmax)))), -1);
-            const double eta0 = 1e-12 * (mag + lw + 1.0);
-            int n = 0;
-#pragma unroll
-            for (int q = 0; q < NQU; ++q) {
-                double sc0 = c0 + lane < nseg ? seg_d2_screen(qx[q], qy[q], sx[0], sy[0], sbx[0], sby[0], sinv[0])
-                                               : INFINITY;
-                double sc1 = c0 + lane + 32 < nseg
-                                 ? seg_d2_screen(qx[q], qy[q], sx[1], sy[1], sbx[1], sby[1], sinv[1])
-                                 : INFINITY;
-                const double m = warp_min_d(fmin(sc0, sc1));
-                const double thr = m + 1e-12 * m + eta0;
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const bool cand = (u == 0 ? sc0 : sc1) <= thr;
-                    const unsigned bal = __ballot_sync(FULL, cand);
-                    if (cand) {
-                        const int pos = n + __popc(bal & lanemask_lt());
-                        if (pos < 64) list[pos] = (q << 16) | (c0 + lane + 32 * u);
-                    }
-                    n += __popc(bal);
-                }
-            }
-            __syncwarp();
-            if (n > 64) n = 64;  // cannot happen: >64 segments within 1e-12 relative of the minimum
-            // exact evaluation of the candidates, one per lane
-            for (int k0 = 0; k0 < n; k0 += 32) {
-                const int k = k0 + lane;
-                int q = -1, i = INT_MAX;
-                double d2 = 1e300, hs = 0.0, hd = 0.0, hhw = 0.0;
-                if (k < n) {
-                    const int e = list[k];
-                    q = e >> 16;
-                    i = e & 0xFFFF;
-                    double px, py;
-                    if constexpr (NQU == 1) {
-                        px = qx[0];
-                        py = qy[0];
-                    } else {
-                        px = pick5(q, qx[0], qx[1], qx[2], qx[3], qx[4]);
-                        py = pick5(q, qy[0], qy[1], qy[2], qy[3], qy[4]);
-                    }
-                    double t;
-                    d2 = seg_d2_pre(px, py, X[i], Y[i], ABX[i], ABY[i], LEN2[i], t);
-                    LaneHit h = lane_hit(px, py, X, Y, pk.ln_s + base, pk.ln_hw + base, i, d2, t);
-                    hs = h.s;
-                    hd = h.d;
-                    hhw = h.hw;
-                }
-#pragma unroll
-                for (int q2 = 0; q2 < NQU; ++q2) {
-                    double wd2;
-                    int wi;
-                    warp_argmin(q == q2 ? d2 : 1e300, q == q2 ? i : INT_MAX, wd2, wi);
-                    if (wi != INT_MAX && (wd2 < bd2[q2] || (wd2 == bd2[q2] && wi < bi[q2]))) {
-                        const int src = __ffs(__ballot_sync(FULL, q == q2 && i == wi)) - 1;
-                        bd2[q2] = wd2;
-                        bi[q2] = wi;
-                        bs[q2] = __shfl_sync(FULL, hs, src);
-                        bd[q2] = __shfl_sync(FULL, hd, src);
-                        bhw[q2] = __shfl_sync(FULL, hhw, src);
+            const double px = qx[q], py = qy[q];
+            double ub = 1e300;
+            int ib = INT_MAX;
+            for (int c0 = 0; c0 < C - 1; c0 += 8 * kSegGroup) {
+                const int g = c0 / kSegGroup + gg;
+                const bool gok = lane_ok && g * kSegGroup < nseg;
+                const double lb = gok ? box_lb(px, py, pk.ln_gb[lrow * GC + g]) : INFINITY;
+                // best-bound group of this route lane (ties: lowest group)
+                double bl = lb;
+                int bg = gok ? g : INT_MAX;
+                seg8_argmin(bl, bg);
+                // exact evaluation of its 8 segments, one per lane of the route lane's octet
+                double d2 = 1e300;
+                int i = INT_MAX;
+                if (bg != INT_MAX) {
+                    const int si = bg * kSegGroup + gg;
+                    if (si < nseg) {
+                        double t;
+                        d2 = seg_d2_pre(px, py, pk.ln_x[base + si], pk.ln_y[base + si], pk.ln_abx[base + si],
+                                        pk.ln_aby[base + si], pk.ln_len2[base + si], t);
+                        i = si;
                     }
                 }
+                seg8_argmin(d2, i);
+                if (d2 < ub || (d2 == ub && i < ib)) ub = d2, ib = i;
+                // any other group whose bound admits a segment <= the exact best
+                unsigned extra = __ballot_sync(FULL, gok && g != bg && lb <= ub);
+                while (extra) {
+                    const int src = __ffs(extra) - 1;
+                    extra &= extra - 1;
+                    const int eg = __shfl_sync(FULL, g, src);
+                    const int egl = src >> 3;
+                    double e2 = 1e300;
+                    int ei = INT_MAX;
+                    if (gl == egl) {
+                        const int si = eg * kSegGroup + gg;
+                        if (si < nseg) {
+                            double t;
+                            e2 = seg_d2_pre(px, py, pk.ln_x[base + si], pk.ln_y[base + si], pk.ln_abx[base + si],
+                                            pk.ln_aby[base + si], pk.ln_len2[base + si], t);
+                            ei = si;
+                        }
+                    }
+                    seg8_argmin(e2, ei);
+                    if (gl == egl && (e2 < ub || (e2 == ub && ei < ib))) ub = e2, ib = ei;
+                }
             }
-            __syncwarp();
-        }
-#pragma unroll
-        for (int q = 0; q < NQU; ++q)
-            if (bi[q] != INT_MAX && fabs(bd[q]) <= bhw[q]) in_bits |= 1u << q;
-        if (bi[0] != INT_MAX) {
-            uint32_t id = pk.ln_id[size_t(b) * L + l];
-            if (!have || fabs(bd[0]) < best_abs || (fabs(bd[0]) == best_abs && id < best_id)) {
-                have = true;
-                best_abs = fabs(bd[0]);
-                best_s = bs[0];
-                best_d = bd[0];
-                best_id = id;
+            // the first lane of each octet evaluates its route lane's winner:
+            // s, signed d, half-width (roads.cpp:130-139)
+            bool ok = false;
+            double hs = 0.0, hd = 0.0;
+            if (gg == 0 && lane_ok && ib != INT_MAX) {
+                const double* X = pk.ln_x + base;
+                const double* Y = pk.ln_y + base;
+                double t;
+                const double d2 = seg_d2_pre(px, py, X[ib], Y[ib], pk.ln_abx[base + ib], pk.ln_aby[base + ib],
+                                             pk.ln_len2[base + ib], t);
+                const LaneHit h = lane_hit(px, py, X, Y, pk.ln_s + base, pk.ln_hw + base, ib, d2, t);
+                hs = h.s;
+                hd = h.d;
+                ok = fabs(h.d) <= h.hw;
+            }
+            if (__ballot_sync(FULL, ok)) in_bits |= 1u << q;
+            if (q == 0) {
+                for (int k = 0; k < 4 && l0 + k < nl; ++k) {
+                    const double s0 = __shfl_sync(FULL, hs, k * 8), d0 = __shfl_sync(FULL, hd, k * 8);
+                    const int w0 = __shfl_sync(FULL, ib, k * 8);
+                    if (w0 == INT_MAX) continue;
+                    const uint32_t id = pk.ln_id[size_t(b) * L + l0 + k];
+                    if (!have || fabs(d0) < best_abs || (fabs(d0) == best_abs && id < best_id)) {
+                        have = true;
+                        best_abs = fabs(d0);
+                        best_s = s0;
+                        best_d = d0;
+                        best_id = id;
+                    }
+                }
             }
         }
     }
@@ -403,6 +400,8 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int b, size_
     for (int k = 0; k < 4; ++k) {
         w.agx[4 * j + k] = X[k];
         w.agy[4 * j + k] = Y[k];
+        w.agxf[4 * j + k] = float(X[k]);
+        w.agyf[4 * j + k] = float(Y[k]);
     }
     return boxes_overlap(eb, EX, EY, ab, X, Y) ? 1 : 0;
 }
@@ -933,32 +932,88 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     __syncwarp();
     const double* GX = w.egx;
     const double* GY = w.egy;
+    // (1) fp32 screening of the 32 pairs of every non-overlapping survivor
+    //     (one pass per survivor, lane = pair), (2) exact fp64 evaluation of
+    //     only the pairs within the screening error of each survivor's
+    //     minimum, compacted across survivors, (3) per-survivor min via a
+    //     64-bit atomicMin on the (non-negative) double bit patterns.
+    unsigned long long* dbits = reinterpret_cast<unsigned long long*>(w.agd);
+    const float egxf = lane < 4 ? float(pick5(lane, EX[0], EX[1], EX[2], EX[3], EX[3])) : 0.f;
+    const float egyf = lane < 4 ? float(pick5(lane, EY[0], EY[1], EY[2], EY[3], EY[3])) : 0.f;
+    const int e = lane & 15, pi = e >> 2, sj = e & 3, sj1 = (sj + 1) & 3;
+    const float exf_pi = __shfl_sync(FULL, egxf, pi), eyf_pi = __shfl_sync(FULL, egyf, pi);
+    const float exf_s0 = __shfl_sync(FULL, egxf, sj), eyf_s0 = __shfl_sync(FULL, egyf, sj);
+    const float exf_s1 = __shfl_sync(FULL, egxf, sj1), eyf_s1 = __shfl_sync(FULL, egyf, sj1);
+    const float mag = float(fabs(r.x) + fabs(r.y)) + 100.f;
+    int ncand = 0;
     for (int s = 0; s < nsurv; ++s) {
         const int j = w.surv[s];
         if (w.agf[j] == 1) {
             if (lane == 0) w.agd[j] = 0.0;  // obb_overlap => distance 0
             continue;
         }
-        const double* AX = w.agx + 4 * j;
-        const double* AY = w.agy + 4 * j;
-        const int e = lane & 15, pi = e >> 2, sj = e & 3, sj1 = (sj + 1) & 3;
-        double d2;
+        if (lane == 0) dbits[j] = 0x7FF0000000000000ull;  // +inf
+        const float* AX = w.agxf + 4 * j;
+        const float* AY = w.agyf + 4 * j;
+        float px, py, ax, ay, bx, by;
         if (lane < 16) {  // ego corner pi vs agent edge sj
-            d2 = seg_dist2(GX[pi], GY[pi], AX[sj], AY[sj], AX[sj1], AY[sj1]);
+            px = exf_pi, py = eyf_pi, ax = AX[sj], ay = AY[sj], bx = AX[sj1], by = AY[sj1];
         } else {  // agent corner pi vs ego edge sj
-            d2 = seg_dist2(AX[pi], AY[pi], GX[sj], GY[sj], GX[sj1], GY[sj1]);
+            px = AX[pi], py = AY[pi], ax = exf_s0, ay = eyf_s0, bx = exf_s1, by = eyf_s1;
         }
+        const float abx = bx - ax, aby = by - ay;
+        const float len2 = abx * abx + aby * aby;
+        float t = len2 > 0.f ? __fdividef((px - ax) * abx + (py - ay) * aby, len2) : 0.f;
+        t = fminf(fmaxf(t, 0.f), 1.f);
+        const float qx = px - (ax + abx * t), qy = py - (ay + aby * t);
+        const float d = sqrtf(qx * qx + qy * qy);
+        const float dmin = __uint_as_float(__reduce_min_sync(FULL, __float_as_uint(d)));
+        // fp32 rounding of the corners (<= 2^-24 |c|), of the arithmetic and of t
+        const bool cand = d <= dmin + 2e-6f * (mag + dmin) + 1e-4f;
+        const unsigned bal = __ballot_sync(FULL, cand);
+        if (cand) {
+            const int q = ncand + __popc(bal & lanemask_lt());
+            if (q < a.cand_cap) w.acand[q] = (s << 5) | lane;
+        }
+        ncand += __popc(bal);
+    }
+    __syncwarp();
+    if (ncand <= a.cand_cap) {
+        for (int k = lane; k < ncand; k += 32) {
+            const int s = w.acand[k] >> 5, ln = w.acand[k] & 31;
+            const int j = w.surv[s];
+            const double* AX = w.agx + 4 * j;
+            const double* AY = w.agy + 4 * j;
+            const int ee = ln & 15, ci = ee >> 2, ei = ee & 3, ei1 = (ei + 1) & 3;
+            const double d2 = ln < 16 ? seg_dist2(GX[ci], GY[ci], AX[ei], AY[ei], AX[ei1], AY[ei1])
+                                      : seg_dist2(AX[ci], AY[ci], GX[ei], GY[ei], GX[ei1], GY[ei1]);
+            atomicMin(&dbits[j], static_cast<unsigned long long>(__double_as_longlong(d2)));
+        }
+    } else {
+        // too many near-ties to list: every pair of every survivor exactly
+        for (int s = 0; s < nsurv; ++s) {
+            const int j = w.surv[s];
+            if (w.agf[j] == 1) continue;
+            const double* AX = w.agx + 4 * j;
+            const double* AY = w.agy + 4 * j;
+            const double d2 = lane < 16 ? seg_dist2(GX[pi], GY[pi], AX[sj], AY[sj], AX[sj1], AY[sj1])
+                                        : seg_dist2(AX[pi], AY[pi], GX[sj], GY[sj], GX[sj1], GY[sj1]);
+            atomicMin(&dbits[j], static_cast<unsigned long long>(__double_as_longlong(d2)));
+        }
+    }
+    __syncwarp();
+    // (near-)contact: a strict edge crossing is possible, so take the
+    // reference's full segment_segment_distance over the 16 pairs.
+    for (int s = 0; s < nsurv; ++s) {
+        const int j = w.surv[s];
+        if (w.agf[j] == 1 || !(w.agd[j] < 1e-18)) continue;
+        double v = INFINITY;
+        if (lane < 16) v = box_edge_pair_dist2(GX, GY, w.agx + 4 * j, w.agy + 4 * j, lane >> 2, lane & 3);
         double md2;
         int dummy;
-        warp_argmin(d2, 0, md2, dummy);
-        if (md2 < 1e-18) {
-            // (near-)contact: a strict edge crossing is possible, so take the
-            // reference's full segment_segment_distance over the 16 pairs.
-            double v = INFINITY;
-            if (lane < 16) v = box_edge_pair_dist2(GX, GY, AX, AY, lane >> 2, lane & 3);
-            warp_argmin(v, 0, md2, dummy);
-        }
+        warp_argmin(v, 0, md2, dummy);
         if (lane == 0) w.agd[j] = md2;
+        __syncwarp();
     }
     __syncwarp();
     for (int s = lane; s < nsurv; s += 32) {
@@ -1004,6 +1059,10 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     }
 
     // ---- road network points: nearest_features (roads.cpp:210-236) ----
+    // the top-k region overlays the (now dead) agent buffers: clear the histogram
+    __syncwarp();
+    for (int k = lane; k < 32 * 32; k += 32) w.hist[k] = 0;
+    __syncwarp();
     {
         const int n = pk.n_road[b];
         const float2* pts = pk.road_xy + size_t(b) * pk.d.P;
@@ -1134,16 +1193,18 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
     eb.c = sc1.y;
     eb.s = sc1.x;
     box_corners(eb, EX, EY);
-    double qx[NQ], qy[NQ];
-    {
+    if (lane == 0) {
         Box inf = eb;
         inf.hl = eb.hl + cfg.footprint_margin;
         inf.hw = eb.hw + cfg.footprint_margin;
-        qx[0] = r.x;
-        qy[0] = r.y;
-        box_corners(inf, qx + 1, qy + 1);
+        double X[4], Y[4];
+        box_corners(inf, X, Y);
+        w.qx[0] = r.x;
+        w.qy[0] = r.y;
+        for (int k = 0; k < 4; ++k) w.qx[k + 1] = X[k], w.qy[k + 1] = Y[k];
     }
-    const Proj p1 = warp_project<NQ>(pk, b, qx, qy, w.plist);
+    __syncwarp();
+    const Proj p1 = warp_project<NQ>(pk, b, w.qx, w.qy, nullptr);
 
     // collision with the agents valid at t+1 (simcore.cpp:323-331); boxes kept for observe(t+1)
     int hit = 0;
@@ -1260,11 +1321,9 @@ __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int b, int t) 
 }
 
 template <bool STEP, bool OBS>
-__global__ void __launch_bounds__(kThreads, 4) k_step_observe(const KernelArgs a) {
+__global__ void __launch_bounds__(kThreads, 7) k_step_observe(const KernelArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const WarpBuf w = carve(dsm, a);
-    for (int k = lane_id(); k < 32 * 32; k += 32) w.hist[k] = 0;  // warp_topk leaves it cleared (u16)
-    __syncwarp();
     const int wpb = kThreads / 32;
     const int stride = gridDim.x * wpb;
     int b = blockIdx.x * wpb + warp_in_block();
@@ -1372,12 +1431,14 @@ static int persistent_grid(K kern, const KernelArgs& a, size_t smem) {
 
 cudaError_t launch_step_observe(const KernelArgs& a, int mode, int grid, cudaStream_t stream) {
     (void)grid;
-    const size_t smem = smem_bytes(a);
+    KernelArgs am = a;
+    if (mode == kModeStep) am.cand_cap = 0;  // the step-only kernel carves no top-k buffers
+    const size_t smem = smem_bytes(am);
     auto launch = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
-        const int g = persistent_grid(kern, a, smem);
-        kern<<<g, kThreads, smem, stream>>>(a);
+        const int g = persistent_grid(kern, am, smem);
+        kern<<<g, kThreads, smem, stream>>>(am);
         return cudaGetLastError();
     };
     switch (mode) {

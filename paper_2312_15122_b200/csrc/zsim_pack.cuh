@@ -29,7 +29,10 @@ namespace zs {
 struct PackDims {
     int32_t B, T, A, P, R, L, C, NL, NS;
     int32_t PC, RC;  // 32-point chunks of the road / route point sets
+    int32_t GC;      // 8-segment groups per lane centerline
 };
+
+constexpr int kSegGroup = 8;  // segments per centerline group (bounding box)
 
 constexpr int kChunk = 32;  // points per spatial chunk (one warp-wide load)
 
@@ -85,6 +88,7 @@ struct DevPack {
     const double* ln_aby;
     const double* ln_len2;  // |b - a|^2 with the reference's op order
     const double* ln_inv2;  // 1 / len2 (0 for a degenerate segment): division-free candidate screening
+    const float4* ln_gb;    // [B][L][GC] bounding boxes of 8-segment groups (rounded outward)
     const int32_t* ln_n;
     const uint32_t* ln_id;
     const float4* road_box;   // [B] (min x, min y, max x, max y) of the road points
