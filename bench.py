@@ -17,6 +17,7 @@ Rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -238,12 +239,15 @@ def run_ours(args) -> None:
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     resets = 0
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.disable()  # a collector pause in the launch loop would idle the GPU inside the timed region
     start.record(stream)
     for i in range(args.steps):
         resets += 1 if k_state["k"] % EPISODE == 0 else 0
         cur, nxt = one_step(cur, nxt, ev[i])
     end.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     clk = clocks.stop()
     if dist:
         dist.barrier()

@@ -50,32 +50,41 @@ def _run(cmd: list[str]) -> str:
     return r.stdout + r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+# Diagnostic variant (tools/episode_profile.py): the same sources with
+# per-path counters compiled in (ZS_PATHSTATS); never loaded by the product.
+PATHSTATS_OUT = BUILD / "pathstats" / "libzsim_gpu_pathstats.so"
+
+
+def build(force: bool = False, verbose: bool = False, pathstats: bool = False) -> Path:
     """Compile libzsim_gpu.so (no-op when up to date)."""
-    if not force and not _stale():
-        return OUT
-    BUILD.mkdir(exist_ok=True)
+    out, bdir, defs = OUT, BUILD, []
+    if pathstats:
+        out, bdir, defs = PATHSTATS_OUT, PATHSTATS_OUT.parent, ["-DZS_PATHSTATS"]
+    if not force and not (_stale() if not pathstats else not out.exists() or any(
+            p.stat().st_mtime > out.stat().st_mtime for p in _sources())):
+        return out
+    bdir.mkdir(parents=True, exist_ok=True)
     jobs = []
     for s in CU_SOURCES:
-        o = BUILD / (s + ".o")
+        o = bdir / (s + ".o")
         extra = ["-Xptxas", "-v"] if verbose else []
-        jobs.append([NVCC, *CUDA_FLAGS, *extra, "-I", str(PKG.parent / "include"), "-c", str(CSRC / s), "-o", str(o)])
+        jobs.append([NVCC, *CUDA_FLAGS, *defs, *extra, "-I", str(PKG.parent / "include"), "-c", str(CSRC / s), "-o",
+                     str(o)])
     for s in CXX_SOURCES:
-        o = BUILD / (s + ".o")
+        o = bdir / (s + ".o")
         jobs.append([CXX, *CXX_FLAGS, "-I", str(PKG.parent / "include"), "-c", str(CSRC / s), "-o", str(o)])
     logs = []
     with cf.ThreadPoolExecutor(max_workers=min(4, os.cpu_count() or 1)) as ex:
         for log in ex.map(_run, jobs):
             logs.append(log)
-    objs = [str(BUILD / (s + ".o")) for s in CU_SOURCES + CXX_SOURCES]
-    tmp = OUT.with_suffix(".so.tmp")
+    objs = [str(bdir / (s + ".o")) for s in CU_SOURCES + CXX_SOURCES]
+    tmp = out.with_suffix(".so.tmp")
     _run([NVCC, "-shared", *ARCH, "-Xcompiler", "-fPIC", "-o", str(tmp), *objs, "-lpthread"])
-    os.replace(tmp, OUT)
+    os.replace(tmp, out)
     if verbose:
         sys.stderr.write("\n".join(l for l in logs if l.strip()) + "\n")
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(OUT)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, pathstats="--pathstats" in sys.argv))

@@ -422,7 +422,6 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
             if (s.ego_x.empty()) raise(Err::invalid_argument, "scenario `" + s.id + "`: empty ego log");
         }
     }
-    d.GC = (d.C - 1 + kSegGroup - 1) / kSegGroup;
     d.PC = (d.P + kChunk - 1) / kChunk;
     d.RC = (d.R + kChunk - 1) / kChunk;
     if (d.L > kMaxLanes) {
@@ -449,9 +448,9 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     const size_t nln = size_t(B) * d.L * d.C;
     size_t o_lx = pb.reserve<double>(nln), o_ly = pb.reserve<double>(nln), o_ls = pb.reserve<double>(nln),
            o_lhw = pb.reserve<double>(nln);
-    size_t o_labx = pb.reserve<double>(nln), o_laby = pb.reserve<double>(nln), o_llen2 = pb.reserve<double>(nln),
-           o_linv2 = pb.reserve<double>(nln);
-    size_t o_lgb = pb.reserve<float>(size_t(B) * d.L * d.GC * 4);
+    size_t o_labx = pb.reserve<double>(nln), o_laby = pb.reserve<double>(nln), o_llen2 = pb.reserve<double>(nln);
+    size_t o_lf4 = pb.reserve<float>(nln * 4), o_lorg = pb.reserve<double>(size_t(B) * 2),
+           o_lfe = pb.reserve<float>(size_t(B));
     size_t o_ln = pb.reserve<int32_t>(size_t(B) * d.L), o_lid = pb.reserve<uint32_t>(size_t(B) * d.L);
     size_t o_rbox = pb.reserve<float>(size_t(B) * 4), o_tbox = pb.reserve<float>(size_t(B) * 4);
     size_t o_lts = pb.reserve<double>(size_t(B) * d.NL), o_ltst = pb.reserve<uint8_t>(size_t(B) * d.NL * d.T);
@@ -548,22 +547,12 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
             tb[0] = tx0, tb[1] = ty0, tb[2] = tx1, tb[3] = ty1;
         }
 
+        // origin of the fp32 screening copy: the first vertex of the first lane
+        double ox = 0.0, oy = 0.0;
+        if (!c.lanes.empty() && !c.lanes[0].x.empty()) ox = c.lanes[0].x[0], oy = c.lanes[0].y[0];
+        double fe_s = 0.0, fe_l = 0.0;
         for (size_t l = 0; l < c.lanes.size(); ++l) {
             const LaneFrame& lf = c.lanes[l];
-            // group boxes: segments [g*8, g*8+8) touch vertices [g*8, g*8+8]
-            const int nseg = int(lf.x.size()) - 1;
-            for (int g = 0; g * kSegGroup < nseg; ++g) {
-                double x0 = 1e300, y0 = 1e300, x1 = -1e300, y1 = -1e300;
-                for (int v = g * kSegGroup; v <= std::min(nseg, (g + 1) * kSegGroup); ++v) {
-                    x0 = std::min(x0, lf.x[size_t(v)]), x1 = std::max(x1, lf.x[size_t(v)]);
-                    y0 = std::min(y0, lf.y[size_t(v)]), y1 = std::max(y1, lf.y[size_t(v)]);
-                }
-                float* gb = pb.at<float>(o_lgb) + ((size_t(b) * d.L + l) * d.GC + size_t(g)) * 4;
-                gb[0] = std::nextafter(float(x0), -3e38f);
-                gb[1] = std::nextafter(float(y0), -3e38f);
-                gb[2] = std::nextafter(float(x1), 3e38f);
-                gb[3] = std::nextafter(float(y1), 3e38f);
-            }
             pb.at<int32_t>(o_ln)[size_t(b) * d.L + l] = int32_t(lf.x.size());
             pb.at<uint32_t>(o_lid)[size_t(b) * d.L + l] = lf.lane_id;
             for (size_t i = 0; i < lf.x.size(); ++i) {
@@ -572,6 +561,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
                 pb.at<double>(o_ly)[k] = lf.y[i];
                 pb.at<double>(o_ls)[k] = lf.s[i];
                 pb.at<double>(o_lhw)[k] = lf.hw[i];
+                fe_s = std::max(fe_s, std::fabs(lf.x[i] - ox) + std::fabs(lf.y[i] - oy));
                 if (i + 1 < lf.x.size()) {
                     // point_segment_dist2's ab = b - a and len2 = ab.norm2() (geometry.cpp:18-19)
                     double abx = lf.x[i + 1] - lf.x[i], aby = lf.y[i + 1] - lf.y[i];
@@ -579,10 +569,18 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
                     pb.at<double>(o_laby)[k] = aby;
                     double len2 = abx * abx + aby * aby;
                     pb.at<double>(o_llen2)[k] = len2;
-                    pb.at<double>(o_linv2)[k] = len2 > 0.0 ? 1.0 / len2 : 0.0;
+                    fe_l = std::max(fe_l, std::fabs(abx) + std::fabs(aby));
+                    float* f4 = pb.at<float>(o_lf4) + 4 * k;
+                    f4[0] = float(lf.x[i] - ox);
+                    f4[1] = float(lf.y[i] - oy);
+                    f4[2] = float(abx);
+                    f4[3] = float(aby);
                 }
             }
         }
+        pb.at<double>(o_lorg)[2 * size_t(b)] = ox;
+        pb.at<double>(o_lorg)[2 * size_t(b) + 1] = oy;
+        pb.at<float>(o_lfe)[b] = float((fe_s + fe_l) * (1.0 + 1e-6)) + 1e-6f;
         for (size_t k = 0; k < c.lights.size(); ++k) {
             pb.at<double>(o_lts)[size_t(b) * d.NL + k] = c.lights[k].second;
             const auto& st = s.lights[size_t(c.lights[k].first)].state;
@@ -641,8 +639,9 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.ln_abx = reinterpret_cast<const double*>(D + o_labx);
     pk.ln_aby = reinterpret_cast<const double*>(D + o_laby);
     pk.ln_len2 = reinterpret_cast<const double*>(D + o_llen2);
-    pk.ln_inv2 = reinterpret_cast<const double*>(D + o_linv2);
-    pk.ln_gb = reinterpret_cast<const float4*>(D + o_lgb);
+    pk.ln_f4 = reinterpret_cast<const float4*>(D + o_lf4);
+    pk.ln_org = reinterpret_cast<const double2*>(D + o_lorg);
+    pk.ln_fe = reinterpret_cast<const float*>(D + o_lfe);
     pk.road_box = reinterpret_cast<const float4*>(D + o_rbox);
     pk.route_box = reinterpret_cast<const float4*>(D + o_tbox);
     pk.ln_n = reinterpret_cast<const int32_t*>(D + o_ln);

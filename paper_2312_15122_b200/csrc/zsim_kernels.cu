@@ -43,6 +43,31 @@ constexpr int NQ = 5;     // projection queries per step: ego position + 4 infla
 constexpr int NB2 = 256;  // counting-sort buckets over the exact keys
 constexpr int kUnroll = 8;  // independent point loads in flight per lane in the key passes
 
+// Diagnostic path counters, compiled only into the ZS_PATHSTATS variant
+// (build.py --pathstats); the product library has none of this code.
+#ifdef ZS_PATHSTATS
+__device__ unsigned long long g_pstats[32];
+#define PSTAT(i, v)                                                          \
+    do {                                                                     \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_pstats[(i)], (unsigned long long)(v)); \
+    } while (0)
+// per-row SM clock stamps (low 32 bits) at marks 0..7; the host differences them
+constexpr int kMaxStatRows = 65536;
+__device__ unsigned g_rowcyc[kMaxStatRows][8];
+__device__ __forceinline__ void row_mark(int b, int k) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0 && b < kMaxStatRows) g_rowcyc[b][k] = unsigned(clock64());
+}
+#define ROW_MARK(b, k) row_mark((b), (k))
+#else
+#define PSTAT(i, v) \
+    do {            \
+    } while (0)
+#define ROW_MARK(b, k) \
+    do {               \
+    } while (0)
+#endif
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int warp_in_block() { return threadIdx.x >> 5; }
 __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
@@ -92,66 +117,49 @@ struct WarpBuf {
     double* qy;
     double* agx;           // [A*4] agent corners
     double* agy;
-    float* agxf;           // [A*4] the same corners rounded to fp32 (distance screening)
-    float* agyf;
     double* agd;           // [A] bbox distance
     int* agf;              // [A] -1 invalid, 0 separate, 1 overlap
-    int* surv;             // [A] agents whose bounds can reach the top n_agents
     unsigned short* hist;  // [32*32] lane-private u16 histogram; reused as counting-sort counts u32[NB2]
     int* cidx;             // [cap] candidate indices
     double* ckey;          // [cap] exact keys
     int* cinfo;            // [cap] bucket << 16 | slot
     int* order;            // [cap] candidates grouped by bucket
     int* sel;              // [Ka] selected agents (road/route selections land in `order`)
-    int* acand;            // [cap] agent distance candidates (shares the top-k region)
     unsigned char* sflag;  // [NS] pre-step stopped flags
 };
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) / 16 * 16; }
 
-// Per-warp layout: [ego corners 64 B][union: agent phase | top-k phase][stop flags].
+// Per-warp layout: [ego corners 64 B][queries 80 B][union: agent phase | top-k phase][stop flags].
 // The agent buffers (boxes at t+1 from the step, distances, selection) are
 // dead once the agent features are written, before the road/route top-k, so
 // both phases share one region.
-struct WarpLayout {
-    size_t agx, agy, agxf, agyf, agd, agf, surv, sel, acand;  // agent phase
-    size_t hist, cidx, ckey, cinfo, order;                    // top-k phase
-    size_t sflag, total;
-};
-
-__host__ __device__ inline WarpLayout warp_layout(int A, int cap, int ka, int ns) {
-    WarpLayout L;
+inline SmemLayout warp_layout(int A, int cap, int ka, int ns) {
+    SmemLayout L;
     size_t o = 64 + 80 + 16;  // ego corners (64 B), projection queries (80 B), pad
     const size_t u0 = o;
-    L.agx = o, o += al16(size_t(A) * 4 * 8);
-    L.agy = o, o += al16(size_t(A) * 4 * 8);
-    L.agxf = o, o += al16(size_t(A) * 4 * 4);
-    L.agyf = o, o += al16(size_t(A) * 4 * 4);
-    L.agd = o, o += al16(size_t(A) * 8);
-    L.agf = o, o += al16(size_t(A) * 4);
-    L.surv = o, o += al16(size_t(A) * 4);
-    L.sel = o, o += al16(size_t(ka) * 4);
-    L.acand = o, o += al16(size_t(cap > 0 ? cap : 0) * 4);  // agent screening candidates
+    auto put = [&](uint32_t& f, size_t bytes) { f = uint32_t(o), o += al16(bytes); };
+    put(L.agx, size_t(A) * 4 * 8);
+    put(L.agy, size_t(A) * 4 * 8);
+    put(L.agd, size_t(A) * 8);
+    put(L.agf, size_t(A) * 4);
+    put(L.sel, size_t(ka) * 4);
     const size_t agents_end = o;
     o = u0;
-    L.hist = o, o += cap > 0 ? 32 * 32 * 2 : 0;  // no top-k buffers in the step-only kernel (cap = 0)
-    L.cidx = o, o += al16(size_t(cap) * 4);
-    L.ckey = o, o += al16(size_t(cap) * 8);
-    L.cinfo = o, o += al16(size_t(cap) * 4);
-    L.order = o, o += al16(size_t(cap) * 4);
+    put(L.hist, cap > 0 ? 32 * 32 * 2 : 0);  // no top-k buffers in the step-only kernel (cap = 0)
+    put(L.cidx, size_t(cap) * 4);
+    put(L.ckey, size_t(cap) * 8);
+    put(L.cinfo, size_t(cap) * 4);
+    put(L.order, size_t(cap) * 4);
     o = o > agents_end ? o : agents_end;
-    L.sflag = o, o += al16(size_t(ns) + 1);
-    L.total = al16(o);
+    put(L.sflag, size_t(ns) + 1);
+    L.total = uint32_t(al16(o));
     return L;
 }
 
-__host__ __device__ inline size_t warp_smem_bytes(int A, int cap, int ka, int ns) {
-    return warp_layout(A, cap, ka, ns).total;
-}
-
-__device__ WarpBuf carve(unsigned char* base, const KernelArgs& a) {
-    const WarpLayout L = warp_layout(a.pk.d.A, a.cand_cap, a.cfg.n_agents, a.pk.d.NS);
-    unsigned char* p = base + L.total * size_t(warp_in_block());
+__device__ __forceinline__ WarpBuf carve(unsigned char* base, const KernelArgs& a) {
+    const SmemLayout& L = a.lay;
+    unsigned char* p = base + L.total * unsigned(warp_in_block());
     WarpBuf w;
     w.egx = reinterpret_cast<double*>(p);
     w.egy = reinterpret_cast<double*>(p + 32);
@@ -160,13 +168,9 @@ __device__ WarpBuf carve(unsigned char* base, const KernelArgs& a) {
     w.qy = reinterpret_cast<double*>(p + 104);
     w.agx = reinterpret_cast<double*>(p + L.agx);
     w.agy = reinterpret_cast<double*>(p + L.agy);
-    w.agxf = reinterpret_cast<float*>(p + L.agxf);
-    w.agyf = reinterpret_cast<float*>(p + L.agyf);
     w.agd = reinterpret_cast<double*>(p + L.agd);
     w.agf = reinterpret_cast<int*>(p + L.agf);
-    w.surv = reinterpret_cast<int*>(p + L.surv);
     w.sel = reinterpret_cast<int*>(p + L.sel);
-    w.acand = reinterpret_cast<int*>(p + L.acand);
     w.hist = reinterpret_cast<unsigned short*>(p + L.hist);
     w.cidx = reinterpret_cast<int*>(p + L.cidx);
     w.ckey = reinterpret_cast<double*>(p + L.ckey);
@@ -256,119 +260,211 @@ __device__ __forceinline__ void seg8_argmin(double& d2, int& idx) {
     }
 }
 
-// Squared distance from a query to a (outward-rounded) box: a lower bound on
-// the exact fp64 point_segment_dist2 of every segment inside the box.
-__device__ __forceinline__ double box_lb(double qx, double qy, float4 bb) {
-    const double dx = fmax(fmax(double(bb.x) - qx, qx - double(bb.z)), 0.0);
-    const double dy = fmax(fmax(double(bb.y) - qy, qy - double(bb.w)), 0.0);
-    return (dx * dx + dy * dy) * (1.0 - 1e-12);
+__device__ __forceinline__ float octet_minf(float v) {
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) v = fminf(v, __shfl_xor_sync(FULL, v, off));
+    return v;
+}
+
+// fp32 screening distance^2 from (qx, qy) (origin-relative) to segment f =
+// (a - origin, b - a); inv ~ 1/|b-a|^2 (0 for a degenerate segment).
+__device__ __forceinline__ float seg_d2_f(float qx, float qy, float4 f, float inv) {
+    const float dx = qx - f.x, dy = qy - f.y;
+    float t = __fmul_rn(__fmaf_rn(dx, f.z, __fmul_rn(dy, f.w)), inv);
+    t = fminf(fmaxf(t, 0.f), 1.f);
+    const float ex = __fmaf_rn(-f.z, t, dx), ey = __fmaf_rn(-f.w, t, dy);
+    return __fmaf_rn(ex, ex, __fmul_rn(ey, ey));
+}
+
+__device__ __forceinline__ float seg_inv_f(float4 f) {
+    const float l2 = __fmaf_rn(f.z, f.z, __fmul_rn(f.w, f.w));
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l2));  // <= 1 ulp: inside the screening bound
+    return l2 > 1e-30f ? r : 0.f;
 }
 
 // roads::project for NQU queries (q0 = the point; q1..4 = footprint corners
 // when NQU == 5): per route lane the first strictly smaller d2 segment
 // (roads.cpp:125-143), across lanes min |d| then lane_id (roads.cpp:147-166).
 //
-// Blocks of 4 route lanes x 64 segments map onto the warp as lane =
-// (route lane, 8-segment group).  Per query and route lane, the group with the
-// smallest box lower bound is evaluated exactly (8 lanes, one segment each);
-// every other group whose bound does not exceed that exact minimum is
-// evaluated too; the exact lexicographic (d2, segment) minimum is the
-// reference's argmin.  Uniform result.
+// Blocks of 4 route lanes map onto the warp's 4 octets; lane gg of an octet
+// owns segments gg, gg+8, ...  Screening is fp32 on an origin-relative copy
+// (ln_f4).  Error bound: the copy moves every segment point by <= 2^-24
+// (|a-o|_1 + |b-a|_1) and a query by <= 2^-24 |q-o|_1; the fp32 arithmetic
+// (approximate t, clamped, so the evaluated point stays on the segment) adds
+// <= 2^-20 (d + |b-a|); so |d_f32 - d_exact| <= delta = 2^-18 (fe + |q-o|_1 + d)
+// with fe = ln_fe.
+//  1. fp32 distance of every segment to q0, minimum m0.
+//  2. The corners lie within R of q0, so (triangle inequality) the exact
+//     minimiser of any query lies among the "near" segments with
+//     d0 <= sqrt(m0) + 2R + 4 delta; their fp32 distances give each query's
+//     minimum m_q.
+//  3. Near segments with d_q <= sqrt(m_q) + 2 delta (every segment that can
+//     tie the exact minimum) are evaluated in fp64 with the reference's
+//     expressions; the exact lexicographic (d2, segment) minimum per octet is
+//     the reference's argmin.
+// The winners' s / signed d / half-width run one (query, route lane) pair per
+// lane.  Uniform result.
 template <int NQU>
-__device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const double* qy, int* /*list*/) {
-    const int L = pk.d.L, C = pk.d.C, GC = pk.d.GC;
+__device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const double* qy) {
+    const int L = pk.d.L, C = pk.d.C;
     const int nl = pk.n_lanes[b];
     const int lane = lane_id();
     const int gl = lane >> 3, gg = lane & 7;
+    PSTAT(22, 1);
+    const double2 org = pk.ln_org[b];
+    const float fe = pk.ln_fe[b];
+    float qxf[NQU], qyf[NQU];
+#pragma unroll
+    for (int q = 0; q < NQU; ++q) {
+        qxf[q] = float(qx[q] - org.x);
+        qyf[q] = float(qy[q] - org.y);
+    }
+    float R = 0.f;  // max distance of a corner from q0
+#pragma unroll
+    for (int q = 1; q < NQU; ++q) {
+        const float dx = qxf[q] - qxf[0], dy = qyf[q] - qyf[0];
+        R = fmaxf(R, sqrtf(dx * dx + dy * dy));
+    }
+    R = R * (1.f + 0x1p-16f) + 1e-6f;
+    // lanes (q, k) = (lane >> 2, lane & 3) run the lane_hit of query q on route lane l0 + k
+    const int hq = lane >> 2, hk = lane & 3;
+    const double hpx = hq < NQU ? qx[NQU == 1 ? 0 : hq] : 0.0, hpy = hq < NQU ? qy[NQU == 1 ? 0 : hq] : 0.0;
     bool have = false;
     double best_abs = 0.0, best_s = 0.0, best_d = 0.0;
     uint32_t best_id = 0;
     unsigned in_bits = 0;
+#pragma unroll 1
     for (int l0 = 0; l0 < nl; l0 += 4) {
         const int l = l0 + gl;
         const bool lane_ok = l < nl;
         const size_t lrow = size_t(b) * L + (lane_ok ? l : 0);
         const size_t base = lrow * C;
         const int nseg = lane_ok ? pk.ln_n[lrow] - 1 : 0;
-#pragma unroll 1
+        const float4* F = pk.ln_f4 + base;
+        // ---- 1. q0 over every segment ----
+        float m0 = INFINITY;
+#pragma unroll 4
+        for (int si = gg; si < nseg; si += 8) {
+            const float4 f = F[si];
+            m0 = fminf(m0, seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)));
+        }
+        m0 = octet_minf(m0);
+        float near_thr;
+        {
+            const float dm = sqrtf(m0);
+            const float d0 = 0x1p-18f * (fe + fabsf(qxf[0]) + fabsf(qyf[0]) + dm + 4.f * R) + 1e-30f;
+            const float r = dm + 2.f * R + 4.f * d0;
+            near_thr = NQU == 1 ? 0.f : r * r * (1.f + 0x1p-20f);
+        }
+        // ---- 2. near segments: per-query minimum ----
+        float m[NQU];
+        m[0] = m0;
+#pragma unroll
+        for (int q = 1; q < NQU; ++q) m[q] = INFINITY;
+        unsigned long long nearm = 0;  // bit k: segment gg + 8k is near (k < 64)
+        if (NQU > 1) {
+#pragma unroll 2
+            for (int si = gg, k = 0; si < nseg; si += 8, ++k) {
+                const float4 f = F[si];
+                const float inv = seg_inv_f(f);
+                if (seg_d2_f(qxf[0], qyf[0], f, inv) <= near_thr) {
+                    if (k < 64) nearm |= 1ull << k;
+#pragma unroll
+                    for (int q = 1; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f, inv));
+                }
+            }
+        }
+        float thr[NQU];
+#pragma unroll
         for (int q = 0; q < NQU; ++q) {
-            const double px = qx[q], py = qy[q];
-            double ub = 1e300;
-            int ib = INT_MAX;
-            for (int c0 = 0; c0 < C - 1; c0 += 8 * kSegGroup) {
-                const int g = c0 / kSegGroup + gg;
-                const bool gok = lane_ok && g * kSegGroup < nseg;
-                const double lb = gok ? box_lb(px, py, pk.ln_gb[lrow * GC + g]) : INFINITY;
-                // best-bound group of this route lane (ties: lowest group)
-                double bl = lb;
-                int bg = gok ? g : INT_MAX;
-                seg8_argmin(bl, bg);
-                // exact evaluation of its 8 segments, one per lane of the route lane's octet
-                double d2 = 1e300;
-                int i = INT_MAX;
-                if (bg != INT_MAX) {
-                    const int si = bg * kSegGroup + gg;
-                    if (si < nseg) {
+            const float mm = q == 0 ? m[0] : octet_minf(m[q]);
+            const float dm = sqrtf(mm);
+            const float delta = 0x1p-18f * (fe + fabsf(qxf[q]) + fabsf(qyf[q]) + dm) + 1e-30f;
+            const float r = dm + 2.f * delta;
+            thr[q] = r * r * (1.f + 0x1p-20f);
+        }
+        // ---- 3. exact fp64 distances of the candidates ----
+        double bd[NQU];
+        int bi[NQU];
+#pragma unroll
+        for (int q = 0; q < NQU; ++q) bd[q] = 1e300, bi[q] = INT_MAX;
+        auto exact = [&](int si, const float4 f) {
+            const float inv = seg_inv_f(f);
+            unsigned cm = 0;
+#pragma unroll
+            for (int q = 0; q < NQU; ++q) cm |= seg_d2_f(qxf[q], qyf[q], f, inv) <= thr[q] ? 1u << q : 0u;
+            if (cm) {
+                const double ax = pk.ln_x[base + si], ay = pk.ln_y[base + si];
+                const double abx = pk.ln_abx[base + si], aby = pk.ln_aby[base + si], l2 = pk.ln_len2[base + si];
+#pragma unroll
+                for (int q = 0; q < NQU; ++q) {
+                    if (cm & (1u << q)) {
                         double t;
-                        d2 = seg_d2_pre(px, py, pk.ln_x[base + si], pk.ln_y[base + si], pk.ln_abx[base + si],
-                                        pk.ln_aby[base + si], pk.ln_len2[base + si], t);
-                        i = si;
+                        const double d2 = seg_d2_pre(qx[q], qy[q], ax, ay, abx, aby, l2, t);
+                        PSTAT(21, 1);
+                        if (d2 < bd[q] || (d2 == bd[q] && si < bi[q])) bd[q] = d2, bi[q] = si;
                     }
-                }
-                seg8_argmin(d2, i);
-                if (d2 < ub || (d2 == ub && i < ib)) ub = d2, ib = i;
-                // any other group whose bound admits a segment <= the exact best
-                unsigned extra = __ballot_sync(FULL, gok && g != bg && lb <= ub);
-                while (extra) {
-                    const int src = __ffs(extra) - 1;
-                    extra &= extra - 1;
-                    const int eg = __shfl_sync(FULL, g, src);
-                    const int egl = src >> 3;
-                    double e2 = 1e300;
-                    int ei = INT_MAX;
-                    if (gl == egl) {
-                        const int si = eg * kSegGroup + gg;
-                        if (si < nseg) {
-                            double t;
-                            e2 = seg_d2_pre(px, py, pk.ln_x[base + si], pk.ln_y[base + si], pk.ln_abx[base + si],
-                                            pk.ln_aby[base + si], pk.ln_len2[base + si], t);
-                            ei = si;
-                        }
-                    }
-                    seg8_argmin(e2, ei);
-                    if (gl == egl && (e2 < ub || (e2 == ub && ei < ib))) ub = e2, ib = ei;
                 }
             }
-            // the first lane of each octet evaluates its route lane's winner:
-            // s, signed d, half-width (roads.cpp:130-139)
-            bool ok = false;
-            double hs = 0.0, hd = 0.0;
-            if (gg == 0 && lane_ok && ib != INT_MAX) {
-                const double* X = pk.ln_x + base;
-                const double* Y = pk.ln_y + base;
-                double t;
-                const double d2 = seg_d2_pre(px, py, X[ib], Y[ib], pk.ln_abx[base + ib], pk.ln_aby[base + ib],
-                                             pk.ln_len2[base + ib], t);
-                const LaneHit h = lane_hit(px, py, X, Y, pk.ln_s + base, pk.ln_hw + base, ib, d2, t);
-                hs = h.s;
-                hd = h.d;
-                ok = fabs(h.d) <= h.hw;
+        };
+        if (NQU == 1) {
+#pragma unroll 1
+            for (int si = gg; si < nseg; si += 8) {
+                const float4 f = F[si];
+                if (seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)) <= thr[0]) exact(si, f);
             }
-            if (__ballot_sync(FULL, ok)) in_bits |= 1u << q;
-            if (q == 0) {
-                for (int k = 0; k < 4 && l0 + k < nl; ++k) {
-                    const double s0 = __shfl_sync(FULL, hs, k * 8), d0 = __shfl_sync(FULL, hd, k * 8);
-                    const int w0 = __shfl_sync(FULL, ib, k * 8);
-                    if (w0 == INT_MAX) continue;
-                    const uint32_t id = pk.ln_id[size_t(b) * L + l0 + k];
-                    if (!have || fabs(d0) < best_abs || (fabs(d0) == best_abs && id < best_id)) {
-                        have = true;
-                        best_abs = fabs(d0);
-                        best_s = s0;
-                        best_d = d0;
-                        best_id = id;
-                    }
-                }
+        } else {
+            while (nearm) {
+                const int k = __ffsll(nearm) - 1;
+                nearm &= nearm - 1;
+                const int si = gg + 8 * k;
+                exact(si, F[si]);
+            }
+#pragma unroll 1
+            for (int si = gg + 8 * 64; si < nseg; si += 8) {  // beyond the 64-bit near mask
+                const float4 f = F[si];
+                if (seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)) <= near_thr) exact(si, f);
+            }
+        }
+        // ---- per-octet exact argmin, then s / signed d / half-width per (query, route lane) ----
+        int hi_ = INT_MAX;
+#pragma unroll
+        for (int q = 0; q < NQU; ++q) {
+            seg8_argmin(bd[q], bi[q]);
+            const int v = __shfl_sync(FULL, bi[q], hk * 8);
+            if (hq == q) hi_ = v;
+        }
+        bool ok = false;
+        double hs = 0.0, hd = 0.0;
+        if (hq < NQU && l0 + hk < nl && hi_ != INT_MAX) {
+            const size_t hb = (size_t(b) * L + l0 + hk) * C;
+            const double* X = pk.ln_x + hb;
+            const double* Y = pk.ln_y + hb;
+            double t;
+            const double d2 = seg_d2_pre(hpx, hpy, X[hi_], Y[hi_], pk.ln_abx[hb + hi_], pk.ln_aby[hb + hi_],
+                                         pk.ln_len2[hb + hi_], t);
+            const LaneHit h = lane_hit(hpx, hpy, X, Y, pk.ln_s + hb, pk.ln_hw + hb, hi_, d2, t);
+            hs = h.s;
+            hd = h.d;
+            ok = fabs(h.d) <= h.hw;
+        }
+        const unsigned okb = __ballot_sync(FULL, ok);
+#pragma unroll
+        for (int q = 0; q < NQU; ++q)
+            if ((okb >> (4 * q)) & 15u) in_bits |= 1u << q;
+        // query 0: across route lanes min |d| then lane_id (lanes 0..3 hold route lanes l0..l0+3)
+        for (int k = 0; k < 4 && l0 + k < nl; ++k) {
+            const double s0 = __shfl_sync(FULL, hs, k), d0 = __shfl_sync(FULL, hd, k);
+            const int w0 = __shfl_sync(FULL, hi_, k);
+            if (w0 == INT_MAX) continue;
+            const uint32_t id = pk.ln_id[size_t(b) * L + l0 + k];
+            if (!have || fabs(d0) < best_abs || (fabs(d0) == best_abs && id < best_id)) {
+                have = true;
+                best_abs = fabs(d0);
+                best_s = s0;
+                best_d = d0;
+                best_id = id;
             }
         }
     }
@@ -400,8 +496,6 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int b, size_
     for (int k = 0; k < 4; ++k) {
         w.agx[4 * j + k] = X[k];
         w.agy[4 * j + k] = Y[k];
-        w.agxf[4 * j + k] = float(X[k]);
-        w.agyf[4 * j + k] = float(Y[k]);
     }
     return boxes_overlap(eb, EX, EY, ab, X, Y) ? 1 : 0;
 }
@@ -544,6 +638,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
             T = rr * rr * (1.0 + 1e-9);
         }
     }
+    PSTAT(1 + 8 * which, T < INFINITY ? 1 : 0);
     if (!(T < INFINITY) && ps.nch <= cap) {
         // smallest far bound covering >= K points: chunk far bounds staged in
         // ckey (free until the candidates), extracted in increasing order
@@ -568,7 +663,9 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
             acc += min(kChunk, n - mc * kChunk);
             if (acc >= K) T = md;
         }
+        PSTAT(2 + 8 * which, T < INFINITY ? 1 : 0);
     }
+    PSTAT(3 + 8 * which, T < INFINITY ? 0 : 1);
     if (use_r && T < INFINITY && !(T <= r2)) T = INFINITY;  // the k points might not all qualify
     float tc = T < INFINITY ? fminf(__double2float_ru(T + key_margin(T, ep)), hi) : hi;
 
@@ -605,9 +702,12 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     };
     build_list(tc);
     int C = compact_chunks(tc);
+    PSTAT(7 + 8 * which, C);
+    PSTAT(8 + 8 * which, nlist);
 
     // ---- 3. tighten the bound when the candidates overflow ----
     if (C > cap) {
+        PSTAT(4 + 8 * which, 1);
         const int top = int(__float_as_uint(tc) >> 22);
         const int base = max(top - 31, 0);
         over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a) {
@@ -627,6 +727,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
                 C = compact_chunks(tc);
             }
             if (C > cap) {
+                PSTAT(5 + 8 * which, 1);
                 // linear sub-buckets inside bucket kstar
                 const float lo = kstar == 0 ? 0.f : __uint_as_float(unsigned(kstar + base) << 22);
                 const float hi2 = float(tsel);
@@ -653,6 +754,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     }
     if (C > cap) {
         // Pathological crowding at the threshold: exact iterative selection.
+        PSTAT(6 + 8 * which, 1);
         double pk_ = -1.0;
         int po = -1, nsel = 0;
         for (int k = 0; k < K; ++k) {
@@ -773,6 +875,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
 // ---------------------------------------------------------------------------
 __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const WarpBuf& w, bool boxes_ready,
                             const Box& eb_in, const double* EX_in, const double* EY_in) {
+    ROW_MARK(b, 2);
     const DevPack& pk = a.pk;
     const DevCfg& cfg = a.cfg;
     const int lane = lane_id();
@@ -798,6 +901,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     }
 
     const int t = r.t;
+    PSTAT(0, 1);
     Box eb;
     double EX[4], EY[4];
     if (boxes_ready) {
@@ -880,51 +984,17 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         }
         __syncwarp();
     }
-    // Distance bounds: d <= |c_e - c_a| (both centres lie inside their boxes)
-    // and d >= |c_e - c_a| - r_e - r_a (circumradii).  An agent whose lower
-    // bound exceeds U, with >= Ka agents at upper bound <= U, cannot rank.
-    const float re = float(sqrt(eb.hl * eb.hl + eb.hw * eb.hw));
-    float my_min_ub = INFINITY;
-    for (int j = lane; j < na; j += 32) {
-        if (w.agf[j] < 0) continue;
-        float cx = 0.5f * float(w.agx[4 * j] + w.agx[4 * j + 2]);
-        float cy = 0.5f * float(w.agy[4 * j] + w.agy[4 * j + 2]);
-        float dx = cx - float(eb.cx), dy = cy - float(eb.cy);
-        float ub = sqrtf(dx * dx + dy * dy) * 1.0001f + 1e-3f;
-        my_min_ub = fminf(my_min_ub, ub);
-    }
-    float U = INFINITY;
-    {
-        // Ka-th smallest per-lane minimum: >= Ka distinct agents lie at or under it
-        int rank = 0;
-#pragma unroll 4
-        for (int k = 0; k < 32; ++k) {
-            float o = __shfl_sync(FULL, my_min_ub, k);
-            rank += (o < my_min_ub || (o == my_min_ub && k < lane)) ? 1 : 0;
-        }
-        unsigned m = __ballot_sync(FULL, rank == Ka - 1 && my_min_ub < INFINITY);
-        if (Ka <= 32 && m) U = __shfl_sync(FULL, my_min_ub, __ffs(m) - 1);
-    }
-    int nsurv = 0;
-    for (int j0 = 0; j0 < na; j0 += 32) {
-        int j = j0 + lane;
-        bool keep = false;
-        if (j < na && w.agf[j] >= 0) {
-            float cx = 0.5f * float(w.agx[4 * j] + w.agx[4 * j + 2]);
-            float cy = 0.5f * float(w.agy[4 * j] + w.agy[4 * j + 2]);
-            float dx = cx - float(eb.cx), dy = cy - float(eb.cy);
-            double L2 = double(pk.ag_len[size_t(b) * A + j]), W2 = double(pk.ag_wid[size_t(b) * A + j]);
-            float ra = float(sqrt(L2 * L2 * 0.25 + W2 * W2 * 0.25));
-            float lb = sqrtf(dx * dx + dy * dy) * 0.9999f - re - ra - 1e-3f;
-            keep = lb <= U;
-        }
-        unsigned m = __ballot_sync(FULL, keep);
-        if (keep) w.surv[nsurv + __popc(m & lanemask_lt())] = j;
-        nsurv += __popc(m);
-    }
-    __syncwarp();
-    // Exact distance of each survivor: the 32 distinct point-to-edge d2 of
-    // obb_distance's 16 edge pairs (geometry.cpp:77-88), one per lane.
+    // obb_distance (geometry.cpp:77-88), ONE AGENT PER LANE.  Overlap => 0.
+    // Otherwise the minimum of the 32 point-to-edge d2 (ego corner vs agent
+    // edge, agent corner vs ego edge; segment_segment_distance's endpoint
+    // terms).  fp32 screening in ego-centred coordinates: rounding the corners
+    // moves each by <= 2^-24 S (S = largest centred coordinate) and the fp32
+    // arithmetic (approximate division, clamped t) adds <= 2^-20 (d + |edge|),
+    // so |d_f32 - d| <= delta = 2^-18 (S + E + d) (E bounds the edge lengths).
+    // A pair enters the candidate mask when d_f32 <= (running min) + 2 delta
+    // -- a superset of the final cut -- and only candidates get the fp64
+    // expressions.  A (near-)contact (min d2 < 1e-18) takes the reference's
+    // full segment_segment_distance over the 16 edge pairs.
     if (lane < 4) {
         w.egx[lane] = pick5(lane, EX[0], EX[1], EX[2], EX[3], EX[3]);
         w.egy[lane] = pick5(lane, EY[0], EY[1], EY[2], EY[3], EY[3]);
@@ -932,111 +1002,96 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     __syncwarp();
     const double* GX = w.egx;
     const double* GY = w.egy;
-    // (1) fp32 screening of the 32 pairs of every non-overlapping survivor
-    //     (one pass per survivor, lane = pair), (2) exact fp64 evaluation of
-    //     only the pairs within the screening error of each survivor's
-    //     minimum, compacted across survivors, (3) per-survivor min via a
-    //     64-bit atomicMin on the (non-negative) double bit patterns.
-    unsigned long long* dbits = reinterpret_cast<unsigned long long*>(w.agd);
-    const float egxf = lane < 4 ? float(pick5(lane, EX[0], EX[1], EX[2], EX[3], EX[3])) : 0.f;
-    const float egyf = lane < 4 ? float(pick5(lane, EY[0], EY[1], EY[2], EY[3], EY[3])) : 0.f;
-    const int e = lane & 15, pi = e >> 2, sj = e & 3, sj1 = (sj + 1) & 3;
-    const float exf_pi = __shfl_sync(FULL, egxf, pi), eyf_pi = __shfl_sync(FULL, egyf, pi);
-    const float exf_s0 = __shfl_sync(FULL, egxf, sj), eyf_s0 = __shfl_sync(FULL, egyf, sj);
-    const float exf_s1 = __shfl_sync(FULL, egxf, sj1), eyf_s1 = __shfl_sync(FULL, egyf, sj1);
-    const float mag = float(fabs(r.x) + fabs(r.y)) + 100.f;
-    int ncand = 0;
-    for (int s = 0; s < nsurv; ++s) {
-        const int j = w.surv[s];
-        if (w.agf[j] == 1) {
-            if (lane == 0) w.agd[j] = 0.0;  // obb_overlap => distance 0
-            continue;
-        }
-        if (lane == 0) dbits[j] = 0x7FF0000000000000ull;  // +inf
-        const float* AX = w.agxf + 4 * j;
-        const float* AY = w.agyf + 4 * j;
-        float px, py, ax, ay, bx, by;
-        if (lane < 16) {  // ego corner pi vs agent edge sj
-            px = exf_pi, py = eyf_pi, ax = AX[sj], ay = AY[sj], bx = AX[sj1], by = AY[sj1];
-        } else {  // agent corner pi vs ego edge sj
-            px = AX[pi], py = AY[pi], ax = exf_s0, ay = eyf_s0, bx = exf_s1, by = eyf_s1;
-        }
-        const float abx = bx - ax, aby = by - ay;
-        const float len2 = abx * abx + aby * aby;
-        float t = len2 > 0.f ? __fdividef((px - ax) * abx + (py - ay) * aby, len2) : 0.f;
-        t = fminf(fmaxf(t, 0.f), 1.f);
-        const float qx = px - (ax + abx * t), qy = py - (ay + aby * t);
-        const float d = sqrtf(qx * qx + qy * qy);
-        const float dmin = __uint_as_float(__reduce_min_sync(FULL, __float_as_uint(d)));
-        // fp32 rounding of the corners (<= 2^-24 |c|), of the arithmetic and of t
-        const bool cand = d <= dmin + 2e-6f * (mag + dmin) + 1e-4f;
-        const unsigned bal = __ballot_sync(FULL, cand);
-        if (cand) {
-            const int q = ncand + __popc(bal & lanemask_lt());
-            if (q < a.cand_cap) w.acand[q] = (s << 5) | lane;
-        }
-        ncand += __popc(bal);
+    float gxf[4], gyf[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        gxf[k] = float(EX[k] - eb.cx);
+        gyf[k] = float(EY[k] - eb.cy);
     }
-    __syncwarp();
-    if (ncand <= a.cand_cap) {
-        for (int k = lane; k < ncand; k += 32) {
-            const int s = w.acand[k] >> 5, ln = w.acand[k] & 31;
-            const int j = w.surv[s];
+    const float ge = float(2.0 * (eb.hl + eb.hw)) + 1e-3f;  // >= any ego edge length
+    int nvalid = 0;
+    for (int j0 = 0; j0 < na; j0 += 32) {
+        const int j = j0 + lane;
+        const int fl = j < na ? w.agf[j] : -1;
+        if (fl == 0) {
             const double* AX = w.agx + 4 * j;
             const double* AY = w.agy + 4 * j;
-            const int ee = ln & 15, ci = ee >> 2, ei = ee & 3, ei1 = (ei + 1) & 3;
-            const double d2 = ln < 16 ? seg_dist2(GX[ci], GY[ci], AX[ei], AY[ei], AX[ei1], AY[ei1])
-                                      : seg_dist2(AX[ci], AY[ci], GX[ei], GY[ei], GX[ei1], GY[ei1]);
-            atomicMin(&dbits[j], static_cast<unsigned long long>(__double_as_longlong(d2)));
+            float axf[4], ayf[4];
+            float S = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                axf[k] = float(AX[k] - eb.cx);
+                ayf[k] = float(AY[k] - eb.cy);
+                S = fmaxf(S, fmaxf(fabsf(axf[k]), fabsf(ayf[k])));
+            }
+            float E = ge;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) E = fmaxf(E, fabsf(axf[(k + 1) & 3] - axf[k]) + fabsf(ayf[(k + 1) & 3] - ayf[k]));
+            const float c0 = 0x1p-18f * (S + ge + E);  // ge also bounds the centred ego corners
+            float min2 = INFINITY, thr2 = INFINITY;
+            unsigned cmask = 0;
+            auto consider = [&](int p, float d2) {
+                if (d2 < min2) {
+                    min2 = d2;
+                    const float m = sqrtf(d2);
+                    const float r = m + 2.f * (c0 + 0x1p-18f * m) + 1e-30f;
+                    thr2 = r * r * (1.f + 0x1p-20f);
+                }
+                if (d2 <= thr2) cmask |= 1u << p;
+            };
+            // ego corner ci vs agent edge ei: pairs 4 ci + ei
+#pragma unroll
+            for (int ei = 0; ei < 4; ++ei) {
+                const float4 f = make_float4(axf[ei], ayf[ei], axf[(ei + 1) & 3] - axf[ei], ayf[(ei + 1) & 3] - ayf[ei]);
+                const float inv = seg_inv_f(f);
+#pragma unroll
+                for (int ci = 0; ci < 4; ++ci) consider(4 * ci + ei, seg_d2_f(gxf[ci], gyf[ci], f, inv));
+            }
+            // agent corner ci vs ego edge ei: pairs 16 + 4 ci + ei
+#pragma unroll
+            for (int ei = 0; ei < 4; ++ei) {
+                const float4 f = make_float4(gxf[ei], gyf[ei], gxf[(ei + 1) & 3] - gxf[ei], gyf[(ei + 1) & 3] - gyf[ei]);
+                const float inv = seg_inv_f(f);
+#pragma unroll
+                for (int ci = 0; ci < 4; ++ci) consider(16 + 4 * ci + ei, seg_d2_f(axf[ci], ayf[ci], f, inv));
+            }
+            // exact candidates
+            double d2min = INFINITY;
+            while (cmask) {
+                const int pr = __ffs(cmask) - 1;
+                cmask &= cmask - 1;
+                const int ci = (pr >> 2) & 3, ei = pr & 3, ei1 = (ei + 1) & 3;
+                const double d2 = pr < 16 ? seg_dist2(GX[ci], GY[ci], AX[ei], AY[ei], AX[ei1], AY[ei1])
+                                          : seg_dist2(AX[ci], AY[ci], GX[ei], GY[ei], GX[ei1], GY[ei1]);
+                d2min = fmin(d2min, d2);
+            }
+            if (!(d2min >= 1e-18)) {
+                PSTAT(20, 1);
+                d2min = INFINITY;
+                for (int pr = 0; pr < 16; ++pr) d2min = fmin(d2min, box_edge_pair_dist2(GX, GY, AX, AY, pr >> 2, pr & 3));
+            }
+            w.agd[j] = sqrt(d2min);  // obb_distance returns sqrt of the min d2
+        } else if (fl == 1) {
+            w.agd[j] = 0.0;
         }
-    } else {
-        // too many near-ties to list: every pair of every survivor exactly
-        for (int s = 0; s < nsurv; ++s) {
-            const int j = w.surv[s];
-            if (w.agf[j] == 1) continue;
-            const double* AX = w.agx + 4 * j;
-            const double* AY = w.agy + 4 * j;
-            const double d2 = lane < 16 ? seg_dist2(GX[pi], GY[pi], AX[sj], AY[sj], AX[sj1], AY[sj1])
-                                        : seg_dist2(AX[pi], AY[pi], GX[sj], GY[sj], GX[sj1], GY[sj1]);
-            atomicMin(&dbits[j], static_cast<unsigned long long>(__double_as_longlong(d2)));
-        }
+        nvalid += __popc(__ballot_sync(FULL, fl >= 0));
     }
     __syncwarp();
-    // (near-)contact: a strict edge crossing is possible, so take the
-    // reference's full segment_segment_distance over the 16 pairs.
-    for (int s = 0; s < nsurv; ++s) {
-        const int j = w.surv[s];
-        if (w.agf[j] == 1 || !(w.agd[j] < 1e-18)) continue;
-        double v = INFINITY;
-        if (lane < 16) v = box_edge_pair_dist2(GX, GY, w.agx + 4 * j, w.agy + 4 * j, lane >> 2, lane & 3);
-        double md2;
-        int dummy;
-        warp_argmin(v, 0, md2, dummy);
-        if (lane == 0) w.agd[j] = md2;
-        __syncwarp();
-    }
-    __syncwarp();
-    for (int s = lane; s < nsurv; s += 32) {
-        const int j = w.surv[s];
-        w.agd[j] = sqrt(w.agd[j]);  // obb_distance returns sqrt of the min d2 (0 on overlap)
-    }
-    __syncwarp();
-    for (int s0 = 0; s0 < nsurv; s0 += 32) {
-        int s = s0 + lane;
-        if (s < nsurv) {
-            int j = w.surv[s];
-            double dj = w.agd[j];
+    // rank by (distance, index) among the valid agents
+    for (int j0 = 0; j0 < na; j0 += 32) {
+        const int j = j0 + lane;
+        if (j < na && w.agf[j] >= 0) {
+            const double dj = w.agd[j];
             int rank = 0;
-#pragma unroll 1
-            for (int q = 0; q < nsurv; ++q) {
-                int k = w.surv[q];
-                double dk = w.agd[k];
-                rank += (dk < dj || (dk == dj && k < j)) ? 1 : 0;
+#pragma unroll 4
+            for (int k = 0; k < na; ++k) {
+                const double dk = w.agd[k];
+                rank += (w.agf[k] >= 0 && (dk < dj || (dk == dj && k < j))) ? 1 : 0;
             }
             if (rank < Ka) w.sel[rank] = j;
         }
     }
-    const int nsel_ag = min(Ka, nsurv);
+    const int nsel_ag = min(Ka, nvalid);
     __syncwarp();
     for (int k = lane; k < Ka; k += 32) {
         float f[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -1060,6 +1115,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
 
     // ---- road network points: nearest_features (roads.cpp:210-236) ----
     // the top-k region overlays the (now dead) agent buffers: clear the histogram
+    ROW_MARK(b, 3);
     __syncwarp();
     for (int k = lane; k < 32 * 32; k += 32) w.hist[k] = 0;
     __syncwarp();
@@ -1072,6 +1128,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         const PointSet ps{pts, oidx, pk.road_cb + size_t(b) * pk.d.PC, n, (n + kChunk - 1) / kChunk};
         const int nsel = warp_topk(ps, Kr, r.x, r.y, true, R * R, pk.road_box[b], a.cand_cap, w.hist, w.cidx, w.ckey,
                                    w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 0);
+        ROW_MARK(b, 4);
         const uint8_t* kd = pk.road_kd + size_t(b) * pk.d.P;
         for (int k = lane; k < Kr; k += 32) {
             float f[12];
@@ -1100,6 +1157,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     }
 
     // ---- route border points: top n_route by (d2, idx), no radius (simcore.cpp:503-529) ----
+    ROW_MARK(b, 5);
     {
         const int n = pk.n_route[b];
         const float2* pts = pk.route_xy + size_t(b) * pk.d.R;
@@ -1108,6 +1166,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         const PointSet ps{pts, oidx, pk.route_cb + size_t(b) * pk.d.RC, n, (n + kChunk - 1) / kChunk};
         const int nsel = warp_topk(ps, Kl, r.x, r.y, false, 0.0, pk.route_box[b], a.cand_cap, w.hist, w.cidx, w.ckey,
                                    w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 1);
+        ROW_MARK(b, 6);
         const uint8_t* fl = pk.route_fl + size_t(b) * pk.d.R;
         for (int k = lane; k < Kl; k += 32) {
             float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
@@ -1172,6 +1231,7 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
         return r0;
     }
 
+    PSTAT(23, 1);
     const double accel = cfg.accel_bins[ai], rate = cfg.steer_bins[si];
     const double dt = pk.dt;
     // dyn::bicycle_step (dynamics.cpp:10-19)
@@ -1204,7 +1264,8 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
         for (int k = 0; k < 4; ++k) w.qx[k + 1] = X[k], w.qy[k + 1] = Y[k];
     }
     __syncwarp();
-    const Proj p1 = warp_project<NQ>(pk, b, w.qx, w.qy, nullptr);
+    const Proj p1 = warp_project<NQ>(pk, b, w.qx, w.qy);
+    ROW_MARK(b, 1);
 
     // collision with the agents valid at t+1 (simcore.cpp:323-331); boxes kept for observe(t+1)
     int hit = 0;
@@ -1315,6 +1376,7 @@ __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int b, int t) 
         case 15: ptr = pk.ag_valid + as; bytes = size_t(A); break;
         case 16: ptr = pk.ag_len + size_t(b) * A; bytes = size_t(A) * 4; break;
         case 17: ptr = pk.ag_wid + size_t(b) * A; bytes = size_t(A) * 4; break;
+        case 18: ptr = STEP ? pk.ln_f4 + lb : nullptr; bytes = LC * 16; break;
         default: break;
     }
     if (ptr) prefetch_l2(ptr, unsigned(bytes < (1u << 24) ? bytes : (1u << 24)));
@@ -1332,11 +1394,13 @@ __global__ void __launch_bounds__(kThreads, 7) k_step_observe(const KernelArgs a
         Row r = load_row(a.in, b);
         // the warp's next row: its static data streams into L2 while this row computes
         if (b + stride < a.pk.d.B) prefetch_row<STEP, OBS>(a, b + stride, r.t + (STEP ? 1 : 0));
+        ROW_MARK(b, 0);
         bool boxes_ready = false;
         Box eb{};
         double EX[4] = {0, 0, 0, 0}, EY[4] = {0, 0, 0, 0};
         if (STEP) r = step_row(a, b, r, w, boxes_ready, eb, EX, EY);
         if (OBS) observe_row(a, b, r, w, boxes_ready && !r.done, eb, EX, EY);
+        ROW_MARK(b, 7);
     }
 }
 
@@ -1346,10 +1410,9 @@ __global__ void __launch_bounds__(kThreads) k_reset(const KernelArgs a) {
     const DevCfg& cfg = a.cfg;
     const int lane = lane_id();
     const int wpb = kThreads / 32;
-    __shared__ int lists[kThreads / 32][64];
     for (int b = blockIdx.x * wpb + warp_in_block(); b < pk.d.B; b += gridDim.x * wpb) {
         double qx[1] = {pk.init_x[b]}, qy[1] = {pk.init_y[b]};
-        const Proj p = warp_project<1>(pk, b, qx, qy, lists[warp_in_block()]);
+        const Proj p = warp_project<1>(pk, b, qx, qy);
         if (lane == 0) {
             a.out.x[b] = pk.init_x[b];
             a.out.y[b] = pk.init_y[b];
@@ -1405,9 +1468,24 @@ __global__ void __launch_bounds__(256) k_episode_stats(const KernelArgs a, const
 
 }  // namespace
 
+#ifdef ZS_PATHSTATS
+extern "C" __attribute__((visibility("default"))) int zsimdbg_pathstats(unsigned long long* out, int reset, unsigned* rowcyc, int nrows) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+    if (cudaMemcpyFromSymbol(out, g_pstats, sizeof(g_pstats)) != cudaSuccess) return 1;
+    if (rowcyc && nrows > 0 &&
+        cudaMemcpyFromSymbol(rowcyc, g_rowcyc, sizeof(unsigned) * 8 * size_t(nrows < kMaxStatRows ? nrows : kMaxStatRows)) !=
+            cudaSuccess)
+        return 1;
+    if (reset) {
+        static const unsigned long long z[32] = {};
+        if (cudaMemcpyToSymbol(g_pstats, z, sizeof(z)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+#endif
+
 size_t smem_bytes(const KernelArgs& a) {
-    return warp_smem_bytes(a.pk.d.A, a.cand_cap, a.cfg.n_agents, a.pk.d.NS) *
-           size_t(kThreads / 32);
+    return size_t(warp_layout(a.pk.d.A, a.cand_cap, a.cfg.n_agents, a.pk.d.NS).total) * size_t(kThreads / 32);
 }
 
 static int grid_for(const KernelArgs& a) {
@@ -1433,6 +1511,7 @@ cudaError_t launch_step_observe(const KernelArgs& a, int mode, int grid, cudaStr
     (void)grid;
     KernelArgs am = a;
     if (mode == kModeStep) am.cand_cap = 0;  // the step-only kernel carves no top-k buffers
+    am.lay = warp_layout(am.pk.d.A, am.cand_cap, am.cfg.n_agents, am.pk.d.NS);
     const size_t smem = smem_bytes(am);
     auto launch = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

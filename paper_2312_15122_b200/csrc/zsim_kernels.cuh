@@ -15,6 +15,14 @@ constexpr int kStatsLen = 8;  // episode-stats vector length
 
 enum { kModeStep = 0, kModeObserve = 1, kModeStepObserve = 2 };
 
+// Per-warp shared-memory carve-up, byte offsets (computed on the host so the
+// kernels read them from the parameter bank instead of recomputing them).
+struct SmemLayout {
+    uint32_t agx, agy, agd, agf, sel;          // agent phase
+    uint32_t hist, cidx, ckey, cinfo, order;                    // top-k phase (overlays the agent phase)
+    uint32_t sflag, total;
+};
+
 struct KernelArgs {
     DevPack pk;
     DevCfg cfg;
@@ -30,6 +38,7 @@ struct KernelArgs {
     float4* hint;      // [B] per-row top-k threshold hints (speed only; see warp_topk), may be null
     int32_t key_cap;   // >= max(P, R)
     int32_t cand_cap;  // top-k candidate capacity per warp (= 32 x kMaxCandPerLane)
+    SmemLayout lay;    // filled by the launchers
 };
 
 size_t smem_bytes(const KernelArgs& a);

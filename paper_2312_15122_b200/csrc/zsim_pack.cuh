@@ -12,6 +12,7 @@
 //                      build_route_points order (simcore.cpp:181-200), chunked likewise
 //   lanes   [B][L][C]  centerline x, y, s, half_width f64 after RouteFrame::build
 //                      clipping (roads.cpp:43-103) + per-segment b-a and |b-a|^2;
+//                      an fp32 copy (a - origin, b - a) for screening;
 //                      n vertices + lane_id per lane
 //   lights  [B][NL]    route s f64 + state u8[T] for lights kept by
 //                      RouteContext::build (roads.cpp:245-249)
@@ -29,10 +30,7 @@ namespace zs {
 struct PackDims {
     int32_t B, T, A, P, R, L, C, NL, NS;
     int32_t PC, RC;  // 32-point chunks of the road / route point sets
-    int32_t GC;      // 8-segment groups per lane centerline
 };
-
-constexpr int kSegGroup = 8;  // segments per centerline group (bounding box)
 
 constexpr int kChunk = 32;  // points per spatial chunk (one warp-wide load)
 
@@ -87,8 +85,9 @@ struct DevPack {
     const double* ln_abx;   // [B][L][C] segment vectors b - a (geometry.cpp:18), last slot unused
     const double* ln_aby;
     const double* ln_len2;  // |b - a|^2 with the reference's op order
-    const double* ln_inv2;  // 1 / len2 (0 for a degenerate segment): division-free candidate screening
-    const float4* ln_gb;    // [B][L][GC] bounding boxes of 8-segment groups (rounded outward)
+    const float4* ln_f4;    // [B][L][C] fp32 screening copy: (a - origin, b - a) per segment
+    const double2* ln_org;  // [B] origin of the fp32 copy
+    const float* ln_fe;     // [B] max |a - origin|_1 over vertices + max segment length (error scale)
     const int32_t* ln_n;
     const uint32_t* ln_id;
     const float4* road_box;   // [B] (min x, min y, max x, max y) of the road points
