@@ -422,6 +422,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
             if (s.ego_x.empty()) raise(Err::invalid_argument, "scenario `" + s.id + "`: empty ego log");
         }
     }
+    d.GC = std::max(1, (d.C - 1 + kSegGroup - 1) / kSegGroup);
     d.PC = (d.P + kChunk - 1) / kChunk;
     d.RC = (d.R + kChunk - 1) / kChunk;
     if (d.L > kMaxLanes) {
@@ -446,15 +447,16 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     size_t o_txy = pb.reserve<float>(size_t(B) * d.R * 2), o_tfl = pb.reserve<uint8_t>(size_t(B) * d.R);
     size_t o_toi = pb.reserve<int32_t>(size_t(B) * d.R), o_tcb = pb.reserve<float>(size_t(B) * d.RC * 4);
     const size_t nln = size_t(B) * d.L * d.C;
-    size_t o_lx = pb.reserve<double>(nln), o_ly = pb.reserve<double>(nln), o_ls = pb.reserve<double>(nln),
-           o_lhw = pb.reserve<double>(nln);
-    size_t o_labx = pb.reserve<double>(nln), o_laby = pb.reserve<double>(nln), o_llen2 = pb.reserve<double>(nln);
+    size_t o_lv = pb.reserve<LaneVtx>(nln);
+    size_t o_lgb = pb.reserve<float>(size_t(B) * d.L * d.GC * 4);
     size_t o_lf4 = pb.reserve<float>(nln * 4), o_lorg = pb.reserve<double>(size_t(B) * 2),
            o_lfe = pb.reserve<float>(size_t(B));
     size_t o_ln = pb.reserve<int32_t>(size_t(B) * d.L), o_lid = pb.reserve<uint32_t>(size_t(B) * d.L);
     size_t o_rbox = pb.reserve<float>(size_t(B) * 4), o_tbox = pb.reserve<float>(size_t(B) * 4);
     size_t o_lts = pb.reserve<double>(size_t(B) * d.NL), o_ltst = pb.reserve<uint8_t>(size_t(B) * d.NL * d.T);
     size_t o_sts = pb.reserve<double>(size_t(B) * d.NS);
+    constexpr int kPf = 12;
+    size_t o_pf = pb.reserve<PfDesc>(kPf);
     pb.host.assign(pb.cursor, 0);
 
     env->goal_s.assign(size_t(B), 0.0);
@@ -553,22 +555,36 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
         double fe_s = 0.0, fe_l = 0.0;
         for (size_t l = 0; l < c.lanes.size(); ++l) {
             const LaneFrame& lf = c.lanes[l];
+            // group boxes: segments [8g, 8g+8) touch vertices [8g, 8g+8]; origin-relative, rounded outward
+            const int nseg = int(lf.x.size()) - 1;
+            for (int g = 0; g * kSegGroup < nseg; ++g) {
+                double x0 = 1e300, y0 = 1e300, x1 = -1e300, y1 = -1e300;
+                for (int v = g * kSegGroup; v <= std::min(nseg, (g + 1) * kSegGroup); ++v) {
+                    x0 = std::min(x0, lf.x[size_t(v)] - ox), x1 = std::max(x1, lf.x[size_t(v)] - ox);
+                    y0 = std::min(y0, lf.y[size_t(v)] - oy), y1 = std::max(y1, lf.y[size_t(v)] - oy);
+                }
+                float* gb = pb.at<float>(o_lgb) + ((size_t(b) * d.L + l) * d.GC + size_t(g)) * 4;
+                gb[0] = std::nextafter(float(x0), -3e38f);
+                gb[1] = std::nextafter(float(y0), -3e38f);
+                gb[2] = std::nextafter(float(x1), 3e38f);
+                gb[3] = std::nextafter(float(y1), 3e38f);
+            }
             pb.at<int32_t>(o_ln)[size_t(b) * d.L + l] = int32_t(lf.x.size());
             pb.at<uint32_t>(o_lid)[size_t(b) * d.L + l] = lf.lane_id;
             for (size_t i = 0; i < lf.x.size(); ++i) {
                 size_t k = (size_t(b) * d.L + l) * d.C + i;
-                pb.at<double>(o_lx)[k] = lf.x[i];
-                pb.at<double>(o_ly)[k] = lf.y[i];
-                pb.at<double>(o_ls)[k] = lf.s[i];
-                pb.at<double>(o_lhw)[k] = lf.hw[i];
+                LaneVtx& v = pb.at<LaneVtx>(o_lv)[k];
+                v.x = lf.x[i];
+                v.y = lf.y[i];
+                v.s = lf.s[i];
+                v.hw = lf.hw[i];
                 fe_s = std::max(fe_s, std::fabs(lf.x[i] - ox) + std::fabs(lf.y[i] - oy));
                 if (i + 1 < lf.x.size()) {
                     // point_segment_dist2's ab = b - a and len2 = ab.norm2() (geometry.cpp:18-19)
                     double abx = lf.x[i + 1] - lf.x[i], aby = lf.y[i + 1] - lf.y[i];
-                    pb.at<double>(o_labx)[k] = abx;
-                    pb.at<double>(o_laby)[k] = aby;
-                    double len2 = abx * abx + aby * aby;
-                    pb.at<double>(o_llen2)[k] = len2;
+                    v.abx = abx;
+                    v.aby = aby;
+                    v.len2 = abx * abx + aby * aby;
                     fe_l = std::max(fe_l, std::fabs(abx) + std::fabs(aby));
                     float* f4 = pb.at<float>(o_lf4) + 4 * k;
                     f4[0] = float(lf.x[i] - ox);
@@ -632,14 +648,9 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.route_fl = D + o_tfl;
     pk.route_oi = reinterpret_cast<const int32_t*>(D + o_toi);
     pk.route_cb = reinterpret_cast<const float4*>(D + o_tcb);
-    pk.ln_x = reinterpret_cast<const double*>(D + o_lx);
-    pk.ln_y = reinterpret_cast<const double*>(D + o_ly);
-    pk.ln_s = reinterpret_cast<const double*>(D + o_ls);
-    pk.ln_hw = reinterpret_cast<const double*>(D + o_lhw);
-    pk.ln_abx = reinterpret_cast<const double*>(D + o_labx);
-    pk.ln_aby = reinterpret_cast<const double*>(D + o_laby);
-    pk.ln_len2 = reinterpret_cast<const double*>(D + o_llen2);
+    pk.ln_v = reinterpret_cast<const LaneVtx*>(D + o_lv);
     pk.ln_f4 = reinterpret_cast<const float4*>(D + o_lf4);
+    pk.ln_gb = reinterpret_cast<const float4*>(D + o_lgb);
     pk.ln_org = reinterpret_cast<const double2*>(D + o_lorg);
     pk.ln_fe = reinterpret_cast<const float*>(D + o_lfe);
     pk.road_box = reinterpret_cast<const float4*>(D + o_rbox);
@@ -649,6 +660,27 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.lt_s = reinterpret_cast<const double*>(D + o_lts);
     pk.lt_state = D + o_ltst;
     pk.st_s = reinterpret_cast<const double*>(D + o_sts);
+    {
+        // L2 prefetch table (zsim_kernels.cu prefetch_row): the per-row arrays a step touches
+        const uint32_t LC = uint32_t(d.L) * uint32_t(d.C), TA = uint32_t(d.T) * uint32_t(d.A), A = uint32_t(d.A);
+        const PfDesc tab[kPf] = {
+            {pk.ln_f4, LC * 16, 0, LC * 16, 1},
+            {pk.ln_gb, uint32_t(d.L) * uint32_t(d.GC) * 16, 0, uint32_t(d.L) * uint32_t(d.GC) * 16, 1},
+            {pk.road_cb, uint32_t(d.PC) * 16, 0, uint32_t(d.PC) * 16, 2},
+            {pk.route_cb, uint32_t(d.RC) * 16, 0, uint32_t(d.RC) * 16, 2},
+            {pk.ag_x, TA * 4, A * 4, A * 4, 0},
+            {pk.ag_y, TA * 4, A * 4, A * 4, 0},
+            {pk.ag_h, TA * 4, A * 4, A * 4, 0},
+            {pk.ag_sp, TA * 4, A * 4, A * 4, 2},
+            {pk.ag_valid, TA, A, A, 0},
+            {pk.ag_len, A * 4, 0, A * 4, 0},
+            {pk.ag_wid, A * 4, 0, A * 4, 0},
+            {pk.lt_state, uint32_t(d.NL) * uint32_t(d.T), 0, uint32_t(d.NL) * uint32_t(d.T), 0},
+        };
+        cuda_check(cudaMemcpy(D + o_pf, tab, sizeof(tab), cudaMemcpyHostToDevice), "upload prefetch table");
+        pk.pf = reinterpret_cast<const PfDesc*>(D + o_pf);
+        pk.n_pf = kPf;
+    }
 
     env->B = B;
     env->horizon = horizon;

@@ -53,7 +53,7 @@ __device__ unsigned long long g_pstats[32];
     } while (0)
 // per-row SM clock stamps (low 32 bits) at marks 0..7; the host differences them
 constexpr int kMaxStatRows = 65536;
-__device__ unsigned g_rowcyc[kMaxStatRows][8];
+__device__ unsigned g_rowcyc[kMaxStatRows][16];
 __device__ __forceinline__ void row_mark(int b, int k) {
     __syncwarp();
     if ((threadIdx.x & 31) == 0 && b < kMaxStatRows) g_rowcyc[b][k] = unsigned(clock64());
@@ -241,6 +241,14 @@ __device__ __forceinline__ double seg_d2_pre(double px, double py, double ax, do
     return ex * ex + ey * ey;
 }
 
+// point_segment_dist2 (geometry.cpp:17-25) through seg_d2_pre: identical d2,
+// division only for an interior projection.
+__device__ __forceinline__ double seg_dist2_fast(double px, double py, double ax, double ay, double bx, double by) {
+    const double abx = bx - ax, aby = by - ay;
+    double t;
+    return seg_d2_pre(px, py, ax, ay, abx, aby, abx * abx + aby * aby, t);
+}
+
 struct Proj {
     double s, d;
     int in_corr;   // query 0 lies in some lane corridor (roads.cpp:154)
@@ -342,10 +350,51 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
         const size_t base = lrow * C;
         const int nseg = lane_ok ? pk.ln_n[lrow] - 1 : 0;
         const float4* F = pk.ln_f4 + base;
-        // ---- 1. q0 over every segment ----
+        // ---- 0. 8-segment groups that can hold q0's minimum or a near segment ----
+        // Group boxes (origin-relative, rounded outward) bound the exact
+        // distance of every segment inside from below (LB) and above (far
+        // corner, FD); d_f32 is within delta of exact, so m0 <= U = min FD + delta
+        // and only groups with LB <= U + 2R + 5 delta can matter.
+        const int ngr = (nseg + kSegGroup - 1) / kSegGroup;
+        unsigned long long need = 0;  // bit g: group g is scanned (octet-uniform)
+        {
+            float lbv[2], fdmin = INFINITY;
+            const int GC = pk.d.GC;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {  // groups gg and gg + 8 (lanes up to 129 vertices)
+                const int g = gg + 8 * c;
+                lbv[c] = INFINITY;
+                if (g < ngr) {
+                    const float4 bb = pk.ln_gb[lrow * GC + g];
+                    const float x0 = bb.x - qxf[0], x1 = qxf[0] - bb.z, y0 = bb.y - qyf[0], y1 = qyf[0] - bb.w;
+                    const float nx = fmaxf(fmaxf(x0, x1), 0.f), ny = fmaxf(fmaxf(y0, y1), 0.f);
+                    const float fx = fmaxf(fabsf(x0), fabsf(x1)), fy = fmaxf(fabsf(y0), fabsf(y1));
+                    lbv[c] = sqrtf(nx * nx + ny * ny);
+                    fdmin = fminf(fdmin, sqrtf(fx * fx + fy * fy));
+                }
+            }
+            fdmin = octet_minf(fdmin);
+            const float dl = 0x1p-18f * (fe + fabsf(qxf[0]) + fabsf(qyf[0]) + fdmin + 4.f * R) + 1e-6f;
+            const float lim = (fdmin + 2.f * R + 8.f * dl) * (1.f + 0x1p-20f);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const unsigned bal = __ballot_sync(FULL, lbv[c] <= lim);
+                need |= (unsigned long long)((bal >> (8 * gl)) & 0xFFu) << (8 * c);
+            }
+            if (ngr > 16) need |= ~0ull << 16;  // longer lanes: groups past 16 always scanned
+        }
+        if (l0 == 0) ROW_MARK(b, 10);
+        // ---- 1. q0 over the needed groups ----
         float m0 = INFINITY;
-#pragma unroll 4
-        for (int si = gg; si < nseg; si += 8) {
+        for (unsigned long long mm = need & ((ngr >= 64) ? ~0ull : ((1ull << ngr) - 1)); mm; mm &= mm - 1) {
+            const int si = (__ffsll(mm) - 1) * kSegGroup + gg;
+            if (si < nseg) {
+                const float4 f = F[si];
+                m0 = fminf(m0, seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)));
+            }
+        }
+#pragma unroll 1
+        for (int si = 64 * kSegGroup + gg; si < nseg; si += 8) {  // beyond the 64-bit group mask
             const float4 f = F[si];
             m0 = fminf(m0, seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)));
         }
@@ -355,24 +404,35 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
             const float dm = sqrtf(m0);
             const float d0 = 0x1p-18f * (fe + fabsf(qxf[0]) + fabsf(qyf[0]) + dm + 4.f * R) + 1e-30f;
             const float r = dm + 2.f * R + 4.f * d0;
-            near_thr = NQU == 1 ? 0.f : r * r * (1.f + 0x1p-20f);
+            near_thr = r * r * (1.f + 0x1p-20f);
         }
+        if (l0 == 0) ROW_MARK(b, 11);
         // ---- 2. near segments: per-query minimum ----
         float m[NQU];
         m[0] = m0;
 #pragma unroll
         for (int q = 1; q < NQU; ++q) m[q] = INFINITY;
-        unsigned long long nearm = 0;  // bit k: segment gg + 8k is near (k < 64)
-        if (NQU > 1) {
-#pragma unroll 2
-            for (int si = gg, k = 0; si < nseg; si += 8, ++k) {
+        unsigned long long nearm = 0;  // bit g: this lane's segment of group g is near
+        for (unsigned long long mm = need & ((ngr >= 64) ? ~0ull : ((1ull << ngr) - 1)); mm; mm &= mm - 1) {
+            const int g = __ffsll(mm) - 1;
+            const int si = g * kSegGroup + gg;
+            if (si < nseg) {
                 const float4 f = F[si];
                 const float inv = seg_inv_f(f);
                 if (seg_d2_f(qxf[0], qyf[0], f, inv) <= near_thr) {
-                    if (k < 64) nearm |= 1ull << k;
+                    nearm |= 1ull << g;
 #pragma unroll
                     for (int q = 1; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f, inv));
                 }
+            }
+        }
+#pragma unroll 1
+        for (int si = 64 * kSegGroup + gg; si < nseg; si += 8) {
+            const float4 f = F[si];
+            const float inv = seg_inv_f(f);
+            if (seg_d2_f(qxf[0], qyf[0], f, inv) <= near_thr) {
+#pragma unroll
+                for (int q = 1; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f, inv));
             }
         }
         float thr[NQU];
@@ -384,6 +444,7 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
             const float r = dm + 2.f * delta;
             thr[q] = r * r * (1.f + 0x1p-20f);
         }
+        if (l0 == 0) ROW_MARK(b, 12);
         // ---- 3. exact fp64 distances of the candidates ----
         double bd[NQU];
         int bi[NQU];
@@ -395,8 +456,9 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
 #pragma unroll
             for (int q = 0; q < NQU; ++q) cm |= seg_d2_f(qxf[q], qyf[q], f, inv) <= thr[q] ? 1u << q : 0u;
             if (cm) {
-                const double ax = pk.ln_x[base + si], ay = pk.ln_y[base + si];
-                const double abx = pk.ln_abx[base + si], aby = pk.ln_aby[base + si], l2 = pk.ln_len2[base + si];
+                const double2* V = reinterpret_cast<const double2*>(pk.ln_v + base + si);
+                const double2 v0 = V[0], v1 = V[1], v2 = V[2];
+                const double ax = v0.x, ay = v0.y, abx = v1.x, aby = v1.y, l2 = v2.x;
 #pragma unroll
                 for (int q = 0; q < NQU; ++q) {
                     if (cm & (1u << q)) {
@@ -408,25 +470,17 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
                 }
             }
         };
-        if (NQU == 1) {
-#pragma unroll 1
-            for (int si = gg; si < nseg; si += 8) {
-                const float4 f = F[si];
-                if (seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)) <= thr[0]) exact(si, f);
-            }
-        } else {
-            while (nearm) {
-                const int k = __ffsll(nearm) - 1;
-                nearm &= nearm - 1;
-                const int si = gg + 8 * k;
-                exact(si, F[si]);
-            }
-#pragma unroll 1
-            for (int si = gg + 8 * 64; si < nseg; si += 8) {  // beyond the 64-bit near mask
-                const float4 f = F[si];
-                if (seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)) <= near_thr) exact(si, f);
-            }
+        while (nearm) {
+            const int si = (__ffsll(nearm) - 1) * kSegGroup + gg;
+            nearm &= nearm - 1;
+            exact(si, F[si]);
         }
+#pragma unroll 1
+        for (int si = 64 * kSegGroup + gg; si < nseg; si += 8) {  // beyond the 64-bit group mask
+            const float4 f = F[si];
+            if (seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)) <= near_thr) exact(si, f);
+        }
+        if (l0 == 0) ROW_MARK(b, 13);
         // ---- per-octet exact argmin, then s / signed d / half-width per (query, route lane) ----
         int hi_ = INT_MAX;
 #pragma unroll
@@ -438,13 +492,12 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
         bool ok = false;
         double hs = 0.0, hd = 0.0;
         if (hq < NQU && l0 + hk < nl && hi_ != INT_MAX) {
-            const size_t hb = (size_t(b) * L + l0 + hk) * C;
-            const double* X = pk.ln_x + hb;
-            const double* Y = pk.ln_y + hb;
+            const double2* V = reinterpret_cast<const double2*>(pk.ln_v + (size_t(b) * L + l0 + hk) * C + hi_);
+            const double2 a0 = V[0], a1 = V[1], a2 = V[2], a3 = V[3], b0 = V[4], b2 = V[6], b3 = V[7];
             double t;
-            const double d2 = seg_d2_pre(hpx, hpy, X[hi_], Y[hi_], pk.ln_abx[hb + hi_], pk.ln_aby[hb + hi_],
-                                         pk.ln_len2[hb + hi_], t);
-            const LaneHit h = lane_hit(hpx, hpy, X, Y, pk.ln_s + hb, pk.ln_hw + hb, hi_, d2, t);
+            const double d2 = seg_d2_pre(hpx, hpy, a0.x, a0.y, a1.x, a1.y, a2.x, t);
+            const double X[2] = {a0.x, b0.x}, Y[2] = {a0.y, b0.y}, S[2] = {a2.y, b2.y}, HW[2] = {a3.x, b3.x};
+            const LaneHit h = lane_hit(hpx, hpy, X, Y, S, HW, 0, d2, t);
             hs = h.s;
             hd = h.d;
             ok = fabs(h.d) <= h.hw;
@@ -1061,8 +1114,8 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
                 const int pr = __ffs(cmask) - 1;
                 cmask &= cmask - 1;
                 const int ci = (pr >> 2) & 3, ei = pr & 3, ei1 = (ei + 1) & 3;
-                const double d2 = pr < 16 ? seg_dist2(GX[ci], GY[ci], AX[ei], AY[ei], AX[ei1], AY[ei1])
-                                          : seg_dist2(AX[ci], AY[ci], GX[ei], GY[ei], GX[ei1], GY[ei1]);
+                const double d2 = pr < 16 ? seg_dist2_fast(GX[ci], GY[ci], AX[ei], AY[ei], AX[ei1], AY[ei1])
+                                          : seg_dist2_fast(AX[ci], AY[ci], GX[ei], GY[ei], GX[ei1], GY[ei1]);
                 d2min = fmin(d2min, d2);
             }
             if (!(d2min >= 1e-18)) {
@@ -1077,18 +1130,38 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
         nvalid += __popc(__ballot_sync(FULL, fl >= 0));
     }
     __syncwarp();
-    // rank by (distance, index) among the valid agents
-    for (int j0 = 0; j0 < na; j0 += 32) {
-        const int j = j0 + lane;
-        if (j < na && w.agf[j] >= 0) {
-            const double dj = w.agd[j];
-            int rank = 0;
-#pragma unroll 4
-            for (int k = 0; k < na; ++k) {
-                const double dk = w.agd[k];
-                rank += (w.agf[k] >= 0 && (dk < dj || (dk == dj && k < j))) ? 1 : 0;
+    // order by (distance, index) among the valid agents
+    if (na <= 32) {
+        // bitonic sort across the warp on (distance bits, index); distances are
+        // >= +0 so their bit patterns order like the values; invalid = +inf last
+        const bool ok = lane < na && w.agf[lane] >= 0;
+        unsigned long long key = ok ? (unsigned long long)__double_as_longlong(w.agd[lane]) : 0xFFF0000000000000ull;
+        int idx = lane;
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                const unsigned long long ok_ = __shfl_xor_sync(FULL, key, jj);
+                const int oi = __shfl_xor_sync(FULL, idx, jj);
+                const bool other_less = ok_ < key || (ok_ == key && oi < idx);
+                const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
+                if (keep_min == other_less) key = ok_, idx = oi;
             }
-            if (rank < Ka) w.sel[rank] = j;
+        }
+        if (lane < Ka && lane < nvalid) w.sel[lane] = idx;
+    } else {
+        for (int j0 = 0; j0 < na; j0 += 32) {
+            const int j = j0 + lane;
+            if (j < na && w.agf[j] >= 0) {
+                const double dj = w.agd[j];
+                int rank = 0;
+#pragma unroll 4
+                for (int k = 0; k < na; ++k) {
+                    const double dk = w.agd[k];
+                    rank += (w.agf[k] >= 0 && (dk < dj || (dk == dj && k < j))) ? 1 : 0;
+                }
+                if (rank < Ka) w.sel[rank] = j;
+            }
         }
     }
     const int nsel_ag = min(Ka, nvalid);
@@ -1204,6 +1277,7 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
     boxes_ready = false;
     for (int j = lane; j < ns; j += 32) w.sflag[j] = a.in.stopped_flags[soff + j];
     __syncwarp();
+    ROW_MARK(b, 8);
 
     bool skip = r0.done != 0;
     int ai = 0, si = 0;
@@ -1264,6 +1338,7 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
         for (int k = 0; k < 4; ++k) w.qx[k + 1] = X[k], w.qy[k + 1] = Y[k];
     }
     __syncwarp();
+    ROW_MARK(b, 9);
     const Proj p1 = warp_project<NQ>(pk, b, w.qx, w.qy);
     ROW_MARK(b, 1);
 
@@ -1344,42 +1419,20 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
     return r;
 }
 
-// Prefetch row b's static scenario data (the arrays one step touches) into L2.
-// `t` is the log index of the agent slice the step will read (t+1 of the row).
+// Prefetch row b's static scenario data (the arrays one step touches, from
+// the pack's prefetch table: one array per lane) into L2.  `t` is the log
+// index of the agent slice the kernel will read.
 template <bool STEP, bool OBS>
 __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int b, int t) {
     const DevPack& pk = a.pk;
     const int lane = lane_id();
-    const size_t LC = size_t(pk.d.L) * pk.d.C;
-    const size_t lb = size_t(b) * LC;
-    const int T = pk.d.T, A = pk.d.A;
+    if (lane >= pk.n_pf) return;
+    const PfDesc d = pk.pf[lane];
+    if (((d.mode & 1) && !STEP) || ((d.mode & 2) && !OBS) || d.bytes == 0) return;
+    const int T = pk.d.T;
     const int ts = t < T ? (t >= 0 ? t : 0) : T - 1;
-    const size_t as = (size_t(b) * T + ts) * A;
-    const void* ptr = nullptr;
-    size_t bytes = 0;
-    switch (lane) {
-        case 0: ptr = STEP ? pk.ln_x + lb : nullptr; bytes = LC * 8; break;
-        case 1: ptr = STEP ? pk.ln_y + lb : nullptr; bytes = LC * 8; break;
-        case 2: ptr = STEP ? pk.ln_abx + lb : nullptr; bytes = LC * 8; break;
-        case 3: ptr = STEP ? pk.ln_aby + lb : nullptr; bytes = LC * 8; break;
-        case 4: ptr = STEP ? pk.ln_len2 + lb : nullptr; bytes = LC * 8; break;
-        case 5: ptr = STEP ? pk.ln_s + lb : nullptr; bytes = LC * 8; break;
-        case 6: ptr = STEP ? pk.ln_hw + lb : nullptr; bytes = LC * 8; break;
-        case 7: ptr = OBS ? pk.road_cb + size_t(b) * pk.d.PC : nullptr; bytes = size_t(pk.d.PC) * 16; break;
-        case 8: ptr = OBS ? pk.route_cb + size_t(b) * pk.d.RC : nullptr; bytes = size_t(pk.d.RC) * 16; break;
-        case 9: ptr = OBS ? pk.route_xy + size_t(b) * pk.d.R : nullptr; bytes = size_t(pk.d.R) * 8; break;
-        case 10: ptr = OBS ? pk.route_oi + size_t(b) * pk.d.R : nullptr; bytes = size_t(pk.d.R) * 4; break;
-        case 11: ptr = pk.ag_x + as; bytes = size_t(A) * 4; break;
-        case 12: ptr = pk.ag_y + as; bytes = size_t(A) * 4; break;
-        case 13: ptr = pk.ag_h + as; bytes = size_t(A) * 4; break;
-        case 14: ptr = pk.ag_sp + as; bytes = size_t(A) * 4; break;
-        case 15: ptr = pk.ag_valid + as; bytes = size_t(A); break;
-        case 16: ptr = pk.ag_len + size_t(b) * A; bytes = size_t(A) * 4; break;
-        case 17: ptr = pk.ag_wid + size_t(b) * A; bytes = size_t(A) * 4; break;
-        case 18: ptr = STEP ? pk.ln_f4 + lb : nullptr; bytes = LC * 16; break;
-        default: break;
-    }
-    if (ptr) prefetch_l2(ptr, unsigned(bytes < (1u << 24) ? bytes : (1u << 24)));
+    const char* p = static_cast<const char*>(d.base) + size_t(b) * d.row_stride + size_t(ts) * d.t_stride;
+    prefetch_l2(p, d.bytes < (1u << 24) ? d.bytes : (1u << 24));
 }
 
 template <bool STEP, bool OBS>
@@ -1473,7 +1526,7 @@ extern "C" __attribute__((visibility("default"))) int zsimdbg_pathstats(unsigned
     if (cudaDeviceSynchronize() != cudaSuccess) return 1;
     if (cudaMemcpyFromSymbol(out, g_pstats, sizeof(g_pstats)) != cudaSuccess) return 1;
     if (rowcyc && nrows > 0 &&
-        cudaMemcpyFromSymbol(rowcyc, g_rowcyc, sizeof(unsigned) * 8 * size_t(nrows < kMaxStatRows ? nrows : kMaxStatRows)) !=
+        cudaMemcpyFromSymbol(rowcyc, g_rowcyc, sizeof(unsigned) * 16 * size_t(nrows < kMaxStatRows ? nrows : kMaxStatRows)) !=
             cudaSuccess)
         return 1;
     if (reset) {

@@ -10,8 +10,8 @@
 //                      Morton order as 32-point chunks with bounding boxes [B][PC]
 //   route   [B][R]     float2 xy + u8 is_left|lane_valid<<1 + i32 index in
 //                      build_route_points order (simcore.cpp:181-200), chunked likewise
-//   lanes   [B][L][C]  centerline x, y, s, half_width f64 after RouteFrame::build
-//                      clipping (roads.cpp:43-103) + per-segment b-a and |b-a|^2;
+//   lanes   [B][L][C]  centerline records {x, y, b-a, |b-a|^2, s, half_width} f64
+//                      after RouteFrame::build clipping (roads.cpp:43-103);
 //                      an fp32 copy (a - origin, b - a) for screening;
 //                      n vertices + lane_id per lane
 //   lights  [B][NL]    route s f64 + state u8[T] for lights kept by
@@ -30,9 +30,26 @@ namespace zs {
 struct PackDims {
     int32_t B, T, A, P, R, L, C, NL, NS;
     int32_t PC, RC;  // 32-point chunks of the road / route point sets
+    int32_t GC;      // 8-segment groups per lane centreline
 };
 
+constexpr int kSegGroup = 8;  // segments per centreline group (bounding box)
+
 constexpr int kChunk = 32;  // points per spatial chunk (one warp-wide load)
+
+// One centreline vertex with its outgoing segment (i -> i+1), 64 B: an exact
+// projection touches one or two consecutive records.  abx/aby/len2 follow
+// point_segment_dist2's expressions (geometry.cpp:18-19); unused on the last vertex.
+struct __align__(16) LaneVtx {
+    double x, y, abx, aby, len2, s, hw, pad;
+};
+
+// One per-row array the kernels prefetch into L2 at row start:
+// address = base + row * row_stride + t * t_stride, `bytes` long.
+struct PfDesc {
+    const void* base;
+    uint32_t row_stride, t_stride, bytes, mode;  // mode bit 0: step kernels only, bit 1: observe kernels only
+};
 
 struct DevPack {
     PackDims d;
@@ -78,20 +95,17 @@ struct DevPack {
     const int32_t* route_oi;
     const float4* route_cb;  // [B][RC]
     // lanes
-    const double* ln_x;
-    const double* ln_y;
-    const double* ln_s;
-    const double* ln_hw;
-    const double* ln_abx;   // [B][L][C] segment vectors b - a (geometry.cpp:18), last slot unused
-    const double* ln_aby;
-    const double* ln_len2;  // |b - a|^2 with the reference's op order
+    const LaneVtx* ln_v;    // [B][L][C] exact centreline records
     const float4* ln_f4;    // [B][L][C] fp32 screening copy: (a - origin, b - a) per segment
+    const float4* ln_gb;    // [B][L][GC] group boxes (origin-relative, rounded outward)
     const double2* ln_org;  // [B] origin of the fp32 copy
     const float* ln_fe;     // [B] max |a - origin|_1 over vertices + max segment length (error scale)
     const int32_t* ln_n;
     const uint32_t* ln_id;
     const float4* road_box;   // [B] (min x, min y, max x, max y) of the road points
     const float4* route_box;  // [B] same for the route border points
+    const PfDesc* pf;  // prefetch table
+    int32_t n_pf;
     // lights / stops
     const double* lt_s;
     const uint8_t* lt_state;  // [B][NL][T]

@@ -43,7 +43,7 @@ def main():
         fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int, C.c_void_p, C.c_int]
         fn.restype = C.c_int
     res = {"B": B, "ms": [], "stats": [], "phases": {}}
-    cyc = np.zeros((B, 8), dtype=np.uint32)
+    cyc = np.zeros((B, 16), dtype=np.uint32)
     PH = ["project", "collide+flags", "active+agents", "road_topk", "road_feat", "route_topk", "route_feat"]
     gc.disable()
     for ep in range(int(next((a[5:] for a in sys.argv if a.startswith("--eps")), "2"))):  # episode 0 warms up
@@ -64,7 +64,9 @@ def main():
                 if ep == 1:
                     res["stats"].append(list(buf)[:len(NAMES)])
                 if ep == 1 and t in (5, 40, 80):
-                    d = np.diff(cyc.astype(np.int64), axis=1) % (1 << 32)  # [B][7]
+                    d = np.diff(cyc[:, :8].astype(np.int64), axis=1) % (1 << 32)  # [B][7]
+                    seq = [0, 8, 9, 10, 11, 12, 13, 1]
+                    sub = np.diff(cyc[:, seq].astype(np.int64), axis=1) % (1 << 32)
                     tot = d.sum(1)
                     slow = np.argsort(tot)[-max(1, B // 100):]
                     res["phases"][t] = {
@@ -72,6 +74,11 @@ def main():
                                       "max": float(tot.max())},
                         "mean": dict(zip(PH, d.mean(0).round(0).tolist())),
                         "slowest_1pct_mean": dict(zip(PH, d[slow].mean(0).round(0).tolist())),
+                        "project_split": dict(zip(["load+flags", "bicycle+queries", "groups", "pass1", "pass2",
+                                                   "exact", "hit+rest"], sub.mean(0).round(0).tolist())),
+                        "project_split_slowest_1pct": dict(zip(["load+flags", "bicycle+queries", "groups", "pass1",
+                                                                "pass2", "exact", "hit+rest"],
+                                                               sub[slow].mean(0).round(0).tolist())),
                         "slowest_row": int(np.argmax(tot)), "slowest_row_phases": dict(zip(PH, d[np.argmax(tot)].tolist())),
                     }
             if ep >= 1:
