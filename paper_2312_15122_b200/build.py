@@ -55,12 +55,17 @@ def _run(cmd: list[str]) -> str:
 PATHSTATS_OUT = BUILD / "pathstats" / "libzsim_gpu_pathstats.so"
 
 
-def build(force: bool = False, verbose: bool = False, pathstats: bool = False) -> Path:
-    """Compile libzsim_gpu.so (no-op when up to date)."""
+def build(force: bool = False, verbose: bool = False, pathstats: bool = False, variant: str | None = None,
+          defines: list[str] | None = None) -> Path:
+    """Compile libzsim_gpu.so (no-op when up to date).  `variant` builds an
+    experiment copy with extra -D flags under _build/<variant>/ (tools only)."""
     out, bdir, defs = OUT, BUILD, []
     if pathstats:
         out, bdir, defs = PATHSTATS_OUT, PATHSTATS_OUT.parent, ["-DZS_PATHSTATS"]
-    if not force and not (_stale() if not pathstats else not out.exists() or any(
+    if variant:
+        bdir = BUILD / variant
+        out, defs = bdir / "libzsim_gpu.so", defs + [f"-D{d}" for d in (defines or [])]
+    if not force and not (_stale() if out == OUT else not out.exists() or any(
             p.stat().st_mtime > out.stat().st_mtime for p in _sources())):
         return out
     bdir.mkdir(parents=True, exist_ok=True)
@@ -87,4 +92,7 @@ def build(force: bool = False, verbose: bool = False, pathstats: bool = False) -
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, pathstats="--pathstats" in sys.argv))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, pathstats="--pathstats" in sys.argv,
+                variant=var, defines=defs))

@@ -584,7 +584,8 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
                     double abx = lf.x[i + 1] - lf.x[i], aby = lf.y[i + 1] - lf.y[i];
                     v.abx = abx;
                     v.aby = aby;
-                    v.len2 = abx * abx + aby * aby;
+                    v.ds = lf.s[i + 1] - lf.s[i];
+                    v.dhw = lf.hw[i + 1] - lf.hw[i];
                     fe_l = std::max(fe_l, std::fabs(abx) + std::fabs(aby));
                     float* f4 = pb.at<float>(o_lf4) + 4 * k;
                     f4[0] = float(lf.x[i] - ox);
@@ -687,7 +688,10 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     env->dt = dt;
     env->total_stop = total_stop;
     env->base.key_cap = std::max(d.P, d.R);
-    env->base.cand_cap = 256;  // = 32 lanes x kMaxCandPerLane in the top-k kernel
+#ifndef ZS_CAND_CAP
+#define ZS_CAND_CAP 256
+#endif
+    env->base.cand_cap = ZS_CAND_CAP;  // top-k candidates per warp before the histogram refinement
     env->sl = state_layout(B, total_stop);
     env->sol = stepout_layout(B);
     env->ol = obs_layout(B, env->cfg.n_agents, env->cfg.n_road, env->cfg.n_route);

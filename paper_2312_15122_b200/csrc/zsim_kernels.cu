@@ -108,13 +108,28 @@ __device__ __forceinline__ T pick5(int k, T a0, T a1, T a2, T a3, T a4) {
     return k == 0 ? a0 : k == 1 ? a1 : k == 2 ? a2 : k == 3 ? a3 : a4;
 }
 
+// Row state, uniform across the warp.
+struct Row {
+    double x, y, h, v, steer, proj_s, proj_d;
+    unsigned long long rng;
+    int t, done, reason, events, in_corr;
+};
+
+// Warp-uniform row state lives in shared memory, not in 32 copies of
+// registers: the step reads r0 and writes r / the ego box, observe reads them.
+struct RowSh {
+    Row r0;                // pre-step state as loaded
+    Row r;                 // post-step state (what observe sees)
+    Box eb;                // ego box of r
+    double ex[4], ey[4];   // its corners (obb_distance reads them lane-indexed)
+    double qx[5], qy[5];   // projection queries (position + inflated corners)
+    double a_lat;          // step: v^2 tan(steer) / wheelbase (simcore.cpp:309-316)
+    int boxes_ready;       // agent boxes at r.t + overlap flags are in agx/agy/agf
+};
+
 // Per-warp shared-memory carve-up (host mirror: smem_bytes()).
 struct WarpBuf {
-    double* egx;           // [4] ego box corners (lane-indexed reads)
-    double* egy;
-    int* plist;            // unused
-    double* qx;            // [5] projection queries (ego position + inflated corners)
-    double* qy;
+    RowSh* rs;
     double* agx;           // [A*4] agent corners
     double* agy;
     double* agd;           // [A] bbox distance
@@ -130,13 +145,13 @@ struct WarpBuf {
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) / 16 * 16; }
 
-// Per-warp layout: [ego corners 64 B][queries 80 B][union: agent phase | top-k phase][stop flags].
+// Per-warp layout: [RowSh][union: agent phase | top-k phase][stop flags].
 // The agent buffers (boxes at t+1 from the step, distances, selection) are
 // dead once the agent features are written, before the road/route top-k, so
 // both phases share one region.
 inline SmemLayout warp_layout(int A, int cap, int ka, int ns) {
     SmemLayout L;
-    size_t o = 64 + 80 + 16;  // ego corners (64 B), projection queries (80 B), pad
+    size_t o = al16(sizeof(RowSh));  // warp-uniform row state
     const size_t u0 = o;
     auto put = [&](uint32_t& f, size_t bytes) { f = uint32_t(o), o += al16(bytes); };
     put(L.agx, size_t(A) * 4 * 8);
@@ -161,11 +176,7 @@ __device__ __forceinline__ WarpBuf carve(unsigned char* base, const KernelArgs& 
     const SmemLayout& L = a.lay;
     unsigned char* p = base + L.total * unsigned(warp_in_block());
     WarpBuf w;
-    w.egx = reinterpret_cast<double*>(p);
-    w.egy = reinterpret_cast<double*>(p + 32);
-    w.plist = nullptr;
-    w.qx = reinterpret_cast<double*>(p + 64);
-    w.qy = reinterpret_cast<double*>(p + 104);
+    w.rs = reinterpret_cast<RowSh*>(p);
     w.agx = reinterpret_cast<double*>(p + L.agx);
     w.agy = reinterpret_cast<double*>(p + L.agy);
     w.agd = reinterpret_cast<double*>(p + L.agd);
@@ -179,13 +190,6 @@ __device__ __forceinline__ WarpBuf carve(unsigned char* base, const KernelArgs& 
     w.sflag = p + L.sflag;
     return w;
 }
-
-// Row state, uniform across the warp (every lane holds the same values).
-struct Row {
-    double x, y, h, v, steer, proj_s, proj_d;
-    unsigned long long rng;
-    int t, done, reason, events, in_corr;
-};
 
 __device__ __forceinline__ Row load_row(const zsim_state_view& in, int b) {
     Row r;
@@ -322,6 +326,7 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
     PSTAT(22, 1);
     const double2 org = pk.ln_org[b];
     const float fe = pk.ln_fe[b];
+    const double route_len = pk.route_len[b];
     float qxf[NQU], qyf[NQU];
 #pragma unroll
     for (int q = 0; q < NQU; ++q) {
@@ -457,8 +462,8 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
             for (int q = 0; q < NQU; ++q) cm |= seg_d2_f(qxf[q], qyf[q], f, inv) <= thr[q] ? 1u << q : 0u;
             if (cm) {
                 const double2* V = reinterpret_cast<const double2*>(pk.ln_v + base + si);
-                const double2 v0 = V[0], v1 = V[1], v2 = V[2];
-                const double ax = v0.x, ay = v0.y, abx = v1.x, aby = v1.y, l2 = v2.x;
+                const double2 v0 = V[0], v1 = V[1];
+                const double ax = v0.x, ay = v0.y, abx = v1.x, aby = v1.y, l2 = abx * abx + aby * aby;
 #pragma unroll
                 for (int q = 0; q < NQU; ++q) {
                     if (cm & (1u << q)) {
@@ -482,6 +487,7 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
         }
         if (l0 == 0) ROW_MARK(b, 13);
         // ---- per-octet exact argmin, then s / signed d / half-width per (query, route lane) ----
+        const uint32_t my_id = lane < 4 && l0 + lane < nl ? pk.ln_id[size_t(b) * L + l0 + lane] : 0u;
         int hi_ = INT_MAX;
 #pragma unroll
         for (int q = 0; q < NQU; ++q) {
@@ -489,20 +495,28 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
             const int v = __shfl_sync(FULL, bi[q], hk * 8);
             if (hq == q) hi_ = v;
         }
+        if (l0 == 0) ROW_MARK(b, 14);
         bool ok = false;
         double hs = 0.0, hd = 0.0;
         if (hq < NQU && l0 + hk < nl && hi_ != INT_MAX) {
             const double2* V = reinterpret_cast<const double2*>(pk.ln_v + (size_t(b) * L + l0 + hk) * C + hi_);
-            const double2 a0 = V[0], a1 = V[1], a2 = V[2], a3 = V[3], b0 = V[4], b2 = V[6], b3 = V[7];
+            const double2 a0 = V[0], a1 = V[1], a2 = V[2], a3 = V[3];
             double t;
-            const double d2 = seg_d2_pre(hpx, hpy, a0.x, a0.y, a1.x, a1.y, a2.x, t);
-            const double X[2] = {a0.x, b0.x}, Y[2] = {a0.y, b0.y}, S[2] = {a2.y, b2.y}, HW[2] = {a3.x, b3.x};
-            const LaneHit h = lane_hit(hpx, hpy, X, Y, S, HW, 0, d2, t);
+            const double d2 = seg_d2_pre(hpx, hpy, a0.x, a0.y, a1.x, a1.y, a1.x * a1.x + a1.y * a1.y, t);
+            // lane_hit (roads.cpp:130-139) with b - a, s and half-width increments from the record
+            const double qx_ = a0.x + a1.x * t, qy_ = a0.y + a1.y * t;
+            const double rx = hpx - qx_, ry = hpy - qy_;
+            const double sign = (a1.x * ry - a1.y * rx) >= 0.0 ? 1.0 : -1.0;
+            LaneHit h;
+            h.s = a2.x + a2.y * t;
+            h.d = sign * sqrt(d2);
+            h.hw = a3.x + a3.y * t;
             hs = h.s;
             hd = h.d;
             ok = fabs(h.d) <= h.hw;
         }
         const unsigned okb = __ballot_sync(FULL, ok);
+        if (l0 == 0) ROW_MARK(b, 15);
 #pragma unroll
         for (int q = 0; q < NQU; ++q)
             if ((okb >> (4 * q)) & 15u) in_bits |= 1u << q;
@@ -511,7 +525,7 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
             const double s0 = __shfl_sync(FULL, hs, k), d0 = __shfl_sync(FULL, hd, k);
             const int w0 = __shfl_sync(FULL, hi_, k);
             if (w0 == INT_MAX) continue;
-            const uint32_t id = pk.ln_id[size_t(b) * L + l0 + k];
+            const uint32_t id = __shfl_sync(FULL, my_id, k);
             if (!have || fabs(d0) < best_abs || (fabs(d0) == best_abs && id < best_id)) {
                 have = true;
                 best_abs = fabs(d0);
@@ -522,7 +536,7 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
         }
     }
     Proj p;
-    p.s = clampd(best_s, 0.0, pk.route_len[b]);
+    p.s = clampd(best_s, 0.0, route_len);
     p.d = best_d;
     p.in_corr = int(in_bits & 1u);
     p.on_route = NQU == 5 ? int((in_bits & 0x1Eu) == 0x1Eu) : 1;
@@ -922,16 +936,17 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
 }
 
 // ---------------------------------------------------------------------------
-// observe one row (simcore.cpp:423-538).  When `boxes_ready`, the agent boxes
-// at r.t and their overlap with the ego box `eb_in` are already in
-// w.agx/agy/agf (fused step+observe).
+// observe one row (simcore.cpp:423-538) from w.rs->r.  When
+// w.rs->boxes_ready, the ego box and the agent boxes at r.t with their
+// overlap flags are already in smem (fused step+observe).
 // ---------------------------------------------------------------------------
-__device__ void observe_row(const KernelArgs& a, int b, const Row& r, const WarpBuf& w, bool boxes_ready,
-                            const Box& eb_in, const double* EX_in, const double* EY_in) {
+__device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     ROW_MARK(b, 2);
     const DevPack& pk = a.pk;
     const DevCfg& cfg = a.cfg;
     const int lane = lane_id();
+    RowSh& rs = *w.rs;
+    const Row& r = rs.r;
     const int Ka = cfg.n_agents, Kr = cfg.n_road, Kl = cfg.n_route;
     float* act = a.obs.active + size_t(b) * 9;
     float* agt = a.obs.agents + size_t(b) * Ka * 6;
@@ -955,28 +970,25 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
 
     const int t = r.t;
     PSTAT(0, 1);
-    Box eb;
-    double EX[4], EY[4];
-    if (boxes_ready) {
-        eb = eb_in;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            EX[k] = EX_in[k];
-            EY[k] = EY_in[k];
-        }
-    } else {
+    const bool boxes_ready = rs.boxes_ready != 0;
+    if (!boxes_ready) {
         const double2 sc = sincos2(r.h);
-        const double c = sc.y, s = sc.x;
-        eb.cx = r.x + c * cfg.ego_center_offset;
-        eb.cy = r.y + s * cfg.ego_center_offset;
-        eb.hl = cfg.ego_length * 0.5;
-        eb.hw = cfg.ego_width * 0.5;
-        eb.c = c;
-        eb.s = s;
-        box_corners(eb, EX, EY);
+        if (lane == 0) {
+            const double c = sc.y, s = sc.x;
+            Box eb;
+            eb.cx = r.x + c * cfg.ego_center_offset;
+            eb.cy = r.y + s * cfg.ego_center_offset;
+            eb.hl = cfg.ego_length * 0.5;
+            eb.hw = cfg.ego_width * 0.5;
+            eb.c = c;
+            eb.s = s;
+            rs.eb = eb;
+            box_corners(eb, rs.ex, rs.ey);
+        }
+        __syncwarp();
     }
     // ego-frame rotation by -heading (simcore.cpp:432): cos(-h) = cos h, sin(-h) = -sin h
-    const double oc = eb.c, os = -eb.s;
+    const double oc = rs.eb.c, os = -rs.eb.s;
 
     // ---- active features: roads::stop_info (roads.cpp:253-277), simcore.cpp:440-455 ----
     {
@@ -1030,9 +1042,10 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     const bool t_ok = t < pk.num_steps[b];
     const size_t aslice = (size_t(b) * pk.d.T + (t_ok ? t : 0)) * A;
     if (!boxes_ready) {
+        const Box eb = rs.eb;
         for (int j = lane; j < na; j += 32) {
             int f = -1;
-            if (t_ok && pk.ag_valid[aslice + j]) f = agent_box_overlap(pk, b, aslice, j, eb, EX, EY, w);
+            if (t_ok && pk.ag_valid[aslice + j]) f = agent_box_overlap(pk, b, aslice, j, eb, rs.ex, rs.ey, w);
             w.agf[j] = f;
         }
         __syncwarp();
@@ -1048,20 +1061,16 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
     // -- a superset of the final cut -- and only candidates get the fp64
     // expressions.  A (near-)contact (min d2 < 1e-18) takes the reference's
     // full segment_segment_distance over the 16 edge pairs.
-    if (lane < 4) {
-        w.egx[lane] = pick5(lane, EX[0], EX[1], EX[2], EX[3], EX[3]);
-        w.egy[lane] = pick5(lane, EY[0], EY[1], EY[2], EY[3], EY[3]);
-    }
-    __syncwarp();
-    const double* GX = w.egx;
-    const double* GY = w.egy;
+    const double* GX = rs.ex;
+    const double* GY = rs.ey;
+    const double ecx = rs.eb.cx, ecy = rs.eb.cy;
     float gxf[4], gyf[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        gxf[k] = float(EX[k] - eb.cx);
-        gyf[k] = float(EY[k] - eb.cy);
+        gxf[k] = float(GX[k] - ecx);
+        gyf[k] = float(GY[k] - ecy);
     }
-    const float ge = float(2.0 * (eb.hl + eb.hw)) + 1e-3f;  // >= any ego edge length
+    const float ge = float(2.0 * (rs.eb.hl + rs.eb.hw)) + 1e-3f;  // >= any ego edge length
     int nvalid = 0;
     for (int j0 = 0; j0 < na; j0 += 32) {
         const int j = j0 + lane;
@@ -1073,8 +1082,8 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
             float S = 0.f;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                axf[k] = float(AX[k] - eb.cx);
-                ayf[k] = float(AY[k] - eb.cy);
+                axf[k] = float(AX[k] - ecx);
+                ayf[k] = float(AY[k] - ecy);
                 S = fmaxf(S, fmaxf(fabsf(axf[k]), fabsf(ayf[k])));
             }
             float E = ge;
@@ -1263,23 +1272,23 @@ __device__ void observe_row(const KernelArgs& a, int b, const Row& r, const Warp
 }
 
 // ---------------------------------------------------------------------------
-// step one row (simcore.cpp:278-404).  Returns the post-step row; when the
-// row was simulated (not passed through) the agent boxes at t+1 and their
-// overlap with the new ego box stay in smem for a fused observe.
+// step one row (simcore.cpp:278-404): reads w.rs->r0, writes the post-step
+// row to w.rs->r (+ output buffers).  When the row is simulated (not passed
+// through) the ego box, the agent boxes at t+1 and their overlap flags stay in
+// smem for a fused observe (w.rs->boxes_ready).
 // ---------------------------------------------------------------------------
-__device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf& w, bool& boxes_ready, Box& eb,
-                        double* EX, double* EY) {
+__device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     const DevPack& pk = a.pk;
     const DevCfg& cfg = a.cfg;
     const int lane = lane_id();
+    RowSh& rs = *w.rs;
     const int ns = pk.n_stops[b];
     const int soff = pk.stop_off[b];
-    boxes_ready = false;
     for (int j = lane; j < ns; j += 32) w.sflag[j] = a.in.stopped_flags[soff + j];
     __syncwarp();
     ROW_MARK(b, 8);
 
-    bool skip = r0.done != 0;
+    bool skip = rs.r0.done != 0;
     int ai = 0, si = 0;
     if (!skip) {
         ai = a.accel[b];
@@ -1292,6 +1301,9 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
     if (skip) {
         // absorbing pass-through (simcore.cpp:281-299); bad-action rows are left unchanged
         if (lane == 0) {
+            const Row r0 = rs.r0;
+            rs.r = r0;
+            rs.boxes_ready = 0;
             store_row(a.out, b, r0);
             a.so.reward[b] = 0.f;
             a.so.event[b] = 0;
@@ -1302,73 +1314,86 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
         }
         for (int j = lane; j < ns; j += 32) a.out.stopped_flags[soff + j] = w.sflag[j];
         __syncwarp();
-        return r0;
+        return;
     }
 
     PSTAT(23, 1);
     const double accel = cfg.accel_bins[ai], rate = cfg.steer_bins[si];
     const double dt = pk.dt;
-    // dyn::bicycle_step (dynamics.cpp:10-19)
-    const double2 sc0 = sincos2(r0.h);
-    const double tan_steer = tan1(r0.steer);
-    Row r = r0;
-    r.x = r0.x + r0.v * sc0.y * dt;
-    r.y = r0.y + r0.v * sc0.x * dt;
-    r.h = wrap1(r0.h + r0.v / cfg.wheelbase * tan_steer * dt);
-    r.v = maxd(r0.v + accel * dt, cfg.v_min);
-    r.steer = clampd(r0.steer + rate * dt, -cfg.delta_max, cfg.delta_max);
-    r.t = r0.t + 1;
-    // ego_box(e1) (simcore.cpp:156-160) and its margin-inflated corners (roads.cpp:202-204)
-    const double2 sc1 = sincos2(r.h);
-    eb.cx = r.x + sc1.y * cfg.ego_center_offset;
-    eb.cy = r.y + sc1.x * cfg.ego_center_offset;
-    eb.hl = cfg.ego_length * 0.5;
-    eb.hw = cfg.ego_width * 0.5;
-    eb.c = sc1.y;
-    eb.s = sc1.x;
-    box_corners(eb, EX, EY);
-    if (lane == 0) {
-        Box inf = eb;
-        inf.hl = eb.hl + cfg.footprint_margin;
-        inf.hw = eb.hw + cfg.footprint_margin;
-        double X[4], Y[4];
-        box_corners(inf, X, Y);
-        w.qx[0] = r.x;
-        w.qy[0] = r.y;
-        for (int k = 0; k < 4; ++k) w.qx[k + 1] = X[k], w.qy[k + 1] = Y[k];
+    {
+        // dyn::bicycle_step (dynamics.cpp:10-19)
+        const double x0 = rs.r0.x, y0 = rs.r0.y, h0 = rs.r0.h, v0 = rs.r0.v, st0 = rs.r0.steer;
+        const double2 sc0 = sincos2(h0);
+        const double tan_steer = tan1(st0);
+        const double x = x0 + v0 * sc0.y * dt;
+        const double y = y0 + v0 * sc0.x * dt;
+        const double h = wrap1(h0 + v0 / cfg.wheelbase * tan_steer * dt);
+        // ego_box(e1) (simcore.cpp:156-160) and its margin-inflated corners (roads.cpp:202-204)
+        const double2 sc1 = sincos2(h);
+        if (lane == 0) {
+            Row& r = rs.r;
+            r.x = x;
+            r.y = y;
+            r.h = h;
+            r.v = maxd(v0 + accel * dt, cfg.v_min);
+            r.steer = clampd(st0 + rate * dt, -cfg.delta_max, cfg.delta_max);
+            r.t = rs.r0.t + 1;
+            r.rng = rs.r0.rng;
+            Box eb;
+            eb.cx = x + sc1.y * cfg.ego_center_offset;
+            eb.cy = y + sc1.x * cfg.ego_center_offset;
+            eb.hl = cfg.ego_length * 0.5;
+            eb.hw = cfg.ego_width * 0.5;
+            eb.c = sc1.y;
+            eb.s = sc1.x;
+            rs.eb = eb;
+            box_corners(eb, rs.ex, rs.ey);
+            Box inf = eb;
+            inf.hl = eb.hl + cfg.footprint_margin;
+            inf.hw = eb.hw + cfg.footprint_margin;
+            double X[4], Y[4];
+            box_corners(inf, X, Y);
+            rs.qx[0] = x;
+            rs.qy[0] = y;
+            for (int k = 0; k < 4; ++k) rs.qx[k + 1] = X[k], rs.qy[k + 1] = Y[k];
+            rs.a_lat = v0 * v0 * tan_steer / cfg.wheelbase;
+        }
+        __syncwarp();
     }
-    __syncwarp();
+    const double a_lat = rs.a_lat;
     ROW_MARK(b, 9);
-    const Proj p1 = warp_project<NQ>(pk, b, w.qx, w.qy);
+    const Proj p1 = warp_project<NQ>(pk, b, rs.qx, rs.qy);
     ROW_MARK(b, 1);
 
     // collision with the agents valid at t+1 (simcore.cpp:323-331); boxes kept for observe(t+1)
     int hit = 0;
     {
         const int na = pk.n_agents[b];
-        const bool t_ok = r.t < pk.num_steps[b];
-        const size_t slice = (size_t(b) * pk.d.T + (t_ok ? r.t : 0)) * pk.d.A;
+        const int t1 = rs.r.t;
+        const bool t_ok = t1 < pk.num_steps[b];
+        const size_t slice = (size_t(b) * pk.d.T + (t_ok ? t1 : 0)) * pk.d.A;
+        const Box eb = rs.eb;
         for (int j = lane; j < na; j += 32) {
             int f = -1;
-            if (t_ok && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, b, slice, j, eb, EX, EY, w);
+            if (t_ok && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, b, slice, j, eb, rs.ex, rs.ey, w);
             w.agf[j] = f;
             hit |= f == 1;
         }
         hit = __any_sync(FULL, hit);
-        __syncwarp();
-        boxes_ready = true;
     }
 
+    const double ps0 = rs.r0.proj_s, v0 = rs.r0.v, vn = rs.r.v;
+    const int t0 = rs.r0.t;
     const bool hit_off_route = !p1.on_route;
     bool hit_red = false;
     {
         const int nsteps = pk.num_steps[b];
-        const int t_light = r0.t < nsteps - 1 ? r0.t : nsteps - 1;
+        const int t_light = t0 < nsteps - 1 ? t0 : nsteps - 1;
         const int nlt = pk.n_lights[b];
 #pragma unroll 1
         for (int k = 0; k < nlt; ++k) {
             double ls = pk.lt_s[size_t(b) * pk.d.NL + k];
-            if (r0.proj_s < ls && ls <= p1.s && pk.lt_state[(size_t(b) * pk.d.NL + k) * pk.d.T + t_light] == 0)
+            if (ps0 < ls && ls <= p1.s && pk.lt_state[(size_t(b) * pk.d.NL + k) * pk.d.T + t_light] == 0)
                 hit_red = true;
         }
     }
@@ -1376,16 +1401,15 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
 #pragma unroll 1
     for (int j = 0; j < ns; ++j) {
         double ss = pk.st_s[size_t(b) * pk.d.NS + j];
-        if (r0.proj_s < ss && ss <= p1.s && r0.v > cfg.stop_cross_speed && !w.sflag[j]) hit_stop = true;
+        if (ps0 < ss && ss <= p1.s && v0 > cfg.stop_cross_speed && !w.sflag[j]) hit_stop = true;
     }
     const bool hit_goal = fabs(p1.s - pk.goal_s[b]) <= cfg.goal_radius;
-    const double progress = p1.s - r0.proj_s;
-    const double a_lat = r0.v * r0.v * tan_steer / cfg.wheelbase;
+    const double progress = p1.s - ps0;
     const double a_lon = accel;
-    double reward = cfg.w_progress * progress - cfg.w_speed * maxd(0.0, r.v - double(pk.speed_limit[b])) * dt -
+    double reward = cfg.w_progress * progress - cfg.w_speed * maxd(0.0, vn - double(pk.speed_limit[b])) * dt -
                     cfg.w_lat * a_lat * a_lat * dt - cfg.w_lon * a_lon * a_lon * dt;
     const int reason = hit ? 1 : hit_off_route ? 2 : hit_red ? 3 : hit_stop ? 4 : hit_goal ? 5 : 0;
-    int events = r0.events;
+    int events = rs.r0.events;
     if (cfg.disable_dones) {
         events |= (hit ? 1 : 0) | (hit_off_route ? 2 : 0) | (hit_red ? 4 : 0) | (hit_stop ? 8 : 0) |
                   (hit_goal ? 16 : 0);
@@ -1393,30 +1417,33 @@ __device__ Row step_row(const KernelArgs& a, int b, const Row& r0, const WarpBuf
         events |= 1 << (reason - 1);
         if (reason != 5) reward -= cfg.terminal_penalty;
     }
-    r.done = (!cfg.disable_dones && reason != 0) ? 1 : 0;
-    r.reason = r.done ? reason : 0;
-    r.proj_s = p1.s;
-    r.proj_d = p1.d;
-    r.in_corr = p1.in_corr;
-    r.events = events;
+    const int done = (!cfg.disable_dones && reason != 0) ? 1 : 0;
+    __syncwarp();
     if (lane == 0) {
+        Row& r = rs.r;
+        r.done = done;
+        r.reason = done ? reason : 0;
+        r.proj_s = p1.s;
+        r.proj_d = p1.d;
+        r.in_corr = p1.in_corr;
+        r.events = events;
+        rs.boxes_ready = 1;
         store_row(a.out, b, r);
         a.so.reward[b] = float(reward);
         a.so.event[b] = uint8_t(reason);
         a.so.s[b] = float(p1.s);
         a.so.a_lat[b] = float(a_lat);
         a.so.a_lon[b] = float(a_lon);
-        a.so.v[b] = float(r.v);
+        a.so.v[b] = float(vn);
     }
     // stopped-flag update with the post-step state (simcore.cpp:390-396)
     for (int j = lane; j < ns; j += 32) {
-        double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - r.proj_s;
+        double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - p1.s;
         uint8_t fl = w.sflag[j];
-        if (ahead >= 0.0 && ahead <= cfg.stop_zone && r.v < cfg.stop_slow_speed) fl = 1;
+        if (ahead >= 0.0 && ahead <= cfg.stop_zone && vn < cfg.stop_slow_speed) fl = 1;
         a.out.stopped_flags[soff + j] = fl;
     }
     __syncwarp();
-    return r;
 }
 
 // Prefetch row b's static scenario data (the arrays one step touches, from
@@ -1436,7 +1463,10 @@ __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int b, int t) 
 }
 
 template <bool STEP, bool OBS>
-__global__ void __launch_bounds__(kThreads, 7) k_step_observe(const KernelArgs a) {
+#ifndef ZS_MIN_BLOCKS
+#define ZS_MIN_BLOCKS 7  // 72 registers: 28 resident warps per SM
+#endif
+__global__ void __launch_bounds__(kThreads, ZS_MIN_BLOCKS) k_step_observe(const KernelArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const WarpBuf w = carve(dsm, a);
     const int wpb = kThreads / 32;
@@ -1444,15 +1474,21 @@ __global__ void __launch_bounds__(kThreads, 7) k_step_observe(const KernelArgs a
     int b = blockIdx.x * wpb + warp_in_block();
     if (b < a.pk.d.B) prefetch_row<STEP, OBS>(a, b, a.in.t[b] + (STEP ? 1 : 0));
     for (; b < a.pk.d.B; b += stride) {
-        Row r = load_row(a.in, b);
+        if (lane_id() == 0) w.rs->r0 = load_row(a.in, b);
+        __syncwarp();
         // the warp's next row: its static data streams into L2 while this row computes
-        if (b + stride < a.pk.d.B) prefetch_row<STEP, OBS>(a, b + stride, r.t + (STEP ? 1 : 0));
+        if (b + stride < a.pk.d.B) prefetch_row<STEP, OBS>(a, b + stride, w.rs->r0.t + (STEP ? 1 : 0));
         ROW_MARK(b, 0);
-        bool boxes_ready = false;
-        Box eb{};
-        double EX[4] = {0, 0, 0, 0}, EY[4] = {0, 0, 0, 0};
-        if (STEP) r = step_row(a, b, r, w, boxes_ready, eb, EX, EY);
-        if (OBS) observe_row(a, b, r, w, boxes_ready && !r.done, eb, EX, EY);
+        if (STEP) {
+            step_row(a, b, w);
+        } else {
+            if (lane_id() == 0) {
+                w.rs->r = w.rs->r0;
+                w.rs->boxes_ready = 0;
+            }
+            __syncwarp();
+        }
+        if (OBS) observe_row(a, b, w);
         ROW_MARK(b, 7);
     }
 }

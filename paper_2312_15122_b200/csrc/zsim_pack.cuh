@@ -38,10 +38,11 @@ constexpr int kSegGroup = 8;  // segments per centreline group (bounding box)
 constexpr int kChunk = 32;  // points per spatial chunk (one warp-wide load)
 
 // One centreline vertex with its outgoing segment (i -> i+1), 64 B: an exact
-// projection touches one or two consecutive records.  abx/aby/len2 follow
-// point_segment_dist2's expressions (geometry.cpp:18-19); unused on the last vertex.
+// projection and its lane_hit touch only this record.  The differences
+// follow the reference's expressions: ab = b - a (geometry.cpp:18), s and
+// half-width increments (roads.cpp:130-139); unused on the last vertex.
 struct __align__(16) LaneVtx {
-    double x, y, abx, aby, len2, s, hw, pad;
+    double x, y, abx, aby, s, ds, hw, dhw;
 };
 
 // One per-row array the kernels prefetch into L2 at row start:

@@ -65,7 +65,7 @@ def main():
                     res["stats"].append(list(buf)[:len(NAMES)])
                 if ep == 1 and t in (5, 40, 80):
                     d = np.diff(cyc[:, :8].astype(np.int64), axis=1) % (1 << 32)  # [B][7]
-                    seq = [0, 8, 9, 10, 11, 12, 13, 1]
+                    seq = [0, 8, 9, 10, 11, 12, 13, 14, 15, 1]
                     sub = np.diff(cyc[:, seq].astype(np.int64), axis=1) % (1 << 32)
                     tot = d.sum(1)
                     slow = np.argsort(tot)[-max(1, B // 100):]
@@ -75,9 +75,9 @@ def main():
                         "mean": dict(zip(PH, d.mean(0).round(0).tolist())),
                         "slowest_1pct_mean": dict(zip(PH, d[slow].mean(0).round(0).tolist())),
                         "project_split": dict(zip(["load+flags", "bicycle+queries", "groups", "pass1", "pass2",
-                                                   "exact", "hit+rest"], sub.mean(0).round(0).tolist())),
+                                                   "exact", "argmin", "lane_hit", "rest"], sub.mean(0).round(0).tolist())),
                         "project_split_slowest_1pct": dict(zip(["load+flags", "bicycle+queries", "groups", "pass1",
-                                                                "pass2", "exact", "hit+rest"],
+                                                                "pass2", "exact", "argmin", "lane_hit", "rest"],
                                                                sub[slow].mean(0).round(0).tolist())),
                         "slowest_row": int(np.argmax(tot)), "slowest_row_phases": dict(zip(PH, d[np.argmax(tot)].tolist())),
                     }
