@@ -123,6 +123,7 @@ struct RowSh {
     Box eb;                // ego box of r
     double ex[4], ey[4];   // its corners (obb_distance reads them lane-indexed)
     double qx[5], qy[5];   // projection queries (position + inflated corners)
+    float4 hint;           // the row's top-k hint, loaded at row start
     double a_lat;          // step: v^2 tan(steer) / wheelbase (simcore.cpp:309-316)
     int boxes_ready;       // agent boxes at r.t + overlap flags are in agx/agy/agf
 };
@@ -635,8 +636,8 @@ __device__ __forceinline__ void chunk_bounds(float4 bb, double px, double py, do
 }
 
 // One warp pass over the listed chunks (32 points each, one per lane), loads
-// batched for memory-level parallelism; calls f(position, approx_key) for
-// every existing point.
+// batched for memory-level parallelism; calls f(position, approx_key, point)
+// for every existing point.
 template <class F>
 __device__ __forceinline__ void over_chunks(const PointSet& ps, const int* list, int nlist, float pxf, float pyf,
                                             F&& f) {
@@ -658,7 +659,7 @@ __device__ __forceinline__ void over_chunks(const PointSet& ps, const int* list,
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            if (j0 + u < nlist) f(pos[u], approx_key(pb[u], pxf, pyf));
+            if (j0 + u < nlist) f(pos[u], approx_key(pb[u], pxf, pyf), pb[u]);
         }
     }
 }
@@ -682,7 +683,7 @@ __device__ __forceinline__ void over_chunks(const PointSet& ps, const int* list,
 __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, bool use_r, double r2, float4 bbox,
                                       int cap, unsigned short* __restrict__ hist, int* __restrict__ cidx,
                                       double* __restrict__ ckey, int* __restrict__ cinfo, int* __restrict__ order,
-                                      float4* hint, int which) {
+                                      float4 hv, float4* hint, int which) {
     const int lane = lane_id();
     const int n = ps.n;
     if (n <= 0) return 0;
@@ -696,7 +697,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     // ---- 1. upper bound on the k-th exact key ----
     double T = INFINITY;
     if (hint != nullptr) {
-        const float4 h = *hint;
+        const float4 h = hv;  // loaded at row start (the road call writes only .z, the route call reads .w/.x/.y)
         const float kth = which == 0 ? h.z : h.w;
         if (isfinite(h.x) && isfinite(h.y) && kth >= 0.f && isfinite(kth)) {
             const double ddx = px - double(h.x), ddy = py - double(h.y);
@@ -755,12 +756,15 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     };
     auto compact_chunks = [&](float t) {
         int C = 0;
-        over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a) {
+        over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a, float2 p) {
             const bool take = pos >= 0 && a <= t;
             const unsigned bal = __ballot_sync(FULL, take);
             if (take) {
                 const int q = C + __popc(bal & lanemask_lt());
-                if (q < cap) cidx[q] = pos;
+                if (q < cap) {
+                    cidx[q] = pos;
+                    reinterpret_cast<float2*>(ckey)[q] = p;  // staged point; its exact key replaces it
+                }
             }
             C += __popc(bal);
         });
@@ -777,7 +781,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
         PSTAT(4 + 8 * which, 1);
         const int top = int(__float_as_uint(tc) >> 22);
         const int base = max(top - 31, 0);
-        over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a) {
+        over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a, float2) {
             if (pos >= 0 && a <= tc) hist[min(31, max(0, int(__float_as_uint(a) >> 22) - base)) * 32 + lane] += 1;
         });
         __syncwarp();
@@ -801,7 +805,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
                 const unsigned below = __shfl_sync(FULL, incl - cnt, kstar);
                 const float w2 = (hi2 - lo) * (1.0f / 32.0f);
                 const float inv2 = w2 > 0.f ? 1.0f / w2 : 0.f;
-                over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a) {
+                over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a, float2) {
                     if (pos >= 0 && a >= lo && a < hi2) hist[min(31, max(0, int((a - lo) * inv2))) * 32 + lane] += 1;
                 });
                 __syncwarp();
@@ -858,17 +862,30 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     unsigned* cntb = reinterpret_cast<unsigned*>(hist);  // NB2 u32 counters
     const double sc2 = double(NB2) / (double(tc) > 0.0 ? double(tc) : 1.0);
     int nvalid_local = 0;
-    for (int c = lane; c < C; c += 32) {
-        const int pos = cidx[c];
-        const float2 p = ps.xy[pos];
-        const double dx = double(p.x) - px, dy = double(p.y) - py;
-        const double e = dx * dx + dy * dy;
-        const bool ok = !use_r || e <= r2;
-        ckey[c] = ok ? e : INFINITY;
-        cinfo[c] = ps.oi[pos];
-        if (ok) {
-            atomicAdd(&cntb[min(NB2 - 1, int(e * sc2))], 1u);
-            ++nvalid_local;
+    for (int c0 = 0; c0 < C; c0 += 32 * 8) {
+        // reference indices of 8 candidates per lane in flight, then the exact
+        // keys from the points staged at compaction
+        int oiv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int c = c0 + 32 * u + lane;
+            oiv[u] = c < C ? ps.oi[cidx[c]] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int c = c0 + 32 * u + lane;
+            if (c < C) {
+                const float2 p = reinterpret_cast<const float2*>(ckey)[c];
+                const double dx = double(p.x) - px, dy = double(p.y) - py;
+                const double e = dx * dx + dy * dy;
+                const bool ok = !use_r || e <= r2;
+                ckey[c] = ok ? e : INFINITY;
+                cinfo[c] = oiv[u];
+                if (ok) {
+                    atomicAdd(&cntb[min(NB2 - 1, int(e * sc2))], 1u);
+                    ++nvalid_local;
+                }
+            }
         }
     }
     const int nvalid = int(__reduce_add_sync(FULL, unsigned(nvalid_local)));
@@ -1209,7 +1226,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const int* sel = w.order;
         const PointSet ps{pts, oidx, pk.road_cb + size_t(b) * pk.d.PC, n, (n + kChunk - 1) / kChunk};
         const int nsel = warp_topk(ps, Kr, r.x, r.y, true, R * R, pk.road_box[b], a.cand_cap, w.hist, w.cidx, w.ckey,
-                                   w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 0);
+                                   w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 0);
         ROW_MARK(b, 4);
         const uint8_t* kd = pk.road_kd + size_t(b) * pk.d.P;
         for (int k = lane; k < Kr; k += 32) {
@@ -1247,7 +1264,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const int* sel = w.order;
         const PointSet ps{pts, oidx, pk.route_cb + size_t(b) * pk.d.RC, n, (n + kChunk - 1) / kChunk};
         const int nsel = warp_topk(ps, Kl, r.x, r.y, false, 0.0, pk.route_box[b], a.cand_cap, w.hist, w.cidx, w.ckey,
-                                   w.cinfo, w.order, a.hint ? a.hint + b : nullptr, 1);
+                                   w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 1);
         ROW_MARK(b, 6);
         const uint8_t* fl = pk.route_fl + size_t(b) * pk.d.R;
         for (int k = lane; k < Kl; k += 32) {
@@ -1474,7 +1491,10 @@ __global__ void __launch_bounds__(kThreads, ZS_MIN_BLOCKS) k_step_observe(const 
     int b = blockIdx.x * wpb + warp_in_block();
     if (b < a.pk.d.B) prefetch_row<STEP, OBS>(a, b, a.in.t[b] + (STEP ? 1 : 0));
     for (; b < a.pk.d.B; b += stride) {
-        if (lane_id() == 0) w.rs->r0 = load_row(a.in, b);
+        if (lane_id() == 0) {
+            w.rs->r0 = load_row(a.in, b);
+            if (OBS && a.hint) w.rs->hint = a.hint[b];
+        }
         __syncwarp();
         // the warp's next row: its static data streams into L2 while this row computes
         if (b + stride < a.pk.d.B) prefetch_row<STEP, OBS>(a, b + stride, w.rs->r0.t + (STEP ? 1 : 0));
