@@ -449,6 +449,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     const size_t nln = size_t(B) * d.L * d.C;
     size_t o_lv = pb.reserve<LaneVtx>(nln);
     size_t o_lgb = pb.reserve<float>(size_t(B) * d.L * d.GC * 4);
+    size_t o_lhwb = pb.reserve<float>(size_t(B) * d.L * 2);
     size_t o_lf4 = pb.reserve<float>(nln * 4), o_lorg = pb.reserve<double>(size_t(B) * 2),
            o_lfe = pb.reserve<float>(size_t(B));
     size_t o_ln = pb.reserve<int32_t>(size_t(B) * d.L), o_lid = pb.reserve<uint32_t>(size_t(B) * d.L);
@@ -569,6 +570,13 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
                 gb[2] = std::nextafter(float(x1), 3e38f);
                 gb[3] = std::nextafter(float(y1), 3e38f);
             }
+            {
+                double h0 = 1e300, h1 = -1e300;
+                for (double h : lf.hw) h0 = std::min(h0, h), h1 = std::max(h1, h);
+                float* hb = pb.at<float>(o_lhwb) + 2 * (size_t(b) * d.L + l);
+                hb[0] = lf.hw.empty() ? 0.f : std::nextafter(float(h0), -3e38f);
+                hb[1] = lf.hw.empty() ? 0.f : std::nextafter(float(h1), 3e38f);
+            }
             pb.at<int32_t>(o_ln)[size_t(b) * d.L + l] = int32_t(lf.x.size());
             pb.at<uint32_t>(o_lid)[size_t(b) * d.L + l] = lf.lane_id;
             for (size_t i = 0; i < lf.x.size(); ++i) {
@@ -652,6 +660,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.ln_v = reinterpret_cast<const LaneVtx*>(D + o_lv);
     pk.ln_f4 = reinterpret_cast<const float4*>(D + o_lf4);
     pk.ln_gb = reinterpret_cast<const float4*>(D + o_lgb);
+    pk.ln_hwb = reinterpret_cast<const float2*>(D + o_lhwb);
     pk.ln_org = reinterpret_cast<const double2*>(D + o_lorg);
     pk.ln_fe = reinterpret_cast<const float*>(D + o_lfe);
     pk.road_box = reinterpret_cast<const float4*>(D + o_rbox);

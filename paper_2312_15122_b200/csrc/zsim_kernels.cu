@@ -441,6 +441,12 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
                 for (int q = 1; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f, inv));
             }
         }
+        // A corner only needs its in-corridor bit (roads.cpp:202-208): when its
+        // fp32 distance to this route lane is below the lane's smallest
+        // half-width (or above the largest) by more than delta, the verdict is
+        // certain and no exact evaluation is needed for it.
+        const float2 hwb = lane_ok ? pk.ln_hwb[lrow] : make_float2(0.f, 0.f);
+        unsigned cin = 0;  // octet-uniform bit q: corner q certainly inside this lane's corridor
         float thr[NQU];
 #pragma unroll
         for (int q = 0; q < NQU; ++q) {
@@ -449,6 +455,12 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
             const float delta = 0x1p-18f * (fe + fabsf(qxf[q]) + fabsf(qyf[q]) + dm) + 1e-30f;
             const float r = dm + 2.f * delta;
             thr[q] = r * r * (1.f + 0x1p-20f);
+            if (q > 0) {
+                const bool in = dm + delta < hwb.x;
+                const bool out = dm - delta > hwb.y;
+                cin |= in ? 1u << q : 0u;
+                if (in || out) thr[q] = -1.f;
+            }
         }
         if (l0 == 0) ROW_MARK(b, 12);
         // ---- 3. exact fp64 distances of the candidates ----
@@ -497,9 +509,10 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
             if (hq == q) hi_ = v;
         }
         if (l0 == 0) ROW_MARK(b, 14);
-        bool ok = false;
+        const unsigned cin_k = __shfl_sync(FULL, cin, hk * 8);
+        bool ok = hq > 0 && hq < NQU && ((cin_k >> hq) & 1u);
         double hs = 0.0, hd = 0.0;
-        if (hq < NQU && l0 + hk < nl && hi_ != INT_MAX) {
+        if (!ok && hq < NQU && l0 + hk < nl && hi_ != INT_MAX) {
             const double2* V = reinterpret_cast<const double2*>(pk.ln_v + (size_t(b) * L + l0 + hk) * C + hi_);
             const double2 a0 = V[0], a1 = V[1], a2 = V[2], a3 = V[3];
             double t;

@@ -99,6 +99,7 @@ struct DevPack {
     const LaneVtx* ln_v;    // [B][L][C] exact centreline records
     const float4* ln_f4;    // [B][L][C] fp32 screening copy: (a - origin, b - a) per segment
     const float4* ln_gb;    // [B][L][GC] group boxes (origin-relative, rounded outward)
+    const float2* ln_hwb;   // [B][L] (min, max) centreline half-width, rounded outward
     const double2* ln_org;  // [B] origin of the fp32 copy
     const float* ln_fe;     // [B] max |a - origin|_1 over vertices + max segment length (error scale)
     const int32_t* ln_n;
