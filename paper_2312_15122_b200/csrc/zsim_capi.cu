@@ -449,14 +449,13 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     const size_t nln = size_t(B) * d.L * d.C;
     size_t o_lv = pb.reserve<LaneVtx>(nln);
     size_t o_lgb = pb.reserve<float>(size_t(B) * d.L * d.GC * 4);
-    size_t o_lhwb = pb.reserve<float>(size_t(B) * d.L * 2);
     size_t o_lf4 = pb.reserve<float>(nln * 4), o_lorg = pb.reserve<double>(size_t(B) * 2),
            o_lfe = pb.reserve<float>(size_t(B));
-    size_t o_ln = pb.reserve<int32_t>(size_t(B) * d.L), o_lid = pb.reserve<uint32_t>(size_t(B) * d.L);
+    size_t o_lninfo = pb.reserve<LaneInfo>(size_t(B) * d.L);
     size_t o_rbox = pb.reserve<float>(size_t(B) * 4), o_tbox = pb.reserve<float>(size_t(B) * 4);
     size_t o_lts = pb.reserve<double>(size_t(B) * d.NL), o_ltst = pb.reserve<uint8_t>(size_t(B) * d.NL * d.T);
     size_t o_sts = pb.reserve<double>(size_t(B) * d.NS);
-    constexpr int kPf = 12;
+    constexpr int kPf = 13;
     size_t o_pf = pb.reserve<PfDesc>(kPf);
     pb.host.assign(pb.cursor, 0);
 
@@ -573,12 +572,12 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
             {
                 double h0 = 1e300, h1 = -1e300;
                 for (double h : lf.hw) h0 = std::min(h0, h), h1 = std::max(h1, h);
-                float* hb = pb.at<float>(o_lhwb) + 2 * (size_t(b) * d.L + l);
-                hb[0] = lf.hw.empty() ? 0.f : std::nextafter(float(h0), -3e38f);
-                hb[1] = lf.hw.empty() ? 0.f : std::nextafter(float(h1), 3e38f);
+                LaneInfo& li = pb.at<LaneInfo>(o_lninfo)[size_t(b) * d.L + l];
+                li.n = int32_t(lf.x.size());
+                li.id = lf.lane_id;
+                li.hw_min = lf.hw.empty() ? 0.f : std::nextafter(float(h0), -3e38f);
+                li.hw_max = lf.hw.empty() ? 0.f : std::nextafter(float(h1), 3e38f);
             }
-            pb.at<int32_t>(o_ln)[size_t(b) * d.L + l] = int32_t(lf.x.size());
-            pb.at<uint32_t>(o_lid)[size_t(b) * d.L + l] = lf.lane_id;
             for (size_t i = 0; i < lf.x.size(); ++i) {
                 size_t k = (size_t(b) * d.L + l) * d.C + i;
                 LaneVtx& v = pb.at<LaneVtx>(o_lv)[k];
@@ -660,13 +659,11 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.ln_v = reinterpret_cast<const LaneVtx*>(D + o_lv);
     pk.ln_f4 = reinterpret_cast<const float4*>(D + o_lf4);
     pk.ln_gb = reinterpret_cast<const float4*>(D + o_lgb);
-    pk.ln_hwb = reinterpret_cast<const float2*>(D + o_lhwb);
     pk.ln_org = reinterpret_cast<const double2*>(D + o_lorg);
     pk.ln_fe = reinterpret_cast<const float*>(D + o_lfe);
     pk.road_box = reinterpret_cast<const float4*>(D + o_rbox);
     pk.route_box = reinterpret_cast<const float4*>(D + o_tbox);
-    pk.ln_n = reinterpret_cast<const int32_t*>(D + o_ln);
-    pk.ln_id = reinterpret_cast<const uint32_t*>(D + o_lid);
+    pk.ln_info = reinterpret_cast<const LaneInfo*>(D + o_lninfo);
     pk.lt_s = reinterpret_cast<const double*>(D + o_lts);
     pk.lt_state = D + o_ltst;
     pk.st_s = reinterpret_cast<const double*>(D + o_sts);
@@ -676,6 +673,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
         const PfDesc tab[kPf] = {
             {pk.ln_f4, LC * 16, 0, LC * 16, 1},
             {pk.ln_gb, uint32_t(d.L) * uint32_t(d.GC) * 16, 0, uint32_t(d.L) * uint32_t(d.GC) * 16, 1},
+            {pk.ln_info, uint32_t(d.L) * 16, 0, uint32_t(d.L) * 16, 0},
             {pk.road_cb, uint32_t(d.PC) * 16, 0, uint32_t(d.PC) * 16, 2},
             {pk.route_cb, uint32_t(d.RC) * 16, 0, uint32_t(d.RC) * 16, 2},
             {pk.ag_x, TA * 4, A * 4, A * 4, 0},

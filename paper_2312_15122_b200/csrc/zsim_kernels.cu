@@ -354,7 +354,8 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
         const bool lane_ok = l < nl;
         const size_t lrow = size_t(b) * L + (lane_ok ? l : 0);
         const size_t base = lrow * C;
-        const int nseg = lane_ok ? pk.ln_n[lrow] - 1 : 0;
+        const LaneInfo li = lane_ok ? pk.ln_info[lrow] : LaneInfo{1, 0u, 0.f, 0.f};
+        const int nseg = li.n - 1;
         const float4* F = pk.ln_f4 + base;
         // ---- 0. 8-segment groups that can hold q0's minimum or a near segment ----
         // Group boxes (origin-relative, rounded outward) bound the exact
@@ -445,7 +446,7 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
         // fp32 distance to this route lane is below the lane's smallest
         // half-width (or above the largest) by more than delta, the verdict is
         // certain and no exact evaluation is needed for it.
-        const float2 hwb = lane_ok ? pk.ln_hwb[lrow] : make_float2(0.f, 0.f);
+        const float2 hwb = make_float2(li.hw_min, li.hw_max);
         unsigned cin = 0;  // octet-uniform bit q: corner q certainly inside this lane's corridor
         float thr[NQU];
 #pragma unroll
@@ -500,7 +501,6 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
         }
         if (l0 == 0) ROW_MARK(b, 13);
         // ---- per-octet exact argmin, then s / signed d / half-width per (query, route lane) ----
-        const uint32_t my_id = lane < 4 && l0 + lane < nl ? pk.ln_id[size_t(b) * L + l0 + lane] : 0u;
         int hi_ = INT_MAX;
 #pragma unroll
         for (int q = 0; q < NQU; ++q) {
@@ -539,7 +539,7 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
             const double s0 = __shfl_sync(FULL, hs, k), d0 = __shfl_sync(FULL, hd, k);
             const int w0 = __shfl_sync(FULL, hi_, k);
             if (w0 == INT_MAX) continue;
-            const uint32_t id = __shfl_sync(FULL, my_id, k);
+            const uint32_t id = __shfl_sync(FULL, li.id, k * 8);
             if (!have || fabs(d0) < best_abs || (fabs(d0) == best_abs && id < best_id)) {
                 have = true;
                 best_abs = fabs(d0);

@@ -41,6 +41,14 @@ constexpr int kChunk = 32;  // points per spatial chunk (one warp-wide load)
 // projection and its lane_hit touch only this record.  The differences
 // follow the reference's expressions: ab = b - a (geometry.cpp:18), s and
 // half-width increments (roads.cpp:130-139); unused on the last vertex.
+// Per route lane: vertex count, lane_id (the projection tie-break,
+// roads.cpp:147-166) and the (min, max) centreline half-width rounded outward.
+struct __align__(16) LaneInfo {
+    int32_t n;
+    uint32_t id;
+    float hw_min, hw_max;
+};
+
 struct __align__(16) LaneVtx {
     double x, y, abx, aby, s, ds, hw, dhw;
 };
@@ -99,11 +107,9 @@ struct DevPack {
     const LaneVtx* ln_v;    // [B][L][C] exact centreline records
     const float4* ln_f4;    // [B][L][C] fp32 screening copy: (a - origin, b - a) per segment
     const float4* ln_gb;    // [B][L][GC] group boxes (origin-relative, rounded outward)
-    const float2* ln_hwb;   // [B][L] (min, max) centreline half-width, rounded outward
     const double2* ln_org;  // [B] origin of the fp32 copy
     const float* ln_fe;     // [B] max |a - origin|_1 over vertices + max segment length (error scale)
-    const int32_t* ln_n;
-    const uint32_t* ln_id;
+    const LaneInfo* ln_info;  // [B][L] vertex count, lane_id, half-width bounds
     const float4* road_box;   // [B] (min x, min y, max x, max y) of the road points
     const float4* route_box;  // [B] same for the route border points
     const PfDesc* pf;  // prefetch table
