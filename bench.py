@@ -146,10 +146,17 @@ def cpu_baseline(cfg_name: str, seed: int) -> dict | None:
     A, S = z.random_actions(EPISODE, rows, seed=123)
     threads = os.cpu_count() or 1
     secs = refpy.bench(zsim, rows, 92, z.SimConfig(disable_dones=True), threads, 0, EPISODE, A, S)
+    # single-thread leg on a C0-sized sample (64 scenarios), SURVEY 8d
+    r1 = min(64, rows)
+    z1 = z.stress_scenarios(z.StressConfig(count=r1, agents=c["agents"], road_points=c["road_points"]), seed)
+    A1, S1 = z.random_actions(EPISODE, r1, seed=123)
+    secs1 = refpy.bench(z1, r1, 92, z.SimConfig(disable_dones=True), 1, 0, EPISODE, A1, S1)
     return {"value": rows * c["agents"] * EPISODE / secs, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"{rows} of the {c['scenarios']} {cfg_name} scenarios x {EPISODE} steps (observe+step), "
                       f"{threads} per-thread Env shards, oracle/_ref (-O2 -ffp-contract=off)",
-            "seconds": secs}
+            "seconds": secs,
+            "value_1thread": r1 * c["agents"] * EPISODE / secs1,
+            "sample_1thread": f"{r1} scenarios x {EPISODE} steps on 1 thread ({secs1:.2f} s)"}
 
 
 def run_reference(args) -> None:
@@ -230,29 +237,70 @@ def run_ours(args) -> None:
     for _ in range(args.warmup):
         cur, nxt = one_step(cur, nxt)
     env.check_errors(stream)
+
+    # Kernel timing (roofline): one eager episode, CUDA events around every fused launch.
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(EPISODE)]
+    k_state["k"] = 0
+    for i in range(EPISODE):
+        cur, nxt = one_step(cur, nxt, kev[i])
+    torch.cuda.synchronize()
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+
+    # Timed region: whole rollouts (reset + 91 fused steps) replayed from a CUDA graph
+    # (SURVEY 8d); a step count that is not a whole number of rollouts runs eagerly.
+    use_graph = args.steps % EPISODE == 0 and not args.no_graph
+    graph = None
+    if use_graph:
+        gstream = torch.cuda.Stream()
+        gstream.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gstream, capture_error_mode="relaxed"):
+            g_cur, g_nxt = s0, s1
+            env.reset_device(42, g_cur, gstream)
+            for t in range(EPISODE):
+                env.step_observe_device(g_cur, dA[t].data_ptr(), dS[t].data_ptr(), g_nxt, so, ob, gstream)
+                g_cur, g_nxt = g_nxt, g_cur
+        final_state = g_cur
+        stream = torch.cuda.current_stream()  # CUDAGraph.replay() launches on the current stream
+        graph.replay()  # warm replay
+        torch.cuda.synchronize()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)  # let the sampler start before the timed region
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     resets = 0
+    rollout_ms = []
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     gc.collect()
     gc.disable()  # a collector pause in the launch loop would idle the GPU inside the timed region
-    start.record(stream)
-    for i in range(args.steps):
-        resets += 1 if k_state["k"] % EPISODE == 0 else 0
-        cur, nxt = one_step(cur, nxt, ev[i])
-    end.record(stream)
+    if use_graph:
+        n_roll = args.steps // EPISODE
+        rev = [torch.cuda.Event(enable_timing=True) for _ in range(n_roll + 1)]
+        start.record(stream)
+        rev[0].record(stream)
+        for i in range(n_roll):
+            graph.replay()
+            rev[i + 1].record(stream)
+        end.record(stream)
+        resets = n_roll
+        cur = final_state
+    else:
+        k_state["k"] = 0
+        start.record(stream)
+        for i in range(args.steps):
+            resets += 1 if k_state["k"] % EPISODE == 0 else 0
+            cur, nxt = one_step(cur, nxt)
+        end.record(stream)
     torch.cuda.synchronize()
     gc.enable()
     clk = clocks.stop()
+    if use_graph:
+        rollout_ms = [rev[i].elapsed_time(rev[i + 1]) for i in range(n_roll)]
     if dist:
         dist.barrier()
     elapsed_ms = start.elapsed_time(end)
-    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     env.check_errors(stream)
     t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
     env.episode_stats(cur, stats.data_ptr(), stream)
@@ -325,6 +373,11 @@ def run_ours(args) -> None:
                      "kernel": "k_step_observe<true,true>", "kernel_ms": kern_ms, "peak_source": peak_src},
         "gpu_launches": args.steps + resets,
         "scenario_steps_per_s": B * args.steps * world / (elapsed_ms / 1e3),
+        "controlled_agent_steps_per_s": B * args.steps * world / (elapsed_ms / 1e3),
+        "timing": {"mode": "cuda-graph rollouts (reset + 91 fused steps)" if use_graph else "eager launches",
+                   "rollout_ms_median": float(np.median(rollout_ms)) if rollout_ms else None,
+                   "rollout_ms_best": float(np.min(rollout_ms)) if rollout_ms else None,
+                   "kernel_ms_source": "one eager episode, CUDA events around each fused launch"},
         "episode_stats": stats.cpu().tolist(),
     }
     if e2e:
@@ -349,6 +402,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph rollouts")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
