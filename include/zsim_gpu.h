@@ -39,7 +39,7 @@ extern "C" {
 #define ZSIM_API
 #endif
 
-#define ZSIM_ABI_VERSION 1
+#define ZSIM_ABI_VERSION 2
 
 enum zsim_status {
     ZSIM_OK = 0,
@@ -141,6 +141,8 @@ typedef struct zsim_env_info {
     int32_t cap_steps, cap_agents, cap_road, cap_route, cap_lanes, cap_vertices, cap_lights, cap_stops;
     int32_t device;
     uint64_t static_bytes; /* device bytes of the immutable scenario pack */
+    int32_t scenarios;     /* scenarios staged (== batch unless controlled) */
+    int32_t controlled;    /* 1: rows are controlled actors (zsim_env_create_controlled) */
 } zsim_env_info;
 
 typedef struct zsim_env zsim_env;
@@ -163,6 +165,30 @@ ZSIM_API int zsim_sim_config_defaults(zsim_sim_config* cfg);
 ZSIM_API int zsim_env_create(const uint8_t* zsim_file, size_t nbytes, const int64_t* indices, int32_t n_indices,
                              int32_t horizon, const zsim_sim_config* cfg, const double* accel_bins, int32_t n_accel,
                              const double* steer_bins, int32_t n_steer, int32_t device, zsim_env** out);
+/* "All agents controlled" (the reference has no such
+ * mode, its ego-only path is simcore.cpp:300-304).  Same arguments as
+ * zsim_env_create; the env has one row per controllable actor of every
+ * scenario (actor 0 = the logged ego, actor k = agent k-1; an agent is
+ * controllable when valid at every logged step), scenario-major.  Row
+ * (s, j) is exactly a reference Env row over the scenario that
+ * zsim_controlled_expand writes for it: ego log = actor j's log, goal 4 m past
+ * its last logged point along its last heading, every other actor
+ * log-replayed in actor order (the logged ego as an agent with the SimConfig
+ * ego box).  Roadgraph, route corridor, lights and stop lines are staged once
+ * per scenario and shared by its rows. */
+ZSIM_API int zsim_env_create_controlled(const uint8_t* zsim_file, size_t nbytes, const int64_t* indices,
+                                        int32_t n_indices, int32_t horizon, const zsim_sim_config* cfg,
+                                        const double* accel_bins, int32_t n_accel, const double* steer_bins,
+                                        int32_t n_steer, int32_t device, zsim_env** out);
+/* Row table: scenario index (into the staged scenarios) and controlled actor
+ * (-1 in ego mode) of each of the env's `batch` rows; either may be NULL. */
+ZSIM_API int zsim_env_get_rows(const zsim_env* env, int32_t* scenario, int32_t* actor);
+/* The per-row scenarios of zsim_env_create_controlled as a ZSIM container
+ * image (row order), for running the reference Env on exactly those rows.
+ * Free with zsim_free_buffer. */
+ZSIM_API int zsim_controlled_expand(const uint8_t* zsim_file, size_t nbytes, const int64_t* indices,
+                                    int32_t n_indices, const zsim_sim_config* cfg, uint8_t** out_buf,
+                                    size_t* out_len);
 ZSIM_API int zsim_env_destroy(zsim_env* env);
 ZSIM_API int zsim_env_get_info(const zsim_env* env, zsim_env_info* out);
 /* Env::goal_s / initial_s / logged_progress (simcore.hpp:207-209): host arrays of B doubles (any may be NULL). */
@@ -265,7 +291,7 @@ typedef struct zsim_stress_config {
     double speed_limit;     /* 10 m/s */
     double lane_width;      /* 3.5 m */
     int32_t first_index;    /* global index of the first scenario (shards of one global set) */
-    int32_t reserved;
+    int32_t flags;          /* bit 0: C2 actors -- every agent valid at all steps, same-direction route lanes */
 } zsim_stress_config;
 
 ZSIM_API int zsim_stress_config_defaults(zsim_stress_config* cfg);

@@ -7,8 +7,9 @@ and fails loudly when it is missing -- there is no CPU fallback.
 """
 from ._abi import ZsimError, lib  # noqa: F401
 from .env import (DONE_REASONS, DeviceObs, DeviceState, DeviceStepOut, Env, ObservationBatch,  # noqa: F401
-                  SimConfig, SimStateBatch, StepOut, StressConfig, event_bit, random_actions, stress_scenarios)
+                  STRESS_C2, SimConfig, SimStateBatch, StepOut, StressConfig, controlled_expand, event_bit,
+                  random_actions, stress_scenarios)
 
 __all__ = ["Env", "SimConfig", "SimStateBatch", "StepOut", "ObservationBatch", "DeviceState", "DeviceStepOut",
            "DeviceObs", "StressConfig", "stress_scenarios", "random_actions", "ZsimError", "DONE_REASONS",
-           "event_bit", "lib"]
+           "event_bit", "lib", "controlled_expand", "STRESS_C2"]

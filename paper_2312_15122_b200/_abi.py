@@ -58,7 +58,7 @@ class EnvInfo(C.Structure):
         ("num_steer", C.c_int32), ("cap_steps", C.c_int32), ("cap_agents", C.c_int32), ("cap_road", C.c_int32),
         ("cap_route", C.c_int32), ("cap_lanes", C.c_int32), ("cap_vertices", C.c_int32),
         ("cap_lights", C.c_int32), ("cap_stops", C.c_int32), ("device", C.c_int32),
-        ("static_bytes", C.c_uint64),
+        ("static_bytes", C.c_uint64), ("scenarios", C.c_int32), ("controlled", C.c_int32),
     ]
 
 
@@ -66,7 +66,7 @@ class StressConfigC(C.Structure):
     _fields_ = [("count", C.c_int32), ("num_steps", C.c_int32), ("agents", C.c_int32),
                 ("road_points", C.c_int32), ("lanes", C.c_int32), ("lane_vertices", C.c_int32),
                 ("dt", C.c_double), ("speed_limit", C.c_double), ("lane_width", C.c_double),
-                ("first_index", C.c_int32), ("reserved", C.c_int32)]
+                ("first_index", C.c_int32), ("flags", C.c_int32)]
 
 
 # name -> (restype, argtypes); every symbol include/zsim_gpu.h declares.
@@ -78,6 +78,12 @@ SIGNATURES = {
     "zsim_env_create": (C.c_int, [_P, C.c_size_t, C.POINTER(C.c_int64), C.c_int32, C.c_int32,
                                   C.POINTER(SimConfigC), c_double_p, C.c_int32, c_double_p, C.c_int32,
                                   C.c_int32, C.POINTER(_P)]),
+    "zsim_env_create_controlled": (C.c_int, [_P, C.c_size_t, C.POINTER(C.c_int64), C.c_int32, C.c_int32,
+                                             C.POINTER(SimConfigC), c_double_p, C.c_int32, c_double_p, C.c_int32,
+                                             C.c_int32, C.POINTER(_P)]),
+    "zsim_env_get_rows": (C.c_int, [_P, c_int32_p, c_int32_p]),
+    "zsim_controlled_expand": (C.c_int, [_P, C.c_size_t, C.POINTER(C.c_int64), C.c_int32, C.POINTER(SimConfigC),
+                                         C.POINTER(_P), C.POINTER(C.c_size_t)]),
     "zsim_env_destroy": (C.c_int, [_P]),
     "zsim_env_get_info": (C.c_int, [_P, C.POINTER(EnvInfo)]),
     "zsim_env_get_scalars": (C.c_int, [_P, c_double_p, c_double_p, c_double_p]),

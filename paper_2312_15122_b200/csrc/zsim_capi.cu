@@ -167,6 +167,8 @@ struct zsim_env {
     int zero_accel = 0, zero_steer = 0;
     std::vector<double> accel_bins, steer_bins;
     std::vector<double> goal_s, initial_s, logged_progress;
+    std::vector<int32_t> row_scen, row_actor;  // row -> (scenario, controlled actor; -1 = ego mode)
+    int n_scen = 0;
     zsim_sim_config cfg{};
     StateLayout sl{};
     StepoutLayout sol{};
@@ -305,12 +307,6 @@ zs::DevCfg make_dev_cfg(const zsim_sim_config& c, const std::vector<double>& ab,
     return d;
 }
 
-int next_pow2(int v) {
-    int p = 1;
-    while (p < v) p <<= 1;
-    return p;
-}
-
 // Spatial order of a point set: stable sort by the Morton code of (x, y)
 // quantised over the set's bounding box.  Chunks of 32 consecutive points then
 // cover compact regions; the reference index rides along for tie-breaks.
@@ -370,10 +366,14 @@ void write_points(unsigned char* host, size_t o_xy, size_t o_attr, size_t o_oi, 
 }
 
 // Env::Env (simcore.cpp:203-233) over make_batch (scenario_io.cpp:404-437).
-void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon) {
+// Stages the device pack.  Ego mode (controlled = false): one row per
+// scenario, as Env::Env.  Controlled mode: one row per
+// controllable actor of every scenario (zsim_scenario.hpp, controlled_scene);
+// scenario data is stored once and rows index it (row_scen / row_actor).
+void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon, bool controlled) {
     using namespace zs;
     if (scenes.empty()) raise(Err::invalid_argument, "make_batch: empty scenario list");
-    const int B = int(scenes.size());
+    const int S = int(scenes.size());
     const double dt = scenes[0].dt;
     for (const auto& s : scenes) {
         if (int(s.num_steps) > horizon) {
@@ -383,10 +383,9 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
         if (s.dt != dt) raise(Err::invalid_argument, "mixed dt within batch");
     }
     // Route contexts and route border points (host fp64, reference op order).
-    std::vector<RouteCtx> ctx(static_cast<size_t>(B));
-    std::vector<std::vector<RoutePt>> rpts(static_cast<size_t>(B));
+    std::vector<RouteCtx> ctx(static_cast<size_t>(S));
+    std::vector<std::vector<RoutePt>> rpts(static_cast<size_t>(S));
     PackDims d{};
-    d.B = B;
     d.T = 1;
     d.A = 1;
     d.P = 1;
@@ -395,12 +394,12 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     d.C = 2;
     d.NL = 1;
     d.NS = 1;
-    for (int b = 0; b < B; ++b) {
+    for (int b = 0; b < S; ++b) {
         const Scene& s = scenes[size_t(b)];
         ctx[size_t(b)] = build_context(s);
         rpts[size_t(b)] = build_route_points(s);
         d.T = std::max(d.T, int(s.num_steps));
-        d.A = std::max(d.A, int(s.agents.size()));
+        d.A = std::max(d.A, controlled ? num_actors(s) : int(s.agents.size()));
         size_t np = 0;
         for (const auto& f : s.features) np += f.xy.size() / 2;
         d.P = std::max(d.P, int(np));
@@ -422,6 +421,20 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
             if (s.ego_x.empty()) raise(Err::invalid_argument, "scenario `" + s.id + "`: empty ego log");
         }
     }
+    // rows: (scenario, controlled actor); actor -1 = the scenario's own ego (ego mode)
+    std::vector<std::pair<int, int>> rows;
+    for (int b = 0; b < S; ++b) {
+        if (!controlled) {
+            rows.emplace_back(b, -1);
+            continue;
+        }
+        for (int j = 0; j < num_actors(scenes[size_t(b)]); ++j)
+            if (actor_controllable(scenes[size_t(b)], j)) rows.emplace_back(b, j);
+    }
+    const int B = int(rows.size());
+    d.B = B;
+    d.S = S;
+    const EgoBoxDims ebd{env->cfg.ego_length, env->cfg.ego_width, env->cfg.ego_center_offset};
     d.GC = std::max(1, (d.C - 1 + kSegGroup - 1) / kSegGroup);
     d.PC = (d.P + kChunk - 1) / kChunk;
     d.RC = (d.R + kChunk - 1) / kChunk;
@@ -431,30 +444,34 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     }
 
     PackBuilder pb;
-    size_t o_num_steps = pb.reserve<int32_t>(B), o_na = pb.reserve<int32_t>(B), o_nr = pb.reserve<int32_t>(B),
-           o_nrt = pb.reserve<int32_t>(B), o_nl = pb.reserve<int32_t>(B), o_nlt = pb.reserve<int32_t>(B),
-           o_ns = pb.reserve<int32_t>(B), o_soff = pb.reserve<int32_t>(B);
-    size_t o_sl = pb.reserve<float>(B), o_gx = pb.reserve<float>(B), o_gy = pb.reserve<float>(B);
-    size_t o_gs = pb.reserve<double>(B), o_rl = pb.reserve<double>(B);
-    size_t o_ix = pb.reserve<double>(B), o_iy = pb.reserve<double>(B), o_ih = pb.reserve<double>(B),
-           o_iv = pb.reserve<double>(B), o_ist = pb.reserve<double>(B);
-    const size_t nag = size_t(B) * d.T * d.A;
+    // scenario-level arrays [S...]
+    size_t o_num_steps = pb.reserve<int32_t>(S), o_na = pb.reserve<int32_t>(S), o_nr = pb.reserve<int32_t>(S),
+           o_nrt = pb.reserve<int32_t>(S), o_nl = pb.reserve<int32_t>(S), o_nlt = pb.reserve<int32_t>(S),
+           o_ns = pb.reserve<int32_t>(S);
+    size_t o_sl = pb.reserve<float>(S), o_rl = pb.reserve<double>(S);
+    const size_t nag = size_t(S) * d.T * d.A;
     size_t o_agx = pb.reserve<float>(nag), o_agy = pb.reserve<float>(nag), o_agh = pb.reserve<float>(nag),
            o_ags = pb.reserve<float>(nag), o_agv = pb.reserve<uint8_t>(nag);
-    size_t o_agl = pb.reserve<float>(size_t(B) * d.A), o_agw = pb.reserve<float>(size_t(B) * d.A);
-    size_t o_rxy = pb.reserve<float>(size_t(B) * d.P * 2), o_rkd = pb.reserve<uint8_t>(size_t(B) * d.P);
-    size_t o_roi = pb.reserve<int32_t>(size_t(B) * d.P), o_rcb = pb.reserve<float>(size_t(B) * d.PC * 4);
-    size_t o_txy = pb.reserve<float>(size_t(B) * d.R * 2), o_tfl = pb.reserve<uint8_t>(size_t(B) * d.R);
-    size_t o_toi = pb.reserve<int32_t>(size_t(B) * d.R), o_tcb = pb.reserve<float>(size_t(B) * d.RC * 4);
-    const size_t nln = size_t(B) * d.L * d.C;
+    size_t o_agl = pb.reserve<float>(size_t(S) * d.A), o_agw = pb.reserve<float>(size_t(S) * d.A);
+    size_t o_rxy = pb.reserve<float>(size_t(S) * d.P * 2), o_rkd = pb.reserve<uint8_t>(size_t(S) * d.P);
+    size_t o_roi = pb.reserve<int32_t>(size_t(S) * d.P), o_rcb = pb.reserve<float>(size_t(S) * d.PC * 4);
+    size_t o_txy = pb.reserve<float>(size_t(S) * d.R * 2), o_tfl = pb.reserve<uint8_t>(size_t(S) * d.R);
+    size_t o_toi = pb.reserve<int32_t>(size_t(S) * d.R), o_tcb = pb.reserve<float>(size_t(S) * d.RC * 4);
+    const size_t nln = size_t(S) * d.L * d.C;
     size_t o_lv = pb.reserve<LaneVtx>(nln);
-    size_t o_lgb = pb.reserve<float>(size_t(B) * d.L * d.GC * 4);
-    size_t o_lf4 = pb.reserve<float>(nln * 4), o_lorg = pb.reserve<double>(size_t(B) * 2),
-           o_lfe = pb.reserve<float>(size_t(B));
-    size_t o_lninfo = pb.reserve<LaneInfo>(size_t(B) * d.L);
-    size_t o_rbox = pb.reserve<float>(size_t(B) * 4), o_tbox = pb.reserve<float>(size_t(B) * 4);
-    size_t o_lts = pb.reserve<double>(size_t(B) * d.NL), o_ltst = pb.reserve<uint8_t>(size_t(B) * d.NL * d.T);
-    size_t o_sts = pb.reserve<double>(size_t(B) * d.NS);
+    size_t o_lgb = pb.reserve<float>(size_t(S) * d.L * d.GC * 4);
+    size_t o_lf4 = pb.reserve<float>(nln * 4), o_lorg = pb.reserve<double>(size_t(S) * 2),
+           o_lfe = pb.reserve<float>(size_t(S));
+    size_t o_lninfo = pb.reserve<LaneInfo>(size_t(S) * d.L);
+    size_t o_rbox = pb.reserve<float>(size_t(S) * 4), o_tbox = pb.reserve<float>(size_t(S) * 4);
+    size_t o_lts = pb.reserve<double>(size_t(S) * d.NL), o_ltst = pb.reserve<uint8_t>(size_t(S) * d.NL * d.T);
+    size_t o_sts = pb.reserve<double>(size_t(S) * d.NS);
+    // row-level arrays [B]
+    size_t o_soff = pb.reserve<int32_t>(B), o_gx = pb.reserve<float>(B), o_gy = pb.reserve<float>(B);
+    size_t o_gs = pb.reserve<double>(B);
+    size_t o_ix = pb.reserve<double>(B), o_iy = pb.reserve<double>(B), o_ih = pb.reserve<double>(B),
+           o_iv = pb.reserve<double>(B), o_ist = pb.reserve<double>(B);
+    size_t o_rsc = pb.reserve<int32_t>(B), o_rac = pb.reserve<int32_t>(B);
     constexpr int kPf = 13;
     size_t o_pf = pb.reserve<PfDesc>(kPf);
     pb.host.assign(pb.cursor, 0);
@@ -462,13 +479,43 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     env->goal_s.assign(size_t(B), 0.0);
     env->initial_s.assign(size_t(B), 0.0);
     env->logged_progress.assign(size_t(B), 0.0);
+    env->row_scen.assign(size_t(B), 0);
+    env->row_actor.assign(size_t(B), -1);
     int total_stop = 0;
-    for (int b = 0; b < B; ++b) {
+    for (int r = 0; r < B; ++r) {
+        // row-level: the controlled actor's initial state and goal (simcore.cpp:217-223, 237-276)
+        const int sb = rows[size_t(r)].first, actor = rows[size_t(r)].second;
+        const Scene& s = scenes[size_t(sb)];
+        const RouteCtx& c = ctx[size_t(sb)];
+        Scene eg;
+        actor_as_ego(s, actor < 0 ? 0 : actor, eg);
+        env->row_scen[size_t(r)] = sb;
+        env->row_actor[size_t(r)] = actor;
+        pb.at<int32_t>(o_rsc)[r] = sb;
+        pb.at<int32_t>(o_rac)[r] = actor;
+        pb.at<int32_t>(o_soff)[r] = total_stop;
+        total_stop += int(c.stops.size());
+        pb.at<float>(o_gx)[r] = eg.goal_x;
+        pb.at<float>(o_gy)[r] = eg.goal_y;
+        double gs = project_host(double(eg.goal_x), double(eg.goal_y), c).s;
+        double s0 = project_host(double(eg.ego_x.front()), double(eg.ego_y.front()), c).s;
+        double s1 = project_host(double(eg.ego_x[s.num_steps - 1]), double(eg.ego_y[s.num_steps - 1]), c).s;
+        env->goal_s[size_t(r)] = gs;
+        env->initial_s[size_t(r)] = s0;
+        env->logged_progress[size_t(r)] = s1 - s0;
+        pb.at<double>(o_gs)[r] = gs;
+        pb.at<double>(o_ix)[r] = double(eg.ego_x[0]);
+        pb.at<double>(o_iy)[r] = double(eg.ego_y[0]);
+        pb.at<double>(o_ih)[r] = double(eg.ego_h[0]);
+        pb.at<double>(o_iv)[r] = double(eg.ego_v[0]);
+        pb.at<double>(o_ist)[r] = initial_steering(eg, env->cfg.wheelbase, env->cfg.delta_max);
+    }
+    for (int b = 0; b < S; ++b) {
         const Scene& s = scenes[size_t(b)];
         const RouteCtx& c = ctx[size_t(b)];
         const int T = d.T, A = d.A;
         pb.at<int32_t>(o_num_steps)[b] = int32_t(s.num_steps);
-        pb.at<int32_t>(o_na)[b] = int32_t(s.agents.size());
+        pb.at<int32_t>(o_na)[b] = int32_t(controlled ? num_actors(s) : int(s.agents.size()));
         size_t np = 0;
         for (const auto& f : s.features) np += f.xy.size() / 2;
         pb.at<int32_t>(o_nr)[b] = int32_t(np);
@@ -476,27 +523,19 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
         pb.at<int32_t>(o_nl)[b] = int32_t(c.lanes.size());
         pb.at<int32_t>(o_nlt)[b] = int32_t(c.lights.size());
         pb.at<int32_t>(o_ns)[b] = int32_t(c.stops.size());
-        pb.at<int32_t>(o_soff)[b] = total_stop;
-        total_stop += int(c.stops.size());
         pb.at<float>(o_sl)[b] = s.speed_limit;
-        pb.at<float>(o_gx)[b] = s.goal_x;
-        pb.at<float>(o_gy)[b] = s.goal_y;
-        // simcore.cpp:217-223
-        double gs = project_host(double(s.goal_x), double(s.goal_y), c).s;
-        double s0 = project_host(double(s.ego_x.front()), double(s.ego_y.front()), c).s;
-        double s1 = project_host(double(s.ego_x[s.num_steps - 1]), double(s.ego_y[s.num_steps - 1]), c).s;
-        env->goal_s[size_t(b)] = gs;
-        env->initial_s[size_t(b)] = s0;
-        env->logged_progress[size_t(b)] = s1 - s0;
-        pb.at<double>(o_gs)[b] = gs;
         pb.at<double>(o_rl)[b] = c.route_length;
-        pb.at<double>(o_ix)[b] = double(s.ego_x[0]);
-        pb.at<double>(o_iy)[b] = double(s.ego_y[0]);
-        pb.at<double>(o_ih)[b] = double(s.ego_h[0]);
-        pb.at<double>(o_iv)[b] = double(s.ego_v[0]);
-        pb.at<double>(o_ist)[b] = initial_steering(s, env->cfg.wheelbase, env->cfg.delta_max);
-        for (size_t j = 0; j < s.agents.size(); ++j) {
-            const AgentLog& ag = s.agents[j];
+        // agent columns: the logged agents, or in controlled mode the actors
+        // (column 0 = the logged ego as an agent, column k = agents[k-1])
+        std::vector<const AgentLog*> cols;
+        AgentLog ego_ag;
+        if (controlled) {
+            ego_ag = ego_as_agent(s, ebd);
+            cols.push_back(&ego_ag);
+        }
+        for (const auto& ag : s.agents) cols.push_back(&ag);
+        for (size_t j = 0; j < cols.size(); ++j) {
+            const AgentLog& ag = *cols[j];
             pb.at<float>(o_agl)[size_t(b) * A + j] = ag.length;
             pb.at<float>(o_agw)[size_t(b) * A + j] = ag.width;
             for (uint32_t t = 0; t < s.num_steps; ++t) {
@@ -667,6 +706,8 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     pk.lt_s = reinterpret_cast<const double*>(D + o_lts);
     pk.lt_state = D + o_ltst;
     pk.st_s = reinterpret_cast<const double*>(D + o_sts);
+    pk.row_scen = controlled ? reinterpret_cast<const int32_t*>(D + o_rsc) : nullptr;
+    pk.row_actor = controlled ? reinterpret_cast<const int32_t*>(D + o_rac) : nullptr;
     {
         // L2 prefetch table (zsim_kernels.cu prefetch_row): the per-row arrays a step touches
         const uint32_t LC = uint32_t(d.L) * uint32_t(d.C), TA = uint32_t(d.T) * uint32_t(d.A), A = uint32_t(d.A);
@@ -691,6 +732,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon)
     }
 
     env->B = B;
+    env->n_scen = S;
     env->horizon = horizon;
     env->dt = dt;
     env->total_stop = total_stop;
@@ -774,9 +816,27 @@ ZSIM_API int zsim_sim_config_defaults(zsim_sim_config* c) {
     });
 }
 
-ZSIM_API int zsim_env_create(const uint8_t* file, size_t nbytes, const int64_t* indices, int32_t n_indices,
-                             int32_t horizon, const zsim_sim_config* cfg, const double* accel_bins, int32_t n_accel,
-                             const double* steer_bins, int32_t n_steer, int32_t device, zsim_env** out) {
+namespace {
+
+std::vector<zs::Scene> decode_batch(const uint8_t* file, size_t nbytes, const int64_t* indices, int32_t n_indices) {
+    if (!file) zs::raise(zs::Err::invalid_argument, "null ZSIM buffer");
+    zs::ZsimIndex idx = zs::zsim_index(file, nbytes);
+    std::vector<int64_t> rows;
+    if (indices) {
+        if (n_indices <= 0) zs::raise(zs::Err::invalid_argument, "load_batch: empty index list");
+        rows.assign(indices, indices + n_indices);
+    } else {
+        for (int64_t i = 0; i < int64_t(idx.records.size()); ++i) rows.push_back(i);
+    }
+    std::vector<zs::Scene> scenes;
+    scenes.reserve(rows.size());
+    for (int64_t r : rows) scenes.push_back(zs::zsim_decode(file, nbytes, idx, r));
+    return scenes;
+}
+
+int create_env(const uint8_t* file, size_t nbytes, const int64_t* indices, int32_t n_indices, int32_t horizon,
+               const zsim_sim_config* cfg, const double* accel_bins, int32_t n_accel, const double* steer_bins,
+               int32_t n_steer, int32_t device, zsim_env** out, bool controlled) {
     return guarded([&] {
         if (!out) raise(Err::invalid_argument, "null output pointer");
         *out = nullptr;
@@ -805,25 +865,13 @@ ZSIM_API int zsim_env_create(const uint8_t* file, size_t nbytes, const int64_t* 
         env->zero_accel = zs::nearest_bin(env->accel_bins, 0.0);
         env->zero_steer = zs::nearest_bin(env->steer_bins, 0.0);
 
-        zs::ZsimIndex idx = zs::zsim_index(file, nbytes);
-        std::vector<int64_t> rows;
-        if (indices) {
-            if (n_indices <= 0) raise(Err::invalid_argument, "load_batch: empty index list");
-            rows.assign(indices, indices + n_indices);
-        } else {
-            for (int64_t i = 0; i < int64_t(idx.records.size()); ++i) rows.push_back(i);
-        }
-        std::vector<zs::Scene> scenes;
-        scenes.reserve(rows.size());
+        std::vector<zs::Scene> scenes = decode_batch(file, nbytes, indices, n_indices);
         int maxsteps = 2;
-        for (int64_t r : rows) {
-            scenes.push_back(zs::zsim_decode(file, nbytes, idx, r));
-            maxsteps = std::max(maxsteps, int(scenes.back().num_steps));
-        }
+        for (const auto& sc : scenes) maxsteps = std::max(maxsteps, int(sc.num_steps));
         if (horizon <= 0) horizon = maxsteps;
         set_device(env.get());
         env->base.cfg = make_dev_cfg(env->cfg, env->accel_bins, env->steer_bins);
-        stage_env(env.get(), scenes, horizon);
+        stage_env(env.get(), scenes, horizon, controlled);
         cuda_check(cudaMalloc(&env->d_hint, sizeof(float4) * size_t(env->B)), "cudaMalloc(hint)");
         cuda_check(cudaMemset(env->d_hint, 0xFF, sizeof(float4) * size_t(env->B)), "cudaMemset(hint)");  // NaN: no hint
         env->base.hint = env->d_hint;
@@ -831,6 +879,57 @@ ZSIM_API int zsim_env_create(const uint8_t* file, size_t nbytes, const int64_t* 
         cuda_check(cudaMemset(env->d_err, 0, 4), "cudaMemset(err)");
         env->base.err = env->d_err;
         *out = env.release();
+    });
+}
+
+}  // namespace
+
+ZSIM_API int zsim_env_create(const uint8_t* file, size_t nbytes, const int64_t* indices, int32_t n_indices,
+                             int32_t horizon, const zsim_sim_config* cfg, const double* accel_bins, int32_t n_accel,
+                             const double* steer_bins, int32_t n_steer, int32_t device, zsim_env** out) {
+    return create_env(file, nbytes, indices, n_indices, horizon, cfg, accel_bins, n_accel, steer_bins, n_steer, device,
+                      out, false);
+}
+
+ZSIM_API int zsim_env_create_controlled(const uint8_t* file, size_t nbytes, const int64_t* indices, int32_t n_indices,
+                                        int32_t horizon, const zsim_sim_config* cfg, const double* accel_bins,
+                                        int32_t n_accel, const double* steer_bins, int32_t n_steer, int32_t device,
+                                        zsim_env** out) {
+    return create_env(file, nbytes, indices, n_indices, horizon, cfg, accel_bins, n_accel, steer_bins, n_steer, device,
+                      out, true);
+}
+
+ZSIM_API int zsim_env_get_rows(const zsim_env* env, int32_t* scenario, int32_t* actor) {
+    return guarded([&] {
+        if (!env) raise(Err::invalid_argument, "null env");
+        if (scenario) std::memcpy(scenario, env->row_scen.data(), sizeof(int32_t) * env->row_scen.size());
+        if (actor) std::memcpy(actor, env->row_actor.data(), sizeof(int32_t) * env->row_actor.size());
+    });
+}
+
+ZSIM_API int zsim_controlled_expand(const uint8_t* file, size_t nbytes, const int64_t* indices, int32_t n_indices,
+                                    const zsim_sim_config* cfg, uint8_t** out_buf, size_t* out_len) {
+    return guarded([&] {
+        if (!out_buf || !out_len) raise(Err::invalid_argument, "null output pointer");
+        *out_buf = nullptr;
+        *out_len = 0;
+        zsim_sim_config c;
+        if (cfg) {
+            c = *cfg;
+        } else {
+            zsim_sim_config_defaults(&c);
+        }
+        std::vector<zs::Scene> scenes = decode_batch(file, nbytes, indices, n_indices);
+        const zs::EgoBoxDims ebd{c.ego_length, c.ego_width, c.ego_center_offset};
+        std::string img = zs::zsim_header(scenes.empty() ? 0.1 : scenes[0].dt);
+        for (const auto& sc : scenes)
+            for (int j = 0; j < zs::num_actors(sc); ++j)
+                if (zs::actor_controllable(sc, j)) zs::zsim_encode_append(img, zs::controlled_scene(sc, j, ebd));
+        uint8_t* buf = static_cast<uint8_t*>(std::malloc(img.size()));
+        if (!buf) raise(Err::runtime, "out of host memory");
+        std::memcpy(buf, img.data(), img.size());
+        *out_buf = buf;
+        *out_len = img.size();
     });
 }
 
@@ -871,6 +970,8 @@ ZSIM_API int zsim_env_get_info(const zsim_env* env, zsim_env_info* out) {
         out->cap_stops = d.NS;
         out->device = env->device;
         out->static_bytes = env->pack_bytes;
+        out->scenarios = env->n_scen;
+        out->controlled = env->base.pk.row_scen ? 1 : 0;
     });
 }
 
@@ -1200,7 +1301,7 @@ ZSIM_API int zsim_stress_config_defaults(zsim_stress_config* c) {
         c->speed_limit = 10.0;
         c->lane_width = 3.5;
         c->first_index = 0;
-        c->reserved = 0;
+        c->flags = 0;
     });
 }
 

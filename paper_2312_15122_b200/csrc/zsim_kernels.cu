@@ -108,6 +108,9 @@ __device__ __forceinline__ T pick5(int k, T a0, T a1, T a2, T a3, T a4) {
     return k == 0 ? a0 : k == 1 ? a1 : k == 2 ? a2 : k == 3 ? a3 : a4;
 }
 
+__device__ __forceinline__ int scen_of(const DevPack& pk, int b) { return pk.row_scen ? pk.row_scen[b] : b; }
+__device__ __forceinline__ int skip_of(const DevPack& pk, int b) { return pk.row_actor ? pk.row_actor[b] : -1; }
+
 // Row state, uniform across the warp.
 struct Row {
     double x, y, h, v, steer, proj_s, proj_d;
@@ -124,6 +127,8 @@ struct RowSh {
     double ex[4], ey[4];   // its corners (obb_distance reads them lane-indexed)
     double qx[5], qy[5];   // projection queries (position + inflated corners)
     float4 hint;           // the row's top-k hint, loaded at row start
+    int sc;                // scenario of the row (== row in ego mode)
+    int skip;              // agent column of the controlled actor (-1 in ego mode)
     double a_lat;          // step: v^2 tan(steer) / wheelbase (simcore.cpp:309-316)
     int boxes_ready;       // agent boxes at r.t + overlap flags are in agx/agy/agf
 };
@@ -319,7 +324,7 @@ __device__ __forceinline__ float seg_inv_f(float4 f) {
 // The winners' s / signed d / half-width run one (query, route lane) pair per
 // lane.  Uniform result.
 template <int NQU>
-__device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const double* qy) {
+__device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const double* qx, const double* qy) {
     const int L = pk.d.L, C = pk.d.C;
     const int nl = pk.n_lanes[b];
     const int lane = lane_id();
@@ -559,18 +564,18 @@ __device__ Proj warp_project(const DevPack& pk, int b, const double* qx, const d
 
 // Agent box at log slice `slice` (agent_box, simcore.cpp:162-165): corners
 // into smem and the SAT overlap with the ego box (geometry.cpp:65-75).
-__device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int b, size_t slice, int j, const Box& eb,
+__device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size_t slice, int j, const Box& eb,
                                                  const double* EX, const double* EY, const WarpBuf& w) {
     const int A = pk.d.A;
     double h = double(pk.ag_h[slice + j]);
     Box ab;
     ab.cx = double(pk.ag_x[slice + j]);
     ab.cy = double(pk.ag_y[slice + j]);
-    ab.hl = double(pk.ag_len[size_t(b) * A + j]) * 0.5;
-    ab.hw = double(pk.ag_wid[size_t(b) * A + j]) * 0.5;
-    const double2 sc = sincos2(h);
-    ab.s = sc.x;
-    ab.c = sc.y;
+    ab.hl = double(pk.ag_len[size_t(sc) * A + j]) * 0.5;
+    ab.hw = double(pk.ag_wid[size_t(sc) * A + j]) * 0.5;
+    const double2 hs = sincos2(h);
+    ab.s = hs.x;
+    ab.c = hs.y;
     double X[4], Y[4];
     box_corners(ab, X, Y);
 #pragma unroll
@@ -999,6 +1004,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     }
 
     const int t = r.t;
+    const int sc = rs.sc, skip = rs.skip;  // scenario data index, controlled actor's agent column
     PSTAT(0, 1);
     const bool boxes_ready = rs.boxes_ready != 0;
     if (!boxes_ready) {
@@ -1023,18 +1029,18 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     // ---- active features: roads::stop_info (roads.cpp:253-277), simcore.cpp:440-455 ----
     {
         double best_stop = 1e300;
-        const int ns = pk.n_stops[b];
+        const int ns = pk.n_stops[sc];
 #pragma unroll 1
         for (int j = 0; j < ns; ++j) {
-            double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - r.proj_s;
+            double ahead = pk.st_s[size_t(sc) * pk.d.NS + j] - r.proj_s;
             if (ahead > 0.0 && ahead < best_stop) best_stop = ahead;
         }
         double best_light = 1e300;
         int best_k = -1;
-        const int nlt = pk.n_lights[b];
+        const int nlt = pk.n_lights[sc];
 #pragma unroll 1
         for (int k = 0; k < nlt; ++k) {
-            double ahead = pk.lt_s[size_t(b) * pk.d.NL + k] - r.proj_s;
+            double ahead = pk.lt_s[size_t(sc) * pk.d.NL + k] - r.proj_s;
             if (ahead > 0.0 && ahead < best_light) {
                 best_light = ahead;
                 best_k = k;
@@ -1042,10 +1048,10 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         }
         int light = 3;
         if (best_k >= 0) {
-            int nsteps = pk.num_steps[b];
+            int nsteps = pk.num_steps[sc];
             int step = t < nsteps - 1 ? t : nsteps - 1;
             step = step > 0 ? step : 0;
-            light = pk.lt_state[(size_t(b) * pk.d.NL + best_k) * pk.d.T + step];
+            light = pk.lt_state[(size_t(sc) * pk.d.NL + best_k) * pk.d.T + step];
         }
         const double R = cfg.feature_radius;
         if (lane < 9) {
@@ -1055,7 +1061,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
             if (lane == 2) f = float(best_stop < 1e300 ? mind(best_stop, R) : R);
             if (lane >= 3 && lane <= 6) f = (lane - 3 == light) ? 1.f : 0.f;
             if (lane == 7) f = float(best_k >= 0 ? mind(best_light, R) : R);
-            if (lane == 8) f = pk.speed_limit[b];
+            if (lane == 8) f = pk.speed_limit[sc];
             act[lane] = f;
         }
         // value-only features (simcore.cpp:531-537)
@@ -1068,14 +1074,14 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
 
     // ---- other agents: obb_distance, sorted by (dist, idx) (simcore.cpp:457-486) ----
     const int A = pk.d.A;
-    const int na = pk.n_agents[b];
-    const bool t_ok = t < pk.num_steps[b];
-    const size_t aslice = (size_t(b) * pk.d.T + (t_ok ? t : 0)) * A;
+    const int na = pk.n_agents[sc];
+    const bool t_ok = t < pk.num_steps[sc];
+    const size_t aslice = (size_t(sc) * pk.d.T + (t_ok ? t : 0)) * A;
     if (!boxes_ready) {
         const Box eb = rs.eb;
         for (int j = lane; j < na; j += 32) {
             int f = -1;
-            if (t_ok && pk.ag_valid[aslice + j]) f = agent_box_overlap(pk, b, aslice, j, eb, rs.ex, rs.ey, w);
+            if (t_ok && j != skip && pk.ag_valid[aslice + j]) f = agent_box_overlap(pk, sc, aslice, j, eb, rs.ex, rs.ey, w);
             w.agf[j] = f;
         }
         __syncwarp();
@@ -1222,7 +1228,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         o[0] = make_float2(f[0], f[1]);
         o[1] = make_float2(f[2], f[3]);
         o[2] = make_float2(f[4], f[5]);
-        if (dbg) dbg[k] = j;
+        if (dbg) dbg[k] = (skip >= 0 && j > skip) ? j - 1 : j;  // index among the row's agents
     }
 
     // ---- road network points: nearest_features (roads.cpp:210-236) ----
@@ -1232,16 +1238,16 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     for (int k = lane; k < 32 * 32; k += 32) w.hist[k] = 0;
     __syncwarp();
     {
-        const int n = pk.n_road[b];
-        const float2* pts = pk.road_xy + size_t(b) * pk.d.P;
-        const int32_t* oidx = pk.road_oi + size_t(b) * pk.d.P;
+        const int n = pk.n_road[sc];
+        const float2* pts = pk.road_xy + size_t(sc) * pk.d.P;
+        const int32_t* oidx = pk.road_oi + size_t(sc) * pk.d.P;
         const double R = cfg.feature_radius;
         const int* sel = w.order;
-        const PointSet ps{pts, oidx, pk.road_cb + size_t(b) * pk.d.PC, n, (n + kChunk - 1) / kChunk};
-        const int nsel = warp_topk(ps, Kr, r.x, r.y, true, R * R, pk.road_box[b], a.cand_cap, w.hist, w.cidx, w.ckey,
+        const PointSet ps{pts, oidx, pk.road_cb + size_t(sc) * pk.d.PC, n, (n + kChunk - 1) / kChunk};
+        const int nsel = warp_topk(ps, Kr, r.x, r.y, true, R * R, pk.road_box[sc], a.cand_cap, w.hist, w.cidx, w.ckey,
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 0);
         ROW_MARK(b, 4);
-        const uint8_t* kd = pk.road_kd + size_t(b) * pk.d.P;
+        const uint8_t* kd = pk.road_kd + size_t(sc) * pk.d.P;
         for (int k = lane; k < Kr; k += 32) {
             float f[12];
 #pragma unroll
@@ -1271,15 +1277,15 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     // ---- route border points: top n_route by (d2, idx), no radius (simcore.cpp:503-529) ----
     ROW_MARK(b, 5);
     {
-        const int n = pk.n_route[b];
-        const float2* pts = pk.route_xy + size_t(b) * pk.d.R;
-        const int32_t* oidx = pk.route_oi + size_t(b) * pk.d.R;
+        const int n = pk.n_route[sc];
+        const float2* pts = pk.route_xy + size_t(sc) * pk.d.R;
+        const int32_t* oidx = pk.route_oi + size_t(sc) * pk.d.R;
         const int* sel = w.order;
-        const PointSet ps{pts, oidx, pk.route_cb + size_t(b) * pk.d.RC, n, (n + kChunk - 1) / kChunk};
-        const int nsel = warp_topk(ps, Kl, r.x, r.y, false, 0.0, pk.route_box[b], a.cand_cap, w.hist, w.cidx, w.ckey,
+        const PointSet ps{pts, oidx, pk.route_cb + size_t(sc) * pk.d.RC, n, (n + kChunk - 1) / kChunk};
+        const int nsel = warp_topk(ps, Kl, r.x, r.y, false, 0.0, pk.route_box[sc], a.cand_cap, w.hist, w.cidx, w.ckey,
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 1);
         ROW_MARK(b, 6);
-        const uint8_t* fl = pk.route_fl + size_t(b) * pk.d.R;
+        const uint8_t* fl = pk.route_fl + size_t(sc) * pk.d.R;
         for (int k = lane; k < Kl; k += 32) {
             float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
             int i = -1;
@@ -1312,23 +1318,24 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     const DevCfg& cfg = a.cfg;
     const int lane = lane_id();
     RowSh& rs = *w.rs;
-    const int ns = pk.n_stops[b];
+    const int sc = rs.sc, skip = rs.skip;  // scenario data index, controlled actor's agent column
+    const int ns = pk.n_stops[sc];
     const int soff = pk.stop_off[b];
     for (int j = lane; j < ns; j += 32) w.sflag[j] = a.in.stopped_flags[soff + j];
     __syncwarp();
     ROW_MARK(b, 8);
 
-    bool skip = rs.r0.done != 0;
+    bool pass = rs.r0.done != 0;
     int ai = 0, si = 0;
-    if (!skip) {
+    if (!pass) {
         ai = a.accel[b];
         si = a.steer[b];
         if (ai < 0 || ai >= cfg.n_accel || si < 0 || si >= cfg.n_steer) {
             if (lane == 0) atomicOr(a.err, 1);
-            skip = true;
+            pass = true;
         }
     }
-    if (skip) {
+    if (pass) {
         // absorbing pass-through (simcore.cpp:281-299); bad-action rows are left unchanged
         if (lane == 0) {
             const Row r0 = rs.r0;
@@ -1392,20 +1399,20 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     }
     const double a_lat = rs.a_lat;
     ROW_MARK(b, 9);
-    const Proj p1 = warp_project<NQ>(pk, b, rs.qx, rs.qy);
+    const Proj p1 = warp_project<NQ>(pk, sc, rs.qx, rs.qy);
     ROW_MARK(b, 1);
 
     // collision with the agents valid at t+1 (simcore.cpp:323-331); boxes kept for observe(t+1)
     int hit = 0;
     {
-        const int na = pk.n_agents[b];
+        const int na = pk.n_agents[sc];
         const int t1 = rs.r.t;
-        const bool t_ok = t1 < pk.num_steps[b];
-        const size_t slice = (size_t(b) * pk.d.T + (t_ok ? t1 : 0)) * pk.d.A;
+        const bool t_ok = t1 < pk.num_steps[sc];
+        const size_t slice = (size_t(sc) * pk.d.T + (t_ok ? t1 : 0)) * pk.d.A;
         const Box eb = rs.eb;
         for (int j = lane; j < na; j += 32) {
             int f = -1;
-            if (t_ok && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, b, slice, j, eb, rs.ex, rs.ey, w);
+            if (t_ok && j != skip && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, sc, slice, j, eb, rs.ex, rs.ey, w);
             w.agf[j] = f;
             hit |= f == 1;
         }
@@ -1417,26 +1424,26 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     const bool hit_off_route = !p1.on_route;
     bool hit_red = false;
     {
-        const int nsteps = pk.num_steps[b];
+        const int nsteps = pk.num_steps[sc];
         const int t_light = t0 < nsteps - 1 ? t0 : nsteps - 1;
-        const int nlt = pk.n_lights[b];
+        const int nlt = pk.n_lights[sc];
 #pragma unroll 1
         for (int k = 0; k < nlt; ++k) {
-            double ls = pk.lt_s[size_t(b) * pk.d.NL + k];
-            if (ps0 < ls && ls <= p1.s && pk.lt_state[(size_t(b) * pk.d.NL + k) * pk.d.T + t_light] == 0)
+            double ls = pk.lt_s[size_t(sc) * pk.d.NL + k];
+            if (ps0 < ls && ls <= p1.s && pk.lt_state[(size_t(sc) * pk.d.NL + k) * pk.d.T + t_light] == 0)
                 hit_red = true;
         }
     }
     bool hit_stop = false;
 #pragma unroll 1
     for (int j = 0; j < ns; ++j) {
-        double ss = pk.st_s[size_t(b) * pk.d.NS + j];
+        double ss = pk.st_s[size_t(sc) * pk.d.NS + j];
         if (ps0 < ss && ss <= p1.s && v0 > cfg.stop_cross_speed && !w.sflag[j]) hit_stop = true;
     }
     const bool hit_goal = fabs(p1.s - pk.goal_s[b]) <= cfg.goal_radius;
     const double progress = p1.s - ps0;
     const double a_lon = accel;
-    double reward = cfg.w_progress * progress - cfg.w_speed * maxd(0.0, vn - double(pk.speed_limit[b])) * dt -
+    double reward = cfg.w_progress * progress - cfg.w_speed * maxd(0.0, vn - double(pk.speed_limit[sc])) * dt -
                     cfg.w_lat * a_lat * a_lat * dt - cfg.w_lon * a_lon * a_lon * dt;
     const int reason = hit ? 1 : hit_off_route ? 2 : hit_red ? 3 : hit_stop ? 4 : hit_goal ? 5 : 0;
     int events = rs.r0.events;
@@ -1468,7 +1475,7 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     }
     // stopped-flag update with the post-step state (simcore.cpp:390-396)
     for (int j = lane; j < ns; j += 32) {
-        double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - p1.s;
+        double ahead = pk.st_s[size_t(sc) * pk.d.NS + j] - p1.s;
         uint8_t fl = w.sflag[j];
         if (ahead >= 0.0 && ahead <= cfg.stop_zone && vn < cfg.stop_slow_speed) fl = 1;
         a.out.stopped_flags[soff + j] = fl;
@@ -1476,11 +1483,11 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     __syncwarp();
 }
 
-// Prefetch row b's static scenario data (the arrays one step touches, from
-// the pack's prefetch table: one array per lane) into L2.  `t` is the log
+// Prefetch scenario sc's static data (the arrays one step touches, from the
+// pack's prefetch table: one array per lane) into L2.  `t` is the log
 // index of the agent slice the kernel will read.
 template <bool STEP, bool OBS>
-__device__ __forceinline__ void prefetch_row(const KernelArgs& a, int b, int t) {
+__device__ __forceinline__ void prefetch_row(const KernelArgs& a, int sc, int t) {
     const DevPack& pk = a.pk;
     const int lane = lane_id();
     if (lane >= pk.n_pf) return;
@@ -1488,7 +1495,7 @@ __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int b, int t) 
     if (((d.mode & 1) && !STEP) || ((d.mode & 2) && !OBS) || d.bytes == 0) return;
     const int T = pk.d.T;
     const int ts = t < T ? (t >= 0 ? t : 0) : T - 1;
-    const char* p = static_cast<const char*>(d.base) + size_t(b) * d.row_stride + size_t(ts) * d.t_stride;
+    const char* p = static_cast<const char*>(d.base) + size_t(sc) * d.row_stride + size_t(ts) * d.t_stride;
     prefetch_l2(p, d.bytes < (1u << 24) ? d.bytes : (1u << 24));
 }
 
@@ -1502,15 +1509,18 @@ __global__ void __launch_bounds__(kThreads, ZS_MIN_BLOCKS) k_step_observe(const 
     const int wpb = kThreads / 32;
     const int stride = gridDim.x * wpb;
     int b = blockIdx.x * wpb + warp_in_block();
-    if (b < a.pk.d.B) prefetch_row<STEP, OBS>(a, b, a.in.t[b] + (STEP ? 1 : 0));
+    if (b < a.pk.d.B) prefetch_row<STEP, OBS>(a, scen_of(a.pk, b), a.in.t[b] + (STEP ? 1 : 0));
     for (; b < a.pk.d.B; b += stride) {
         if (lane_id() == 0) {
             w.rs->r0 = load_row(a.in, b);
             if (OBS && a.hint) w.rs->hint = a.hint[b];
+            w.rs->sc = scen_of(a.pk, b);
+            w.rs->skip = skip_of(a.pk, b);
         }
         __syncwarp();
         // the warp's next row: its static data streams into L2 while this row computes
-        if (b + stride < a.pk.d.B) prefetch_row<STEP, OBS>(a, b + stride, w.rs->r0.t + (STEP ? 1 : 0));
+        if (b + stride < a.pk.d.B)
+            prefetch_row<STEP, OBS>(a, scen_of(a.pk, b + stride), w.rs->r0.t + (STEP ? 1 : 0));
         ROW_MARK(b, 0);
         if (STEP) {
             step_row(a, b, w);
@@ -1533,8 +1543,9 @@ __global__ void __launch_bounds__(kThreads) k_reset(const KernelArgs a) {
     const int lane = lane_id();
     const int wpb = kThreads / 32;
     for (int b = blockIdx.x * wpb + warp_in_block(); b < pk.d.B; b += gridDim.x * wpb) {
+        const int sc = scen_of(pk, b);
         double qx[1] = {pk.init_x[b]}, qy[1] = {pk.init_y[b]};
-        const Proj p = warp_project<1>(pk, b, qx, qy);
+        const Proj p = warp_project<1>(pk, sc, qx, qy);
         if (lane == 0) {
             a.out.x[b] = pk.init_x[b];
             a.out.y[b] = pk.init_y[b];
@@ -1550,10 +1561,10 @@ __global__ void __launch_bounds__(kThreads) k_reset(const KernelArgs a) {
             a.out.proj_in_corridor[b] = uint8_t(p.in_corr);
             a.out.events[b] = 0;
         }
-        const int ns = pk.n_stops[b];
+        const int ns = pk.n_stops[sc];
         const int soff = pk.stop_off[b];
         for (int j = lane; j < ns; j += 32) {
-            double ahead = pk.st_s[size_t(b) * pk.d.NS + j] - p.s;
+            double ahead = pk.st_s[size_t(sc) * pk.d.NS + j] - p.s;
             bool st = ahead >= 0.0 && ahead <= cfg.stop_zone && pk.init_v[b] < cfg.stop_slow_speed;
             a.out.stopped_flags[soff + j] = st ? 1 : 0;
         }

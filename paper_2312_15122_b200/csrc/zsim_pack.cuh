@@ -2,7 +2,8 @@
 // device-side SimConfig.  One contiguous allocation, every array 256-B
 // aligned, padded to per-batch capacities with per-scenario counts.
 //
-// Per scenario b (reference types in /root/reference/proj/src/core/):
+// Per scenario (reference types in /root/reference/proj/src/core/); the
+// row-level arrays (initial ego, goal, stop-flag offset) are per row:
 //   agents  [B][T][A]  x, y, heading, speed f32 + valid u8   (LoggedAgent, scenario.hpp:37-44)
 //   dims    [B][A]     length, width f32
 //   road    [B][P]     float2 xy + u8 kind|dir<<4 + i32 index in nearest_features'
@@ -29,6 +30,7 @@ namespace zs {
 
 struct PackDims {
     int32_t B, T, A, P, R, L, C, NL, NS;
+    int32_t S;       // scenarios (B rows index them through row_scen; S == B in ego mode)
     int32_t PC, RC;  // 32-point chunks of the road / route point sets
     int32_t GC;      // 8-segment groups per lane centreline
 };
@@ -112,6 +114,9 @@ struct DevPack {
     const LaneInfo* ln_info;  // [B][L] vertex count, lane_id, half-width bounds
     const float4* road_box;   // [B] (min x, min y, max x, max y) of the road points
     const float4* route_box;  // [B] same for the route border points
+    // rows -> scenario data (null in ego mode: identity / no skipped actor)
+    const int32_t* row_scen;   // [B] scenario of the row
+    const int32_t* row_actor;  // [B] controlled actor (its agent column is skipped)
     const PfDesc* pf;  // prefetch table
     int32_t n_pf;
     // lights / stops

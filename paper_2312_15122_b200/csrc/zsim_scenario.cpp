@@ -374,6 +374,71 @@ std::vector<RoutePt> build_route_points(const Scene& sc) {
     return pts;
 }
 
+bool actor_controllable(const Scene& s, int actor) {
+    if (actor == 0) return true;
+    if (actor < 0 || actor > int(s.agents.size())) return false;
+    const AgentLog& a = s.agents[size_t(actor - 1)];
+    if (a.valid.size() < s.num_steps) return false;
+    for (uint32_t t = 0; t < s.num_steps; ++t)
+        if (!a.valid[t]) return false;
+    return true;
+}
+
+AgentLog ego_as_agent(const Scene& s, const EgoBoxDims& d) {
+    AgentLog a;
+    a.id = "ego";
+    a.length = float(d.length);
+    a.width = float(d.width);
+    const size_t n = s.num_steps;
+    a.x.resize(n), a.y.resize(n), a.heading.resize(n), a.speed.resize(n), a.valid.assign(n, 1);
+    for (size_t t = 0; t < n; ++t) {
+        const double h = double(s.ego_h[t]);
+        // ego_box centre (simcore.cpp:156-160) of the logged pose
+        a.x[t] = float(double(s.ego_x[t]) + std::cos(h) * d.center_offset);
+        a.y[t] = float(double(s.ego_y[t]) + std::sin(h) * d.center_offset);
+        a.heading[t] = s.ego_h[t];
+        a.speed[t] = s.ego_v[t];
+    }
+    return a;
+}
+
+void actor_as_ego(const Scene& s, int actor, Scene& out) {
+    out.num_steps = s.num_steps;
+    out.dt = s.dt;
+    if (actor == 0) {
+        out.ego_x = s.ego_x, out.ego_y = s.ego_y, out.ego_h = s.ego_h, out.ego_v = s.ego_v;
+        out.goal_x = s.goal_x, out.goal_y = s.goal_y;
+        return;
+    }
+    const AgentLog& a = s.agents[size_t(actor - 1)];
+    const size_t n = s.num_steps;
+    out.ego_x.assign(a.x.begin(), a.x.begin() + long(n));
+    out.ego_y.assign(a.y.begin(), a.y.begin() + long(n));
+    out.ego_h.assign(a.heading.begin(), a.heading.begin() + long(n));
+    out.ego_v.assign(a.speed.begin(), a.speed.begin() + long(n));
+    const size_t last = n - 1;
+    const double h = double(a.heading[last]);
+    out.goal_x = float(double(a.x[last]) + 4.0 * std::cos(h));
+    out.goal_y = float(double(a.y[last]) + 4.0 * std::sin(h));
+}
+
+Scene controlled_scene(const Scene& s, int actor, const EgoBoxDims& d) {
+    if (!actor_controllable(s, actor)) raise(Err::invalid_argument, "actor " + std::to_string(actor) + " of `" + s.id +
+                                                                          "` is not controllable");
+    Scene c;
+    c.id = s.id + "#" + std::to_string(actor);
+    actor_as_ego(s, actor, c);
+    if (actor != 0) c.agents.push_back(ego_as_agent(s, d));
+    for (size_t k = 0; k < s.agents.size(); ++k)
+        if (int(k) + 1 != actor) c.agents.push_back(s.agents[k]);
+    c.lanes = s.lanes;
+    c.features = s.features;
+    c.lights = s.lights;
+    c.stops = s.stops;
+    c.speed_limit = s.speed_limit;
+    return c;
+}
+
 double initial_steering(const Scene& sc, double wheelbase, double delta_max) {
     if (sc.num_steps < 2) return 0.0;
     double v0 = double(sc.ego_v[0]);

@@ -103,6 +103,27 @@ std::vector<RoutePt> build_route_points(const Scene& sc);
 // recover_initial_steering (simcore.cpp:620-627).
 double initial_steering(const Scene& sc, double wheelbase, double delta_max);
 
+// ---------------------------------------------------------------------------
+// "All agents controlled" (no reference code).  Actors
+// of a scenario: actor 0 = the logged ego, actor k = agents[k-1].  The row of
+// actor j is exactly a reference Env row over controlled_scene(s, j): the ego
+// log is actor j's log (heading/speed as logged), the goal lies 4 m past its
+// last logged point along its last heading, and the other actors log-replay in
+// actor order.  The logged ego, when it is not the controlled actor, is an
+// agent whose box is the SimConfig ego box (centre ego_center_offset ahead of
+// its logged point).  An agent is controllable when it is valid at every
+// logged step.  Roadgraph, route corridor, lights and stop lines are shared.
+// ---------------------------------------------------------------------------
+struct EgoBoxDims {
+    double length, width, center_offset;
+};
+inline int num_actors(const Scene& s) { return 1 + int(s.agents.size()); }
+bool actor_controllable(const Scene& s, int actor);
+AgentLog ego_as_agent(const Scene& s, const EgoBoxDims& d);
+// ego log + goal of actor `actor` written into `out` (num_steps/dt copied)
+void actor_as_ego(const Scene& s, int actor, Scene& out);
+Scene controlled_scene(const Scene& s, int actor, const EgoBoxDims& d);
+
 // ActionTable::validated / nearest_bin (dynamics.cpp:30-64).
 void check_bins(const std::vector<double>& bins, const char* name);
 int nearest_bin(const std::vector<double>& bins, double v);

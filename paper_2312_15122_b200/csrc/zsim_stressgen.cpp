@@ -206,7 +206,14 @@ Scene make_scene(const zsim_stress_config& cfg, Stream rng, int index) {
         int kind = int(rng.unit() * 3.0);
         double lat, sa, sp = rng.uni(6.0, 12.0);
         bool oncoming = false;
-        if (kind == 0) {
+        if (cfg.flags & 1) {
+            // C2 actor: a route lane, same direction, inside the corridor for the whole log
+            const int ln = int(rng.unit() * double(std::max(1, cfg.lanes - 1)));
+            lat = double(ln) * w + rng.uni(-0.3, 0.3);
+            sp = std::max(0.5, std::min(sp, (route_end - 12.0) / (cfg.dt * double(T - 1))));  // log ends on the route
+            const double span = sp * cfg.dt * double(T - 1);
+            sa = rng.uni(0.0, std::max(1.0, route_end - span - 6.0));
+        } else if (kind == 0) {
             lat = double(1 + int(rng.unit() * std::max(1, cfg.lanes - 1))) * w + rng.uni(-0.3, 0.3);
             sa = rng.uni(-30.0, route_end + 20.0);
         } else if (kind == 1) {
@@ -218,7 +225,7 @@ Scene make_scene(const zsim_stress_config& cfg, Stream rng, int index) {
             oncoming = true;
         }
         int inv_from = T, inv_to = T;
-        if (rng.unit() < 0.15) {
+        if (!(cfg.flags & 1) && rng.unit() < 0.15) {
             inv_from = int(rng.unit() * T);
             inv_to = std::min(T, inv_from + 5 + int(rng.unit() * 30.0));
         }

@@ -257,7 +257,10 @@ class Env:
     """The batched log-replay environment on one B200 (simcore.hpp:188-245)."""
 
     def __init__(self, zsim, indices=None, horizon: int = 0, config: SimConfig | None = None,
-                 accel_bins=None, steer_bins=None, device: int = 0):
+                 accel_bins=None, steer_bins=None, device: int = 0, controlled: bool = False):
+        """`controlled=True`: one row per controllable actor of every scenario
+        ("all agents controlled"; see
+        zsim_env_create_controlled in include/zsim_gpu.h and `rows`)."""
         if isinstance(zsim, (str, os.PathLike)):
             zsim = Path(zsim).read_bytes()
         self._bytes = bytes(zsim)
@@ -273,10 +276,11 @@ class Env:
         sb = np.ascontiguousarray(steer_bins, dtype=np.float64) if steer_bins is not None else None
         h = C.c_void_p()
         buf = C.create_string_buffer(self._bytes, len(self._bytes))
-        check(lib.zsim_env_create(C.cast(buf, C.c_void_p), C.c_size_t(len(self._bytes)), idx, n_idx, int(horizon),
-                                  C.byref(cfg), None if ab is None else _ptr(ab, C.c_double),
-                                  0 if ab is None else int(ab.size), None if sb is None else _ptr(sb, C.c_double),
-                                  0 if sb is None else int(sb.size), int(device), C.byref(h)))
+        create = lib.zsim_env_create_controlled if controlled else lib.zsim_env_create
+        check(create(C.cast(buf, C.c_void_p), C.c_size_t(len(self._bytes)), idx, n_idx, int(horizon),
+                     C.byref(cfg), None if ab is None else _ptr(ab, C.c_double),
+                     0 if ab is None else int(ab.size), None if sb is None else _ptr(sb, C.c_double),
+                     0 if sb is None else int(sb.size), int(device), C.byref(h)))
         self.handle = h.value
         info = EnvInfo()
         check(lib.zsim_env_get_info(self.handle, C.byref(info)))
@@ -291,6 +295,9 @@ class Env:
         sb_, so_, ob_ = C.c_size_t(), C.c_size_t(), C.c_size_t()
         check(lib.zsim_layout_bytes(self.handle, C.byref(sb_), C.byref(so_), C.byref(ob_)))
         self.layout = (sb_.value, so_.value, ob_.value)
+        self.row_scenario = np.zeros(B, dtype=np.int32)
+        self.row_actor = np.zeros(B, dtype=np.int32)
+        check(lib.zsim_env_get_rows(self.handle, _ptr(self.row_scenario, C.c_int32), _ptr(self.row_actor, C.c_int32)))
 
     def close(self):
         if getattr(self, "handle", None):
@@ -453,14 +460,37 @@ class StressConfig:
     speed_limit: float = 10.0
     lane_width: float = 3.5
     first_index: int = 0
+    flags: int = 0  # bit 0: C2 actors (all agents valid, same-direction route lanes)
+
+
+STRESS_C2 = 1
 
 
 def stress_scenarios(cfg: StressConfig, seed: int = 7) -> bytes:
     """ZSIM container image of `cfg.count` stress scenarios (host-only call)."""
-    c = StressConfigC(**{f.name: getattr(cfg, f.name) for f in fields(cfg)}, reserved=0)
+    c = StressConfigC(**{f.name: getattr(cfg, f.name) for f in fields(cfg)})
     p = C.c_void_p()
     n = C.c_size_t()
     check(lib.zsim_stress_generate(C.byref(c), C.c_uint64(seed), C.byref(p), C.byref(n)))
+    try:
+        return C.string_at(p.value, n.value)
+    finally:
+        lib.zsim_free_buffer(p)
+
+
+def controlled_expand(zsim: bytes, indices=None, config: SimConfig | None = None) -> bytes:
+    """The per-row scenarios of a controlled Env (row order) as a ZSIM image:
+    the reference Env over these is the oracle for Env(controlled=True)."""
+    cfg = (config or SimConfig()).to_c()
+    idx, n_idx = None, 0
+    if indices is not None:
+        arr = np.ascontiguousarray(np.asarray(indices, dtype=np.int64))
+        idx, n_idx = arr.ctypes.data_as(C.POINTER(C.c_int64)), int(arr.size)
+    buf = C.create_string_buffer(bytes(zsim), len(zsim))
+    p = C.c_void_p()
+    n = C.c_size_t()
+    check(lib.zsim_controlled_expand(C.cast(buf, C.c_void_p), C.c_size_t(len(zsim)), idx, n_idx, C.byref(cfg),
+                                     C.byref(p), C.byref(n)))
     try:
         return C.string_at(p.value, n.value)
     finally:

@@ -45,7 +45,7 @@ def test_library_hides_internal_symbols():
 
 
 def test_abi_version_and_defaults():
-    assert z.lib.zsim_abi_version() == 1
+    assert z.lib.zsim_abi_version() == 2
     c = _abi.SimConfigC()
     assert z.lib.zsim_sim_config_defaults(C.byref(c)) == 0
     # SimConfig defaults (simcore.hpp:14-45)
