@@ -46,6 +46,9 @@ CONFIGS = {
                workload="C3 per-GPU shard: 8192 scenarios x 64 agents, 4k roadgraph points"),
     "C4": dict(scenarios=16384, agents=128, road_points=8192,
                workload="C4 per-GPU shard at 8 GPUs: 16384 scenarios x 128 agents, 8k roadgraph points"),
+    "C2": dict(scenarios=4096, agents=128, road_points=8192, controlled=True,
+               workload="C2 dense: 4096 scenarios x 128 agents all controlled (524,288 ego rows), 8k roadgraph "
+                        "points; agent-steps = controlled rows x steps (SURVEY 8a row 20)"),
 }
 LANES, LANE_VERTICES = 4, 64
 
@@ -57,6 +60,16 @@ def scenario_step_bytes(A: int, P: int, R: int = 2 * LANES * LANE_VERTICES, L: i
     10P, route 10R, lane centerlines 32LC, lights/stops/goal 64; writes state
     80, StepOut 21, observation 7852."""
     return 80 + 8 + 38 * (A - 1) + 10 * P + 10 * R + 32 * L * C + 64 + 80 + 21 + 7852
+
+
+def controlled_row_step_bytes(A: int, P: int, R: int = 2 * LANES * LANE_VERTICES, L: int = LANES,
+                              C: int = LANE_VERTICES) -> float:
+    """C2: the scenario's static data (agent slices of all A actors, road,
+    route, lanes, lights/stops) is read once per scenario-step and shared by
+    its A rows; each row reads state + actions and writes state, StepOut and
+    its observation (~1.14 MB per scenario-step at A=128, P=8192)."""
+    shared = 38 * A + 10 * P + 10 * R + 32 * L * C + 64
+    return shared / A + 80 + 8 + 80 + 21 + 7852
 
 
 def hbm_peak() -> tuple[float, str]:
@@ -130,6 +143,18 @@ def dist_setup():
     return world, rank, local
 
 
+def _ref_workload(c: dict, n_scen: int, seed: int):
+    """(ZSIM bytes, rows, agents per row) of a reference-arm sample: stress
+    scenarios, or for C2 the per-row scenarios of their controlled actors."""
+    import paper_2312_15122_b200 as z
+    controlled = bool(c.get("controlled"))
+    zsim = z.stress_scenarios(z.StressConfig(count=n_scen, agents=c["agents"], road_points=c["road_points"],
+                                             flags=z.STRESS_C2 if controlled else 0), seed)
+    if controlled:
+        return z.controlled_expand(zsim), n_scen * c["agents"], 1
+    return zsim, n_scen, c["agents"]
+
+
 def cpu_baseline(cfg_name: str, seed: int) -> dict | None:
     """Reference simulator (oracle/_ref) timed on this host's cores over a
     bounded sample of the same workload (rank 0, N=1 only)."""
@@ -141,22 +166,22 @@ def cpu_baseline(cfg_name: str, seed: int) -> dict | None:
         return None
     import paper_2312_15122_b200 as z
     c = CONFIGS[cfg_name]
-    rows = min(1024, c["scenarios"])
-    zsim = z.stress_scenarios(z.StressConfig(count=rows, agents=c["agents"], road_points=c["road_points"]), seed)
+    n_scen = min(16 if c.get("controlled") else 1024, c["scenarios"])
+    zsim, rows, apr = _ref_workload(c, n_scen, seed)
     A, S = z.random_actions(EPISODE, rows, seed=123)
     threads = os.cpu_count() or 1
     secs = refpy.bench(zsim, rows, 92, z.SimConfig(disable_dones=True), threads, 0, EPISODE, A, S)
-    # single-thread leg on a C0-sized sample (64 scenarios), SURVEY 8d
-    r1 = min(64, rows)
-    z1 = z.stress_scenarios(z.StressConfig(count=r1, agents=c["agents"], road_points=c["road_points"]), seed)
+    # single-thread leg on a C0-sized sample (64 rows), SURVEY 8d
+    z1, r1, _ = _ref_workload(c, 1 if c.get("controlled") else min(64, n_scen), seed)
+    r1 = min(r1, 64)
     A1, S1 = z.random_actions(EPISODE, r1, seed=123)
     secs1 = refpy.bench(z1, r1, 92, z.SimConfig(disable_dones=True), 1, 0, EPISODE, A1, S1)
-    return {"value": rows * c["agents"] * EPISODE / secs, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{rows} of the {c['scenarios']} {cfg_name} scenarios x {EPISODE} steps (observe+step), "
-                      f"{threads} per-thread Env shards, oracle/_ref (-O2 -ffp-contract=off)",
+    return {"value": rows * apr * EPISODE / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{rows} rows ({n_scen} of the {c['scenarios']} {cfg_name} scenarios) x {EPISODE} steps "
+                      f"(observe+step), {threads} per-thread Env shards, oracle/_ref (-O2 -ffp-contract=off)",
             "seconds": secs,
-            "value_1thread": r1 * c["agents"] * EPISODE / secs1,
-            "sample_1thread": f"{r1} scenarios x {EPISODE} steps on 1 thread ({secs1:.2f} s)"}
+            "value_1thread": r1 * apr * EPISODE / secs1,
+            "sample_1thread": f"{r1} rows x {EPISODE} steps on 1 thread ({secs1:.2f} s)"}
 
 
 def run_reference(args) -> None:
@@ -166,23 +191,25 @@ def run_reference(args) -> None:
     import paper_2312_15122_b200 as z
     from oracle import refpy
     c = CONFIGS[args.config]
-    B = c["scenarios"]
     if not refpy.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libzsim_ref.so not built"}))
         return
-    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=c["agents"], road_points=c["road_points"]), 7)
+    # C2 has 524,288 rows: the reference times a bounded sample of them
+    n_scen = min(32, c["scenarios"]) if c.get("controlled") else c["scenarios"]
+    zsim, B, apr = _ref_workload(c, n_scen, 7)
     A, S = z.random_actions(EPISODE, B, seed=123)
     threads = os.cpu_count() or 1
     secs = refpy.bench(zsim, B, 92, z.SimConfig(disable_dones=True), threads, args.warmup, args.steps, A, S)
-    value = B * c["agents"] * args.steps / secs
+    value = B * apr * args.steps / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (stress generator seed 7)",
-        "config": {"workload": c["workload"], "scenarios": B, "agents": c["agents"],
+        "config": {"workload": c["workload"], "scenarios": n_scen, "rows": B, "agents": c["agents"],
                    "road_points": c["road_points"], "steps_per_episode": EPISODE, "disable_dones": True},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"all {B} scenarios, {args.steps} observe+step iterations, {threads} threads"},
+                         "sample": f"{B} rows ({n_scen} scenarios), {args.steps} observe+step iterations, "
+                                   f"{threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -202,15 +229,20 @@ def run_ours(args) -> None:
     from paper_2312_15122_b200.shard import allreduce_stats, shard_rows
     c = CONFIGS[args.config]
     A_, P = c["agents"], c["road_points"]
+    controlled = bool(c.get("controlled"))
+    rpr = A_ if controlled else 1  # rows per scenario
     # weak scaling: the global set holds world x scenarios; rank r owns one contiguous shard
     lo, hi = shard_rows(c["scenarios"] * world, world, rank)
-    B = hi - lo
-    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=A_, road_points=P, first_index=lo), 7)
-    env = z.Env(zsim, config=z.SimConfig(disable_dones=True), device=local)
+    S_ = hi - lo
+    zsim = z.stress_scenarios(z.StressConfig(count=S_, agents=A_, road_points=P, first_index=lo,
+                                             flags=z.STRESS_C2 if controlled else 0), 7)
+    env = z.Env(zsim, config=z.SimConfig(disable_dones=True), device=local, controlled=controlled)
     del zsim
-    accel_all, steer_all = z.random_actions(EPISODE, c["scenarios"] * world, seed=123)
-    accel = np.ascontiguousarray(accel_all[:, lo:hi])
-    steer = np.ascontiguousarray(steer_all[:, lo:hi])
+    B = env.info.batch
+    assert B == S_ * rpr, (B, S_, rpr)
+    accel_all, steer_all = z.random_actions(EPISODE, c["scenarios"] * world * rpr, seed=123)
+    accel = np.ascontiguousarray(accel_all[:, lo * rpr:hi * rpr])
+    steer = np.ascontiguousarray(steer_all[:, lo * rpr:hi * rpr])
     dA = torch.from_numpy(accel).cuda()
     dS = torch.from_numpy(steer).cuda()
     s0, s1 = env.device_state(), env.device_state()
@@ -308,7 +340,8 @@ def run_ours(args) -> None:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     allreduce_stats(stats)  # the one data collective: int64 episode stats over NCCL
     elapsed_ms = float(t_max.item())
-    agent_steps = B * A_ * args.steps * world
+    agents_per_row = 1 if controlled else A_  # C2 counts controlled rows
+    agent_steps = B * agents_per_row * args.steps * world
     value = agent_steps / (elapsed_ms / 1e3)
 
     # ---- e2e through the host-vector API (the drop-in overloads) ----
@@ -317,7 +350,7 @@ def run_ours(args) -> None:
         st_h, nx_h = env.new_state(pinned=True), env.new_state(pinned=True)
         so_h, ob_h = env.new_stepout(pinned=True), env.new_obs(pinned=True)
         env.init_state(42, out=st_h)
-        ke = min(args.steps, EPISODE)
+        ke = min(args.steps, 3 if controlled else EPISODE)  # C2 moves 4 GB of observations per step over PCIe
         for t in range(min(3, ke)):
             env.step(st_h, accel[t], steer[t], nx_h, so_h)
             env.observe(nx_h, ob_h)
@@ -337,7 +370,7 @@ def run_ours(args) -> None:
         sb, sob, obb = env.layout
         h2d = 2 * sb + 8 * B  # step uploads state + actions, observe uploads state
         d2h = sb + sob + obb
-        e2e = {"value": B * A_ * ke * world / float(e_s.item()), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": B * agents_per_row * ke * world / float(e_s.item()), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": ke,
                "path": "Env.step + Env.observe host-vector API (zsim_step_host / zsim_observe_host), pinned buffers"}
 
@@ -345,7 +378,7 @@ def run_ours(args) -> None:
         if dist:
             dist.destroy_process_group()
         return
-    per_scen = scenario_step_bytes(A_, P)
+    per_scen = controlled_row_step_bytes(A_, P) if controlled else scenario_step_bytes(A_, P)
     peak, peak_src = hbm_peak()
     achieved = per_scen * B / (kern_ms / 1e3) / 1e9
     traffic = None
@@ -363,16 +396,17 @@ def run_ours(args) -> None:
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: stress generator (seed 7; rank r owns global rows [r*B, (r+1)*B)), random actions "
                 "(splitmix64 seed 123)",
-        "config": {"workload": c["workload"], "scenarios_per_gpu": B, "agents": A_, "road_points": P,
+        "config": {"workload": c["workload"], "scenarios_per_gpu": S_, "rows_per_gpu": B, "agents": A_,
+                   "road_points": P, "controlled": controlled,
                    "route_points": 2 * LANES * LANE_VERTICES, "lanes": LANES, "lane_vertices": LANE_VERTICES,
                    "steps_per_episode": EPISODE, "disable_dones": True,
                    "l2": f"inputs larger than L2 (static pack {env.info.static_bytes / 1e6:.0f} MB per GPU)",
                    "parallelism": f"scenario-sharded x{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "bytes_per_scenario_step": per_scen,
+                     "traffic": traffic, ("bytes_per_row_step" if controlled else "bytes_per_scenario_step"): per_scen,
                      "kernel": "k_step_observe<true,true>", "kernel_ms": kern_ms, "peak_source": peak_src},
         "gpu_launches": args.steps + resets,
-        "scenario_steps_per_s": B * args.steps * world / (elapsed_ms / 1e3),
+        "scenario_steps_per_s": S_ * args.steps * world / (elapsed_ms / 1e3),
         "controlled_agent_steps_per_s": B * args.steps * world / (elapsed_ms / 1e3),
         "timing": {"mode": "cuda-graph rollouts (reset + 91 fused steps)" if use_graph else "eager launches",
                    "rollout_ms_median": float(np.median(rollout_ms)) if rollout_ms else None,

@@ -1175,25 +1175,45 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         nvalid += __popc(__ballot_sync(FULL, fl >= 0));
     }
     __syncwarp();
-    // order by (distance, index) among the valid agents
-    if (na <= 32) {
-        // bitonic sort across the warp on (distance bits, index); distances are
-        // >= +0 so their bit patterns order like the values; invalid = +inf last
-        const bool ok = lane < na && w.agf[lane] >= 0;
-        unsigned long long key = ok ? (unsigned long long)__double_as_longlong(w.agd[lane]) : 0xFFF0000000000000ull;
-        int idx = lane;
+    // order by (distance, index) among the valid agents: bitonic sorts across
+    // the warp on (distance bits, index) -- distances are >= +0 so their bit
+    // patterns order like the values; invalid = +inf, last.  More than 32
+    // agents: the best 16 so far (lanes 0-15) are merged with each further
+    // chunk's best 16 (lanes 16-31) by one more sort.
+    if (na <= 32 || Ka <= 16) {
+        auto sort32 = [&](unsigned long long& key, int& idx) {
 #pragma unroll
-        for (int k = 2; k <= 32; k <<= 1) {
+            for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
-            for (int jj = k >> 1; jj > 0; jj >>= 1) {
-                const unsigned long long ok_ = __shfl_xor_sync(FULL, key, jj);
-                const int oi = __shfl_xor_sync(FULL, idx, jj);
-                const bool other_less = ok_ < key || (ok_ == key && oi < idx);
-                const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
-                if (keep_min == other_less) key = ok_, idx = oi;
+                for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                    const unsigned long long ok_ = __shfl_xor_sync(FULL, key, jj);
+                    const int oi = __shfl_xor_sync(FULL, idx, jj);
+                    const bool other_less = ok_ < key || (ok_ == key && oi < idx);
+                    const bool keep_min = ((lane & jj) == 0) == ((lane & k) == 0);
+                    if (keep_min == other_less) key = ok_, idx = oi;
+                }
             }
+        };
+        unsigned long long bkey = 0xFFF0000000000000ull;
+        int bidx = INT_MAX;
+        for (int j0 = 0; j0 < na; j0 += 32) {
+            const int j = j0 + lane;
+            const bool ok = j < na && w.agf[j] >= 0;
+            unsigned long long key = ok ? (unsigned long long)__double_as_longlong(w.agd[j]) : 0xFFF0000000000000ull;
+            int idx = ok ? j : INT_MAX;
+            sort32(key, idx);
+            if (j0 > 0) {
+                // lanes 16-31 take this chunk's best 16, lanes 0-15 keep the running best
+                const unsigned long long ck = __shfl_sync(FULL, key, lane - 16);
+                const int ci = __shfl_sync(FULL, idx, lane - 16);
+                key = lane < 16 ? bkey : ck;
+                idx = lane < 16 ? bidx : ci;
+                sort32(key, idx);
+            }
+            bkey = key;
+            bidx = idx;
         }
-        if (lane < Ka && lane < nvalid) w.sel[lane] = idx;
+        if (lane < Ka && lane < nvalid) w.sel[lane] = bidx;
     } else {
         for (int j0 = 0; j0 < na; j0 += 32) {
             const int j = j0 + lane;

@@ -84,15 +84,16 @@ def test_reference_accepts_expanded_scenarios():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("dones_off", [True, False])
-def test_controlled_env_matches_reference(dones_off):
-    src = _c2(count=3, agents=8)
+@pytest.mark.parametrize("dones_off,agents", [(True, 8), (False, 8), (True, 40)])
+def test_controlled_env_matches_reference(dones_off, agents):
+    """agents=40: more than 32 agents per row (the chunked agent ordering)."""
+    src = _c2(count=3, agents=agents)
     exp = z.controlled_expand(src)
     cfg = z.SimConfig(disable_dones=dones_off)
     genv = z.Env(src, config=cfg, controlled=True)
-    assert genv.info.controlled == 1 and genv.info.scenarios == 3 and genv.info.batch == 24
-    assert list(genv.row_scenario) == [s for s in range(3) for _ in range(8)]
-    assert list(genv.row_actor) == list(range(8)) * 3
+    assert genv.info.controlled == 1 and genv.info.scenarios == 3 and genv.info.batch == 3 * agents
+    assert list(genv.row_scenario) == [s for s in range(3) for _ in range(agents)]
+    assert list(genv.row_actor) == list(range(agents)) * 3
     renv = refpy.RefEnv(exp, config=cfg) if refpy.available() else None
     if renv is None:
         from oracle import portpy
@@ -100,10 +101,11 @@ def test_controlled_env_matches_reference(dones_off):
     g, i, l = renv.scalars()
     assert np.array_equal(g, genv._goal_s) and np.array_equal(i, genv._initial_s) and np.array_equal(l, genv._logged)
     B = genv.info.batch
-    A, S = z.random_actions(91, B, seed=5)
+    steps = 91 if agents <= 8 else 30
+    A, S = z.random_actions(steps, B, seed=5)
     sg, sr = genv.init_state(42), renv.init_state(42)
     errs = compare_state(sg, sr, "reset ")
-    for t in range(91):
+    for t in range(steps):
         errs += compare_obs(genv.observe(sg), renv.observe(sr), f"t{t} ")
         ng, sog = genv.step(sg, A[t], S[t])
         nr, sor = renv.step(sr, A[t], S[t])
