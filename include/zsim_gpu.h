@@ -262,6 +262,90 @@ ZSIM_API int zsim_check_errors(zsim_env* env, void* stream);
  * rows with latched collision, off_route, red_light, stop_line, goal_reached
  * event bits, sum over rows of (proj_s - initial_s) in micrometres}.  Integer
  * so a cross-GPU ncclAllReduce(sum) is exact.  `out_dev` is device memory. */
+/* ---- Device rollout recording --------------------
+ * EpisodeBatch (simcore.hpp:167-186) in device memory: [B][T] row-major
+ * arrays (index b*horizon + t) and B-vectors. */
+typedef struct zsim_episode_view {
+    int32_t* accel_idx;
+    int32_t* steer_idx;
+    float* logp;
+    float* value;
+    float* reward;
+    float* s;
+    float* a_lat;
+    float* a_lon;
+    float* v;
+    uint8_t* done;
+    uint8_t* mask;
+    float* bootstrap;       /* [B] */
+    uint8_t* terminal;      /* [B] DoneReason */
+    uint8_t* events;        /* [B] */
+    float* initial_s;       /* [B] */
+    float* logged_progress; /* [B] */
+    int32_t horizon;        /* T of these buffers */
+    int32_t reserved;
+} zsim_episode_view;
+
+/* One device allocation for an EpisodeBatch of `horizon` steps. */
+ZSIM_API int zsim_episode_alloc(zsim_env* env, int32_t horizon, zsim_episode_view* out);
+ZSIM_API int zsim_episode_free(zsim_env* env, zsim_episode_view* ep);
+/* Bytes of one EpisodeBatch blob and carving of caller memory (host or device)
+ * into a view; copies between carved views are single DMAs (dir 0 h2d, 1 d2h, 2 d2d). */
+ZSIM_API int zsim_episode_bytes(const zsim_env* env, int32_t horizon, size_t* bytes);
+ZSIM_API int zsim_episode_carve(const zsim_env* env, int32_t horizon, void* base, zsim_episode_view* out);
+ZSIM_API int zsim_episode_copy(const zsim_env* env, const zsim_episode_view* dst, const zsim_episode_view* src,
+                               int32_t dir, void* stream);
+/* Env::rollout(ScriptedPolicy, horizon, seed) (simcore.cpp:554-618 with
+ * simcore.cpp:69-84) on the device: `accel` / `steer` are a device action
+ * script [script_len][B] (time-major) read at each row's state.t (the zero
+ * action past its end, as ScriptedPolicy); logp and value are 0 (the scripted
+ * policy's PolicyOut).  Records every EpisodeBatch field into `ep`; `obs`
+ * (NULL or horizon+1 device observation views) receives obs[0..T-1] and the
+ * final observation; `final_state` (NULL or a device state) receives the
+ * final state.  Stream-ordered, graph-capturable; bad action indices are
+ * reported by zsim_check_errors. */
+ZSIM_API int zsim_rollout(zsim_env* env, uint64_t seed, int32_t horizon, const int32_t* accel, const int32_t* steer,
+                          int32_t script_len, const zsim_episode_view* ep, const zsim_obs_view* obs,
+                          const zsim_state_view* final_state, void* stream);
+
+/* ---- Episode metrics on the device (metrics.cpp:13-131) ---- */
+typedef struct zsim_score_bounds {
+    double progress, collision, off_route, stop_line, traffic_light, comfort;
+} zsim_score_bounds;
+typedef struct zsim_comfort_weights {
+    double w_accel, w_jerk;
+} zsim_comfort_weights;
+ZSIM_API int zsim_score_defaults(zsim_score_bounds* bounds, zsim_comfort_weights* weights);
+/* Per-row MetricReport (metrics.hpp:25-38), device [B] arrays; any may be NULL. */
+typedef struct zsim_metric_view {
+    double* relative_progress_raw;
+    double* relative_progress;
+    double* collision_free;
+    double* off_route_free;
+    double* stop_line_free;
+    double* traffic_light_free;
+    double* mixed_comfort;
+    double* scenario_score;
+    uint8_t* degenerate;
+    uint8_t* failed;
+    uint8_t* goal_reached;
+} zsim_metric_view;
+/* Aggregate partial sums: [non-degenerate rows, degenerate rows, sum score,
+ * sum relative_progress, sum raw ratio, sum collision_free, sum off_route_free,
+ * sum stop_line_free, sum traffic_light_free, sum comfort, failed rows, goal rows]. */
+#define ZSIM_AGG_LEN 12
+/* score_episode for every row of `ep` + this GPU's Aggregate partial sums
+ * (fixed-order reduction: deterministic for a given B) into device double[12]. */
+ZSIM_API int zsim_episode_metrics(zsim_env* env, const zsim_episode_view* ep, const zsim_score_bounds* bounds,
+                                  const zsim_comfort_weights* weights, const zsim_metric_view* rows, double* sums_dev,
+                                  void* stream);
+/* metrics::aggregate (metrics.cpp:97-131) from `n_parts` host partial-sum
+ * vectors summed in order (e.g. rank order after an all-gather): out12 =
+ * [scenarios, degenerate, mean_score, mean_relative_progress,
+ * mean_progress_ratio_raw, mean_collision_free, mean_off_route_free,
+ * mean_stop_line_free, mean_traffic_light_free, mean_comfort, failure_rate, goal_rate]. */
+ZSIM_API int zsim_aggregate_finalize(const double* sums, int32_t n_parts, double* out12);
+
 #define ZSIM_STATS_LEN 8
 ZSIM_API int zsim_episode_stats(zsim_env* env, const zsim_state_view* state, int64_t* out_dev, void* stream);
 

@@ -299,6 +299,48 @@ __attribute__((visibility("default"))) int zref_aggregate(int32_t B, int32_t T, 
     });
 }
 
+// Env::rollout (simcore.cpp:554-618) with the reference ScriptedPolicy
+// (simcore.cpp:69-84) over a per-row script [B][script_len] of action
+// indices; copies every EpisodeBatch array out ([B][T] row-major, B-vectors).
+__attribute__((visibility("default"))) int zref_rollout(zref_env* e, int32_t horizon, int32_t script_len,
+                                                        const int32_t* accel, const int32_t* steer, uint64_t seed,
+                                                        int32_t* o_accel, int32_t* o_steer, float* o_logp,
+                                                        float* o_value, float* o_reward, float* o_s, float* o_alat,
+                                                        float* o_alon, float* o_v, uint8_t* o_done, uint8_t* o_mask,
+                                                        float* o_bootstrap, uint8_t* o_terminal, uint8_t* o_events,
+                                                        float* o_initial_s, float* o_logged) {
+    return guarded([&] {
+        const int B = e->env->batch_size();
+        std::vector<std::vector<std::pair<int32_t, int32_t>>> script(static_cast<size_t>(B));
+        for (int b = 0; b < B; ++b)
+            for (int t = 0; t < script_len; ++t)
+                script[size_t(b)].emplace_back(accel[size_t(b) * script_len + t], steer[size_t(b) * script_len + t]);
+        const auto& tab = e->env->action_table();
+        sim::ScriptedPolicy pol(std::move(script), tab.nearest_accel(0.0), tab.nearest_steer(0.0));
+        sim::EpisodeBatch ep = e->env->rollout(pol, horizon, seed);
+        const size_t n = size_t(B) * size_t(horizon);
+        std::copy(ep.accel_idx.begin(), ep.accel_idx.end(), o_accel);
+        std::copy(ep.steer_idx.begin(), ep.steer_idx.end(), o_steer);
+        std::copy(ep.logp.begin(), ep.logp.end(), o_logp);
+        std::copy(ep.value.begin(), ep.value.end(), o_value);
+        std::copy(ep.reward.begin(), ep.reward.end(), o_reward);
+        std::copy(ep.s.begin(), ep.s.end(), o_s);
+        std::copy(ep.a_lat.begin(), ep.a_lat.end(), o_alat);
+        std::copy(ep.a_lon.begin(), ep.a_lon.end(), o_alon);
+        std::copy(ep.v.begin(), ep.v.end(), o_v);
+        std::copy(ep.done.begin(), ep.done.end(), o_done);
+        std::copy(ep.mask.begin(), ep.mask.end(), o_mask);
+        (void)n;
+        for (int b = 0; b < B; ++b) {
+            o_bootstrap[b] = ep.bootstrap[size_t(b)];
+            o_terminal[b] = uint8_t(ep.terminal[size_t(b)]);
+            o_events[b] = ep.events[size_t(b)];
+            o_initial_s[b] = ep.initial_s[size_t(b)];
+            o_logged[b] = ep.logged_progress[size_t(b)];
+        }
+    });
+}
+
 // CPU baseline: `threads` per-thread Env shards (threads = 1 each, which
 // avoids the Env::Pool startup race) over a contiguous split of
 // rows [0, n_rows) of `path` (row r is record r % size).  Each shard runs

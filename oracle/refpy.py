@@ -38,6 +38,11 @@ _SIGS = {
     "zref_aggregate": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                  C.POINTER(C.c_float), C.POINTER(C.c_uint8), C.POINTER(C.c_uint8),
                                  C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_double)]),
+    "zref_rollout": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_uint64,
+                               C.POINTER(C.c_int32), C.POINTER(C.c_int32)] + [C.POINTER(C.c_float)] * 7
+                     + [C.POINTER(C.c_uint8)] * 2 + [C.POINTER(C.c_float), C.POINTER(C.c_uint8),
+                                                     C.POINTER(C.c_uint8), C.POINTER(C.c_float),
+                                                     C.POINTER(C.c_float)]),
     "zref_bench": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(SimConfigC), C.c_int32, C.c_int32,
                              C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_uint64,
                              C.POINTER(C.c_double)]),
@@ -145,6 +150,31 @@ class RefEnv:
         vi, vo = state.view(), ob.view()
         _check(lib().zref_observe(self.handle, C.byref(vi), C.byref(vo)))
         return ob
+
+    def rollout(self, horizon: int, accel, steer, seed: int = 42) -> dict:
+        """Env::rollout with ScriptedPolicy over a per-row script ([B][L] indices):
+        every EpisodeBatch array ([B][T] / [B])."""
+        B = self.batch
+        a = np.ascontiguousarray(accel, dtype=np.int32)
+        s = np.ascontiguousarray(steer, dtype=np.int32)
+        assert a.shape[0] == B and a.shape == s.shape
+        L = a.shape[1]
+        o = {k: np.zeros((B, horizon), dtype=dt) for k, dt in (
+            ("accel_idx", np.int32), ("steer_idx", np.int32), ("logp", np.float32), ("value", np.float32),
+            ("reward", np.float32), ("s", np.float32), ("a_lat", np.float32), ("a_lon", np.float32),
+            ("v", np.float32), ("done", np.uint8), ("mask", np.uint8))}
+        o.update({k: np.zeros(B, dtype=dt) for k, dt in (
+            ("bootstrap", np.float32), ("terminal", np.uint8), ("events", np.uint8), ("initial_s", np.float32),
+            ("logged_progress", np.float32))})
+        P = lambda k, ct: _ptr(o[k], ct)  # noqa: E731
+        _check(lib().zref_rollout(
+            self.handle, int(horizon), int(L), _ptr(a, C.c_int32), _ptr(s, C.c_int32), C.c_uint64(seed),
+            P("accel_idx", C.c_int32), P("steer_idx", C.c_int32), P("logp", C.c_float), P("value", C.c_float),
+            P("reward", C.c_float), P("s", C.c_float), P("a_lat", C.c_float), P("a_lon", C.c_float),
+            P("v", C.c_float), P("done", C.c_uint8), P("mask", C.c_uint8), P("bootstrap", C.c_float),
+            P("terminal", C.c_uint8), P("events", C.c_uint8), P("initial_s", C.c_float),
+            P("logged_progress", C.c_float)))
+        return o
 
 
 def validate(zsim, index: int) -> str:

@@ -62,6 +62,30 @@ class EnvInfo(C.Structure):
     ]
 
 
+class EpisodeView(C.Structure):
+    _fields_ = [("accel_idx", c_int32_p), ("steer_idx", c_int32_p), ("logp", c_float_p), ("value", c_float_p),
+                ("reward", c_float_p), ("s", c_float_p), ("a_lat", c_float_p), ("a_lon", c_float_p),
+                ("v", c_float_p), ("done", c_uint8_p), ("mask", c_uint8_p), ("bootstrap", c_float_p),
+                ("terminal", c_uint8_p), ("events", c_uint8_p), ("initial_s", c_float_p),
+                ("logged_progress", c_float_p), ("horizon", C.c_int32), ("reserved", C.c_int32)]
+
+
+class ScoreBounds(C.Structure):
+    _fields_ = [("progress", C.c_double), ("collision", C.c_double), ("off_route", C.c_double),
+                ("stop_line", C.c_double), ("traffic_light", C.c_double), ("comfort", C.c_double)]
+
+
+class ComfortWeights(C.Structure):
+    _fields_ = [("w_accel", C.c_double), ("w_jerk", C.c_double)]
+
+
+class MetricView(C.Structure):
+    _fields_ = [(n, c_double_p) for n in ("relative_progress_raw", "relative_progress", "collision_free",
+                                          "off_route_free", "stop_line_free", "traffic_light_free",
+                                          "mixed_comfort", "scenario_score")] + \
+               [(n, c_uint8_p) for n in ("degenerate", "failed", "goal_reached")]
+
+
 class StressConfigC(C.Structure):
     _fields_ = [("count", C.c_int32), ("num_steps", C.c_int32), ("agents", C.c_int32),
                 ("road_points", C.c_int32), ("lanes", C.c_int32), ("lane_vertices", C.c_int32),
@@ -85,6 +109,17 @@ SIGNATURES = {
     "zsim_controlled_expand": (C.c_int, [_P, C.c_size_t, C.POINTER(C.c_int64), C.c_int32, C.POINTER(SimConfigC),
                                          C.POINTER(_P), C.POINTER(C.c_size_t)]),
     "zsim_env_destroy": (C.c_int, [_P]),
+    "zsim_episode_alloc": (C.c_int, [_P, C.c_int32, C.POINTER(EpisodeView)]),
+    "zsim_episode_free": (C.c_int, [_P, C.POINTER(EpisodeView)]),
+    "zsim_episode_bytes": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_size_t)]),
+    "zsim_episode_carve": (C.c_int, [_P, C.c_int32, _P, C.POINTER(EpisodeView)]),
+    "zsim_episode_copy": (C.c_int, [_P, C.POINTER(EpisodeView), C.POINTER(EpisodeView), C.c_int32, _P]),
+    "zsim_rollout": (C.c_int, [_P, C.c_uint64, C.c_int32, c_int32_p, c_int32_p, C.c_int32, C.POINTER(EpisodeView),
+                               C.POINTER(ObsView), C.POINTER(StateView), _P]),
+    "zsim_score_defaults": (C.c_int, [C.POINTER(ScoreBounds), C.POINTER(ComfortWeights)]),
+    "zsim_episode_metrics": (C.c_int, [_P, C.POINTER(EpisodeView), C.POINTER(ScoreBounds),
+                                       C.POINTER(ComfortWeights), C.POINTER(MetricView), c_double_p, _P]),
+    "zsim_aggregate_finalize": (C.c_int, [c_double_p, C.c_int32, c_double_p]),
     "zsim_env_get_info": (C.c_int, [_P, C.POINTER(EnvInfo)]),
     "zsim_env_get_scalars": (C.c_int, [_P, c_double_p, c_double_p, c_double_p]),
     "zsim_state_alloc": (C.c_int, [_P, C.POINTER(StateView)]),

@@ -181,6 +181,12 @@ struct zsim_env {
     int32_t* h_act = nullptr;
     cudaStream_t h_stream = nullptr;
     double* d_initial_s = nullptr;
+    double* d_logged = nullptr;          // logged_progress (device rollout recording)
+    void* roll_buf = nullptr;            // zsim_rollout scratch: two states + one observation
+    zsim_state_view roll_s[2]{};
+    zsim_obs_view roll_obs{};
+    zsim_stepout_view roll_so{};
+    double* d_metrics_scratch = nullptr;  // per-block Aggregate partials
     float4* d_hint = nullptr;
     int grid = 0;
 };
@@ -942,6 +948,9 @@ ZSIM_API int zsim_env_destroy(zsim_env* env) {
         cudaFree(env->d_pack);
         cudaFree(env->d_err);
         cudaFree(env->d_initial_s);
+        cudaFree(env->d_logged);
+        cudaFree(env->roll_buf);
+        cudaFree(env->d_metrics_scratch);
         cudaFree(env->d_hint);
         delete env;
     });
@@ -1202,6 +1211,245 @@ ZSIM_API int zsim_episode_stats(zsim_env* env, const zsim_state_view* state, int
         cuda_check(zs::launch_episode_stats(a, env->d_initial_s, reinterpret_cast<long long*>(out_dev),
                                             as_stream(stream)),
                    "episode_stats kernel");
+    });
+}
+
+namespace {
+
+// EpisodeBatch blob: [B][T] arrays then B-vectors, 256-B aligned.
+struct EpisodeLayout {
+    size_t off[16];
+    size_t bytes;
+};
+
+EpisodeLayout episode_layout(int B, int T) {
+    const size_t bt = size_t(B) * size_t(T), b = size_t(B);
+    const size_t sz[16] = {4 * bt, 4 * bt, 4 * bt, 4 * bt, 4 * bt, 4 * bt, 4 * bt, 4 * bt,
+                           4 * bt, bt,     bt,     4 * b,  b,      b,      4 * b,  4 * b};
+    EpisodeLayout L;
+    size_t o = 0;
+    for (int i = 0; i < 16; ++i) {
+        L.off[i] = o;
+        o += al(std::max<size_t>(sz[i], 1));
+    }
+    L.bytes = o;
+    return L;
+}
+
+void carve_episode(unsigned char* p, const EpisodeLayout& L, int T, zsim_episode_view* v) {
+    std::memset(v, 0, sizeof(*v));
+    v->accel_idx = reinterpret_cast<int32_t*>(p + L.off[0]);
+    v->steer_idx = reinterpret_cast<int32_t*>(p + L.off[1]);
+    v->logp = reinterpret_cast<float*>(p + L.off[2]);
+    v->value = reinterpret_cast<float*>(p + L.off[3]);
+    v->reward = reinterpret_cast<float*>(p + L.off[4]);
+    v->s = reinterpret_cast<float*>(p + L.off[5]);
+    v->a_lat = reinterpret_cast<float*>(p + L.off[6]);
+    v->a_lon = reinterpret_cast<float*>(p + L.off[7]);
+    v->v = reinterpret_cast<float*>(p + L.off[8]);
+    v->done = p + L.off[9];
+    v->mask = p + L.off[10];
+    v->bootstrap = reinterpret_cast<float*>(p + L.off[11]);
+    v->terminal = p + L.off[12];
+    v->events = p + L.off[13];
+    v->initial_s = reinterpret_cast<float*>(p + L.off[14]);
+    v->logged_progress = reinterpret_cast<float*>(p + L.off[15]);
+    v->horizon = T;
+}
+
+void check_episode(const zsim_env* env, const zsim_episode_view* ep, const char* what) {
+    check_view(ep, what);
+    if (ep->horizon <= 0 || !ep->reward || !ep->mask || !ep->bootstrap)
+        raise(Err::invalid_argument, std::string(what) + ": episode view not allocated");
+    (void)env;
+}
+
+void ensure_host_arrays(zsim_env* env) {
+    if (!env->d_initial_s) {
+        cuda_check(cudaMalloc(&env->d_initial_s, sizeof(double) * size_t(env->B)), "cudaMalloc(initial_s)");
+        cuda_check(cudaMemcpy(env->d_initial_s, env->initial_s.data(), sizeof(double) * size_t(env->B),
+                              cudaMemcpyHostToDevice),
+                   "upload initial_s");
+    }
+    if (!env->d_logged) {
+        cuda_check(cudaMalloc(&env->d_logged, sizeof(double) * size_t(env->B)), "cudaMalloc(logged_progress)");
+        cuda_check(cudaMemcpy(env->d_logged, env->logged_progress.data(), sizeof(double) * size_t(env->B),
+                              cudaMemcpyHostToDevice),
+                   "upload logged_progress");
+    }
+}
+
+}  // namespace
+
+ZSIM_API int zsim_episode_bytes(const zsim_env* env, int32_t horizon, size_t* bytes) {
+    return guarded([&] {
+        check_view(env, "episode_bytes");
+        check_view(bytes, "episode_bytes");
+        if (horizon <= 0) raise(Err::invalid_argument, "episode: horizon must be > 0");
+        *bytes = episode_layout(env->B, horizon).bytes;
+    });
+}
+
+ZSIM_API int zsim_episode_carve(const zsim_env* env, int32_t horizon, void* base, zsim_episode_view* out) {
+    return guarded([&] {
+        check_view(env, "episode_carve");
+        check_view(base, "episode_carve");
+        check_view(out, "episode_carve");
+        if (horizon <= 0) raise(Err::invalid_argument, "episode: horizon must be > 0");
+        carve_episode(static_cast<unsigned char*>(base), episode_layout(env->B, horizon), horizon, out);
+    });
+}
+
+ZSIM_API int zsim_episode_alloc(zsim_env* env, int32_t horizon, zsim_episode_view* out) {
+    return guarded([&] {
+        check_view(env, "episode_alloc");
+        check_view(out, "episode_alloc");
+        if (horizon <= 0) raise(Err::invalid_argument, "episode: horizon must be > 0");
+        set_device(env);
+        const EpisodeLayout L = episode_layout(env->B, horizon);
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, L.bytes), "cudaMalloc(episode)");
+        cuda_check(cudaMemset(p, 0, L.bytes), "cudaMemset(episode)");
+        carve_episode(static_cast<unsigned char*>(p), L, horizon, out);
+    });
+}
+
+ZSIM_API int zsim_episode_free(zsim_env* env, zsim_episode_view* ep) {
+    return guarded([&] {
+        if (!env || !ep) return;
+        set_device(env);
+        cudaFree(ep->accel_idx);
+        std::memset(ep, 0, sizeof(*ep));
+    });
+}
+
+ZSIM_API int zsim_episode_copy(const zsim_env* env, const zsim_episode_view* dst, const zsim_episode_view* src,
+                               int32_t dir, void* stream) {
+    return guarded([&] {
+        check_view(env, "episode_copy");
+        check_episode(env, dst, "episode_copy");
+        check_episode(env, src, "episode_copy");
+        if (dst->horizon != src->horizon) raise(Err::invalid_argument, "episode_copy: horizon mismatch");
+        const EpisodeLayout L = episode_layout(env->B, src->horizon);
+        cudaSetDevice(env->device);
+        // carved views are one contiguous blob
+        cuda_check(cudaMemcpyAsync(dst->accel_idx, src->accel_idx, L.bytes, kind_of(dir), as_stream(stream)),
+                   "episode copy");
+    });
+}
+
+ZSIM_API int zsim_rollout(zsim_env* env, uint64_t seed, int32_t horizon, const int32_t* accel, const int32_t* steer,
+                          int32_t script_len, const zsim_episode_view* ep, const zsim_obs_view* obs,
+                          const zsim_state_view* final_state, void* stream) {
+    return guarded([&] {
+        check_view(env, "rollout");
+        if (horizon <= 0) raise(Err::invalid_argument, "rollout: horizon must be > 0");
+        if (script_len < 0 || (script_len > 0 && (!accel || !steer)))
+            raise(Err::invalid_argument, "rollout: bad action script");
+        if (ep) {
+            check_episode(env, ep, "rollout");
+            if (ep->horizon != horizon) raise(Err::invalid_argument, "rollout: episode horizon mismatch");
+        }
+        set_device(env);
+        ensure_host_arrays(env);
+        if (!env->roll_buf) {
+            cuda_check(cudaMalloc(&env->roll_buf, 2 * env->sl.bytes + env->ol.bytes + env->sol.bytes),
+                       "cudaMalloc(rollout scratch)");
+            unsigned char* p = static_cast<unsigned char*>(env->roll_buf);
+            carve_state(p, env->sl, &env->roll_s[0]);
+            carve_state(p + env->sl.bytes, env->sl, &env->roll_s[1]);
+            carve_obs(p + 2 * env->sl.bytes, env->ol, &env->roll_obs);
+            carve_stepout(p + 2 * env->sl.bytes + env->ol.bytes, env->sol, &env->roll_so);
+        }
+        cudaStream_t s = as_stream(stream);
+        zs::KernelArgs a = args_for(env);
+        a.seed = seed;
+        a.out = env->roll_s[0];
+        cuda_check(zs::launch_reset(a, env->grid, s), "reset kernel");
+        // obs[0] = observe(reset state)
+        a = args_for(env);
+        a.in = env->roll_s[0];
+        a.obs = obs ? obs[0] : env->roll_obs;
+        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->grid, s), "observe kernel");
+        int cur = 0;
+        for (int t = 0; t < horizon; ++t) {
+            a = args_for(env);
+            a.in = env->roll_s[cur];
+            a.out = env->roll_s[cur ^ 1];
+            a.accel = accel;
+            a.steer = steer;
+            a.act_len = script_len > 0 ? script_len : -1;  // -1: empty script, every row takes the zero action
+            a.zero_accel = env->zero_accel;
+            a.zero_steer = env->zero_steer;
+            a.so = env->roll_so;
+            if (ep) {
+                a.ep = *ep;
+                a.ep_t = t;
+            }
+            a.obs = obs ? obs[t + 1] : env->roll_obs;
+            cuda_check(zs::launch_step_observe(a, zs::kModeStepObserve, env->grid, s), "step+observe kernel");
+            cur ^= 1;
+        }
+        if (ep) {
+            a = args_for(env);
+            a.in = env->roll_s[cur];
+            a.ep = *ep;
+            cuda_check(zs::launch_episode_finalize(a, env->d_initial_s, env->d_logged, s), "episode finalize");
+        }
+        if (final_state) copy_state(env, final_state, &env->roll_s[cur], 2, s);
+    });
+}
+
+ZSIM_API int zsim_score_defaults(zsim_score_bounds* b, zsim_comfort_weights* w) {
+    return guarded([&] {
+        if (b) *b = zsim_score_bounds{0.8, 0.05, 0.5, 0.5, 0.5, 0.8};  // metrics.hpp:11-18
+        if (w) *w = zsim_comfort_weights{0.1, 0.05};                   // metrics.hpp:20-23
+    });
+}
+
+ZSIM_API int zsim_episode_metrics(zsim_env* env, const zsim_episode_view* ep, const zsim_score_bounds* bounds,
+                                  const zsim_comfort_weights* weights, const zsim_metric_view* rows, double* sums_dev,
+                                  void* stream) {
+    return guarded([&] {
+        check_view(env, "episode_metrics");
+        check_episode(env, ep, "episode_metrics");
+        check_view(sums_dev, "episode_metrics");
+        set_device(env);
+        zsim_score_bounds bb;
+        zsim_comfort_weights cw;
+        zsim_score_defaults(&bb, &cw);
+        if (bounds) bb = *bounds;
+        if (weights) cw = *weights;
+        for (double l : {bb.progress, bb.collision, bb.off_route, bb.stop_line, bb.traffic_light, bb.comfort})
+            if (!(l >= 0.0 && l < 1.0)) raise(Err::invalid_argument, "map_score: l outside [0,1)");
+        if (!env->d_metrics_scratch) {
+            cuda_check(cudaMalloc(&env->d_metrics_scratch, sizeof(double) * size_t(zs::metrics_scratch_doubles(env->B))),
+                       "cudaMalloc(metrics scratch)");
+        }
+        zs::KernelArgs a = args_for(env);
+        a.ep = *ep;
+        zsim_metric_view mv{};
+        if (rows) mv = *rows;
+        cuda_check(zs::launch_episode_metrics(a, bb, cw, mv, sums_dev, env->d_metrics_scratch, as_stream(stream)),
+                   "episode_metrics kernel");
+    });
+}
+
+ZSIM_API int zsim_aggregate_finalize(const double* sums, int32_t n_parts, double* out12) {
+    return guarded([&] {
+        if (!sums || !out12 || n_parts <= 0) raise(Err::invalid_argument, "aggregate_finalize: bad arguments");
+        double t[ZSIM_AGG_LEN] = {};
+        for (int p = 0; p < n_parts; ++p)
+            for (int k = 0; k < ZSIM_AGG_LEN; ++k) t[k] += sums[size_t(p) * ZSIM_AGG_LEN + k];
+        // metrics::aggregate (metrics.cpp:120-130)
+        double o[ZSIM_AGG_LEN] = {t[0], t[1], 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (t[0] > 0) {
+            const double n = t[0];
+            for (int k = 2; k <= 9; ++k) o[k] = t[k] / n;
+            o[10] = t[10] / n;
+            o[11] = t[11] / n;
+        }
+        std::memcpy(out12, o, sizeof(o));
     });
 }
 

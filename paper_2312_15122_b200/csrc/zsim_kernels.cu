@@ -1327,6 +1327,25 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     }
 }
 
+// EpisodeBatch cell (b, a.ep_t) of Env::rollout's recording loop
+// (simcore.cpp:596-608); the scripted policy's logp and value are 0.
+__device__ __forceinline__ void record_step(const KernelArgs& a, int b, int mask, int ai, int si, float reward,
+                                            float s, float a_lat, float a_lon, float v, int done) {
+    if (!a.ep.reward) return;
+    const size_t k = size_t(b) * size_t(a.ep.horizon) + size_t(a.ep_t);
+    a.ep.mask[k] = uint8_t(mask);
+    a.ep.accel_idx[k] = ai;
+    a.ep.steer_idx[k] = si;
+    a.ep.logp[k] = 0.f;
+    a.ep.value[k] = 0.f;
+    a.ep.reward[k] = reward;
+    a.ep.s[k] = s;
+    a.ep.a_lat[k] = a_lat;
+    a.ep.a_lon[k] = a_lon;
+    a.ep.v[k] = v;
+    a.ep.done[k] = uint8_t(done);
+}
+
 // ---------------------------------------------------------------------------
 // step one row (simcore.cpp:278-404): reads w.rs->r0, writes the post-step
 // row to w.rs->r (+ output buffers).  When the row is simulated (not passed
@@ -1347,13 +1366,23 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
 
     bool pass = rs.r0.done != 0;
     int ai = 0, si = 0;
-    if (!pass) {
+    if (a.act_len != 0) {
+        // ScriptedPolicy::act (simcore.cpp:69-84): the script at the row's t, else the zero action
+        const int tt = rs.r0.t;
+        if (a.act_len > 0 && tt >= 0 && tt < a.act_len) {
+            ai = a.accel[size_t(tt) * pk.d.B + b];
+            si = a.steer[size_t(tt) * pk.d.B + b];
+        } else {
+            ai = a.zero_accel;
+            si = a.zero_steer;
+        }
+    } else if (!pass) {
         ai = a.accel[b];
         si = a.steer[b];
-        if (ai < 0 || ai >= cfg.n_accel || si < 0 || si >= cfg.n_steer) {
-            if (lane == 0) atomicOr(a.err, 1);
-            pass = true;
-        }
+    }
+    if (!pass && (ai < 0 || ai >= cfg.n_accel || si < 0 || si >= cfg.n_steer)) {
+        if (lane == 0) atomicOr(a.err, 1);
+        pass = true;
     }
     if (pass) {
         // absorbing pass-through (simcore.cpp:281-299); bad-action rows are left unchanged
@@ -1368,6 +1397,7 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
             a.so.a_lat[b] = 0.f;
             a.so.a_lon[b] = 0.f;
             a.so.v[b] = float(r0.v);
+            record_step(a, b, r0.done ? 0 : 1, ai, si, 0.f, float(r0.proj_s), 0.f, 0.f, float(r0.v), r0.done);
         }
         for (int j = lane; j < ns; j += 32) a.out.stopped_flags[soff + j] = w.sflag[j];
         __syncwarp();
@@ -1492,6 +1522,7 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
         a.so.a_lat[b] = float(a_lat);
         a.so.a_lon[b] = float(a_lon);
         a.so.v[b] = float(vn);
+        record_step(a, b, 1, ai, si, float(reward), float(p1.s), float(a_lat), float(a_lon), float(vn), done);
     }
     // stopped-flag update with the post-step state (simcore.cpp:390-396)
     for (int j = lane; j < ns; j += 32) {
@@ -1619,6 +1650,128 @@ __global__ void __launch_bounds__(256) k_episode_stats(const KernelArgs a, const
         atomicAdd(reinterpret_cast<unsigned long long*>(&out[threadIdx.x]), (unsigned long long)acc[threadIdx.x]);
 }
 
+// EpisodeBatch tail (simcore.cpp:580-587, 610-617): bootstrap = done ? 0 :
+// value (the scripted policy's value is 0), terminal reason, latched events,
+// initial_s and logged_progress as float.
+__global__ void __launch_bounds__(256) k_episode_finalize(const KernelArgs a, const double* initial_s,
+                                                          const double* logged) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < a.pk.d.B; b += gridDim.x * blockDim.x) {
+        a.ep.bootstrap[b] = 0.f;
+        a.ep.terminal[b] = a.in.reason[b];
+        a.ep.events[b] = a.in.events[b];
+        a.ep.initial_s[b] = float(initial_s[b]);
+        a.ep.logged_progress[b] = float(logged[b]);
+    }
+}
+
+constexpr int kMetricsThreads = 256;
+constexpr int kAggLen = 12;
+
+// map_score (metrics.cpp:13-17); arguments are in range by construction.
+__device__ __forceinline__ double map_score(double s, double l) { return s * (1.0 - l) + l; }
+
+// metrics::score_episode (metrics.cpp:54-95) per row, thread per row, and
+// this block's Aggregate partial sums (metrics.cpp:97-131) in a fixed order:
+// each thread sums its rows in index order, then a fixed smem tree.
+__global__ void __launch_bounds__(kMetricsThreads) k_episode_metrics(const KernelArgs a, zsim_score_bounds bb,
+                                                                    zsim_comfort_weights cw, zsim_metric_view out,
+                                                                    double* part) {
+    __shared__ double red[kAggLen][kMetricsThreads];
+    double acc[kAggLen];
+#pragma unroll
+    for (int k = 0; k < kAggLen; ++k) acc[k] = 0.0;
+    const zsim_episode_view& ep = a.ep;
+    const int T = ep.horizon;
+    const double dt = a.pk.dt;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < a.pk.d.B; b += gridDim.x * blockDim.x) {
+        const size_t row = size_t(b) * size_t(T);
+        const double logged = double(ep.logged_progress[b]);
+        int last_live = -1;
+        for (int t = 0; t < T; ++t)
+            if (ep.mask[row + t]) last_live = t;
+        const double init = double(ep.initial_s[b]);
+        const double final_s = last_live >= 0 ? double(ep.s[row + last_live]) : init;
+        const double moved = final_s - init;
+        const bool degenerate = logged <= 0.1;
+        const double raw = degenerate ? 0.0 : moved / logged;
+        const double rel = degenerate ? 0.0 : clampd(raw, 0.0, 1.0);
+        const int ev = ep.events[b];
+        const double coll = (ev & 1) ? 0.0 : 1.0, off = (ev & 2) ? 0.0 : 1.0, light = (ev & 4) ? 0.0 : 1.0,
+                     stop = (ev & 8) ? 0.0 : 1.0;
+        const bool goal = (ev & 16) != 0;
+        const bool failed = coll == 0.0 || off == 0.0;
+        // mixed_comfort (metrics.cpp:29-52)
+        double cacc = 0.0, prev_lat = 0.0, prev_lon = 0.0;
+        bool have_prev = false;
+        long long live = 0;
+        for (int t = 0; t < T; ++t) {
+            if (!ep.mask[row + t]) break;
+            const double al = ep.a_lat[row + t], ao = ep.a_lon[row + t];
+            double jl = 0.0, jo = 0.0;
+            if (have_prev) {
+                jl = (al - prev_lat) / dt;
+                jo = (ao - prev_lon) / dt;
+            }
+            cacc += cw.w_accel * (al * al + ao * ao) + cw.w_jerk * (jl * jl + jo * jo);
+            prev_lat = al;
+            prev_lon = ao;
+            have_prev = true;
+            ++live;
+        }
+        const double comfort = live == 0 ? 1.0 : exp(-cacc / double(live));
+        double score = map_score(rel, bb.progress);
+        score *= map_score(coll, bb.collision);
+        score *= map_score(off, bb.off_route);
+        score *= map_score(stop, bb.stop_line);
+        score *= map_score(light, bb.traffic_light);
+        score *= map_score(comfort, bb.comfort);
+        if (out.relative_progress_raw) out.relative_progress_raw[b] = raw;
+        if (out.relative_progress) out.relative_progress[b] = rel;
+        if (out.collision_free) out.collision_free[b] = coll;
+        if (out.off_route_free) out.off_route_free[b] = off;
+        if (out.stop_line_free) out.stop_line_free[b] = stop;
+        if (out.traffic_light_free) out.traffic_light_free[b] = light;
+        if (out.mixed_comfort) out.mixed_comfort[b] = comfort;
+        if (out.scenario_score) out.scenario_score[b] = score;
+        if (out.degenerate) out.degenerate[b] = degenerate ? 1 : 0;
+        if (out.failed) out.failed[b] = failed ? 1 : 0;
+        if (out.goal_reached) out.goal_reached[b] = goal ? 1 : 0;
+        if (degenerate) {
+            acc[1] += 1.0;
+            continue;
+        }
+        acc[0] += 1.0;
+        acc[2] += score;
+        acc[3] += rel;
+        acc[4] += raw;
+        acc[5] += coll;
+        acc[6] += off;
+        acc[7] += stop;
+        acc[8] += light;
+        acc[9] += comfort;
+        acc[10] += failed ? 1.0 : 0.0;
+        acc[11] += goal ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kAggLen; ++k) red[k][threadIdx.x] = acc[k];
+    __syncthreads();
+    for (int half = kMetricsThreads / 2; half > 0; half >>= 1) {
+        if (threadIdx.x < half)
+            for (int k = 0; k < kAggLen; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + half];
+        __syncthreads();
+    }
+    if (threadIdx.x < kAggLen) part[size_t(blockIdx.x) * kAggLen + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// Block partials summed in block order (deterministic for a given B).
+__global__ void k_metrics_sum(const double* part, int nblk, double* sums) {
+    const int k = threadIdx.x;
+    if (k >= kAggLen) return;
+    double s = 0.0;
+    for (int i = 0; i < nblk; ++i) s += part[size_t(i) * kAggLen + k];
+    sums[k] = s;
+}
+
 }  // namespace
 
 #ifdef ZS_PATHSTATS
@@ -1692,6 +1845,32 @@ cudaError_t launch_episode_stats(const KernelArgs& a, const double* initial_s, l
     int grid = (a.pk.d.B + 255) / 256;
     if (grid > 148 * 4) grid = 148 * 4;
     k_episode_stats<<<grid, 256, 0, stream>>>(a, initial_s, out);
+    return cudaGetLastError();
+}
+
+static int metrics_blocks(int B) {
+    int g = (B + kMetricsThreads - 1) / kMetricsThreads;
+    return g < 148 * 2 ? (g > 0 ? g : 1) : 148 * 2;
+}
+
+int metrics_scratch_doubles(int B) { return metrics_blocks(B) * kAggLen; }
+
+cudaError_t launch_episode_finalize(const KernelArgs& a, const double* initial_s, const double* logged,
+                                    cudaStream_t stream) {
+    int grid = (a.pk.d.B + 255) / 256;
+    if (grid > 148 * 4) grid = 148 * 4;
+    k_episode_finalize<<<grid > 0 ? grid : 1, 256, 0, stream>>>(a, initial_s, logged);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_episode_metrics(const KernelArgs& a, const zsim_score_bounds& bounds,
+                                   const zsim_comfort_weights& weights, const zsim_metric_view& rows, double* sums,
+                                   double* scratch, cudaStream_t stream) {
+    const int nblk = metrics_blocks(a.pk.d.B);
+    k_episode_metrics<<<nblk, kMetricsThreads, 0, stream>>>(a, bounds, weights, rows, scratch);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_metrics_sum<<<1, 32, 0, stream>>>(scratch, nblk, sums);
     return cudaGetLastError();
 }
 

@@ -39,11 +39,24 @@ struct KernelArgs {
     int32_t key_cap;   // >= max(P, R)
     int32_t cand_cap;  // top-k candidate capacity per warp (= 32 x kMaxCandPerLane)
     SmemLayout lay;    // filled by the launchers
+    // device rollout (zsim_rollout): recording target and scripted actions
+    zsim_episode_view ep;  // ep.reward == nullptr: no recording
+    int32_t ep_t;          // rollout step being recorded
+    int32_t act_len;       // > 0: accel/steer are a [act_len][B] script read at state.t (ScriptedPolicy); -1: empty
+    int32_t zero_accel, zero_steer;
 };
 
 size_t smem_bytes(const KernelArgs& a);
 cudaError_t launch_step_observe(const KernelArgs& a, int mode, int grid, cudaStream_t stream);
 cudaError_t launch_reset(const KernelArgs& a, int grid, cudaStream_t stream);
 cudaError_t launch_episode_stats(const KernelArgs& a, const double* initial_s, long long* out, cudaStream_t stream);
+// EpisodeBatch tail (bootstrap / terminal / events / initial_s / logged_progress) from the final state a.in
+cudaError_t launch_episode_finalize(const KernelArgs& a, const double* initial_s, const double* logged,
+                                   cudaStream_t stream);
+// score_episode per row + fixed-order Aggregate partial sums (double[12]) of a.ep
+cudaError_t launch_episode_metrics(const KernelArgs& a, const zsim_score_bounds& bounds,
+                                   const zsim_comfort_weights& weights, const zsim_metric_view& rows, double* sums,
+                                   double* scratch, cudaStream_t stream);
+int metrics_scratch_doubles(int B);
 
 }  // namespace zs

@@ -23,7 +23,8 @@ from pathlib import Path
 
 import numpy as np
 
-from ._abi import (EnvInfo, ObsView, SimConfigC, StateView, StepOutView, StressConfigC, ZsimError, check, lib)
+from ._abi import (ComfortWeights, EnvInfo, EpisodeView, MetricView, ObsView, ScoreBounds, SimConfigC, StateView,
+                   StepOutView, StressConfigC, ZsimError, check, lib)
 
 DONE_REASONS = ("none", "collision", "off_route", "red_light", "stop_line", "goal_reached")
 ACTIVE_FEAT, AGENT_FEAT, ROAD_FEAT, ROUTE_FEAT, VALUE_FEAT = 9, 6, 12, 5, 2  # ObsSpec (simcore.hpp:60-72)
@@ -245,6 +246,25 @@ class DeviceObs(_DeviceBuf):
     pass
 
 
+class DeviceEpisode(_DeviceBuf):
+    """A device EpisodeBatch (zsim_episode_alloc)."""
+
+
+EPISODE_BT = ("accel_idx", "steer_idx", "logp", "value", "reward", "s", "a_lat", "a_lon", "v", "done", "mask")
+EPISODE_B = ("bootstrap", "terminal", "events", "initial_s", "logged_progress")
+AGGREGATE_FIELDS = ("scenarios", "degenerate", "mean_score", "mean_relative_progress", "mean_progress_ratio_raw",
+                    "mean_collision_free", "mean_off_route_free", "mean_stop_line_free",
+                    "mean_traffic_light_free", "mean_comfort", "failure_rate", "goal_rate")
+
+
+def aggregate_finalize(partials) -> dict:
+    """metrics::aggregate from per-GPU partial sums ([n][12], summed in order)."""
+    p = np.ascontiguousarray(np.atleast_2d(np.asarray(partials, dtype=np.float64)))
+    out = np.zeros(12)
+    check(lib.zsim_aggregate_finalize(_ptr(p, C.c_double), int(p.shape[0]), _ptr(out, C.c_double)))
+    return dict(zip(AGGREGATE_FIELDS, out.tolist()))
+
+
 def _stream(s) -> C.c_void_p:
     if s is None:
         return C.c_void_p(0)
@@ -417,6 +437,79 @@ class Env:
         """int64[8] episode-stats vector of `state` into device memory `out_ptr`."""
         check(lib.zsim_episode_stats(self.handle, C.byref(state.v), C.cast(C.c_void_p(out_ptr),
                                                                            C.POINTER(C.c_int64)), _stream(stream)))
+
+    # ---- device rollout recording + metrics (SURVEY.md 8f rows 1-2) ----
+    def device_episode(self, horizon: int) -> DeviceEpisode:
+        v = EpisodeView()
+        check(lib.zsim_episode_alloc(self.handle, int(horizon), C.byref(v)))
+        return DeviceEpisode(self, v, lib.zsim_episode_free)
+
+    def rollout_device(self, seed: int, horizon: int, accel_ptr: int, steer_ptr: int, script_len: int,
+                       episode: DeviceEpisode | None = None, obs: list | None = None,
+                       final_state: DeviceState | None = None, stream=None) -> None:
+        """Env::rollout(ScriptedPolicy) on the device: the script is a device
+        int32 [script_len][B] pair read at each row's t.  `obs`: None or a list
+        of horizon+1 DeviceObs (obs[0..T-1] and the final observation)."""
+        ov = None
+        if obs is not None:
+            assert len(obs) == horizon + 1
+            arr = (ObsView * (horizon + 1))(*[o.v for o in obs])
+            ov = arr
+        check(lib.zsim_rollout(self.handle, C.c_uint64(seed), int(horizon),
+                               C.cast(C.c_void_p(accel_ptr), C.POINTER(C.c_int32)),
+                               C.cast(C.c_void_p(steer_ptr), C.POINTER(C.c_int32)), int(script_len),
+                               C.byref(episode.v) if episode is not None else None, ov,
+                               C.byref(final_state.v) if final_state is not None else None, _stream(stream)))
+
+    def download_episode(self, ep: DeviceEpisode) -> dict:
+        """Host copy of a device EpisodeBatch: [B][T] and [B] numpy arrays."""
+        B, T = self.info.batch, ep.v.horizon
+        n = C.c_size_t()
+        check(lib.zsim_episode_bytes(self.handle, T, C.byref(n)))
+        buf = np.zeros(n.value, dtype=np.uint8)
+        hv = EpisodeView()
+        check(lib.zsim_episode_carve(self.handle, T, C.c_void_p(buf.ctypes.data), C.byref(hv)))
+        check(lib.zsim_episode_copy(self.handle, C.byref(hv), C.byref(ep.v), 1, None))
+        check(lib.zsim_check_errors(self.handle, None))
+        out = {}
+        types = {"accel_idx": np.int32, "steer_idx": np.int32, "done": np.uint8, "mask": np.uint8,
+                 "terminal": np.uint8, "events": np.uint8}
+        for f in EPISODE_BT + EPISODE_B:
+            dt = types.get(f, np.float32)
+            cnt = B * T if f in EPISODE_BT else B
+            addr = C.cast(getattr(hv, f), C.c_void_p).value
+            out[f] = np.frombuffer((C.c_char * (cnt * np.dtype(dt).itemsize)).from_address(addr),
+                                   dtype=dt).copy().reshape((B, T) if f in EPISODE_BT else (B,))
+        return out
+
+    def episode_metrics(self, ep: DeviceEpisode, rows: bool = True, bounds: dict | None = None,
+                        weights: dict | None = None):
+        """metrics::score_episode per row (host dict of [B] arrays, or None)
+        and this GPU's Aggregate partial sums (12 doubles)."""
+        import torch  # device buffers for the outputs
+        B = self.info.batch
+        dev = torch.device("cuda", self.info.device)
+        sums = torch.zeros(12, dtype=torch.float64, device=dev)
+        bb, cw = ScoreBounds(), ComfortWeights()
+        check(lib.zsim_score_defaults(C.byref(bb), C.byref(cw)))
+        for k, v in (bounds or {}).items():
+            setattr(bb, k, v)
+        for k, v in (weights or {}).items():
+            setattr(cw, k, v)
+        mv = MetricView()
+        keep = {}
+        if rows:
+            for name, ct in MetricView._fields_:
+                t = torch.zeros(B, dtype=torch.float64 if ct is not C.POINTER(C.c_uint8) else torch.uint8,
+                                device=dev)
+                keep[name] = t
+                setattr(mv, name, C.cast(C.c_void_p(t.data_ptr()), ct))
+        check(lib.zsim_episode_metrics(self.handle, C.byref(ep.v), C.byref(bb), C.byref(cw),
+                                       C.byref(mv) if rows else None,
+                                       C.cast(C.c_void_p(sums.data_ptr()), C.POINTER(C.c_double)), None))
+        torch.cuda.synchronize(dev)
+        per_row = {k: v.cpu().numpy() for k, v in keep.items()} if rows else None
+        return per_row, sums.cpu().numpy()
 
     def set_debug_topk(self, dev_ptr: int | None) -> None:
         check(lib.zsim_set_debug_topk(self.handle, C.cast(C.c_void_p(dev_ptr or 0), C.POINTER(C.c_int32))))
