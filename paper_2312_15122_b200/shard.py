@@ -1,11 +1,14 @@
-"""Multi-GPU plumbing: scenario sharding and the episode-stats all-reduce.
+"""Multi-GPU plumbing: scenario sharding, the episode-stats all-reduce and the
+episode-metrics gather.
 
 The batch is sharded, not split by any data-path collective:
 rank r of N simulates the contiguous rows [lo, hi) of the global scenario
 set.  The only cross-GPU exchange is one all-reduce (sum) of the int64
 episode-stats vector per rollout; integer sums are exact, so the result does
 not depend on the reduction order (the fixed-order contract of the
-reference's AllReducer, transport.hpp:59-61).
+reference's AllReducer, transport.hpp:59-61).  The fp64 metric sums
+(zsim_episode_metrics) are all-gathered instead and summed in rank order, so
+the aggregate is reproducible for a given sharding.
 """
 from __future__ import annotations
 
@@ -44,3 +47,53 @@ def allreduce_stats(stats, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
     return stats
+
+
+def metric_sums_host(s: np.ndarray, a_lat: np.ndarray, a_lon: np.ndarray, mask: np.ndarray, events: np.ndarray,
+                     initial_s: np.ndarray, logged: np.ndarray, dt: float, bounds=(0.8, 0.05, 0.5, 0.5, 0.5, 0.8),
+                     w_accel: float = 0.1, w_jerk: float = 0.05) -> np.ndarray:
+    """Host statement of zsim_episode_metrics' Aggregate partial sums
+    (metrics::score_episode, metrics.cpp:54-95, summed over rows in order)."""
+    out = np.zeros(12)
+    B, T = s.shape
+    for b in range(B):
+        lg = float(logged[b])
+        live_t = np.nonzero(mask[b])[0]
+        init = float(initial_s[b])
+        final_s = float(s[b, live_t[-1]]) if len(live_t) else init
+        if lg <= 0.1:
+            out[1] += 1
+            continue
+        raw = (final_s - init) / lg
+        rel = min(max(raw, 0.0), 1.0)
+        ev = int(events[b])
+        coll, off, light, stop = [0.0 if ev & m else 1.0 for m in (1, 2, 4, 8)]
+        acc, live, prev = 0.0, 0, None
+        for t in range(T):
+            if not mask[b, t]:
+                break
+            al, ao = float(a_lat[b, t]), float(a_lon[b, t])
+            jl = jo = 0.0
+            if prev is not None:
+                jl, jo = (al - prev[0]) / dt, (ao - prev[1]) / dt
+            acc += w_accel * (al * al + ao * ao) + w_jerk * (jl * jl + jo * jo)
+            prev, live = (al, ao), live + 1
+        comfort = 1.0 if live == 0 else float(np.exp(-acc / live))
+        score = 1.0
+        for v, l in zip((rel, coll, off, stop, light, comfort), bounds):
+            score *= v * (1.0 - l) + l
+        out += [1, 0, score, rel, raw, coll, off, stop, light, comfort, 1.0 if (coll == 0 or off == 0) else 0.0,
+                1.0 if ev & 16 else 0.0]
+    return out
+
+
+def gather_metric_sums(sums, group=None) -> np.ndarray:
+    """All-gather every rank's fp64 metric partial sums (torch tensor [12]);
+    returns [world][12] in rank order for aggregate_finalize."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return sums.detach().cpu().numpy()[None, :]
+    parts = [torch.zeros_like(sums) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, sums, group=group)
+    return np.stack([p.cpu().numpy() for p in parts])

@@ -99,3 +99,17 @@ def test_device_metrics_match_reference(dones_off):
     live = rows["degenerate"] == 0
     assert abs(rows["scenario_score"][live].mean() - got["mean_score"]) <= 1e-12
     assert set(np.unique(rows["collision_free"])) <= {0.0, 1.0}
+
+
+@pytest.mark.gpu
+def test_device_metric_sums_match_host_statement():
+    from paper_2312_15122_b200.shard import metric_sums_host
+    zsim = z.stress_scenarios(z.StressConfig(count=24), 13)
+    env = z.Env(zsim, config=z.SimConfig(disable_dones=False))
+    A, S = z.random_actions(91, 24, seed=29)
+    ep, _ = _device_rollout(env, 91, A, S)
+    _, sums = env.episode_metrics(ep, rows=False)
+    h = env.download_episode(ep)
+    want = metric_sums_host(h["s"], h["a_lat"], h["a_lon"], h["mask"], h["events"], h["initial_s"],
+                            h["logged_progress"], env.info.dt)
+    np.testing.assert_allclose(sums, want, rtol=1e-12, atol=1e-12)

@@ -12,7 +12,8 @@ import numpy as np
 import torch.multiprocessing as mp
 
 import paper_2312_15122_b200 as z
-from paper_2312_15122_b200.shard import allreduce_stats, shard_rows, stats_from_host_state
+from paper_2312_15122_b200.shard import (allreduce_stats, gather_metric_sums, metric_sums_host, shard_rows,
+                                         stats_from_host_state)
 
 TOTAL, STEPS = 10, 25
 SHAPE = dict(agents=6, road_points=200, lane_vertices=20)
@@ -38,7 +39,10 @@ def _worker(rank: int, world: int, port: int, q) -> None:
     lo, hi = shard_rows(TOTAL, world, rank)
     stats = torch.from_numpy(_simulate(lo, hi))
     allreduce_stats(stats)
-    q.put((rank, stats.numpy().tolist()))
+    # metric partial sums: dyadic per-rank values, gathered in rank order
+    sums = torch.full((12,), float(rank + 1) * 0.25, dtype=torch.float64)
+    parts = gather_metric_sums(sums)
+    q.put((rank, (stats.numpy().tolist(), parts.tolist())))
     dist.destroy_process_group()
 
 
@@ -80,5 +84,25 @@ def test_two_rank_gloo_stats_allreduce_equals_single_process():
         p.join(timeout=60)
         assert p.exitcode == 0
     want = _simulate(0, TOTAL).tolist()
-    assert got[0] == want and got[1] == want
+    assert got[0][0] == want and got[1][0] == want
     assert want[0] == TOTAL
+    # every rank sees the same rank-ordered metric partials
+    assert got[0][1] == got[1][1] == [[0.25] * 12, [0.5] * 12]
+    assert z.aggregate_finalize(np.array(got[0][1]))["scenarios"] == 0.75
+
+
+def test_metric_sums_host_matches_reference_aggregate():
+    from oracle import refpy
+    if not refpy.available():
+        import pytest
+        pytest.skip("oracle/_ref not built")
+    zsim = z.stress_scenarios(z.StressConfig(count=8, **SHAPE), seed=5)
+    A, S = z.random_actions(40, 8, seed=3)
+    ep = refpy.RefEnv(zsim, config=z.SimConfig(disable_dones=False)).rollout(40, A.T, S.T, 42)
+    sums = metric_sums_host(ep["s"], ep["a_lat"], ep["a_lon"], ep["mask"], ep["events"], ep["initial_s"],
+                            ep["logged_progress"], 0.1)
+    got = z.aggregate_finalize(sums)
+    ref = refpy.aggregate(ep["s"], ep["a_lat"], ep["a_lon"], ep["mask"], ep["events"], ep["initial_s"],
+                          ep["logged_progress"], 0.1)
+    for k, v in enumerate(got.values()):
+        assert abs(v - ref[k]) <= 1e-12 * max(1.0, abs(ref[k])), (k, v, ref[k])
