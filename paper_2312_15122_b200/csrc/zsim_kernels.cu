@@ -589,7 +589,8 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size
 // Upper bound on |fp32 key - fp64 key| for points within sqrt(T)+1 of the
 // query; `ep` is the fp32 rounding error of the query coordinates.
 __device__ __forceinline__ double key_margin(double T, double ep) {
-    double D = sqrt(T) + 1.0;
+    // D >= sqrt(T) + 1: fp32 square root rounded up of T rounded up
+    double D = double(__fsqrt_ru(__double2float_ru(T))) + 1.0;
     double eta = ep + 0x1p-24 * (D + ep);
     double m = 2.0 * eta * (2.0 * D + eta);
     m += 0x1p-22 * (T + m) + 0x1p-50 * T;
@@ -878,8 +879,8 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     // counting-sort counters / cursors live in the (clear) histogram area and
     // the selection is written to `order` after the ranking is complete.
     unsigned* cntb = reinterpret_cast<unsigned*>(hist);  // NB2 u32 counters
-    const double sc2 = double(NB2) / (double(tc) > 0.0 ? double(tc) : 1.0);
     int nvalid_local = 0;
+    double kmax = 0.0;
     for (int c0 = 0; c0 < C; c0 += 32 * 8) {
         // reference indices of 8 candidates per lane in flight, then the exact
         // keys from the points staged at compaction
@@ -900,11 +901,20 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
                 ckey[c] = ok ? e : INFINITY;
                 cinfo[c] = oiv[u];
                 if (ok) {
-                    atomicAdd(&cntb[min(NB2 - 1, int(e * sc2))], 1u);
+                    kmax = fmax(kmax, e);
                     ++nvalid_local;
                 }
             }
         }
+    }
+    // buckets span [0, largest candidate key] (not the looser threshold), so
+    // they stay short; any monotone bucketing keeps the order exact
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) kmax = fmax(kmax, __shfl_xor_sync(FULL, kmax, off));
+    const double sc2 = double(NB2) / (kmax * (1.0 + 0x1p-40) + 1e-300);
+    for (int c = lane; c < C; c += 32) {
+        const double e = ckey[c];
+        if (e < INFINITY) atomicAdd(&cntb[min(NB2 - 1, int(e * sc2))], 1u);
     }
     const int nvalid = int(__reduce_add_sync(FULL, unsigned(nvalid_local)));
     __syncwarp();
@@ -938,6 +948,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
         const int bk = min(NB2 - 1, int(e * sc2));
         const int o_self = cinfo[c];
         const unsigned start = cntb[bk];
+        if (start >= unsigned(K)) continue;  // every key of an earlier bucket is smaller: cannot rank < K
         const unsigned end = bk + 1 < NB2 ? cntb[bk + 1] : unsigned(nvalid);
         unsigned rank = start;
 #pragma unroll 1
@@ -965,7 +976,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
         }
     }
     __syncwarp();
-    for (int k = lane; k < 2 * NB2; k += 32) cntb[k] = 0;
+    for (int k = lane; k < 2 * NB2 / 4; k += 32) reinterpret_cast<uint4*>(cntb)[k] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     return nsel_out;
 }
