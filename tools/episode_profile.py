@@ -29,8 +29,11 @@ def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     B = int(args[0]) if args else 4096
     pathstats = "--pathstats" in sys.argv
-    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=32, road_points=2048), 7)
-    env = z.Env(zsim, config=z.SimConfig(disable_dones=True))
+    c2 = "--c2" in sys.argv  # C2 shapes: B scenarios x 128 controlled actors, 8k road points
+    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=128 if c2 else 32, road_points=8192 if c2 else 2048,
+                                             flags=z.STRESS_C2 if c2 else 0), 7)
+    env = z.Env(zsim, config=z.SimConfig(disable_dones=True), controlled=c2)
+    B = env.info.batch
     acc, st = z.random_actions(91, B, seed=123)
     dA, dS = torch.from_numpy(acc).cuda(), torch.from_numpy(st).cuda()
     s0, s1, so, ob = env.device_state(), env.device_state(), env.device_stepout(), env.device_obs()
