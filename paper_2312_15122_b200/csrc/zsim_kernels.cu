@@ -139,7 +139,6 @@ struct WarpBuf {
     double* agx;           // [A*4] agent corners
     double* agy;
     double* agd;           // [A] bbox distance
-    int* surv;             // [A] agents whose distance bounds can reach the top n_agents
     int* agf;              // [A] -1 invalid, 0 separate, 1 overlap
     unsigned short* hist;  // [32*32] lane-private u16 histogram; reused as counting-sort counts u32[NB2]
     int* cidx;             // [cap] candidate indices
@@ -165,7 +164,6 @@ inline SmemLayout warp_layout(int A, int cap, int ka, int ns) {
     put(L.agy, size_t(A) * 4 * 8);
     put(L.agd, size_t(A) * 8);
     put(L.agf, size_t(A) * 4);
-    put(L.surv, size_t(A) * 4);
     put(L.sel, size_t(ka) * 4);
     const size_t agents_end = o;
     o = u0;
@@ -189,7 +187,6 @@ __device__ __forceinline__ WarpBuf carve(unsigned char* base, const KernelArgs& 
     w.agy = reinterpret_cast<double*>(p + L.agy);
     w.agd = reinterpret_cast<double*>(p + L.agd);
     w.agf = reinterpret_cast<int*>(p + L.agf);
-    w.surv = reinterpret_cast<int*>(p + L.surv);
     w.sel = reinterpret_cast<int*>(p + L.sel);
     w.hist = reinterpret_cast<unsigned short*>(p + L.hist);
     w.cidx = reinterpret_cast<int*>(p + L.cidx);
@@ -565,9 +562,10 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
     return p;
 }
 
-// Agent box corners at log slice `slice` (agent_box, simcore.cpp:162-165,
-// Obb::corners geometry.cpp:7-15) into smem; returns the box.
-__device__ __forceinline__ Box agent_corners(const DevPack& pk, int sc, size_t slice, int j, const WarpBuf& w) {
+// Agent box at log slice `slice` (agent_box, simcore.cpp:162-165): corners
+// into smem and the SAT overlap with the ego box (geometry.cpp:65-75).
+__device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size_t slice, int j, const Box& eb,
+                                                 const double* EX, const double* EY, const WarpBuf& w) {
     const int A = pk.d.A;
     double h = double(pk.ag_h[slice + j]);
     Box ab;
@@ -585,26 +583,7 @@ __device__ __forceinline__ Box agent_corners(const DevPack& pk, int sc, size_t s
         w.agx[4 * j + k] = X[k];
         w.agy[4 * j + k] = Y[k];
     }
-    return ab;
-}
-
-// Agent flags in w.agf: -1 not valid at the slice; 0 separate / 1 overlap
-// (obb_overlap, geometry.cpp:65-75; corners in smem); 2 separate by the
-// circumcircle test (corners not computed).
-constexpr int kAgSeparateFar = 2;
-
-// Collision test of agent j against the ego box.  Circumcircles further apart
-// than the sum of radii + 1e-6 m imply disjoint boxes with a gap many orders
-// above the SAT's rounding, i.e. obb_overlap == false, without the box.
-__device__ __forceinline__ int agent_collide(const DevPack& pk, int sc, size_t slice, int j, const Box& eb, double re,
-                                             const double* EX, const double* EY, const WarpBuf& w) {
-    const int A = pk.d.A;
-    const double dx = double(pk.ag_x[slice + j]) - eb.cx, dy = double(pk.ag_y[slice + j]) - eb.cy;
-    const double l = double(pk.ag_len[size_t(sc) * A + j]) * 0.5, wd = double(pk.ag_wid[size_t(sc) * A + j]) * 0.5;
-    const double rr = re + sqrt(l * l + wd * wd) + 1e-6 + 1e-12 * (fabs(eb.cx) + fabs(eb.cy));
-    if (dx * dx + dy * dy > rr * rr * (1.0 + 1e-12)) return kAgSeparateFar;
-    const Box ab = agent_corners(pk, sc, slice, j, w);
-    return boxes_overlap(eb, EX, EY, ab, w.agx + 4 * j, w.agy + 4 * j) ? 1 : 0;
+    return boxes_overlap(eb, EX, EY, ab, X, Y) ? 1 : 0;
 }
 
 // Upper bound on |fp32 key - fp64 key| for points within sqrt(T)+1 of the
@@ -1111,10 +1090,9 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     const size_t aslice = (size_t(sc) * pk.d.T + (t_ok ? t : 0)) * A;
     if (!boxes_ready) {
         const Box eb = rs.eb;
-        const double re = sqrt(eb.hl * eb.hl + eb.hw * eb.hw);
         for (int j = lane; j < na; j += 32) {
             int f = -1;
-            if (t_ok && j != skip && pk.ag_valid[aslice + j]) f = agent_collide(pk, sc, aslice, j, eb, re, rs.ex, rs.ey, w);
+            if (t_ok && j != skip && pk.ag_valid[aslice + j]) f = agent_box_overlap(pk, sc, aslice, j, eb, rs.ex, rs.ey, w);
             w.agf[j] = f;
         }
         __syncwarp();
@@ -1140,79 +1118,10 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         gyf[k] = float(GY[k] - ecy);
     }
     const float ge = float(2.0 * (rs.eb.hl + rs.eb.hw)) + 1e-3f;  // >= any ego edge length
-    // More than 32 agents: only agents whose distance can reach the top Ka
-    // are measured.  obb_distance <= |c_e - c_a| (both centres lie in their
-    // boxes) and >= |c_e - c_a| - r_e - r_a (circumradii); U = the Ka-th
-    // smallest per-lane minimum upper bound (>= Ka distinct agents lie within
-    // it) -- an agent whose lower bound exceeds U cannot rank.  Margins cover
-    // the fp32 evaluation.
-    int nlist = na;
-    const int* list = nullptr;
-#ifndef ZS_PRUNE_AGENTS_ABOVE
-#define ZS_PRUNE_AGENTS_ABOVE 32
-#endif
-    if (na > ZS_PRUNE_AGENTS_ABOVE && na <= 128 && Ka <= 32) {
-        // centre distances (fp32, rounded up) of the <= 4 agents of this lane,
-        // kept sorted; U = the exact Ka-th smallest of them over the warp
-        // (REDUX min over the lanes' heads, Ka times)
-        const float re = float(sqrt(rs.eb.hl * rs.eb.hl + rs.eb.hw * rs.eb.hw));
-        float ub[4], lbv[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int j = lane + 32 * k;
-            ub[k] = INFINITY;
-            lbv[k] = INFINITY;
-            if (j < na && w.agf[j] >= 0) {
-                const float dx = float(double(pk.ag_x[aslice + j]) - ecx), dy = float(double(pk.ag_y[aslice + j]) - ecy);
-                const float l = pk.ag_len[size_t(sc) * A + j] * 0.5f, wd = pk.ag_wid[size_t(sc) * A + j] * 0.5f;
-                const float dc = sqrtf(dx * dx + dy * dy);
-                ub[k] = dc * 1.0001f + 1e-3f;
-                lbv[k] = dc * 0.9999f - re - sqrtf(l * l + wd * wd) * 1.0001f - 1e-3f;
-            }
-        }
-        float sv[4] = {ub[0], ub[1], ub[2], ub[3]};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int k = 0; k < 3 - i; ++k)
-                if (sv[k + 1] < sv[k]) {
-                    const float x = sv[k];
-                    sv[k] = sv[k + 1];
-                    sv[k + 1] = x;
-                }
-        float U = INFINITY;
-        int head = 0;
-#pragma unroll 1
-        for (int r = 0; r < Ka; ++r) {
-            const float mine = head < 4 ? (head == 0 ? sv[0] : head == 1 ? sv[1] : head == 2 ? sv[2] : sv[3]) : INFINITY;
-            const unsigned mb = __reduce_min_sync(FULL, __float_as_uint(mine));  // non-negative floats order as bits
-            U = __uint_as_float(mb);
-            if (!(U < INFINITY)) break;  // fewer than Ka valid agents: all survive
-            const unsigned who = __ballot_sync(FULL, __float_as_uint(mine) == mb);
-            if (lane == __ffs(who) - 1) ++head;
-        }
-        int ns = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int j = lane + 32 * k;
-            const bool keep = lbv[k] < INFINITY && lbv[k] <= U;  // valid agents only
-            const unsigned bal = __ballot_sync(FULL, keep);
-            if (keep) w.surv[ns + __popc(bal & lanemask_lt())] = j;
-            ns += __popc(bal);
-        }
-        __syncwarp();
-        nlist = ns;
-        list = w.surv;
-    }
     int nvalid = 0;
-    for (int j0 = 0; j0 < nlist; j0 += 32) {
-        const int jl = j0 + lane;
-        const int j = jl < nlist ? (list ? list[jl] : jl) : -1;
-        int fl = j >= 0 ? w.agf[j] : -1;
-        if (fl == kAgSeparateFar) {
-            agent_corners(pk, sc, aslice, j, w);  // pruned at the collision test, needed now
-            fl = 0;
-        }
+    for (int j0 = 0; j0 < na; j0 += 32) {
+        const int j = j0 + lane;
+        const int fl = j < na ? w.agf[j] : -1;
         if (fl == 0) {
             const double* AX = w.agx + 4 * j;
             const double* AY = w.agy + 4 * j;
@@ -1282,7 +1191,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     // patterns order like the values; invalid = +inf, last.  More than 32
     // agents: the best 16 so far (lanes 0-15) are merged with each further
     // chunk's best 16 (lanes 16-31) by one more sort.
-    if (nlist <= 32 || Ka <= 16) {
+    if (na <= 32 || Ka <= 16) {
         auto sort32 = [&](unsigned long long& key, int& idx) {
 #pragma unroll
             for (int k = 2; k <= 32; k <<= 1) {
@@ -1298,10 +1207,9 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         };
         unsigned long long bkey = 0xFFF0000000000000ull;
         int bidx = INT_MAX;
-        for (int j0 = 0; j0 < nlist; j0 += 32) {
-            const int jl = j0 + lane;
-            const int j = jl < nlist ? (list ? list[jl] : jl) : -1;
-            const bool ok = j >= 0 && w.agf[j] >= 0;
+        for (int j0 = 0; j0 < na; j0 += 32) {
+            const int j = j0 + lane;
+            const bool ok = j < na && w.agf[j] >= 0;
             unsigned long long key = ok ? (unsigned long long)__double_as_longlong(w.agd[j]) : 0xFFF0000000000000ull;
             int idx = ok ? j : INT_MAX;
             sort32(key, idx);
@@ -1318,15 +1226,13 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         }
         if (lane < Ka && lane < nvalid) w.sel[lane] = bidx;
     } else {
-        for (int j0 = 0; j0 < nlist; j0 += 32) {
-            const int jl = j0 + lane;
-            const int j = jl < nlist ? (list ? list[jl] : jl) : -1;
-            if (j >= 0 && w.agf[j] >= 0) {
+        for (int j0 = 0; j0 < na; j0 += 32) {
+            const int j = j0 + lane;
+            if (j < na && w.agf[j] >= 0) {
                 const double dj = w.agd[j];
                 int rank = 0;
 #pragma unroll 4
-                for (int q = 0; q < nlist; ++q) {
-                    const int k = list ? list[q] : q;
+                for (int k = 0; k < na; ++k) {
                     const double dk = w.agd[k];
                     rank += (w.agf[k] >= 0 && (dk < dj || (dk == dj && k < j))) ? 1 : 0;
                 }
@@ -1565,10 +1471,9 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const bool t_ok = t1 < pk.num_steps[sc];
         const size_t slice = (size_t(sc) * pk.d.T + (t_ok ? t1 : 0)) * pk.d.A;
         const Box eb = rs.eb;
-        const double re = sqrt(eb.hl * eb.hl + eb.hw * eb.hw);
         for (int j = lane; j < na; j += 32) {
             int f = -1;
-            if (t_ok && j != skip && pk.ag_valid[slice + j]) f = agent_collide(pk, sc, slice, j, eb, re, rs.ex, rs.ey, w);
+            if (t_ok && j != skip && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, sc, slice, j, eb, rs.ex, rs.ey, w);
             w.agf[j] = f;
             hit |= f == 1;
         }
