@@ -986,6 +986,13 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
 // w.rs->boxes_ready, the ego box and the agent boxes at r.t with their
 // overlap flags are already in smem (fused step+observe).
 // ---------------------------------------------------------------------------
+// Observation parts: kObsAgents = active features + agents + value-only,
+// kObsMap = road + route top-k.  Large batches run them as separate kernels
+// (smaller code per kernel: rows of a multi-wave batch are out of phase and a
+// fused kernel's code then thrashes the instruction cache).
+constexpr int kObsAgents = 1, kObsMap = 2, kObsAll = 3;
+
+template <int PARTS>
 __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     ROW_MARK(b, 2);
     const DevPack& pk = a.pk;
@@ -1003,14 +1010,20 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
 
     if (r.done) {
         // ObservationBatch::zero_row (simcore.cpp:37-43)
-        for (int i = lane; i < 9; i += 32) act[i] = 0.f;
-        for (int i = lane; i < Ka * 6; i += 32) agt[i] = 0.f;
-        float4* rd4 = reinterpret_cast<float4*>(rd);
-        for (int i = lane; i < Kr * 3; i += 32) rd4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int i = lane; i < Kl * 5; i += 32) rt[i] = 0.f;
-        if (lane < 2) val[lane] = 0.f;
-        if (dbg)
-            for (int i = lane; i < Ka + Kr + Kl; i += 32) dbg[i] = -1;
+        if (PARTS & kObsAgents) {
+            for (int i = lane; i < 9; i += 32) act[i] = 0.f;
+            for (int i = lane; i < Ka * 6; i += 32) agt[i] = 0.f;
+            if (lane < 2) val[lane] = 0.f;
+            if (dbg)
+                for (int i = lane; i < Ka; i += 32) dbg[i] = -1;
+        }
+        if (PARTS & kObsMap) {
+            float4* rd4 = reinterpret_cast<float4*>(rd);
+            for (int i = lane; i < Kr * 3; i += 32) rd4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = lane; i < Kl * 5; i += 32) rt[i] = 0.f;
+            if (dbg)
+                for (int i = Ka + lane; i < Ka + Kr + Kl; i += 32) dbg[i] = -1;
+        }
         return;
     }
 
@@ -1037,6 +1050,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     // ego-frame rotation by -heading (simcore.cpp:432): cos(-h) = cos h, sin(-h) = -sin h
     const double oc = rs.eb.c, os = -rs.eb.s;
 
+    if (PARTS & kObsAgents) {
     // ---- active features: roads::stop_info (roads.cpp:253-277), simcore.cpp:440-455 ----
     {
         double best_stop = 1e300;
@@ -1262,6 +1276,9 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         if (dbg) dbg[k] = (skip >= 0 && j > skip) ? j - 1 : j;  // index among the row's agents
     }
 
+    }  // PARTS & kObsAgents
+
+    if (PARTS & kObsMap) {
     // ---- road network points: nearest_features (roads.cpp:210-236) ----
     // the top-k region overlays the (now dead) agent buffers: clear the histogram
     ROW_MARK(b, 3);
@@ -1336,6 +1353,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
             if (dbg) dbg[Ka + Kr + k] = i < 0 ? -1 : oidx[i];
         }
     }
+    }  // PARTS & kObsMap
 }
 
 // EpisodeBatch cell (b, a.ep_t) of Env::rollout's recording loop
@@ -1548,7 +1566,7 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
 // Prefetch scenario sc's static data (the arrays one step touches, from the
 // pack's prefetch table: one array per lane) into L2.  `t` is the log
 // index of the agent slice the kernel will read.
-template <bool STEP, bool OBS>
+template <bool STEP, int OBS>
 __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int sc, int t) {
     const DevPack& pk = a.pk;
     const int lane = lane_id();
@@ -1561,7 +1579,7 @@ __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int sc, int t)
     prefetch_l2(p, d.bytes < (1u << 24) ? d.bytes : (1u << 24));
 }
 
-template <bool STEP, bool OBS>
+template <bool STEP, int OBS>
 #ifndef ZS_MIN_BLOCKS
 #define ZS_MIN_BLOCKS 7  // 72 registers: 28 resident warps per SM
 #endif
@@ -1575,7 +1593,7 @@ __global__ void __launch_bounds__(kThreads, ZS_MIN_BLOCKS) k_step_observe(const 
     for (; b < a.pk.d.B; b += stride) {
         if (lane_id() == 0) {
             w.rs->r0 = load_row(a.in, b);
-            if (OBS && a.hint) w.rs->hint = a.hint[b];
+            if ((OBS & kObsMap) && a.hint) w.rs->hint = a.hint[b];
             w.rs->sc = scen_of(a.pk, b);
             w.rs->skip = skip_of(a.pk, b);
         }
@@ -1593,7 +1611,7 @@ __global__ void __launch_bounds__(kThreads, ZS_MIN_BLOCKS) k_step_observe(const 
             }
             __syncwarp();
         }
-        if (OBS) observe_row(a, b, w);
+        if (OBS) observe_row<OBS>(a, b, w);
         ROW_MARK(b, 7);
     }
 }
@@ -1826,21 +1844,48 @@ static int persistent_grid(K kern, const KernelArgs& a, size_t smem) {
 
 cudaError_t launch_step_observe(const KernelArgs& a, int mode, int grid, cudaStream_t stream) {
     (void)grid;
-    KernelArgs am = a;
-    if (mode == kModeStep) am.cand_cap = 0;  // the step-only kernel carves no top-k buffers
-    am.lay = warp_layout(am.pk.d.A, am.cand_cap, am.cfg.n_agents, am.pk.d.NS);
-    const size_t smem = smem_bytes(am);
-    auto launch = [&](auto kern) -> cudaError_t {
+    auto launch = [&](auto kern, KernelArgs am, bool topk) -> cudaError_t {
+        if (!topk) am.cand_cap = 0;  // no top-k buffers in kernels without the map part
+        am.lay = warp_layout(am.pk.d.A, am.cand_cap, am.cfg.n_agents, am.pk.d.NS);
+        const size_t smem = smem_bytes(am);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
         const int g = persistent_grid(kern, am, smem);
         kern<<<g, kThreads, smem, stream>>>(am);
         return cudaGetLastError();
     };
+    // More rows than one wave of the fused kernel: the rows run out of phase,
+    // so the observation parts go to separate, smaller kernels.
+    bool split = false;
+    if (mode != kModeStep) {
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        KernelArgs t = a;
+        t.lay = warp_layout(t.pk.d.A, t.cand_cap, t.cfg.n_agents, t.pk.d.NS);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_observe<true, kObsAll>, kThreads,
+                                                          smem_bytes(t)) != cudaSuccess || per_sm < 1)
+            per_sm = 1;
+        split = a.pk.d.B > sms * per_sm * (kThreads / 32);
+    }
     switch (mode) {
-        case kModeStep: return launch(k_step_observe<true, false>);
-        case kModeObserve: return launch(k_step_observe<false, true>);
-        default: return launch(k_step_observe<true, true>);
+        case kModeStep: return launch(k_step_observe<true, 0>, a, false);
+        case kModeObserve: {
+            if (!split) return launch(k_step_observe<false, kObsAll>, a, true);
+            cudaError_t e = launch(k_step_observe<false, kObsAgents>, a, false);
+            return e != cudaSuccess ? e : launch(k_step_observe<false, kObsMap>, a, true);
+        }
+        default: {
+            if (!split) return launch(k_step_observe<true, kObsAll>, a, true);
+            // step + agents (the agent boxes at t+1 are reused), then the map
+            // parts on the post-step state
+            cudaError_t e = launch(k_step_observe<true, kObsAgents>, a, false);
+            if (e != cudaSuccess) return e;
+            KernelArgs m = a;
+            m.in = a.out;
+            m.ep = zsim_episode_view{};
+            return launch(k_step_observe<false, kObsMap>, m, true);
+        }
     }
 }
 

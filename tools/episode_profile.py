@@ -56,7 +56,11 @@ def main():
         for t in range(91):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            env.step_observe_device(s0, dA[t].data_ptr(), dS[t].data_ptr(), s1, so, ob, stream)
+            if "--split" in sys.argv:  # separate step and observe kernels
+                env.step_device(s0, dA[t].data_ptr(), dS[t].data_ptr(), s1, so, stream)
+                env.observe_device(s1, ob, stream)
+            else:
+                env.step_observe_device(s0, dA[t].data_ptr(), dS[t].data_ptr(), s1, so, ob, stream)
             e1.record(stream)
             s0, s1 = s1, s0
             if "--sync" in sys.argv:
