@@ -146,6 +146,7 @@ SIGNATURES = {
     "zsim_episode_stats": (C.c_int, [_P, C.POINTER(StateView), C.POINTER(C.c_int64), _P]),
     "zsim_set_debug_topk": (C.c_int, [_P, c_int32_p]),
     "zsim_check_errors": (C.c_int, [_P, _P]),
+    "zsim_set_launch_policy": (C.c_int, [_P, C.c_int32]),
     "zsim_reset_host": (C.c_int, [_P, C.c_uint64, C.POINTER(StateView)]),
     "zsim_step_host": (C.c_int, [_P, C.POINTER(StateView), c_int32_p, c_int32_p, C.POINTER(StateView),
                                  C.POINTER(StepOutView)]),

@@ -189,6 +189,7 @@ struct zsim_env {
     double* d_metrics_scratch = nullptr;  // per-block Aggregate partials
     float4* d_hint = nullptr;
     int grid = 0;
+    int launch_policy = 0;  // zsim_set_launch_policy: 0 auto, 1 fused, 2 split observation kernels
 };
 
 namespace {
@@ -1154,7 +1155,7 @@ ZSIM_API int zsim_step(zsim_env* env, const zsim_state_view* in, const int32_t* 
         a.accel = accel;
         a.steer = steer;
         a.so = *so;
-        cuda_check(zs::launch_step_observe(a, zs::kModeStep, env->grid, as_stream(stream)), "step kernel");
+        cuda_check(zs::launch_step_observe(a, zs::kModeStep, env->launch_policy, as_stream(stream)), "step kernel");
     });
 }
 
@@ -1167,7 +1168,7 @@ ZSIM_API int zsim_observe(zsim_env* env, const zsim_state_view* in, const zsim_o
         zs::KernelArgs a = args_for(env);
         a.in = *in;
         a.obs = *obs;
-        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->grid, as_stream(stream)), "observe kernel");
+        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->launch_policy, as_stream(stream)), "observe kernel");
     });
 }
 
@@ -1189,7 +1190,7 @@ ZSIM_API int zsim_step_observe(zsim_env* env, const zsim_state_view* in, const i
         a.steer = steer;
         a.so = *so;
         a.obs = *obs;
-        cuda_check(zs::launch_step_observe(a, zs::kModeStepObserve, env->grid, as_stream(stream)),
+        cuda_check(zs::launch_step_observe(a, zs::kModeStepObserve, env->launch_policy, as_stream(stream)),
                    "step_observe kernel");
     });
 }
@@ -1370,7 +1371,7 @@ ZSIM_API int zsim_rollout(zsim_env* env, uint64_t seed, int32_t horizon, const i
         a = args_for(env);
         a.in = env->roll_s[0];
         a.obs = obs ? obs[0] : env->roll_obs;
-        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->grid, s), "observe kernel");
+        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->launch_policy, s), "observe kernel");
         int cur = 0;
         for (int t = 0; t < horizon; ++t) {
             a = args_for(env);
@@ -1387,7 +1388,7 @@ ZSIM_API int zsim_rollout(zsim_env* env, uint64_t seed, int32_t horizon, const i
                 a.ep_t = t;
             }
             a.obs = obs ? obs[t + 1] : env->roll_obs;
-            cuda_check(zs::launch_step_observe(a, zs::kModeStepObserve, env->grid, s), "step+observe kernel");
+            cuda_check(zs::launch_step_observe(a, zs::kModeStepObserve, env->launch_policy, s), "step+observe kernel");
             cur ^= 1;
         }
         if (ep) {
@@ -1453,6 +1454,14 @@ ZSIM_API int zsim_aggregate_finalize(const double* sums, int32_t n_parts, double
     });
 }
 
+ZSIM_API int zsim_set_launch_policy(zsim_env* env, int32_t policy) {
+    return guarded([&] {
+        check_view(env, "set_launch_policy");
+        if (policy < 0 || policy > 2) raise(Err::invalid_argument, "launch policy must be 0, 1 or 2");
+        env->launch_policy = policy;
+    });
+}
+
 ZSIM_API int zsim_set_debug_topk(zsim_env* env, int32_t* dev_idx) {
     return guarded([&] {
         check_view(env, "set_debug_topk");
@@ -1511,7 +1520,7 @@ ZSIM_API int zsim_step_host(zsim_env* env, const zsim_state_view* in_host, const
         a.accel = env->h_act;
         a.steer = env->h_act + B;
         a.so = env->h_so;
-        cuda_check(zs::launch_step_observe(a, zs::kModeStep, env->grid, s), "step kernel");
+        cuda_check(zs::launch_step_observe(a, zs::kModeStep, env->launch_policy, s), "step kernel");
         copy_state(env, out_host, &env->h_out, 1, s);
         copy_stepout(env, so_host, &env->h_so, 1, s);
         cuda_check(cudaStreamSynchronize(s), "stream sync");
@@ -1530,7 +1539,7 @@ ZSIM_API int zsim_observe_host(zsim_env* env, const zsim_state_view* in_host, co
         zs::KernelArgs a = args_for(env);
         a.in = env->h_in;
         a.obs = env->h_obs;
-        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->grid, s), "observe kernel");
+        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->launch_policy, s), "observe kernel");
         copy_obs(env, obs_host, &env->h_obs, 1, s);
         cuda_check(cudaStreamSynchronize(s), "stream sync");
     });

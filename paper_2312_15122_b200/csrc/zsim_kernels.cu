@@ -1842,8 +1842,7 @@ static int persistent_grid(K kern, const KernelArgs& a, size_t smem) {
     return g < need ? g : need;
 }
 
-cudaError_t launch_step_observe(const KernelArgs& a, int mode, int grid, cudaStream_t stream) {
-    (void)grid;
+cudaError_t launch_step_observe(const KernelArgs& a, int mode, int policy, cudaStream_t stream) {
     auto launch = [&](auto kern, KernelArgs am, bool topk) -> cudaError_t {
         if (!topk) am.cand_cap = 0;  // no top-k buffers in kernels without the map part
         am.lay = warp_layout(am.pk.d.A, am.cand_cap, am.cfg.n_agents, am.pk.d.NS);
@@ -1868,6 +1867,8 @@ cudaError_t launch_step_observe(const KernelArgs& a, int mode, int grid, cudaStr
             per_sm = 1;
         split = a.pk.d.B > sms * per_sm * (kThreads / 32);
     }
+    if (policy == 1) split = false;
+    if (policy == 2) split = true;
     switch (mode) {
         case kModeStep: return launch(k_step_observe<true, 0>, a, false);
         case kModeObserve: {

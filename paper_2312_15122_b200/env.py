@@ -514,6 +514,10 @@ class Env:
     def set_debug_topk(self, dev_ptr: int | None) -> None:
         check(lib.zsim_set_debug_topk(self.handle, C.cast(C.c_void_p(dev_ptr or 0), C.POINTER(C.c_int32))))
 
+    def set_launch_policy(self, policy: int) -> None:
+        """0 automatic, 1 fused kernel, 2 split observation kernels (identical results)."""
+        check(lib.zsim_set_launch_policy(self.handle, int(policy)))
+
     def check_errors(self, stream=None) -> None:
         check(lib.zsim_check_errors(self.handle, _stream(stream)))
 

@@ -236,3 +236,38 @@ def test_all_done_batch_is_absorbing(stress16):
     assert (so.reward == 0).all() and (so.event == 0).all()
     ob = env.observe(nxt)
     assert not ob.road.any() and not ob.active.any()
+
+
+@pytest.mark.parametrize("controlled", [False, True])
+def test_split_observation_kernels_equal_fused(controlled):
+    """zsim_set_launch_policy: the split kernel arrangement (step + agents,
+    then road/route top-k) is bit-identical to the fused kernel."""
+    import torch
+    if controlled:
+        zsim = z.stress_scenarios(z.StressConfig(count=3, agents=40, road_points=512, flags=z.STRESS_C2), 9)
+    else:
+        zsim = z.stress_scenarios(z.StressConfig(count=24), 9)
+    outs = []
+    for policy in (1, 2):
+        env = z.Env(zsim, config=z.SimConfig(disable_dones=False), controlled=controlled)
+        env.set_launch_policy(policy)
+        B = env.info.batch
+        A, S = z.random_actions(40, B, seed=2)
+        dA, dS = torch.from_numpy(A).cuda(), torch.from_numpy(S).cuda()
+        s0, s1, so, ob = env.device_state(), env.device_state(), env.device_stepout(), env.device_obs()
+        env.reset_device(42, s0)
+        rec = []
+        for t in range(40):
+            env.step_observe_device(s0, dA[t].data_ptr(), dS[t].data_ptr(), s1, so, ob)
+            s0, s1 = s1, s0
+            o = env.download_obs(ob)
+            rec.append([getattr(o, f).copy() for f in ("active", "agents", "road", "route", "value_only")])
+        env.observe_device(s0, ob)  # observe-only arrangement too
+        o = env.download_obs(ob)
+        rec.append([getattr(o, f).copy() for f in ("active", "agents", "road", "route", "value_only")])
+        st = env.download_state(s0)
+        rec.append([st.x.copy(), st.done.copy(), st.events.copy()])
+        outs.append(rec)
+    for a, b in zip(*outs):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
