@@ -405,7 +405,7 @@ def run_ours(args) -> None:
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, ("bytes_per_row_step" if controlled else "bytes_per_scenario_step"): per_scen,
                      "kernel": "k_step_observe<true,true>", "kernel_ms": kern_ms, "peak_source": peak_src},
-        "gpu_launches": args.steps + resets,
+        "gpu_launches": args.steps * env.info.step_observe_kernels + resets,
         "scenario_steps_per_s": S_ * args.steps * world / (elapsed_ms / 1e3),
         "controlled_agent_steps_per_s": B * args.steps * world / (elapsed_ms / 1e3),
         "timing": {"mode": "cuda-graph rollouts (reset + 91 fused steps)" if use_graph else "eager launches",

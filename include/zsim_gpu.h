@@ -143,6 +143,8 @@ typedef struct zsim_env_info {
     uint64_t static_bytes; /* device bytes of the immutable scenario pack */
     int32_t scenarios;     /* scenarios staged (== batch unless controlled) */
     int32_t controlled;    /* 1: rows are controlled actors (zsim_env_create_controlled) */
+    int32_t step_observe_kernels; /* kernels one zsim_step_observe launches (launch policy) */
+    int32_t reserved0;
 } zsim_env_info;
 
 typedef struct zsim_env zsim_env;

@@ -59,6 +59,7 @@ class EnvInfo(C.Structure):
         ("cap_route", C.c_int32), ("cap_lanes", C.c_int32), ("cap_vertices", C.c_int32),
         ("cap_lights", C.c_int32), ("cap_stops", C.c_int32), ("device", C.c_int32),
         ("static_bytes", C.c_uint64), ("scenarios", C.c_int32), ("controlled", C.c_int32),
+        ("step_observe_kernels", C.c_int32), ("reserved0", C.c_int32),
     ]
 
 

@@ -982,6 +982,8 @@ ZSIM_API int zsim_env_get_info(const zsim_env* env, zsim_env_info* out) {
         out->static_bytes = env->pack_bytes;
         out->scenarios = env->n_scen;
         out->controlled = env->base.pk.row_scen ? 1 : 0;
+        cudaSetDevice(env->device);
+        out->step_observe_kernels = zs::observe_split(env->base, env->launch_policy) ? 2 : 1;
     });
 }
 

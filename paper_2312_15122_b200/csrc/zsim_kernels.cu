@@ -1842,6 +1842,22 @@ static int persistent_grid(K kern, const KernelArgs& a, size_t smem) {
     return g < need ? g : need;
 }
 
+// More rows than one wave of the fused kernel: the rows run out of phase, so
+// the observation parts go to separate, smaller kernels.
+bool observe_split(const KernelArgs& a, int policy) {
+    if (policy == 1) return false;
+    if (policy == 2) return true;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    KernelArgs t = a;
+    t.lay = warp_layout(t.pk.d.A, t.cand_cap, t.cfg.n_agents, t.pk.d.NS);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_observe<true, kObsAll>, kThreads,
+                                                      smem_bytes(t)) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return a.pk.d.B > sms * per_sm * (kThreads / 32);
+}
+
 cudaError_t launch_step_observe(const KernelArgs& a, int mode, int policy, cudaStream_t stream) {
     auto launch = [&](auto kern, KernelArgs am, bool topk) -> cudaError_t {
         if (!topk) am.cand_cap = 0;  // no top-k buffers in kernels without the map part
@@ -1853,22 +1869,7 @@ cudaError_t launch_step_observe(const KernelArgs& a, int mode, int policy, cudaS
         kern<<<g, kThreads, smem, stream>>>(am);
         return cudaGetLastError();
     };
-    // More rows than one wave of the fused kernel: the rows run out of phase,
-    // so the observation parts go to separate, smaller kernels.
-    bool split = false;
-    if (mode != kModeStep) {
-        int dev = 0, sms = 148, per_sm = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        KernelArgs t = a;
-        t.lay = warp_layout(t.pk.d.A, t.cand_cap, t.cfg.n_agents, t.pk.d.NS);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_observe<true, kObsAll>, kThreads,
-                                                          smem_bytes(t)) != cudaSuccess || per_sm < 1)
-            per_sm = 1;
-        split = a.pk.d.B > sms * per_sm * (kThreads / 32);
-    }
-    if (policy == 1) split = false;
-    if (policy == 2) split = true;
+    const bool split = mode != kModeStep && observe_split(a, policy);
     switch (mode) {
         case kModeStep: return launch(k_step_observe<true, 0>, a, false);
         case kModeObserve: {

@@ -49,6 +49,7 @@ struct KernelArgs {
 size_t smem_bytes(const KernelArgs& a);
 // policy: 0 auto (split the observation into separate kernels beyond one wave), 1 fused, 2 split
 cudaError_t launch_step_observe(const KernelArgs& a, int mode, int policy, cudaStream_t stream);
+bool observe_split(const KernelArgs& a, int policy);  // the arrangement launch_step_observe picks
 cudaError_t launch_reset(const KernelArgs& a, int grid, cudaStream_t stream);
 cudaError_t launch_episode_stats(const KernelArgs& a, const double* initial_s, long long* out, cudaStream_t stream);
 // EpisodeBatch tail (bootstrap / terminal / events / initial_s / logged_progress) from the final state a.in

@@ -517,6 +517,7 @@ class Env:
     def set_launch_policy(self, policy: int) -> None:
         """0 automatic, 1 fused kernel, 2 split observation kernels (identical results)."""
         check(lib.zsim_set_launch_policy(self.handle, int(policy)))
+        check(lib.zsim_env_get_info(self.handle, C.byref(self.info)))
 
     def check_errors(self, stream=None) -> None:
         check(lib.zsim_check_errors(self.handle, _stream(stream)))
