@@ -258,7 +258,7 @@ ZSIM_API int zsim_set_debug_topk(zsim_env* env, int32_t* dev_idx);
  * ZSIM_INVALID_ARGUMENT ("action index out of range") if any step since the
  * last check saw a bad action index. */
 /* Kernel arrangement of step+observe / observe: 0 = automatic (one fused
- * kernel while the batch fits one wave of the GPU, otherwise step+agents and
+ * kernel up to three waves of rows on the GPU, otherwise step+agents and
  * road/route top-k as separate kernels), 1 = always fused, 2 = always split.
  * Results are identical; only speed differs. */
 ZSIM_API int zsim_set_launch_policy(zsim_env* env, int32_t policy);

@@ -1842,8 +1842,8 @@ static int persistent_grid(K kern, const KernelArgs& a, size_t smem) {
     return g < need ? g : need;
 }
 
-// More rows than one wave of the fused kernel: the rows run out of phase, so
-// the observation parts go to separate, smaller kernels.
+// Several waves of rows: the rows run out of phase, so the observation parts
+// go to separate, smaller kernels.
 bool observe_split(const KernelArgs& a, int policy) {
     if (policy == 1) return false;
     if (policy == 2) return true;
@@ -1855,7 +1855,8 @@ bool observe_split(const KernelArgs& a, int policy) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_observe<true, kObsAll>, kThreads,
                                                       smem_bytes(t)) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-    return a.pk.d.B > sms * per_sm * (kThreads / 32);
+    // measured: equal at 2 waves (C1 shapes), split clearly ahead at many waves (C2)
+    return a.pk.d.B > 3 * sms * per_sm * (kThreads / 32);
 }
 
 cudaError_t launch_step_observe(const KernelArgs& a, int mode, int policy, cudaStream_t stream) {

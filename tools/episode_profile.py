@@ -34,6 +34,9 @@ def main():
                                              flags=z.STRESS_C2 if c2 else 0), 7)
     env = z.Env(zsim, config=z.SimConfig(disable_dones=True), controlled=c2)
     B = env.info.batch
+    pol = next((int(a[9:]) for a in sys.argv if a.startswith("--policy=")), None)
+    if pol is not None:
+        env.set_launch_policy(pol)
     acc, st = z.random_actions(91, B, seed=123)
     dA, dS = torch.from_numpy(acc).cuda(), torch.from_numpy(st).cuda()
     s0, s1, so, ob = env.device_state(), env.device_state(), env.device_stepout(), env.device_obs()
