@@ -589,8 +589,7 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size
 // Upper bound on |fp32 key - fp64 key| for points within sqrt(T)+1 of the
 // query; `ep` is the fp32 rounding error of the query coordinates.
 __device__ __forceinline__ double key_margin(double T, double ep) {
-    // D >= sqrt(T) + 1: fp32 square root rounded up of T rounded up
-    double D = double(__fsqrt_ru(__double2float_ru(T))) + 1.0;
+    double D = sqrt(T) + 1.0;
     double eta = ep + 0x1p-24 * (D + ep);
     double m = 2.0 * eta * (2.0 * D + eta);
     m += 0x1p-22 * (T + m) + 0x1p-50 * T;
@@ -879,8 +878,8 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     // counting-sort counters / cursors live in the (clear) histogram area and
     // the selection is written to `order` after the ranking is complete.
     unsigned* cntb = reinterpret_cast<unsigned*>(hist);  // NB2 u32 counters
+    const double sc2 = double(NB2) / (double(tc) > 0.0 ? double(tc) : 1.0);
     int nvalid_local = 0;
-    double kmax = 0.0;
     for (int c0 = 0; c0 < C; c0 += 32 * 8) {
         // reference indices of 8 candidates per lane in flight, then the exact
         // keys from the points staged at compaction
@@ -901,20 +900,11 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
                 ckey[c] = ok ? e : INFINITY;
                 cinfo[c] = oiv[u];
                 if (ok) {
-                    kmax = fmax(kmax, e);
+                    atomicAdd(&cntb[min(NB2 - 1, int(e * sc2))], 1u);
                     ++nvalid_local;
                 }
             }
         }
-    }
-    // buckets span [0, largest candidate key] (not the looser threshold), so
-    // they stay short; any monotone bucketing keeps the order exact
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) kmax = fmax(kmax, __shfl_xor_sync(FULL, kmax, off));
-    const double sc2 = double(NB2) / (kmax * (1.0 + 0x1p-40) + 1e-300);
-    for (int c = lane; c < C; c += 32) {
-        const double e = ckey[c];
-        if (e < INFINITY) atomicAdd(&cntb[min(NB2 - 1, int(e * sc2))], 1u);
     }
     const int nvalid = int(__reduce_add_sync(FULL, unsigned(nvalid_local)));
     __syncwarp();
@@ -1381,6 +1371,7 @@ __device__ __forceinline__ void record_step(const KernelArgs& a, int b, int mask
 // through) the ego box, the agent boxes at t+1 and their overlap flags stay in
 // smem for a fused observe (w.rs->boxes_ready).
 // ---------------------------------------------------------------------------
+template <bool REC>
 __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     const DevPack& pk = a.pk;
     const DevCfg& cfg = a.cfg;
@@ -1395,7 +1386,7 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
 
     bool pass = rs.r0.done != 0;
     int ai = 0, si = 0;
-    if (a.act_len != 0) {
+    if (REC && a.act_len != 0) {
         // ScriptedPolicy::act (simcore.cpp:69-84): the script at the row's t, else the zero action
         const int tt = rs.r0.t;
         if (a.act_len > 0 && tt >= 0 && tt < a.act_len) {
@@ -1426,7 +1417,7 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
             a.so.a_lat[b] = 0.f;
             a.so.a_lon[b] = 0.f;
             a.so.v[b] = float(r0.v);
-            record_step(a, b, r0.done ? 0 : 1, ai, si, 0.f, float(r0.proj_s), 0.f, 0.f, float(r0.v), r0.done);
+            if (REC) record_step(a, b, r0.done ? 0 : 1, ai, si, 0.f, float(r0.proj_s), 0.f, 0.f, float(r0.v), r0.done);
         }
         for (int j = lane; j < ns; j += 32) a.out.stopped_flags[soff + j] = w.sflag[j];
         __syncwarp();
@@ -1551,7 +1542,7 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
         a.so.a_lat[b] = float(a_lat);
         a.so.a_lon[b] = float(a_lon);
         a.so.v[b] = float(vn);
-        record_step(a, b, 1, ai, si, float(reward), float(p1.s), float(a_lat), float(a_lon), float(vn), done);
+        if (REC) record_step(a, b, 1, ai, si, float(reward), float(p1.s), float(a_lat), float(a_lon), float(vn), done);
     }
     // stopped-flag update with the post-step state (simcore.cpp:390-396)
     for (int j = lane; j < ns; j += 32) {
@@ -1579,7 +1570,7 @@ __device__ __forceinline__ void prefetch_row(const KernelArgs& a, int sc, int t)
     prefetch_l2(p, d.bytes < (1u << 24) ? d.bytes : (1u << 24));
 }
 
-template <bool STEP, int OBS>
+template <bool STEP, int OBS, bool REC>
 #ifndef ZS_MIN_BLOCKS
 #define ZS_MIN_BLOCKS 7  // 72 registers: 28 resident warps per SM
 #endif
@@ -1603,7 +1594,7 @@ __global__ void __launch_bounds__(kThreads, ZS_MIN_BLOCKS) k_step_observe(const 
             prefetch_row<STEP, OBS>(a, scen_of(a.pk, b + stride), w.rs->r0.t + (STEP ? 1 : 0));
         ROW_MARK(b, 0);
         if (STEP) {
-            step_row(a, b, w);
+            step_row<REC>(a, b, w);
         } else {
             if (lane_id() == 0) {
                 w.rs->r = w.rs->r0;
@@ -1852,7 +1843,7 @@ bool observe_split(const KernelArgs& a, int policy) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     KernelArgs t = a;
     t.lay = warp_layout(t.pk.d.A, t.cand_cap, t.cfg.n_agents, t.pk.d.NS);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_observe<true, kObsAll>, kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_observe<true, kObsAll, false>, kThreads,
                                                       smem_bytes(t)) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     // measured: equal at 2 waves (C1 shapes), split clearly ahead at many waves (C2)
@@ -1871,23 +1862,30 @@ cudaError_t launch_step_observe(const KernelArgs& a, int mode, int policy, cudaS
         return cudaGetLastError();
     };
     const bool split = mode != kModeStep && observe_split(a, policy);
+    // recording / scripted actions (zsim_rollout) use their own instantiations
+    const bool rec = a.ep.reward != nullptr || a.act_len != 0;
     switch (mode) {
-        case kModeStep: return launch(k_step_observe<true, 0>, a, false);
+        case kModeStep:
+            return rec ? launch(k_step_observe<true, 0, true>, a, false) : launch(k_step_observe<true, 0, false>, a, false);
         case kModeObserve: {
-            if (!split) return launch(k_step_observe<false, kObsAll>, a, true);
-            cudaError_t e = launch(k_step_observe<false, kObsAgents>, a, false);
-            return e != cudaSuccess ? e : launch(k_step_observe<false, kObsMap>, a, true);
+            if (!split) return launch(k_step_observe<false, kObsAll, false>, a, true);
+            cudaError_t e = launch(k_step_observe<false, kObsAgents, false>, a, false);
+            return e != cudaSuccess ? e : launch(k_step_observe<false, kObsMap, false>, a, true);
         }
         default: {
-            if (!split) return launch(k_step_observe<true, kObsAll>, a, true);
+            if (!split)
+                return rec ? launch(k_step_observe<true, kObsAll, true>, a, true)
+                           : launch(k_step_observe<true, kObsAll, false>, a, true);
             // step + agents (the agent boxes at t+1 are reused), then the map
             // parts on the post-step state
-            cudaError_t e = launch(k_step_observe<true, kObsAgents>, a, false);
+            cudaError_t e = rec ? launch(k_step_observe<true, kObsAgents, true>, a, false)
+                                : launch(k_step_observe<true, kObsAgents, false>, a, false);
             if (e != cudaSuccess) return e;
             KernelArgs m = a;
             m.in = a.out;
             m.ep = zsim_episode_view{};
-            return launch(k_step_observe<false, kObsMap>, m, true);
+            m.act_len = 0;
+            return launch(k_step_observe<false, kObsMap, false>, m, true);
         }
     }
 }
