@@ -192,6 +192,23 @@ ZSIM_API int zsim_controlled_expand(const uint8_t* zsim_file, size_t nbytes, con
                                     int32_t n_indices, const zsim_sim_config* cfg, uint8_t** out_buf,
                                     size_t* out_len);
 ZSIM_API int zsim_env_destroy(zsim_env* env);
+
+/* BatchStream (scenario_stream.hpp:12-40): the dataset
+ * in file order as batches of `batch_size` (the last may be short), each
+ * staged as a device Env.  With `prefetch`, batch k+1 is decoded, staged on
+ * the host and uploaded from pinned memory on a copy stream while the caller
+ * simulates batch k; delivered batches are identical either way.
+ * `controlled` = stage each batch like zsim_env_create_controlled. */
+typedef struct zsim_stream zsim_stream;
+ZSIM_API int zsim_stream_create(const uint8_t* zsim_file, size_t nbytes, int32_t batch_size, int32_t horizon,
+                                const zsim_sim_config* cfg, const double* accel_bins, int32_t n_accel,
+                                const double* steer_bins, int32_t n_steer, int32_t device, int32_t prefetch,
+                                int32_t controlled, zsim_stream** out);
+ZSIM_API int zsim_stream_num_batches(const zsim_stream* stream, int64_t* out);
+/* The next batch's Env, owned by the stream and valid until the next call (or
+ * destroy); *env = NULL once the dataset is exhausted. */
+ZSIM_API int zsim_stream_next(zsim_stream* stream, zsim_env** env);
+ZSIM_API int zsim_stream_destroy(zsim_stream* stream);
 ZSIM_API int zsim_env_get_info(const zsim_env* env, zsim_env_info* out);
 /* Env::goal_s / initial_s / logged_progress (simcore.hpp:207-209): host arrays of B doubles (any may be NULL). */
 ZSIM_API int zsim_env_get_scalars(const zsim_env* env, double* goal_s, double* initial_s, double* logged_progress);

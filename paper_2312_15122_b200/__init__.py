@@ -6,7 +6,7 @@ the reference's ``zsim::sim::Env`` API.  Importing it loads the native library
 and fails loudly when it is missing -- there is no CPU fallback.
 """
 from ._abi import ZsimError, lib  # noqa: F401
-from .env import (AGGREGATE_FIELDS, DONE_REASONS, DeviceEpisode, DeviceObs, DeviceState, DeviceStepOut,  # noqa: F401
+from .env import (AGGREGATE_FIELDS, DONE_REASONS, BatchStream, DeviceEpisode, DeviceObs, DeviceState, DeviceStepOut,  # noqa: F401
                   Env, ObservationBatch, aggregate_finalize,
                   STRESS_C2, SimConfig, SimStateBatch, StepOut, StressConfig, controlled_expand, event_bit,
                   random_actions, stress_scenarios)
@@ -14,4 +14,4 @@ from .env import (AGGREGATE_FIELDS, DONE_REASONS, DeviceEpisode, DeviceObs, Devi
 __all__ = ["Env", "SimConfig", "SimStateBatch", "StepOut", "ObservationBatch", "DeviceState", "DeviceStepOut",
            "DeviceObs", "StressConfig", "stress_scenarios", "random_actions", "ZsimError", "DONE_REASONS",
            "event_bit", "lib", "controlled_expand", "STRESS_C2", "DeviceEpisode", "aggregate_finalize",
-           "AGGREGATE_FIELDS"]
+           "AGGREGATE_FIELDS", "BatchStream"]

@@ -110,6 +110,12 @@ SIGNATURES = {
     "zsim_controlled_expand": (C.c_int, [_P, C.c_size_t, C.POINTER(C.c_int64), C.c_int32, C.POINTER(SimConfigC),
                                          C.POINTER(_P), C.POINTER(C.c_size_t)]),
     "zsim_env_destroy": (C.c_int, [_P]),
+    "zsim_stream_create": (C.c_int, [_P, C.c_size_t, C.c_int32, C.c_int32, C.POINTER(SimConfigC), c_double_p,
+                                     C.c_int32, c_double_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(_P)]),
+    "zsim_stream_num_batches": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "zsim_stream_next": (C.c_int, [_P, C.POINTER(_P)]),
+    "zsim_stream_destroy": (C.c_int, [_P]),
     "zsim_episode_alloc": (C.c_int, [_P, C.c_int32, C.POINTER(EpisodeView)]),
     "zsim_episode_free": (C.c_int, [_P, C.POINTER(EpisodeView)]),
     "zsim_episode_bytes": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_size_t)]),

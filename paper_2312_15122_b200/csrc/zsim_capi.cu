@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <future>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -377,7 +378,15 @@ void write_points(unsigned char* host, size_t o_xy, size_t o_attr, size_t o_oi, 
 // scenario, as Env::Env.  Controlled mode: one row per
 // controllable actor of every scenario (zsim_scenario.hpp, controlled_scene);
 // scenario data is stored once and rows index it (row_scen / row_actor).
-void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon, bool controlled) {
+// Pinned staging buffer + copy stream of a BatchStream slot.
+struct Uploader {
+    void* pinned = nullptr;
+    size_t cap = 0;
+    cudaStream_t stream = nullptr;
+};
+
+void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon, bool controlled,
+               Uploader* up = nullptr) {
     using namespace zs;
     if (scenes.empty()) raise(Err::invalid_argument, "make_batch: empty scenario list");
     const int S = int(scenes.size());
@@ -662,7 +671,6 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
 
     cuda_check(cudaMalloc(&env->d_pack, pb.cursor), "cudaMalloc(pack)");
     env->pack_bytes = pb.cursor;
-    cuda_check(cudaMemcpy(env->d_pack, pb.host.data(), pb.cursor, cudaMemcpyHostToDevice), "upload pack");
     unsigned char* D = static_cast<unsigned char*>(env->d_pack);
     DevPack& pk = env->base.pk;
     pk.d = d;
@@ -733,9 +741,25 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
             {pk.ag_wid, A * 4, 0, A * 4, 0},
             {pk.lt_state, uint32_t(d.NL) * uint32_t(d.T), 0, uint32_t(d.NL) * uint32_t(d.T), 0},
         };
-        cuda_check(cudaMemcpy(D + o_pf, tab, sizeof(tab), cudaMemcpyHostToDevice), "upload prefetch table");
+        std::memcpy(pb.host.data() + o_pf, tab, sizeof(tab));
         pk.pf = reinterpret_cast<const PfDesc*>(D + o_pf);
         pk.n_pf = kPf;
+    }
+    // one upload of the whole image: synchronous, or (BatchStream) through a
+    // pinned staging buffer on a copy stream
+    if (up) {
+        if (up->cap < pb.cursor) {
+            if (up->pinned) cudaFreeHost(up->pinned);
+            up->pinned = nullptr;
+            up->cap = 0;
+            cuda_check(cudaHostAlloc(&up->pinned, pb.cursor, cudaHostAllocDefault), "cudaHostAlloc(stream staging)");
+            up->cap = pb.cursor;
+        }
+        std::memcpy(up->pinned, pb.host.data(), pb.cursor);
+        cuda_check(cudaMemcpyAsync(env->d_pack, up->pinned, pb.cursor, cudaMemcpyHostToDevice, up->stream),
+                   "upload pack");
+    } else {
+        cuda_check(cudaMemcpy(env->d_pack, pb.host.data(), pb.cursor, cudaMemcpyHostToDevice), "upload pack");
     }
 
     env->B = B;
@@ -841,6 +865,52 @@ std::vector<zs::Scene> decode_batch(const uint8_t* file, size_t nbytes, const in
     return scenes;
 }
 
+std::unique_ptr<zsim_env> build_env(std::vector<zs::Scene> scenes, int32_t horizon, const zsim_sim_config* cfg,
+                                    const double* accel_bins, int32_t n_accel, const double* steer_bins,
+                                    int32_t n_steer, int32_t device, bool controlled, Uploader* up) {
+    std::unique_ptr<zsim_env> env(new zsim_env());
+    env->device = device;
+    if (cfg) {
+        env->cfg = *cfg;
+    } else {
+        zsim_sim_config_defaults(&env->cfg);
+    }
+    if (env->cfg.n_agents <= 0 || env->cfg.n_road <= 0 || env->cfg.n_route <= 0)
+        raise(Err::invalid_argument, "nearest_features: k must be > 0");
+    if (accel_bins && n_accel > 0)
+        env->accel_bins.assign(accel_bins, accel_bins + n_accel);
+    else
+        env->accel_bins = {-4.0, -2.0, -0.5, 0.0, 0.5, 2.0, 4.0};
+    if (steer_bins && n_steer > 0)
+        env->steer_bins.assign(steer_bins, steer_bins + n_steer);
+    else
+        env->steer_bins = {-0.4, -0.1, 0.0, 0.1, 0.4};
+    zs::check_bins(env->accel_bins, "accel_bins");
+    zs::check_bins(env->steer_bins, "steer_rate_bins");
+    if (env->accel_bins.size() > 16 || env->steer_bins.size() > 16)
+        raise(Err::invalid_argument, "at most 16 bins per action head on the device path");
+    env->zero_accel = zs::nearest_bin(env->accel_bins, 0.0);
+    env->zero_steer = zs::nearest_bin(env->steer_bins, 0.0);
+    int maxsteps = 2;
+    for (const auto& sc : scenes) maxsteps = std::max(maxsteps, int(sc.num_steps));
+    if (horizon <= 0) horizon = maxsteps;
+    set_device(env.get());
+    env->base.cfg = make_dev_cfg(env->cfg, env->accel_bins, env->steer_bins);
+    stage_env(env.get(), scenes, horizon, controlled, up);
+    cuda_check(cudaMalloc(&env->d_hint, sizeof(float4) * size_t(env->B)), "cudaMalloc(hint)");
+    cuda_check(cudaMalloc(&env->d_err, 4), "cudaMalloc(err)");
+    if (up) {
+        cuda_check(cudaMemsetAsync(env->d_hint, 0xFF, sizeof(float4) * size_t(env->B), up->stream), "cudaMemset(hint)");
+        cuda_check(cudaMemsetAsync(env->d_err, 0, 4, up->stream), "cudaMemset(err)");
+    } else {
+        cuda_check(cudaMemset(env->d_hint, 0xFF, sizeof(float4) * size_t(env->B)), "cudaMemset(hint)");  // NaN: no hint
+        cuda_check(cudaMemset(env->d_err, 0, 4), "cudaMemset(err)");
+    }
+    env->base.hint = env->d_hint;
+    env->base.err = env->d_err;
+    return env;
+}
+
 int create_env(const uint8_t* file, size_t nbytes, const int64_t* indices, int32_t n_indices, int32_t horizon,
                const zsim_sim_config* cfg, const double* accel_bins, int32_t n_accel, const double* steer_bins,
                int32_t n_steer, int32_t device, zsim_env** out, bool controlled) {
@@ -848,44 +918,9 @@ int create_env(const uint8_t* file, size_t nbytes, const int64_t* indices, int32
         if (!out) raise(Err::invalid_argument, "null output pointer");
         *out = nullptr;
         if (!file) raise(Err::invalid_argument, "null ZSIM buffer");
-        std::unique_ptr<zsim_env> env(new zsim_env());
-        env->device = device;
-        if (cfg) {
-            env->cfg = *cfg;
-        } else {
-            zsim_sim_config_defaults(&env->cfg);
-        }
-        if (env->cfg.n_agents <= 0 || env->cfg.n_road <= 0 || env->cfg.n_route <= 0)
-            raise(Err::invalid_argument, "nearest_features: k must be > 0");
-        if (accel_bins && n_accel > 0)
-            env->accel_bins.assign(accel_bins, accel_bins + n_accel);
-        else
-            env->accel_bins = {-4.0, -2.0, -0.5, 0.0, 0.5, 2.0, 4.0};
-        if (steer_bins && n_steer > 0)
-            env->steer_bins.assign(steer_bins, steer_bins + n_steer);
-        else
-            env->steer_bins = {-0.4, -0.1, 0.0, 0.1, 0.4};
-        zs::check_bins(env->accel_bins, "accel_bins");
-        zs::check_bins(env->steer_bins, "steer_rate_bins");
-        if (env->accel_bins.size() > 16 || env->steer_bins.size() > 16)
-            raise(Err::invalid_argument, "at most 16 bins per action head on the device path");
-        env->zero_accel = zs::nearest_bin(env->accel_bins, 0.0);
-        env->zero_steer = zs::nearest_bin(env->steer_bins, 0.0);
-
-        std::vector<zs::Scene> scenes = decode_batch(file, nbytes, indices, n_indices);
-        int maxsteps = 2;
-        for (const auto& sc : scenes) maxsteps = std::max(maxsteps, int(sc.num_steps));
-        if (horizon <= 0) horizon = maxsteps;
-        set_device(env.get());
-        env->base.cfg = make_dev_cfg(env->cfg, env->accel_bins, env->steer_bins);
-        stage_env(env.get(), scenes, horizon, controlled);
-        cuda_check(cudaMalloc(&env->d_hint, sizeof(float4) * size_t(env->B)), "cudaMalloc(hint)");
-        cuda_check(cudaMemset(env->d_hint, 0xFF, sizeof(float4) * size_t(env->B)), "cudaMemset(hint)");  // NaN: no hint
-        env->base.hint = env->d_hint;
-        cuda_check(cudaMalloc(&env->d_err, 4), "cudaMalloc(err)");
-        cuda_check(cudaMemset(env->d_err, 0, 4), "cudaMemset(err)");
-        env->base.err = env->d_err;
-        *out = env.release();
+        *out = build_env(decode_batch(file, nbytes, indices, n_indices), horizon, cfg, accel_bins, n_accel, steer_bins,
+                         n_steer, device, controlled, nullptr)
+                   .release();
     });
 }
 
@@ -904,6 +939,117 @@ ZSIM_API int zsim_env_create_controlled(const uint8_t* file, size_t nbytes, cons
                                         zsim_env** out) {
     return create_env(file, nbytes, indices, n_indices, horizon, cfg, accel_bins, n_accel, steer_bins, n_steer, device,
                       out, true);
+}
+
+// ---------------------------------------------------------------------------
+// BatchStream (scenario_stream.hpp:12-40, scenario_stream.cpp:35-46) feeding
+// device Envs: while the caller simulates batch k, a staging thread decodes
+// batch k+1, builds its route frames / pack on the host, and uploads it from
+// a pinned buffer on a copy stream (two buffers alternate).
+// ---------------------------------------------------------------------------
+struct zsim_stream {
+    std::vector<uint8_t> file;
+    zs::ZsimIndex idx;
+    int32_t batch_size = 0, horizon = 0, device = 0;
+    bool prefetch = true, controlled = false;
+    bool has_cfg = false;
+    zsim_sim_config cfg{};
+    std::vector<double> ab, sb;
+    int64_t cursor = 0, num_batches = 0;
+    zsim_env* current = nullptr;
+    std::future<zsim_env*> staged;
+    Uploader up[2];
+    int slot = 0;
+
+    zsim_env* load(int64_t k, int sl) {
+        cudaSetDevice(device);
+        const int64_t n = int64_t(idx.records.size());
+        const int64_t begin = k * batch_size, end = std::min(begin + batch_size, n);
+        std::vector<zs::Scene> scenes;
+        scenes.reserve(size_t(end - begin));
+        for (int64_t i = begin; i < end; ++i) scenes.push_back(zs::zsim_decode(file.data(), file.size(), idx, i));
+        auto env = build_env(std::move(scenes), horizon, has_cfg ? &cfg : nullptr, ab.empty() ? nullptr : ab.data(),
+                             int32_t(ab.size()), sb.empty() ? nullptr : sb.data(), int32_t(sb.size()), device,
+                             controlled, &up[sl]);
+        cuda_check(cudaStreamSynchronize(up[sl].stream), "stream upload");
+        return env.release();
+    }
+};
+
+ZSIM_API int zsim_stream_create(const uint8_t* file, size_t nbytes, int32_t batch_size, int32_t horizon,
+                                const zsim_sim_config* cfg, const double* accel_bins, int32_t n_accel,
+                                const double* steer_bins, int32_t n_steer, int32_t device, int32_t prefetch,
+                                int32_t controlled, zsim_stream** out) {
+    return guarded([&] {
+        if (!out) raise(Err::invalid_argument, "null output pointer");
+        *out = nullptr;
+        if (!file) raise(Err::invalid_argument, "null ZSIM buffer");
+        if (batch_size <= 0) raise(Err::invalid_argument, "batch_size must be > 0");  // scenario_stream.cpp:9
+        std::unique_ptr<zsim_stream> st(new zsim_stream());
+        st->file.assign(file, file + nbytes);
+        st->idx = zs::zsim_index(st->file.data(), st->file.size());
+        if (st->idx.records.empty()) raise(Err::invalid_argument, "batch_iterator: dataset is empty");
+        st->batch_size = batch_size;
+        st->horizon = horizon;
+        st->device = device;
+        st->prefetch = prefetch != 0;
+        st->controlled = controlled != 0;
+        if (cfg) st->cfg = *cfg, st->has_cfg = true;
+        if (accel_bins && n_accel > 0) st->ab.assign(accel_bins, accel_bins + n_accel);
+        if (steer_bins && n_steer > 0) st->sb.assign(steer_bins, steer_bins + n_steer);
+        st->num_batches = (int64_t(st->idx.records.size()) + batch_size - 1) / batch_size;
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        for (auto& u : st->up) cuda_check(cudaStreamCreateWithFlags(&u.stream, cudaStreamNonBlocking), "copy stream");
+        *out = st.release();
+    });
+}
+
+ZSIM_API int zsim_stream_num_batches(const zsim_stream* st, int64_t* out) {
+    return guarded([&] {
+        if (!st || !out) raise(Err::invalid_argument, "null stream/output");
+        *out = st->num_batches;
+    });
+}
+
+ZSIM_API int zsim_stream_next(zsim_stream* st, zsim_env** out) {
+    return guarded([&] {
+        if (!st || !out) raise(Err::invalid_argument, "null stream/output");
+        *out = nullptr;
+        if (st->current) {  // the previous batch's Env ends here
+            zsim_env_destroy(st->current);
+            st->current = nullptr;
+        }
+        if (st->cursor >= st->num_batches) return;
+        zsim_env* env = st->staged.valid() ? st->staged.get() : st->load(st->cursor, st->slot);
+        st->slot ^= 1;
+        ++st->cursor;
+        if (st->prefetch && st->cursor < st->num_batches) {
+            const int64_t k = st->cursor;
+            const int sl = st->slot;
+            st->staged = std::async(std::launch::async, [st, k, sl] { return st->load(k, sl); });
+        }
+        st->current = env;
+        *out = env;
+    });
+}
+
+ZSIM_API int zsim_stream_destroy(zsim_stream* st) {
+    return guarded([&] {
+        if (!st) return;
+        if (st->staged.valid()) {
+            try {
+                zsim_env_destroy(st->staged.get());
+            } catch (...) {
+            }
+        }
+        if (st->current) zsim_env_destroy(st->current);
+        cudaSetDevice(st->device);
+        for (auto& u : st->up) {
+            if (u.stream) cudaStreamDestroy(u.stream);
+            if (u.pinned) cudaFreeHost(u.pinned);
+        }
+        delete st;
+    });
 }
 
 ZSIM_API int zsim_env_get_rows(const zsim_env* env, int32_t* scenario, int32_t* actor) {

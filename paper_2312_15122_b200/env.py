@@ -302,6 +302,21 @@ class Env:
                      0 if ab is None else int(ab.size), None if sb is None else _ptr(sb, C.c_double),
                      0 if sb is None else int(sb.size), int(device), C.byref(h)))
         self.handle = h.value
+        self._owned = True
+        self._attach()
+
+    @classmethod
+    def _borrowed(cls, handle: int, config: SimConfig) -> "Env":
+        """An Env over a handle owned elsewhere (a BatchStream batch)."""
+        self = cls.__new__(cls)
+        self._bytes = b""
+        self._config = config
+        self.handle = handle
+        self._owned = False
+        self._attach()
+        return self
+
+    def _attach(self) -> None:
         info = EnvInfo()
         check(lib.zsim_env_get_info(self.handle, C.byref(info)))
         self.info = info
@@ -321,7 +336,8 @@ class Env:
 
     def close(self):
         if getattr(self, "handle", None):
-            lib.zsim_env_destroy(self.handle)
+            if getattr(self, "_owned", True):
+                lib.zsim_env_destroy(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -574,6 +590,63 @@ def stress_scenarios(cfg: StressConfig, seed: int = 7) -> bytes:
         return C.string_at(p.value, n.value)
     finally:
         lib.zsim_free_buffer(p)
+
+
+class BatchStream:
+    """scenario::BatchStream (scenario_stream.hpp:12-40) feeding device Envs:
+    iterate to get one Env per batch; batch k+1 is decoded, staged and
+    uploaded (pinned buffer, copy stream) while batch k is simulated.  Each
+    Env is valid until the next batch is requested."""
+
+    def __init__(self, zsim, batch_size: int, horizon: int = 0, config: SimConfig | None = None,
+                 accel_bins=None, steer_bins=None, device: int = 0, prefetch: bool = True, controlled: bool = False):
+        if isinstance(zsim, (str, os.PathLike)):
+            zsim = Path(zsim).read_bytes()
+        self._config = config or SimConfig()
+        cfg = self._config.to_c()
+        ab = np.ascontiguousarray(accel_bins, dtype=np.float64) if accel_bins is not None else None
+        sb = np.ascontiguousarray(steer_bins, dtype=np.float64) if steer_bins is not None else None
+        buf = C.create_string_buffer(bytes(zsim), len(zsim))
+        h = C.c_void_p()
+        check(lib.zsim_stream_create(C.cast(buf, C.c_void_p), C.c_size_t(len(zsim)), int(batch_size), int(horizon),
+                                     C.byref(cfg), None if ab is None else _ptr(ab, C.c_double),
+                                     0 if ab is None else int(ab.size), None if sb is None else _ptr(sb, C.c_double),
+                                     0 if sb is None else int(sb.size), int(device), int(bool(prefetch)),
+                                     int(bool(controlled)), C.byref(h)))
+        self.handle = h.value
+        self._env = None
+
+    def __len__(self) -> int:
+        n = C.c_int64()
+        check(lib.zsim_stream_num_batches(self.handle, C.byref(n)))
+        return n.value
+
+    def __iter__(self):
+        return self
+
+    def __next__(self) -> "Env":
+        if self._env is not None:
+            self._env.handle = None  # the stream destroys it on the next call
+        h = C.c_void_p()
+        check(lib.zsim_stream_next(self.handle, C.byref(h)))
+        if not h.value:
+            self._env = None
+            raise StopIteration
+        self._env = Env._borrowed(h.value, self._config)
+        return self._env
+
+    def close(self):
+        if getattr(self, "handle", None):
+            if self._env is not None:
+                self._env.handle = None
+            lib.zsim_stream_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def controlled_expand(zsim: bytes, indices=None, config: SimConfig | None = None) -> bytes:
