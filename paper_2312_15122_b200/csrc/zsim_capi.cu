@@ -3,8 +3,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <exception>
+#include <functional>
 #include <future>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -378,6 +382,50 @@ void write_points(unsigned char* host, size_t o_xy, size_t o_attr, size_t o_oi, 
 // scenario, as Env::Env.  Controlled mode: one row per
 // controllable actor of every scenario (zsim_scenario.hpp, controlled_scene);
 // scenario data is stored once and rows index it (row_scen / row_actor).
+// Runs f(i) for i in [0, n) on the host cores (staging is per scenario / per
+// row and writes disjoint regions).  The lowest failing index's exception is
+// rethrown, as a serial loop would.
+void parallel_for(int n, const std::function<void(int)>& f) {
+    int nt = int(std::min(32u, std::max(1u, std::thread::hardware_concurrency())));
+    if (nt <= 1 || n < 64) {
+        for (int i = 0; i < n; ++i) f(i);
+        return;
+    }
+    struct Slot {
+        std::exception_ptr ex;
+        int at = INT32_MAX;
+    };
+    std::atomic<int> next{0};
+    std::vector<Slot> slots(static_cast<size_t>(nt));
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+        Slot* my = slots.data() + t;
+        th.emplace_back([&next, &f, n, my] {
+            for (;;) {
+                const int i0 = next.fetch_add(16);
+                if (i0 >= n) return;
+                const int i1 = std::min(n, i0 + 16);
+                for (int i = i0; i < i1; ++i) {
+                    try {
+                        f(i);
+                    } catch (...) {
+                        if (i < my->at) {
+                            my->at = i;
+                            my->ex = std::current_exception();
+                        }
+                        return;
+                    }
+                }
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    const Slot* best = nullptr;
+    for (const Slot& sl : slots)
+        if (sl.ex && (!best || sl.at < best->at)) best = &sl;
+    if (best) std::rethrow_exception(best->ex);
+}
+
 // Pinned staging buffer + copy stream of a BatchStream slot.
 struct Uploader {
     void* pinned = nullptr;
@@ -410,10 +458,12 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     d.C = 2;
     d.NL = 1;
     d.NS = 1;
+    parallel_for(S, [&](int b) {
+        ctx[size_t(b)] = build_context(scenes[size_t(b)]);
+        rpts[size_t(b)] = build_route_points(scenes[size_t(b)]);
+    });
     for (int b = 0; b < S; ++b) {
         const Scene& s = scenes[size_t(b)];
-        ctx[size_t(b)] = build_context(s);
-        rpts[size_t(b)] = build_route_points(s);
         d.T = std::max(d.T, int(s.num_steps));
         d.A = std::max(d.A, controlled ? num_actors(s) : int(s.agents.size()));
         size_t np = 0;
@@ -499,6 +549,10 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     env->row_actor.assign(size_t(B), -1);
     int total_stop = 0;
     for (int r = 0; r < B; ++r) {
+        pb.at<int32_t>(o_soff)[r] = total_stop;
+        total_stop += int(ctx[size_t(rows[size_t(r)].first)].stops.size());
+    }
+    parallel_for(B, [&](int r) {
         // row-level: the controlled actor's initial state and goal (simcore.cpp:217-223, 237-276)
         const int sb = rows[size_t(r)].first, actor = rows[size_t(r)].second;
         const Scene& s = scenes[size_t(sb)];
@@ -509,8 +563,6 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
         env->row_actor[size_t(r)] = actor;
         pb.at<int32_t>(o_rsc)[r] = sb;
         pb.at<int32_t>(o_rac)[r] = actor;
-        pb.at<int32_t>(o_soff)[r] = total_stop;
-        total_stop += int(c.stops.size());
         pb.at<float>(o_gx)[r] = eg.goal_x;
         pb.at<float>(o_gy)[r] = eg.goal_y;
         double gs = project_host(double(eg.goal_x), double(eg.goal_y), c).s;
@@ -525,8 +577,8 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
         pb.at<double>(o_ih)[r] = double(eg.ego_h[0]);
         pb.at<double>(o_iv)[r] = double(eg.ego_v[0]);
         pb.at<double>(o_ist)[r] = initial_steering(eg, env->cfg.wheelbase, env->cfg.delta_max);
-    }
-    for (int b = 0; b < S; ++b) {
+    });
+    parallel_for(S, [&](int b) {
         const Scene& s = scenes[size_t(b)];
         const RouteCtx& c = ctx[size_t(b)];
         const int T = d.T, A = d.A;
@@ -667,7 +719,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
                 pb.at<uint8_t>(o_ltst)[(size_t(b) * d.NL + k) * d.T + t] = st[t];
         }
         for (size_t j = 0; j < c.stops.size(); ++j) pb.at<double>(o_sts)[size_t(b) * d.NS + j] = c.stops[j].second;
-    }
+    });
 
     cuda_check(cudaMalloc(&env->d_pack, pb.cursor), "cudaMalloc(pack)");
     env->pack_bytes = pb.cursor;
@@ -859,9 +911,8 @@ std::vector<zs::Scene> decode_batch(const uint8_t* file, size_t nbytes, const in
     } else {
         for (int64_t i = 0; i < int64_t(idx.records.size()); ++i) rows.push_back(i);
     }
-    std::vector<zs::Scene> scenes;
-    scenes.reserve(rows.size());
-    for (int64_t r : rows) scenes.push_back(zs::zsim_decode(file, nbytes, idx, r));
+    std::vector<zs::Scene> scenes(rows.size());
+    parallel_for(int(rows.size()), [&](int i) { scenes[size_t(i)] = zs::zsim_decode(file, nbytes, idx, rows[size_t(i)]); });
     return scenes;
 }
 
@@ -965,9 +1016,10 @@ struct zsim_stream {
         cudaSetDevice(device);
         const int64_t n = int64_t(idx.records.size());
         const int64_t begin = k * batch_size, end = std::min(begin + batch_size, n);
-        std::vector<zs::Scene> scenes;
-        scenes.reserve(size_t(end - begin));
-        for (int64_t i = begin; i < end; ++i) scenes.push_back(zs::zsim_decode(file.data(), file.size(), idx, i));
+        std::vector<zs::Scene> scenes(size_t(end - begin));
+        parallel_for(int(end - begin), [&](int i) {
+            scenes[size_t(i)] = zs::zsim_decode(file.data(), file.size(), idx, begin + i);
+        });
         auto env = build_env(std::move(scenes), horizon, has_cfg ? &cfg : nullptr, ab.empty() ? nullptr : ab.data(),
                              int32_t(ab.size()), sb.empty() ? nullptr : sb.data(), int32_t(sb.size()), device,
                              controlled, &up[sl]);
