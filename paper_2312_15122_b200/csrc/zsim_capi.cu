@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <exception>
 #include <functional>
@@ -145,7 +147,12 @@ void carve_obs(unsigned char* base, const ObsLayout& L, zsim_obs_view* v) {
 
 // Host image of the pack: offsets into one buffer, then a single upload.
 struct PackBuilder {
-    std::vector<unsigned char> host;
+    // the image: caller memory (a BatchStream's pinned buffer) or owned
+    struct Buf {
+        unsigned char* p = nullptr;
+        unsigned char* data() { return p; }
+    } host;
+    std::unique_ptr<unsigned char[]> own;
     size_t cursor = 0;
     template <class T>
     size_t reserve(size_t n) {
@@ -426,6 +433,18 @@ void parallel_for(int n, const std::function<void(int)>& f) {
     if (best) std::rethrow_exception(best->ex);
 }
 
+// ZSIM_STAGE_TIMING=1: per-phase wall times of the host staging on stderr.
+struct StageTimer {
+    bool on = std::getenv("ZSIM_STAGE_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[stage] %-22s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+
 // Pinned staging buffer + copy stream of a BatchStream slot.
 struct Uploader {
     void* pinned = nullptr;
@@ -438,6 +457,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     using namespace zs;
     if (scenes.empty()) raise(Err::invalid_argument, "make_batch: empty scenario list");
     const int S = int(scenes.size());
+    StageTimer tm;
     const double dt = scenes[0].dt;
     for (const auto& s : scenes) {
         if (int(s.num_steps) > horizon) {
@@ -487,6 +507,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
             if (s.ego_x.empty()) raise(Err::invalid_argument, "scenario `" + s.id + "`: empty ego log");
         }
     }
+    tm.mark("contexts");
     // rows: (scenario, controlled actor); actor -1 = the scenario's own ego (ego mode)
     std::vector<std::pair<int, int>> rows;
     for (int b = 0; b < S; ++b) {
@@ -540,7 +561,28 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     size_t o_rsc = pb.reserve<int32_t>(B), o_rac = pb.reserve<int32_t>(B);
     constexpr int kPf = 13;
     size_t o_pf = pb.reserve<PfDesc>(kPf);
-    pb.host.assign(pb.cursor, 0);
+    if (up) {
+        if (up->cap < pb.cursor) {
+            if (up->pinned) cudaFreeHost(up->pinned);
+            up->pinned = nullptr;
+            up->cap = 0;
+            cuda_check(cudaHostAlloc(&up->pinned, pb.cursor, cudaHostAllocDefault), "cudaHostAlloc(stream staging)");
+            up->cap = pb.cursor;
+        }
+        pb.host.p = static_cast<unsigned char*>(up->pinned);
+    } else {
+        pb.own.reset(new unsigned char[pb.cursor]);
+        pb.host.p = pb.own.get();
+    }
+    {
+        // zero the image (padding must be 0) in parallel 4 MB chunks
+        const size_t chunk = size_t(4) << 20;
+        parallel_for(int((pb.cursor + chunk - 1) / chunk), [&](int i) {
+            const size_t o = size_t(i) * chunk;
+            std::memset(pb.host.p + o, 0, std::min(chunk, pb.cursor - o));
+        });
+    }
+    tm.mark("host image alloc");
 
     env->goal_s.assign(size_t(B), 0.0);
     env->initial_s.assign(size_t(B), 0.0);
@@ -578,6 +620,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
         pb.at<double>(o_iv)[r] = double(eg.ego_v[0]);
         pb.at<double>(o_ist)[r] = initial_steering(eg, env->cfg.wheelbase, env->cfg.delta_max);
     });
+    tm.mark("rows");
     parallel_for(S, [&](int b) {
         const Scene& s = scenes[size_t(b)];
         const RouteCtx& c = ctx[size_t(b)];
@@ -721,6 +764,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
         for (size_t j = 0; j < c.stops.size(); ++j) pb.at<double>(o_sts)[size_t(b) * d.NS + j] = c.stops[j].second;
     });
 
+    tm.mark("scenario pack");
     cuda_check(cudaMalloc(&env->d_pack, pb.cursor), "cudaMalloc(pack)");
     env->pack_bytes = pb.cursor;
     unsigned char* D = static_cast<unsigned char*>(env->d_pack);
@@ -800,20 +844,14 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     // one upload of the whole image: synchronous, or (BatchStream) through a
     // pinned staging buffer on a copy stream
     if (up) {
-        if (up->cap < pb.cursor) {
-            if (up->pinned) cudaFreeHost(up->pinned);
-            up->pinned = nullptr;
-            up->cap = 0;
-            cuda_check(cudaHostAlloc(&up->pinned, pb.cursor, cudaHostAllocDefault), "cudaHostAlloc(stream staging)");
-            up->cap = pb.cursor;
-        }
-        std::memcpy(up->pinned, pb.host.data(), pb.cursor);
+        // built in place in the pinned buffer
         cuda_check(cudaMemcpyAsync(env->d_pack, up->pinned, pb.cursor, cudaMemcpyHostToDevice, up->stream),
                    "upload pack");
     } else {
         cuda_check(cudaMemcpy(env->d_pack, pb.host.data(), pb.cursor, cudaMemcpyHostToDevice), "upload pack");
     }
 
+    tm.mark("upload");
     env->B = B;
     env->n_scen = S;
     env->horizon = horizon;
