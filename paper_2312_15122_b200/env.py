@@ -70,6 +70,11 @@ class SimConfig:
         return c
 
 
+def _take_bytes(addr: int, n: int) -> bytes:
+    """Copy n bytes at addr (ctypes.string_at takes a C int size: > 2 GiB images need this)."""
+    return np.ctypeslib.as_array((C.c_uint8 * n).from_address(addr)).tobytes() if n else b""
+
+
 def _ptr(a: np.ndarray, ctype):
     assert a.flags["C_CONTIGUOUS"]
     return a.ctypes.data_as(C.POINTER(ctype))
@@ -587,7 +592,7 @@ def stress_scenarios(cfg: StressConfig, seed: int = 7) -> bytes:
     n = C.c_size_t()
     check(lib.zsim_stress_generate(C.byref(c), C.c_uint64(seed), C.byref(p), C.byref(n)))
     try:
-        return C.string_at(p.value, n.value)
+        return _take_bytes(p.value, n.value)
     finally:
         lib.zsim_free_buffer(p)
 
@@ -663,7 +668,7 @@ def controlled_expand(zsim: bytes, indices=None, config: SimConfig | None = None
     check(lib.zsim_controlled_expand(C.cast(buf, C.c_void_p), C.c_size_t(len(zsim)), idx, n_idx, C.byref(cfg),
                                      C.byref(p), C.byref(n)))
     try:
-        return C.string_at(p.value, n.value)
+        return _take_bytes(p.value, n.value)
     finally:
         lib.zsim_free_buffer(p)
 
