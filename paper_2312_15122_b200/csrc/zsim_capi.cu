@@ -192,6 +192,8 @@ struct zsim_env {
     zsim_obs_view h_obs{};
     int32_t* h_act = nullptr;
     cudaStream_t h_stream = nullptr;
+    cudaStream_t h_copy = nullptr;  // observe_host's chunked D2H
+    cudaEvent_t h_ev[4]{};
     double* d_initial_s = nullptr;
     double* d_logged = nullptr;          // logged_progress (device rollout recording)
     void* roll_buf = nullptr;            // zsim_rollout scratch: two states + one observation
@@ -1181,6 +1183,9 @@ ZSIM_API int zsim_env_destroy(zsim_env* env) {
         if (!env) return;
         cudaSetDevice(env->device);
         if (env->h_stream) cudaStreamDestroy(env->h_stream);
+        if (env->h_copy) cudaStreamDestroy(env->h_copy);
+        for (auto e : env->h_ev)
+            if (e) cudaEventDestroy(e);
         cudaFree(env->h_dev);
         cudaFree(env->d_pack);
         cudaFree(env->d_err);
@@ -1774,11 +1779,37 @@ ZSIM_API int zsim_observe_host(zsim_env* env, const zsim_state_view* in_host, co
         ensure_host_scratch(env);
         cudaStream_t s = env->h_stream;
         copy_state(env, &env->h_in, in_host, 0, s);
-        zs::KernelArgs a = args_for(env);
-        a.in = env->h_in;
-        a.obs = env->h_obs;
-        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->launch_policy, s), "observe kernel");
-        copy_obs(env, obs_host, &env->h_obs, 1, s);
+        // row chunks: the observation of chunk k streams to the host (copy
+        // stream) while chunk k+1 is computed
+        const int B = env->B;
+        const int nch = B >= 2048 ? 2 : 1;
+        if (!env->h_copy) {
+            cuda_check(cudaStreamCreateWithFlags(&env->h_copy, cudaStreamNonBlocking), "cudaStreamCreate");
+            for (auto& e : env->h_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        }
+        const ObsLayout& L = env->ol;
+        const int K[5] = {9, env->cfg.n_agents * 6, env->cfg.n_road * 12, env->cfg.n_route * 5, 2};
+        float* dst[5] = {obs_host->active, obs_host->agents, obs_host->road, obs_host->route, obs_host->value_only};
+        const float* src[5] = {env->h_obs.active, env->h_obs.agents, env->h_obs.road, env->h_obs.route,
+                               env->h_obs.value_only};
+        (void)L;
+        for (int c = 0; c < nch; ++c) {
+            const int lo = int(int64_t(B) * c / nch), hi = int(int64_t(B) * (c + 1) / nch);
+            zs::KernelArgs a = args_for(env);
+            a.in = env->h_in;
+            a.obs = env->h_obs;
+            a.row_lo = lo;
+            a.row_hi = hi;
+            cuda_check(zs::launch_step_observe(a, zs::kModeObserve, 1, s), "observe kernel");
+            cuda_check(cudaEventRecord(env->h_ev[c], s), "event");
+            cuda_check(cudaStreamWaitEvent(env->h_copy, env->h_ev[c], 0), "event wait");
+            for (int k = 0; k < 5; ++k) {
+                const size_t o = size_t(lo) * size_t(K[k]), n = size_t(hi - lo) * size_t(K[k]);
+                cuda_check(cudaMemcpyAsync(dst[k] + o, src[k] + o, 4 * n, cudaMemcpyDeviceToHost, env->h_copy),
+                           "obs copy");
+            }
+        }
+        cuda_check(cudaStreamSynchronize(env->h_copy), "stream sync");
         cuda_check(cudaStreamSynchronize(s), "stream sync");
     });
 }

@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <mutex>
+#include <vector>
 
 #include "zsim_geom.cuh"
 #include "zsim_kernels.cuh"
@@ -1579,9 +1581,10 @@ __global__ void __launch_bounds__(kThreads, ZS_MIN_BLOCKS) k_step_observe(const 
     const WarpBuf w = carve(dsm, a);
     const int wpb = kThreads / 32;
     const int stride = gridDim.x * wpb;
-    int b = blockIdx.x * wpb + warp_in_block();
-    if (b < a.pk.d.B) prefetch_row<STEP, OBS>(a, scen_of(a.pk, b), a.in.t[b] + (STEP ? 1 : 0));
-    for (; b < a.pk.d.B; b += stride) {
+    const int b_end = a.row_hi > 0 ? a.row_hi : a.pk.d.B;
+    int b = a.row_lo + blockIdx.x * wpb + warp_in_block();
+    if (b < b_end) prefetch_row<STEP, OBS>(a, scen_of(a.pk, b), a.in.t[b] + (STEP ? 1 : 0));
+    for (; b < b_end; b += stride) {
         if (lane_id() == 0) {
             w.rs->r0 = load_row(a.in, b);
             if ((OBS & kObsMap) && a.hint) w.rs->hint = a.hint[b];
@@ -1590,7 +1593,7 @@ __global__ void __launch_bounds__(kThreads, ZS_MIN_BLOCKS) k_step_observe(const 
         }
         __syncwarp();
         // the warp's next row: its static data streams into L2 while this row computes
-        if (b + stride < a.pk.d.B)
+        if (b + stride < b_end)
             prefetch_row<STEP, OBS>(a, scen_of(a.pk, b + stride), w.rs->r0.t + (STEP ? 1 : 0));
         ROW_MARK(b, 0);
         if (STEP) {
@@ -1816,19 +1819,47 @@ size_t smem_bytes(const KernelArgs& a) {
 
 static int grid_for(const KernelArgs& a) {
     const int wpb = kThreads / 32;
-    return (a.pk.d.B + wpb - 1) / wpb;
+    const int rows = (a.row_hi > 0 ? a.row_hi : a.pk.d.B) - a.row_lo;
+    return rows > 0 ? (rows + wpb - 1) / wpb : 1;
 }
 
 // Persistent grid: as many CTAs as fit on the device at once (each warp then
 // walks rows with a stride and prefetches its next row), capped by the work.
-template <class K>
-static int persistent_grid(K kern, const KernelArgs& a, size_t smem) {
-    int dev = 0, sms = 148, per_sm = 1;
+// The smem attribute and occupancy of a (kernel, smem) pair are queried once.
+struct LaunchCfg {
+    const void* fn;
+    size_t smem;
+    int dev, per_sm;
+};
+
+static int blocks_per_sm(const void* fn, size_t smem) {
+    static std::mutex mu;
+    static std::vector<LaunchCfg> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& c : cache)
+        if (c.fn == fn && c.smem == smem && c.dev == dev) return c.per_sm;
+    int per_sm = 1;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return -1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    cache.push_back({fn, smem, dev, per_sm});
+    return per_sm;
+}
+
+static int sm_count() {
+    int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
-        per_sm = 1;
-    int g = sms * per_sm;
+    return sms > 0 ? sms : 148;
+}
+
+template <class K>
+static int persistent_grid(K kern, const KernelArgs& a, size_t smem) {
+    int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), smem);
+    if (per_sm < 1) per_sm = 1;
+    int g = sm_count() * per_sm;
     int need = grid_for(a);
     return g < need ? g : need;
 }
@@ -1838,14 +1869,11 @@ static int persistent_grid(K kern, const KernelArgs& a, size_t smem) {
 bool observe_split(const KernelArgs& a, int policy) {
     if (policy == 1) return false;
     if (policy == 2) return true;
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     KernelArgs t = a;
     t.lay = warp_layout(t.pk.d.A, t.cand_cap, t.cfg.n_agents, t.pk.d.NS);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_observe<true, kObsAll, false>, kThreads,
-                                                      smem_bytes(t)) != cudaSuccess || per_sm < 1)
-        per_sm = 1;
+    int per_sm = blocks_per_sm(reinterpret_cast<const void*>(k_step_observe<true, kObsAll, false>), smem_bytes(t));
+    if (per_sm < 1) per_sm = 1;
+    const int sms = sm_count();
     // measured: equal at 2 waves (C1 shapes), split clearly ahead at many waves (C2)
     return a.pk.d.B > 3 * sms * per_sm * (kThreads / 32);
 }
@@ -1855,8 +1883,7 @@ cudaError_t launch_step_observe(const KernelArgs& a, int mode, int policy, cudaS
         if (!topk) am.cand_cap = 0;  // no top-k buffers in kernels without the map part
         am.lay = warp_layout(am.pk.d.A, am.cand_cap, am.cfg.n_agents, am.pk.d.NS);
         const size_t smem = smem_bytes(am);
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
+        if (blocks_per_sm(reinterpret_cast<const void*>(kern), smem) < 0) return cudaErrorInvalidValue;
         const int g = persistent_grid(kern, am, smem);
         kern<<<g, kThreads, smem, stream>>>(am);
         return cudaGetLastError();

@@ -44,6 +44,7 @@ struct KernelArgs {
     int32_t ep_t;          // rollout step being recorded
     int32_t act_len;       // > 0: accel/steer are a [act_len][B] script read at state.t (ScriptedPolicy); -1: empty
     int32_t zero_accel, zero_steer;
+    int32_t row_lo, row_hi;  // rows [row_lo, row_hi) of the batch; row_hi == 0: all rows
 };
 
 size_t smem_bytes(const KernelArgs& a);
