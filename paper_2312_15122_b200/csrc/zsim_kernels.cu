@@ -1834,14 +1834,26 @@ struct LaunchCfg {
 
 static int blocks_per_sm(const void* fn, size_t smem) {
     static std::mutex mu;
-    static std::vector<LaunchCfg> cache;
+    static std::vector<LaunchCfg> cache;     // occupancy per (kernel, smem, device)
+    static std::vector<LaunchCfg> attr_max;  // largest dynamic smem attribute set per (kernel, device)
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
+    // the attribute only ever grows: a smaller later request must not shrink
+    // it under another Env's larger launches
+    LaunchCfg* am = nullptr;
+    for (auto& c : attr_max)
+        if (c.fn == fn && c.dev == dev) am = &c;
+    if (!am || am->smem < smem) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return -1;
+        if (am)
+            am->smem = smem;
+        else
+            attr_max.push_back({fn, smem, dev, 0});
+    }
     for (const auto& c : cache)
         if (c.fn == fn && c.smem == smem && c.dev == dev) return c.per_sm;
     int per_sm = 1;
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return -1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     cache.push_back({fn, smem, dev, per_sm});
