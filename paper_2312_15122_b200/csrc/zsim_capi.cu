@@ -542,6 +542,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     size_t o_agx = pb.reserve<float>(nag), o_agy = pb.reserve<float>(nag), o_agh = pb.reserve<float>(nag),
            o_ags = pb.reserve<float>(nag), o_agv = pb.reserve<uint8_t>(nag);
     size_t o_agl = pb.reserve<float>(size_t(S) * d.A), o_agw = pb.reserve<float>(size_t(S) * d.A);
+    size_t o_agcs = pb.reserve<double>(nag * 2);
     size_t o_rxy = pb.reserve<float>(size_t(S) * d.P * 2), o_rkd = pb.reserve<uint8_t>(size_t(S) * d.P);
     size_t o_roi = pb.reserve<int32_t>(size_t(S) * d.P), o_rcb = pb.reserve<float>(size_t(S) * d.PC * 4);
     size_t o_txy = pb.reserve<float>(size_t(S) * d.R * 2), o_tfl = pb.reserve<uint8_t>(size_t(S) * d.R);
@@ -561,7 +562,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     size_t o_ix = pb.reserve<double>(B), o_iy = pb.reserve<double>(B), o_ih = pb.reserve<double>(B),
            o_iv = pb.reserve<double>(B), o_ist = pb.reserve<double>(B);
     size_t o_rsc = pb.reserve<int32_t>(B), o_rac = pb.reserve<int32_t>(B);
-    constexpr int kPf = 13;
+    constexpr int kPf = 14;
     size_t o_pf = pb.reserve<PfDesc>(kPf);
     if (up) {
         if (up->cap < pb.cursor) {
@@ -658,6 +659,12 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
                 pb.at<float>(o_agh)[k] = ag.heading[t];
                 pb.at<float>(o_ags)[k] = ag.speed[t];
                 pb.at<uint8_t>(o_agv)[k] = ag.valid[t];
+                // Obb::corners' cos / sin of the logged heading (geometry.cpp:8), computed with
+                // the host libm exactly as the reference does; the device builds the corners
+                // from them with the same IEEE operations
+                const double h = double(ag.heading[t]);
+                pb.at<double>(o_agcs)[2 * k] = std::cos(h);
+                pb.at<double>(o_agcs)[2 * k + 1] = std::sin(h);
             }
         }
         {
@@ -800,6 +807,7 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     pk.ag_valid = D + o_agv;
     pk.ag_len = reinterpret_cast<const float*>(D + o_agl);
     pk.ag_wid = reinterpret_cast<const float*>(D + o_agw);
+    pk.ag_cs = reinterpret_cast<const double2*>(D + o_agcs);
     pk.road_xy = reinterpret_cast<const float2*>(D + o_rxy);
     pk.road_kd = D + o_rkd;
     pk.road_oi = reinterpret_cast<const int32_t*>(D + o_roi);
@@ -832,7 +840,8 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
             {pk.route_cb, uint32_t(d.RC) * 16, 0, uint32_t(d.RC) * 16, 2},
             {pk.ag_x, TA * 4, A * 4, A * 4, 0},
             {pk.ag_y, TA * 4, A * 4, A * 4, 0},
-            {pk.ag_h, TA * 4, A * 4, A * 4, 0},
+            {pk.ag_h, TA * 4, A * 4, A * 4, 2},
+            {pk.ag_cs, TA * 16, A * 16, A * 16, 0},
             {pk.ag_sp, TA * 4, A * 4, A * 4, 2},
             {pk.ag_valid, TA, A, A, 0},
             {pk.ag_len, A * 4, 0, A * 4, 0},

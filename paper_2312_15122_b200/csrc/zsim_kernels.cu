@@ -569,15 +569,14 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
 __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size_t slice, int j, const Box& eb,
                                                  const double* EX, const double* EY, const WarpBuf& w) {
     const int A = pk.d.A;
-    double h = double(pk.ag_h[slice + j]);
     Box ab;
     ab.cx = double(pk.ag_x[slice + j]);
     ab.cy = double(pk.ag_y[slice + j]);
     ab.hl = double(pk.ag_len[size_t(sc) * A + j]) * 0.5;
     ab.hw = double(pk.ag_wid[size_t(sc) * A + j]) * 0.5;
-    const double2 hs = sincos2(h);
-    ab.s = hs.x;
-    ab.c = hs.y;
+    const double2 cs = pk.ag_cs[slice + j];  // host libm cos / sin of the heading, as the reference
+    ab.c = cs.x;
+    ab.s = cs.y;
     double X[4], Y[4];
     box_corners(ab, X, Y);
 #pragma unroll

@@ -94,6 +94,7 @@ struct DevPack {
     const uint8_t* ag_valid;
     const float* ag_len;
     const float* ag_wid;
+    const double2* ag_cs;  // [S][T][A] (cos, sin) of the logged heading, host libm as the reference (geometry.cpp:8)
     // road / route points
     // point sets in spatial (Morton) order, 32-point chunks with bounding boxes;
     // *_oi is each point's index in the reference order (the tie-break key)
