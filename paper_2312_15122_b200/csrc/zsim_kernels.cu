@@ -455,6 +455,7 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
         // certain and no exact evaluation is needed for it.
         const float2 hwb = make_float2(li.hw_min, li.hw_max);
         unsigned cin = 0;  // octet-uniform bit q: corner q certainly inside this lane's corridor
+        unsigned cunc = 0;  // bit q: corner q needs the exact argmin in this lane
         float thr[NQU];
 #pragma unroll
         for (int q = 0; q < NQU; ++q) {
@@ -467,7 +468,10 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
                 const bool in = dm + delta < hwb.x;
                 const bool out = dm - delta > hwb.y;
                 cin |= in ? 1u << q : 0u;
-                if (in || out) thr[q] = -1.f;
+                if (in || out)
+                    thr[q] = -1.f;
+                else
+                    cunc |= 1u << q;
             }
         }
         if (l0 == 0) ROW_MARK(b, 12);
@@ -509,8 +513,11 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
         if (l0 == 0) ROW_MARK(b, 13);
         // ---- per-octet exact argmin, then s / signed d / half-width per (query, route lane) ----
         int hi_ = INT_MAX;
+        // corners whose corridor verdict is certain in every route lane need no argmin
+        const unsigned open_q = __reduce_or_sync(FULL, cunc);
 #pragma unroll
         for (int q = 0; q < NQU; ++q) {
+            if (q > 0 && !((open_q >> q) & 1u)) continue;
             seg8_argmin(bd[q], bi[q]);
             const int v = __shfl_sync(FULL, bi[q], hk * 8);
             if (hq == q) hi_ = v;
