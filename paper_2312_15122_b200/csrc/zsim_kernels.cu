@@ -548,18 +548,29 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
 #pragma unroll
         for (int q = 0; q < NQU; ++q)
             if ((okb >> (4 * q)) & 15u) in_bits |= 1u << q;
-        // query 0: across route lanes min |d| then lane_id (lanes 0..3 hold route lanes l0..l0+3)
-        for (int k = 0; k < 4 && l0 + k < nl; ++k) {
-            const double s0 = __shfl_sync(FULL, hs, k), d0 = __shfl_sync(FULL, hd, k);
-            const int w0 = __shfl_sync(FULL, hi_, k);
-            if (w0 == INT_MAX) continue;
-            const uint32_t id = __shfl_sync(FULL, li.id, k * 8);
-            if (!have || fabs(d0) < best_abs || (fabs(d0) == best_abs && id < best_id)) {
-                have = true;
-                best_abs = fabs(d0);
-                best_s = s0;
-                best_d = d0;
-                best_id = id;
+        // query 0: across route lanes min |d| then lane_id (lanes 0..3 hold route
+        // lanes l0..l0+3): REDUX argmin on (|d| bits, lane_id), |d| >= 0
+        {
+            const uint32_t my_id = __shfl_sync(FULL, li.id, (lane & 3) * 8);
+            const bool cand = lane < 4 && l0 + lane < nl && hi_ != INT_MAX;
+            const double key = cand ? fabs(hd) : INFINITY;
+            const unsigned khi = unsigned(__double2hiint(key)), klo = unsigned(__double2loint(key));
+            const unsigned mhi = __reduce_min_sync(FULL, khi);
+            const unsigned mlo = __reduce_min_sync(FULL, khi == mhi ? klo : 0xffffffffu);
+            const bool eq = cand && khi == mhi && klo == mlo;
+            const unsigned mid = __reduce_min_sync(FULL, eq ? my_id : 0xffffffffu);
+            const unsigned wl = __ballot_sync(FULL, eq && my_id == mid);
+            if (wl) {
+                const int src = __ffs(wl) - 1;
+                const double babs = __hiloint2double(int(mhi), int(mlo));
+                const double s0 = __shfl_sync(FULL, hs, src), d0 = __shfl_sync(FULL, hd, src);
+                if (!have || babs < best_abs || (babs == best_abs && mid < best_id)) {
+                    have = true;
+                    best_abs = babs;
+                    best_s = s0;
+                    best_d = d0;
+                    best_id = mid;
+                }
             }
         }
     }
