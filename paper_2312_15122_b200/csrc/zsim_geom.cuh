@@ -25,7 +25,9 @@ constexpr double kPi = 3.14159265358979323846;
 
 // common.hpp:53-59
 ZS_HD double wrap_angle(double a) {
-    a = fmod(a, kTwoPi);
+    // fmod(a, 2pi) is a itself when |a| < 2pi (exact, sign kept): skip the
+    // general remainder loop in that (usual) case
+    if (!(fabs(a) < kTwoPi)) a = fmod(a, kTwoPi);
     if (a <= -kPi) a += kTwoPi;
     if (a > kPi) a -= kTwoPi;
     return a;
