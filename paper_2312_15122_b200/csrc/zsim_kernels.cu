@@ -55,7 +55,7 @@ __device__ unsigned long long g_pstats[32];
     } while (0)
 // per-row SM clock stamps (low 32 bits) at marks 0..7; the host differences them
 constexpr int kMaxStatRows = 65536;
-__device__ unsigned g_rowcyc[kMaxStatRows][16];
+__device__ unsigned g_rowcyc[kMaxStatRows][24];
 __device__ __forceinline__ void row_mark(int b, int k) {
     __syncwarp();
     if ((threadIdx.x & 31) == 0 && b < kMaxStatRows) g_rowcyc[b][k] = unsigned(clock64());
@@ -605,6 +605,29 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size
     return boxes_overlap(eb, EX, EY, ab, X, Y) ? 1 : 0;
 }
 
+// Agent boxes at one slice + overlap flags into w.agx/agy/agf for a row
+// (-1 = invalid / skipped / t past the log); returns whether any overlaps.
+// (Inlined: a __noinline__ call forces the WarpBuf into local memory.)
+__device__ __forceinline__ bool agent_boxes(const DevPack& pk, int sc, size_t slice, int na, int skip, bool t_ok, const Box& eb,
+                                             const double* EX, const double* EY, const WarpBuf& w) {
+    bool hit = false;
+    for (int j = lane_id(); j < na; j += 32) {
+        int f = -1;
+        if (t_ok && j != skip && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
+        w.agf[j] = f;
+        hit |= f == 1;
+    }
+    return hit;
+}
+
+// geometry.cpp:77-88 in full over the 16 edge pairs (contact case, rare).
+__device__ __forceinline__ double contact_dist2(const double* GX, const double* GY, const double* AX, const double* AY) {
+    double d2min = INFINITY;
+#pragma unroll 1
+    for (int pr = 0; pr < 16; ++pr) d2min = fmin(d2min, box_edge_pair_dist2(GX, GY, AX, AY, pr >> 2, pr & 3));
+    return d2min;
+}
+
 // Upper bound on |fp32 key - fp64 key| for points within sqrt(T)+1 of the
 // query; `ep` is the fp32 rounding error of the query coordinates.
 __device__ __forceinline__ double key_margin(double T, double ep) {
@@ -1106,18 +1129,14 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         }
     }
 
+    ROW_MARK(b, 16);
     // ---- other agents: obb_distance, sorted by (dist, idx) (simcore.cpp:457-486) ----
     const int A = pk.d.A;
     const int na = pk.n_agents[sc];
     const bool t_ok = t < pk.num_steps[sc];
     const size_t aslice = (size_t(sc) * pk.d.T + (t_ok ? t : 0)) * A;
     if (!boxes_ready) {
-        const Box eb = rs.eb;
-        for (int j = lane; j < na; j += 32) {
-            int f = -1;
-            if (t_ok && j != skip && pk.ag_valid[aslice + j]) f = agent_box_overlap(pk, sc, aslice, j, eb, rs.ex, rs.ey, w);
-            w.agf[j] = f;
-        }
+        agent_boxes(pk, sc, aslice, na, skip, t_ok, rs.eb, rs.ex, rs.ey, w);
         __syncwarp();
     }
     // obb_distance (geometry.cpp:77-88), ONE AGENT PER LANE.  Overlap => 0.
@@ -1165,28 +1184,32 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
             auto consider = [&](int p, float d2) {
                 if (d2 < min2) {
                     min2 = d2;
-                    const float m = sqrtf(d2);
+                    float m;  // sqrt.approx (rel. error < 2^-22), scaled up to an upper bound
+                    asm("sqrt.approx.f32 %0, %1;" : "=f"(m) : "f"(d2));
+                    m *= 1.f + 0x1p-20f;
                     const float r = m + 2.f * (c0 + 0x1p-18f * m) + 1e-30f;
                     thr2 = r * r * (1.f + 0x1p-20f);
                 }
                 if (d2 <= thr2) cmask |= 1u << p;
             };
-            // ego corner ci vs agent edge ei: pairs 4 ci + ei
+            // pairs base + 4 ci + ei: corner ci of (qx, qy) vs edge ei of (px, py).
+            // The edge loop stays rolled (code size: the fused kernel is far
+            // larger than the instruction cache); the edge's polygon rotates
+            // through registers so every index stays static.
+            auto side = [&](float (&px)[4], float (&py)[4], const float (&qx)[4], const float (&qy)[4], int base) {
+#pragma unroll 1
+                for (int ei = 0; ei < 4; ++ei) {
+                    const float4 f = make_float4(px[0], py[0], px[1] - px[0], py[1] - py[0]);
+                    const float inv = seg_inv_f(f);
 #pragma unroll
-            for (int ei = 0; ei < 4; ++ei) {
-                const float4 f = make_float4(axf[ei], ayf[ei], axf[(ei + 1) & 3] - axf[ei], ayf[(ei + 1) & 3] - ayf[ei]);
-                const float inv = seg_inv_f(f);
-#pragma unroll
-                for (int ci = 0; ci < 4; ++ci) consider(4 * ci + ei, seg_d2_f(gxf[ci], gyf[ci], f, inv));
-            }
-            // agent corner ci vs ego edge ei: pairs 16 + 4 ci + ei
-#pragma unroll
-            for (int ei = 0; ei < 4; ++ei) {
-                const float4 f = make_float4(gxf[ei], gyf[ei], gxf[(ei + 1) & 3] - gxf[ei], gyf[(ei + 1) & 3] - gyf[ei]);
-                const float inv = seg_inv_f(f);
-#pragma unroll
-                for (int ci = 0; ci < 4; ++ci) consider(16 + 4 * ci + ei, seg_d2_f(axf[ci], ayf[ci], f, inv));
-            }
+                    for (int ci = 0; ci < 4; ++ci) consider(base + 4 * ci + ei, seg_d2_f(qx[ci], qy[ci], f, inv));
+                    const float tx = px[0], ty = py[0];
+                    px[0] = px[1], py[0] = py[1], px[1] = px[2], py[1] = py[2], px[2] = px[3], py[2] = py[3];
+                    px[3] = tx, py[3] = ty;
+                }
+            };
+            side(axf, ayf, gxf, gyf, 0);
+            side(gxf, gyf, axf, ayf, 16);
             // exact candidates
             double d2min = INFINITY;
             while (cmask) {
@@ -1199,8 +1222,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
             }
             if (!(d2min >= 1e-18)) {
                 PSTAT(20, 1);
-                d2min = INFINITY;
-                for (int pr = 0; pr < 16; ++pr) d2min = fmin(d2min, box_edge_pair_dist2(GX, GY, AX, AY, pr >> 2, pr & 3));
+                d2min = contact_dist2(GX, GY, AX, AY);
             }
             w.agd[j] = sqrt(d2min);  // obb_distance returns sqrt of the min d2
         } else if (fl == 1) {
@@ -1209,6 +1231,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         nvalid += __popc(__ballot_sync(FULL, fl >= 0));
     }
     __syncwarp();
+    ROW_MARK(b, 17);
     // order by (distance, index) among the valid agents: bitonic sorts across
     // the warp on (distance bits, index) -- distances are >= +0 so their bit
     // patterns order like the values; invalid = +inf, last.  More than 32
@@ -1263,6 +1286,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
             }
         }
     }
+    ROW_MARK(b, 18);
     const int nsel_ag = min(Ka, nvalid);
     __syncwarp();
     for (int k = lane; k < Ka; k += 32) {
@@ -1498,14 +1522,7 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const int t1 = rs.r.t;
         const bool t_ok = t1 < pk.num_steps[sc];
         const size_t slice = (size_t(sc) * pk.d.T + (t_ok ? t1 : 0)) * pk.d.A;
-        const Box eb = rs.eb;
-        for (int j = lane; j < na; j += 32) {
-            int f = -1;
-            if (t_ok && j != skip && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, sc, slice, j, eb, rs.ex, rs.ey, w);
-            w.agf[j] = f;
-            hit |= f == 1;
-        }
-        hit = __any_sync(FULL, hit);
+        hit = __any_sync(FULL, agent_boxes(pk, sc, slice, na, skip, t_ok, rs.eb, rs.ex, rs.ey, w));
     }
 
     const double ps0 = rs.r0.proj_s, v0 = rs.r0.v, vn = rs.r.v;
@@ -1819,7 +1836,7 @@ extern "C" __attribute__((visibility("default"))) int zsimdbg_pathstats(unsigned
     if (cudaDeviceSynchronize() != cudaSuccess) return 1;
     if (cudaMemcpyFromSymbol(out, g_pstats, sizeof(g_pstats)) != cudaSuccess) return 1;
     if (rowcyc && nrows > 0 &&
-        cudaMemcpyFromSymbol(rowcyc, g_rowcyc, sizeof(unsigned) * 16 * size_t(nrows < kMaxStatRows ? nrows : kMaxStatRows)) !=
+        cudaMemcpyFromSymbol(rowcyc, g_rowcyc, sizeof(unsigned) * 24 * size_t(nrows < kMaxStatRows ? nrows : kMaxStatRows)) !=
             cudaSuccess)
         return 1;
     if (reset) {

@@ -49,7 +49,7 @@ def main():
         fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int, C.c_void_p, C.c_int]
         fn.restype = C.c_int
     res = {"B": B, "ms": [], "stats": [], "phases": {}}
-    cyc = np.zeros((B, 16), dtype=np.uint32)
+    cyc = np.zeros((B, 24), dtype=np.uint32)
     PH = ["project", "collide+flags", "active+agents", "road_topk", "road_feat", "route_topk", "route_feat"]
     gc.disable()
     for ep in range(int(next((a[5:] for a in sys.argv if a.startswith("--eps")), "2"))):  # episode 0 warms up
@@ -89,6 +89,9 @@ def main():
                         "project_split_slowest_1pct": dict(zip(["load+flags", "bicycle+queries", "groups", "pass1",
                                                                 "pass2", "exact", "argmin", "lane_hit", "rest"],
                                                                sub[slow].mean(0).round(0).tolist())),
+                        "agents_split": dict(zip(["active", "distances", "order", "features"],
+                                                 (np.diff(cyc[:, [2, 16, 17, 18, 3]].astype(np.int64), axis=1)
+                                                  % (1 << 32)).mean(0).round(0).tolist())),
                         "slowest_row": int(np.argmax(tot)), "slowest_row_phases": dict(zip(PH, d[np.argmax(tot)].tolist())),
                     }
             if ep >= 1:
