@@ -180,7 +180,7 @@ def load_library(path: Path | str = LIB_PATH) -> C.CDLL:
     path = Path(path)
     if not path.exists():
         raise ImportError(
-            f"native library {path} is missing; build it with `python -m paper_2312_15122_b200.build` "
+            f"native library {path} is missing; build it with `python paper_2312_15122_b200/build.py` "
             "(there is no CPU fallback on the product path)")
     lib = C.CDLL(str(path))
     for name, (res, args) in SIGNATURES.items():
