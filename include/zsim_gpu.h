@@ -386,6 +386,51 @@ ZSIM_API int zsim_step_host(zsim_env* env, const zsim_state_view* in_host, const
 /* Env::observe with host vectors. */
 ZSIM_API int zsim_observe_host(zsim_env* env, const zsim_state_view* in_host, const zsim_obs_view* obs_host);
 
+
+/* ---- on-device policy inference ------------------
+ * NNPolicy::act (train/policy.hpp:27-58) over forward_row
+ * (nn/model.hpp:464-585): the perceiver-style encoder (self attention over
+ * the 17 latent tokens, cross attention to road / route / active tokens),
+ * the policy and value trunks and heads, then argmax or sampling per row.
+ * Parameters are the reference's flat Model<float>::params in ParamIndex
+ * order (nn/model.hpp:101-167; matrices column-major as Eigen maps them). */
+
+/* ModelConfig (nn/model.hpp:20-27) with its ObsSpec. */
+typedef struct zsim_model_config {
+    int32_t latent;       /* 128 */
+    int32_t heads;        /* 2 */
+    int32_t trunk_blocks; /* 2 */
+    int32_t value_embed;  /* 32 */
+    int32_t n_agents;     /* ObsSpec: 16 */
+    int32_t n_road;       /* 128 */
+    int32_t n_route;      /* 64 */
+    int32_t n_accel;      /* 7 */
+    int32_t n_steer;      /* 5 */
+    int32_t reserved;
+} zsim_model_config;
+
+typedef struct zsim_policy zsim_policy;
+
+/* ModelConfig{} defaults. */
+ZSIM_API int zsim_model_config_defaults(zsim_model_config* cfg);
+/* Model::param_count (nn/model.hpp:181); ZSIM_CONFIG for configurations the
+ * device kernels are not built for (ModelConfig::validate, model.hpp:29-36). */
+ZSIM_API int zsim_policy_param_count(const zsim_model_config* cfg, int64_t* out);
+/* Model::init(seed) (nn/model.hpp:199-212) on the host, bit-exact. */
+ZSIM_API int zsim_policy_init_params(const zsim_model_config* cfg, uint64_t seed, float* out, int64_t n);
+/* PolicySnapshot -> device weights (train/policy.hpp:12-15, 21-22). */
+ZSIM_API int zsim_policy_create(const zsim_model_config* cfg, const float* params, int64_t n, int32_t device,
+                                zsim_policy** out);
+ZSIM_API int zsim_policy_destroy(zsim_policy* policy);
+/* NNPolicy::act (train/policy.hpp:27-58) on device buffers: obs rows [0, batch)
+ * of a device observation view; rng [batch] is the per-row stream
+ * (SimStateBatch::rng), advanced in place when sampling (unused for argmax).
+ * Outputs accel / steer / logp / value [batch]; logits (nullable)
+ * [batch][n_accel + n_steer].  Stream-ordered. */
+ZSIM_API int zsim_policy_act(zsim_policy* policy, const zsim_obs_view* obs, int32_t batch, uint64_t* rng,
+                             int32_t use_argmax, int32_t* accel, int32_t* steer, float* logp, float* value,
+                             float* logits, void* stream);
+
 /* ---- synthetic stress scenarios ---- */
 
 typedef struct zsim_stress_config {

@@ -10,8 +10,9 @@ from .env import (AGGREGATE_FIELDS, DONE_REASONS, BatchStream, DeviceEpisode, De
                   Env, ObservationBatch, aggregate_finalize,
                   STRESS_C2, SimConfig, SimStateBatch, StepOut, StressConfig, controlled_expand, event_bit,
                   random_actions, stress_scenarios)
+from .policy import ModelConfig, NNPolicy, init_params  # noqa: F401
 
 __all__ = ["Env", "SimConfig", "SimStateBatch", "StepOut", "ObservationBatch", "DeviceState", "DeviceStepOut",
            "DeviceObs", "StressConfig", "stress_scenarios", "random_actions", "ZsimError", "DONE_REASONS",
            "event_bit", "lib", "controlled_expand", "STRESS_C2", "DeviceEpisode", "aggregate_finalize",
-           "AGGREGATE_FIELDS", "BatchStream"]
+           "AGGREGATE_FIELDS", "BatchStream", "ModelConfig", "NNPolicy", "init_params"]

@@ -51,6 +51,11 @@ class ObsView(C.Structure):
                 ("value_only", c_float_p)]
 
 
+class ModelConfigC(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("latent", "heads", "trunk_blocks", "value_embed", "n_agents", "n_road",
+                                          "n_route", "n_accel", "n_steer", "reserved")]
+
+
 class EnvInfo(C.Structure):
     _fields_ = [
         ("batch", C.c_int32), ("horizon", C.c_int32), ("dt", C.c_double), ("total_stop_lines", C.c_int32),
@@ -162,6 +167,12 @@ SIGNATURES = {
     "zsim_stress_generate": (C.c_int, [C.POINTER(StressConfigC), C.c_uint64, C.POINTER(_P),
                                        C.POINTER(C.c_size_t)]),
     "zsim_free_buffer": (None, [_P]),
+    "zsim_model_config_defaults": (C.c_int, [C.POINTER(ModelConfigC)]),
+    "zsim_policy_param_count": (C.c_int, [C.POINTER(ModelConfigC), C.POINTER(C.c_int64)]),
+    "zsim_policy_init_params": (C.c_int, [C.POINTER(ModelConfigC), C.c_uint64, c_float_p, C.c_int64]),
+    "zsim_policy_create": (C.c_int, [C.POINTER(ModelConfigC), c_float_p, C.c_int64, C.c_int32, C.POINTER(_P)]),
+    "zsim_policy_destroy": (C.c_int, [_P]),
+    "zsim_policy_act": (C.c_int, [_P, C.POINTER(ObsView), C.c_int32, _P, C.c_int32, _P, _P, _P, _P, _P, _P]),
 }
 
 

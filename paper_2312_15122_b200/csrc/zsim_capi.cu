@@ -919,6 +919,10 @@ ZSIM_API int zsim_abi_version(void) { return ZSIM_ABI_VERSION; }
 
 ZSIM_API const char* zsim_last_error(void) { return g_last_error.c_str(); }
 
+// the other C-ABI translation unit (zsim_policy.cu) reports through the same
+// slot (C linkage inside this block; hidden like everything not ZSIM_API)
+void zsim_internal_set_last_error(const char* m) { g_last_error = m; }
+
 ZSIM_API int zsim_sim_config_defaults(zsim_sim_config* c) {
     return guarded([&] {
         if (!c) raise(Err::invalid_argument, "null config");

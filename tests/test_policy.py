@@ -1,0 +1,164 @@
+"""On-device policy inference: NNPolicy::act over
+forward_row (train/policy.hpp:27-58, nn/model.hpp:464-585) against the float64
+numpy restatement in oracle/policy_oracle.py.
+
+Tolerances (the reference computes in float32 with Eigen's summation order;
+the device in float32 with folded cross-attention weights): logits and value
+within 2e-4 absolute + 1e-3 relative of the float64 oracle; log-probs within
+5e-4.  Sampled / argmax indices must be identical wherever the oracle's
+decision margin exceeds 1e-3 (a closer call may legitimately flip under
+float32 rounding on either side); rng streams advance bit-exactly."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import policy_oracle as po
+
+LOGIT_ATOL, LOGIT_RTOL, LOGP_ATOL, MARGIN = 2e-4, 1e-3, 5e-4, 1e-3
+
+
+def test_init_params_bit_exact_vs_oracle():
+    import paper_2312_15122_b200 as z
+    for seed in (0, 7):
+        a = z.init_params(z.ModelConfig(), seed)
+        b = po.init_params(po.ModelConfig(), seed)
+        assert a.dtype == np.float32 and a.size == b.size == 425837
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_param_layout_matches_reference_order():
+    ix = po.param_index(po.ModelConfig())
+    names = [e.name for e in ix.entries]
+    assert names[:4] == ["emb.agents.w", "emb.agents.b", "emb.road.w", "emb.road.b"]
+    assert names[-2:] == ["value.head.w", "value.head.b"]
+    assert ix.by_name["enc.self.wq"].rows == 128 and ix.by_name["value.in.w"].cols == 160
+
+
+def test_config_errors():
+    import paper_2312_15122_b200 as z
+    with pytest.raises(z.ZsimError) as e:
+        z.ModelConfig(latent=96, heads=5).param_count()
+    assert e.value.kind == "config"
+    with pytest.raises(z.ZsimError) as e:
+        z.ModelConfig(latent=64).param_count()
+    assert e.value.kind == "config"
+    with pytest.raises(z.ZsimError) as e:
+        z.ModelConfig(trunk_blocks=0).param_count()
+    assert e.value.kind == "config"
+
+
+def random_obs(B, rng):
+    """Observation rows with the value ranges the simulator produces, plus
+    all-zero (done) rows and partially masked token sets."""
+    obs = {
+        "active": rng.normal(0, 3, (B, 9)).astype(np.float32),
+        "agents": rng.normal(0, 20, (B, 16, 6)).astype(np.float32),
+        "road": rng.normal(0, 30, (B, 128, 12)).astype(np.float32),
+        "route": rng.normal(0, 30, (B, 64, 5)).astype(np.float32),
+        "value_only": np.abs(rng.normal(0, 50, (B, 2))).astype(np.float32),
+    }
+    obs["agents"][..., 5] = rng.random((B, 16)) < 0.7
+    obs["road"][..., 2:11] = rng.random((B, 128, 9)) < 0.3
+    obs["road"][..., 11] = rng.random((B, 128)) < 0.8
+    obs["route"][..., 2:4] = rng.random((B, 64, 2)) < 0.5
+    obs["route"][..., 4] = rng.random((B, 64)) < 0.9
+    for k in obs:
+        obs[k][1] = 0.0  # a done row
+    obs["agents"][2, :, 5] = 0.0  # no valid agents: only the null latent token
+    obs["road"][3, :, 11] = 0.0  # no valid road tokens
+    return obs
+
+
+def run_device(pol, obs, rng_state, B):
+    import torch
+    from paper_2312_15122_b200._abi import ObsView
+    dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in obs.items()}
+    view = ObsView()
+    for k, t in dev.items():
+        setattr(view, k, C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_float)))
+    rng = torch.from_numpy(rng_state.view(np.int64).copy()).cuda()
+    accel = torch.zeros(B, dtype=torch.int32, device="cuda")
+    steer = torch.zeros_like(accel)
+    logp = torch.zeros(B, dtype=torch.float32, device="cuda")
+    value = torch.zeros_like(logp)
+    na, ns = pol.cfg.n_accel, pol.cfg.n_steer
+    logits = torch.zeros(B, na + ns, dtype=torch.float32, device="cuda")
+    pol.act_device(view, B, rng.data_ptr(), accel.data_ptr(), steer.data_ptr(), logp.data_ptr(), value.data_ptr(),
+                   logits.data_ptr())
+    torch.cuda.synchronize()
+    return dict(accel=accel.cpu().numpy(), steer=steer.cpu().numpy(), logp=logp.cpu().numpy(),
+                value=value.cpu().numpy(), rng=rng.cpu().numpy().view(np.uint64),
+                logits=logits.cpu().numpy())
+
+
+def margins_ok(logits, u, use_argmax):
+    """Decision margin of the oracle: top-2 logit gap (argmax) or the distance
+    of u to the nearest CDF boundary (sampling)."""
+    if use_argmax:
+        s = np.sort(logits)
+        return s[-1] - s[-2] > MARGIN
+    p = np.exp(po.log_softmax(logits))
+    return np.min(np.abs(np.cumsum(p) - u)) > MARGIN
+
+
+def check_against_oracle(cfg_o, params, obs, B, use_argmax, seed=3):
+    import paper_2312_15122_b200 as z
+    rng0 = np.array([(0x1234567 * (b + 1) + seed) & ((1 << 64) - 1) for b in range(B)], np.uint64)
+    pol = z.NNPolicy(z.ModelConfig(), params, use_argmax=use_argmax)
+    got = run_device(pol, obs, rng0, B)
+    ref = po.act(po.Model(cfg_o, params), obs, rng0, use_argmax)
+    na = cfg_o.n_accel
+    np.testing.assert_allclose(got["logits"][:, :na], ref["logits_accel"], atol=LOGIT_ATOL, rtol=LOGIT_RTOL)
+    np.testing.assert_allclose(got["logits"][:, na:], ref["logits_steer"], atol=LOGIT_ATOL, rtol=LOGIT_RTOL)
+    np.testing.assert_allclose(got["value"], ref["value"], atol=LOGIT_ATOL, rtol=LOGIT_RTOL)
+    checked = 0
+    for b in range(B):
+        if margins_ok(ref["logits_accel"][b], ref["u"][b][0], use_argmax) and \
+                margins_ok(ref["logits_steer"][b], ref["u"][b][1], use_argmax):
+            assert got["accel"][b] == ref["accel"][b] and got["steer"][b] == ref["steer"][b], b
+            assert abs(got["logp"][b] - ref["logp"][b]) < LOGP_ATOL, b
+            checked += 1
+    assert checked >= B * 3 // 4
+    if not use_argmax:
+        assert np.array_equal(got["rng"], ref["rng"])  # two draws per row
+    return got, ref
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("use_argmax", [True, False])
+def test_policy_act_random_obs(use_argmax):
+    cfg_o = po.ModelConfig()
+    params = po.init_params(cfg_o, 11)
+    obs = random_obs(10, np.random.default_rng(5))  # 10 rows: the last CTA is partial
+    check_against_oracle(cfg_o, params, obs, 10, use_argmax)
+
+
+@pytest.mark.gpu
+def test_policy_act_on_simulator_observations():
+    import torch
+
+    import paper_2312_15122_b200 as z
+    zsim = z.stress_scenarios(z.StressConfig(count=8, agents=20, road_points=900), seed=3)
+    env = z.Env(zsim, config=z.SimConfig(disable_dones=False), device=0)
+    st, nxt, so, ob = env.device_state(), env.device_state(), env.device_stepout(), env.device_obs()
+    env.reset_device(4, st)
+    A, S = z.random_actions(5, 8, seed=9)
+    for t in range(5):
+        a, s = torch.from_numpy(A[t]).cuda(), torch.from_numpy(S[t]).cuda()
+        env.step_observe_device(st, a.data_ptr(), s.data_ptr(), nxt, so, ob)
+        st, nxt = nxt, st
+    torch.cuda.synchronize()
+    h = env.download_obs(ob)
+    obs = {k: getattr(h, k).copy() for k in ("active", "agents", "road", "route", "value_only")}
+    cfg_o = po.ModelConfig()
+    check_against_oracle(cfg_o, po.init_params(cfg_o, 2), obs, 8, False)
+
+
+@pytest.mark.gpu
+def test_policy_errors():
+    import paper_2312_15122_b200 as z
+    p = po.init_params(po.ModelConfig(), 1)
+    with pytest.raises(z.ZsimError) as e:
+        z.NNPolicy(z.ModelConfig(), p[:-1])
+    assert e.value.kind == "invalid_argument"
