@@ -422,6 +422,11 @@ ZSIM_API int zsim_policy_init_params(const zsim_model_config* cfg, uint64_t seed
 ZSIM_API int zsim_policy_create(const zsim_model_config* cfg, const float* params, int64_t n, int32_t device,
                                 zsim_policy** out);
 ZSIM_API int zsim_policy_destroy(zsim_policy* policy);
+/* Arithmetic of the ten 128x128 token-tile projections: 0 (default) =
+ * tcgen05 tensor cores, tf32 operands, fp32 accumulation; 1 = fp32 CUDA
+ * cores (the reference's Model<float> arithmetic).  Everything else is fp32
+ * in both modes. */
+ZSIM_API int zsim_policy_set_precision(zsim_policy* policy, int32_t mode);
 /* NNPolicy::act (train/policy.hpp:27-58) on device buffers: obs rows [0, batch)
  * of a device observation view; rng [batch] is the per-row stream
  * (SimStateBatch::rng), advanced in place when sampling (unused for argmax).

@@ -172,6 +172,7 @@ SIGNATURES = {
     "zsim_policy_init_params": (C.c_int, [C.POINTER(ModelConfigC), C.c_uint64, c_float_p, C.c_int64]),
     "zsim_policy_create": (C.c_int, [C.POINTER(ModelConfigC), c_float_p, C.c_int64, C.c_int32, C.POINTER(_P)]),
     "zsim_policy_destroy": (C.c_int, [_P]),
+    "zsim_policy_set_precision": (C.c_int, [_P, C.c_int32]),
     "zsim_policy_act": (C.c_int, [_P, C.POINTER(ObsView), C.c_int32, _P, C.c_int32, _P, _P, _P, _P, _P, _P]),
 }
 

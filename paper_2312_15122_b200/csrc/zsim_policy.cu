@@ -2,22 +2,32 @@
 // (train/policy.hpp:27-58) over forward_row (nn/model.hpp:464-585) for a whole
 // observation batch, plus Model::init (nn/model.hpp:199-212) on the host.
 //
-// Execution model: one CTA (256 threads) per group of kRows observation rows.
-// A row's 17 latent tokens (learned null + 16 agent slots) live in shared
-// memory as rows of a [kTok][128] token tile for the whole forward pass; the
-// key/value token sets (road 129, route 65, active 2) are never materialised:
+// Execution model: one CTA (256 threads) per group of observation rows.  The
+// rows' latent tokens (learned null + 16 agent slots each, 17 per row) form a
+// token tile that stays on chip for the whole forward pass.  The key/value
+// token sets (road 129, route 65, active 2 per row) are never materialised:
 // a cross-attention block's keys and values are affine in the row's raw
 // features (kv = W_emb f + b_emb is not normalised, model.hpp:326-336), so
 // the host folds W_k W_emb and W_v W_emb once and each query works in the
 // feature space (12 / 5 / 9 dims) instead of the 128-dim latent space:
 //   score_j = q . (Kf f_j + ck) = (Kf^T q) . f_j + q . ck
 //   out     = Vf (sum_j p_j f_j) + (sum_j p_j) cv + p_null v_null
-// The 128x128 projections over the token tile (Q/K/V/O of the four attention
-// blocks) are the dense contractions.
+// The 128x128 projections over the token tile (Q/K/V/O of the self block,
+// Q/O of the three cross blocks) are the dense contractions:
 //
-// Numerics: fp32 as the reference (Model<float>); the folding and the
-// summation order differ from Eigen's, so results match to fp32 rounding
-// (tests/test_policy.py states the tolerance against the float64 oracle).
+//  * k_policy_tc (default): 7 rows = 119 tokens in a 128-row tile; the
+//    residual stream X and the projection accumulators live in TMEM
+//    (lane = token); each projection is 16 tcgen05.mma.kind::tf32
+//    (M=128, N=128, K=8) from shared-memory operands in the canonical
+//    K-major layout, weights streamed in by bulk-async copies (prearranged
+//    and rounded to tf32 on the host).  Attention, LayerNorm and epilogues run
+//    one thread per (token, column half / head) straight off TMEM.
+//  * k_policy_fp32: 3 rows per CTA, every contraction on the FP32 pipe
+//    (exact fp32 arithmetic like the reference's Model<float>).
+//
+// Numerics: fp32 accumulation everywhere; the tensor-core path rounds the
+// projection inputs to tf32 (10-bit mantissa).  tests/test_policy.py states
+// the tolerance of each path against the float64 oracle.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -38,11 +48,14 @@ constexpr int kHeads = 2, kDh = 64;     // heads, head width
 constexpr int kAgents = 16, kRoad = 128, kRoute = 64;  // ObsSpec (simcore.hpp:60-63)
 constexpr int kAgF = 6, kRoadF = 12, kRouteF = 5, kActF = 9, kValF = 2;
 constexpr int kLat = kAgents + 1;       // latent tokens per row
-constexpr int kRows = 3;                // observation rows per CTA
-constexpr int kTok = 64;                // token tile (kRows * kLat = 51, padded)
-constexpr int kLd = kD + 4;             // smem row stride of a token tile (floats)
 constexpr int kThreads = 256;
 constexpr int kMaxTrunk = 4, kMaxHead = 16, kMaxVE = 64;
+constexpr int kRows32 = 3;              // rows per CTA, fp32 kernel (51 tokens in a 64-row tile)
+constexpr int kTok32 = 64;
+constexpr int kLd = kD + 4;             // smem row stride of the fp32 kernel's token tiles
+constexpr int kRowsTc = 7;              // rows per CTA, tensor-core kernel (119 tokens in a 128-row tile)
+constexpr int kTokTc = 128;
+constexpr int kNumProj = 10;            // projection weights in the tensor-core layout
 
 // fixed input normalisation (model.hpp:56-63)
 __constant__ float c_act_scale[kActF] = {0.1f, 1.8f, 0.02f, 1.f, 1.f, 1.f, 1.f, 0.02f, 0.1f};
@@ -68,6 +81,9 @@ struct PolicyW {
     MlpW pblk[kMaxTrunk], vblk[kMaxTrunk];
     const float *acc_w, *acc_b, *str_w, *str_b;
     const float *vemb_w, *vemb_b, *vin_w, *vin_b, *vhead_w, *vhead_b;
+    // tensor-core copies of the projections, [N=128][K=128] canonical K-major
+    // tf32 tiles of 64 KB: self q k v o, road q o, route q o, active q o
+    const float* tc[kNumProj];
     int trunk, ve, n_accel, n_steer;
 };
 
@@ -84,28 +100,6 @@ struct ActArgs {
     float* logits;  // optional [B][n_accel + n_steer]
 };
 
-struct Smem {
-    float X[kTok][kLd];   // residual token stream
-    float A[kTok][kLd];   // LayerNorm output, then attention output (concat)
-    float Q[kTok][kLd];
-    float K[kTok][kLd];
-    float V[kTok][kLd];
-    float road[kRows][kRoad][kRoadF];
-    float route[kRows][kRoute][kRouteF];
-    float act[kRows][kActF];
-    float val[kRows][kValF];
-    unsigned char mroad[kRows][kRoad];
-    unsigned char mroute[kRows][kRoute];
-    unsigned char mlat[kRows][kLat];
-    unsigned char mact[kRows][1];  // the active token is always valid
-    float vec[kRows][2][kD + kMaxVE];  // trunk vectors (policy / value), ping-pong
-    float tmp[kRows][kD];
-    float pooled[kRows][kD];
-    float lnv[kRows][kD];
-    float logit[kRows][2 * kMaxHead];
-    float vout[kRows];
-};
-
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -119,181 +113,79 @@ __device__ __forceinline__ float warp_max(float v) {
 
 __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752440f)); }
 
-// ln_forward (model.hpp:287-303) of every token row of X into A: one warp per token.
-__device__ void ln_tokens(const float (*X)[kLd], float (*A)[kLd], const float* g, const float* b) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int s = warp; s < kTok; s += kThreads / 32) {
-        float v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = X[s][lane + 32 * k];
-        const float mu = warp_sum(v[0] + v[1] + v[2] + v[3]) / float(kD);
-        float q = 0.f;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) q += (v[k] - mu) * (v[k] - mu);
-        const float var = warp_sum(q) / float(kD);
-        const float rstd = 1.f / sqrtf(var + 1e-5f);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int c = lane + 32 * k;
-            A[s][c] = (v[k] - mu) * rstd * g[c] + b[c];
-        }
+// ---------------------------------------------------------------------------
+// Per-row inputs and the post-encoder trunk, shared by both kernels.
+// ---------------------------------------------------------------------------
+template <int R>
+struct RowSm {
+    float road[R][kRoad][kRoadF];  // scaled features (model.hpp:470-503)
+    float route[R][kRoute][kRouteF];
+    float act[R][kActF];
+    float val[R][kValF];
+    unsigned char mroad[R][kRoad];
+    unsigned char mroute[R][kRoute];
+    unsigned char mlat[R][kLat];
+    unsigned char mact[R][1];  // the active token is always valid
+    float vec[R][2][kD + kMaxVE];  // trunk vectors, ping-pong
+    float tmp[R][kD];
+    float pooled[R][kD];
+    float lnv[R][kD];
+    float logit[R][2 * kMaxHead];
+    float vout[R];
+};
+
+template <int R>
+__device__ void load_row_inputs(RowSm<R>& sm, const ActArgs& a, int b0) {
+    const int tid = threadIdx.x;
+    for (int e = tid; e < R * kRoad * kRoadF; e += kThreads) {
+        const int g = e / (kRoad * kRoadF), r = e % (kRoad * kRoadF);
+        const int b = b0 + g;
+        const float v = b < a.B ? a.obs.road[size_t(b) * kRoad * kRoadF + r] : 0.f;
+        sm.road[g][r / kRoadF][r % kRoadF] = v * c_rd_scale[r % kRoadF];
+        if (r % kRoadF == kRoadF - 1) sm.mroad[g][r / kRoadF] = v > 0.5f;
+    }
+    for (int e = tid; e < R * kRoute * kRouteF; e += kThreads) {
+        const int g = e / (kRoute * kRouteF), r = e % (kRoute * kRouteF);
+        const int b = b0 + g;
+        const float v = b < a.B ? a.obs.route[size_t(b) * kRoute * kRouteF + r] : 0.f;
+        sm.route[g][r / kRouteF][r % kRouteF] = v * c_rt_scale[r % kRouteF];
+        if (r % kRouteF == kRouteF - 1) sm.mroute[g][r / kRouteF] = v > 0.5f;
+    }
+    if (tid < R * kActF) {
+        const int g = tid / kActF, f = tid % kActF, b = b0 + g;
+        sm.act[g][f] = (b < a.B ? a.obs.active[size_t(b) * kActF + f] : 0.f) * c_act_scale[f];
+    }
+    if (tid < R) sm.mact[tid][0] = 1;
+    if (tid < R * kValF) {
+        const int g = tid / kValF, f = tid % kValF, b = b0 + g;
+        sm.val[g][f] = (b < a.B ? a.obs.value_only[size_t(b) * kValF + f] : 0.f) * c_val_scale[f];
+    }
+    // latent mask: learned null always, agent slot when its valid feature > 0.5 (model.hpp:505-509)
+    for (int e = tid; e < R * kLat; e += kThreads) {
+        const int g = e / kLat, i = e % kLat, b = b0 + g;
+        sm.mlat[g][i] = i == 0 ? 1 : (b < a.B ? a.obs.agents[(size_t(b) * kAgents + (i - 1)) * kAgF + 5] : 0.f) > 0.5f;
     }
 }
 
-// out[s][n] = sum_k A[s][k] W(n, k) + bias[n] (+ res[s][n]) over the token
-// tile; W column-major [k][n].  Thread: 4 tokens x 8 outputs.
-__device__ void gemm_tile(const float (*A)[kLd], const float* __restrict__ W, const float* __restrict__ bias,
-                          float (*out)[kLd], bool residual) {
-    const int t = threadIdx.x;
-    const int s0 = (t >> 4) * 4, n0 = (t & 15) * 8;
-    float acc[4][8];
+// latent token embedding (model.hpp:510-513): column c of token slot i of row b
+__device__ __forceinline__ float embed_latent(const PolicyW& W, const ActArgs& a, int b, int i, int c) {
+    if (i == 0) return W.null_ag[c];
+    if (b >= a.B) return W.emb_ag_b[c];
+    const float* ag = a.obs.agents + (size_t(b) * kAgents + (i - 1)) * kAgF;
+    float acc = 0.f;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-#pragma unroll 2
-    for (int k = 0; k < kD; k += 4) {
-        float4 a[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(&A[s0 + i][k]);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            const float4 w0 = __ldg(reinterpret_cast<const float4*>(W + (k + kk) * kD + n0));
-            const float4 w1 = __ldg(reinterpret_cast<const float4*>(W + (k + kk) * kD + n0 + 4));
-            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av, wv[j], acc[i][j]);
-            }
-        }
-    }
-    // each output element is read (residual) and written by its owner only
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            float v = acc[i][j] + bias[n0 + j];
-            if (residual) v += out[s0 + i][n0 + j];
-            out[s0 + i][n0 + j] = v;
-        }
+    for (int f = 0; f < kAgF; ++f) acc = fmaf(W.emb_ag_w[f * kD + c], ag[f] * c_ag_scale[f], acc);
+    return acc + W.emb_ag_b[c];
 }
 
-// Self attention of each row's 17 latent tokens (model.hpp:340-364), heads
-// concatenated into A.  One warp per (row, head, query); lane j < 17 = key j.
-__device__ void self_attention(Smem& sm) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const float scale = 0.125f;  // 1 / sqrt(64)
-    for (int task = warp; task < kRows * kHeads * kLat; task += kThreads / 32) {
-        const int g = task / (kHeads * kLat), h = (task / kLat) % kHeads, i = task % kLat;
-        const int qs = g * kLat + i;
-        float s = -INFINITY;
-        const bool valid = lane < kLat && sm.mlat[g][lane];
-        if (lane < kLat) {
-            const float* q = &sm.Q[qs][h * kDh];
-            const float* k = &sm.K[g * kLat + lane][h * kDh];
-            float d = 0.f;
-#pragma unroll 16
-            for (int c = 0; c < kDh; ++c) d = fmaf(q[c], k[c], d);
-            s = d * scale;
-        }
-        const float mx = warp_max(valid ? s : -INFINITY);
-        const float e = valid ? expf(s - mx) : 0.f;
-        const float p = e / warp_sum(e);
-        // out[c] = sum_j p_j V[j][c]; lane owns c = lane, lane + 32
-        float o0 = 0.f, o1 = 0.f;
-        for (int j = 0; j < kLat; ++j) {
-            const float pj = __shfl_sync(0xffffffffu, p, j);
-            o0 = fmaf(pj, sm.V[g * kLat + j][h * kDh + lane], o0);
-            o1 = fmaf(pj, sm.V[g * kLat + j][h * kDh + lane + 32], o1);
-        }
-        sm.A[qs][h * kDh + lane] = o0;
-        sm.A[qs][h * kDh + lane + 32] = o1;
-    }
-}
-
-// Cross attention against a row's feature tokens (null + n tokens of F raw
-// scaled features; attn_forward with self_mode false, model.hpp:326-367),
-// through the folded weights.  One warp per (row, head, query).
-template <int F, int N>
-__device__ void cross_attention(Smem& sm, const AttnW& w, const float (*feat)[N][F], const unsigned char (*mask)[N]) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const float scale = 0.125f;
-    for (int task = warp; task < kRows * kHeads * kLat; task += kThreads / 32) {
-        const int g = task / (kHeads * kLat), h = (task / kLat) % kHeads, i = task % kLat;
-        const int qs = g * kLat + i;
-        const int c0 = h * kDh + lane, c1 = c0 + 32;
-        const float q0 = sm.Q[qs][c0], q1 = sm.Q[qs][c1];
-        // qf = Kf_h^T q, qn = q . ck_h, null score = q . k_null_h
-        float qf[F];
-#pragma unroll
-        for (int f = 0; f < F; ++f) qf[f] = warp_sum(fmaf(w.kf[f * kD + c0], q0, w.kf[f * kD + c1] * q1));
-        const float qn = warp_sum(fmaf(w.ck[c0], q0, w.ck[c1] * q1));
-        const float sn = warp_sum(fmaf(w.kn[c0], q0, w.kn[c1] * q1)) * scale;
-        // feature-token scores, lane owns tokens lane + 32 m
-        constexpr int M = (N + 31) / 32;
-        float s[M];
-        float mx = sn;
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-            const int j = lane + 32 * m;
-            s[m] = -INFINITY;
-            if (j < N && mask[g][j]) {
-                float d = qn;
-#pragma unroll
-                for (int f = 0; f < F; ++f) d = fmaf(qf[f], feat[g][j][f], d);
-                s[m] = d * scale;
-            }
-            mx = fmaxf(mx, s[m]);
-        }
-        mx = warp_max(mx);
-        float esum = 0.f;
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-            s[m] = s[m] == -INFINITY ? 0.f : expf(s[m] - mx);
-            esum += s[m];
-        }
-        const float en = expf(sn - mx);
-        const float tot = warp_sum(esum) + en;
-        const float inv = 1.f / tot;
-        // aggregated features sum_j p_j f_j and sum_j p_j
-        float ag[F];
-#pragma unroll
-        for (int f = 0; f < F; ++f) ag[f] = 0.f;
-        float ps = 0.f;
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-            const int j = lane + 32 * m;
-            if (j < N && s[m] != 0.f) {
-                const float p = s[m] / tot;
-                ps += p;
-#pragma unroll
-                for (int f = 0; f < F; ++f) ag[f] = fmaf(p, feat[g][j][f], ag[f]);
-            }
-        }
-#pragma unroll
-        for (int f = 0; f < F; ++f) ag[f] = warp_sum(ag[f]);
-        ps = warp_sum(ps);
-        const float pn = en * inv;
-        float o0 = fmaf(ps, w.cv[c0], pn * w.vn[c0]), o1 = fmaf(ps, w.cv[c1], pn * w.vn[c1]);
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-            o0 = fmaf(w.vf[f * kD + c0], ag[f], o0);
-            o1 = fmaf(w.vf[f * kD + c1], ag[f], o1);
-        }
-        sm.A[qs][c0] = o0;
-        sm.A[qs][c1] = o1;
-    }
-}
-
-// mlp_forward (model.hpp:431-440) of vec[.][src] into vec[.][dst].
-__device__ __forceinline__ void mlp_rows(Smem& sm, const MlpW& w, int src, int dst) {
+// mlp_forward (model.hpp:431-440) of vec[.][src] into vec[.][dst] for every row.
+template <int R>
+__device__ void mlp_rows(RowSm<R>& sm, const MlpW& w, int src, int dst) {
     __syncthreads();
     {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        if (warp < kRows) {
-            const float* xv = sm.vec[warp][src];
+        for (int g = warp; g < R; g += kThreads / 32) {
+            const float* xv = sm.vec[g][src];
             float v[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) v[k] = xv[lane + 32 * k];
@@ -305,19 +197,19 @@ __device__ __forceinline__ void mlp_rows(Smem& sm, const MlpW& w, int src, int d
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int c = lane + 32 * k;
-                sm.lnv[warp][c] = (v[k] - mu) * rstd * w.ln_g[c] + w.ln_b[c];
+                sm.lnv[g][c] = (v[k] - mu) * rstd * w.ln_g[c] + w.ln_b[c];
             }
         }
     }
     __syncthreads();
-    for (int task = threadIdx.x; task < kRows * kD; task += kThreads) {
+    for (int task = threadIdx.x; task < R * kD; task += kThreads) {
         const int g = task / kD, n = task % kD;
         float acc = 0.f;
         for (int k = 0; k < kD; ++k) acc = fmaf(__ldg(w.w1 + k * kD + n), sm.lnv[g][k], acc);
         sm.tmp[g][n] = gelu(acc + w.b1[n]);
     }
     __syncthreads();
-    for (int task = threadIdx.x; task < kRows * kD; task += kThreads) {
+    for (int task = threadIdx.x; task < R * kD; task += kThreads) {
         const int g = task / kD, n = task % kD;
         float acc = 0.f;
         for (int k = 0; k < kD; ++k) acc = fmaf(__ldg(w.w2 + k * kD + n), sm.tmp[g][k], acc);
@@ -365,117 +257,24 @@ __device__ int argmax_first(const float* z, int n) {
     return best;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_policy_act(const ActArgs a) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    Smem& sm = *reinterpret_cast<Smem*>(dsm);
+// From the pooled encodings (sm.pooled): policy trunk and heads, value trunk
+// (model.hpp:556-584), then NNPolicy::act's selection (policy.hpp:33-56).
+template <int R>
+__device__ void trunk_and_act(RowSm<R>& sm, const ActArgs& a, int b0) {
     const PolicyW& W = a.w;
     const int tid = threadIdx.x;
-    const int b0 = blockIdx.x * kRows;
-
-    // ---- raw features of the CTA's rows, scaled (forward_row, model.hpp:470-503) ----
-    for (int e = tid; e < kRows * kRoad * kRoadF; e += kThreads) {
-        const int g = e / (kRoad * kRoadF), r = e % (kRoad * kRoadF);
-        const int b = b0 + g;
-        const float v = b < a.B ? a.obs.road[size_t(b) * kRoad * kRoadF + r] : 0.f;
-        sm.road[g][r / kRoadF][r % kRoadF] = v * c_rd_scale[r % kRoadF];
-        if (r % kRoadF == kRoadF - 1) sm.mroad[g][r / kRoadF] = v > 0.5f;
-    }
-    for (int e = tid; e < kRows * kRoute * kRouteF; e += kThreads) {
-        const int g = e / (kRoute * kRouteF), r = e % (kRoute * kRouteF);
-        const int b = b0 + g;
-        const float v = b < a.B ? a.obs.route[size_t(b) * kRoute * kRouteF + r] : 0.f;
-        sm.route[g][r / kRouteF][r % kRouteF] = v * c_rt_scale[r % kRouteF];
-        if (r % kRouteF == kRouteF - 1) sm.mroute[g][r / kRouteF] = v > 0.5f;
-    }
-    if (tid < kRows * kActF) {
-        const int g = tid / kActF, f = tid % kActF, b = b0 + g;
-        sm.act[g][f] = (b < a.B ? a.obs.active[size_t(b) * kActF + f] : 0.f) * c_act_scale[f];
-    }
-    if (tid < kRows) sm.mact[tid][0] = 1;
-    if (tid < kRows * kValF) {
-        const int g = tid / kValF, f = tid % kValF, b = b0 + g;
-        sm.val[g][f] = (b < a.B ? a.obs.value_only[size_t(b) * kValF + f] : 0.f) * c_val_scale[f];
-    }
-    // latent tokens: null + agent embeddings (model.hpp:505-513); padding tokens 0
-    for (int e = tid; e < kTok * kD; e += kThreads) {
-        const int s = e / kD, c = e % kD;
-        const int g = s / kLat, i = s % kLat, b = b0 + g;
-        float v = 0.f;
-        if (g < kRows) {
-            if (i == 0) {
-                v = W.null_ag[c];
-            } else {
-                const float* ag = a.obs.agents + (size_t(b) * kAgents + (i - 1)) * kAgF;
-                float acc = 0.f;
-#pragma unroll
-                for (int f = 0; f < kAgF; ++f) {
-                    const float x = b < a.B ? ag[f] * c_ag_scale[f] : 0.f;
-                    acc = fmaf(W.emb_ag_w[f * kD + c], x, acc);
-                }
-                v = acc + W.emb_ag_b[c];
-                if (c == 0) sm.mlat[g][i] = (b < a.B ? ag[5] : 0.f) > 0.5f;
-            }
-            if (i == 0 && c == 0) sm.mlat[g][0] = 1;
-        }
-        sm.X[s][c] = v;
-    }
     __syncthreads();
-
-    // ---- encoder (model.hpp:530-543) ----
-    ln_tokens(sm.X, sm.A, W.self.ln_g, W.self.ln_b);
-    __syncthreads();
-    gemm_tile(sm.A, W.self.wq, W.self.bq, sm.Q, false);
-    gemm_tile(sm.A, W.self.wk, W.self.bk, sm.K, false);
-    gemm_tile(sm.A, W.self.wv, W.self.bv, sm.V, false);
-    __syncthreads();
-    self_attention(sm);
-    __syncthreads();
-    gemm_tile(sm.A, W.self.wo, W.self.bo, sm.X, true);
-    __syncthreads();
-
-    // (explicit blocks: indexing the kernel-parameter struct dynamically would
-    // copy it to local memory)
-    auto cross_block = [&](const AttnW& aw, int m) {
-        ln_tokens(sm.X, sm.A, aw.ln_g, aw.ln_b);
-        __syncthreads();
-        gemm_tile(sm.A, aw.wq, aw.bq, sm.Q, false);
-        __syncthreads();
-        if (m == 0) cross_attention<kRoadF, kRoad>(sm, aw, sm.road, sm.mroad);
-        if (m == 1) cross_attention<kRouteF, kRoute>(sm, aw, sm.route, sm.mroute);
-        // the active token set is one always-valid token per row
-        if (m == 2) cross_attention<kActF, 1>(sm, aw, reinterpret_cast<const float(*)[1][kActF]>(sm.act), sm.mact);
-        __syncthreads();
-        gemm_tile(sm.A, aw.wo, aw.bo, sm.X, true);
-        __syncthreads();
-    };
-    cross_block(W.road, 0);
-    cross_block(W.route, 1);
-    cross_block(W.active, 2);
-
-    // ---- mean pool over valid latent tokens (model.hpp:545-554) ----
-    for (int e = tid; e < kRows * kD; e += kThreads) {
-        const int g = e / kD, c = e % kD;
-        float acc = 0.f;
-        int n = 0;
-        for (int i = 0; i < kLat; ++i)
-            if (sm.mlat[g][i]) {
-                acc += sm.X[g * kLat + i][c];
-                ++n;
-            }
-        sm.vec[g][0][c] = acc / float(n);
-        sm.pooled[g][c] = acc / float(n);  // kept for the value trunk
-    }
-    // ---- policy trunk + heads (model.hpp:556-568) ----
+    for (int e = tid; e < R * kD; e += kThreads) sm.vec[e / kD][0][e % kD] = sm.pooled[e / kD][e % kD];
     int cur = 0;
 #pragma unroll
     for (int i = 0; i < kMaxTrunk; ++i)
         if (i < W.trunk) {
-            mlp_rows(sm, W.pblk[i], cur, cur ^ 1);
+            mlp_rows<R>(sm, W.pblk[i], cur, cur ^ 1);
             cur ^= 1;
         }
     __syncthreads();
     const int na = W.n_accel, ns = W.n_steer;
-    for (int e = tid; e < kRows * (na + ns); e += kThreads) {
+    for (int e = tid; e < R * (na + ns); e += kThreads) {
         const int g = e / (na + ns), n = e % (na + ns);
         const bool isa = n < na;
         const float* Wm = isa ? W.acc_w : W.str_w;
@@ -485,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_act(const ActArgs a) {
         sm.logit[g][n] = acc + (isa ? W.acc_b[o] : W.str_b[o]);
     }
     __syncthreads();
-    // ---- value trunk (model.hpp:570-584): concat [pooled; gelu(W_e v + b_e)] ----
-    for (int e = tid; e < kRows * (kD + W.ve); e += kThreads) {
+    // value trunk: concat [pooled; gelu(W_e v + b_e)] -> value.in -> blocks -> head
+    for (int e = tid; e < R * (kD + W.ve); e += kThreads) {
         const int g = e / (kD + W.ve), c = e % (kD + W.ve);
         float v;
         if (c < kD) {
@@ -501,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_act(const ActArgs a) {
         sm.vec[g][0][c] = v;
     }
     __syncthreads();
-    for (int e = tid; e < kRows * kD; e += kThreads) {
+    for (int e = tid; e < R * kD; e += kThreads) {
         const int g = e / kD, n = e % kD;
         float acc = 0.f;
         for (int k = 0; k < kD + W.ve; ++k) acc = fmaf(__ldg(W.vin_w + size_t(k) * kD + n), sm.vec[g][0][k], acc);
@@ -511,23 +310,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_act(const ActArgs a) {
 #pragma unroll
     for (int i = 0; i < kMaxTrunk; ++i)
         if (i < W.trunk) {
-            mlp_rows(sm, W.vblk[i], cur, cur ^ 1);
+            mlp_rows<R>(sm, W.vblk[i], cur, cur ^ 1);
             cur ^= 1;
         }
     __syncthreads();
     {
         const int lane = tid & 31, warp = tid >> 5;
-        if (warp < kRows) {
+        for (int g = warp; g < R; g += kThreads / 32) {
             float acc = 0.f;
-            for (int k = lane; k < kD; k += 32) acc = fmaf(W.vhead_w[k], sm.vec[warp][cur][k], acc);
+            for (int k = lane; k < kD; k += 32) acc = fmaf(W.vhead_w[k], sm.vec[g][cur][k], acc);
             acc = warp_sum(acc);
-            if (lane == 0) sm.vout[warp] = acc + W.vhead_b[0];
+            if (lane == 0) sm.vout[g] = acc + W.vhead_b[0];
         }
     }
     __syncthreads();
-
-    // ---- NNPolicy::act (policy.hpp:33-56): one thread per row ----
-    if (tid < kRows && b0 + tid < a.B) {
+    if (tid < R && b0 + tid < a.B) {
         const int g = tid, b = b0 + tid;
         float la[kMaxHead], ls[kMaxHead];
         for (int i = 0; i < na; ++i) la[i] = sm.logit[g][i];
@@ -559,6 +356,596 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_act(const ActArgs a) {
         a.logp[b] = lp;
     }
 }
+
+// Folded cross attention of ONE query (one head) against a row's feature
+// tokens (null + N tokens of F scaled features, model.hpp:326-367): q is the
+// head's 64 query values, out receives the head's 64 output values.
+template <int F, int N>
+__device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* q, const float (*feat)[F],
+                                            const unsigned char* mask, float* out) {
+    const float scale = 0.125f;  // 1 / sqrt(64)
+    const float* kf = w.kf + h * kDh;
+    float qf[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+        float acc = 0.f;
+#pragma unroll 16
+        for (int c = 0; c < kDh; ++c) acc = fmaf(__ldg(kf + f * kD + c), q[c], acc);
+        qf[f] = acc;
+    }
+    float qn = 0.f, sn = 0.f;
+#pragma unroll 16
+    for (int c = 0; c < kDh; ++c) {
+        qn = fmaf(__ldg(w.ck + h * kDh + c), q[c], qn);
+        sn = fmaf(__ldg(w.kn + h * kDh + c), q[c], sn);
+    }
+    sn *= scale;
+    float mx = sn;
+    for (int j = 0; j < N; ++j) {
+        if (!mask[j]) continue;
+        float d = qn;
+#pragma unroll
+        for (int f = 0; f < F; ++f) d = fmaf(qf[f], feat[j][f], d);
+        mx = fmaxf(mx, d * scale);
+    }
+    const float en = expf(sn - mx);
+    float tot = en, ps = 0.f;
+    float ag[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) ag[f] = 0.f;
+    for (int j = 0; j < N; ++j) {
+        if (!mask[j]) continue;
+        float d = qn;
+#pragma unroll
+        for (int f = 0; f < F; ++f) d = fmaf(qf[f], feat[j][f], d);
+        const float e = expf(d * scale - mx);
+        tot += e;
+        ps += e;
+#pragma unroll
+        for (int f = 0; f < F; ++f) ag[f] = fmaf(e, feat[j][f], ag[f]);
+    }
+    const float inv = 1.f / tot;
+    ps *= inv;
+    const float pn = en * inv;
+#pragma unroll
+    for (int f = 0; f < F; ++f) ag[f] *= inv;
+    const float* vf = w.vf + h * kDh;
+#pragma unroll 8
+    for (int c = 0; c < kDh; ++c) {
+        float o = fmaf(ps, __ldg(w.cv + h * kDh + c), pn * __ldg(w.vn + h * kDh + c));
+#pragma unroll
+        for (int f = 0; f < F; ++f) o = fmaf(__ldg(vf + f * kD + c), ag[f], o);
+        out[c] = o;
+    }
+}
+
+// ===========================================================================
+// k_policy_fp32: every contraction on the FP32 pipe, 3 rows per CTA.
+// ===========================================================================
+struct Smem32 {
+    float X[kTok32][kLd];  // residual token stream
+    float A[kTok32][kLd];  // LayerNorm output, then attention output
+    float Q[kTok32][kLd];
+    float K[kTok32][kLd];
+    float V[kTok32][kLd];
+    RowSm<kRows32> rs;
+};
+
+// ln_forward (model.hpp:287-303) of every token row of X into A: one warp per token.
+__device__ void ln_tokens32(const float (*X)[kLd], float (*A)[kLd], const float* g, const float* b) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = warp; s < kTok32; s += kThreads / 32) {
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = X[s][lane + 32 * k];
+        const float mu = warp_sum(v[0] + v[1] + v[2] + v[3]) / float(kD);
+        float q = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q += (v[k] - mu) * (v[k] - mu);
+        const float rstd = 1.f / sqrtf(warp_sum(q) / float(kD) + 1e-5f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int c = lane + 32 * k;
+            A[s][c] = (v[k] - mu) * rstd * g[c] + b[c];
+        }
+    }
+}
+
+// out[s][n] = sum_k A[s][k] W(n, k) + bias[n] (+ out[s][n]) over the token
+// tile; W column-major [k][n].  Thread: 4 tokens x 8 outputs.
+__device__ void gemm32(const float (*A)[kLd], const float* __restrict__ W, const float* __restrict__ bias,
+                       float (*out)[kLd], bool residual) {
+    const int t = threadIdx.x;
+    const int s0 = (t >> 4) * 4, n0 = (t & 15) * 8;
+    float acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+    for (int k = 0; k < kD; k += 4) {
+        float4 a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(&A[s0 + i][k]);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const float4 w0 = __ldg(reinterpret_cast<const float4*>(W + (k + kk) * kD + n0));
+            const float4 w1 = __ldg(reinterpret_cast<const float4*>(W + (k + kk) * kD + n0 + 4));
+            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av, wv[j], acc[i][j]);
+            }
+        }
+    }
+    // each output element is read (residual) and written by its owner only
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float v = acc[i][j] + bias[n0 + j];
+            if (residual) v += out[s0 + i][n0 + j];
+            out[s0 + i][n0 + j] = v;
+        }
+}
+
+// Self attention (model.hpp:340-364) of each row's 17 latent tokens, one
+// thread per (token, head): keys / values of the row from smem.
+template <class KV>
+__device__ __forceinline__ void self_query(int h, const float* q, const unsigned char* mlat, KV kv, float* out) {
+    const float scale = 0.125f;
+    float s[kLat];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kLat; ++j) {
+        float d = 0.f;
+#pragma unroll 16
+        for (int c = 0; c < kDh; ++c) d = fmaf(q[c], kv.k(j, h * kDh + c), d);
+        s[j] = d * scale;
+        if (mlat[j]) mx = fmaxf(mx, s[j]);
+    }
+    float tot = 0.f;
+#pragma unroll
+    for (int j = 0; j < kLat; ++j) {
+        s[j] = mlat[j] ? expf(s[j] - mx) : 0.f;
+        tot += s[j];
+    }
+    const float inv = 1.f / tot;
+#pragma unroll 8
+    for (int c = 0; c < kDh; ++c) {
+        float o = 0.f;
+#pragma unroll
+        for (int j = 0; j < kLat; ++j) o = fmaf(s[j], kv.v(j, h * kDh + c), o);
+        out[c] = o * inv;
+    }
+}
+
+struct KV32 {
+    const float (*K)[kLd];
+    const float (*V)[kLd];
+    int base;
+    __device__ float k(int j, int c) const { return K[base + j][c]; }
+    __device__ float v(int j, int c) const { return V[base + j][c]; }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_policy_fp32(const ActArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    Smem32& sm = *reinterpret_cast<Smem32*>(dsm);
+    const PolicyW& W = a.w;
+    const int tid = threadIdx.x;
+    const int b0 = blockIdx.x * kRows32;
+    load_row_inputs<kRows32>(sm.rs, a, b0);
+    for (int e = tid; e < kTok32 * kD; e += kThreads) {
+        const int s = e / kD, c = e % kD, g = s / kLat;
+        sm.X[s][c] = g < kRows32 ? embed_latent(W, a, b0 + g, s % kLat, c) : 0.f;
+    }
+    __syncthreads();
+    // self attention block
+    ln_tokens32(sm.X, sm.A, W.self.ln_g, W.self.ln_b);
+    __syncthreads();
+    gemm32(sm.A, W.self.wq, W.self.bq, sm.Q, false);
+    gemm32(sm.A, W.self.wk, W.self.bk, sm.K, false);
+    gemm32(sm.A, W.self.wv, W.self.bv, sm.V, false);
+    __syncthreads();
+    if (tid < kRows32 * kLat * kHeads) {
+        const int s = tid >> 1, h = tid & 1, g = s / kLat;
+        self_query(h, &sm.Q[s][h * kDh], sm.rs.mlat[g], KV32{sm.K, sm.V, g * kLat}, &sm.A[s][h * kDh]);
+    }
+    __syncthreads();
+    gemm32(sm.A, W.self.wo, W.self.bo, sm.X, true);
+    __syncthreads();
+    // cross blocks (explicit: indexing the kernel-parameter struct dynamically
+    // would copy it to local memory)
+    auto cross_block = [&](const AttnW& aw, int m) {
+        ln_tokens32(sm.X, sm.A, aw.ln_g, aw.ln_b);
+        __syncthreads();
+        gemm32(sm.A, aw.wq, aw.bq, sm.Q, false);
+        __syncthreads();
+        if (tid < kRows32 * kLat * kHeads) {
+            const int s = tid >> 1, h = tid & 1, g = s / kLat;
+            if (m == 0) cross_query<kRoadF, kRoad>(aw, h, &sm.Q[s][h * kDh], sm.rs.road[g], sm.rs.mroad[g], &sm.A[s][h * kDh]);
+            if (m == 1) cross_query<kRouteF, kRoute>(aw, h, &sm.Q[s][h * kDh], sm.rs.route[g], sm.rs.mroute[g], &sm.A[s][h * kDh]);
+            if (m == 2) cross_query<kActF, 1>(aw, h, &sm.Q[s][h * kDh], reinterpret_cast<const float(*)[kActF]>(sm.rs.act[g]), sm.rs.mact[g], &sm.A[s][h * kDh]);
+        }
+        __syncthreads();
+        gemm32(sm.A, aw.wo, aw.bo, sm.X, true);
+        __syncthreads();
+    };
+    cross_block(W.road, 0);
+    cross_block(W.route, 1);
+    cross_block(W.active, 2);
+    // mean pool over valid latent tokens (model.hpp:545-554)
+    for (int e = tid; e < kRows32 * kD; e += kThreads) {
+        const int g = e / kD, c = e % kD;
+        float acc = 0.f;
+        int n = 0;
+        for (int i = 0; i < kLat; ++i)
+            if (sm.rs.mlat[g][i]) {
+                acc += sm.X[g * kLat + i][c];
+                ++n;
+            }
+        sm.rs.pooled[g][c] = acc / float(n);
+    }
+    trunk_and_act<kRows32>(sm.rs, a, b0);
+}
+
+// ===========================================================================
+// k_policy_tc: projections on the 5th-generation tensor cores (tcgen05).
+// ===========================================================================
+// TMEM columns (512 allocated, lane = token): X residual stream [0,128),
+// projection accumulators D0 [128,256), D1 [256,384), D2 [384,512).
+constexpr uint32_t kColX = 0, kColD0 = 128, kColD1 = 256, kColD2 = 384;
+
+struct SmemTc {
+    float opA[kTokTc * kD];  // A operand: 128 tokens x 128 K, canonical K-major tf32 (64 KB)
+    float opW[kD * kD];      // B operand: 128 outputs x 128 K, canonical K-major tf32 (64 KB)
+    RowSm<kRowsTc> rs;
+    float red[2][kTokTc];    // LayerNorm partial sums of the two column halves
+    float red2[2][kTokTc];
+    unsigned long long mbar_w, mbar_mma;
+    uint32_t tmem_base;
+};
+static_assert(offsetof(SmemTc, opW) == 65536, "operand tiles must be contiguous (K/V staging spans both)");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+// canonical no-swizzle K-major layout: core matrices of 8 rows x 16 B;
+// K-adjacent core matrices 2048 B apart (LBO), row-group-adjacent 128 B (SBO)
+__device__ __forceinline__ uint32_t canon_off(int row, int k) {  // in floats
+    return uint32_t(((k >> 2) * 16 + (row >> 3)) * 32 + (row & 7) * 4 + (k & 3));
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(2048 >> 4) << 16) | (uint64_t(128 >> 4) << 32) |
+           (1ull << 46);
+}
+
+// kind::tf32, D f32, A/B tf32 K-major, N = 128, M = 128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+    return u;
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* m, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(m)),
+        "r"(phase));
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 32 consecutive TMEM columns of this thread's lane (warp w reads lanes 32 (w % 4) ..)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+        "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+        "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+        "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+        "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+        "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+        "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+        "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31])));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+struct TcCtx {
+    SmemTc& sm;
+    uint32_t tmem;      // allocated base
+    uint32_t lane_base; // this warp's TMEM lane quarter << 16
+    int tok;            // this thread's token (TMEM lane)
+    int half;           // column half / head of this thread
+    uint32_t ph_w = 0, ph_mma = 0;
+
+    __device__ uint32_t col(uint32_t c) const { return tmem + lane_base + c; }
+
+    // 64 columns [c0 + 64 half, +64) of this thread's token
+    __device__ void ld64(uint32_t c0, float* v) const {
+        tmem_ld32(col(c0 + 64 * half), v);
+        tmem_ld32(col(c0 + 64 * half + 32), v + 32);
+    }
+    __device__ void st64(uint32_t c0, const float* v) const {
+        tmem_st32(col(c0 + 64 * half), v);
+        tmem_st32(col(c0 + 64 * half + 32), v + 32);
+    }
+
+    // stream a 64 KB weight tile into opW (one thread issues; async proxy)
+    __device__ void load_w(const float* src) {
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t mb = smem_u32(&sm.mbar_w);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(65536u) : "memory");
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(sm.opW) + 16384u * i),
+                    "l"(src + 4096 * i), "r"(16384u), "r"(mb)
+                    : "memory");
+            }
+        }
+    }
+    __device__ void wait_w() {
+        mbar_wait(&sm.mbar_w, ph_w);
+        ph_w ^= 1;
+    }
+
+    // D[dcol] = opA . opW^T (M = N = 128, K = 128): one thread issues 16 MMAs
+    // and commits to mbar_mma; every thread waits for the result.  The caller
+    // has made opA (generic stores + proxy fence) and opW (wait_w) visible.
+    __device__ void mma(uint32_t dcol) {
+        tc_fence_before();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sm.opA), w0 = smem_u32(sm.opW);
+#pragma unroll
+            for (int kk = 0; kk < kD / 8; ++kk) {
+                const uint64_t da = umma_desc(a0 + kk * 2 * 2048), dw = umma_desc(w0 + kk * 2 * 2048);
+                const uint32_t acc = kk > 0;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + dcol),
+                    "l"(da), "l"(dw), "r"(kIdesc), "r"(acc)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&sm.mbar_mma))
+                         : "memory");
+        }
+        mbar_wait(&sm.mbar_mma, ph_mma);
+        ph_mma ^= 1;
+        tc_fence_after();
+    }
+
+    // 64 values of this thread's token / column half into opA (tf32, canonical)
+    __device__ void put_a(const float* v) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int k = 64 * half + 4 * q;
+            uint4 u = make_uint4(to_tf32(v[4 * q]), to_tf32(v[4 * q + 1]), to_tf32(v[4 * q + 2]), to_tf32(v[4 * q + 3]));
+            *reinterpret_cast<uint4*>(sm.opA + canon_off(tok, k)) = u;
+        }
+    }
+
+    // LayerNorm of this thread's token from X (TMEM) into opA; the two column
+    // halves of a token combine their partial sums through smem.
+    __device__ void ln_to_a(const float* g, const float* b) {
+        float v[64];
+        ld64(kColX, v);
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) s += v[i];
+        sm.red[half][tok] = s;
+        __syncthreads();
+        const float mu = (sm.red[0][tok] + sm.red[1][tok]) / float(kD);
+        float q = 0.f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) q += (v[i] - mu) * (v[i] - mu);
+        sm.red2[half][tok] = q;
+        __syncthreads();
+        const float rstd = 1.f / sqrtf((sm.red2[0][tok] + sm.red2[1][tok]) / float(kD) + 1e-5f);
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            const int c = 64 * half + i;
+            v[i] = (v[i] - mu) * rstd * __ldg(g + c) + __ldg(b + c);
+        }
+        put_a(v);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+
+    // X += D[dcol] + bias (the block's residual output projection)
+    __device__ void residual_add(uint32_t dcol, const float* bias) {
+        float x[64], d[64];
+        ld64(kColX, x);
+        ld64(dcol, d);
+#pragma unroll
+        for (int i = 0; i < 64; ++i) x[i] += d[i] + __ldg(bias + 64 * half + i);
+        st64(kColX, x);
+    }
+};
+
+struct KVTc {  // self-attention K / V copies in smem: [128 tokens][128], float4 chunks XOR-swizzled by row
+    const float* K;
+    const float* V;
+    int base;
+    __device__ static int idx(int r, int c) { return r * kD + ((((c >> 2) ^ (r & 7)) << 2) | (c & 3)); }
+    __device__ float k(int j, int c) const { return K[idx(base + j, c)]; }
+    __device__ float v(int j, int c) const { return V[idx(base + j, c)]; }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    SmemTc& sm = *reinterpret_cast<SmemTc*>(dsm);
+    const PolicyW& W = a.w;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int b0 = blockIdx.x * kRowsTc;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        mbar_init(&sm.mbar_w, 1);
+        mbar_init(&sm.mbar_mma, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    TcCtx cx{sm, sm.tmem_base, uint32_t((warp & 3) * 32) << 16, (warp & 3) * 32 + (tid & 31), warp >> 2};
+    const int tok = cx.tok, half = cx.half;
+    const int g = tok / kLat, slot = tok % kLat;
+    const bool real = g < kRowsTc;
+
+    cx.load_w(W.tc[0]);  // self Wq streams in while the inputs are staged
+    load_row_inputs<kRowsTc>(sm.rs, a, b0);
+    {
+        float v[64];
+#pragma unroll 4
+        for (int i = 0; i < 64; ++i) v[i] = real ? embed_latent(W, a, b0 + g, slot, 64 * half + i) : 0.f;
+        cx.st64(kColX, v);
+    }
+    __syncthreads();
+
+    // ---- self attention block (model.hpp:326-367, self_mode) ----
+    cx.ln_to_a(W.self.ln_g, W.self.ln_b);
+    cx.wait_w();
+    cx.mma(kColD0);  // Q
+    cx.load_w(W.tc[1]);
+    cx.wait_w();
+    cx.mma(kColD1);  // K
+    cx.load_w(W.tc[2]);
+    cx.wait_w();
+    cx.mma(kColD2);  // V
+    {
+        // K, V (+ bias) to smem over both operand tiles (swizzled rows)
+        float v[64];
+        cx.ld64(kColD1, v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int c = 64 * half + 4 * q;
+            float4 f = make_float4(v[4 * q] + __ldg(W.self.bk + c), v[4 * q + 1] + __ldg(W.self.bk + c + 1),
+                                   v[4 * q + 2] + __ldg(W.self.bk + c + 2), v[4 * q + 3] + __ldg(W.self.bk + c + 3));
+            *reinterpret_cast<float4*>(sm.opA + KVTc::idx(tok, c)) = f;
+        }
+        cx.ld64(kColD2, v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int c = 64 * half + 4 * q;
+            float4 f = make_float4(v[4 * q] + __ldg(W.self.bv + c), v[4 * q + 1] + __ldg(W.self.bv + c + 1),
+                                   v[4 * q + 2] + __ldg(W.self.bv + c + 2), v[4 * q + 3] + __ldg(W.self.bv + c + 3));
+            *reinterpret_cast<float4*>(sm.opW + KVTc::idx(tok, c)) = f;
+        }
+    }
+    __syncthreads();
+    {
+        float q[64], o[64];
+        cx.ld64(kColD0, q);
+#pragma unroll
+        for (int i = 0; i < 64; ++i) q[i] += __ldg(W.self.bq + 64 * half + i);
+        if (real) {
+            self_query(half, q, sm.rs.mlat[g], KVTc{sm.opA, sm.opW, g * kLat}, o);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) o[i] = 0.f;
+        }
+        __syncthreads();  // K / V reads done: the operand tiles are free
+        cx.load_w(W.tc[3]);
+        cx.put_a(o);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    cx.wait_w();
+    cx.mma(kColD1);
+    cx.residual_add(kColD1, W.self.bo);
+
+    // ---- cross blocks: road, route, active (model.hpp:534-543) ----
+    auto cross_block = [&](const AttnW& aw, const float* wq_tc, const float* wo_tc, int m) {
+        cx.load_w(wq_tc);
+        cx.ln_to_a(aw.ln_g, aw.ln_b);
+        cx.wait_w();
+        cx.mma(kColD0);
+        cx.load_w(wo_tc);  // the output projection streams in during the attention
+        float q[64], o[64];
+        cx.ld64(kColD0, q);
+#pragma unroll
+        for (int i = 0; i < 64; ++i) q[i] += __ldg(aw.bq + 64 * half + i);
+        if (real) {
+            if (m == 0) cross_query<kRoadF, kRoad>(aw, half, q, sm.rs.road[g], sm.rs.mroad[g], o);
+            if (m == 1) cross_query<kRouteF, kRoute>(aw, half, q, sm.rs.route[g], sm.rs.mroute[g], o);
+            if (m == 2) cross_query<kActF, 1>(aw, half, q, reinterpret_cast<const float(*)[kActF]>(sm.rs.act[g]), sm.rs.mact[g], o);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) o[i] = 0.f;
+        }
+        cx.put_a(o);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        cx.wait_w();
+        cx.mma(kColD1);
+        cx.residual_add(kColD1, aw.bo);
+    };
+    cross_block(W.road, W.tc[4], W.tc[5], 0);
+    cross_block(W.route, W.tc[6], W.tc[7], 1);
+    cross_block(W.active, W.tc[8], W.tc[9], 2);
+
+    // ---- mean pool over valid latent tokens (model.hpp:545-554) ----
+    {
+        float x[64];
+        cx.ld64(kColX, x);
+        float* xs = sm.opA;  // [128][132] fp32 over both operand tiles
+#pragma unroll
+        for (int i = 0; i < 64; ++i) xs[tok * (kD + 4) + 64 * half + i] = x[i];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(sm.tmem_base));
+    for (int e = tid; e < kRowsTc * kD; e += kThreads) {
+        const int gg = e / kD, c = e % kD;
+        float acc = 0.f;
+        int n = 0;
+        for (int i = 0; i < kLat; ++i)
+            if (sm.rs.mlat[gg][i]) {
+                acc += sm.opA[(gg * kLat + i) * (kD + 4) + c];
+                ++n;
+            }
+        sm.rs.pooled[gg][c] = acc / float(n);
+    }
+    trunk_and_act<kRowsTc>(sm.rs, a, b0);
+}
+
+}  // namespace zp
+
+namespace zp {
 
 // ---------------------------------------------------------------------------
 // host: ParamIndex::build (model.hpp:101-167) and Model::init (:199-212)
@@ -649,7 +1036,7 @@ struct zsim_policy {
     int device = 0;
     float* blob = nullptr;  // device: reference params followed by the folded cross-attention weights
     zp::PolicyW w{};
-    size_t smem = 0;
+    int precision = 0;  // 0: tcgen05 tf32 projections, 1: fp32 CUDA cores
 };
 
 namespace {
@@ -783,11 +1170,34 @@ ZSIM_API int zsim_policy_create(const zsim_model_config* c, const float* params,
                 extra[size_t(fo.vn + o)] = float(vn);
             }
         }
+        // tensor-core tiles of the ten projections: W(n, k) at the canonical
+        // K-major no-swizzle position, rounded to tf32 (nearest, ties away)
+        const char* proj[zp::kNumProj] = {"enc.self.wq", "enc.self.wk", "enc.self.wv", "enc.self.wo",
+                                          "enc.cross.road.wq", "enc.cross.road.wo", "enc.cross.route.wq",
+                                          "enc.cross.route.wo", "enc.cross.active.wq", "enc.cross.active.wo"};
+        int64_t tc_off[zp::kNumProj];
+        extra.resize((extra.size() + 255) / 256 * 256);  // 1 KB alignment of the tiles
+        for (int i = 0; i < zp::kNumProj; ++i) {
+            const zp::Entry& e = find(proj[i]);
+            tc_off[i] = int64_t(extra.size());
+            extra.resize(extra.size() + size_t(d) * d);
+            float* t = extra.data() + tc_off[i];
+            for (int n2 = 0; n2 < d; ++n2)
+                for (int k = 0; k < d; ++k) {
+                    uint32_t u;
+                    const float v = params[e.off + int64_t(k) * d + n2];
+                    std::memcpy(&u, &v, 4);
+                    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+                    float r;
+                    std::memcpy(&r, &u, 4);
+                    t[((k >> 2) * 16 + (n2 >> 3)) * 32 + (n2 & 7) * 4 + (k & 3)] = r;
+                }
+        }
         std::unique_ptr<zsim_policy> pol(new zsim_policy());
         pol->cfg = *c;
         pol->device = device;
         ccheck(cudaSetDevice(device), "cudaSetDevice");
-        const size_t base = (size_t(total) + 63) / 64 * 64;
+        const size_t base = (size_t(total) + 255) / 256 * 256;
         ccheck(cudaMalloc(&pol->blob, (base + extra.size()) * sizeof(float)), "cudaMalloc(policy)");
         ccheck(cudaMemcpy(pol->blob, params, size_t(total) * sizeof(float), cudaMemcpyHostToDevice), "H2D(policy)");
         ccheck(cudaMemcpy(pol->blob + base, extra.data(), extra.size() * sizeof(float), cudaMemcpyHostToDevice),
@@ -848,10 +1258,22 @@ ZSIM_API int zsim_policy_create(const zsim_model_config* c, const float* params,
         w.ve = c->value_embed;
         w.n_accel = c->n_accel;
         w.n_steer = c->n_steer;
-        pol->smem = sizeof(zp::Smem);
-        ccheck(cudaFuncSetAttribute(zp::k_policy_act, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pol->smem)),
-               "cudaFuncSetAttribute(policy)");
+        for (int i = 0; i < zp::kNumProj; ++i) w.tc[i] = D + base + tc_off[i];
+        ccheck(cudaFuncSetAttribute(zp::k_policy_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(sizeof(zp::SmemTc))),
+               "cudaFuncSetAttribute(policy tc)");
+        ccheck(cudaFuncSetAttribute(zp::k_policy_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(sizeof(zp::Smem32))),
+               "cudaFuncSetAttribute(policy fp32)");
         *out = pol.release();
+    });
+}
+
+ZSIM_API int zsim_policy_set_precision(zsim_policy* p, int32_t mode) {
+    return pguarded([&] {
+        if (!p) zs::raise(zs::Err::invalid_argument, "policy_set_precision: null policy");
+        if (mode != 0 && mode != 1) zs::raise(zs::Err::invalid_argument, "policy_set_precision: mode must be 0 or 1");
+        p->precision = mode;
     });
 }
 
@@ -884,9 +1306,15 @@ ZSIM_API int zsim_policy_act(zsim_policy* p, const zsim_obs_view* obs, int32_t b
         a.logp = logp;
         a.value = value;
         a.logits = logits;
-        const int grid = (batch + zp::kRows - 1) / zp::kRows;
-        zp::k_policy_act<<<grid, zp::kThreads, p->smem, static_cast<cudaStream_t>(stream)>>>(a);
-        ccheck(cudaGetLastError(), "k_policy_act launch");
+        const cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (p->precision == 0) {
+            const int grid = (batch + zp::kRowsTc - 1) / zp::kRowsTc;
+            zp::k_policy_tc<<<grid, zp::kThreads, sizeof(zp::SmemTc), s>>>(a);
+        } else {
+            const int grid = (batch + zp::kRows32 - 1) / zp::kRows32;
+            zp::k_policy_fp32<<<grid, zp::kThreads, sizeof(zp::Smem32), s>>>(a);
+        }
+        ccheck(cudaGetLastError(), "policy kernel launch");
     });
 }
 

@@ -56,7 +56,10 @@ class NNPolicy:
     (use_argmax) or sample_categorical on each head with the row's rng
     stream, advanced in place.  All pointers are device addresses (ints)."""
 
-    def __init__(self, cfg: ModelConfig, params: np.ndarray, use_argmax: bool = False, device: int = 0):
+    PRECISIONS = {"tf32": 0, "fp32": 1}
+
+    def __init__(self, cfg: ModelConfig, params: np.ndarray, use_argmax: bool = False, device: int = 0,
+                 precision: str = "tf32"):
         self.cfg = cfg
         self.argmax = bool(use_argmax)
         p = np.ascontiguousarray(params, np.float32)
@@ -64,6 +67,8 @@ class NNPolicy:
         check(lib.zsim_policy_create(C.byref(cfg.to_c()), p.ctypes.data_as(C.POINTER(C.c_float)), p.size, device,
                                      C.byref(h)))
         self._h = h
+        self.precision = precision
+        check(lib.zsim_policy_set_precision(h, self.PRECISIONS[precision]))
 
     @property
     def handle(self) -> C.c_void_p:

@@ -2,12 +2,17 @@
 forward_row (train/policy.hpp:27-58, nn/model.hpp:464-585) against the float64
 numpy restatement in oracle/policy_oracle.py.
 
-Tolerances (the reference computes in float32 with Eigen's summation order;
-the device in float32 with folded cross-attention weights): logits and value
-within 2e-4 absolute + 1e-3 relative of the float64 oracle; log-probs within
-5e-4.  Sampled / argmax indices must be identical wherever the oracle's
-decision margin exceeds 1e-3 (a closer call may legitimately flip under
-float32 rounding on either side); rng streams advance bit-exactly."""
+Tolerances against the float64 oracle (the reference itself computes in
+float32 with Eigen's summation order, so it sits within the fp32 bound too):
+  precision "fp32" (every contraction on the FP32 pipe): logits / value within
+      1e-5 absolute + 1e-4 relative, log-probs within 2e-5 (measured: 4e-7);
+  precision "tf32" (the default: the ten 128x128 projections on tcgen05 with
+      tf32 operands, fp32 accumulation): logits / value within 1e-3 absolute +
+      5e-3 relative, log-probs within 2e-3 (measured: 1.8e-4).
+Sampled / argmax indices must be identical wherever the oracle's decision
+margin exceeds the path's margin (1e-4 fp32, 2e-3 tf32; a closer call may
+legitimately flip under rounding on either side); rng streams advance
+bit-exactly."""
 import ctypes as C
 
 import numpy as np
@@ -15,7 +20,8 @@ import pytest
 
 from oracle import policy_oracle as po
 
-LOGIT_ATOL, LOGIT_RTOL, LOGP_ATOL, MARGIN = 2e-4, 1e-3, 5e-4, 1e-3
+TOL = {"fp32": dict(atol=1e-5, rtol=1e-4, logp=2e-5, margin=1e-4),
+       "tf32": dict(atol=1e-3, rtol=5e-3, logp=2e-3, margin=2e-3)}
 
 
 def test_init_params_bit_exact_vs_oracle():
@@ -92,58 +98,65 @@ def run_device(pol, obs, rng_state, B):
                 logits=logits.cpu().numpy())
 
 
-def margins_ok(logits, u, use_argmax):
+def margins_ok(logits, u, use_argmax, margin):
     """Decision margin of the oracle: top-2 logit gap (argmax) or the distance
     of u to the nearest CDF boundary (sampling)."""
     if use_argmax:
         s = np.sort(logits)
-        return s[-1] - s[-2] > MARGIN
+        return s[-1] - s[-2] > margin
     p = np.exp(po.log_softmax(logits))
-    return np.min(np.abs(np.cumsum(p) - u)) > MARGIN
+    return np.min(np.abs(np.cumsum(p) - u)) > margin
 
 
-def check_against_oracle(cfg_o, params, obs, B, use_argmax, seed=3):
+def check_against_oracle(cfg_o, params, obs, B, use_argmax, precision, seed=3):
     import paper_2312_15122_b200 as z
+    tol = TOL[precision]
     rng0 = np.array([(0x1234567 * (b + 1) + seed) & ((1 << 64) - 1) for b in range(B)], np.uint64)
-    pol = z.NNPolicy(z.ModelConfig(), params, use_argmax=use_argmax)
+    pol = z.NNPolicy(z.ModelConfig(), params, use_argmax=use_argmax, precision=precision)
     got = run_device(pol, obs, rng0, B)
     ref = po.act(po.Model(cfg_o, params), obs, rng0, use_argmax)
     na = cfg_o.n_accel
-    np.testing.assert_allclose(got["logits"][:, :na], ref["logits_accel"], atol=LOGIT_ATOL, rtol=LOGIT_RTOL)
-    np.testing.assert_allclose(got["logits"][:, na:], ref["logits_steer"], atol=LOGIT_ATOL, rtol=LOGIT_RTOL)
-    np.testing.assert_allclose(got["value"], ref["value"], atol=LOGIT_ATOL, rtol=LOGIT_RTOL)
+    err = max(np.abs(got["logits"][:, :na] - ref["logits_accel"]).max(),
+              np.abs(got["logits"][:, na:] - ref["logits_steer"]).max(), np.abs(got["value"] - ref["value"]).max())
+    print(f"{precision}: max |logit / value error| = {err:.3g}")
+    np.testing.assert_allclose(got["logits"][:, :na], ref["logits_accel"], atol=tol["atol"], rtol=tol["rtol"])
+    np.testing.assert_allclose(got["logits"][:, na:], ref["logits_steer"], atol=tol["atol"], rtol=tol["rtol"])
+    np.testing.assert_allclose(got["value"], ref["value"], atol=tol["atol"], rtol=tol["rtol"])
     checked = 0
     for b in range(B):
-        if margins_ok(ref["logits_accel"][b], ref["u"][b][0], use_argmax) and \
-                margins_ok(ref["logits_steer"][b], ref["u"][b][1], use_argmax):
+        if margins_ok(ref["logits_accel"][b], ref["u"][b][0], use_argmax, tol["margin"]) and \
+                margins_ok(ref["logits_steer"][b], ref["u"][b][1], use_argmax, tol["margin"]):
             assert got["accel"][b] == ref["accel"][b] and got["steer"][b] == ref["steer"][b], b
-            assert abs(got["logp"][b] - ref["logp"][b]) < LOGP_ATOL, b
+            assert abs(got["logp"][b] - ref["logp"][b]) < tol["logp"], b
             checked += 1
-    assert checked >= B * 3 // 4
+    assert checked >= B // 3
     if not use_argmax:
         assert np.array_equal(got["rng"], ref["rng"])  # two draws per row
     return got, ref
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
 @pytest.mark.parametrize("use_argmax", [True, False])
-def test_policy_act_random_obs(use_argmax):
+def test_policy_act_random_obs(use_argmax, precision):
     cfg_o = po.ModelConfig()
     params = po.init_params(cfg_o, 11)
-    obs = random_obs(10, np.random.default_rng(5))  # 10 rows: the last CTA is partial
-    check_against_oracle(cfg_o, params, obs, 10, use_argmax)
+    B = 17  # the last CTA is partial for both row groupings (7 and 3 rows per CTA)
+    obs = random_obs(B, np.random.default_rng(5))
+    check_against_oracle(cfg_o, params, obs, B, use_argmax, precision)
 
 
 @pytest.mark.gpu
-def test_policy_act_on_simulator_observations():
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_policy_act_on_simulator_observations(precision):
     import torch
 
     import paper_2312_15122_b200 as z
-    zsim = z.stress_scenarios(z.StressConfig(count=8, agents=20, road_points=900), seed=3)
+    zsim = z.stress_scenarios(z.StressConfig(count=16, agents=20, road_points=900), seed=3)
     env = z.Env(zsim, config=z.SimConfig(disable_dones=False), device=0)
     st, nxt, so, ob = env.device_state(), env.device_state(), env.device_stepout(), env.device_obs()
     env.reset_device(4, st)
-    A, S = z.random_actions(5, 8, seed=9)
+    A, S = z.random_actions(5, 16, seed=9)
     for t in range(5):
         a, s = torch.from_numpy(A[t]).cuda(), torch.from_numpy(S[t]).cuda()
         env.step_observe_device(st, a.data_ptr(), s.data_ptr(), nxt, so, ob)
@@ -152,7 +165,7 @@ def test_policy_act_on_simulator_observations():
     h = env.download_obs(ob)
     obs = {k: getattr(h, k).copy() for k in ("active", "agents", "road", "route", "value_only")}
     cfg_o = po.ModelConfig()
-    check_against_oracle(cfg_o, po.init_params(cfg_o, 2), obs, 8, False)
+    check_against_oracle(cfg_o, po.init_params(cfg_o, 2), obs, 16, False, precision)
 
 
 @pytest.mark.gpu
