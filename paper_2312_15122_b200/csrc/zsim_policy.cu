@@ -132,6 +132,7 @@ struct RowSm {
     float lnv[R][kD];
     float logit[R][2 * kMaxHead];
     float vout[R];
+    float part[2][R][kD];  // GEMV partial sums of the two K halves
 };
 
 template <int R>
@@ -178,6 +179,28 @@ __device__ __forceinline__ float embed_latent(const PolicyW& W, const ActArgs& a
     return acc + W.emb_ag_b[c];
 }
 
+// Partial products sum_k W(n, k) x[g][k] of every row over one half of K
+// into sm.part[half][g][n]: thread (n, half) loads each weight once and
+// applies it to all R rows (R independent accumulation chains).  W column-major
+// [K][128]; ends with a block barrier.
+template <int R>
+__device__ void gemv_rows(RowSm<R>& sm, const float* __restrict__ W, int K, const float* x, int xstride) {
+    const int n = threadIdx.x & (kD - 1), kh = threadIdx.x >> 7;
+    const int k0 = kh * (K / 2), k1 = kh ? K : K / 2;
+    float acc[R];
+#pragma unroll
+    for (int g = 0; g < R; ++g) acc[g] = 0.f;
+#pragma unroll 8
+    for (int k = k0; k < k1; ++k) {
+        const float wv = __ldg(W + size_t(k) * kD + n);
+#pragma unroll
+        for (int g = 0; g < R; ++g) acc[g] = fmaf(wv, x[g * xstride + k], acc[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < R; ++g) sm.part[kh][g][n] = acc[g];
+    __syncthreads();
+}
+
 // mlp_forward (model.hpp:431-440) of vec[.][src] into vec[.][dst] for every row.
 template <int R>
 __device__ void mlp_rows(RowSm<R>& sm, const MlpW& w, int src, int dst) {
@@ -202,18 +225,16 @@ __device__ void mlp_rows(RowSm<R>& sm, const MlpW& w, int src, int dst) {
         }
     }
     __syncthreads();
+    gemv_rows<R>(sm, w.w1, kD, &sm.lnv[0][0], kD);
     for (int task = threadIdx.x; task < R * kD; task += kThreads) {
         const int g = task / kD, n = task % kD;
-        float acc = 0.f;
-        for (int k = 0; k < kD; ++k) acc = fmaf(__ldg(w.w1 + k * kD + n), sm.lnv[g][k], acc);
-        sm.tmp[g][n] = gelu(acc + w.b1[n]);
+        sm.tmp[g][n] = gelu(sm.part[0][g][n] + sm.part[1][g][n] + w.b1[n]);
     }
     __syncthreads();
+    gemv_rows<R>(sm, w.w2, kD, &sm.tmp[0][0], kD);
     for (int task = threadIdx.x; task < R * kD; task += kThreads) {
         const int g = task / kD, n = task % kD;
-        float acc = 0.f;
-        for (int k = 0; k < kD; ++k) acc = fmaf(__ldg(w.w2 + k * kD + n), sm.tmp[g][k], acc);
-        sm.vec[g][dst][n] = acc + w.b2[n] + sm.vec[g][src][n];
+        sm.vec[g][dst][n] = sm.part[0][g][n] + sm.part[1][g][n] + w.b2[n] + sm.vec[g][src][n];
     }
 }
 
@@ -300,11 +321,10 @@ __device__ void trunk_and_act(RowSm<R>& sm, const ActArgs& a, int b0) {
         sm.vec[g][0][c] = v;
     }
     __syncthreads();
+    gemv_rows<R>(sm, W.vin_w, kD + W.ve, &sm.vec[0][0][0], 2 * (kD + kMaxVE));
     for (int e = tid; e < R * kD; e += kThreads) {
         const int g = e / kD, n = e % kD;
-        float acc = 0.f;
-        for (int k = 0; k < kD + W.ve; ++k) acc = fmaf(__ldg(W.vin_w + size_t(k) * kD + n), sm.vec[g][0][k], acc);
-        sm.vec[g][1][n] = acc + W.vin_b[n];
+        sm.vec[g][1][n] = sm.part[0][g][n] + sm.part[1][g][n] + W.vin_b[n];
     }
     cur = 1;
 #pragma unroll
@@ -367,29 +387,19 @@ __device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* 
     const float* kf = w.kf + h * kDh;
     float qf[F];
 #pragma unroll
-    for (int f = 0; f < F; ++f) {
-        float acc = 0.f;
-#pragma unroll 16
-        for (int c = 0; c < kDh; ++c) acc = fmaf(__ldg(kf + f * kD + c), q[c], acc);
-        qf[f] = acc;
-    }
+    for (int f = 0; f < F; ++f) qf[f] = 0.f;
     float qn = 0.f, sn = 0.f;
-#pragma unroll 16
-    for (int c = 0; c < kDh; ++c) {
+#pragma unroll
+    for (int c = 0; c < kDh; ++c) {  // F + 2 independent chains
+#pragma unroll
+        for (int f = 0; f < F; ++f) qf[f] = fmaf(__ldg(kf + f * kD + c), q[c], qf[f]);
         qn = fmaf(__ldg(w.ck + h * kDh + c), q[c], qn);
         sn = fmaf(__ldg(w.kn + h * kDh + c), q[c], sn);
     }
     sn *= scale;
-    float mx = sn;
-    for (int j = 0; j < N; ++j) {
-        if (!mask[j]) continue;
-        float d = qn;
-#pragma unroll
-        for (int f = 0; f < F; ++f) d = fmaf(qf[f], feat[j][f], d);
-        mx = fmaxf(mx, d * scale);
-    }
-    const float en = expf(sn - mx);
-    float tot = en, ps = 0.f;
+    // one pass, running maximum (the softmax is shift-invariant; every
+    // accumulated term is rescaled when the maximum moves)
+    float mx = sn, tot = 1.f, ps = 0.f;
     float ag[F];
 #pragma unroll
     for (int f = 0; f < F; ++f) ag[f] = 0.f;
@@ -398,19 +408,29 @@ __device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* 
         float d = qn;
 #pragma unroll
         for (int f = 0; f < F; ++f) d = fmaf(qf[f], feat[j][f], d);
-        const float e = expf(d * scale - mx);
+        d *= scale;
+        if (d > mx) {
+            const float r = expf(mx - d);
+            tot *= r;
+            ps *= r;
+#pragma unroll
+            for (int f = 0; f < F; ++f) ag[f] *= r;
+            mx = d;
+        }
+        const float e = expf(d - mx);
         tot += e;
         ps += e;
 #pragma unroll
         for (int f = 0; f < F; ++f) ag[f] = fmaf(e, feat[j][f], ag[f]);
     }
+    const float en = expf(sn - mx);  // the null token's term, already inside tot (started as exp(0) = 1)
     const float inv = 1.f / tot;
     ps *= inv;
     const float pn = en * inv;
 #pragma unroll
     for (int f = 0; f < F; ++f) ag[f] *= inv;
     const float* vf = w.vf + h * kDh;
-#pragma unroll 8
+#pragma unroll
     for (int c = 0; c < kDh; ++c) {
         float o = fmaf(ps, __ldg(w.cv + h * kDh + c), pn * __ldg(w.vn + h * kDh + c));
 #pragma unroll
@@ -497,13 +517,18 @@ template <class KV>
 __device__ __forceinline__ void self_query(int h, const float* q, const unsigned char* mlat, KV kv, float* out) {
     const float scale = 0.125f;
     float s[kLat];
+#pragma unroll
+    for (int j = 0; j < kLat; ++j) s[j] = 0.f;
+    // q / out are register arrays in the tensor-core kernel: every loop over
+    // the head's 64 columns is fully unrolled so the indices stay static
+#pragma unroll
+    for (int c = 0; c < kDh; ++c)  // 17 independent chains
+#pragma unroll
+        for (int j = 0; j < kLat; ++j) s[j] = fmaf(q[c], kv.k(j, h * kDh + c), s[j]);
     float mx = -INFINITY;
 #pragma unroll
     for (int j = 0; j < kLat; ++j) {
-        float d = 0.f;
-#pragma unroll 16
-        for (int c = 0; c < kDh; ++c) d = fmaf(q[c], kv.k(j, h * kDh + c), d);
-        s[j] = d * scale;
+        s[j] *= scale;
         if (mlat[j]) mx = fmaxf(mx, s[j]);
     }
     float tot = 0.f;
@@ -513,7 +538,7 @@ __device__ __forceinline__ void self_query(int h, const float* q, const unsigned
         tot += s[j];
     }
     const float inv = 1.f / tot;
-#pragma unroll 8
+#pragma unroll
     for (int c = 0; c < kDh; ++c) {
         float o = 0.f;
 #pragma unroll
