@@ -84,6 +84,11 @@ struct PolicyW {
     // tensor-core copies of the projections, [N=128][K=128] canonical K-major
     // tf32 tiles of 64 KB: self q k v o, road q o, route q o, active q o
     const float* tc[kNumProj];
+    // tensor-core tiles of the trunks: policy block i W1 / W2 at 2i / 2i+1,
+    // value block i W1 / W2 at 2i / 2i+1 (K = 128), value.in (K = 128 + ve)
+    const float* tc_pblk[2 * kMaxTrunk];
+    const float* tc_vblk[2 * kMaxTrunk];
+    const float* tc_vin;
     int trunk, ve, n_accel, n_steer;
 };
 
@@ -98,6 +103,7 @@ struct ActArgs {
     float* logp;
     float* value;
     float* logits;  // optional [B][n_accel + n_steer]
+    float* pooled;  // [B][128] scratch: encoder output (tensor-core path)
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -126,6 +132,11 @@ struct RowSm {
     unsigned char mroute[R][kRoute];
     unsigned char mlat[R][kLat];
     unsigned char mact[R][1];  // the active token is always valid
+};
+
+// post-encoder trunk state of the fp32 kernel
+template <int R>
+struct TrunkSm {
     float vec[R][2][kD + kMaxVE];  // trunk vectors, ping-pong
     float tmp[R][kD];
     float pooled[R][kD];
@@ -184,7 +195,7 @@ __device__ __forceinline__ float embed_latent(const PolicyW& W, const ActArgs& a
 // applies it to all R rows (R independent accumulation chains).  W column-major
 // [K][128]; ends with a block barrier.
 template <int R>
-__device__ void gemv_rows(RowSm<R>& sm, const float* __restrict__ W, int K, const float* x, int xstride) {
+__device__ void gemv_rows(TrunkSm<R>& sm, const float* __restrict__ W, int K, const float* x, int xstride) {
     const int n = threadIdx.x & (kD - 1), kh = threadIdx.x >> 7;
     const int k0 = kh * (K / 2), k1 = kh ? K : K / 2;
     float acc[R];
@@ -203,7 +214,7 @@ __device__ void gemv_rows(RowSm<R>& sm, const float* __restrict__ W, int K, cons
 
 // mlp_forward (model.hpp:431-440) of vec[.][src] into vec[.][dst] for every row.
 template <int R>
-__device__ void mlp_rows(RowSm<R>& sm, const MlpW& w, int src, int dst) {
+__device__ void mlp_rows(TrunkSm<R>& sm, const MlpW& w, int src, int dst) {
     __syncthreads();
     {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -281,7 +292,7 @@ __device__ int argmax_first(const float* z, int n) {
 // From the pooled encodings (sm.pooled): policy trunk and heads, value trunk
 // (model.hpp:556-584), then NNPolicy::act's selection (policy.hpp:33-56).
 template <int R>
-__device__ void trunk_and_act(RowSm<R>& sm, const ActArgs& a, int b0) {
+__device__ void trunk_and_act(const RowSm<R>& in, TrunkSm<R>& sm, const ActArgs& a, int b0) {
     const PolicyW& W = a.w;
     const int tid = threadIdx.x;
     __syncthreads();
@@ -315,7 +326,7 @@ __device__ void trunk_and_act(RowSm<R>& sm, const ActArgs& a, int b0) {
             const int j = c - kD;
             float acc = 0.f;
 #pragma unroll
-            for (int f = 0; f < kValF; ++f) acc = fmaf(W.vemb_w[f * W.ve + j], sm.val[g][f], acc);
+            for (int f = 0; f < kValF; ++f) acc = fmaf(W.vemb_w[f * W.ve + j], in.val[g][f], acc);
             v = gelu(acc + W.vemb_b[j]);
         }
         sm.vec[g][0][c] = v;
@@ -390,11 +401,17 @@ __device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* 
     for (int f = 0; f < F; ++f) qf[f] = 0.f;
     float qn = 0.f, sn = 0.f;
 #pragma unroll
-    for (int c = 0; c < kDh; ++c) {  // F + 2 independent chains
+    for (int c4 = 0; c4 < kDh / 4; ++c4) {  // F + 2 independent chains, float4 weight loads
+        const int c = 4 * c4;
 #pragma unroll
-        for (int f = 0; f < F; ++f) qf[f] = fmaf(__ldg(kf + f * kD + c), q[c], qf[f]);
-        qn = fmaf(__ldg(w.ck + h * kDh + c), q[c], qn);
-        sn = fmaf(__ldg(w.kn + h * kDh + c), q[c], sn);
+        for (int f = 0; f < F; ++f) {
+            const float4 k = __ldg(reinterpret_cast<const float4*>(kf + f * kD + c));
+            qf[f] = fmaf(k.x, q[c], fmaf(k.y, q[c + 1], fmaf(k.z, q[c + 2], fmaf(k.w, q[c + 3], qf[f]))));
+        }
+        const float4 ck = __ldg(reinterpret_cast<const float4*>(w.ck + h * kDh + c));
+        const float4 kn = __ldg(reinterpret_cast<const float4*>(w.kn + h * kDh + c));
+        qn = fmaf(ck.x, q[c], fmaf(ck.y, q[c + 1], fmaf(ck.z, q[c + 2], fmaf(ck.w, q[c + 3], qn))));
+        sn = fmaf(kn.x, q[c], fmaf(kn.y, q[c + 1], fmaf(kn.z, q[c + 2], fmaf(kn.w, q[c + 3], sn))));
     }
     sn *= scale;
     // one pass, running maximum (the softmax is shift-invariant; every
@@ -431,11 +448,24 @@ __device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* 
     for (int f = 0; f < F; ++f) ag[f] *= inv;
     const float* vf = w.vf + h * kDh;
 #pragma unroll
-    for (int c = 0; c < kDh; ++c) {
-        float o = fmaf(ps, __ldg(w.cv + h * kDh + c), pn * __ldg(w.vn + h * kDh + c));
+    for (int c4 = 0; c4 < kDh / 4; ++c4) {
+        const int c = 4 * c4;
+        const float4 cv = __ldg(reinterpret_cast<const float4*>(w.cv + h * kDh + c));
+        const float4 vn = __ldg(reinterpret_cast<const float4*>(w.vn + h * kDh + c));
+        float o0 = fmaf(ps, cv.x, pn * vn.x), o1 = fmaf(ps, cv.y, pn * vn.y), o2 = fmaf(ps, cv.z, pn * vn.z),
+              o3 = fmaf(ps, cv.w, pn * vn.w);
 #pragma unroll
-        for (int f = 0; f < F; ++f) o = fmaf(__ldg(vf + f * kD + c), ag[f], o);
-        out[c] = o;
+        for (int f = 0; f < F; ++f) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(vf + f * kD + c));
+            o0 = fmaf(v.x, ag[f], o0);
+            o1 = fmaf(v.y, ag[f], o1);
+            o2 = fmaf(v.z, ag[f], o2);
+            o3 = fmaf(v.w, ag[f], o3);
+        }
+        out[c] = o0;
+        out[c + 1] = o1;
+        out[c + 2] = o2;
+        out[c + 3] = o3;
     }
 }
 
@@ -449,6 +479,8 @@ struct Smem32 {
     float K[kTok32][kLd];
     float V[kTok32][kLd];
     RowSm<kRows32> rs;
+    TrunkSm<kRows32> tr;
+    float sc[kThreads][kLat];  // self-attention scores of each thread's query
 };
 
 // ln_forward (model.hpp:287-303) of every token row of X into A: one warp per token.
@@ -514,36 +546,50 @@ __device__ void gemm32(const float (*A)[kLd], const float* __restrict__ W, const
 // Self attention (model.hpp:340-364) of each row's 17 latent tokens, one
 // thread per (token, head): keys / values of the row from smem.
 template <class KV>
-__device__ __forceinline__ void self_query(int h, const float* q, const unsigned char* mlat, KV kv, float* out) {
+__device__ __forceinline__ void self_query(int h, const float* q, const unsigned char* mlat, KV kv, float* out,
+                                           float* sc) {
     const float scale = 0.125f;
-    float s[kLat];
-#pragma unroll
-    for (int j = 0; j < kLat; ++j) s[j] = 0.f;
-    // q / out are register arrays in the tensor-core kernel: every loop over
-    // the head's 64 columns is fully unrolled so the indices stay static
-#pragma unroll
-    for (int c = 0; c < kDh; ++c)  // 17 independent chains
-#pragma unroll
-        for (int j = 0; j < kLat; ++j) s[j] = fmaf(q[c], kv.k(j, h * kDh + c), s[j]);
-    float mx = -INFINITY;
-#pragma unroll
+    // q / out may be register arrays (tensor-core kernel): every loop over the
+    // head's 64 columns is fully unrolled so their indices stay static; the
+    // key loops stay rolled (scores in the thread's smem scratch `sc`) so the
+    // compiler does not hoist 17 rows of K into registers.
+#pragma unroll 1
     for (int j = 0; j < kLat; ++j) {
-        s[j] *= scale;
-        if (mlat[j]) mx = fmaxf(mx, s[j]);
+        float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+#pragma unroll
+        for (int c4 = 0; c4 < kDh / 4; ++c4) {
+            const float4 kk = kv.k4(j, h * (kDh / 4) + c4);
+            p0 = fmaf(q[4 * c4], kk.x, p0);
+            p1 = fmaf(q[4 * c4 + 1], kk.y, p1);
+            p2 = fmaf(q[4 * c4 + 2], kk.z, p2);
+            p3 = fmaf(q[4 * c4 + 3], kk.w, p3);
+        }
+        sc[j] = ((p0 + p1) + (p2 + p3)) * scale;
     }
+    float mx = -INFINITY;
+    for (int j = 0; j < kLat; ++j)
+        if (mlat[j]) mx = fmaxf(mx, sc[j]);
     float tot = 0.f;
-#pragma unroll
     for (int j = 0; j < kLat; ++j) {
-        s[j] = mlat[j] ? expf(s[j] - mx) : 0.f;
-        tot += s[j];
+        const float e = mlat[j] ? expf(sc[j] - mx) : 0.f;
+        sc[j] = e;
+        tot += e;
     }
     const float inv = 1.f / tot;
 #pragma unroll
-    for (int c = 0; c < kDh; ++c) {
-        float o = 0.f;
+    for (int c = 0; c < kDh; ++c) out[c] = 0.f;
+#pragma unroll 1
+    for (int j = 0; j < kLat; ++j) {
+        const float pj = sc[j] * inv;
+        if (pj == 0.f) continue;
 #pragma unroll
-        for (int j = 0; j < kLat; ++j) o = fmaf(s[j], kv.v(j, h * kDh + c), o);
-        out[c] = o * inv;
+        for (int c4 = 0; c4 < kDh / 4; ++c4) {
+            const float4 vv = kv.v4(j, h * (kDh / 4) + c4);
+            out[4 * c4] = fmaf(pj, vv.x, out[4 * c4]);
+            out[4 * c4 + 1] = fmaf(pj, vv.y, out[4 * c4 + 1]);
+            out[4 * c4 + 2] = fmaf(pj, vv.z, out[4 * c4 + 2]);
+            out[4 * c4 + 3] = fmaf(pj, vv.w, out[4 * c4 + 3]);
+        }
     }
 }
 
@@ -551,8 +597,8 @@ struct KV32 {
     const float (*K)[kLd];
     const float (*V)[kLd];
     int base;
-    __device__ float k(int j, int c) const { return K[base + j][c]; }
-    __device__ float v(int j, int c) const { return V[base + j][c]; }
+    __device__ float4 k4(int j, int q) const { return *reinterpret_cast<const float4*>(&K[base + j][4 * q]); }
+    __device__ float4 v4(int j, int q) const { return *reinterpret_cast<const float4*>(&V[base + j][4 * q]); }
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_policy_fp32(const ActArgs a) {
@@ -576,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_fp32(const ActArgs a) {
     __syncthreads();
     if (tid < kRows32 * kLat * kHeads) {
         const int s = tid >> 1, h = tid & 1, g = s / kLat;
-        self_query(h, &sm.Q[s][h * kDh], sm.rs.mlat[g], KV32{sm.K, sm.V, g * kLat}, &sm.A[s][h * kDh]);
+        self_query(h, &sm.Q[s][h * kDh], sm.rs.mlat[g], KV32{sm.K, sm.V, g * kLat}, &sm.A[s][h * kDh], sm.sc[tid]);
     }
     __syncthreads();
     gemm32(sm.A, W.self.wo, W.self.bo, sm.X, true);
@@ -611,9 +657,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_fp32(const ActArgs a) {
                 acc += sm.X[g * kLat + i][c];
                 ++n;
             }
-        sm.rs.pooled[g][c] = acc / float(n);
+        sm.tr.pooled[g][c] = acc / float(n);
     }
-    trunk_and_act<kRows32>(sm.rs, a, b0);
+    trunk_and_act<kRows32>(sm.rs, sm.tr, a, b0);
 }
 
 // ===========================================================================
@@ -627,6 +673,7 @@ struct SmemTc {
     float opA[kTokTc * kD];  // A operand: 128 tokens x 128 K, canonical K-major tf32 (64 KB)
     float opW[kD * kD];      // B operand: 128 outputs x 128 K, canonical K-major tf32 (64 KB)
     RowSm<kRowsTc> rs;
+    float sc[kThreads][kLat];  // self-attention scores of each thread's query (odd stride: no bank conflicts)
     float red[2][kTokTc];    // LayerNorm partial sums of the two column halves
     float red2[2][kTokTc];
     unsigned long long mbar_w, mbar_mma;
@@ -825,8 +872,14 @@ struct KVTc {  // self-attention K / V copies in smem: [128 tokens][128], float4
     const float* V;
     int base;
     __device__ static int idx(int r, int c) { return r * kD + ((((c >> 2) ^ (r & 7)) << 2) | (c & 3)); }
-    __device__ float k(int j, int c) const { return K[idx(base + j, c)]; }
-    __device__ float v(int j, int c) const { return V[idx(base + j, c)]; }
+    __device__ float4 k4(int j, int q) const {
+        const int r = base + j;
+        return *reinterpret_cast<const float4*>(K + r * kD + ((q ^ (r & 7)) << 2));
+    }
+    __device__ float4 v4(int j, int q) const {
+        const int r = base + j;
+        return *reinterpret_cast<const float4*>(V + r * kD + ((q ^ (r & 7)) << 2));
+    }
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
@@ -856,9 +909,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
     cx.load_w(W.tc[0]);  // self Wq streams in while the inputs are staged
     load_row_inputs<kRowsTc>(sm.rs, a, b0);
     {
+        // latent token embedding (model.hpp:510-513), this thread's 64 columns
         float v[64];
-#pragma unroll 4
-        for (int i = 0; i < 64; ++i) v[i] = real ? embed_latent(W, a, b0 + g, slot, 64 * half + i) : 0.f;
+        const int b = b0 + g, c0 = 64 * half;
+        if (!real) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = 0.f;
+        } else if (slot == 0) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = __ldg(W.null_ag + c0 + i);
+        } else {
+            float x[kAgF];
+            const float* ag = a.obs.agents + (size_t(b) * kAgents + (slot - 1)) * kAgF;
+#pragma unroll
+            for (int f = 0; f < kAgF; ++f) x[f] = b < a.B ? ag[f] * c_ag_scale[f] : 0.f;
+#pragma unroll
+            for (int c4 = 0; c4 < 16; ++c4) {
+                const float4 bb = __ldg(reinterpret_cast<const float4*>(W.emb_ag_b + c0 + 4 * c4));
+                float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+#pragma unroll
+                for (int f = 0; f < kAgF; ++f) {
+                    const float4 w4 = __ldg(reinterpret_cast<const float4*>(W.emb_ag_w + f * kD + c0 + 4 * c4));
+                    o0 = fmaf(w4.x, x[f], o0);
+                    o1 = fmaf(w4.y, x[f], o1);
+                    o2 = fmaf(w4.z, x[f], o2);
+                    o3 = fmaf(w4.w, x[f], o3);
+                }
+                v[4 * c4] = o0 + bb.x;
+                v[4 * c4 + 1] = o1 + bb.y;
+                v[4 * c4 + 2] = o2 + bb.z;
+                v[4 * c4 + 3] = o3 + bb.w;
+            }
+        }
         cx.st64(kColX, v);
     }
     __syncthreads();
@@ -900,7 +982,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
 #pragma unroll
         for (int i = 0; i < 64; ++i) q[i] += __ldg(W.self.bq + 64 * half + i);
         if (real) {
-            self_query(half, q, sm.rs.mlat[g], KVTc{sm.opA, sm.opW, g * kLat}, o);
+            self_query(half, q, sm.rs.mlat[g], KVTc{sm.opA, sm.opW, g * kLat}, o, sm.sc[tid]);
         } else {
 #pragma unroll
             for (int i = 0; i < 64; ++i) o[i] = 0.f;
@@ -963,9 +1045,278 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
                 acc += sm.opA[(gg * kLat + i) * (kD + 4) + c];
                 ++n;
             }
-        sm.rs.pooled[gg][c] = acc / float(n);
+        if (b0 + gg < a.B) a.pooled[size_t(b0 + gg) * kD + c] = acc / float(n);
     }
-    trunk_and_act<kRowsTc>(sm.rs, a, b0);
+}
+
+// ===========================================================================
+// k_policy_heads: policy / value trunks, heads and the action choice for 128
+// rows per CTA (thread = row = TMEM lane); every trunk matrix product is a
+// tcgen05.mma.kind::tf32 (M = 128 rows, N = 128, K = 128 or 128 + ve).
+// ===========================================================================
+constexpr int kHeadRows = 128;
+constexpr int kHeadThreads = 128;
+constexpr int kMaxK = kD + kMaxVE;  // value.in's K
+// TMEM columns: trunk activation H [0,128), products D [128,256), pooled P [256,384)
+constexpr uint32_t kHColH = 0, kHColD = 128, kHColP = 256;
+
+struct SmemHeads {
+    float opA[kHeadRows * kMaxK];  // canonical K-major tf32, K up to 192
+    float opW[kD * kMaxK];
+    float hw[2 * kMaxHead][kD];    // accel / steer head weights, row-major [out][k]
+    float vhead[kD];
+    unsigned long long mbar_w, mbar_mma;
+    uint32_t tmem_base;
+};
+
+// canonical offset for an M x K tile with K-chunk stride M/8 * 128 B (M = N = 128 here)
+__device__ __forceinline__ void heads_put(float* opA, int row, int k0, const float* v, int n) {
+    for (int q = 0; q < n / 4; ++q) {
+        const int k = k0 + 4 * q;
+        uint4 u = make_uint4(to_tf32(v[4 * q]), to_tf32(v[4 * q + 1]), to_tf32(v[4 * q + 2]), to_tf32(v[4 * q + 3]));
+        *reinterpret_cast<uint4*>(opA + canon_off(row, k)) = u;
+    }
+}
+
+struct HeadsCtx {
+    SmemHeads& sm;
+    uint32_t tmem, lane_base;
+    int row;
+    uint32_t ph_w = 0, ph_mma = 0;
+    __device__ uint32_t col(uint32_t c) const { return tmem + lane_base + c; }
+    __device__ void load_w(const float* src, uint32_t bytes) {
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t mb = smem_u32(&sm.mbar_w);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+            for (uint32_t o = 0; o < bytes; o += 16384u) {
+                const uint32_t n = bytes - o < 16384u ? bytes - o : 16384u;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(sm.opW) + o),
+                    "l"(reinterpret_cast<const char*>(src) + o), "r"(n), "r"(mb)
+                    : "memory");
+            }
+        }
+    }
+    __device__ void wait_w() {
+        mbar_wait(&sm.mbar_w, ph_w);
+        ph_w ^= 1;
+    }
+    __device__ void mma(uint32_t dcol, int K) {
+        tc_fence_before();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sm.opA), w0 = smem_u32(sm.opW);
+            for (int kk = 0; kk < K / 8; ++kk) {
+                const uint64_t da = umma_desc(a0 + kk * 2 * 2048), dw = umma_desc(w0 + kk * 2 * 2048);
+                const uint32_t acc = kk > 0;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + dcol),
+                    "l"(da), "l"(dw), "r"(kIdesc), "r"(acc)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&sm.mbar_mma))
+                         : "memory");
+        }
+        mbar_wait(&sm.mbar_mma, ph_mma);
+        ph_mma ^= 1;
+        tc_fence_after();
+    }
+    // LayerNorm (model.hpp:287-303) of this row's H into opA
+    __device__ void ln_to_a(const float* g, const float* b) {
+        float v[32];
+        float s = 0.f;
+        for (int c = 0; c < kD; c += 32) {
+            tmem_ld32(col(kHColH + c), v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) s += v[i];
+        }
+        const float mu = s / float(kD);
+        float q = 0.f;
+        for (int c = 0; c < kD; c += 32) {
+            tmem_ld32(col(kHColH + c), v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) q += (v[i] - mu) * (v[i] - mu);
+        }
+        const float rstd = 1.f / sqrtf(q / float(kD) + 1e-5f);
+        for (int c = 0; c < kD; c += 32) {
+            tmem_ld32(col(kHColH + c), v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = (v[i] - mu) * rstd * __ldg(g + c + i) + __ldg(b + c + i);
+            heads_put(sm.opA, row, c, v, 32);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    // mlp_forward (model.hpp:431-440): H += W2 gelu(W1 LN(H) + b1) + b2
+    __device__ void mlp(const MlpW& w, const float* w1_tc, const float* w2_tc) {
+        load_w(w1_tc, kD * kD * 4);
+        ln_to_a(w.ln_g, w.ln_b);
+        wait_w();
+        mma(kHColD, kD);
+        load_w(w2_tc, kD * kD * 4);
+        float v[32];
+        for (int c = 0; c < kD; c += 32) {
+            tmem_ld32(col(kHColD + c), v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = gelu(v[i] + __ldg(w.b1 + c + i));
+            heads_put(sm.opA, row, c, v, 32);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        wait_w();
+        mma(kHColD, kD);
+        float h[32];
+        for (int c = 0; c < kD; c += 32) {
+            tmem_ld32(col(kHColD + c), v);
+            tmem_ld32(col(kHColH + c), h);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) h[i] += v[i] + __ldg(w.b2 + c + i);
+            tmem_st32(col(kHColH + c), h);
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs a) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    SmemHeads& sm = *reinterpret_cast<SmemHeads*>(dsm);
+    const PolicyW& W = a.w;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int b = blockIdx.x * kHeadRows + tid;
+    const bool live = b < a.B;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        mbar_init(&sm.mbar_w, 1);
+        mbar_init(&sm.mbar_mma, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const int na = W.n_accel, ns = W.n_steer;
+    for (int e = tid; e < (na + ns) * kD; e += kHeadThreads) {
+        const int o = e / kD, k = e % kD;
+        sm.hw[o][k] = o < na ? W.acc_w[k * na + o] : W.str_w[k * ns + (o - na)];
+    }
+    for (int k = tid; k < kD; k += kHeadThreads) sm.vhead[k] = W.vhead_w[k];
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    HeadsCtx cx{sm, sm.tmem_base, uint32_t(warp * 32) << 16, tid};
+
+    // pooled encoding -> H and P
+    {
+        float v[32];
+        for (int c = 0; c < kD; c += 32) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = live ? a.pooled[size_t(b) * kD + c + i] : 0.f;
+            tmem_st32(cx.col(kHColH + c), v);
+            tmem_st32(cx.col(kHColP + c), v);
+        }
+    }
+    // ---- policy trunk + heads (model.hpp:556-568) ----
+#pragma unroll
+    for (int i = 0; i < kMaxTrunk; ++i)
+        if (i < W.trunk) cx.mlp(W.pblk[i], W.tc_pblk[2 * i], W.tc_pblk[2 * i + 1]);
+    float logit[2 * kMaxHead];
+    {
+        for (int o = 0; o < na + ns; ++o) logit[o] = o < na ? __ldg(W.acc_b + o) : __ldg(W.str_b + o - na);
+        float v[32];
+        for (int c = 0; c < kD; c += 32) {
+            tmem_ld32(cx.col(kHColH + c), v);
+            for (int o = 0; o < na + ns; ++o) {
+                float acc = logit[o];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) acc = fmaf(sm.hw[o][c + i], v[i], acc);
+                logit[o] = acc;
+            }
+        }
+    }
+    // ---- value trunk (model.hpp:570-584) ----
+    cx.load_w(W.tc_vin, uint32_t(kD * (kD + W.ve) * 4));
+    {
+        float v[32];
+        for (int c = 0; c < kD; c += 32) {
+            tmem_ld32(cx.col(kHColP + c), v);
+            heads_put(sm.opA, tid, c, v, 32);
+        }
+        // value embedding gelu(W_e v + b_e), ve <= 64 columns after the pooled ones
+        float vf[kValF];
+#pragma unroll
+        for (int f = 0; f < kValF; ++f) vf[f] = live ? a.obs.value_only[size_t(b) * kValF + f] * c_val_scale[f] : 0.f;
+        for (int c = 0; c < W.ve; c += 32) {
+            const int n = W.ve - c < 32 ? W.ve - c : 32;
+            for (int i = 0; i < 32; ++i) {
+                float acc = 0.f;
+                if (i < n) {
+#pragma unroll
+                    for (int f = 0; f < kValF; ++f) acc = fmaf(__ldg(W.vemb_w + f * W.ve + c + i), vf[f], acc);
+                    acc = gelu(acc + __ldg(W.vemb_b + c + i));
+                }
+                v[i] = acc;
+            }
+            heads_put(sm.opA, tid, kD + c, v, (n + 3) / 4 * 4);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    cx.wait_w();
+    cx.mma(kHColD, kD + W.ve);
+    {
+        float v[32];
+        for (int c = 0; c < kD; c += 32) {
+            tmem_ld32(cx.col(kHColD + c), v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += __ldg(W.vin_b + c + i);
+            tmem_st32(cx.col(kHColH + c), v);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxTrunk; ++i)
+        if (i < W.trunk) cx.mlp(W.vblk[i], W.tc_vblk[2 * i], W.tc_vblk[2 * i + 1]);
+    float value = __ldg(W.vhead_b);
+    {
+        float v[32];
+        for (int c = 0; c < kD; c += 32) {
+            tmem_ld32(cx.col(kHColH + c), v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) value = fmaf(sm.vhead[c + i], v[i], value);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(sm.tmem_base));
+    if (!live) return;
+    // ---- NNPolicy::act (policy.hpp:33-56) ----
+    if (a.logits) {
+        for (int i = 0; i < na + ns; ++i) a.logits[size_t(b) * (na + ns) + i] = logit[i];
+    }
+    a.value[b] = value;
+    float la[kMaxHead], ls[kMaxHead];
+    for (int i = 0; i < na; ++i) la[i] = logit[i];
+    for (int i = 0; i < ns; ++i) ls[i] = logit[na + i];
+    int ai, si;
+    float lp;
+    if (a.argmax) {
+        ai = argmax_first(la, na);
+        si = argmax_first(ls, ns);
+        log_softmax(la, na);
+        log_softmax(ls, ns);
+        lp = la[ai] + ls[si];
+    } else {
+        uint64_t st = a.rng[b];
+        log_softmax(la, na);
+        log_softmax(ls, ns);
+        double lpa, lps;
+        ai = sample_ls(la, na, st, lpa);
+        si = sample_ls(ls, ns, st, lps);
+        lp = float(lpa + lps);
+        a.rng[b] = st;
+    }
+    a.accel[b] = ai;
+    a.steer[b] = si;
+    a.logp[b] = lp;
 }
 
 }  // namespace zp
@@ -1048,10 +1399,10 @@ void validate(const zsim_model_config* c) {
     // what the device kernels are specialised for
     if (c->latent != kD || c->heads != kHeads || c->n_agents != kAgents || c->n_road != kRoad ||
         c->n_route != kRoute || c->trunk_blocks > kMaxTrunk || c->value_embed > kMaxVE || c->n_accel > kMaxHead ||
-        c->n_steer > kMaxHead)
+        c->n_steer > kMaxHead || c->value_embed % 8 != 0)
         zs::raise(Err::config, "model: the device policy supports latent 128, 2 heads, obs spec 16/128/64, <= " +
                                    std::to_string(kMaxTrunk) + " trunk blocks, value_embed <= " +
-                                   std::to_string(kMaxVE) + ", <= 16 bins per head");
+                                   std::to_string(kMaxVE) + " (a multiple of 8), <= 16 bins per head");
 }
 
 }  // namespace zp
@@ -1062,6 +1413,8 @@ struct zsim_policy {
     float* blob = nullptr;  // device: reference params followed by the folded cross-attention weights
     zp::PolicyW w{};
     int precision = 0;  // 0: tcgen05 tf32 projections, 1: fp32 CUDA cores
+    float* pooled = nullptr;  // [cap][128] encoder output scratch (tensor-core path)
+    int pooled_cap = 0;
 };
 
 namespace {
@@ -1200,24 +1553,34 @@ ZSIM_API int zsim_policy_create(const zsim_model_config* c, const float* params,
         const char* proj[zp::kNumProj] = {"enc.self.wq", "enc.self.wk", "enc.self.wv", "enc.self.wo",
                                           "enc.cross.road.wq", "enc.cross.road.wo", "enc.cross.route.wq",
                                           "enc.cross.route.wo", "enc.cross.active.wq", "enc.cross.active.wo"};
-        int64_t tc_off[zp::kNumProj];
-        extra.resize((extra.size() + 255) / 256 * 256);  // 1 KB alignment of the tiles
-        for (int i = 0; i < zp::kNumProj; ++i) {
-            const zp::Entry& e = find(proj[i]);
-            tc_off[i] = int64_t(extra.size());
-            extra.resize(extra.size() + size_t(d) * d);
-            float* t = extra.data() + tc_off[i];
+        // tile of an out x in weight (128 outputs, K inputs), 1 KB aligned
+        auto make_tile = [&](const zp::Entry& e, int K) {
+            extra.resize((extra.size() + 255) / 256 * 256);
+            const int64_t off = int64_t(extra.size());
+            extra.resize(extra.size() + size_t(d) * size_t(K));
+            float* t = extra.data() + off;
             for (int n2 = 0; n2 < d; ++n2)
-                for (int k = 0; k < d; ++k) {
+                for (int k = 0; k < K; ++k) {
                     uint32_t u;
-                    const float v = params[e.off + int64_t(k) * d + n2];
+                    const float v = params[e.off + int64_t(k) * e.rows + n2];
                     std::memcpy(&u, &v, 4);
                     if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
                     float r;
                     std::memcpy(&r, &u, 4);
                     t[((k >> 2) * 16 + (n2 >> 3)) * 32 + (n2 & 7) * 4 + (k & 3)] = r;
                 }
+            return off;
+        };
+        int64_t tc_off[zp::kNumProj], pblk_off[2 * zp::kMaxTrunk], vblk_off[2 * zp::kMaxTrunk];
+        for (int i = 0; i < zp::kNumProj; ++i) tc_off[i] = make_tile(find(proj[i]), d);
+        for (int i = 0; i < c->trunk_blocks; ++i) {
+            const std::string pp = "policy.block" + std::to_string(i), vp = "value.block" + std::to_string(i);
+            pblk_off[2 * i] = make_tile(find(pp + ".w1"), d);
+            pblk_off[2 * i + 1] = make_tile(find(pp + ".w2"), d);
+            vblk_off[2 * i] = make_tile(find(vp + ".w1"), d);
+            vblk_off[2 * i + 1] = make_tile(find(vp + ".w2"), d);
         }
+        const int64_t vin_off = make_tile(find("value.in.w"), d + c->value_embed);
         std::unique_ptr<zsim_policy> pol(new zsim_policy());
         pol->cfg = *c;
         pol->device = device;
@@ -1284,6 +1647,16 @@ ZSIM_API int zsim_policy_create(const zsim_model_config* c, const float* params,
         w.n_accel = c->n_accel;
         w.n_steer = c->n_steer;
         for (int i = 0; i < zp::kNumProj; ++i) w.tc[i] = D + base + tc_off[i];
+        for (int i = 0; i < c->trunk_blocks; ++i) {
+            w.tc_pblk[2 * i] = D + base + pblk_off[2 * i];
+            w.tc_pblk[2 * i + 1] = D + base + pblk_off[2 * i + 1];
+            w.tc_vblk[2 * i] = D + base + vblk_off[2 * i];
+            w.tc_vblk[2 * i + 1] = D + base + vblk_off[2 * i + 1];
+        }
+        w.tc_vin = D + base + vin_off;
+        ccheck(cudaFuncSetAttribute(zp::k_policy_heads, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(sizeof(zp::SmemHeads))),
+               "cudaFuncSetAttribute(policy heads)");
         ccheck(cudaFuncSetAttribute(zp::k_policy_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(sizeof(zp::SmemTc))),
                "cudaFuncSetAttribute(policy tc)");
@@ -1307,6 +1680,7 @@ ZSIM_API int zsim_policy_destroy(zsim_policy* p) {
         if (!p) return;
         cudaSetDevice(p->device);
         cudaFree(p->blob);
+        cudaFree(p->pooled);
         delete p;
     });
 }
@@ -1333,8 +1707,20 @@ ZSIM_API int zsim_policy_act(zsim_policy* p, const zsim_obs_view* obs, int32_t b
         a.logits = logits;
         const cudaStream_t s = static_cast<cudaStream_t>(stream);
         if (p->precision == 0) {
+            if (p->pooled_cap < batch) {
+                // grows outside any stream order: the first call at a new size synchronises
+                ccheck(cudaDeviceSynchronize(), "policy scratch");
+                cudaFree(p->pooled);
+                p->pooled = nullptr;
+                p->pooled_cap = 0;
+                ccheck(cudaMalloc(&p->pooled, size_t(batch) * zp::kD * sizeof(float)), "cudaMalloc(policy scratch)");
+                p->pooled_cap = batch;
+            }
+            a.pooled = p->pooled;
             const int grid = (batch + zp::kRowsTc - 1) / zp::kRowsTc;
             zp::k_policy_tc<<<grid, zp::kThreads, sizeof(zp::SmemTc), s>>>(a);
+            const int hgrid = (batch + zp::kHeadRows - 1) / zp::kHeadRows;
+            zp::k_policy_heads<<<hgrid, zp::kHeadThreads, sizeof(zp::SmemHeads), s>>>(a);
         } else {
             const int grid = (batch + zp::kRows32 - 1) / zp::kRows32;
             zp::k_policy_fp32<<<grid, zp::kThreads, sizeof(zp::Smem32), s>>>(a);
