@@ -124,7 +124,7 @@ __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.f + erff(x
 // ---------------------------------------------------------------------------
 template <int R>
 struct RowSm {
-    float road[R][kRoad][kRoadF];  // scaled features (model.hpp:470-503)
+    alignas(16) float road[R][kRoad][kRoadF];  // scaled features (model.hpp:470-503)
     float route[R][kRoute][kRouteF];
     float act[R][kActF];
     float val[R][kValF];
@@ -391,7 +391,7 @@ __device__ void trunk_and_act(const RowSm<R>& in, TrunkSm<R>& sm, const ActArgs&
 // Folded cross attention of ONE query (one head) against a row's feature
 // tokens (null + N tokens of F scaled features, model.hpp:326-367): q is the
 // head's 64 query values, out receives the head's 64 output values.
-template <int F, int N>
+template <int F, int N, bool FAST>
 __device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* q, const float (*feat)[F],
                                             const unsigned char* mask, float* out) {
     const float scale = 0.125f;  // 1 / sqrt(64)
@@ -422,25 +422,36 @@ __device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* 
     for (int f = 0; f < F; ++f) ag[f] = 0.f;
     for (int j = 0; j < N; ++j) {
         if (!mask[j]) continue;
+        float x[F];
+        if constexpr (F % 4 == 0) {  // 16-B aligned rows: vector loads
+#pragma unroll
+            for (int f = 0; f < F; f += 4) {
+                const float4 t = *reinterpret_cast<const float4*>(&feat[j][f]);
+                x[f] = t.x, x[f + 1] = t.y, x[f + 2] = t.z, x[f + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int f = 0; f < F; ++f) x[f] = feat[j][f];
+        }
         float d = qn;
 #pragma unroll
-        for (int f = 0; f < F; ++f) d = fmaf(qf[f], feat[j][f], d);
+        for (int f = 0; f < F; ++f) d = fmaf(qf[f], x[f], d);
         d *= scale;
         if (d > mx) {
-            const float r = expf(mx - d);
+            const float r = FAST ? __expf(mx - d) : expf(mx - d);
             tot *= r;
             ps *= r;
 #pragma unroll
             for (int f = 0; f < F; ++f) ag[f] *= r;
             mx = d;
         }
-        const float e = expf(d - mx);
+        const float e = FAST ? __expf(d - mx) : expf(d - mx);
         tot += e;
         ps += e;
 #pragma unroll
-        for (int f = 0; f < F; ++f) ag[f] = fmaf(e, feat[j][f], ag[f]);
+        for (int f = 0; f < F; ++f) ag[f] = fmaf(e, x[f], ag[f]);
     }
-    const float en = expf(sn - mx);  // the null token's term, already inside tot (started as exp(0) = 1)
+    const float en = FAST ? __expf(sn - mx) : expf(sn - mx);  // the null token's term, already inside tot (started as exp(0) = 1)
     const float inv = 1.f / tot;
     ps *= inv;
     const float pn = en * inv;
@@ -545,7 +556,7 @@ __device__ void gemm32(const float (*A)[kLd], const float* __restrict__ W, const
 
 // Self attention (model.hpp:340-364) of each row's 17 latent tokens, one
 // thread per (token, head): keys / values of the row from smem.
-template <class KV>
+template <bool FAST, class KV>
 __device__ __forceinline__ void self_query(int h, const float* q, const unsigned char* mlat, KV kv, float* out,
                                            float* sc) {
     const float scale = 0.125f;
@@ -571,7 +582,7 @@ __device__ __forceinline__ void self_query(int h, const float* q, const unsigned
         if (mlat[j]) mx = fmaxf(mx, sc[j]);
     float tot = 0.f;
     for (int j = 0; j < kLat; ++j) {
-        const float e = mlat[j] ? expf(sc[j] - mx) : 0.f;
+        const float e = mlat[j] ? (FAST ? __expf(sc[j] - mx) : expf(sc[j] - mx)) : 0.f;
         sc[j] = e;
         tot += e;
     }
@@ -602,7 +613,7 @@ struct KV32 {
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_policy_fp32(const ActArgs a) {
-    extern __shared__ __align__(16) unsigned char dsm[];
+    extern __shared__ __align__(1024) unsigned char dsm[];
     Smem32& sm = *reinterpret_cast<Smem32*>(dsm);
     const PolicyW& W = a.w;
     const int tid = threadIdx.x;
@@ -622,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_fp32(const ActArgs a) {
     __syncthreads();
     if (tid < kRows32 * kLat * kHeads) {
         const int s = tid >> 1, h = tid & 1, g = s / kLat;
-        self_query(h, &sm.Q[s][h * kDh], sm.rs.mlat[g], KV32{sm.K, sm.V, g * kLat}, &sm.A[s][h * kDh], sm.sc[tid]);
+        self_query<false>(h, &sm.Q[s][h * kDh], sm.rs.mlat[g], KV32{sm.K, sm.V, g * kLat}, &sm.A[s][h * kDh], sm.sc[tid]);
     }
     __syncthreads();
     gemm32(sm.A, W.self.wo, W.self.bo, sm.X, true);
@@ -636,9 +647,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_fp32(const ActArgs a) {
         __syncthreads();
         if (tid < kRows32 * kLat * kHeads) {
             const int s = tid >> 1, h = tid & 1, g = s / kLat;
-            if (m == 0) cross_query<kRoadF, kRoad>(aw, h, &sm.Q[s][h * kDh], sm.rs.road[g], sm.rs.mroad[g], &sm.A[s][h * kDh]);
-            if (m == 1) cross_query<kRouteF, kRoute>(aw, h, &sm.Q[s][h * kDh], sm.rs.route[g], sm.rs.mroute[g], &sm.A[s][h * kDh]);
-            if (m == 2) cross_query<kActF, 1>(aw, h, &sm.Q[s][h * kDh], reinterpret_cast<const float(*)[kActF]>(sm.rs.act[g]), sm.rs.mact[g], &sm.A[s][h * kDh]);
+            if (m == 0) cross_query<kRoadF, kRoad, false>(aw, h, &sm.Q[s][h * kDh], sm.rs.road[g], sm.rs.mroad[g], &sm.A[s][h * kDh]);
+            if (m == 1) cross_query<kRouteF, kRoute, false>(aw, h, &sm.Q[s][h * kDh], sm.rs.route[g], sm.rs.mroute[g], &sm.A[s][h * kDh]);
+            if (m == 2) cross_query<kActF, 1, false>(aw, h, &sm.Q[s][h * kDh], reinterpret_cast<const float(*)[kActF]>(sm.rs.act[g]), sm.rs.mact[g], &sm.A[s][h * kDh]);
         }
         __syncthreads();
         gemm32(sm.A, aw.wo, aw.bo, sm.X, true);
@@ -982,7 +993,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
 #pragma unroll
         for (int i = 0; i < 64; ++i) q[i] += __ldg(W.self.bq + 64 * half + i);
         if (real) {
-            self_query(half, q, sm.rs.mlat[g], KVTc{sm.opA, sm.opW, g * kLat}, o, sm.sc[tid]);
+            self_query<true>(half, q, sm.rs.mlat[g], KVTc{sm.opA, sm.opW, g * kLat}, o, sm.sc[tid]);
         } else {
 #pragma unroll
             for (int i = 0; i < 64; ++i) o[i] = 0.f;
@@ -1008,9 +1019,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
 #pragma unroll
         for (int i = 0; i < 64; ++i) q[i] += __ldg(aw.bq + 64 * half + i);
         if (real) {
-            if (m == 0) cross_query<kRoadF, kRoad>(aw, half, q, sm.rs.road[g], sm.rs.mroad[g], o);
-            if (m == 1) cross_query<kRouteF, kRoute>(aw, half, q, sm.rs.route[g], sm.rs.mroute[g], o);
-            if (m == 2) cross_query<kActF, 1>(aw, half, q, reinterpret_cast<const float(*)[kActF]>(sm.rs.act[g]), sm.rs.mact[g], o);
+            if (m == 0) cross_query<kRoadF, kRoad, true>(aw, half, q, sm.rs.road[g], sm.rs.mroad[g], o);
+            if (m == 1) cross_query<kRouteF, kRoute, true>(aw, half, q, sm.rs.route[g], sm.rs.mroute[g], o);
+            if (m == 2) cross_query<kActF, 1, true>(aw, half, q, reinterpret_cast<const float(*)[kActF]>(sm.rs.act[g]), sm.rs.mact[g], o);
         } else {
 #pragma unroll
             for (int i = 0; i < 64; ++i) o[i] = 0.f;
@@ -1055,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
 // tcgen05.mma.kind::tf32 (M = 128 rows, N = 128, K = 128 or 128 + ve).
 // ===========================================================================
 constexpr int kHeadRows = 128;
-constexpr int kHeadThreads = 128;
+constexpr int kHeadThreads = 512;   // 4 threads per row: warp w owns TMEM lanes 32 (w % 4), columns 32 (w / 4)
 constexpr int kMaxK = kD + kMaxVE;  // value.in's K
 // TMEM columns: trunk activation H [0,128), products D [128,256), pooled P [256,384)
 constexpr uint32_t kHColH = 0, kHColD = 128, kHColP = 256;
@@ -1065,25 +1076,26 @@ struct SmemHeads {
     float opW[kD * kMaxK];
     float hw[2 * kMaxHead][kD];    // accel / steer head weights, row-major [out][k]
     float vhead[kD];
+    float red[4][kHeadRows];       // LayerNorm partial sums of the four column quarters
+    float red2[4][kHeadRows];
     unsigned long long mbar_w, mbar_mma;
     uint32_t tmem_base;
 };
 
-// canonical offset for an M x K tile with K-chunk stride M/8 * 128 B (M = N = 128 here)
-__device__ __forceinline__ void heads_put(float* opA, int row, int k0, const float* v, int n) {
-    for (int q = 0; q < n / 4; ++q) {
-        const int k = k0 + 4 * q;
-        uint4 u = make_uint4(to_tf32(v[4 * q]), to_tf32(v[4 * q + 1]), to_tf32(v[4 * q + 2]), to_tf32(v[4 * q + 3]));
-        *reinterpret_cast<uint4*>(opA + canon_off(row, k)) = u;
-    }
-}
-
 struct HeadsCtx {
     SmemHeads& sm;
     uint32_t tmem, lane_base;
-    int row;
+    int row, c0;  // this thread's row (TMEM lane) and first column (32 columns)
     uint32_t ph_w = 0, ph_mma = 0;
     __device__ uint32_t col(uint32_t c) const { return tmem + lane_base + c; }
+    __device__ void put(const float* v, int k0) {  // 32 values at columns k0.. of this row, tf32 canonical
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint4 u = make_uint4(to_tf32(v[4 * q]), to_tf32(v[4 * q + 1]), to_tf32(v[4 * q + 2]),
+                                       to_tf32(v[4 * q + 3]));
+            *reinterpret_cast<uint4*>(sm.opA + canon_off(row, k0 + 4 * q)) = u;
+        }
+    }
     __device__ void load_w(const float* src, uint32_t bytes) {
         if (threadIdx.x == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1126,29 +1138,28 @@ struct HeadsCtx {
         ph_mma ^= 1;
         tc_fence_after();
     }
-    // LayerNorm (model.hpp:287-303) of this row's H into opA
+    // LayerNorm (model.hpp:287-303) of this row's H into opA; the four column
+    // quarters of a row combine their partial sums through smem
     __device__ void ln_to_a(const float* g, const float* b) {
+        const int qt = c0 >> 5;
         float v[32];
+        tmem_ld32(col(kHColH + c0), v);
         float s = 0.f;
-        for (int c = 0; c < kD; c += 32) {
-            tmem_ld32(col(kHColH + c), v);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) s += v[i];
-        }
-        const float mu = s / float(kD);
+        for (int i = 0; i < 32; ++i) s += v[i];
+        sm.red[qt][row] = s;
+        __syncthreads();
+        const float mu = ((sm.red[0][row] + sm.red[1][row]) + (sm.red[2][row] + sm.red[3][row])) / float(kD);
         float q = 0.f;
-        for (int c = 0; c < kD; c += 32) {
-            tmem_ld32(col(kHColH + c), v);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) q += (v[i] - mu) * (v[i] - mu);
-        }
-        const float rstd = 1.f / sqrtf(q / float(kD) + 1e-5f);
-        for (int c = 0; c < kD; c += 32) {
-            tmem_ld32(col(kHColH + c), v);
+        for (int i = 0; i < 32; ++i) q += (v[i] - mu) * (v[i] - mu);
+        sm.red2[qt][row] = q;
+        __syncthreads();
+        const float var = ((sm.red2[0][row] + sm.red2[1][row]) + (sm.red2[2][row] + sm.red2[3][row])) / float(kD);
+        const float rstd = 1.f / sqrtf(var + 1e-5f);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = (v[i] - mu) * rstd * __ldg(g + c + i) + __ldg(b + c + i);
-            heads_put(sm.opA, row, c, v, 32);
-        }
+        for (int i = 0; i < 32; ++i) v[i] = (v[i] - mu) * rstd * __ldg(g + c0 + i) + __ldg(b + c0 + i);
+        put(v, c0);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     // mlp_forward (model.hpp:431-440): H += W2 gelu(W1 LN(H) + b1) + b2
@@ -1159,23 +1170,19 @@ struct HeadsCtx {
         mma(kHColD, kD);
         load_w(w2_tc, kD * kD * 4);
         float v[32];
-        for (int c = 0; c < kD; c += 32) {
-            tmem_ld32(col(kHColD + c), v);
+        tmem_ld32(col(kHColD + c0), v);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = gelu(v[i] + __ldg(w.b1 + c + i));
-            heads_put(sm.opA, row, c, v, 32);
-        }
+        for (int i = 0; i < 32; ++i) v[i] = gelu(v[i] + __ldg(w.b1 + c0 + i));
+        put(v, c0);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         wait_w();
         mma(kHColD, kD);
         float h[32];
-        for (int c = 0; c < kD; c += 32) {
-            tmem_ld32(col(kHColD + c), v);
-            tmem_ld32(col(kHColH + c), h);
+        tmem_ld32(col(kHColD + c0), v);
+        tmem_ld32(col(kHColH + c0), h);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) h[i] += v[i] + __ldg(w.b2 + c + i);
-            tmem_st32(col(kHColH + c), h);
-        }
+        for (int i = 0; i < 32; ++i) h[i] += v[i] + __ldg(w.b2 + c0 + i);
+        tmem_st32(col(kHColH + c0), h);
     }
 };
 
@@ -1184,7 +1191,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs 
     SmemHeads& sm = *reinterpret_cast<SmemHeads*>(dsm);
     const PolicyW& W = a.w;
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int b = blockIdx.x * kHeadRows + tid;
+    const int row = (warp & 3) * 32 + (tid & 31), c0 = (warp >> 2) * 32;
+    const int b = blockIdx.x * kHeadRows + row;
     const bool live = b < a.B;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem_base)));
@@ -1204,24 +1212,27 @@ __global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    HeadsCtx cx{sm, sm.tmem_base, uint32_t(warp * 32) << 16, tid};
+    HeadsCtx cx{sm, sm.tmem_base, uint32_t((warp & 3) * 32) << 16, row, c0};
 
     // pooled encoding -> H and P
     {
         float v[32];
-        for (int c = 0; c < kD; c += 32) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = live ? a.pooled[size_t(b) * kD + c + i] : 0.f;
-            tmem_st32(cx.col(kHColH + c), v);
-            tmem_st32(cx.col(kHColP + c), v);
+        for (int i = 0; i < 32; i += 4) {
+            const float4 t = live ? *reinterpret_cast<const float4*>(a.pooled + size_t(b) * kD + c0 + i)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[i] = t.x, v[i + 1] = t.y, v[i + 2] = t.z, v[i + 3] = t.w;
         }
+        tmem_st32(cx.col(kHColH + c0), v);
+        tmem_st32(cx.col(kHColP + c0), v);
     }
-    // ---- policy trunk + heads (model.hpp:556-568) ----
+    // ---- policy trunk (model.hpp:556-562) ----
 #pragma unroll
     for (int i = 0; i < kMaxTrunk; ++i)
         if (i < W.trunk) cx.mlp(W.pblk[i], W.tc_pblk[2 * i], W.tc_pblk[2 * i + 1]);
+    // ---- heads (model.hpp:563-568): the row's quarter-0 thread, all 128 columns ----
     float logit[2 * kMaxHead];
-    {
+    if (c0 == 0) {
         for (int o = 0; o < na + ns; ++o) logit[o] = o < na ? __ldg(W.acc_b + o) : __ldg(W.str_b + o - na);
         float v[32];
         for (int c = 0; c < kD; c += 32) {
@@ -1234,30 +1245,30 @@ __global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs 
             }
         }
     }
-    // ---- value trunk (model.hpp:570-584) ----
+    // ---- value trunk (model.hpp:570-584): concat [pooled; gelu(W_e v + b_e)] ----
     cx.load_w(W.tc_vin, uint32_t(kD * (kD + W.ve) * 4));
     {
         float v[32];
-        for (int c = 0; c < kD; c += 32) {
-            tmem_ld32(cx.col(kHColP + c), v);
-            heads_put(sm.opA, tid, c, v, 32);
-        }
-        // value embedding gelu(W_e v + b_e), ve <= 64 columns after the pooled ones
-        float vf[kValF];
+        tmem_ld32(cx.col(kHColP + c0), v);
+        cx.put(v, c0);
+        // value embedding, 32 columns per quarter (ve <= 64, a multiple of 8)
+        if (c0 < W.ve) {
+            float vf[kValF];
 #pragma unroll
-        for (int f = 0; f < kValF; ++f) vf[f] = live ? a.obs.value_only[size_t(b) * kValF + f] * c_val_scale[f] : 0.f;
-        for (int c = 0; c < W.ve; c += 32) {
-            const int n = W.ve - c < 32 ? W.ve - c : 32;
+            for (int f = 0; f < kValF; ++f)
+                vf[f] = live ? a.obs.value_only[size_t(b) * kValF + f] * c_val_scale[f] : 0.f;
+            const int n = W.ve - c0 < 32 ? W.ve - c0 : 32;
+#pragma unroll
             for (int i = 0; i < 32; ++i) {
                 float acc = 0.f;
                 if (i < n) {
 #pragma unroll
-                    for (int f = 0; f < kValF; ++f) acc = fmaf(__ldg(W.vemb_w + f * W.ve + c + i), vf[f], acc);
-                    acc = gelu(acc + __ldg(W.vemb_b + c + i));
+                    for (int f = 0; f < kValF; ++f) acc = fmaf(__ldg(W.vemb_w + f * W.ve + c0 + i), vf[f], acc);
+                    acc = gelu(acc + __ldg(W.vemb_b + c0 + i));
                 }
                 v[i] = acc;
             }
-            heads_put(sm.opA, tid, kD + c, v, (n + 3) / 4 * 4);
+            cx.put(v, kD + c0);  // columns past ve land in K padding the MMA does not read
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -1265,18 +1276,16 @@ __global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs 
     cx.mma(kHColD, kD + W.ve);
     {
         float v[32];
-        for (int c = 0; c < kD; c += 32) {
-            tmem_ld32(cx.col(kHColD + c), v);
+        tmem_ld32(cx.col(kHColD + c0), v);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += __ldg(W.vin_b + c + i);
-            tmem_st32(cx.col(kHColH + c), v);
-        }
+        for (int i = 0; i < 32; ++i) v[i] += __ldg(W.vin_b + c0 + i);
+        tmem_st32(cx.col(kHColH + c0), v);
     }
 #pragma unroll
     for (int i = 0; i < kMaxTrunk; ++i)
         if (i < W.trunk) cx.mlp(W.vblk[i], W.tc_vblk[2 * i], W.tc_vblk[2 * i + 1]);
     float value = __ldg(W.vhead_b);
-    {
+    if (c0 == 0) {
         float v[32];
         for (int c = 0; c < kD; c += 32) {
             tmem_ld32(cx.col(kHColH + c), v);
@@ -1287,7 +1296,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs 
     tc_fence_before();
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(sm.tmem_base));
-    if (!live) return;
+    if (!live || c0 != 0) return;
     // ---- NNPolicy::act (policy.hpp:33-56) ----
     if (a.logits) {
         for (int i = 0; i < na + ns; ++i) a.logits[size_t(b) * (na + ns) + i] = logit[i];
