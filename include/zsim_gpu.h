@@ -427,6 +427,15 @@ ZSIM_API int zsim_policy_destroy(zsim_policy* policy);
  * cores (the reference's Model<float> arithmetic).  Everything else is fp32
  * in both modes. */
 ZSIM_API int zsim_policy_set_precision(zsim_policy* policy, int32_t mode);
+/* Env::rollout(NNPolicy, horizon, seed) (simcore.cpp:554-618 with
+ * train/policy.hpp:27-58) entirely on the device: per step observe -> policy
+ * (argmax or sampling with the rows' rng streams) -> step, recording every
+ * EpisodeBatch field (logp / value from the policy) into `ep`; the bootstrap
+ * is the policy's value on the final observation.  `obs` / `final_state` as
+ * zsim_rollout.  Stream-ordered, graph-capturable after one warm-up call. */
+ZSIM_API int zsim_rollout_policy(zsim_env* env, zsim_policy* policy, int32_t use_argmax, uint64_t seed,
+                                 int32_t horizon, const zsim_episode_view* ep, const zsim_obs_view* obs,
+                                 const zsim_state_view* final_state, void* stream);
 /* NNPolicy::act (train/policy.hpp:27-58) on device buffers: obs rows [0, batch)
  * of a device observation view; rng [batch] is the per-row stream
  * (SimStateBatch::rng), advanced in place when sampling (unused for argmax).

@@ -173,6 +173,8 @@ SIGNATURES = {
     "zsim_policy_create": (C.c_int, [C.POINTER(ModelConfigC), c_float_p, C.c_int64, C.c_int32, C.POINTER(_P)]),
     "zsim_policy_destroy": (C.c_int, [_P]),
     "zsim_policy_set_precision": (C.c_int, [_P, C.c_int32]),
+    "zsim_rollout_policy": (C.c_int, [_P, _P, C.c_int32, C.c_uint64, C.c_int32, C.POINTER(EpisodeView),
+                                      C.POINTER(ObsView), C.POINTER(StateView), _P]),
     "zsim_policy_act": (C.c_int, [_P, C.POINTER(ObsView), C.c_int32, _P, C.c_int32, _P, _P, _P, _P, _P, _P]),
 }
 

@@ -197,6 +197,7 @@ struct zsim_env {
     double* d_initial_s = nullptr;
     double* d_logged = nullptr;          // logged_progress (device rollout recording)
     void* roll_buf = nullptr;            // zsim_rollout scratch: two states + one observation
+    void* pol_buf = nullptr;             // zsim_rollout_policy scratch: accel, steer, logp, value [B]
     zsim_state_view roll_s[2]{};
     zsim_obs_view roll_obs{};
     zsim_stepout_view roll_so{};
@@ -1205,6 +1206,7 @@ ZSIM_API int zsim_env_destroy(zsim_env* env) {
         cudaFree(env->d_initial_s);
         cudaFree(env->d_logged);
         cudaFree(env->roll_buf);
+        cudaFree(env->pol_buf);
         cudaFree(env->d_metrics_scratch);
         cudaFree(env->d_hint);
         delete env;
@@ -1651,6 +1653,83 @@ ZSIM_API int zsim_rollout(zsim_env* env, uint64_t seed, int32_t horizon, const i
             a = args_for(env);
             a.in = env->roll_s[cur];
             a.ep = *ep;
+            cuda_check(zs::launch_episode_finalize(a, env->d_initial_s, env->d_logged, s), "episode finalize");
+        }
+        if (final_state) copy_state(env, final_state, &env->roll_s[cur], 2, s);
+    });
+}
+
+ZSIM_API int zsim_rollout_policy(zsim_env* env, zsim_policy* policy, int32_t use_argmax, uint64_t seed,
+                                 int32_t horizon, const zsim_episode_view* ep, const zsim_obs_view* obs,
+                                 const zsim_state_view* final_state, void* stream) {
+    return guarded([&] {
+        check_view(env, "rollout_policy");
+        if (!policy) raise(Err::invalid_argument, "rollout_policy: null policy");
+        if (horizon <= 0) raise(Err::invalid_argument, "rollout_policy: horizon must be > 0");
+        if (ep) {
+            check_episode(env, ep, "rollout_policy");
+            if (ep->horizon != horizon) raise(Err::invalid_argument, "rollout_policy: episode horizon mismatch");
+        }
+        set_device(env);
+        ensure_host_arrays(env);
+        if (!env->roll_buf) {
+            cuda_check(cudaMalloc(&env->roll_buf, 2 * env->sl.bytes + env->ol.bytes + env->sol.bytes),
+                       "cudaMalloc(rollout scratch)");
+            unsigned char* p = static_cast<unsigned char*>(env->roll_buf);
+            carve_state(p, env->sl, &env->roll_s[0]);
+            carve_state(p + env->sl.bytes, env->sl, &env->roll_s[1]);
+            carve_obs(p + 2 * env->sl.bytes, env->ol, &env->roll_obs);
+            carve_stepout(p + 2 * env->sl.bytes + env->ol.bytes, env->sol, &env->roll_so);
+        }
+        const size_t nb = al(size_t(env->B) * 4);
+        if (!env->pol_buf) cuda_check(cudaMalloc(&env->pol_buf, 4 * nb), "cudaMalloc(policy rollout scratch)");
+        unsigned char* pb = static_cast<unsigned char*>(env->pol_buf);
+        int32_t* pa = reinterpret_cast<int32_t*>(pb);
+        int32_t* ps = reinterpret_cast<int32_t*>(pb + nb);
+        float* plogp = reinterpret_cast<float*>(pb + 2 * nb);
+        float* pvalue = reinterpret_cast<float*>(pb + 3 * nb);
+        cudaStream_t s = as_stream(stream);
+        zs::KernelArgs a = args_for(env);
+        a.seed = seed;
+        a.out = env->roll_s[0];
+        cuda_check(zs::launch_reset(a, env->grid, s), "reset kernel");
+        a = args_for(env);
+        a.in = env->roll_s[0];
+        a.obs = obs ? obs[0] : env->roll_obs;
+        cuda_check(zs::launch_step_observe(a, zs::kModeObserve, env->launch_policy, s), "observe kernel");
+        auto act = [&](const zsim_obs_view* o, const zsim_state_view& st) {
+            // NNPolicy::act on obs[t] with the rows' rng streams (simcore.cpp:591)
+            if (zsim_policy_act(policy, o, env->B, st.rng, use_argmax, pa, ps, plogp, pvalue, nullptr, stream) !=
+                ZSIM_OK)
+                raise(Err::runtime, std::string("rollout_policy: ") + g_last_error);
+        };
+        int cur = 0;
+        for (int t = 0; t < horizon; ++t) {
+            act(obs ? &obs[t] : &env->roll_obs, env->roll_s[cur]);
+            a = args_for(env);
+            a.in = env->roll_s[cur];
+            a.out = env->roll_s[cur ^ 1];
+            a.accel = pa;
+            a.steer = ps;
+            a.act_len = -2;
+            a.pol_logp = plogp;
+            a.pol_value = pvalue;
+            a.so = env->roll_so;
+            if (ep) {
+                a.ep = *ep;
+                a.ep_t = t;
+            }
+            a.obs = obs ? obs[t + 1] : env->roll_obs;
+            cuda_check(zs::launch_step_observe(a, zs::kModeStepObserve, env->launch_policy, s), "step+observe kernel");
+            cur ^= 1;
+        }
+        // the final observation's value is the bootstrap (simcore.cpp:609-613)
+        act(obs ? &obs[horizon] : &env->roll_obs, env->roll_s[cur]);
+        if (ep) {
+            a = args_for(env);
+            a.in = env->roll_s[cur];
+            a.ep = *ep;
+            a.final_value = pvalue;
             cuda_check(zs::launch_episode_finalize(a, env->d_initial_s, env->d_logged, s), "episode finalize");
         }
         if (final_state) copy_state(env, final_state, &env->roll_s[cur], 2, s);

@@ -1396,7 +1396,8 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
 }
 
 // EpisodeBatch cell (b, a.ep_t) of Env::rollout's recording loop
-// (simcore.cpp:596-608); the scripted policy's logp and value are 0.
+// (simcore.cpp:596-608); logp and value from the policy's output (0 for the
+// scripted policy).
 __device__ __forceinline__ void record_step(const KernelArgs& a, int b, int mask, int ai, int si, float reward,
                                             float s, float a_lat, float a_lon, float v, int done) {
     if (!a.ep.reward) return;
@@ -1404,8 +1405,8 @@ __device__ __forceinline__ void record_step(const KernelArgs& a, int b, int mask
     a.ep.mask[k] = uint8_t(mask);
     a.ep.accel_idx[k] = ai;
     a.ep.steer_idx[k] = si;
-    a.ep.logp[k] = 0.f;
-    a.ep.value[k] = 0.f;
+    a.ep.logp[k] = a.pol_logp ? a.pol_logp[b] : 0.f;
+    a.ep.value[k] = a.pol_value ? a.pol_value[b] : 0.f;
     a.ep.reward[k] = reward;
     a.ep.s[k] = s;
     a.ep.a_lat[k] = a_lat;
@@ -1438,7 +1439,10 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     if (REC && a.act_len != 0) {
         // ScriptedPolicy::act (simcore.cpp:69-84): the script at the row's t, else the zero action
         const int tt = rs.r0.t;
-        if (a.act_len > 0 && tt >= 0 && tt < a.act_len) {
+        if (a.act_len == -2) {  // NNPolicy output of this step, every row (done rows still pass through)
+            ai = a.accel[b];
+            si = a.steer[b];
+        } else if (a.act_len > 0 && tt >= 0 && tt < a.act_len) {
             ai = a.accel[size_t(tt) * pk.d.B + b];
             si = a.steer[size_t(tt) * pk.d.B + b];
         } else {
@@ -1719,7 +1723,7 @@ __global__ void __launch_bounds__(256) k_episode_stats(const KernelArgs a, const
 __global__ void __launch_bounds__(256) k_episode_finalize(const KernelArgs a, const double* initial_s,
                                                           const double* logged) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < a.pk.d.B; b += gridDim.x * blockDim.x) {
-        a.ep.bootstrap[b] = 0.f;
+        a.ep.bootstrap[b] = a.in.done[b] || !a.final_value ? 0.f : a.final_value[b];  // simcore.cpp:612
         a.ep.terminal[b] = a.in.reason[b];
         a.ep.events[b] = a.in.events[b];
         a.ep.initial_s[b] = float(initial_s[b]);

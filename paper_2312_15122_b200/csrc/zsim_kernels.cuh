@@ -42,7 +42,11 @@ struct KernelArgs {
     // device rollout (zsim_rollout): recording target and scripted actions
     zsim_episode_view ep;  // ep.reward == nullptr: no recording
     int32_t ep_t;          // rollout step being recorded
-    int32_t act_len;       // > 0: accel/steer are a [act_len][B] script read at state.t (ScriptedPolicy); -1: empty
+    int32_t act_len;       // > 0: accel/steer are a [act_len][B] script read at state.t (ScriptedPolicy); -1: empty;
+                           // -2: accel/steer [B] are this step's policy output (NNPolicy), recorded for every row
+    const float* pol_logp;   // policy rollout: this step's logp / value [B] to record (null: 0, ScriptedPolicy)
+    const float* pol_value;
+    const float* final_value;  // episode finalize: bootstrap value [B] (null: 0)
     int32_t zero_accel, zero_steer;
     int32_t row_lo, row_hi;  // rows [row_lo, row_hi) of the batch; row_hi == 0: all rows
 };

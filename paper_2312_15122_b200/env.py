@@ -482,6 +482,19 @@ class Env:
                                C.byref(episode.v) if episode is not None else None, ov,
                                C.byref(final_state.v) if final_state is not None else None, _stream(stream)))
 
+    def rollout_policy_device(self, policy, seed: int, horizon: int, episode: DeviceEpisode | None = None,
+                              obs: list | None = None, final_state: DeviceState | None = None, stream=None) -> None:
+        """Env::rollout(NNPolicy) on the device (zsim_rollout_policy): the
+        policy (paper_2312_15122_b200.NNPolicy) acts on every observation with
+        the rows' rng streams; `obs` / `final_state` as rollout_device."""
+        ov = None
+        if obs is not None:
+            assert len(obs) == horizon + 1
+            ov = (ObsView * (horizon + 1))(*[o.v for o in obs])
+        check(lib.zsim_rollout_policy(self.handle, policy.handle, int(policy.argmax), C.c_uint64(seed), int(horizon),
+                                      C.byref(episode.v) if episode is not None else None, ov,
+                                      C.byref(final_state.v) if final_state is not None else None, _stream(stream)))
+
     def download_episode(self, ep: DeviceEpisode) -> dict:
         """Host copy of a device EpisodeBatch: [B][T] and [B] numpy arrays."""
         B, T = self.info.batch, ep.v.horizon

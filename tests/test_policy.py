@@ -175,3 +175,65 @@ def test_policy_errors():
     with pytest.raises(z.ZsimError) as e:
         z.NNPolicy(z.ModelConfig(), p[:-1])
     assert e.value.kind == "invalid_argument"
+
+
+def _oracle_env(zsim, cfg):
+    from oracle import portpy, refpy
+    return refpy.RefEnv(zsim, config=cfg) if refpy.available() else portpy.PortEnv(zsim, config=cfg)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("use_argmax", [True, False])
+def test_policy_rollout_matches_oracle_loop(use_argmax):
+    """zsim_rollout_policy = Env::rollout with NNPolicy (simcore.cpp:554-618,
+    train/policy.hpp:27-58) against the oracle loop observe -> act -> step
+    (the reference Env + the float64 policy oracle).  fp32 precision; a row is
+    compared up to the first step whose policy decision margin is below 1e-4
+    (past a legitimately flipped near-tie the trajectories diverge)."""
+    import torch
+
+    import paper_2312_15122_b200 as z
+    zsim = z.stress_scenarios(z.StressConfig(count=6, agents=12, road_points=600), seed=4)
+    cfg = z.SimConfig(disable_dones=False)
+    env = z.Env(zsim, config=cfg, device=0)
+    cfg_o = po.ModelConfig()
+    params = po.init_params(cfg_o, 9)
+    pol = z.NNPolicy(z.ModelConfig(), params, use_argmax=use_argmax, precision="fp32")
+    H, B = 12, 6
+    ep = env.device_episode(H)
+    env.rollout_policy_device(pol, 42, H, episode=ep)
+    torch.cuda.synchronize()
+    got = env.download_episode(ep)
+
+    ref = _oracle_env(zsim, cfg)
+    model = po.Model(cfg_o, params)
+    st = ref.init_state(42)
+    live = np.ones(B, bool)
+    for t in range(H):
+        o = ref.observe(st)
+        obs = {k: getattr(o, k) for k in ("active", "agents", "road", "route", "value_only")}
+        out = po.act(model, obs, st.rng, use_argmax)
+        for b in range(B):
+            if live[b] and not (margins_ok(out["logits_accel"][b], out["u"][b][0], use_argmax, 1e-4) and
+                                margins_ok(out["logits_steer"][b], out["u"][b][1], use_argmax, 1e-4)):
+                live[b] = False
+        st.rng[:] = out["rng"]
+        mask = 1 - st.done.astype(np.int32)
+        nst, so = ref.step(st, out["accel"], out["steer"])
+        for b in np.nonzero(live)[0]:
+            assert got["accel_idx"][b, t] == out["accel"][b] and got["steer_idx"][b, t] == out["steer"][b], (b, t)
+            assert got["mask"][b, t] == mask[b] and got["done"][b, t] == nst.done[b], (b, t)
+            assert abs(got["logp"][b, t] - out["logp"][b]) < 2e-5, (b, t)
+            assert abs(got["value"][b, t] - out["value"][b]) < 1e-5 + 1e-4 * abs(out["value"][b]), (b, t)
+            for f in ("reward", "s", "v"):
+                np.testing.assert_allclose(got[f][b, t], getattr(so, f)[b], rtol=1e-5, atol=1e-6)
+        st = nst
+    assert live.sum() >= B // 2
+    # bootstrap = the policy's value on the final observation (0 for done rows)
+    o = ref.observe(st)
+    out = po.act(model, {k: getattr(o, k) for k in ("active", "agents", "road", "route", "value_only")}, st.rng,
+                 use_argmax)
+    for b in np.nonzero(live)[0]:
+        want = 0.0 if st.done[b] else out["value"][b]
+        assert abs(got["bootstrap"][b] - want) < 1e-5 + 1e-4 * abs(want)
+        assert got["terminal"][b] == st.reason[b] and got["events"][b] == st.events[b]
