@@ -386,6 +386,10 @@ def run_ours(args) -> None:
                "d2h_bytes_per_step": d2h, "steps": ke,
                "path": "Env.step + Env.observe host-vector API (zsim_step_host / zsim_observe_host), pinned buffers"}
 
+    policy = None
+    if rank == 0 and not args.no_policy and not controlled:
+        policy = measure_policy(env, ob, B, A_)
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -432,6 +436,8 @@ def run_ours(args) -> None:
     }
     if e2e:
         line["e2e"] = e2e
+    if policy:
+        line["policy"] = policy
     if clk:
         line["clocks"] = clk
     if world == 1 and not args.no_cpu_baseline:
@@ -441,6 +447,62 @@ def run_ours(args) -> None:
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def measure_policy(env, ob, B, A_):
+    """SURVEY 8f row 4: NNPolicy::act on the device (tcgen05 tf32 projections)
+    over the batch's observations, and the closed simulate -> act loop
+    (zsim_rollout_policy, 91 steps) -- reported beside the headline metric."""
+    import torch
+
+    import paper_2312_15122_b200 as z
+    cfg = z.ModelConfig()
+    pol = z.NNPolicy(cfg, z.init_params(cfg, 1), use_argmax=False, precision="tf32")
+    stream = torch.cuda.current_stream()
+    rng = torch.arange(B, dtype=torch.int64, device="cuda")
+    acc = torch.zeros(B, dtype=torch.int32, device="cuda")
+    ste = torch.zeros_like(acc)
+    lp = torch.zeros(B, dtype=torch.float32, device="cuda")
+    val = torch.zeros_like(lp)
+
+    def act():
+        pol.act_device(ob, B, rng.data_ptr(), acc.data_ptr(), ste.data_ptr(), lp.data_ptr(), val.data_ptr(),
+                       stream=stream)
+    for _ in range(3):
+        act()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = 20
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(n):
+        act()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    env.rollout_policy_device(pol, 42, EPISODE, stream=stream)  # warm-up
+    torch.cuda.synchronize()
+    e0.record(stream)
+    env.rollout_policy_device(pol, 42, EPISODE, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    loop_ms = e0.elapsed_time(e1)
+    # tensor-core work per row: 10 token-tile projections (17 tokens x 128 x 128)
+    # + the trunks (4 x 2 MLP matrices, value.in 160 -> 128), 2 flops per MAC
+    tc_flops = (10 * 17 + 8) * 128 * 128 * 2 + 160 * 128 * 2
+    peak_tf32 = None
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        peak_tf32 = float(json.loads(p.read_text())["bf16_tflops"]) / 2  # tf32 dense rate is half of bf16
+    achieved = tc_flops * B / (ms / 1e3) / 1e12
+    return {"precision": "tf32 projections on tcgen05, fp32 elsewhere", "rows": B, "ms_per_act": ms,
+            "rows_per_s": B / (ms / 1e3),
+            "closed_loop": {"path": "zsim_rollout_policy: observe -> NNPolicy::act -> step, 91 steps, sampling",
+                            "ms": loop_ms, "agent_steps_per_s": B * A_ * EPISODE / (loop_ms / 1e3)},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf32, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf32 if peak_tf32 else None,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (tf32)",
+                         "note": "the folded cross attention and the LayerNorm / softmax work run on the FP32 "
+                                 "pipe and dominate the kernel time; the fraction is of the tf32 tensor peak"}}
 
 
 def main():
@@ -453,6 +515,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph rollouts")
+    ap.add_argument("--no-policy", action="store_true", help="skip the on-device policy measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
