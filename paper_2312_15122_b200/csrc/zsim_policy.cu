@@ -149,12 +149,20 @@ struct TrunkSm {
 template <int R>
 __device__ void load_row_inputs(RowSm<R>& sm, const ActArgs& a, int b0) {
     const int tid = threadIdx.x;
-    for (int e = tid; e < R * kRoad * kRoadF; e += kThreads) {
-        const int g = e / (kRoad * kRoadF), r = e % (kRoad * kRoadF);
-        const int b = b0 + g;
-        const float v = b < a.B ? a.obs.road[size_t(b) * kRoad * kRoadF + r] : 0.f;
-        sm.road[g][r / kRoadF][r % kRoadF] = v * c_rd_scale[r % kRoadF];
-        if (r % kRoadF == kRoadF - 1) sm.mroad[g][r / kRoadF] = v > 0.5f;
+    for (int e = tid; e < R * kRoad; e += kThreads) {  // one road token (3 x float4) per thread
+        const int g = e / kRoad, j = e % kRoad, b = b0 + g;
+        const float4* src = reinterpret_cast<const float4*>(a.obs.road + (size_t(b) * kRoad + j) * kRoadF);
+        float4* dst = reinterpret_cast<float4*>(sm.road[g][j]);
+        float4 last = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < kRoadF / 4; ++q) {
+            float4 v = b < a.B ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            last = v;
+            v.x *= c_rd_scale[4 * q], v.y *= c_rd_scale[4 * q + 1], v.z *= c_rd_scale[4 * q + 2],
+                v.w *= c_rd_scale[4 * q + 3];
+            dst[q] = v;
+        }
+        sm.mroad[g][j] = last.w > 0.5f;  // raw valid feature (model.hpp:536 valid_at 11)
     }
     for (int e = tid; e < R * kRoute * kRouteF; e += kThreads) {
         const int g = e / (kRoute * kRouteF), r = e % (kRoute * kRouteF);
@@ -415,41 +423,52 @@ __device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* 
     }
     sn *= scale;
     // one pass, running maximum (the softmax is shift-invariant; every
-    // accumulated term is rescaled when the maximum moves)
+    // accumulated term is rescaled when the maximum moves), tokens in blocks
+    // of TB so the scores of a block are independent chains
     float mx = sn, tot = 1.f, ps = 0.f;
     float ag[F];
 #pragma unroll
     for (int f = 0; f < F; ++f) ag[f] = 0.f;
-    for (int j = 0; j < N; ++j) {
-        if (!mask[j]) continue;
-        float x[F];
-        if constexpr (F % 4 == 0) {  // 16-B aligned rows: vector loads
+    constexpr int TB = N % 4 == 0 ? 4 : 1;
+    for (int j0 = 0; j0 < N; j0 += TB) {
+        float x[TB][F], d[TB];
+        float bm = -INFINITY;
 #pragma unroll
-            for (int f = 0; f < F; f += 4) {
-                const float4 t = *reinterpret_cast<const float4*>(&feat[j][f]);
-                x[f] = t.x, x[f + 1] = t.y, x[f + 2] = t.z, x[f + 3] = t.w;
+        for (int u = 0; u < TB; ++u) {
+            const int j = j0 + u;
+            if constexpr (F % 4 == 0) {  // 16-B aligned rows: vector loads
+#pragma unroll
+                for (int f = 0; f < F; f += 4) {
+                    const float4 t = *reinterpret_cast<const float4*>(&feat[j][f]);
+                    x[u][f] = t.x, x[u][f + 1] = t.y, x[u][f + 2] = t.z, x[u][f + 3] = t.w;
+                }
+            } else {
+#pragma unroll
+                for (int f = 0; f < F; ++f) x[u][f] = feat[j][f];
             }
-        } else {
+            float dd = qn;
 #pragma unroll
-            for (int f = 0; f < F; ++f) x[f] = feat[j][f];
+            for (int f = 0; f < F; ++f) dd = fmaf(qf[f], x[u][f], dd);
+            d[u] = mask[j] ? dd * scale : -INFINITY;
+            bm = fmaxf(bm, d[u]);
         }
-        float d = qn;
-#pragma unroll
-        for (int f = 0; f < F; ++f) d = fmaf(qf[f], x[f], d);
-        d *= scale;
-        if (d > mx) {
-            const float r = FAST ? __expf(mx - d) : expf(mx - d);
+        if (bm > mx) {
+            const float r = FAST ? __expf(mx - bm) : expf(mx - bm);
             tot *= r;
             ps *= r;
 #pragma unroll
             for (int f = 0; f < F; ++f) ag[f] *= r;
-            mx = d;
+            mx = bm;
         }
-        const float e = FAST ? __expf(d - mx) : expf(d - mx);
-        tot += e;
-        ps += e;
 #pragma unroll
-        for (int f = 0; f < F; ++f) ag[f] = fmaf(e, x[f], ag[f]);
+        for (int u = 0; u < TB; ++u) {
+            // masked tokens: exp(-inf) = 0 exactly
+            const float e = FAST ? __expf(d[u] - mx) : expf(d[u] - mx);
+            tot += e;
+            ps += e;
+#pragma unroll
+            for (int f = 0; f < F; ++f) ag[f] = fmaf(e, x[u][f], ag[f]);
+        }
     }
     const float en = FAST ? __expf(sn - mx) : expf(sn - mx);  // the null token's term, already inside tot (started as exp(0) = 1)
     const float inv = 1.f / tot;
