@@ -387,6 +387,40 @@ ZSIM_API int zsim_step_host(zsim_env* env, const zsim_state_view* in_host, const
 ZSIM_API int zsim_observe_host(zsim_env* env, const zsim_state_view* in_host, const zsim_obs_view* obs_host);
 
 
+/* train::cut_sequences (train/replay.cpp:8-52) output: every sequence is
+ * `seq_len` steps (TransitionSequence, train/replay.hpp:14-26); padded steps
+ * are zero with mask 0.  obs has capacity * seq_len rows ([seq][k]); the
+ * per-step arrays are [capacity][seq_len]; `row` is the episode row b of the
+ * sequence (its scenario), `t0` its first step; `count` (device int32) is the
+ * number of sequences written. */
+typedef struct zsim_sequences_view {
+    int32_t capacity;
+    int32_t seq_len;
+    zsim_obs_view obs;
+    int32_t* accel_idx;
+    int32_t* steer_idx;
+    float* logmu;
+    float* reward;
+    uint8_t* done;
+    uint8_t* mask;
+    float* bootstrap; /* [capacity] */
+    int32_t* row;     /* [capacity] */
+    int32_t* t0;      /* [capacity] */
+    int32_t* count;   /* [1] */
+} zsim_sequences_view;
+
+/* Device buffers for up to batch * ceil(horizon / seq_len) sequences. */
+ZSIM_API int zsim_sequences_alloc(zsim_env* env, int32_t horizon, int32_t seq_len, zsim_sequences_view* out);
+ZSIM_API int zsim_sequences_free(zsim_env* env, zsim_sequences_view* seq);
+/* cut_sequences(ep, seq_len) (train/replay.cpp:8-52) on the device: `ep` a
+ * recorded device EpisodeBatch, `obs` its horizon observation views
+ * (obs[t] precedes step t, as zsim_rollout records them).  Sequences come in
+ * the reference's order (row-major, then t0); a row stops at its first
+ * masked window start.  ZSIM_INVALID_ARGUMENT for seq_len <= 0 (as the
+ * reference) or an undersized output.  Stream-ordered. */
+ZSIM_API int zsim_cut_sequences(zsim_env* env, const zsim_episode_view* ep, const zsim_obs_view* obs,
+                                int32_t seq_len, const zsim_sequences_view* out, void* stream);
+
 /* ---- on-device policy inference ------------------
  * NNPolicy::act (train/policy.hpp:27-58) over forward_row
  * (nn/model.hpp:464-585): the perceiver-style encoder (self attention over

@@ -27,7 +27,7 @@ PORT_OUT = HERE / "_build" / "libzsim_oracle.so"
 NLOHMANN = Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
 
 REF_UNITS = ["common", "config", "geometry", "dynamics", "roads", "scenario_io", "scenario_gen", "simcore",
-             "metrics"]
+             "metrics", "train/replay"]
 CXX = os.environ.get("CXX", "g++")
 
 
@@ -96,7 +96,7 @@ def build_dropin(force: bool = False) -> Path | None:
     deps = [src, lib, HERE.parent / "include" / "zsim_gpu.hpp", HERE.parent / "include" / "zsim_gpu.h"]
     if not force and DROPIN_OUT.exists() and all(d.stat().st_mtime <= DROPIN_OUT.stat().st_mtime for d in deps):
         return DROPIN_OUT
-    objs = [str(HERE / "_ref" / "obj" / f"{u}.o") for u in REF_UNITS]
+    objs = [str(HERE / "_ref" / "obj" / f"{Path(u).name}.o") for u in REF_UNITS]
     tmp = DROPIN_OUT.with_suffix(".tmp")
     _run([CXX, "-std=c++20", "-O2", "-ffp-contract=off", "-I", str(REF_SRC), "-I", str(NLOHMANN), "-I",
           str(HERE.parent / "include"), "-o", str(tmp), str(src), *objs, str(lib),

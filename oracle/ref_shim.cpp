@@ -19,6 +19,7 @@
 #include "../include/zsim_gpu.h"
 #include "core/common.hpp"
 #include "core/metrics.hpp"
+#include "core/train/replay.hpp"
 #include "core/scenario.hpp"
 #include "core/scenario_gen.hpp"
 #include "core/simcore.hpp"
@@ -416,6 +417,53 @@ __attribute__((visibility("default"))) int zref_bench(const char* path, int32_t 
         double mx = 0.0;
         for (auto& s : shards) mx = std::max(mx, s.secs);
         *seconds = mx;
+    });
+}
+
+// Env::rollout(ScriptedPolicy) then train::cut_sequences(ep, seq_len)
+// (replay.cpp:8-52): sequences in the reference's order; `row` is the batch
+// row whose scenario id the sequence carries.  Arrays sized for `cap`
+// sequences ([cap][seq_len] steps; obs [cap * seq_len] rows).
+__attribute__((visibility("default"))) int zref_rollout_cut(
+    zref_env* e, int32_t horizon, int32_t script_len, const int32_t* accel, const int32_t* steer, uint64_t seed,
+    int32_t seq_len, int32_t cap, int32_t* count, int32_t* row, float* bootstrap, int32_t* o_accel,
+    int32_t* o_steer, float* o_logmu, float* o_reward, uint8_t* o_done, uint8_t* o_mask, float* o_active,
+    float* o_agents, float* o_road, float* o_route, float* o_value) {
+    return guarded([&] {
+        const int B = e->env->batch_size();
+        std::vector<std::vector<std::pair<int32_t, int32_t>>> script(static_cast<size_t>(B));
+        for (int b = 0; b < B; ++b)
+            for (int t = 0; t < script_len; ++t)
+                script[size_t(b)].emplace_back(accel[size_t(b) * script_len + t], steer[size_t(b) * script_len + t]);
+        const auto& tab = e->env->action_table();
+        sim::ScriptedPolicy pol(std::move(script), tab.nearest_accel(0.0), tab.nearest_steer(0.0));
+        sim::EpisodeBatch ep = e->env->rollout(pol, horizon, seed);
+        std::vector<train::TransitionSequence> seqs = train::cut_sequences(ep, seq_len);
+        if (int(seqs.size()) > cap) zsim::fail(zsim::ErrorKind::invalid_argument, "zref_rollout_cut: cap too small");
+        *count = int32_t(seqs.size());
+        int cursor = 0;
+        for (size_t i = 0; i < seqs.size(); ++i) {
+            const auto& q = seqs[i];
+            while (cursor < B && ep.scenario_ids[size_t(cursor)] != q.scenario_id) ++cursor;
+            row[i] = cursor;
+            bootstrap[i] = q.bootstrap;
+            const auto& sp = q.obs.spec;
+            for (int k = 0; k < seq_len; ++k) {
+                const size_t o = i * size_t(seq_len) + size_t(k);
+                o_accel[o] = q.accel_idx[size_t(k)];
+                o_steer[o] = q.steer_idx[size_t(k)];
+                o_logmu[o] = q.logmu[size_t(k)];
+                o_reward[o] = q.reward[size_t(k)];
+                o_done[o] = q.done[size_t(k)];
+                o_mask[o] = q.mask[size_t(k)];
+            }
+            const size_t r0 = i * size_t(seq_len);
+            std::copy(q.obs.active.begin(), q.obs.active.end(), o_active + r0 * sim::ObsSpec::active_feat);
+            std::copy(q.obs.agents.begin(), q.obs.agents.end(), o_agents + r0 * size_t(sp.n_agents) * 6);
+            std::copy(q.obs.road.begin(), q.obs.road.end(), o_road + r0 * size_t(sp.n_road) * 12);
+            std::copy(q.obs.route.begin(), q.obs.route.end(), o_route + r0 * size_t(sp.n_route) * 5);
+            std::copy(q.obs.value_only.begin(), q.obs.value_only.end(), o_value + r0 * 2);
+        }
     });
 }
 

@@ -43,6 +43,11 @@ _SIGS = {
                      + [C.POINTER(C.c_uint8)] * 2 + [C.POINTER(C.c_float), C.POINTER(C.c_uint8),
                                                      C.POINTER(C.c_uint8), C.POINTER(C.c_float),
                                                      C.POINTER(C.c_float)]),
+    "zref_rollout_cut": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_uint64,
+                                   C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                   C.POINTER(C.c_float), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                   C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_uint8),
+                                   C.POINTER(C.c_uint8)] + [C.POINTER(C.c_float)] * 5),
     "zref_bench": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(SimConfigC), C.c_int32, C.c_int32,
                              C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_uint64,
                              C.POINTER(C.c_double)]),
@@ -175,6 +180,38 @@ class RefEnv:
             P("terminal", C.c_uint8), P("events", C.c_uint8), P("initial_s", C.c_float),
             P("logged_progress", C.c_float)))
         return o
+
+
+def _rollout_cut(self, horizon: int, accel, steer, seq_len: int, seed: int = 42) -> dict:
+    """Env::rollout(ScriptedPolicy) then train::cut_sequences (replay.cpp:8-52)
+    in the REFERENCE: the written sequences as numpy arrays."""
+    B = self.batch
+    a = np.ascontiguousarray(accel, dtype=np.int32)
+    s = np.ascontiguousarray(steer, dtype=np.int32)
+    L = a.shape[1]
+    cap = B * ((horizon + seq_len - 1) // seq_len)
+    cnt = np.zeros(1, np.int32)
+    o = {"row": np.zeros(cap, np.int32), "bootstrap": np.zeros(cap, np.float32),
+         "accel_idx": np.zeros((cap, seq_len), np.int32), "steer_idx": np.zeros((cap, seq_len), np.int32),
+         "logmu": np.zeros((cap, seq_len), np.float32), "reward": np.zeros((cap, seq_len), np.float32),
+         "done": np.zeros((cap, seq_len), np.uint8), "mask": np.zeros((cap, seq_len), np.uint8),
+         "obs_active": np.zeros((cap, seq_len, 9), np.float32),
+         "obs_agents": np.zeros((cap, seq_len, self._config.n_agents, 6), np.float32),
+         "obs_road": np.zeros((cap, seq_len, self._config.n_road, 12), np.float32),
+         "obs_route": np.zeros((cap, seq_len, self._config.n_route, 5), np.float32),
+         "obs_value_only": np.zeros((cap, seq_len, 2), np.float32)}
+    P = lambda k, ct: _ptr(o[k], ct)  # noqa: E731
+    _check(lib().zref_rollout_cut(
+        self.handle, int(horizon), int(L), _ptr(a, C.c_int32), _ptr(s, C.c_int32), C.c_uint64(seed), int(seq_len),
+        int(cap), _ptr(cnt, C.c_int32), P("row", C.c_int32), P("bootstrap", C.c_float), P("accel_idx", C.c_int32),
+        P("steer_idx", C.c_int32), P("logmu", C.c_float), P("reward", C.c_float), P("done", C.c_uint8),
+        P("mask", C.c_uint8), P("obs_active", C.c_float), P("obs_agents", C.c_float), P("obs_road", C.c_float),
+        P("obs_route", C.c_float), P("obs_value_only", C.c_float)))
+    n = int(cnt[0])
+    return {"count": n, **{k: v[:n] for k, v in o.items()}}
+
+
+RefEnv.rollout_cut = _rollout_cut
 
 
 def validate(zsim, index: int) -> str:

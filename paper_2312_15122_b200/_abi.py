@@ -76,6 +76,13 @@ class EpisodeView(C.Structure):
                 ("logged_progress", c_float_p), ("horizon", C.c_int32), ("reserved", C.c_int32)]
 
 
+class SequencesView(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("seq_len", C.c_int32), ("obs", ObsView), ("accel_idx", c_int32_p),
+                ("steer_idx", c_int32_p), ("logmu", c_float_p), ("reward", c_float_p), ("done", c_uint8_p),
+                ("mask", c_uint8_p), ("bootstrap", c_float_p), ("row", c_int32_p), ("t0", c_int32_p),
+                ("count", c_int32_p)]
+
+
 class ScoreBounds(C.Structure):
     _fields_ = [("progress", C.c_double), ("collision", C.c_double), ("off_route", C.c_double),
                 ("stop_line", C.c_double), ("traffic_light", C.c_double), ("comfort", C.c_double)]
@@ -173,6 +180,10 @@ SIGNATURES = {
     "zsim_policy_create": (C.c_int, [C.POINTER(ModelConfigC), c_float_p, C.c_int64, C.c_int32, C.POINTER(_P)]),
     "zsim_policy_destroy": (C.c_int, [_P]),
     "zsim_policy_set_precision": (C.c_int, [_P, C.c_int32]),
+    "zsim_sequences_alloc": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(SequencesView)]),
+    "zsim_sequences_free": (C.c_int, [_P, C.POINTER(SequencesView)]),
+    "zsim_cut_sequences": (C.c_int, [_P, C.POINTER(EpisodeView), C.POINTER(ObsView), C.c_int32,
+                                     C.POINTER(SequencesView), _P]),
     "zsim_rollout_policy": (C.c_int, [_P, _P, C.c_int32, C.c_uint64, C.c_int32, C.POINTER(EpisodeView),
                                       C.POINTER(ObsView), C.POINTER(StateView), _P]),
     "zsim_policy_act": (C.c_int, [_P, C.POINTER(ObsView), C.c_int32, _P, C.c_int32, _P, _P, _P, _P, _P, _P]),

@@ -198,6 +198,8 @@ struct zsim_env {
     double* d_logged = nullptr;          // logged_progress (device rollout recording)
     void* roll_buf = nullptr;            // zsim_rollout scratch: two states + one observation
     void* pol_buf = nullptr;             // zsim_rollout_policy scratch: accel, steer, logp, value [B]
+    void* seq_buf = nullptr;             // zsim_cut_sequences scratch: offsets [B + 1] + obs views [T]
+    size_t seq_cap = 0;
     zsim_state_view roll_s[2]{};
     zsim_obs_view roll_obs{};
     zsim_stepout_view roll_so{};
@@ -1207,6 +1209,7 @@ ZSIM_API int zsim_env_destroy(zsim_env* env) {
         cudaFree(env->d_logged);
         cudaFree(env->roll_buf);
         cudaFree(env->pol_buf);
+        cudaFree(env->seq_buf);
         cudaFree(env->d_metrics_scratch);
         cudaFree(env->d_hint);
         delete env;
@@ -1579,6 +1582,84 @@ ZSIM_API int zsim_episode_free(zsim_env* env, zsim_episode_view* ep) {
         set_device(env);
         cudaFree(ep->accel_idx);
         std::memset(ep, 0, sizeof(*ep));
+    });
+}
+
+ZSIM_API int zsim_sequences_alloc(zsim_env* env, int32_t horizon, int32_t seq_len, zsim_sequences_view* out) {
+    return guarded([&] {
+        check_view(env, "sequences_alloc");
+        check_view(out, "sequences_alloc");
+        if (horizon <= 0 || seq_len <= 0) raise(Err::invalid_argument, "sequences_alloc: horizon and seq_len must be > 0");
+        set_device(env);
+        const size_t cap = size_t(env->B) * size_t((horizon + seq_len - 1) / seq_len);
+        const size_t rows = cap * size_t(seq_len);
+        const ObsLayout ol = obs_layout(int(rows), env->cfg.n_agents, env->cfg.n_road, env->cfg.n_route);
+        const size_t steps = al(rows * 4);
+        const size_t bytes = ol.bytes + 4 * steps + 2 * al(rows) + 3 * al(cap * 4) + 256;
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(sequences)");
+        cuda_check(cudaMemset(p, 0, bytes), "cudaMemset(sequences)");
+        unsigned char* q = static_cast<unsigned char*>(p);
+        zsim_sequences_view v{};
+        v.capacity = int32_t(cap);
+        v.seq_len = seq_len;
+        carve_obs(q, ol, &v.obs);
+        q += ol.bytes;
+        v.accel_idx = reinterpret_cast<int32_t*>(q), q += steps;
+        v.steer_idx = reinterpret_cast<int32_t*>(q), q += steps;
+        v.logmu = reinterpret_cast<float*>(q), q += steps;
+        v.reward = reinterpret_cast<float*>(q), q += steps;
+        v.done = q, q += al(rows);
+        v.mask = q, q += al(rows);
+        v.bootstrap = reinterpret_cast<float*>(q), q += al(cap * 4);
+        v.row = reinterpret_cast<int32_t*>(q), q += al(cap * 4);
+        v.t0 = reinterpret_cast<int32_t*>(q), q += al(cap * 4);
+        v.count = reinterpret_cast<int32_t*>(q);
+        *out = v;
+    });
+}
+
+ZSIM_API int zsim_sequences_free(zsim_env* env, zsim_sequences_view* seq) {
+    return guarded([&] {
+        if (!env || !seq) return;
+        set_device(env);
+        cudaFree(seq->obs.active);
+        std::memset(seq, 0, sizeof(*seq));
+    });
+}
+
+ZSIM_API int zsim_cut_sequences(zsim_env* env, const zsim_episode_view* ep, const zsim_obs_view* obs,
+                                int32_t seq_len, const zsim_sequences_view* out, void* stream) {
+    return guarded([&] {
+        check_view(env, "cut_sequences");
+        check_episode(env, ep, "cut_sequences");
+        check_view(obs, "cut_sequences");
+        check_view(out, "cut_sequences");
+        // replay.cpp:9
+        if (seq_len <= 0) raise(Err::invalid_argument, "cut_sequences: seq_len must be > 0");
+        const int T = ep->horizon, B = env->B;
+        if (out->seq_len != seq_len || size_t(out->capacity) < size_t(B) * size_t((T + seq_len - 1) / seq_len))
+            raise(Err::invalid_argument, "cut_sequences: output buffers too small for this episode / seq_len");
+        set_device(env);
+        const size_t need = al(size_t(B + 1) * 4) + size_t(T) * sizeof(zsim_obs_view);
+        if (env->seq_cap < need) {
+            cuda_check(cudaDeviceSynchronize(), "sync");
+            cudaFree(env->seq_buf);
+            env->seq_buf = nullptr;
+            env->seq_cap = 0;
+            cuda_check(cudaMalloc(&env->seq_buf, need), "cudaMalloc(sequence scratch)");
+            env->seq_cap = need;
+        }
+        cudaStream_t s = as_stream(stream);
+        unsigned char* q = static_cast<unsigned char*>(env->seq_buf);
+        auto* off = reinterpret_cast<int32_t*>(q);
+        auto* dviews = reinterpret_cast<zsim_obs_view*>(q + al(size_t(B + 1) * 4));
+        cuda_check(cudaMemcpyAsync(dviews, obs, size_t(T) * sizeof(zsim_obs_view), cudaMemcpyHostToDevice, s),
+                   "upload observation views");
+        cuda_check(zs::launch_cut_sequences(B, T, seq_len, *ep, dviews, *out, env->cfg.n_agents, env->cfg.n_road,
+                                            env->cfg.n_route, off, s),
+                   "cut_sequences kernels");
+        // (a pageable H2D copy returns once the caller's view array is staged: it may be freed on return)
     });
 }
 

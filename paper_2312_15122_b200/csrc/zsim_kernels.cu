@@ -28,6 +28,7 @@
 // expression rounds like the reference compiled with -ffp-contract=off.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <mutex>
 #include <vector>
@@ -1994,6 +1995,113 @@ static int metrics_blocks(int B) {
 }
 
 int metrics_scratch_doubles(int B) { return metrics_blocks(B) * kAggLen; }
+
+// ---------------------------------------------------------------------------
+// train::cut_sequences (replay.cpp:8-52)
+// ---------------------------------------------------------------------------
+// Row b yields one sequence per window start t0 = 0, L, 2L, ... until the
+// first masked start (mask is 1 up to the row's first done step, then 0).
+__global__ void k_seq_count(int B, int T, int L, const uint8_t* mask, int32_t* n) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+        int c = 0;
+        for (int t0 = 0; t0 < T && mask[size_t(b) * T + t0]; t0 += L) ++c;
+        n[b] = c;
+    }
+}
+
+// exclusive scan of n[0..B) in place into offsets, n[B] = total (one CTA,
+// each thread a contiguous chunk: deterministic)
+__global__ void __launch_bounds__(1024) k_seq_scan(int B, int32_t* n, int32_t* count) {
+    __shared__ int32_t part[1024];
+    const int t = threadIdx.x, per = (B + 1023) / 1024;
+    const int lo = min(B, t * per), hi = min(B, lo + per);
+    int32_t s = 0;
+    for (int i = lo; i < hi; ++i) s += n[i];
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const int32_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int32_t run = part[t] - s;
+    for (int i = lo; i < hi; ++i) {
+        const int32_t c = n[i];
+        n[i] = run;
+        run += c;
+    }
+    if (t == 1023) {
+        n[B] = part[1023];
+        *count = part[1023];
+    }
+}
+
+__device__ __forceinline__ void warp_copy(float* dst, const float* src, int n, bool zero) {
+    for (int i = lane_id(); i < n; i += 32) dst[i] = zero ? 0.f : src[i];
+}
+
+// one warp per row b: its sequences, step by step (TransitionSequence fill,
+// replay.cpp:14-49; padded steps stay zero with mask 0)
+__global__ void k_seq_fill(int B, int T, int L, const zsim_episode_view ep, const zsim_obs_view* obs,
+                           const zsim_sequences_view out, int ka, int kr, int kl, const int32_t* off) {
+    const int wpb = blockDim.x / 32;
+    for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < B; b += gridDim.x * wpb) {
+        const int s0 = off[b], ns = off[b + 1] - s0;
+        for (int w = 0; w < ns; ++w) {
+            const int s = s0 + w, t0 = w * L;
+            bool terminated = false;
+            bool live = true;
+            for (int k = 0; k < L; ++k) {
+                const int t = t0 + k;
+                const size_t src = size_t(b) * T + t;
+                live = live && t < T && ep.mask[src];
+                const size_t r = size_t(s) * L + k;  // output observation row
+                const int tt = live ? t : 0;
+                const zsim_obs_view& o = obs[tt];
+                warp_copy(out.obs.active + r * 9, o.active + size_t(b) * 9, 9, !live);
+                warp_copy(out.obs.agents + r * ka * 6, o.agents + size_t(b) * ka * 6, ka * 6, !live);
+                warp_copy(out.obs.road + r * kr * 12, o.road + size_t(b) * kr * 12, kr * 12, !live);
+                warp_copy(out.obs.route + r * kl * 5, o.route + size_t(b) * kl * 5, kl * 5, !live);
+                warp_copy(out.obs.value_only + r * 2, o.value_only + size_t(b) * 2, 2, !live);
+                if (lane_id() == 0) {
+                    const size_t q = size_t(s) * L + k;
+                    out.accel_idx[q] = live ? ep.accel_idx[src] : 0;
+                    out.steer_idx[q] = live ? ep.steer_idx[src] : 0;
+                    out.logmu[q] = live ? ep.logp[src] : 0.f;
+                    out.reward[q] = live ? ep.reward[src] : 0.f;
+                    out.done[q] = live ? ep.done[src] : 0;
+                    out.mask[q] = live ? 1 : 0;
+                }
+                if (live && ep.done[src]) terminated = true;
+            }
+            if (lane_id() == 0) {
+                const int next = t0 + L;
+                float bs;
+                if (terminated) {
+                    bs = 0.f;
+                } else if (next < T && ep.mask[size_t(b) * T + next]) {
+                    bs = ep.value[size_t(b) * T + next];  // behaviour value at the next state
+                } else {
+                    bs = ep.bootstrap[b];
+                }
+                out.bootstrap[s] = bs;
+                out.row[s] = b;
+                out.t0[s] = t0;
+            }
+        }
+    }
+}
+
+cudaError_t launch_cut_sequences(int B, int T, int L, const zsim_episode_view& ep, const zsim_obs_view* obs,
+                                 const zsim_sequences_view& out, int ka, int kr, int kl, int32_t* scratch,
+                                 cudaStream_t stream) {
+    const int g = std::min(4096, (B + 255) / 256);
+    k_seq_count<<<g, 256, 0, stream>>>(B, T, L, ep.mask, scratch);
+    k_seq_scan<<<1, 1024, 0, stream>>>(B, scratch, out.count);
+    k_seq_fill<<<std::min(8192, (B + 7) / 8), 256, 0, stream>>>(B, T, L, ep, obs, out, ka, kr, kl, scratch);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_episode_finalize(const KernelArgs& a, const double* initial_s, const double* logged,
                                     cudaStream_t stream) {

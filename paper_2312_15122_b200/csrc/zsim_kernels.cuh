@@ -65,5 +65,10 @@ cudaError_t launch_episode_metrics(const KernelArgs& a, const zsim_score_bounds&
                                    const zsim_comfort_weights& weights, const zsim_metric_view& rows, double* sums,
                                    double* scratch, cudaStream_t stream);
 int metrics_scratch_doubles(int B);
+// train::cut_sequences (replay.cpp:8-52): `obs` is a DEVICE array of T
+// observation views; `scratch` holds B + 1 int32 (per-row sequence offsets)
+cudaError_t launch_cut_sequences(int B, int T, int L, const zsim_episode_view& ep, const zsim_obs_view* obs,
+                                 const zsim_sequences_view& out, int ka, int kr, int kl, int32_t* scratch,
+                                 cudaStream_t stream);
 
 }  // namespace zs

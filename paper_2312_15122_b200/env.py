@@ -23,7 +23,8 @@ from pathlib import Path
 
 import numpy as np
 
-from ._abi import (ComfortWeights, EnvInfo, EpisodeView, MetricView, ObsView, ScoreBounds, SimConfigC, StateView,
+from ._abi import (ComfortWeights, EnvInfo, EpisodeView, MetricView, ObsView, ScoreBounds, SequencesView, SimConfigC,
+                   StateView,
                    StepOutView, StressConfigC, ZsimError, check, lib)
 
 DONE_REASONS = ("none", "collision", "off_route", "red_light", "stop_line", "goal_reached")
@@ -494,6 +495,41 @@ class Env:
         check(lib.zsim_rollout_policy(self.handle, policy.handle, int(policy.argmax), C.c_uint64(seed), int(horizon),
                                       C.byref(episode.v) if episode is not None else None, ov,
                                       C.byref(final_state.v) if final_state is not None else None, _stream(stream)))
+
+    def cut_sequences_device(self, ep: DeviceEpisode, obs: list, seq_len: int, stream=None) -> dict:
+        """train::cut_sequences (replay.cpp:8-52) of a recorded device episode
+        (zsim_cut_sequences); `obs` the episode's observation list as
+        rollout_device records it (obs[t] precedes step t).  Returns torch
+        CUDA tensors sized for the maximum sequence count ("count" holds the
+        number written): per-step [cap][L], obs_<modality> [cap][L][slot][feat],
+        bootstrap / row / t0 [cap]."""
+        import torch
+        T, B, L = ep.v.horizon, self.info.batch, int(seq_len)
+        assert len(obs) >= T
+        cap = B * ((T + L - 1) // L) if L > 0 else 0
+        cfg = self.config()
+        dev = torch.device("cuda", self.info.device)
+        t = {"accel_idx": torch.zeros(cap, L, dtype=torch.int32, device=dev),
+             "steer_idx": torch.zeros(cap, L, dtype=torch.int32, device=dev),
+             "logmu": torch.zeros(cap, L, device=dev), "reward": torch.zeros(cap, L, device=dev),
+             "done": torch.zeros(cap, L, dtype=torch.uint8, device=dev),
+             "mask": torch.zeros(cap, L, dtype=torch.uint8, device=dev),
+             "bootstrap": torch.zeros(cap, device=dev), "row": torch.zeros(cap, dtype=torch.int32, device=dev),
+             "t0": torch.zeros(cap, dtype=torch.int32, device=dev), "count": torch.zeros(1, dtype=torch.int32, device=dev),
+             "obs_active": torch.zeros(cap, L, 9, device=dev),
+             "obs_agents": torch.zeros(cap, L, cfg.n_agents, 6, device=dev),
+             "obs_road": torch.zeros(cap, L, cfg.n_road, 12, device=dev),
+             "obs_route": torch.zeros(cap, L, cfg.n_route, 5, device=dev),
+             "obs_value_only": torch.zeros(cap, L, 2, device=dev)}
+        v = SequencesView()
+        v.capacity, v.seq_len = cap, L
+        for f in ("active", "agents", "road", "route", "value_only"):
+            setattr(v.obs, f, C.cast(C.c_void_p(t["obs_" + f].data_ptr()), C.POINTER(C.c_float)))
+        for f in ("accel_idx", "steer_idx", "logmu", "reward", "done", "mask", "bootstrap", "row", "t0", "count"):
+            setattr(v, f, C.cast(C.c_void_p(t[f].data_ptr()), type(getattr(v, f))))
+        views = (ObsView * T)(*[o.v for o in obs[:T]])
+        check(lib.zsim_cut_sequences(self.handle, C.byref(ep.v), views, L, C.byref(v), _stream(stream)))
+        return t
 
     def download_episode(self, ep: DeviceEpisode) -> dict:
         """Host copy of a device EpisodeBatch: [B][T] and [B] numpy arrays."""

@@ -113,3 +113,42 @@ def test_device_metric_sums_match_host_statement():
     want = metric_sums_host(h["s"], h["a_lat"], h["a_lon"], h["mask"], h["events"], h["initial_s"],
                             h["logged_progress"], env.info.dt)
     np.testing.assert_allclose(sums, want, rtol=1e-12, atol=1e-12)
+
+
+@needs_ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("seq_len,dones", [(16, False), (10, True), (1, True), (91, True)])
+def test_cut_sequences_matches_reference(seq_len, dones):
+    """zsim_cut_sequences = train::cut_sequences (replay.cpp:8-52) over a
+    recorded device episode, against the REFERENCE's cut of its own rollout:
+    sequence count, order (row, t0), per-step actions / done / mask bit-exact,
+    logmu / reward / bootstrap / observations within the north_star tolerance."""
+    B, T = 12, 40
+    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=10, road_points=500), seed=21)
+    cfg = z.SimConfig(disable_dones=not dones)
+    env = z.Env(zsim, config=cfg, device=0)
+    A, S = z.random_actions(T, B, seed=17)
+    ep, ob = _device_rollout(env, T, A, S, obs=True)
+    got = env.cut_sequences_device(ep, ob, seq_len)
+    import torch
+    torch.cuda.synchronize()
+    n = int(got["count"].item())
+    ref = refpy.RefEnv(zsim, config=cfg).rollout_cut(T, A.T.copy(), S.T.copy(), seq_len)
+    assert n == ref["count"] and n > 0
+    g = {k: v[:n].cpu().numpy() for k, v in got.items() if k != "count"}
+    np.testing.assert_array_equal(g["row"], ref["row"])
+    for k in ("accel_idx", "steer_idx", "done", "mask"):
+        np.testing.assert_array_equal(g[k], ref[k], err_msg=k)
+    for k in ("logmu", "reward", "bootstrap", "obs_active", "obs_agents", "obs_road", "obs_route", "obs_value_only"):
+        np.testing.assert_allclose(g[k], ref[k], rtol=RTOL, atol=ATOL, err_msg=k)
+    assert (g["t0"] % seq_len == 0).all()
+
+
+@pytest.mark.gpu
+def test_cut_sequences_rejects_bad_seq_len():
+    env = z.Env(z.stress_scenarios(z.StressConfig(count=2, agents=4, road_points=100), seed=2), device=0)
+    A, S = z.random_actions(5, 2, seed=1)
+    ep, ob = _device_rollout(env, 5, A, S, obs=True)
+    with pytest.raises(z.ZsimError) as e:
+        env.cut_sequences_device(ep, ob, 0)
+    assert e.value.kind == "invalid_argument"
