@@ -169,8 +169,9 @@ inline SmemLayout warp_layout(int A, int cap, int ka, int ns) {
     size_t o = al16(sizeof(RowSh));  // warp-uniform row state
     const size_t u0 = o;
     auto put = [&](uint32_t& f, size_t bytes) { f = uint32_t(o), o += al16(bytes); };
-    put(L.agx, size_t(A) * 4 * 8);
-    put(L.agy, size_t(A) * 4 * 8);
+    const size_t AC = size_t(A < 32 ? A : 32);  // corner slots: one 32-agent chunk
+    put(L.agx, AC * 4 * 8);
+    put(L.agy, AC * 4 * 8);
     put(L.agd, size_t(A) * 8);
     put(L.agf, size_t(A) * 4);
     put(L.sel, size_t(ka) * 4);
@@ -604,12 +605,28 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size
     ab.s = cs.y;
     double X[4], Y[4];
     box_corners(ab, X, Y);
+    // corner slots hold one 32-agent chunk (lane = j mod 32); beyond 32 agents
+    // the observation recomputes each chunk's corners (agent_corners)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        w.agx[4 * j + k] = X[k];
-        w.agy[4 * j + k] = Y[k];
+        w.agx[4 * (j & 31) + k] = X[k];
+        w.agy[4 * (j & 31) + k] = Y[k];
     }
     return boxes_overlap(eb, EX, EY, ab, X, Y) ? 1 : 0;
+}
+// Corners of agent j at log slice `slice` (agent_box, simcore.cpp:162-165)
+// into its chunk slot, without the overlap test.
+__device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t slice, int j, double* agx, double* agy) {
+    const int A = pk.d.A;
+    Box ab;
+    ab.cx = double(pk.ag_x[slice + j]);
+    ab.cy = double(pk.ag_y[slice + j]);
+    ab.hl = double(pk.ag_len[size_t(sc) * A + j]) * 0.5;
+    ab.hw = double(pk.ag_wid[size_t(sc) * A + j]) * 0.5;
+    const double2 cs = pk.ag_cs[slice + j];
+    ab.c = cs.x;
+    ab.s = cs.y;
+    box_corners(ab, agx + 4 * (j & 31), agy + 4 * (j & 31));
 }
 
 // Agent boxes at one slice + overlap flags into w.agx/agy/agf for a row
@@ -1172,8 +1189,9 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const int j = j0 + lane;
         const int fl = j < na ? w.agf[j] : -1;
         if (fl == 0) {
-            const double* AX = w.agx + 4 * j;
-            const double* AY = w.agy + 4 * j;
+            if (na > 32) agent_corners(pk, sc, aslice, j, w.agx, w.agy);  // only one chunk of corners is kept
+            const double* AX = w.agx + 4 * (j & 31);
+            const double* AY = w.agy + 4 * (j & 31);
             float axf[4], ayf[4];
             float S = 0.f;
 #pragma unroll
