@@ -155,6 +155,7 @@ struct WarpBuf {
     int* cinfo;            // [cap] bucket << 16 | slot
     int* order;            // [cap] candidates grouped by bucket
     int* sel;              // [Ka] selected agents (road/route selections land in `order`)
+    int* alist;            // [A] bound keys, then the agents that survive the bound test (beyond 32 agents)
     unsigned char* sflag;  // [NS] pre-step stopped flags
 };
 
@@ -175,6 +176,7 @@ inline SmemLayout warp_layout(int A, int cap, int ka, int ns) {
     put(L.agd, size_t(A) * 8);
     put(L.agf, size_t(A) * 4);
     put(L.sel, size_t(ka) * 4);
+    put(L.alist, size_t(A) * 4);
     const size_t agents_end = o;
     o = u0;
     put(L.hist, cap > 0 ? 32 * 32 * 2 : 0);  // no top-k buffers in the step-only kernel (cap = 0)
@@ -198,6 +200,7 @@ __device__ __forceinline__ WarpBuf carve(unsigned char* base, const KernelArgs& 
     w.agd = reinterpret_cast<double*>(p + L.agd);
     w.agf = reinterpret_cast<int*>(p + L.agf);
     w.sel = reinterpret_cast<int*>(p + L.sel);
+    w.alist = reinterpret_cast<int*>(p + L.alist);
     w.hist = reinterpret_cast<unsigned short*>(p + L.hist);
     w.cidx = reinterpret_cast<int*>(p + L.cidx);
     w.ckey = reinterpret_cast<double*>(p + L.ckey);
@@ -616,7 +619,8 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size
 }
 // Corners of agent j at log slice `slice` (agent_box, simcore.cpp:162-165)
 // into its chunk slot, without the overlap test.
-__device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t slice, int j, double* agx, double* agy) {
+__device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t slice, int j, int slot, double* agx,
+                                              double* agy) {
     const int A = pk.d.A;
     Box ab;
     ab.cx = double(pk.ag_x[slice + j]);
@@ -626,7 +630,25 @@ __device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t 
     const double2 cs = pk.ag_cs[slice + j];
     ab.c = cs.x;
     ab.s = cs.y;
-    box_corners(ab, agx + 4 * (j & 31), agy + 4 * (j & 31));
+    box_corners(ab, agx + 4 * slot, agy + 4 * slot);
+}
+
+// k-th smallest (1-based) of the keys key[0..n) across the warp: MSB-first
+// radix select with warp-wide counts.  Uniform result.
+__device__ __forceinline__ unsigned warp_kth_key(const int* key, int n, int k) {
+    unsigned prefix = 0;
+#pragma unroll 1
+    for (int bit = 31; bit >= 0; --bit) {
+        const unsigned hi = prefix >> bit;  // the bits above, this bit 0
+        unsigned c = 0;
+        for (int j = lane_id(); j < n; j += 32) c += (unsigned(key[j]) >> bit) == hi ? 1u : 0u;
+        c = __reduce_add_sync(FULL, c);
+        if (unsigned(k) > c) {
+            k -= int(c);
+            prefix |= 1u << bit;
+        }
+    }
+    return prefix;
 }
 
 // Agent boxes at one slice + overlap flags into w.agx/agy/agf for a row
@@ -635,9 +657,26 @@ __device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t 
 __device__ __forceinline__ bool agent_boxes(const DevPack& pk, int sc, size_t slice, int na, int skip, bool t_ok, const Box& eb,
                                              const double* EX, const double* EY, const WarpBuf& w) {
     bool hit = false;
+    // beyond 32 agents the corners are not kept (the observation recomputes
+    // them), so agents whose circumscribed circles are apart skip the SAT
+    const double re2 = eb.hl * eb.hl + eb.hw * eb.hw;
     for (int j = lane_id(); j < na; j += 32) {
         int f = -1;
-        if (t_ok && j != skip && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
+        if (t_ok && j != skip && pk.ag_valid[slice + j]) {
+            bool apart = false;
+#ifdef ZS_NO_CIRCLE
+            if (false) {
+#else
+            if (na > 32) {
+#endif
+                const double dx = double(pk.ag_x[slice + j]) - eb.cx, dy = double(pk.ag_y[slice + j]) - eb.cy;
+                const double hl = double(pk.ag_len[size_t(sc) * pk.d.A + j]) * 0.5,
+                             hw = double(pk.ag_wid[size_t(sc) * pk.d.A + j]) * 0.5;
+                const double r = sqrt(re2) + sqrt(hl * hl + hw * hw);
+                apart = dx * dx + dy * dy > r * r * (1.0 + 1e-9) + 1e-9;
+            }
+            f = apart ? 0 : agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
+        }
         w.agf[j] = f;
         hit |= f == 1;
     }
@@ -1184,14 +1223,91 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         gyf[k] = float(GY[k] - ecy);
     }
     const float ge = float(2.0 * (rs.eb.hl + rs.eb.hw)) + 1e-3f;  // >= any ego edge length
-    int nvalid = 0;
-    for (int j0 = 0; j0 < na; j0 += 32) {
-        const int j = j0 + lane;
+    // Beyond 32 agents, agents that cannot be among the n_agents nearest are
+    // pruned before the exact distances.  Along the centre line u (centre
+    // distance D): the boxes' supports r(u) = hl |u.e1| + hw |u.e2| give
+    // D - r_e(u) - r_a(u) <= obb_distance (the separation along u), and the
+    // centre-line points still inside each box (reach t(u) = min(hl / |u.e1|,
+    // hw / |u.e2|)) give obb_distance <= max(0, D - t_e(u) - t_a(u)); margins
+    // cover the rounding.  An agent whose lower bound exceeds the Ka-th
+    // smallest upper bound is strictly farther than the Ka-th nearest, so it
+    // is never selected.
+    int nvalid = 0, nlist = na;
+    bool pruned = false;
+#ifdef ZS_NO_PRUNE
+    if (false) {
+#else
+    if (na > 32 && Ka <= 16) {
+#endif
+        // (lower, upper) bound on obb_distance of separate agent j, in fp32
+        // with margins (1e-4 + 1e-5 D) far above its rounding
+        const float ec = float(rs.eb.c), es = float(rs.eb.s), ehl = float(rs.eb.hl), ehw = float(rs.eb.hw);
+        auto bounds = [&](int j, float& lo, float& hi) {
+            const float dx = float(double(pk.ag_x[aslice + j]) - ecx), dy = float(double(pk.ag_y[aslice + j]) - ecy);
+            const float D = sqrtf(dx * dx + dy * dy);
+            const float m = 1e-4f + 1e-5f * D;
+            if (!(D > 1e-3f)) {
+                lo = 0.f, hi = m + 1e-3f;
+                return;
+            }
+            const float id = 1.f / D, ux = dx * id, uy = dy * id;
+            const double2 cs = pk.ag_cs[aslice + j];
+            const float ac = float(cs.x), as = float(cs.y);
+            const float ahl = pk.ag_len[size_t(sc) * A + j] * 0.5f, ahw = pk.ag_wid[size_t(sc) * A + j] * 0.5f;
+            const float e1 = fabsf(ux * ec + uy * es), e2 = fabsf(uy * ec - ux * es);
+            const float a1 = fabsf(ux * ac + uy * as), a2 = fabsf(uy * ac - ux * as);
+            const float te = fminf(e1 > 0.f ? ehl / e1 : INFINITY, e2 > 0.f ? ehw / e2 : INFINITY);
+            const float ta = fminf(a1 > 0.f ? ahl / a1 : INFINITY, a2 > 0.f ? ahw / a2 : INFINITY);
+            lo = D - (ehl * e1 + ehw * e2) - (ahl * a1 + ahw * a2) - m;
+            hi = fmaxf(0.f, D - te - ta) + m;
+        };
+        for (int j0 = 0; j0 < na; j0 += 32) {
+            const int j = j0 + lane;
+            const int fl = j < na ? w.agf[j] : -1;
+            unsigned key = 0xFFFFFFFFu;
+            if (fl == 1) {
+                key = 0u;
+            } else if (fl == 0) {
+                float lo, hi;
+                bounds(j, lo, hi);
+                key = __float_as_uint(hi);
+                w.agd[j] = double(lo);  // kept for the survivor test (agd is rewritten by the exact distances)
+            }
+            if (j < na) w.alist[j] = int(key);
+            nvalid += __popc(__ballot_sync(FULL, fl >= 0));
+        }
+        __syncwarp();
+        if (nvalid > Ka) {
+            const double U = double(__uint_as_float(warp_kth_key(w.alist, na, Ka)));
+            __syncwarp();
+            int n = 0;
+            for (int j0 = 0; j0 < na; j0 += 32) {
+                const int j = j0 + lane;
+                const int fl = j < na ? w.agf[j] : -1;
+                const bool keep = fl == 1 || (fl == 0 && w.agd[j] <= U);
+                const unsigned bal = __ballot_sync(FULL, keep);
+                if (keep) w.alist[n + __popc(bal & lanemask_lt())] = j;  // positions <= j: keys already consumed
+                n += __popc(bal);
+            }
+            __syncwarp();
+            nlist = n;
+            pruned = true;
+            PSTAT(17, n);
+            PSTAT(18, 1);
+        }
+    }
+    const int nv_all = nvalid;
+    nvalid = 0;
+    for (int k0 = 0; k0 < nlist; k0 += 32) {
+        const int k = k0 + lane;
+        const int j = pruned ? (k < nlist ? w.alist[k] : na) : k;
         const int fl = j < na ? w.agf[j] : -1;
         if (fl == 0) {
-            if (na > 32) agent_corners(pk, sc, aslice, j, w.agx, w.agy);  // only one chunk of corners is kept
-            const double* AX = w.agx + 4 * (j & 31);
-            const double* AY = w.agy + 4 * (j & 31);
+            // beyond 32 agents only one chunk of corners is kept: this lane's slot
+            const int slot = na > 32 ? lane : j;
+            if (na > 32) agent_corners(pk, sc, aslice, j, slot, w.agx, w.agy);
+            const double* AX = w.agx + 4 * slot;
+            const double* AY = w.agy + 4 * slot;
             float axf[4], ayf[4];
             float S = 0.f;
 #pragma unroll
@@ -1255,6 +1371,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         }
         nvalid += __popc(__ballot_sync(FULL, fl >= 0));
     }
+    if (pruned) nvalid = nv_all;  // every valid agent counts; at least Ka of them survived
     __syncwarp();
     ROW_MARK(b, 17);
     // order by (distance, index) among the valid agents: bitonic sorts across
@@ -1278,13 +1395,14 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         };
         unsigned long long bkey = 0xFFF0000000000000ull;
         int bidx = INT_MAX;
-        for (int j0 = 0; j0 < na; j0 += 32) {
-            const int j = j0 + lane;
+        for (int k0 = 0; k0 < nlist; k0 += 32) {
+            const int k = k0 + lane;
+            const int j = pruned ? (k < nlist ? w.alist[k] : na) : k;
             const bool ok = j < na && w.agf[j] >= 0;
             unsigned long long key = ok ? (unsigned long long)__double_as_longlong(w.agd[j]) : 0xFFF0000000000000ull;
             int idx = ok ? j : INT_MAX;
             sort32(key, idx);
-            if (j0 > 0) {
+            if (k0 > 0) {
                 // lanes 16-31 take this chunk's best 16, lanes 0-15 keep the running best
                 const unsigned long long ck = __shfl_sync(FULL, key, lane - 16);
                 const int ci = __shfl_sync(FULL, idx, lane - 16);

@@ -18,7 +18,7 @@ enum { kModeStep = 0, kModeObserve = 1, kModeStepObserve = 2 };
 // Per-warp shared-memory carve-up, byte offsets (computed on the host so the
 // kernels read them from the parameter bank instead of recomputing them).
 struct SmemLayout {
-    uint32_t agx, agy, agd, agf, sel;          // agent phase
+    uint32_t agx, agy, agd, agf, sel, alist;   // agent phase
     uint32_t hist, cidx, ckey, cinfo, order;                    // top-k phase (overlays the agent phase)
     uint32_t sflag, total;
 };

@@ -30,7 +30,8 @@ def main():
     B = int(args[0]) if args else 4096
     pathstats = "--pathstats" in sys.argv
     c2 = "--c2" in sys.argv  # C2 shapes: B scenarios x 128 controlled actors, 8k road points
-    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=128 if c2 else 32, road_points=8192 if c2 else 2048,
+    n_ag = int(next((a[9:] for a in sys.argv if a.startswith("--agents=")), "128" if c2 else "32"))
+    zsim = z.stress_scenarios(z.StressConfig(count=B, agents=n_ag, road_points=8192 if c2 or n_ag > 32 else 2048,
                                              flags=z.STRESS_C2 if c2 else 0), 7)
     env = z.Env(zsim, config=z.SimConfig(disable_dones=True), controlled=c2)
     B = env.info.batch
