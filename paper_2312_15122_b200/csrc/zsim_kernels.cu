@@ -633,12 +633,13 @@ __device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t 
     box_corners(ab, agx + 4 * slot, agy + 4 * slot);
 }
 
-// k-th smallest (1-based) of the keys key[0..n) across the warp: MSB-first
-// radix select with warp-wide counts.  Uniform result.
+// k-th smallest (1-based) of the keys' top 16 bits over key[0..n) across the
+// warp, as key bits (low 16 zero): MSB-first radix select with warp-wide
+// counts.  Uniform result.
 __device__ __forceinline__ unsigned warp_kth_key(const int* key, int n, int k) {
     unsigned prefix = 0;
 #pragma unroll 1
-    for (int bit = 31; bit >= 0; --bit) {
+    for (int bit = 31; bit >= 16; --bit) {  // top 16 bits (the caller rounds the result up)
         const unsigned hi = prefix >> bit;  // the bits above, this bit 0
         unsigned c = 0;
         for (int j = lane_id(); j < n; j += 32) c += (unsigned(key[j]) >> bit) == hi ? 1u : 0u;
@@ -651,33 +652,62 @@ __device__ __forceinline__ unsigned warp_kth_key(const int* key, int n, int k) {
     return prefix;
 }
 
+// Bounds on obb_distance (geometry.cpp:77-88) between the ego box and agent
+// j at log slice `slice`, in fp32 with margins (1e-4 + 1e-5 D) far above its
+// rounding.  Along the centre line u (centre distance D) the supports
+// r(u) = hl |u.e1| + hw |u.e2| give lo = D - r_e(u) - r_a(u) <= distance (the
+// separation along u; lo > 0 also proves the boxes apart), and the
+// centre-line points still inside each box (reach t(u) = min(hl / |u.e1|,
+// hw / |u.e2|)) give distance <= hi = max(0, D - t_e(u) - t_a(u)).
+__device__ __forceinline__ void agent_bounds(const DevPack& pk, int sc, size_t slice, int j, const Box& eb, float& lo,
+                                             float& hi) {
+    const float dx = float(double(pk.ag_x[slice + j]) - eb.cx), dy = float(double(pk.ag_y[slice + j]) - eb.cy);
+    const float D = sqrtf(dx * dx + dy * dy);
+    const float m = 1e-4f + 1e-5f * D;
+    if (!(D > 1e-3f)) {
+        lo = -m, hi = m + 1e-3f;
+        return;
+    }
+    const float id = 1.f / D, ux = dx * id, uy = dy * id;
+    const float ec = float(eb.c), es = float(eb.s), ehl = float(eb.hl), ehw = float(eb.hw);
+    const double2 cs = pk.ag_cs[slice + j];
+    const float ac = float(cs.x), as = float(cs.y);
+    const float ahl = pk.ag_len[size_t(sc) * pk.d.A + j] * 0.5f, ahw = pk.ag_wid[size_t(sc) * pk.d.A + j] * 0.5f;
+    const float e1 = fabsf(ux * ec + uy * es), e2 = fabsf(uy * ec - ux * es);
+    const float a1 = fabsf(ux * ac + uy * as), a2 = fabsf(uy * ac - ux * as);
+    const float te = fminf(e1 > 0.f ? ehl / e1 : INFINITY, e2 > 0.f ? ehw / e2 : INFINITY);
+    const float ta = fminf(a1 > 0.f ? ahl / a1 : INFINITY, a2 > 0.f ? ahw / a2 : INFINITY);
+    lo = D - (ehl * e1 + ehw * e2) - (ahl * a1 + ahw * a2) - m;
+    hi = fmaxf(0.f, D - te - ta) + m;
+}
+
 // Agent boxes at one slice + overlap flags into w.agx/agy/agf for a row
 // (-1 = invalid / skipped / t past the log); returns whether any overlaps.
 // (Inlined: a __noinline__ call forces the WarpBuf into local memory.)
 __device__ __forceinline__ bool agent_boxes(const DevPack& pk, int sc, size_t slice, int na, int skip, bool t_ok, const Box& eb,
                                              const double* EX, const double* EY, const WarpBuf& w) {
     bool hit = false;
-    // beyond 32 agents the corners are not kept (the observation recomputes
-    // them), so agents whose circumscribed circles are apart skip the SAT
-    const double re2 = eb.hl * eb.hl + eb.hw * eb.hw;
+    // Beyond 32 agents the corners are not kept (the observation recomputes
+    // them per chunk) and the distance bounds of the observation's pruning are
+    // computed here, in the same pass over the agents: lower bound into agd,
+    // upper-bound key into alist (0 for an overlap, ~0u for an invalid agent).
+    // A positive lower bound proves the boxes apart and skips the SAT.
     for (int j = lane_id(); j < na; j += 32) {
         int f = -1;
+        unsigned key = 0xFFFFFFFFu;
         if (t_ok && j != skip && pk.ag_valid[slice + j]) {
-            bool apart = false;
-#ifdef ZS_NO_CIRCLE
-            if (false) {
-#else
             if (na > 32) {
-#endif
-                const double dx = double(pk.ag_x[slice + j]) - eb.cx, dy = double(pk.ag_y[slice + j]) - eb.cy;
-                const double hl = double(pk.ag_len[size_t(sc) * pk.d.A + j]) * 0.5,
-                             hw = double(pk.ag_wid[size_t(sc) * pk.d.A + j]) * 0.5;
-                const double r = sqrt(re2) + sqrt(hl * hl + hw * hw);
-                apart = dx * dx + dy * dy > r * r * (1.0 + 1e-9) + 1e-9;
+                float lo, hi;
+                agent_bounds(pk, sc, slice, j, eb, lo, hi);
+                f = lo > 0.f ? 0 : agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
+                w.agd[j] = double(lo);
+                key = f == 1 ? 0u : __float_as_uint(hi);
+            } else {
+                f = agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
             }
-            f = apart ? 0 : agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
         }
         w.agf[j] = f;
+        if (na > 32) w.alist[j] = int(key);
         hit |= f == 1;
     }
     return hit;
@@ -1239,46 +1269,18 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
 #else
     if (na > 32 && Ka <= 16) {
 #endif
-        // (lower, upper) bound on obb_distance of separate agent j, in fp32
-        // with margins (1e-4 + 1e-5 D) far above its rounding
-        const float ec = float(rs.eb.c), es = float(rs.eb.s), ehl = float(rs.eb.hl), ehw = float(rs.eb.hw);
-        auto bounds = [&](int j, float& lo, float& hi) {
-            const float dx = float(double(pk.ag_x[aslice + j]) - ecx), dy = float(double(pk.ag_y[aslice + j]) - ecy);
-            const float D = sqrtf(dx * dx + dy * dy);
-            const float m = 1e-4f + 1e-5f * D;
-            if (!(D > 1e-3f)) {
-                lo = 0.f, hi = m + 1e-3f;
-                return;
-            }
-            const float id = 1.f / D, ux = dx * id, uy = dy * id;
-            const double2 cs = pk.ag_cs[aslice + j];
-            const float ac = float(cs.x), as = float(cs.y);
-            const float ahl = pk.ag_len[size_t(sc) * A + j] * 0.5f, ahw = pk.ag_wid[size_t(sc) * A + j] * 0.5f;
-            const float e1 = fabsf(ux * ec + uy * es), e2 = fabsf(uy * ec - ux * es);
-            const float a1 = fabsf(ux * ac + uy * as), a2 = fabsf(uy * ac - ux * as);
-            const float te = fminf(e1 > 0.f ? ehl / e1 : INFINITY, e2 > 0.f ? ehw / e2 : INFINITY);
-            const float ta = fminf(a1 > 0.f ? ahl / a1 : INFINITY, a2 > 0.f ? ahw / a2 : INFINITY);
-            lo = D - (ehl * e1 + ehw * e2) - (ahl * a1 + ahw * a2) - m;
-            hi = fmaxf(0.f, D - te - ta) + m;
-        };
         for (int j0 = 0; j0 < na; j0 += 32) {
             const int j = j0 + lane;
             const int fl = j < na ? w.agf[j] : -1;
-            unsigned key = 0xFFFFFFFFu;
-            if (fl == 1) {
-                key = 0u;
-            } else if (fl == 0) {
-                float lo, hi;
-                bounds(j, lo, hi);
-                key = __float_as_uint(hi);
-                w.agd[j] = double(lo);  // kept for the survivor test (agd is rewritten by the exact distances)
-            }
-            if (j < na) w.alist[j] = int(key);
+            // (agent_boxes -- the step's collision pass, or the call above
+            // when not fused -- stored the bounds: lower in agd, key in alist)
             nvalid += __popc(__ballot_sync(FULL, fl >= 0));
         }
         __syncwarp();
         if (nvalid > Ka) {
-            const double U = double(__uint_as_float(warp_kth_key(w.alist, na, Ka)));
+            // Ka-th smallest upper bound on the keys' top 16 bits, rounded up
+            // to the bucket's largest key: still an upper bound, half the passes
+            const double U = double(__uint_as_float(warp_kth_key(w.alist, na, Ka) | 0xFFFFu));
             __syncwarp();
             int n = 0;
             for (int j0 = 0; j0 < na; j0 += 32) {
