@@ -385,12 +385,19 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
         {
             float lbv[2], fdmin = INFINITY;
             const int GC = pk.d.GC;
+            // the group boxes are loaded without waiting for the lane's group
+            // count (one memory round trip instead of two); g < GC keeps the
+            // loads inside the lane's slots
+            float4 gbv[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                gbv[c] = gg + 8 * c < GC ? pk.ln_gb[lrow * GC + gg + 8 * c] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < 2; ++c) {  // groups gg and gg + 8 (lanes up to 129 vertices)
                 const int g = gg + 8 * c;
                 lbv[c] = INFINITY;
                 if (g < ngr) {
-                    const float4 bb = pk.ln_gb[lrow * GC + g];
+                    const float4 bb = gbv[c];
                     const float x0 = bb.x - qxf[0], x1 = qxf[0] - bb.z, y0 = bb.y - qyf[0], y1 = qyf[0] - bb.w;
                     const float nx = fmaxf(fmaxf(x0, x1), 0.f), ny = fmaxf(fmaxf(y0, y1), 0.f);
                     const float fx = fmaxf(fabsf(x0), fabsf(x1)), fy = fmaxf(fabsf(y0), fabsf(y1));
