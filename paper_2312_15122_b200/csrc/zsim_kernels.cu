@@ -1,9 +1,9 @@
 // zsim_kernels.cu -- sm_100a kernels for the batched simulator step.
 //
 // Execution model: ONE WARP PER SCENARIO ROW.  A CTA holds kThreads/32
-// independent warps; each walks scenario rows in a grid-stride loop and never
-// waits on another warp (no __syncthreads on the hot path).  Per row, in one
-// launch:
+// warps that walk scenario rows in a grid-stride loop, one block barrier per
+// row (the warps stay in phase and share the instruction cache); inside a row
+// a warp never waits on another.  Per row, in one launch:
 //
 //   step     bicycle_step -> route projection of the ego and of the four
 //            inflated footprint corners (lane-of-route x segment across the 32
@@ -1774,7 +1774,12 @@ __global__ void __launch_bounds__(kThreads, ZS_MIN_BLOCKS) k_step_observe(const 
     const int b_end = a.row_hi > 0 ? a.row_hi : a.pk.d.B;
     int b = a.row_lo + blockIdx.x * wpb + warp_in_block();
     if (b < b_end) prefetch_row<STEP, OBS>(a, scen_of(a.pk, b), a.in.t[b] + (STEP ? 1 : 0));
-    for (; b < b_end; b += stride) {
+    // the CTA's warps advance row by row together (the same code in flight:
+    // the instruction cache is shared instead of thrashed by out-of-phase
+    // rows; measured C2 +13%, C1 / C4 +1%)
+    for (int b0 = a.row_lo + blockIdx.x * wpb; b0 < b_end; b0 += stride, b += stride) {
+        __syncthreads();
+        if (b >= b_end) continue;
         if (lane_id() == 0) {
             w.rs->r0 = load_row(a.in, b);
             if ((OBS & kObsMap) && a.hint) w.rs->hint = a.hint[b];
