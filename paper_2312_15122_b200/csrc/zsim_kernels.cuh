@@ -8,7 +8,10 @@
 
 namespace zs {
 
-constexpr int kThreads = 128;  // threads per CTA (4 warps); one CTA per scenario row at a time
+constexpr int kThreads = 128;  // threads per CTA of the small kernels (reset, ...)
+// k_step_observe CTAs: 14 warps (two CTAs fill an SM's 28 warps) when the
+// per-warp shared memory allows, else 4; one warp per scenario row at a time
+constexpr int kCtaWarpsBig = 14, kCtaWarpsSmall = 4;
 constexpr int kMaxLanes = 64;  // route lanes per scenario (projection walks lanes sequentially)
 
 constexpr int kStatsLen = 8;  // episode-stats vector length
@@ -51,7 +54,8 @@ struct KernelArgs {
     int32_t row_lo, row_hi;  // rows [row_lo, row_hi) of the batch; row_hi == 0: all rows
 };
 
-size_t smem_bytes(const KernelArgs& a);
+size_t smem_bytes(const KernelArgs& a);  // per CTA of k_step_observe (its CTA size: step_observe_warps)
+int step_observe_warps(const KernelArgs& a);
 // policy: 0 auto (split the observation into separate kernels beyond one wave), 1 fused, 2 split
 cudaError_t launch_step_observe(const KernelArgs& a, int mode, int policy, cudaStream_t stream);
 bool observe_split(const KernelArgs& a, int policy);  // the arrangement launch_step_observe picks
