@@ -237,6 +237,8 @@ def run_ours(args) -> None:
     zsim = z.stress_scenarios(z.StressConfig(count=S_, agents=A_, road_points=P, first_index=lo,
                                              flags=z.STRESS_C2 if controlled else 0), 7)
     env = z.Env(zsim, config=z.SimConfig(disable_dones=True), device=local, controlled=controlled)
+    if args.launch_policy:
+        env.set_launch_policy(args.launch_policy)
     del zsim
     B = env.info.batch
     assert B == S_ * rpr, (B, S_, rpr)
@@ -516,6 +518,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph rollouts")
     ap.add_argument("--no-policy", action="store_true", help="skip the on-device policy measurement")
+    ap.add_argument("--launch-policy", type=int, default=0, choices=(0, 1, 2),
+                    help="kernel arrangement: 0 auto, 1 fused step+observe, 2 split observation (diagnostic)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -2090,8 +2090,9 @@ bool observe_split(const KernelArgs& a, int policy) {
     int per_sm = blocks_per_sm(fn, smem_bytes(t), 32 * warps);
     if (per_sm < 1) per_sm = 1;
     const int sms = sm_count();
-    // measured: equal at 2 waves (C1 shapes), split clearly ahead at many waves (C2)
-    return a.pk.d.B > 3 * sms * per_sm * warps;
+    // measured with the in-phase 14-warp CTAs: fused ahead at 1 and 4 waves
+    // (C1; C4 shard +6%), split clearly ahead at many waves (C2, 126 waves: +43%)
+    return a.pk.d.B > 8 * sms * per_sm * warps;
 }
 
 template <int W>
