@@ -1245,12 +1245,17 @@ __global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs 
         tmem_st32(cx.col(kHColH + c0), v);
         tmem_st32(cx.col(kHColP + c0), v);
     }
+    // blockIdx.y selects the trunk: 0 = policy trunk, heads and the action
+    // choice; 1 = value trunk and head (the two are independent given pooled)
+    const bool value_cta = blockIdx.y == 1;
+    float logit[2 * kMaxHead];
+    float value = 0.f;
+    if (!value_cta) {
     // ---- policy trunk (model.hpp:556-562) ----
 #pragma unroll
     for (int i = 0; i < kMaxTrunk; ++i)
         if (i < W.trunk) cx.mlp(W.pblk[i], W.tc_pblk[2 * i], W.tc_pblk[2 * i + 1]);
     // ---- heads (model.hpp:563-568): the row's quarter-0 thread, all 128 columns ----
-    float logit[2 * kMaxHead];
     if (c0 == 0) {
         for (int o = 0; o < na + ns; ++o) logit[o] = o < na ? __ldg(W.acc_b + o) : __ldg(W.str_b + o - na);
         float v[32];
@@ -1264,6 +1269,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs 
             }
         }
     }
+    } else {
     // ---- value trunk (model.hpp:570-584): concat [pooled; gelu(W_e v + b_e)] ----
     cx.load_w(W.tc_vin, uint32_t(kD * (kD + W.ve) * 4));
     {
@@ -1303,7 +1309,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs 
 #pragma unroll
     for (int i = 0; i < kMaxTrunk; ++i)
         if (i < W.trunk) cx.mlp(W.vblk[i], W.tc_vblk[2 * i], W.tc_vblk[2 * i + 1]);
-    float value = __ldg(W.vhead_b);
+    value = __ldg(W.vhead_b);
     if (c0 == 0) {
         float v[32];
         for (int c = 0; c < kD; c += 32) {
@@ -1312,15 +1318,19 @@ __global__ void __launch_bounds__(kHeadThreads, 1) k_policy_heads(const ActArgs 
             for (int i = 0; i < 32; ++i) value = fmaf(sm.vhead[c + i], v[i], value);
         }
     }
+    }  // value trunk
     tc_fence_before();
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(sm.tmem_base));
     if (!live || c0 != 0) return;
+    if (value_cta) {
+        a.value[b] = value;
+        return;
+    }
     // ---- NNPolicy::act (policy.hpp:33-56) ----
     if (a.logits) {
         for (int i = 0; i < na + ns; ++i) a.logits[size_t(b) * (na + ns) + i] = logit[i];
     }
-    a.value[b] = value;
     float la[kMaxHead], ls[kMaxHead];
     for (int i = 0; i < na; ++i) la[i] = logit[i];
     for (int i = 0; i < ns; ++i) ls[i] = logit[na + i];
@@ -1748,7 +1758,7 @@ ZSIM_API int zsim_policy_act(zsim_policy* p, const zsim_obs_view* obs, int32_t b
             const int grid = (batch + zp::kRowsTc - 1) / zp::kRowsTc;
             zp::k_policy_tc<<<grid, zp::kThreads, sizeof(zp::SmemTc), s>>>(a);
             const int hgrid = (batch + zp::kHeadRows - 1) / zp::kHeadRows;
-            zp::k_policy_heads<<<hgrid, zp::kHeadThreads, sizeof(zp::SmemHeads), s>>>(a);
+            zp::k_policy_heads<<<dim3(hgrid, 2), zp::kHeadThreads, sizeof(zp::SmemHeads), s>>>(a);
         } else {
             const int grid = (batch + zp::kRows32 - 1) / zp::kRows32;
             zp::k_policy_fp32<<<grid, zp::kThreads, sizeof(zp::Smem32), s>>>(a);
