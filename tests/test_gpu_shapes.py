@@ -3,7 +3,9 @@ paths the default C1 shapes never take.
 
 * more than 4 route lanes (several lane blocks in the projection),
 * long lane centrelines (more than 16 8-segment groups: groups always scanned),
-* more than 32 agents per row in ego mode (chunked agent ordering; C3/C4),
+* more than 32 agents per row in ego mode (chunked agent ordering, bound
+  pruning; C3/C4), and so many agents that the per-warp shared memory forces
+  the 4-warp CTA arrangement,
 * large roadgraphs (8192 points, 256 chunks: C4),
 * fewer road / route points than k (partially filled top-k, zero padding),
 * a single-scenario batch.
@@ -50,6 +52,8 @@ SHAPES = {
     "long_lanes": dict(count=4, lane_vertices=200, road_points=512),
     "very_long_lanes": dict(count=2, lane_vertices=600, road_points=256),
     "agents_64": dict(count=6, agents=64, road_points=1024),
+    "agents_128": dict(count=4, agents=128, road_points=1024),
+    "agents_900": dict(count=2, agents=900, road_points=512),
     "roadgraph_8k": dict(count=4, agents=16, road_points=8192),
     "sparse_map": dict(count=6, agents=4, road_points=40, lanes=1, lane_vertices=12),
     "single": dict(count=1, agents=8, road_points=300),
