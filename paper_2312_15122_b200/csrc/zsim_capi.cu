@@ -565,8 +565,6 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     size_t o_ix = pb.reserve<double>(B), o_iy = pb.reserve<double>(B), o_ih = pb.reserve<double>(B),
            o_iv = pb.reserve<double>(B), o_ist = pb.reserve<double>(B);
     size_t o_rsc = pb.reserve<int32_t>(B), o_rac = pb.reserve<int32_t>(B);
-    constexpr int kPf = 14;
-    size_t o_pf = pb.reserve<PfDesc>(kPf);
     if (up) {
         if (up->cap < pb.cursor) {
             if (up->pinned) cudaFreeHost(up->pinned);
@@ -832,29 +830,6 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     pk.st_s = reinterpret_cast<const double*>(D + o_sts);
     pk.row_scen = controlled ? reinterpret_cast<const int32_t*>(D + o_rsc) : nullptr;
     pk.row_actor = controlled ? reinterpret_cast<const int32_t*>(D + o_rac) : nullptr;
-    {
-        // L2 prefetch table (zsim_kernels.cu prefetch_row): the per-row arrays a step touches
-        const uint32_t LC = uint32_t(d.L) * uint32_t(d.C), TA = uint32_t(d.T) * uint32_t(d.A), A = uint32_t(d.A);
-        const PfDesc tab[kPf] = {
-            {pk.ln_f4, LC * 16, 0, LC * 16, 1},
-            {pk.ln_gb, uint32_t(d.L) * uint32_t(d.GC) * 16, 0, uint32_t(d.L) * uint32_t(d.GC) * 16, 1},
-            {pk.ln_info, uint32_t(d.L) * 16, 0, uint32_t(d.L) * 16, 0},
-            {pk.road_cb, uint32_t(d.PC) * 16, 0, uint32_t(d.PC) * 16, 2},
-            {pk.route_cb, uint32_t(d.RC) * 16, 0, uint32_t(d.RC) * 16, 2},
-            {pk.ag_x, TA * 4, A * 4, A * 4, 0},
-            {pk.ag_y, TA * 4, A * 4, A * 4, 0},
-            {pk.ag_h, TA * 4, A * 4, A * 4, 2},
-            {pk.ag_cs, TA * 16, A * 16, A * 16, 0},
-            {pk.ag_sp, TA * 4, A * 4, A * 4, 2},
-            {pk.ag_valid, TA, A, A, 0},
-            {pk.ag_len, A * 4, 0, A * 4, 0},
-            {pk.ag_wid, A * 4, 0, A * 4, 0},
-            {pk.lt_state, uint32_t(d.NL) * uint32_t(d.T), 0, uint32_t(d.NL) * uint32_t(d.T), 0},
-        };
-        std::memcpy(pb.host.data() + o_pf, tab, sizeof(tab));
-        pk.pf = reinterpret_cast<const PfDesc*>(D + o_pf);
-        pk.n_pf = kPf;
-    }
     // one upload of the whole image: synchronous, or (BatchStream) through a
     // pinned staging buffer on a copy stream
     if (up) {

@@ -81,15 +81,6 @@ __device__ __forceinline__ void obs_st(T* p, T v) { __stcs(p, v); }
 __device__ __forceinline__ int warp_in_block() { return threadIdx.x >> 5; }
 __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
 
-// TMA-unit bulk prefetch of a byte range into L2 (cp.async.bulk.prefetch,
-// sm_90+): one instruction per array, no registers or smem held.
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-    uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    uintptr_t a0 = a & ~uintptr_t(15);
-    unsigned n = (bytes + unsigned(a - a0) + 15u) & ~15u;
-    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(n) : "memory");
-}
-
 // One out-of-line copy of each fp64 libm routine (the inlined versions
 // multiply the kernel's code size past the instruction cache).
 __device__ __noinline__ double2 sincos2(double x) {
@@ -1746,22 +1737,6 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     __syncwarp();
 }
 
-// Prefetch scenario sc's static data (the arrays one step touches, from the
-// pack's prefetch table: one array per lane) into L2.  `t` is the log
-// index of the agent slice the kernel will read.
-template <bool STEP, int OBS>
-__device__ __forceinline__ void prefetch_row(const KernelArgs& a, int sc, int t) {
-    const DevPack& pk = a.pk;
-    const int lane = lane_id();
-    if (lane >= pk.n_pf) return;
-    const PfDesc d = pk.pf[lane];
-    if (((d.mode & 1) && !STEP) || ((d.mode & 2) && !OBS) || d.bytes == 0) return;
-    const int T = pk.d.T;
-    const int ts = t < T ? (t >= 0 ? t : 0) : T - 1;
-    const char* p = static_cast<const char*>(d.base) + size_t(sc) * d.row_stride + size_t(ts) * d.t_stride;
-    prefetch_l2(p, d.bytes < (1u << 24) ? d.bytes : (1u << 24));
-}
-
 // 28 resident warps per SM (72 registers), WARPS per CTA
 template <bool STEP, int OBS, bool REC, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS, 28 / WARPS) k_step_observe(const KernelArgs a) {
@@ -1771,7 +1746,6 @@ __global__ void __launch_bounds__(32 * WARPS, 28 / WARPS) k_step_observe(const K
     const int stride = gridDim.x * wpb;
     const int b_end = a.row_hi > 0 ? a.row_hi : a.pk.d.B;
     int b = a.row_lo + blockIdx.x * wpb + warp_in_block();
-    if (b < b_end) prefetch_row<STEP, OBS>(a, scen_of(a.pk, b), a.in.t[b] + (STEP ? 1 : 0));
     // the CTA's warps advance row by row together (the same code in flight:
     // the instruction cache is shared instead of thrashed by out-of-phase
     // rows; measured C2 +13%, C1 / C4 +1%)
@@ -1785,9 +1759,6 @@ __global__ void __launch_bounds__(32 * WARPS, 28 / WARPS) k_step_observe(const K
             w.rs->skip = skip_of(a.pk, b);
         }
         __syncwarp();
-        // the warp's next row: its static data streams into L2 while this row computes
-        if (b + stride < b_end)
-            prefetch_row<STEP, OBS>(a, scen_of(a.pk, b + stride), w.rs->r0.t + (STEP ? 1 : 0));
         ROW_MARK(b, 0);
         if (STEP) {
             step_row<REC>(a, b, w);
@@ -2024,7 +1995,7 @@ static int grid_for(const KernelArgs& a, int wpb = kThreads / 32) {
 }
 
 // Persistent grid: as many CTAs as fit on the device at once (each warp then
-// walks rows with a stride and prefetches its next row), capped by the work.
+// walks rows with a stride), capped by the work.
 // The smem attribute and occupancy of a (kernel, smem) pair are queried once.
 struct LaunchCfg {
     const void* fn;

@@ -55,13 +55,6 @@ struct __align__(16) LaneVtx {
     double x, y, abx, aby, s, ds, hw, dhw;
 };
 
-// One per-row array the kernels prefetch into L2 at row start:
-// address = base + row * row_stride + t * t_stride, `bytes` long.
-struct PfDesc {
-    const void* base;
-    uint32_t row_stride, t_stride, bytes, mode;  // mode bit 0: step kernels only, bit 1: observe kernels only
-};
-
 struct DevPack {
     PackDims d;
     double dt;
@@ -118,8 +111,6 @@ struct DevPack {
     // rows -> scenario data (null in ego mode: identity / no skipped actor)
     const int32_t* row_scen;   // [B] scenario of the row
     const int32_t* row_actor;  // [B] controlled actor (its agent column is skipped)
-    const PfDesc* pf;  // prefetch table
-    int32_t n_pf;
     // lights / stops
     const double* lt_s;
     const uint8_t* lt_state;  // [B][NL][T]
