@@ -481,10 +481,19 @@ def measure_policy(env, ob, B, A_):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
-    env.rollout_policy_device(pol, 42, EPISODE, stream=stream)  # warm-up
+    env.rollout_policy_device(pol, 42, EPISODE, stream=stream)  # warm-up (allocates the scratch)
     torch.cuda.synchronize()
+    # the whole closed loop (reset, 91 x [policy encoder + heads, fused step]) as one CUDA graph
+    graph = torch.cuda.CUDAGraph()
+    gs = torch.cuda.Stream()
+    with torch.cuda.stream(gs):
+        with torch.cuda.graph(graph, stream=gs):
+            env.rollout_policy_device(pol, 42, EPISODE, stream=gs)
+    graph.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
     e0.record(stream)
-    env.rollout_policy_device(pol, 42, EPISODE, stream=stream)
+    graph.replay()
     e1.record(stream)
     torch.cuda.synchronize()
     loop_ms = e0.elapsed_time(e1)
@@ -498,7 +507,8 @@ def measure_policy(env, ob, B, A_):
     achieved = tc_flops * B / (ms / 1e3) / 1e12
     return {"precision": "tf32 projections on tcgen05, fp32 elsewhere", "rows": B, "ms_per_act": ms,
             "rows_per_s": B / (ms / 1e3),
-            "closed_loop": {"path": "zsim_rollout_policy: observe -> NNPolicy::act -> step, 91 steps, sampling",
+            "closed_loop": {"path": "zsim_rollout_policy: observe -> NNPolicy::act -> step, 91 steps, sampling, "
+                                    "replayed from a CUDA graph",
                             "ms": loop_ms, "agent_steps_per_s": B * A_ * EPISODE / (loop_ms / 1e3)},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf32, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf32 if peak_tf32 else None,

@@ -1767,7 +1767,7 @@ ZSIM_API int zsim_rollout_policy(zsim_env* env, zsim_policy* policy, int32_t use
             a.out = env->roll_s[cur ^ 1];
             a.accel = pa;
             a.steer = ps;
-            a.act_len = -2;
+            a.act_len = ep ? -2 : 0;  // without recording the plain step kernel reads accel / steer [B]
             a.pol_logp = plogp;
             a.pol_value = pvalue;
             a.so = env->roll_so;
