@@ -456,6 +456,12 @@ ZSIM_API int zsim_policy_init_params(const zsim_model_config* cfg, uint64_t seed
 ZSIM_API int zsim_policy_create(const zsim_model_config* cfg, const float* params, int64_t n, int32_t device,
                                 zsim_policy** out);
 ZSIM_API int zsim_policy_destroy(zsim_policy* policy);
+/* NNPolicy::act on HOST buffers (the RolloutPolicy interface,
+ * simcore.hpp:144-149): obs rows [0, batch) and rng [batch] uploaded, the
+ * device policy run, accel / steer / logp / value [batch] and the advanced
+ * rng streams written back.  Synchronous. */
+ZSIM_API int zsim_policy_act_host(zsim_policy* policy, const zsim_obs_view* obs, int32_t batch, uint64_t* rng,
+                                  int32_t use_argmax, int32_t* accel, int32_t* steer, float* logp, float* value);
 /* Arithmetic of the ten 128x128 token-tile projections: 0 (default) =
  * tcgen05 tensor cores, tf32 operands, fp32 accumulation; 1 = fp32 CUDA
  * cores (the reference's Model<float> arithmetic).  Everything else is fp32

@@ -326,4 +326,48 @@ private:
     std::vector<double> goal_s_, initial_s_, logged_;
 };
 
+// Drop-in for train::NNPolicy (train/policy.hpp:19-58) as a host
+// sim::RolloutPolicy: the snapshot's flat Model<float>::params (ParamIndex
+// order) run on the device policy kernels; usable with either Env::rollout.
+class NNPolicy final : public sim::RolloutPolicy {
+public:
+    NNPolicy(const std::vector<float>& params, bool use_argmax, int device = 0,
+             const zsim_model_config* cfg = nullptr)
+        : argmax_(use_argmax) {
+        zsim_model_config c;
+        if (cfg) {
+            c = *cfg;
+        } else {
+            detail::check(zsim_model_config_defaults(&c));
+        }
+        detail::check(zsim_policy_create(&c, params.data(), int64_t(params.size()), device, &pol_));
+    }
+    NNPolicy(const NNPolicy&) = delete;
+    NNPolicy& operator=(const NNPolicy&) = delete;
+    ~NNPolicy() override {
+        if (pol_) zsim_policy_destroy(pol_);
+    }
+
+    void act(const sim::ObservationBatch& obs, const std::vector<int32_t>& step_index, std::vector<uint64_t>& rng,
+             sim::PolicyOut& out) override {
+        (void)step_index;
+        const int b = obs.batch;
+        out.accel_idx.resize(size_t(b));
+        out.steer_idx.resize(size_t(b));
+        out.logp.resize(size_t(b));
+        out.value.resize(size_t(b));
+        zsim_obs_view v{const_cast<float*>(obs.active.data()), const_cast<float*>(obs.agents.data()),
+                        const_cast<float*>(obs.road.data()), const_cast<float*>(obs.route.data()),
+                        const_cast<float*>(obs.value_only.data())};
+        detail::check(zsim_policy_act_host(pol_, &v, b, rng.data(), argmax_ ? 1 : 0, out.accel_idx.data(),
+                                           out.steer_idx.data(), out.logp.data(), out.value.data()));
+    }
+
+    zsim_policy* handle() const { return pol_; }  // device fast path (zsim_policy_act, zsim_rollout_policy)
+
+private:
+    zsim_policy* pol_ = nullptr;
+    bool argmax_;
+};
+
 }  // namespace zsim::gpu

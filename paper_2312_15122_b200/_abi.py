@@ -180,6 +180,7 @@ SIGNATURES = {
     "zsim_policy_create": (C.c_int, [C.POINTER(ModelConfigC), c_float_p, C.c_int64, C.c_int32, C.POINTER(_P)]),
     "zsim_policy_destroy": (C.c_int, [_P]),
     "zsim_policy_set_precision": (C.c_int, [_P, C.c_int32]),
+    "zsim_policy_act_host": (C.c_int, [_P, C.POINTER(ObsView), C.c_int32, _P, C.c_int32, _P, _P, _P, _P]),
     "zsim_sequences_alloc": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(SequencesView)]),
     "zsim_sequences_free": (C.c_int, [_P, C.POINTER(SequencesView)]),
     "zsim_cut_sequences": (C.c_int, [_P, C.POINTER(EpisodeView), C.POINTER(ObsView), C.c_int32,

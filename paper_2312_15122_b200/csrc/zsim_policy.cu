@@ -1453,6 +1453,8 @@ struct zsim_policy {
     int precision = 0;  // 0: tcgen05 tf32 projections, 1: fp32 CUDA cores
     float* pooled = nullptr;  // [cap][128] encoder output scratch (tensor-core path)
     int pooled_cap = 0;
+    unsigned char* hbuf = nullptr;  // zsim_policy_act_host: device obs + rng + outputs for hcap rows
+    int hcap = 0;
 };
 
 namespace {
@@ -1719,6 +1721,7 @@ ZSIM_API int zsim_policy_destroy(zsim_policy* p) {
         cudaSetDevice(p->device);
         cudaFree(p->blob);
         cudaFree(p->pooled);
+        cudaFree(p->hbuf);
         delete p;
     });
 }
@@ -1764,6 +1767,55 @@ ZSIM_API int zsim_policy_act(zsim_policy* p, const zsim_obs_view* obs, int32_t b
             zp::k_policy_fp32<<<grid, zp::kThreads, sizeof(zp::Smem32), s>>>(a);
         }
         ccheck(cudaGetLastError(), "policy kernel launch");
+    });
+}
+
+// NNPolicy::act on HOST buffers (the reference's RolloutPolicy interface):
+// observations and rng streams are uploaded, the device policy runs, actions
+// / logp / value / advanced rng come back.  Synchronous.
+ZSIM_API int zsim_policy_act_host(zsim_policy* p, const zsim_obs_view* obs, int32_t batch, uint64_t* rng,
+                                  int32_t use_argmax, int32_t* accel, int32_t* steer, float* logp, float* value) {
+    return pguarded([&] {
+        if (!p || !obs || !accel || !steer || !logp || !value || (!use_argmax && !rng))
+            zs::raise(zs::Err::invalid_argument, "policy_act_host: null argument");
+        if (batch < 0) zs::raise(zs::Err::invalid_argument, "policy_act_host: negative batch");
+        if (batch == 0) return;
+        ccheck(cudaSetDevice(p->device), "cudaSetDevice");
+        const size_t B = size_t(batch);
+        const size_t n[5] = {B * zp::kActF, B * zp::kAgents * zp::kAgF, B * zp::kRoad * zp::kRoadF,
+                             B * zp::kRoute * zp::kRouteF, B * zp::kValF};
+        auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+        size_t off[5], o = 0;
+        for (int k = 0; k < 5; ++k) off[k] = o, o += al(n[k] * 4);
+        const size_t o_rng = o, o_out = o + al(B * 8);
+        const size_t bytes = o_out + 4 * al(B * 4);
+        if (p->hcap < batch) {
+            cudaFree(p->hbuf);
+            p->hbuf = nullptr;
+            p->hcap = 0;
+            ccheck(cudaMalloc(&p->hbuf, bytes), "cudaMalloc(policy host scratch)");
+            p->hcap = batch;
+        }
+        const float* src[5] = {obs->active, obs->agents, obs->road, obs->route, obs->value_only};
+        zsim_obs_view dv;
+        float** dst[5] = {&dv.active, &dv.agents, &dv.road, &dv.route, &dv.value_only};
+        for (int k = 0; k < 5; ++k) {
+            *dst[k] = reinterpret_cast<float*>(p->hbuf + off[k]);
+            ccheck(cudaMemcpy(*dst[k], src[k], n[k] * 4, cudaMemcpyHostToDevice), "upload observations");
+        }
+        uint64_t* drng = reinterpret_cast<uint64_t*>(p->hbuf + o_rng);
+        if (rng) ccheck(cudaMemcpy(drng, rng, B * 8, cudaMemcpyHostToDevice), "upload rng");
+        auto* da = reinterpret_cast<int32_t*>(p->hbuf + o_out);
+        auto* ds = reinterpret_cast<int32_t*>(p->hbuf + o_out + al(B * 4));
+        auto* dl = reinterpret_cast<float*>(p->hbuf + o_out + 2 * al(B * 4));
+        auto* dvl = reinterpret_cast<float*>(p->hbuf + o_out + 3 * al(B * 4));
+        if (zsim_policy_act(p, &dv, batch, drng, use_argmax, da, ds, dl, dvl, nullptr, nullptr) != ZSIM_OK)
+            zs::raise(zs::Err::runtime, "policy_act_host: device act failed");
+        ccheck(cudaMemcpy(accel, da, B * 4, cudaMemcpyDeviceToHost), "download accel");
+        ccheck(cudaMemcpy(steer, ds, B * 4, cudaMemcpyDeviceToHost), "download steer");
+        ccheck(cudaMemcpy(logp, dl, B * 4, cudaMemcpyDeviceToHost), "download logp");
+        ccheck(cudaMemcpy(value, dvl, B * 4, cudaMemcpyDeviceToHost), "download value");
+        if (rng && !use_argmax) ccheck(cudaMemcpy(rng, drng, B * 8, cudaMemcpyDeviceToHost), "download rng");
     });
 }
 

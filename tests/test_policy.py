@@ -237,3 +237,35 @@ def test_policy_rollout_matches_oracle_loop(use_argmax):
         want = 0.0 if st.done[b] else out["value"][b]
         assert abs(got["bootstrap"][b] - want) < 1e-5 + 1e-4 * abs(want)
         assert got["terminal"][b] == st.reason[b] and got["events"][b] == st.events[b]
+
+
+@pytest.mark.gpu
+def test_policy_act_host_matches_device_path():
+    """zsim_policy_act_host (the RolloutPolicy-shaped host entry point behind
+    the C++ drop-in zsim::gpu::NNPolicy) equals the device entry point."""
+    import paper_2312_15122_b200 as z
+    from paper_2312_15122_b200._abi import ObsView, lib
+    cfg_o = po.ModelConfig()
+    params = po.init_params(cfg_o, 4)
+    B = 9
+    obs = random_obs(B, np.random.default_rng(8))
+    rng0 = np.arange(1, B + 1, dtype=np.uint64) * np.uint64(977)
+    for use_argmax in (True, False):
+        pol = z.NNPolicy(z.ModelConfig(), params, use_argmax=use_argmax)
+        dev = run_device(pol, obs, rng0.copy(), B)
+        host = {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in obs.items()}
+        v = ObsView()
+        for k, a in host.items():
+            setattr(v, k, a.ctypes.data_as(C.POINTER(C.c_float)))
+        rng = rng0.copy()
+        acc, ste = np.zeros(B, np.int32), np.zeros(B, np.int32)
+        lp, val = np.zeros(B, np.float32), np.zeros(B, np.float32)
+        P = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+        assert lib.zsim_policy_act_host(pol.handle, C.byref(v), B, P(rng), int(use_argmax), P(acc), P(ste), P(lp),
+                                        P(val)) == 0
+        np.testing.assert_array_equal(acc, dev["accel"])
+        np.testing.assert_array_equal(ste, dev["steer"])
+        np.testing.assert_array_equal(lp, dev["logp"])
+        np.testing.assert_array_equal(val, dev["value"])
+        if not use_argmax:
+            np.testing.assert_array_equal(rng, dev["rng"])
