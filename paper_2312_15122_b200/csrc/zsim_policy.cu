@@ -396,6 +396,10 @@ __device__ void trunk_and_act(const RowSm<R>& in, TrunkSm<R>& sm, const ActArgs&
     }
 }
 
+// float4 load through a generic pointer (the folded weights are staged in
+// shared memory by the tensor-core kernel, read from global by the fp32 one)
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
 // Folded cross attention of ONE query (one head) against a row's feature
 // tokens (null + N tokens of F scaled features, model.hpp:326-367): q is the
 // head's 64 query values, out receives the head's 64 output values.
@@ -413,11 +417,11 @@ __device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* 
         const int c = 4 * c4;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
-            const float4 k = __ldg(reinterpret_cast<const float4*>(kf + f * kD + c));
+            const float4 k = ld4((kf + f * kD + c));
             qf[f] = fmaf(k.x, q[c], fmaf(k.y, q[c + 1], fmaf(k.z, q[c + 2], fmaf(k.w, q[c + 3], qf[f]))));
         }
-        const float4 ck = __ldg(reinterpret_cast<const float4*>(w.ck + h * kDh + c));
-        const float4 kn = __ldg(reinterpret_cast<const float4*>(w.kn + h * kDh + c));
+        const float4 ck = ld4((w.ck + h * kDh + c));
+        const float4 kn = ld4((w.kn + h * kDh + c));
         qn = fmaf(ck.x, q[c], fmaf(ck.y, q[c + 1], fmaf(ck.z, q[c + 2], fmaf(ck.w, q[c + 3], qn))));
         sn = fmaf(kn.x, q[c], fmaf(kn.y, q[c + 1], fmaf(kn.z, q[c + 2], fmaf(kn.w, q[c + 3], sn))));
     }
@@ -480,13 +484,13 @@ __device__ __forceinline__ void cross_query(const AttnW& w, int h, const float* 
 #pragma unroll
     for (int c4 = 0; c4 < kDh / 4; ++c4) {
         const int c = 4 * c4;
-        const float4 cv = __ldg(reinterpret_cast<const float4*>(w.cv + h * kDh + c));
-        const float4 vn = __ldg(reinterpret_cast<const float4*>(w.vn + h * kDh + c));
+        const float4 cv = ld4((w.cv + h * kDh + c));
+        const float4 vn = ld4((w.vn + h * kDh + c));
         float o0 = fmaf(ps, cv.x, pn * vn.x), o1 = fmaf(ps, cv.y, pn * vn.y), o2 = fmaf(ps, cv.z, pn * vn.z),
               o3 = fmaf(ps, cv.w, pn * vn.w);
 #pragma unroll
         for (int f = 0; f < F; ++f) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(vf + f * kD + c));
+            const float4 v = ld4((vf + f * kD + c));
             o0 = fmaf(v.x, ag[f], o0);
             o1 = fmaf(v.y, ag[f], o1);
             o2 = fmaf(v.z, ag[f], o2);
@@ -1033,14 +1037,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
         cx.wait_w();
         cx.mma(kColD0);
         cx.load_w(wo_tc);  // the output projection streams in during the attention
+        // the block's folded weights (Kf, Vf [F][128], ck, cv, kn, vn [128]) to
+        // smem, over the self-attention score scratch (dead by now): every
+        // thread reads all of them
+        const int F = m == 0 ? kRoadF : m == 1 ? kRouteF : kActF;
+        float* fw = &sm.sc[0][0];
+        for (int e = tid; e < F * kD; e += kThreads) {
+            fw[e] = aw.kf[e];
+            fw[F * kD + e] = aw.vf[e];
+        }
+        for (int e = tid; e < kD; e += kThreads) {
+            fw[2 * F * kD + e] = aw.ck[e];
+            fw[2 * F * kD + kD + e] = aw.cv[e];
+            fw[2 * F * kD + 2 * kD + e] = aw.kn[e];
+            fw[2 * F * kD + 3 * kD + e] = aw.vn[e];
+        }
+        __syncthreads();
+        AttnW sw = aw;
+        sw.kf = fw;
+        sw.vf = fw + F * kD;
+        sw.ck = fw + 2 * F * kD;
+        sw.cv = sw.ck + kD;
+        sw.kn = sw.ck + 2 * kD;
+        sw.vn = sw.ck + 3 * kD;
         float q[64], o[64];
         cx.ld64(kColD0, q);
 #pragma unroll
         for (int i = 0; i < 64; ++i) q[i] += __ldg(aw.bq + 64 * half + i);
         if (real) {
-            if (m == 0) cross_query<kRoadF, kRoad, true>(aw, half, q, sm.rs.road[g], sm.rs.mroad[g], o);
-            if (m == 1) cross_query<kRouteF, kRoute, true>(aw, half, q, sm.rs.route[g], sm.rs.mroute[g], o);
-            if (m == 2) cross_query<kActF, 1, true>(aw, half, q, reinterpret_cast<const float(*)[kActF]>(sm.rs.act[g]), sm.rs.mact[g], o);
+            if (m == 0) cross_query<kRoadF, kRoad, true>(sw, half, q, sm.rs.road[g], sm.rs.mroad[g], o);
+            if (m == 1) cross_query<kRouteF, kRoute, true>(sw, half, q, sm.rs.route[g], sm.rs.mroute[g], o);
+            if (m == 2) cross_query<kActF, 1, true>(sw, half, q, reinterpret_cast<const float(*)[kActF]>(sm.rs.act[g]), sm.rs.mact[g], o);
         } else {
 #pragma unroll
             for (int i = 0; i < 64; ++i) o[i] = 0.f;
