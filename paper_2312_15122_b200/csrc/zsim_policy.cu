@@ -396,6 +396,15 @@ __device__ void trunk_and_act(const RowSm<R>& in, TrunkSm<R>& sm, const ActArgs&
     }
 }
 
+// v[i] += p[i] for i < 64, p a 16-B aligned global vector (float4 loads)
+__device__ __forceinline__ void add64(float* v, const float* __restrict__ p) {
+#pragma unroll
+    for (int i = 0; i < 64; i += 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p + i));
+        v[i] += t.x, v[i + 1] += t.y, v[i + 2] += t.z, v[i + 3] += t.w;
+    }
+}
+
 // float4 load through a generic pointer (the folded weights are staged in
 // shared memory by the tensor-core kernel, read from global by the fp32 one)
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
@@ -882,9 +891,13 @@ struct TcCtx {
         __syncthreads();
         const float rstd = 1.f / sqrtf((sm.red2[0][tok] + sm.red2[1][tok]) / float(kD) + 1e-5f);
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
+        for (int i = 0; i < 64; i += 4) {
             const int c = 64 * half + i;
-            v[i] = (v[i] - mu) * rstd * __ldg(g + c) + __ldg(b + c);
+            const float4 gg = __ldg(reinterpret_cast<const float4*>(g + c)), bb = __ldg(reinterpret_cast<const float4*>(b + c));
+            v[i] = (v[i] - mu) * rstd * gg.x + bb.x;
+            v[i + 1] = (v[i + 1] - mu) * rstd * gg.y + bb.y;
+            v[i + 2] = (v[i + 2] - mu) * rstd * gg.z + bb.z;
+            v[i + 3] = (v[i + 3] - mu) * rstd * gg.w + bb.w;
         }
         put_a(v);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -895,8 +908,9 @@ struct TcCtx {
         float x[64], d[64];
         ld64(kColX, x);
         ld64(dcol, d);
+        add64(d, bias + 64 * half);
 #pragma unroll
-        for (int i = 0; i < 64; ++i) x[i] += d[i] + __ldg(bias + 64 * half + i);
+        for (int i = 0; i < 64; ++i) x[i] += d[i];
         st64(kColX, x);
     }
 };
@@ -1013,8 +1027,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
     {
         float q[64], o[64];
         cx.ld64(kColD0, q);
-#pragma unroll
-        for (int i = 0; i < 64; ++i) q[i] += __ldg(W.self.bq + 64 * half + i);
+        add64(q, W.self.bq + 64 * half);
         if (real) {
             self_query<true>(half, q, sm.rs.mlat[g], KVTc{sm.opA, sm.opW, g * kLat}, o, sm.sc[tid]);
         } else {
@@ -1062,8 +1075,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_policy_tc(const ActArgs a) {
         sw.vn = sw.ck + 3 * kD;
         float q[64], o[64];
         cx.ld64(kColD0, q);
-#pragma unroll
-        for (int i = 0; i < 64; ++i) q[i] += __ldg(aw.bq + 64 * half + i);
+        add64(q, aw.bq + 64 * half);
         if (real) {
             if (m == 0) cross_query<kRoadF, kRoad, true>(sw, half, q, sm.rs.road[g], sm.rs.mroad[g], o);
             if (m == 1) cross_query<kRouteF, kRoute, true>(sw, half, q, sm.rs.route[g], sm.rs.mroute[g], o);
