@@ -480,7 +480,9 @@ ZSIM_API int zsim_rollout_policy(zsim_env* env, zsim_policy* policy, int32_t use
  * of a device observation view; rng [batch] is the per-row stream
  * (SimStateBatch::rng), advanced in place when sampling (unused for argmax).
  * Outputs accel / steer / logp / value [batch]; logits (nullable)
- * [batch][n_accel + n_steer].  Stream-ordered. */
+ * [batch][n_accel + n_steer].  Stream-ordered; the first call at a larger
+ * batch than before allocates scratch (synchronising), later calls are
+ * graph-capturable. */
 ZSIM_API int zsim_policy_act(zsim_policy* policy, const zsim_obs_view* obs, int32_t batch, uint64_t* rng,
                              int32_t use_argmax, int32_t* accel, int32_t* steer, float* logp, float* value,
                              float* logits, void* stream);
