@@ -269,3 +269,28 @@ def test_policy_act_host_matches_device_path():
         np.testing.assert_array_equal(val, dev["value"])
         if not use_argmax:
             np.testing.assert_array_equal(rng, dev["rng"])
+
+
+def test_policy_oracle_attention_invariances():
+    """CPU check of the float64 policy oracle's attention semantics
+    (model.hpp:326-367): masked key tokens receive probability exactly 0, so
+    their feature values cannot change any output, and cross attention is
+    invariant to the order of the key tokens."""
+    cfg = po.ModelConfig()
+    m = po.Model(cfg, po.init_params(cfg, 6))
+    obs = random_obs(4, np.random.default_rng(3))
+    base = po.forward_row(m, obs, 0)
+    o2 = {k: v.copy() for k, v in obs.items()}
+    masked = o2["road"][0, :, 11] <= 0.5
+    o2["road"][0, masked, :11] = 123.0  # garbage in masked road tokens
+    o2["route"][0, o2["route"][0, :, 4] <= 0.5, :4] = -55.0
+    got = po.forward_row(m, o2, 0)
+    for a, b in zip(base[:2], got[:2]):
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-12)
+    assert abs(base[2] - got[2]) < 1e-12
+    perm = np.random.default_rng(1).permutation(128)
+    o3 = {k: v.copy() for k, v in obs.items()}
+    o3["road"][0] = obs["road"][0][perm]
+    got = po.forward_row(m, o3, 0)
+    np.testing.assert_allclose(base[0], got[0], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(base[1], got[1], rtol=1e-12, atol=1e-12)
