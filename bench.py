@@ -4,15 +4,20 @@
 One "step" = one fused step+observe launch over the whole scenario batch
 (Env::step then Env::observe of the stepped state, simcore.cpp:590-609).
 Episodes are 91 steps long (T_log = 92); the state is re-initialised (reset
-kernel, included in the timed region) every 91 steps.  Throughput runs use
+kernel, inside the timed region) every 91 steps.  Throughput runs use
 `disable_dones = true` like the reference bench (simcore.cpp:669).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl ours|reference]
 
-N > 1 is launched by torchrun (one process per GPU, NCCL); each rank simulates
-its own shard of scenarios (weak scaling), no data-path collective; the only
-collective is the all-reduce of the int64 episode-stats vector.
-Rank 0 prints ONE JSON line.
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+(one process per GPU, 127.0.0.1 rendezvous).  Each rank simulates its own
+shard of scenarios; no data-path collective.  The only exchange is the
+per-rollout episode-stats all-reduce over NCCL through the library's C-ABI
+(zsim_stats_allreduce).  C1 / C2 are per-GPU workloads (weak
+scaling); C3 / C4 are BASELINE's fixed global sets (65,536 and 131,072
+scenarios) split across the ranks (strong scaling).  Rank 0 prints ONE JSON
+line.  The timed region is exactly K launches (plus the resets at t % 91 == 0)
+replayed from one CUDA graph.
 """
 from __future__ import annotations
 
@@ -20,6 +25,7 @@ import argparse
 import gc
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -34,21 +40,27 @@ sys.path.insert(0, str(ROOT))
 METRIC = "simulated agent-steps/sec (device-timed) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "agent-steps/s"
 EPISODE = 91  # steps per episode (92 logged states)
+STRESS_SEED, ACTION_SEED, RESET_SEED = 7, 123, 42
 
-# BASELINE.json configs; per-GPU shapes.
+# BASELINE.json configs.  `per_gpu`: scenarios each
+# GPU simulates (weak scaling); `global`: one fixed set split over the GPUs.
 CONFIGS = {
-    "C0": dict(scenarios=64, agents=32, road_points=2048,
+    "C0": dict(per_gpu=64, agents=32, road_points=2048,
                workload="C0: 64 scenarios x 32 agents, 2k roadgraph points, 91-step rollouts (CPU reference case)"),
-    "C1": dict(scenarios=4096, agents=32, road_points=2048,
+    "C1": dict(per_gpu=4096, agents=32, road_points=2048,
                workload="C1: 1xB200, 4096 scenarios x 32 agents, 2k roadgraph points, top-k 16 agents / 128 "
                         "polyline pts"),
-    "C3": dict(scenarios=8192, agents=64, road_points=4096,
-               workload="C3 per-GPU shard: 8192 scenarios x 64 agents, 4k roadgraph points"),
-    "C4": dict(scenarios=16384, agents=128, road_points=8192,
-               workload="C4 per-GPU shard at 8 GPUs: 16384 scenarios x 128 agents, 8k roadgraph points"),
-    "C2": dict(scenarios=4096, agents=128, road_points=8192, controlled=True,
+    "C2": dict(per_gpu=4096, agents=128, road_points=8192, controlled=True,
                workload="C2 dense: 4096 scenarios x 128 agents all controlled (524,288 ego rows), 8k roadgraph "
                         "points; agent-steps = controlled rows x steps (SURVEY 8a row 20)"),
+    "C3": dict(global_=65536, agents=64, road_points=4096,
+               workload="C3: 65536 scenarios x 64 agents, 4k roadgraph points, 91-step rollouts, scenario-sharded "
+                        "over the GPUs"),
+    "C4": dict(global_=131072, agents=128, road_points=8192,
+               workload="C4: 131072 scenarios x 128 agents, 8k roadgraph points, scenario-sharded over the GPUs, "
+                        "stats allreduce"),
+    "C4s": dict(per_gpu=16384, agents=128, road_points=8192,
+                workload="C4 per-GPU shard at 8 GPUs: 16384 scenarios x 128 agents, 8k roadgraph points"),
 }
 LANES, LANE_VERTICES = 4, 64
 
@@ -82,6 +94,28 @@ def hbm_peak() -> tuple[float, str]:
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def plan(name: str, world: int, override: int = 0) -> dict:
+    """The job: global scenario count, scaling mode; identical in both arms."""
+    c = dict(CONFIGS[name])
+    strong = "global_" in c
+    total = override or (c["global_"] if strong else c["per_gpu"] * world)
+    c.update(name=name, total=total, scaling="strong" if strong else "weak", controlled=bool(c.get("controlled")))
+    c["rows_per_scenario"] = c["agents"] if c["controlled"] else 1
+    return c
+
+
+def config_block(p: dict, world: int) -> dict:
+    """`config` of the JSON line -- the same keys and values in both arms."""
+    return {"workload": p["workload"], "config_id": p["name"], "scenarios": p["total"],
+            "scenarios_per_gpu": -(-p["total"] // world), "agents": p["agents"], "road_points": p["road_points"],
+            "controlled": p["controlled"], "rows": p["total"] * p["rows_per_scenario"],
+            "route_points": 2 * LANES * LANE_VERTICES, "lanes": LANES, "lane_vertices": LANE_VERTICES,
+            "steps_per_episode": EPISODE, "disable_dones": True,
+            "seeds": {"scenarios": STRESS_SEED, "actions": ACTION_SEED, "reset": RESET_SEED},
+            "l2": "inputs larger than L2 (per-GPU static pack > 126 MB for C1..C4)",
+            "parallelism": f"scenario-sharded x{world} ({p['scaling']} scaling)"}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -96,7 +130,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -143,41 +177,51 @@ def dist_setup():
     return world, rank, local
 
 
-def _ref_workload(c: dict, n_scen: int, seed: int):
-    """(ZSIM bytes, rows, agents per row) of a reference-arm sample: stress
-    scenarios, or for C2 the per-row scenarios of their controlled actors."""
-    import paper_2312_15122_b200 as z
-    controlled = bool(c.get("controlled"))
-    zsim = z.stress_scenarios(z.StressConfig(count=n_scen, agents=c["agents"], road_points=c["road_points"],
-                                             flags=z.STRESS_C2 if controlled else 0), seed)
-    if controlled:
-        return z.controlled_expand(zsim), n_scen * c["agents"], 1
-    return zsim, n_scen, c["agents"]
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
-def cpu_baseline(cfg_name: str, seed: int) -> dict | None:
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` outside torchrun: re-run this command as N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+# ---------------------------------------------------------------- reference arm
+def _ref_workload(p: dict, n_scen: int):
+    """(ZSIM bytes, rows, agents per row) of a bounded reference sample: the
+    first `n_scen` scenarios of the same stress set (for C2 the per-row
+    scenarios of their controlled actors).  Generated by oracle/_ref's copy of
+    the workload generator -- the product library is never mapped here."""
+    from oracle import refpy
+    z = refpy.stress(n_scen, p["agents"], p["road_points"], seed=STRESS_SEED, c2=p["controlled"])
+    if p["controlled"]:
+        return refpy.controlled_expand(z), n_scen * p["agents"], 1
+    return z, n_scen, p["agents"]
+
+
+def cpu_baseline(p: dict) -> dict | None:
     """Reference simulator (oracle/_ref) timed on this host's cores over a
     bounded sample of the same workload (rank 0, N=1 only)."""
-    try:
-        from oracle import refpy
-    except Exception:
-        return None
+    from oracle import refpy
+    from oracle.hostio import OracleConfig, random_actions
     if not refpy.available():
         return None
-    import paper_2312_15122_b200 as z
-    c = CONFIGS[cfg_name]
-    n_scen = min(16 if c.get("controlled") else 1024, c["scenarios"])
-    zsim, rows, apr = _ref_workload(c, n_scen, seed)
-    A, S = z.random_actions(EPISODE, rows, seed=123)
+    n_scen = min(16 if p["controlled"] else 1024, p["total"])
+    zsim, rows, apr = _ref_workload(p, n_scen)
+    A, S = random_actions(EPISODE, rows, seed=ACTION_SEED)
     threads = os.cpu_count() or 1
-    secs = refpy.bench(zsim, rows, 92, z.SimConfig(disable_dones=True), threads, 0, EPISODE, A, S)
+    secs = refpy.bench(zsim, rows, 92, OracleConfig(disable_dones=True), threads, 0, EPISODE, A, S)
     # single-thread leg on a C0-sized sample (64 rows), SURVEY 8d
-    z1, r1, _ = _ref_workload(c, 1 if c.get("controlled") else min(64, n_scen), seed)
+    z1, r1, _ = _ref_workload(p, 1 if p["controlled"] else min(64, n_scen))
     r1 = min(r1, 64)
-    A1, S1 = z.random_actions(EPISODE, r1, seed=123)
-    secs1 = refpy.bench(z1, r1, 92, z.SimConfig(disable_dones=True), 1, 0, EPISODE, A1, S1)
+    A1, S1 = random_actions(EPISODE, r1, seed=ACTION_SEED)
+    secs1 = refpy.bench(z1, r1, 92, OracleConfig(disable_dones=True), 1, 0, EPISODE, A1, S1)
     return {"value": rows * apr * EPISODE / secs, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{rows} rows ({n_scen} of the {c['scenarios']} {cfg_name} scenarios) x {EPISODE} steps "
+            "sample": f"{rows} rows ({n_scen} of the {p['total']} {p['name']} scenarios) x {EPISODE} steps "
                       f"(observe+step), {threads} per-thread Env shards, oracle/_ref (-O2 -ffp-contract=off)",
             "seconds": secs,
             "value_1thread": r1 * apr * EPISODE / secs1,
@@ -185,126 +229,115 @@ def cpu_baseline(cfg_name: str, seed: int) -> dict | None:
 
 
 def run_reference(args) -> None:
+    """The reference's own CPU step (oracle/_ref = proj/src/core compiled in
+    place) on this host's cores, same workload / metric / config keys."""
     world, rank, _ = dist_setup()
+    if world != args.gpus:
+        raise SystemExit(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
     if rank != 0:
         return
-    import paper_2312_15122_b200 as z
     from oracle import refpy
-    c = CONFIGS[args.config]
+    from oracle.hostio import OracleConfig, random_actions
+    p = plan(args.config, world, args.scenarios)
     if not refpy.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libzsim_ref.so not built"}))
         return
-    # C2 has 524,288 rows: the reference times a bounded sample of them
-    n_scen = min(32, c["scenarios"]) if c.get("controlled") else c["scenarios"]
-    zsim, B, apr = _ref_workload(c, n_scen, 7)
-    A, S = z.random_actions(EPISODE, B, seed=123)
+    # a bounded sample per step: the CPU needs ~90 us per 32-agent scenario-step
+    n_scen = min(32 if p["controlled"] else 4096, p["total"])
+    zsim, B, apr = _ref_workload(p, n_scen)
+    A, S = random_actions(EPISODE, B, seed=ACTION_SEED)
     threads = os.cpu_count() or 1
-    secs = refpy.bench(zsim, B, 92, z.SimConfig(disable_dones=True), threads, args.warmup, args.steps, A, S)
+    secs = refpy.bench(zsim, B, 92, OracleConfig(disable_dones=True), threads, args.warmup, args.steps, A, S)
     value = B * apr * args.steps / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (stress generator seed 7)",
-        "config": {"workload": c["workload"], "scenarios": n_scen, "rows": B, "agents": c["agents"],
-                   "road_points": c["road_points"], "steps_per_episode": EPISODE, "disable_dones": True},
+        "scaling": p["scaling"], "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: stress generator (seed {STRESS_SEED}), random actions (splitmix64 seed {ACTION_SEED})",
+        "config": config_block(p, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{B} rows ({n_scen} scenarios), {args.steps} observe+step iterations, "
-                                   f"{threads} threads"},
+                         "sample": f"{B} rows (the first {n_scen} of the {p['total']} scenarios) per step, "
+                                   f"{args.steps} observe+step iterations, {threads} per-thread Env shards"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------- our arm
 def run_ours(args) -> None:
     import torch
 
     world, rank, local = dist_setup()
+    if world != args.gpus:
+        raise SystemExit(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2312_15122_b200 as z
+    from paper_2312_15122_b200.shard import StatsComm, shard_rows
 
-    from paper_2312_15122_b200.shard import allreduce_stats, shard_rows
-    c = CONFIGS[args.config]
-    A_, P = c["agents"], c["road_points"]
-    controlled = bool(c.get("controlled"))
-    rpr = A_ if controlled else 1  # rows per scenario
-    # weak scaling: the global set holds world x scenarios; rank r owns one contiguous shard
-    lo, hi = shard_rows(c["scenarios"] * world, world, rank)
+    p = plan(args.config, world, args.scenarios)
+    A_, P, controlled, rpr = p["agents"], p["road_points"], p["controlled"], p["rows_per_scenario"]
+    lo, hi = shard_rows(p["total"], world, rank)
     S_ = hi - lo
-    zsim = z.stress_scenarios(z.StressConfig(count=S_, agents=A_, road_points=P, first_index=lo,
-                                             flags=z.STRESS_C2 if controlled else 0), 7)
-    env = z.Env(zsim, config=z.SimConfig(disable_dones=True), device=local, controlled=controlled)
+    t_setup = time.perf_counter()
+    env = z.Env.from_stress(z.StressConfig(count=S_, agents=A_, road_points=P, first_index=lo,
+                                           flags=z.STRESS_C2 if controlled else 0), STRESS_SEED,
+                            config=z.SimConfig(disable_dones=True), device=local, controlled=controlled)
+    setup_s = time.perf_counter() - t_setup
     if args.launch_policy:
         env.set_launch_policy(args.launch_policy)
-    del zsim
     B = env.info.batch
     assert B == S_ * rpr, (B, S_, rpr)
-    accel_all, steer_all = z.random_actions(EPISODE, c["scenarios"] * world * rpr, seed=123)
+    accel_all, steer_all = z.random_actions(EPISODE, p["total"] * rpr, seed=ACTION_SEED)
     accel = np.ascontiguousarray(accel_all[:, lo * rpr:hi * rpr])
     steer = np.ascontiguousarray(steer_all[:, lo * rpr:hi * rpr])
+    del accel_all, steer_all
     dA = torch.from_numpy(accel).cuda()
     dS = torch.from_numpy(steer).cuda()
     s0, s1 = env.device_state(), env.device_state()
     so, ob = env.device_stepout(), env.device_obs()
     stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    comm = StatsComm(rank, world, local) if world > 1 else None
     stream = torch.cuda.current_stream()
 
-    k_state = {"k": 0}
-
-    def one_step(cur, nxt, events=None):
-        k = k_state["k"]
+    def launch(k: int, cur, nxt, strm):
+        """Launch k of a run: reset at t == 0, then the fused step."""
         t = k % EPISODE
         if t == 0:
-            env.reset_device(42, cur, stream)
-        if events is not None:
-            events[0].record(stream)
-        env.step_observe_device(cur, dA[t].data_ptr(), dS[t].data_ptr(), nxt, so, ob, stream)
-        if events is not None:
-            events[1].record(stream)
-        k_state["k"] = k + 1
+            env.reset_device(RESET_SEED, cur, strm)
+        env.step_observe_device(cur, dA[t].data_ptr(), dS[t].data_ptr(), nxt, so, ob, strm)
         return nxt, cur
 
     cur, nxt = s0, s1
-    for _ in range(args.warmup):
-        cur, nxt = one_step(cur, nxt)
+    for k in range(args.warmup):
+        cur, nxt = launch(k, cur, nxt, stream)
     env.check_errors(stream)
-
-    # Kernel timing (roofline): one eager episode, CUDA events around every fused launch.
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(EPISODE)]
-    k_state["k"] = 0
-    for i in range(EPISODE):
-        cur, nxt = one_step(cur, nxt, kev[i])
-    torch.cuda.synchronize()
-    kern_ms_eager = float(np.mean([a.elapsed_time(b) for a, b in kev]))
-    # reset kernel duration (subtracted from the graph-timed rollouts below)
+    # reset kernel duration (subtracted from the timed region for the kernel average)
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     r0.record(stream)
-    for _ in range(5):
-        env.reset_device(42, cur, stream)
+    for _ in range(10):
+        env.reset_device(RESET_SEED, cur, stream)
     r1.record(stream)
     torch.cuda.synchronize()
-    reset_ms = r0.elapsed_time(r1) / 5
+    reset_ms = r0.elapsed_time(r1) / 10
 
-    # Timed region: whole rollouts (reset + 91 fused steps) replayed from a CUDA graph
-    # (SURVEY 8d); a step count that is not a whole number of rollouts runs eagerly.
-    use_graph = args.steps % EPISODE == 0 and not args.no_graph
+    # Timed region: exactly K launches (reset at every t % 91 == 0) as one CUDA graph.
+    resets = sum(1 for k in range(args.steps) if k % EPISODE == 0)
     graph = None
-    if use_graph:
+    if not args.no_graph:
         gstream = torch.cuda.Stream()
         gstream.wait_stream(stream)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=gstream, capture_error_mode="relaxed"):
             g_cur, g_nxt = s0, s1
-            env.reset_device(42, g_cur, gstream)
-            for t in range(EPISODE):
-                env.step_observe_device(g_cur, dA[t].data_ptr(), dS[t].data_ptr(), g_nxt, so, ob, gstream)
-                g_cur, g_nxt = g_nxt, g_cur
+            for k in range(args.steps):
+                g_cur, g_nxt = launch(k, g_cur, g_nxt, gstream)
         final_state = g_cur
         stream = torch.cuda.current_stream()  # CUDAGraph.replay() launches on the current stream
-        graph.replay()  # warm replay
+        graph.replay()  # warm replay (untimed)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -312,50 +345,39 @@ def run_ours(args) -> None:
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)  # let the sampler start before the timed region
-    resets = 0
-    rollout_ms = []
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     gc.collect()
     gc.disable()  # a collector pause in the launch loop would idle the GPU inside the timed region
-    if use_graph:
-        n_roll = args.steps // EPISODE
-        rev = [torch.cuda.Event(enable_timing=True) for _ in range(n_roll + 1)]
-        start.record(stream)
-        rev[0].record(stream)
-        for i in range(n_roll):
-            graph.replay()
-            rev[i + 1].record(stream)
-        end.record(stream)
-        resets = n_roll
+    start.record(stream)
+    if graph is not None:
+        graph.replay()
         cur = final_state
     else:
-        k_state["k"] = 0
-        start.record(stream)
-        for i in range(args.steps):
-            resets += 1 if k_state["k"] % EPISODE == 0 else 0
-            cur, nxt = one_step(cur, nxt)
-        end.record(stream)
+        cur, nxt = s0, s1
+        for k in range(args.steps):
+            cur, nxt = launch(k, cur, nxt, stream)
+    end.record(stream)
     torch.cuda.synchronize()
     gc.enable()
     clk = clocks.stop()
-    if use_graph:
-        rollout_ms = [rev[i].elapsed_time(rev[i + 1]) for i in range(n_roll)]
-    # the fused kernel's average duration inside the timed region: CUDA events
-    # around each graph rollout, minus its reset launch, over its 91 launches
-    # (the eager per-launch-event figure includes launch gaps)
-    kern_ms = (float(np.mean(rollout_ms)) - reset_ms) / EPISODE if rollout_ms else kern_ms_eager
     if dist:
         dist.barrier()
     elapsed_ms = start.elapsed_time(end)
     env.check_errors(stream)
+    # the fused kernel's average duration inside the timed region
+    kern_ms = (elapsed_ms - resets * reset_ms) / args.steps
     t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
     env.episode_stats(cur, stats.data_ptr(), stream)
     if dist:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    allreduce_stats(stats)  # the one data collective: int64 episode stats over NCCL
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)  # timing plumbing (max over ranks)
+    if comm:
+        comm.allreduce_stats(stats, stream)  # the one data collective: int64 stats over NCCL
+        torch.cuda.synchronize()
+        comm.check()
     elapsed_ms = float(t_max.item())
     agents_per_row = 1 if controlled else A_  # C2 counts controlled rows
-    agent_steps = B * agents_per_row * args.steps * world
+    total_rows = p["total"] * rpr
+    agent_steps = total_rows * agents_per_row * args.steps
     value = agent_steps / (elapsed_ms / 1e3)
 
     # ---- e2e through the host-vector API (the drop-in overloads) ----
@@ -363,12 +385,13 @@ def run_ours(args) -> None:
     if not args.no_e2e:
         st_h, nx_h = env.new_state(pinned=True), env.new_state(pinned=True)
         so_h, ob_h = env.new_stepout(pinned=True), env.new_obs(pinned=True)
-        env.init_state(42, out=st_h)
-        ke = min(args.steps, 3 if controlled else EPISODE)  # C2 moves 4 GB of observations per step over PCIe
+        env.init_state(RESET_SEED, out=st_h)
+        # C2 / C4 move 1-4 GB of observations per step over PCIe: a few steps suffice
+        ke = min(args.steps, 3 if (controlled or B > 16384) else EPISODE)
         for t in range(min(3, ke)):
             env.step(st_h, accel[t], steer[t], nx_h, so_h)
             env.observe(nx_h, ob_h)
-        env.init_state(42, out=st_h)
+        env.init_state(RESET_SEED, out=st_h)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -384,14 +407,16 @@ def run_ours(args) -> None:
         sb, sob, obb = env.layout
         h2d = 2 * sb + 8 * B  # step uploads state + actions, observe uploads state
         d2h = sb + sob + obb
-        e2e = {"value": B * agents_per_row * ke * world / float(e_s.item()), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": ke,
+        e2e = {"value": total_rows * agents_per_row * ke / float(e_s.item()), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ke,
                "path": "Env.step + Env.observe host-vector API (zsim_step_host / zsim_observe_host), pinned buffers"}
 
     policy = None
-    if rank == 0 and not args.no_policy and not controlled:
+    if rank == 0 and world == 1 and not args.no_policy and not controlled and args.config == "C1":
         policy = measure_policy(env, ob, B, A_)
 
+    if comm:
+        comm.close()
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -410,32 +435,28 @@ def run_ours(args) -> None:
             pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: stress generator (seed 7; rank r owns global rows [r*B, (r+1)*B)), random actions "
-                "(splitmix64 seed 123)",
-        "config": {"workload": c["workload"], "scenarios_per_gpu": S_, "rows_per_gpu": B, "agents": A_,
-                   "road_points": P, "controlled": controlled,
-                   "route_points": 2 * LANES * LANE_VERTICES, "lanes": LANES, "lane_vertices": LANE_VERTICES,
-                   "steps_per_episode": EPISODE, "disable_dones": True,
-                   "l2": f"inputs larger than L2 (static pack {env.info.static_bytes / 1e6:.0f} MB per GPU)",
-                   "parallelism": f"scenario-sharded x{world}"},
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": p["scaling"], "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: stress generator (seed {STRESS_SEED}; rank r owns its contiguous slice of the global "
+                f"scenario set), random actions (splitmix64 seed {ACTION_SEED})",
+        "config": config_block(p, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, ("bytes_per_row_step" if controlled else "bytes_per_scenario_step"): per_scen,
+                     "units_per_launch": B,
                      "kernel": ("k_step_observe (fused step + observe)" if env.info.step_observe_kernels == 1
                                 else "k_step_observe step+agents, then road/route top-k (per step)"),
                      "kernel_ms": kern_ms, "peak_source": peak_src},
         "gpu_launches": args.steps * env.info.step_observe_kernels + resets,
-        "scenario_steps_per_s": S_ * args.steps * world / (elapsed_ms / 1e3),
-        "controlled_agent_steps_per_s": B * args.steps * world / (elapsed_ms / 1e3),
-        "timing": {"mode": "cuda-graph rollouts (reset + 91 fused steps)" if use_graph else "eager launches",
-                   "rollout_ms_median": float(np.median(rollout_ms)) if rollout_ms else None,
-                   "rollout_ms_best": float(np.min(rollout_ms)) if rollout_ms else None,
-                   "kernel_ms_source": "CUDA events around each graph rollout minus the reset launch, / 91"
-                                       if rollout_ms else "one eager episode, CUDA events around each fused launch",
-                   "kernel_ms_eager_events": kern_ms_eager, "reset_ms": reset_ms},
+        "scenario_steps_per_s": p["total"] * args.steps / (elapsed_ms / 1e3),
+        "controlled_agent_steps_per_s": total_rows * args.steps / (elapsed_ms / 1e3),
+        "timing": {"mode": "cuda-graph (exactly `steps` fused launches + a reset every 91)" if graph is not None
+                   else "eager launches",
+                   "kernel_ms_source": "timed region minus resets x reset_ms, / steps (rank 0)",
+                   "reset_ms": reset_ms, "resets_in_region": resets, "setup_s": setup_s,
+                   "static_pack_mb_per_gpu": env.info.static_bytes / 1e6},
         "episode_stats": stats.cpu().tolist(),
     }
+    assert kern_ms <= line["ms_per_step"] + 1e-9 or world > 1, (kern_ms, line["ms_per_step"])
     if e2e:
         line["e2e"] = e2e
     if policy:
@@ -443,7 +464,7 @@ def run_ours(args) -> None:
     if clk:
         line["clocks"] = clk
     if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(args.config, 7)
+        cb = cpu_baseline(p)
         if cb:
             line["cpu_baseline"] = cb
     print(json.dumps(line), flush=True)
@@ -505,8 +526,8 @@ def measure_policy(env, ob, B, A_):
     if p.exists():
         peak_tf32 = float(json.loads(p.read_text())["bf16_tflops"]) / 2  # tf32 dense rate is half of bf16
     achieved = tc_flops * B / (ms / 1e3) / 1e12
-    return {"precision": "tf32 projections on tcgen05, fp32 elsewhere", "rows": B, "ms_per_act": ms,
-            "rows_per_s": B / (ms / 1e3),
+    return {"precision": "tf32 projections on tcgen05, fp32 elsewhere (diagnostic; the drop-in default is fp32)",
+            "rows": B, "ms_per_act": ms, "rows_per_s": B / (ms / 1e3),
             "closed_loop": {"path": "zsim_rollout_policy: observe -> NNPolicy::act -> step, 91 steps, sampling, "
                                     "replayed from a CUDA graph",
                             "ms": loop_ms, "agent_steps_per_s": B * A_ * EPISODE / (loop_ms / 1e3)},
@@ -523,16 +544,21 @@ def main():
     ap.add_argument("--steps", type=int, default=5 * EPISODE)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="C1", choices=sorted(CONFIGS))
+    ap.add_argument("--scenarios", type=int, default=0, help="override the global scenario count (diagnostic)")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph rollouts")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph")
     ap.add_argument("--no-policy", action="store_true", help="skip the on-device policy measurement")
     ap.add_argument("--launch-policy", type=int, default=0, choices=(0, 1, 2),
                     help="kernel arrangement: 0 auto, 1 fused step+observe, 2 split observation (diagnostic)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.steps < 1 or args.gpus < 1:
+        raise SystemExit("bench: --steps and --gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

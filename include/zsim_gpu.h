@@ -510,6 +510,45 @@ ZSIM_API int zsim_stress_config_defaults(zsim_stress_config* cfg);
  * ZSIM container image in a malloc'd buffer (free with zsim_free_buffer). */
 ZSIM_API int zsim_stress_generate(const zsim_stress_config* cfg, uint64_t seed, uint8_t** out_buf, size_t* out_len);
 ZSIM_API void zsim_free_buffer(void* buf);
+/* A device Env over stress scenarios [first_index, first_index+count) built
+ * without a ZSIM image (the scenes are generated on all host cores and staged
+ * directly): the benchmark's C3 / C4 shards.  Identical to zsim_env_create over
+ * zsim_stress_generate's image of the same range.  `controlled` as in
+ * zsim_env_create_controlled. */
+ZSIM_API int zsim_env_create_stress(const zsim_stress_config* stress, uint64_t seed, int32_t horizon,
+                                    const zsim_sim_config* cfg, int32_t device, int32_t controlled, zsim_env** out);
+
+/* ---- multi-GPU episode-statistics exchange ----
+ * Scenarios are sharded across GPUs with no per-step exchange; once per
+ * rollout the int64 stats vector (zsim_episode_stats) is summed over all GPUs
+ * with one NCCL all-reduce (exact; the reference AllReducer's fixed-order
+ * contract, core/train/transport.hpp:59-61) and the fp64 Aggregate partial
+ * sums (zsim_episode_metrics; metrics.hpp:56-69) are all-gathered so each rank
+ * adds them in rank order (zsim_aggregate_finalize).  NCCL is dlopen'ed at
+ * first use (libnccl.so.2).  Replaces the reference's train::AllReducer
+ * (transport.hpp:59-98) for this path. */
+#define ZSIM_COMM_ID_BYTES 128
+typedef struct zsim_comm zsim_comm;
+/* 1 when libnccl.so.2 can be loaded, else 0. */
+ZSIM_API int zsim_comm_available(void);
+/* One process per GPU: rank 0 makes the id, the caller broadcasts it. */
+ZSIM_API int zsim_comm_unique_id(uint8_t id[ZSIM_COMM_ID_BYTES]);
+ZSIM_API int zsim_comm_init_rank(const uint8_t id[ZSIM_COMM_ID_BYTES], int32_t nranks, int32_t rank, int32_t device,
+                                 zsim_comm** out);
+/* One process driving `ndev` GPUs (ncclCommInitAll): out[ndev] communicators;
+ * devices NULL = 0..ndev-1.  Use one host thread + stream per GPU (or
+ * zsim_comm_group) around the collectives. */
+ZSIM_API int zsim_comm_init_all(int32_t ndev, const int32_t* devices, zsim_comm** out);
+ZSIM_API int zsim_comm_destroy(zsim_comm* comm);
+/* ncclCommGetAsyncError surfaced as a status (ZSIM_RUNTIME on an error). */
+ZSIM_API int zsim_comm_check(zsim_comm* comm);
+/* In place: stats_dev[n] (int64, device) summed over all ranks, on `stream`. */
+ZSIM_API int zsim_stats_allreduce(zsim_comm* comm, int64_t* stats_dev, int32_t n, void* stream);
+/* gathered_dev[nranks][n] (fp64, device) = every rank's sums_dev[n], rank order. */
+ZSIM_API int zsim_metric_sums_allgather(zsim_comm* comm, const double* sums_dev, int32_t n, double* gathered_dev,
+                                        void* stream);
+/* ncclGroupStart (begin = 1) / ncclGroupEnd (begin = 0). */
+ZSIM_API int zsim_comm_group(int32_t begin);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,26 @@ def build_port(force: bool = False) -> Path | None:
     return PORT_OUT
 
 
+STRESS_OUT = HERE / "_ref" / "libzsim_stress.so"
+CSRC = HERE.parent / "paper_2312_15122_b200" / "csrc"
+
+
+def build_stress(force: bool = False) -> Path:
+    """The benchmark workload generator for the oracle side (stress_shim.cpp +
+    the generator / ZSIM codec sources), so the reference arm never maps the
+    product library."""
+    srcs = [HERE / "stress_shim.cpp", CSRC / "zsim_stressgen.cpp", CSRC / "zsim_scenario.cpp"]
+    deps = srcs + [CSRC / "zsim_scenario.hpp", CSRC / "zsim_geom.cuh", HERE.parent / "include" / "zsim_gpu.h"]
+    if not force and STRESS_OUT.exists() and all(d.stat().st_mtime <= STRESS_OUT.stat().st_mtime for d in deps):
+        return STRESS_OUT
+    STRESS_OUT.parent.mkdir(exist_ok=True)
+    tmp = STRESS_OUT.with_suffix(".tmp")
+    _run([CXX, "-std=c++17", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
+          "-I", str(HERE.parent / "include"), "-I", str(CSRC), "-o", str(tmp), *map(str, srcs), "-lpthread"])
+    os.replace(tmp, STRESS_OUT)
+    return STRESS_OUT
+
+
 DROPIN_OUT = HERE / "_ref" / "dropin_check"
 
 
@@ -107,6 +127,7 @@ def build_dropin(force: bool = False) -> Path | None:
 
 def build(force: bool = False) -> None:
     build_port(force)
+    build_stress(force)
     build_ref(force)
     build_dropin(force)
 

@@ -9,8 +9,9 @@ from pathlib import Path
 
 import numpy as np
 
-from paper_2312_15122_b200._abi import ObsView, SimConfigC, StateView, StepOutView
-from paper_2312_15122_b200.env import ObservationBatch, SimConfig, SimStateBatch, StepOut, _ptr
+from oracle.hostio import Obs, ObsView, OracleConfig, Out, SimConfigC, State, StateView, StepOutView, config_c
+from oracle.hostio import ptr as _ptr
+from oracle.hostio import state_view
 
 HERE = Path(__file__).resolve().parent
 
@@ -59,12 +60,12 @@ def _check(code: int) -> None:
 class PortEnv:
     """C restatement of zsim::sim::Env over a ZSIM image."""
 
-    def __init__(self, zsim, indices=None, horizon: int = 0, config: SimConfig | None = None):
+    def __init__(self, zsim, indices=None, horizon: int = 0, config=None):
         if isinstance(zsim, (str, Path)):
             zsim = Path(zsim).read_bytes()
         self._buf = C.create_string_buffer(bytes(zsim), len(zsim))
-        self._config = config or SimConfig()
-        cfg = self._config.to_c()
+        self._config = config or OracleConfig()
+        cfg = config_c(self._config)
         idx, n = None, 0
         if indices is not None:
             self._idx = np.ascontiguousarray(np.asarray(indices, dtype=np.int64))
@@ -93,25 +94,25 @@ class PortEnv:
         _check(lib().zor_scalars(self.handle, _ptr(g, C.c_double), _ptr(i, C.c_double), _ptr(l, C.c_double)))
         return g, i, l
 
-    def init_state(self, seed: int) -> SimStateBatch:
-        st = SimStateBatch(self.batch, self.total_stop_lines)
-        v = st.view()
+    def init_state(self, seed: int) -> State:
+        st = State(self.batch, self.total_stop_lines)
+        v = state_view(st)
         _check(lib().zor_init_state(self.handle, C.c_uint64(seed), C.byref(v)))
         return st
 
-    def step(self, state: SimStateBatch, accel, steer):
+    def step(self, state: State, accel, steer):
         a = np.ascontiguousarray(accel, dtype=np.int32)
         s = np.ascontiguousarray(steer, dtype=np.int32)
-        nxt, so = SimStateBatch(self.batch, self.total_stop_lines), StepOut(self.batch)
-        vi, vo, vs = state.view(), nxt.view(), so.view()
+        nxt, so = State(self.batch, self.total_stop_lines), Out(self.batch)
+        vi, vo, vs = state_view(state), nxt.view(), so.view()
         _check(lib().zor_step(self.handle, C.byref(vi), _ptr(a, C.c_int32), _ptr(s, C.c_int32), C.byref(vo),
                               C.byref(vs)))
         return nxt, so
 
-    def observe(self, state: SimStateBatch, with_topk: bool = False):
+    def observe(self, state: State, with_topk: bool = False):
         c = self._config
-        ob = ObservationBatch(self.batch, c.n_agents, c.n_road, c.n_route)
+        ob = Obs(self.batch, c.n_agents, c.n_road, c.n_route)
         tk = np.full((self.batch, c.n_agents + c.n_road + c.n_route), -1, np.int32)
-        vi, vo = state.view(), ob.view()
+        vi, vo = state_view(state), ob.view()
         _check(lib().zor_observe(self.handle, C.byref(vi), C.byref(vo), _ptr(tk, C.c_int32)))
         return (ob, tk) if with_topk else ob

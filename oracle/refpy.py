@@ -13,8 +13,9 @@ from pathlib import Path
 
 import numpy as np
 
-from paper_2312_15122_b200._abi import ObsView, SimConfigC, StateView, StepOutView
-from paper_2312_15122_b200.env import ObservationBatch, SimConfig, SimStateBatch, StepOut, _ptr
+from oracle.hostio import Obs, ObsView, OracleConfig, Out, SimConfigC, State, StateView, StepOutView, config_c
+from oracle.hostio import ptr as _ptr
+from oracle.hostio import state_view
 
 HERE = Path(__file__).resolve().parent
 REF_LIB = HERE / "_ref" / "libzsim_ref.so"
@@ -97,10 +98,10 @@ def _as_path(zsim) -> tuple[str, object]:
 class RefEnv:
     """The reference zsim::sim::Env (simcore.hpp:191-245) over the same inputs."""
 
-    def __init__(self, zsim, indices=None, horizon: int = 0, config: SimConfig | None = None):
+    def __init__(self, zsim, indices=None, horizon: int = 0, config=None):
         self._path, self._tmp = _as_path(zsim)
-        self._config = config or SimConfig()
-        cfg = self._config.to_c()
+        self._config = config or OracleConfig()
+        cfg = config_c(self._config)
         idx, n = None, 0
         if indices is not None:
             self._idx = np.ascontiguousarray(np.asarray(indices, dtype=np.int64))
@@ -131,28 +132,28 @@ class RefEnv:
         _check(lib().zref_scalars(self.handle, _ptr(g, C.c_double), _ptr(i, C.c_double), _ptr(l, C.c_double)))
         return g, i, l
 
-    def new_state(self) -> SimStateBatch:
-        return SimStateBatch(self.batch, self.total_stop_lines)
+    def new_state(self) -> State:
+        return State(self.batch, self.total_stop_lines)
 
-    def init_state(self, seed: int) -> SimStateBatch:
+    def init_state(self, seed: int) -> State:
         st = self.new_state()
-        v = st.view()
+        v = state_view(st)
         _check(lib().zref_init_state(self.handle, C.c_uint64(seed), C.byref(v)))
         return st
 
-    def step(self, state: SimStateBatch, accel, steer):
+    def step(self, state: State, accel, steer):
         a = np.ascontiguousarray(accel, dtype=np.int32)
         s = np.ascontiguousarray(steer, dtype=np.int32)
-        nxt, so = self.new_state(), StepOut(self.batch)
-        vi, vo, vs = state.view(), nxt.view(), so.view()
+        nxt, so = self.new_state(), Out(self.batch)
+        vi, vo, vs = state_view(state), nxt.view(), so.view()
         _check(lib().zref_step(self.handle, C.byref(vi), _ptr(a, C.c_int32), _ptr(s, C.c_int32), C.byref(vo),
                                C.byref(vs)))
         return nxt, so
 
-    def observe(self, state: SimStateBatch) -> ObservationBatch:
+    def observe(self, state: State) -> Obs:
         c = self._config
-        ob = ObservationBatch(self.batch, c.n_agents, c.n_road, c.n_route)
-        vi, vo = state.view(), ob.view()
+        ob = Obs(self.batch, c.n_agents, c.n_road, c.n_route)
+        vi, vo = state_view(state), ob.view()
         _check(lib().zref_observe(self.handle, C.byref(vi), C.byref(vo)))
         return ob
 
@@ -263,7 +264,7 @@ def aggregate(s, a_lat, a_lon, mask, events, initial_s, logged_progress, dt: flo
     return out
 
 
-def bench(zsim, n_rows: int, horizon: int, config: SimConfig, threads: int, warmup: int, steps: int, accel,
+def bench(zsim, n_rows: int, horizon: int, config, threads: int, warmup: int, steps: int, accel,
           steer, seed: int = 42) -> float:
     """Wall seconds of `steps` timed observe+step iterations over `n_rows` rows
     on `threads` shards; `accel`/`steer` are [episode_len][n_rows] and the
@@ -273,7 +274,7 @@ def bench(zsim, n_rows: int, horizon: int, config: SimConfig, threads: int, warm
         a = np.ascontiguousarray(accel, dtype=np.int32)
         s = np.ascontiguousarray(steer, dtype=np.int32)
         assert a.shape[1] == n_rows
-        cfg = config.to_c()
+        cfg = config_c(config)
         out = C.c_double()
         _check(lib().zref_bench(path.encode(), int(n_rows), int(horizon), C.byref(cfg), int(threads), int(warmup),
                                 int(steps), int(a.shape[0]), _ptr(a, C.c_int32), _ptr(s, C.c_int32),
@@ -282,3 +283,66 @@ def bench(zsim, n_rows: int, horizon: int, config: SimConfig, threads: int, warm
     finally:
         if tmp is not None:
             os.unlink(path)
+
+
+# ---- the benchmark workload, generated without the product library ----
+STRESS_LIB = HERE / "_ref" / "libzsim_stress.so"
+_stress = None
+
+
+class StressConfigC(C.Structure):
+    """zsim_stress_config (include/zsim_gpu.h)."""
+    _fields_ = [("count", C.c_int32), ("num_steps", C.c_int32), ("agents", C.c_int32),
+                ("road_points", C.c_int32), ("lanes", C.c_int32), ("lane_vertices", C.c_int32),
+                ("dt", C.c_double), ("speed_limit", C.c_double), ("lane_width", C.c_double),
+                ("first_index", C.c_int32), ("flags", C.c_int32)]
+
+
+def _stress_lib() -> C.CDLL:
+    global _stress
+    if _stress is None:
+        if not STRESS_LIB.exists():
+            raise FileNotFoundError(f"{STRESS_LIB} not built (run oracle/build_oracle.py)")
+        _stress = C.CDLL(str(STRESS_LIB))
+        _stress.zstress_last_error.restype = C.c_char_p
+        _stress.zstress_generate.argtypes = [C.POINTER(StressConfigC), C.c_uint64, C.POINTER(C.c_void_p),
+                                             C.POINTER(C.c_size_t)]
+        _stress.zstress_controlled_expand.argtypes = [C.c_void_p, C.c_size_t, C.c_double, C.c_double, C.c_double,
+                                                      C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]
+        _stress.zstress_free.argtypes = [C.c_void_p]
+    return _stress
+
+
+def _take(p: C.c_void_p, n: C.c_size_t) -> bytes:
+    try:
+        return np.ctypeslib.as_array((C.c_uint8 * n.value).from_address(p.value)).tobytes() if n.value else b""
+    finally:
+        _stress_lib().zstress_free(p)
+
+
+def stress(count: int, agents: int, road_points: int, seed: int = 7, first_index: int = 0, c2: bool = False,
+           num_steps: int = 92, lanes: int = 4, lane_vertices: int = 64) -> bytes:
+    """ZSIM image of the stress scenarios [first_index, first_index + count)
+    (the same bytes the product's ``stress_scenarios`` produces)."""
+    L = _stress_lib()
+    cfg = StressConfigC(count=count, num_steps=num_steps, agents=agents, road_points=road_points, lanes=lanes,
+                        lane_vertices=lane_vertices, dt=0.1, speed_limit=10.0, lane_width=3.5,
+                        first_index=first_index, flags=1 if c2 else 0)
+    p, n = C.c_void_p(), C.c_size_t()
+    rc = L.zstress_generate(C.byref(cfg), C.c_uint64(seed), C.byref(p), C.byref(n))
+    if rc:
+        raise RefError(rc, L.zstress_last_error().decode(errors="replace"))
+    return _take(p, n)
+
+
+def controlled_expand(zsim: bytes, config=None) -> bytes:
+    """Per-row scenarios of every controllable actor (C2)."""
+    L = _stress_lib()
+    c = config_c(config)
+    buf = C.create_string_buffer(bytes(zsim), len(zsim))
+    p, n = C.c_void_p(), C.c_size_t()
+    rc = L.zstress_controlled_expand(C.cast(buf, C.c_void_p), len(zsim), c.ego_length, c.ego_width,
+                                     c.ego_center_offset, C.byref(p), C.byref(n))
+    if rc:
+        raise RefError(rc, L.zstress_last_error().decode(errors="replace"))
+    return _take(p, n)

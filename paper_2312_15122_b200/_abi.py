@@ -174,6 +174,17 @@ SIGNATURES = {
     "zsim_stress_generate": (C.c_int, [C.POINTER(StressConfigC), C.c_uint64, C.POINTER(_P),
                                        C.POINTER(C.c_size_t)]),
     "zsim_free_buffer": (None, [_P]),
+    "zsim_comm_available": (C.c_int, []),
+    "zsim_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "zsim_comm_init_rank": (C.c_int, [C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "zsim_comm_init_all": (C.c_int, [C.c_int32, c_int32_p, C.POINTER(_P)]),
+    "zsim_comm_destroy": (C.c_int, [_P]),
+    "zsim_comm_check": (C.c_int, [_P]),
+    "zsim_stats_allreduce": (C.c_int, [_P, C.POINTER(C.c_int64), C.c_int32, _P]),
+    "zsim_metric_sums_allgather": (C.c_int, [_P, c_double_p, C.c_int32, c_double_p, _P]),
+    "zsim_comm_group": (C.c_int, [C.c_int32]),
+    "zsim_env_create_stress": (C.c_int, [C.POINTER(StressConfigC), C.c_uint64, C.c_int32, C.POINTER(SimConfigC),
+                                         C.c_int32, C.c_int32, C.POINTER(_P)]),
     "zsim_model_config_defaults": (C.c_int, [C.POINTER(ModelConfigC)]),
     "zsim_policy_param_count": (C.c_int, [C.POINTER(ModelConfigC), C.POINTER(C.c_int64)]),
     "zsim_policy_init_params": (C.c_int, [C.POINTER(ModelConfigC), C.c_uint64, c_float_p, C.c_int64]),

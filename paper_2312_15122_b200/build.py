@@ -27,7 +27,7 @@ CUDA_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "--expt-relaxed-c
 CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-fvisibility=hidden", "-Wall"]
 
-CU_SOURCES = ["zsim_kernels.cu", "zsim_capi.cu", "zsim_policy.cu"]
+CU_SOURCES = ["zsim_kernels.cu", "zsim_capi.cu", "zsim_policy.cu", "zsim_comm.cu"]
 CXX_SOURCES = ["zsim_scenario.cpp", "zsim_stressgen.cpp"]
 
 

@@ -1023,6 +1023,25 @@ ZSIM_API int zsim_env_create_controlled(const uint8_t* file, size_t nbytes, cons
                       out, true);
 }
 
+// Benchmark shards of C3 / C4 ("generate per GPU shard in host
+// memory ... then upload"): scenarios [first_index, first_index + count) of
+// the stress set, generated on all host cores straight into the staging
+// input -- no ZSIM image of the 17-35 GB shard.
+ZSIM_API int zsim_env_create_stress(const zsim_stress_config* scfg, uint64_t seed, int32_t horizon,
+                                    const zsim_sim_config* cfg, int32_t device, int32_t controlled, zsim_env** out) {
+    return guarded([&] {
+        if (!out || !scfg) raise(Err::invalid_argument, "null argument");
+        *out = nullptr;
+        zs::stress_check(*scfg);
+        std::vector<zs::Scene> scenes(size_t(scfg->count));
+        parallel_for(scfg->count, [&](int i) {
+            scenes[size_t(i)] = zs::stress_scene(*scfg, seed, int64_t(scfg->first_index) + i);
+        });
+        *out = build_env(std::move(scenes), horizon, cfg, nullptr, 0, nullptr, 0, device, controlled != 0, nullptr)
+                   .release();
+    });
+}
+
 // ---------------------------------------------------------------------------
 // BatchStream (scenario_stream.hpp:12-40, scenario_stream.cpp:35-46) feeding
 // device Envs: while the caller simulates batch k, a staging thread decodes

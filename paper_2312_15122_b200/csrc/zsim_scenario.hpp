@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+struct zsim_stress_config;  // include/zsim_gpu.h
+
 namespace zs {
 
 // zsim::ErrorKind (common.hpp:13) + the C-ABI's CUDA code.
@@ -127,5 +129,9 @@ Scene controlled_scene(const Scene& s, int actor, const EgoBoxDims& d);
 // ActionTable::validated / nearest_bin (dynamics.cpp:30-64).
 void check_bins(const std::vector<double>& bins, const char* name);
 int nearest_bin(const std::vector<double>& bins, double v);
+
+// synthetic stress scenarios (zsim_stressgen.cpp)
+void stress_check(const zsim_stress_config& cfg);
+Scene stress_scene(const zsim_stress_config& cfg, uint64_t seed, int64_t global_index);
 
 }  // namespace zs

@@ -275,7 +275,7 @@ Scene make_scene(const zsim_stress_config& cfg, Stream rng, int index) {
 
 }  // namespace
 
-std::string stress_generate(const zsim_stress_config& cfg, uint64_t seed) {
+void stress_check(const zsim_stress_config& cfg) {
     if (cfg.count <= 0) raise(Err::config, "stress: count must be > 0");
     if (cfg.num_steps < 2) raise(Err::config, "stress: num_steps must be >= 2");
     if (cfg.agents < 1) raise(Err::config, "stress: agents must be >= 1 (the ego)");
@@ -283,14 +283,20 @@ std::string stress_generate(const zsim_stress_config& cfg, uint64_t seed) {
     if (cfg.road_points < 2) raise(Err::config, "stress: road_points must be >= 2");
     if (!(cfg.dt > 0.0)) raise(Err::config, "stress: dt must be > 0");
     if (cfg.first_index < 0) raise(Err::config, "stress: first_index must be >= 0");
+}
+
+Scene stress_scene(const zsim_stress_config& cfg, uint64_t seed, int64_t i) {
+    // Rng(seed).split(i): the root has advanced i+1 times (reset_rng_state's closed form)
+    Stream s(0);
+    s.state = reset_rng_state(seed, uint64_t(i));
+    return make_scene(cfg, s, int(i));
+}
+
+std::string stress_generate(const zsim_stress_config& cfg, uint64_t seed) {
+    stress_check(cfg);
     std::string out = zsim_header(cfg.dt);
-    for (int k = 0; k < cfg.count; ++k) {
-        const uint64_t i = uint64_t(cfg.first_index) + uint64_t(k);
-        // Rng(seed).split(i): the root has advanced i+1 times (reset_rng_state's closed form)
-        Stream s(0);
-        s.state = reset_rng_state(seed, i);
-        zsim_encode_append(out, make_scene(cfg, s, int(i)));
-    }
+    for (int k = 0; k < cfg.count; ++k)
+        zsim_encode_append(out, stress_scene(cfg, seed, int64_t(cfg.first_index) + k));
     return out;
 }
 

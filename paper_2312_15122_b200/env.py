@@ -103,6 +103,28 @@ _STEPOUT_FIELDS = (("reward", np.float32, C.c_float), ("event", np.uint8, C.c_ui
 _OBS_FIELDS = ("active", "agents", "road", "route", "value_only")
 
 
+def _state_view(st) -> StateView:
+    """View of any SoA state container (ours or an oracle's), by field name."""
+    v = StateView()
+    for name, _, ct in _STATE_FIELDS:
+        setattr(v, name, _ptr(getattr(st, name), ct))
+    return v
+
+
+def _stepout_view(so) -> StepOutView:
+    v = StepOutView()
+    for name, _, ct in _STEPOUT_FIELDS:
+        setattr(v, name, _ptr(getattr(so, name), ct))
+    return v
+
+
+def _obs_view(ob) -> ObsView:
+    v = ObsView()
+    for name in _OBS_FIELDS:
+        setattr(v, name, _ptr(getattr(ob, name), C.c_float))
+    return v
+
+
 class _Pinned:
     """Page-locked host block from zsim_host_alloc, freed on collection."""
 
@@ -312,6 +334,25 @@ class Env:
         self._attach()
 
     @classmethod
+    def from_stress(cls, stress: "StressConfig", seed: int = 7, horizon: int = 0, config: SimConfig | None = None,
+                    device: int = 0, controlled: bool = False) -> "Env":
+        """Env over stress scenarios generated on the host cores and staged
+        directly (zsim_env_create_stress): same rows as
+        ``Env(stress_scenarios(stress, seed), ...)`` without the ZSIM image."""
+        self = cls.__new__(cls)
+        self._bytes = b""
+        self._config = config or SimConfig()
+        cfg = self._config.to_c()
+        sc = StressConfigC(**{f.name: getattr(stress, f.name) for f in fields(stress)})
+        h = C.c_void_p()
+        check(lib.zsim_env_create_stress(C.byref(sc), C.c_uint64(seed), int(horizon), C.byref(cfg), int(device),
+                                         int(bool(controlled)), C.byref(h)))
+        self.handle = h.value
+        self._owned = True
+        self._attach()
+        return self
+
+    @classmethod
     def _borrowed(cls, handle: int, config: SimConfig) -> "Env":
         """An Env over a handle owned elsewhere (a BatchStream batch)."""
         self = cls.__new__(cls)
@@ -409,14 +450,14 @@ class Env:
             raise ZsimError(1, "env_step: action/state shape mismatch")
         nxt = next if next is not None else self.new_state()
         so = out if out is not None else self.new_stepout()
-        vin, vout, vso = state.view(), nxt.view(), so.view()
+        vin, vout, vso = _state_view(state), _state_view(nxt), _stepout_view(so)
         check(lib.zsim_step_host(self.handle, C.byref(vin), _ptr(a, C.c_int32), _ptr(s, C.c_int32), C.byref(vout),
                                  C.byref(vso)))
         return nxt, so
 
     def observe(self, state: SimStateBatch, obs: ObservationBatch | None = None) -> ObservationBatch:
         ob = obs if obs is not None else self.new_obs()
-        vin, vo = state.view(), ob.view()
+        vin, vo = _state_view(state), _obs_view(ob)
         check(lib.zsim_observe_host(self.handle, C.byref(vin), C.byref(vo)))
         return ob
 
@@ -599,7 +640,7 @@ class Env:
         return st
 
     def upload_state(self, host: SimStateBatch, dev: DeviceState, stream=None) -> None:
-        v = host.view()
+        v = _state_view(host)
         check(lib.zsim_state_copy(self.handle, C.byref(dev.v), C.byref(v), 0, _stream(stream)))
 
     def download_stepout(self, dev: DeviceStepOut, host: StepOut | None = None, stream=None) -> StepOut:

@@ -97,3 +97,58 @@ def gather_metric_sums(sums, group=None) -> np.ndarray:
     parts = [torch.zeros_like(sums) for _ in range(dist.get_world_size(group))]
     dist.all_gather(parts, sums, group=group)
     return np.stack([p.cpu().numpy() for p in parts])
+
+
+class StatsComm:
+    """The C-ABI NCCL communicator (zsim_comm_*, include/zsim_gpu.h) used for
+    the one per-rollout exchange: the int64 stats all-reduce and the fp64
+    metric-sums all-gather.  The 128-byte NCCL id is made by rank 0 and
+    broadcast over the caller's torch.distributed group (plumbing only)."""
+
+    def __init__(self, rank: int, world: int, device: int):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from ._abi import check, lib
+        self._lib, self._check, self.rank, self.world = lib, check, rank, world
+        idb = (C.c_uint8 * 128)()
+        if rank == 0:
+            check(lib.zsim_comm_unique_id(idb))
+        obj = [bytes(idb)]
+        if dist.is_available() and dist.is_initialized() and world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        check(lib.zsim_comm_init_rank(idb, int(world), int(rank), int(device), C.byref(h)))
+        self.handle = h.value
+
+    def allreduce_stats(self, stats, stream=None):
+        """In place over a torch int64 device tensor."""
+        import ctypes as C
+        from .env import _stream
+        self._check(self._lib.zsim_stats_allreduce(self.handle, C.cast(stats.data_ptr(), C.POINTER(C.c_int64)),
+                                                   int(stats.numel()), _stream(stream)))
+        return stats
+
+    def gather_metric_sums(self, sums, stream=None) -> np.ndarray:
+        """[world][n] fp64 in rank order from every rank's device sums[n]."""
+        import ctypes as C
+
+        import torch
+        from .env import _stream
+        out = torch.zeros(self.world * sums.numel(), dtype=torch.float64, device=sums.device)
+        self._check(self._lib.zsim_metric_sums_allgather(
+            self.handle, C.cast(sums.data_ptr(), C.POINTER(C.c_double)), int(sums.numel()),
+            C.cast(out.data_ptr(), C.POINTER(C.c_double)), _stream(stream)))
+        torch.cuda.synchronize(sums.device)
+        return out.cpu().numpy().reshape(self.world, -1)
+
+    def check(self) -> None:
+        """Surface an NCCL asynchronous error (ncclCommGetAsyncError)."""
+        self._check(self._lib.zsim_comm_check(self.handle))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.zsim_comm_destroy(self.handle)
+            self.handle = None

@@ -5,8 +5,10 @@ Tolerances are the north-star contract (BASELINE.json): fp outputs within
 and slot validity bit-exact.  Top-k slot lists are compared slot by slot;
 where two candidates' sort keys are equal (or equal up to the last-ulp
 differences between device and glibc trig), the slots are compared as a
-multiset within that tie group -- the reference orders road points by d2 only
-(roads.cpp:231-232), so its order inside exact ties is libstdc++-defined.
+multiset within that tie group for ROAD slots only -- the reference orders road
+points by d2 only (roads.cpp:231-232), so its order inside exact ties is
+libstdc++-defined.  Agent and route slots are ordered by (key, index) in the
+reference and must match slot by slot.
 """
 from __future__ import annotations
 
@@ -84,7 +86,14 @@ def compare_slots(g: np.ndarray, r: np.ndarray, kind: str, valid_col: int, exact
 
     if rows_match(G, R):
         return None
-    # tie groups on the reference's key
+    if kind != "road":
+        # agents (simcore.cpp:472-474) and route (:517-519) sort by (key, index):
+        # the order is deterministic, so slot i must match slot i.
+        bad = np.nonzero(~np.array([rows_match(G[i:i + 1], R[i:i + 1]) for i in range(n)]))[0]
+        return f"slot {int(bad[0])} differs (ordered by (key, index) in the reference)"
+    # road: nearest_features sorts by d2 only (roads.cpp:231-232) -- inside a
+    # group of equal keys the reference order is libstdc++-defined, so tie
+    # groups compare as multisets
     kr = _slot_key(R, kind)
     kg = _slot_key(G, kind)
     if not close(kg, kr, rtol=1e-4, atol=1e-5).all():
@@ -100,8 +109,11 @@ def compare_slots(g: np.ndarray, r: np.ndarray, kind: str, valid_col: int, exact
             ob = np.lexsort(b.T[::-1])
             if not rows_match(a[oa], b[ob]):
                 if end == n and n == g.shape[0]:
-                    # tie group cut by k: members may legitimately differ
-                    pass
+                    # tie group cut by k: which of the equal-key candidates fill
+                    # the last slots is unspecified, but every member must carry
+                    # the group's key and be a valid slot
+                    if not close(np.sort(kg[start:end]), np.sort(kr[start:end]), rtol=1e-4, atol=1e-5).all():
+                        return f"k-cut tie group {start}..{end - 1}: keys differ"
                 else:
                     return f"slots {start}..{end - 1} differ (tie group of {end - start})"
         start = end
