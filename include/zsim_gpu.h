@@ -271,14 +271,16 @@ ZSIM_API int zsim_step_observe(zsim_env* env, const zsim_state_view* in, const i
  * empty slots.  NULL disables.  Used by the parity suite. */
 ZSIM_API int zsim_set_debug_topk(zsim_env* env, int32_t* dev_idx);
 
-/* Synchronises `stream`, reads and clears the device error word.  Returns
- * ZSIM_INVALID_ARGUMENT ("action index out of range") if any step since the
- * last check saw a bad action index. */
 /* Kernel arrangement of step+observe / observe: 0 = automatic (one fused
  * kernel up to three waves of rows on the GPU, otherwise step+agents and
  * road/route top-k as separate kernels), 1 = always fused, 2 = always split.
  * Results are identical; only speed differs. */
 ZSIM_API int zsim_set_launch_policy(zsim_env* env, int32_t policy);
+/* Synchronises `stream`, reads and clears the device error word.  Returns
+ * ZSIM_INVALID_ARGUMENT ("action index out of range") if any step since the
+ * last check saw a bad action index, else ZSIM_RUNTIME if any step produced a
+ * non-finite ego state (NaN / Inf: failure detection, the step itself is
+ * unchanged -- the reference does not check). */
 ZSIM_API int zsim_check_errors(zsim_env* env, void* stream);
 
 /* Episode-stats vector of a state (the counts behind
@@ -462,10 +464,11 @@ ZSIM_API int zsim_policy_destroy(zsim_policy* policy);
  * rng streams written back.  Synchronous. */
 ZSIM_API int zsim_policy_act_host(zsim_policy* policy, const zsim_obs_view* obs, int32_t batch, uint64_t* rng,
                                   int32_t use_argmax, int32_t* accel, int32_t* steer, float* logp, float* value);
-/* Arithmetic of the ten 128x128 token-tile projections: 0 (default) =
- * tcgen05 tensor cores, tf32 operands, fp32 accumulation; 1 = fp32 CUDA
- * cores (the reference's Model<float> arithmetic).  Everything else is fp32
- * in both modes. */
+/* Arithmetic of the token-tile projections and trunks: 1 (default) = fp32
+ * CUDA cores (the reference's Model<float> arithmetic); 0 = tcgen05 tensor
+ * cores, tf32 operands, fp32 accumulation (faster; logits ~1e-4 from fp32, so
+ * actions can differ where a decision margin is that small).  Everything else
+ * is fp32 in both modes. */
 ZSIM_API int zsim_policy_set_precision(zsim_policy* policy, int32_t mode);
 /* Env::rollout(NNPolicy, horizon, seed) (simcore.cpp:554-618 with
  * train/policy.hpp:27-58) entirely on the device: per step observe -> policy

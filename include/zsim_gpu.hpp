@@ -331,8 +331,12 @@ private:
 // order) run on the device policy kernels; usable with either Env::rollout.
 class NNPolicy final : public sim::RolloutPolicy {
 public:
+    // precision: Fp32 (default) computes like the reference's Model<float>;
+    // Tf32 runs the projections on the tcgen05 tensor cores (logits ~1e-4 from
+    // fp32: an action can differ where its decision margin is that small).
+    enum class Precision { Fp32 = 1, Tf32 = 0 };
     NNPolicy(const std::vector<float>& params, bool use_argmax, int device = 0,
-             const zsim_model_config* cfg = nullptr)
+             const zsim_model_config* cfg = nullptr, Precision precision = Precision::Fp32)
         : argmax_(use_argmax) {
         zsim_model_config c;
         if (cfg) {
@@ -341,6 +345,12 @@ public:
             detail::check(zsim_model_config_defaults(&c));
         }
         detail::check(zsim_policy_create(&c, params.data(), int64_t(params.size()), device, &pol_));
+        const int rc = zsim_policy_set_precision(pol_, int32_t(precision));
+        if (rc != ZSIM_OK) {
+            zsim_policy_destroy(pol_);
+            pol_ = nullptr;
+            detail::check(rc);
+        }
     }
     NNPolicy(const NNPolicy&) = delete;
     NNPolicy& operator=(const NNPolicy&) = delete;
@@ -352,6 +362,8 @@ public:
              sim::PolicyOut& out) override {
         (void)step_index;
         const int b = obs.batch;
+        if (rng.size() < size_t(b))  // one stream per row (train/policy.hpp:40-52)
+            fail(ErrorKind::invalid_argument, "NNPolicy::act: rng has fewer streams than rows");
         out.accel_idx.resize(size_t(b));
         out.steer_idx.resize(size_t(b));
         out.logp.resize(size_t(b));

@@ -1889,7 +1889,8 @@ ZSIM_API int zsim_check_errors(zsim_env* env, void* stream) {
         if (h) {
             cuda_check(cudaMemsetAsync(env->d_err, 0, 4, as_stream(stream)), "clear error word");
             cuda_check(cudaStreamSynchronize(as_stream(stream)), "stream sync");
-            raise(Err::invalid_argument, "action index out of range");
+            if (h & 1) raise(Err::invalid_argument, "action index out of range");
+            raise(Err::runtime, "non-finite ego state (NaN/Inf) after a step");
         }
     });
 }

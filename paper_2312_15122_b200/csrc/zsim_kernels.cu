@@ -45,6 +45,12 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int NQ = 5;     // projection queries per step: ego position + 4 inflated corners
 constexpr int NB2 = 256;  // counting-sort buckets over the exact keys
 constexpr int kUnroll = 8;  // independent point loads in flight per lane in the key passes
+#ifdef ZS_NO_OBS_STAGE
+constexpr bool kObsStage = false;
+#else
+constexpr bool kObsStage = true;  // road / route observation blocks staged in smem, written as 16-byte stores
+#endif
+constexpr int kAgSlots = 32;  // agent corner slots (one 32-agent chunk), the stride of the corner-major layout
 
 // Diagnostic path counters, compiled only into the ZS_PATHSTATS variant
 // (build.py --pathstats); the product library has none of this code.
@@ -136,8 +142,8 @@ struct RowSh {
 // Per-warp shared-memory carve-up (host mirror: smem_bytes()).
 struct WarpBuf {
     RowSh* rs;
-    double* agx;           // [A*4] agent corners
-    double* agy;
+    double* agx;           // [4][32] agent corners, corner-major: corner k of slot j at k * 32 + j
+    double* agy;           //   (lane-per-agent reads are then consecutive: no bank conflicts)
     double* agd;           // [A] bbox distance
     int* agf;              // [A] -1 invalid, 0 separate, 1 overlap
     unsigned short* hist;  // [32*32] lane-private u16 histogram; reused as counting-sort counts u32[NB2]
@@ -161,9 +167,9 @@ inline SmemLayout warp_layout(int A, int cap, int ka, int ns) {
     size_t o = al16(sizeof(RowSh));  // warp-uniform row state
     const size_t u0 = o;
     auto put = [&](uint32_t& f, size_t bytes) { f = uint32_t(o), o += al16(bytes); };
-    const size_t AC = size_t(A < 32 ? A : 32);  // corner slots: one 32-agent chunk
-    put(L.agx, AC * 4 * 8);
-    put(L.agy, AC * 4 * 8);
+    // corner slots: one 32-agent chunk, corner-major with stride kAgSlots
+    put(L.agx, size_t(A > 0 ? kAgSlots : 0) * 4 * 8);
+    put(L.agy, size_t(A > 0 ? kAgSlots : 0) * 4 * 8);
     put(L.agd, size_t(A) * 8);
     put(L.agf, size_t(A) * 4);
     put(L.sel, size_t(ka) * 4);
@@ -610,8 +616,8 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size
     // the observation recomputes each chunk's corners (agent_corners)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        w.agx[4 * (j & 31) + k] = X[k];
-        w.agy[4 * (j & 31) + k] = Y[k];
+        w.agx[k * kAgSlots + (j & 31)] = X[k];
+        w.agy[k * kAgSlots + (j & 31)] = Y[k];
     }
     return boxes_overlap(eb, EX, EY, ab, X, Y) ? 1 : 0;
 }
@@ -628,7 +634,13 @@ __device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t 
     const double2 cs = pk.ag_cs[slice + j];
     ab.c = cs.x;
     ab.s = cs.y;
-    box_corners(ab, agx + 4 * slot, agy + 4 * slot);
+    double X[4], Y[4];
+    box_corners(ab, X, Y);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        agx[k * kAgSlots + slot] = X[k];
+        agy[k * kAgSlots + slot] = Y[k];
+    }
 }
 
 // k-th smallest (1-based) of the keys' top 16 bits over key[0..n) across the
@@ -712,10 +724,15 @@ __device__ __forceinline__ bool agent_boxes(const DevPack& pk, int sc, size_t sl
 }
 
 // geometry.cpp:77-88 in full over the 16 edge pairs (contact case, rare).
+// (box_edge_pair_dist2 for every pair; the agent's corners corner-major, stride kAgSlots)
 __device__ __forceinline__ double contact_dist2(const double* GX, const double* GY, const double* AX, const double* AY) {
     double d2min = INFINITY;
 #pragma unroll 1
-    for (int pr = 0; pr < 16; ++pr) d2min = fmin(d2min, box_edge_pair_dist2(GX, GY, AX, AY, pr >> 2, pr & 3));
+    for (int pr = 0; pr < 16; ++pr) {
+        const int i = pr >> 2, j = pr & 3, i1 = (i + 1) & 3, j1 = (j + 1) & 3;
+        d2min = fmin(d2min, segseg_dist2(GX[i], GY[i], GX[i1], GY[i1], AX[kAgSlots * j], AY[kAgSlots * j],
+                                         AX[kAgSlots * j1], AY[kAgSlots * j1]));
+    }
     return d2min;
 }
 
@@ -741,6 +758,12 @@ __device__ __forceinline__ double box_far_d2(float4 bb, double px, double py) {
     double dy = fmax(fabs(double(bb.y) - py), fabs(double(bb.w) - py));
     return dx * dx + dy * dy;
 }
+
+// Counting-sort bucket b's counter slot: lane L owns buckets 8L..8L+7 in the
+// scan, so bucket 8L+k sits at k*32 + L (the scan's accesses are then
+// bank-conflict-free; a [L][k] layout is an 8-way conflict).
+__device__ __forceinline__ int bslot(int b) { return ((b & 7) << 5) | (b >> 3); }
+static_assert(NB2 == 256, "bslot assumes 256 buckets (8 per lane)");
 
 // Warp-wide bucket counts: lane k returns bucket k's count; clears the histogram.
 __device__ __forceinline__ unsigned hist_reduce(unsigned short* hist) {
@@ -1033,7 +1056,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
                 ckey[c] = ok ? e : INFINITY;
                 cinfo[c] = oiv[u];
                 if (ok) {
-                    atomicAdd(&cntb[min(NB2 - 1, int(e * sc2))], 1u);
+                    atomicAdd(&cntb[bslot(min(NB2 - 1, int(e * sc2)))], 1u);
                     ++nvalid_local;
                 }
             }
@@ -1046,21 +1069,21 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
         unsigned s = 0;
 #pragma unroll
         for (int k = 0; k < NB2 / 32; ++k) {
-            v[k] = cntb[lane * (NB2 / 32) + k];
+            v[k] = cntb[k * 32 + lane];
             s += v[k];
         }
         unsigned run = warp_incl_scan(s) - s;
 #pragma unroll
         for (int k = 0; k < NB2 / 32; ++k) {
-            cntb[lane * (NB2 / 32) + k] = run;            // bucket start
-            cntb[NB2 + lane * (NB2 / 32) + k] = run;      // scatter cursor
+            cntb[k * 32 + lane] = run;        // bucket start
+            cntb[NB2 + k * 32 + lane] = run;  // scatter cursor
             run += v[k];
         }
     }
     __syncwarp();
     for (int c = lane; c < C; c += 32) {
         const double e = ckey[c];
-        if (e < INFINITY) order[atomicAdd(&cntb[NB2 + min(NB2 - 1, int(e * sc2))], 1u)] = c;
+        if (e < INFINITY) order[atomicAdd(&cntb[NB2 + bslot(min(NB2 - 1, int(e * sc2)))], 1u)] = c;
     }
     __syncwarp();
     int* sel_tmp = reinterpret_cast<int*>(cntb + NB2);  // cursors are done: reuse as the selection
@@ -1070,9 +1093,9 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
         if (!(e < INFINITY)) continue;
         const int bk = min(NB2 - 1, int(e * sc2));
         const int o_self = cinfo[c];
-        const unsigned start = cntb[bk];
+        const unsigned start = cntb[bslot(bk)];
         if (start >= unsigned(K)) continue;  // every key of an earlier bucket is smaller: cannot rank < K
-        const unsigned end = bk + 1 < NB2 ? cntb[bk + 1] : unsigned(nvalid);
+        const unsigned end = bk + 1 < NB2 ? cntb[bslot(bk + 1)] : unsigned(nvalid);
         unsigned rank = start;
 #pragma unroll 1
         for (unsigned q = start; q < end; ++q) {
@@ -1306,14 +1329,14 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
             // beyond 32 agents only one chunk of corners is kept: this lane's slot
             const int slot = na > 32 ? lane : j;
             if (na > 32) agent_corners(pk, sc, aslice, j, slot, w.agx, w.agy);
-            const double* AX = w.agx + 4 * slot;
-            const double* AY = w.agy + 4 * slot;
+            const double* AX = w.agx + slot;  // corner k at AX[k * kAgSlots]
+            const double* AY = w.agy + slot;
             float axf[4], ayf[4];
             float S = 0.f;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                axf[k] = float(AX[k] - ecx);
-                ayf[k] = float(AY[k] - ecy);
+                axf[k] = float(AX[k * kAgSlots] - ecx);
+                ayf[k] = float(AY[k * kAgSlots] - ecy);
                 S = fmaxf(S, fmaxf(fabsf(axf[k]), fabsf(ayf[k])));
             }
             float E = ge;
@@ -1357,8 +1380,9 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 const int pr = __ffs(cmask) - 1;
                 cmask &= cmask - 1;
                 const int ci = (pr >> 2) & 3, ei = pr & 3, ei1 = (ei + 1) & 3;
-                const double d2 = pr < 16 ? seg_dist2_fast(GX[ci], GY[ci], AX[ei], AY[ei], AX[ei1], AY[ei1])
-                                          : seg_dist2_fast(AX[ci], AY[ci], GX[ei], GY[ei], GX[ei1], GY[ei1]);
+                const int S = kAgSlots;
+                const double d2 = pr < 16 ? seg_dist2_fast(GX[ci], GY[ci], AX[S * ei], AY[S * ei], AX[S * ei1], AY[S * ei1])
+                                          : seg_dist2_fast(AX[S * ci], AY[S * ci], GX[ei], GY[ei], GX[ei1], GY[ei1]);
                 d2min = fmin(d2min, d2);
             }
             if (!(d2min >= 1e-18)) {
@@ -1472,6 +1496,13 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 0);
         ROW_MARK(b, 4);
         const uint8_t* kd = pk.road_kd + size_t(sc) * pk.d.P;
+        // The row's road block (Kr x 12 floats) is staged in the top-k scratch
+        // (dead once the selection is in `order`) and written out as
+        // consecutive 16-byte stores: one full 128-byte line per quarter warp
+        // instead of 48-byte-strided partial sectors.
+        float4* stg = reinterpret_cast<float4*>(w.hist);
+        const bool staged = kObsStage && reinterpret_cast<const char*>(w.order) - reinterpret_cast<const char*>(w.hist) >=
+                                             ptrdiff_t(Kr) * 48;
         for (int k = lane; k < Kr; k += 32) {
             float f[12];
 #pragma unroll
@@ -1490,11 +1521,26 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 for (int q = 0; q < 4; ++q) f[7 + q] = (kk >> 4) == q ? 1.f : 0.f;
                 f[11] = 1.f;
             }
-            float4* o = reinterpret_cast<float4*>(rd + k * 12);
-            obs_st(o, make_float4(f[0], f[1], f[2], f[3]));
-            obs_st(o + 1, make_float4(f[4], f[5], f[6], f[7]));
-            obs_st(o + 2, make_float4(f[8], f[9], f[10], f[11]));
+            float4* o = staged ? stg + 3 * k : reinterpret_cast<float4*>(rd + k * 12);
+            const float4 v0 = make_float4(f[0], f[1], f[2], f[3]), v1 = make_float4(f[4], f[5], f[6], f[7]),
+                         v2 = make_float4(f[8], f[9], f[10], f[11]);
+            if (staged) {
+                o[0] = v0, o[1] = v1, o[2] = v2;
+            } else {
+                obs_st(o, v0);
+                obs_st(o + 1, v1);
+                obs_st(o + 2, v2);
+            }
             if (dbg) dbg[Ka + k] = i < 0 ? -1 : oidx[i];
+        }
+        if (staged) {
+            __syncwarp();
+            float4* rd4 = reinterpret_cast<float4*>(rd);
+            for (int q = lane; q < Kr * 3; q += 32) obs_st(rd4 + q, stg[q]);
+            __syncwarp();
+            // the next top-k counts into the (now dirty) histogram area: clear it
+            for (int q = lane; q < 32 * 32 * 2 / 16; q += 32) reinterpret_cast<uint4*>(w.hist)[q] = make_uint4(0u, 0u, 0u, 0u);
+            __syncwarp();
         }
     }
 
@@ -1510,6 +1556,12 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 1);
         ROW_MARK(b, 6);
         const uint8_t* fl = pk.route_fl + size_t(sc) * pk.d.R;
+        // staged like the road block (5-float slots: a stride-5 staging write
+        // is bank-conflict-free), then written as 16-byte stores
+        float* stg = reinterpret_cast<float*>(w.hist);
+        const bool staged = kObsStage && (Kl * 5) % 4 == 0 &&
+                            reinterpret_cast<const char*>(w.order) - reinterpret_cast<const char*>(w.hist) >=
+                                ptrdiff_t(Kl) * 20;
         for (int k = lane; k < Kl; k += 32) {
             float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
             int i = -1;
@@ -1523,10 +1575,22 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 f[3] = (fl[i] & 2) ? 1.f : 0.f;
                 f[4] = 1.f;
             }
-            float* o = rt + k * 5;
+            if (staged) {
 #pragma unroll
-            for (int q = 0; q < 5; ++q) obs_st(o + q, f[q]);
+                for (int q = 0; q < 5; ++q) stg[k * 5 + q] = f[q];
+            } else {
+                float* o = rt + k * 5;
+#pragma unroll
+                for (int q = 0; q < 5; ++q) obs_st(o + q, f[q]);
+            }
             if (dbg) dbg[Ka + Kr + k] = i < 0 ? -1 : oidx[i];
+        }
+        if (staged) {
+            __syncwarp();
+            const float4* s4 = reinterpret_cast<const float4*>(stg);
+            float4* rt4 = reinterpret_cast<float4*>(rt);
+            for (int q = lane; q < Kl * 5 / 4; q += 32) obs_st(rt4 + q, s4[q]);
+            __syncwarp();  // (the next row's observe clears the histogram area before its top-k)
         }
     }
     }  // PARTS & kObsMap
@@ -1654,6 +1718,11 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
             rs.qy[0] = y;
             for (int k = 0; k < 4; ++k) rs.qx[k + 1] = X[k], rs.qy[k + 1] = Y[k];
             rs.a_lat = v0 * v0 * tan_steer / cfg.wheelbase;
+            // failure detection: a non-finite ego state (NaN / Inf input or
+            // overflow) is flagged in the error word (bit 1); the step itself
+            // proceeds exactly like the reference, which does not check
+            if (!(isfinite(x) && isfinite(y) && isfinite(h) && isfinite(r.v) && isfinite(r.steer)))
+                atomicOr(a.err, 2);
         }
         __syncwarp();
     }

@@ -1489,7 +1489,7 @@ struct zsim_policy {
     int device = 0;
     float* blob = nullptr;  // device: reference params followed by the folded cross-attention weights
     zp::PolicyW w{};
-    int precision = 0;  // 0: tcgen05 tf32 projections, 1: fp32 CUDA cores
+    int precision = 1;  // 1 (default): fp32 CUDA cores, the reference's Model<float>; 0: tcgen05 tf32 projections
     float* pooled = nullptr;  // [cap][128] encoder output scratch (tensor-core path)
     int pooled_cap = 0;
     unsigned char* hbuf = nullptr;  // zsim_policy_act_host: device obs + rng + outputs for hcap rows

@@ -59,7 +59,12 @@ class NNPolicy:
     PRECISIONS = {"tf32": 0, "fp32": 1}
 
     def __init__(self, cfg: ModelConfig, params: np.ndarray, use_argmax: bool = False, device: int = 0,
-                 precision: str = "tf32"):
+                 precision: str = "fp32"):
+        """precision "fp32" (default): every contraction on the FP32 pipe, the
+        reference's Model<float> arithmetic; "tf32": the projections on the
+        tcgen05 tensor cores (tf32 inputs, fp32 accumulate) -- faster, with
+        logits ~1e-4 from fp32, so sampled / argmax actions can differ where
+        the decision margin is that small."""
         self.cfg = cfg
         self.argmax = bool(use_argmax)
         p = np.ascontiguousarray(params, np.float32)

@@ -224,6 +224,27 @@ def test_device_error_word_reports_bad_action(stress16):
     env.check_errors()  # cleared
 
 
+def test_device_error_word_reports_non_finite_state(stress16):
+    """Failure detection: a NaN ego state is flagged (ZSIM_RUNTIME) while the
+    step itself stays the reference's (the NaN propagates, other rows exact)."""
+    import torch
+    env = z.Env(stress16, config=z.SimConfig(disable_dones=True))
+    st = env.init_state(42)
+    st.v[5] = np.nan
+    s0, s1, so = env.device_state(), env.device_state(), env.device_stepout()
+    env.upload_state(st, s0)
+    A = torch.zeros(16, dtype=torch.int32, device="cuda")
+    S = torch.zeros(16, dtype=torch.int32, device="cuda")
+    env.step_device(s0, A.data_ptr(), S.data_ptr(), s1, so)
+    with pytest.raises(z.ZsimError) as ei:
+        env.check_errors()
+    assert ei.value.kind == "runtime" and "non-finite" in str(ei.value)
+    env.check_errors()  # cleared
+    host = env.download_state(s1)
+    ref, _ = env.step(st, np.zeros(16, np.int32), np.zeros(16, np.int32))
+    assert np.isnan(host.x[5]) and np.array_equal(np.delete(host.x, 5), np.delete(ref.x, 5))
+
+
 def test_all_done_batch_is_absorbing(stress16):
     """all scenarios already done -> state unchanged, rewards 0."""
     env = z.Env(stress16)

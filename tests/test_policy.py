@@ -4,9 +4,9 @@ numpy restatement in oracle/policy_oracle.py.
 
 Tolerances against the float64 oracle (the reference itself computes in
 float32 with Eigen's summation order, so it sits within the fp32 bound too):
-  precision "fp32" (every contraction on the FP32 pipe): logits / value within
+  precision "fp32" (the default: every contraction on the FP32 pipe): logits / value within
       1e-5 absolute + 1e-4 relative, log-probs within 2e-5 (measured: 4e-7);
-  precision "tf32" (the default: the ten 128x128 projections on tcgen05 with
+  precision "tf32" (opt-in: the ten 128x128 projections on tcgen05 with
       tf32 operands, fp32 accumulation): logits / value within 1e-3 absolute +
       5e-3 relative, log-probs within 2e-3 (measured: 1.8e-4).
 Sampled / argmax indices must be identical wherever the oracle's decision
@@ -129,7 +129,7 @@ def check_against_oracle(cfg_o, params, obs, B, use_argmax, precision, seed=3):
             assert got["accel"][b] == ref["accel"][b] and got["steer"][b] == ref["steer"][b], b
             assert abs(got["logp"][b] - ref["logp"][b]) < tol["logp"], b
             checked += 1
-    assert checked >= B // 3
+    assert checked >= (9 * B) // 10, (checked, B)  # decisive-margin rows: actions and logp must match
     if not use_argmax:
         assert np.array_equal(got["rng"], ref["rng"])  # two draws per row
     return got, ref
