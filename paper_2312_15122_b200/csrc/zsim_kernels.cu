@@ -45,11 +45,6 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int NQ = 5;     // projection queries per step: ego position + 4 inflated corners
 constexpr int NB2 = 256;  // counting-sort buckets over the exact keys
 constexpr int kUnroll = 8;  // independent point loads in flight per lane in the key passes
-#ifdef ZS_NO_OBS_STAGE
-constexpr bool kObsStage = false;
-#else
-constexpr bool kObsStage = true;  // road / route observation blocks staged in smem, written as 16-byte stores
-#endif
 constexpr int kAgSlots = 32;  // agent corner slots (one 32-agent chunk), the stride of the corner-major layout
 
 // Diagnostic path counters, compiled only into the ZS_PATHSTATS variant
@@ -1496,13 +1491,6 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 0);
         ROW_MARK(b, 4);
         const uint8_t* kd = pk.road_kd + size_t(sc) * pk.d.P;
-        // The row's road block (Kr x 12 floats) is staged in the top-k scratch
-        // (dead once the selection is in `order`) and written out as
-        // consecutive 16-byte stores: one full 128-byte line per quarter warp
-        // instead of 48-byte-strided partial sectors.
-        float4* stg = reinterpret_cast<float4*>(w.hist);
-        const bool staged = kObsStage && reinterpret_cast<const char*>(w.order) - reinterpret_cast<const char*>(w.hist) >=
-                                             ptrdiff_t(Kr) * 48;
         for (int k = lane; k < Kr; k += 32) {
             float f[12];
 #pragma unroll
@@ -1521,26 +1509,11 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 for (int q = 0; q < 4; ++q) f[7 + q] = (kk >> 4) == q ? 1.f : 0.f;
                 f[11] = 1.f;
             }
-            float4* o = staged ? stg + 3 * k : reinterpret_cast<float4*>(rd + k * 12);
-            const float4 v0 = make_float4(f[0], f[1], f[2], f[3]), v1 = make_float4(f[4], f[5], f[6], f[7]),
-                         v2 = make_float4(f[8], f[9], f[10], f[11]);
-            if (staged) {
-                o[0] = v0, o[1] = v1, o[2] = v2;
-            } else {
-                obs_st(o, v0);
-                obs_st(o + 1, v1);
-                obs_st(o + 2, v2);
-            }
+            float4* o = reinterpret_cast<float4*>(rd + k * 12);
+            obs_st(o, make_float4(f[0], f[1], f[2], f[3]));
+            obs_st(o + 1, make_float4(f[4], f[5], f[6], f[7]));
+            obs_st(o + 2, make_float4(f[8], f[9], f[10], f[11]));
             if (dbg) dbg[Ka + k] = i < 0 ? -1 : oidx[i];
-        }
-        if (staged) {
-            __syncwarp();
-            float4* rd4 = reinterpret_cast<float4*>(rd);
-            for (int q = lane; q < Kr * 3; q += 32) obs_st(rd4 + q, stg[q]);
-            __syncwarp();
-            // the next top-k counts into the (now dirty) histogram area: clear it
-            for (int q = lane; q < 32 * 32 * 2 / 16; q += 32) reinterpret_cast<uint4*>(w.hist)[q] = make_uint4(0u, 0u, 0u, 0u);
-            __syncwarp();
         }
     }
 
@@ -1556,12 +1529,6 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 1);
         ROW_MARK(b, 6);
         const uint8_t* fl = pk.route_fl + size_t(sc) * pk.d.R;
-        // staged like the road block (5-float slots: a stride-5 staging write
-        // is bank-conflict-free), then written as 16-byte stores
-        float* stg = reinterpret_cast<float*>(w.hist);
-        const bool staged = kObsStage && (Kl * 5) % 4 == 0 &&
-                            reinterpret_cast<const char*>(w.order) - reinterpret_cast<const char*>(w.hist) >=
-                                ptrdiff_t(Kl) * 20;
         for (int k = lane; k < Kl; k += 32) {
             float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
             int i = -1;
@@ -1575,22 +1542,10 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 f[3] = (fl[i] & 2) ? 1.f : 0.f;
                 f[4] = 1.f;
             }
-            if (staged) {
+            float* o = rt + k * 5;
 #pragma unroll
-                for (int q = 0; q < 5; ++q) stg[k * 5 + q] = f[q];
-            } else {
-                float* o = rt + k * 5;
-#pragma unroll
-                for (int q = 0; q < 5; ++q) obs_st(o + q, f[q]);
-            }
+            for (int q = 0; q < 5; ++q) obs_st(o + q, f[q]);
             if (dbg) dbg[Ka + Kr + k] = i < 0 ? -1 : oidx[i];
-        }
-        if (staged) {
-            __syncwarp();
-            const float4* s4 = reinterpret_cast<const float4*>(stg);
-            float4* rt4 = reinterpret_cast<float4*>(rt);
-            for (int q = lane; q < Kl * 5 / 4; q += 32) obs_st(rt4 + q, s4[q]);
-            __syncwarp();  // (the next row's observe clears the histogram area before its top-k)
         }
     }
     }  // PARTS & kObsMap

@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py -x -q > gpurun_out/pytest_v1.log 2>&1; echo pytest=$? >> gpurun_out/pytest_v1.log
-bash tools/variant_bench.sh C1 r01 > /dev/null 2>&1
+bash tools/variant_bench.sh C1 cap192 cap160 cap128 > /dev/null 2>&1
+bash tools/variant_bench.sh C4s cap192 cap160 > /dev/null 2>&1
