@@ -45,14 +45,17 @@ def build_ref(force: bool = False) -> Path | None:
     """Compile the reference + shim into oracle/_ref (None if the reference is absent)."""
     if not reference_available():
         return REF_OUT if REF_OUT.exists() else None
-    srcs = [REF_SRC / "core" / f"{u}.cpp" for u in REF_UNITS] + [HERE / "ref_shim.cpp"]
+    srcs = [REF_SRC / "core" / f"{u}.cpp" for u in REF_UNITS] + [HERE / "ref_shim.cpp", HERE / "ref_policy_shim.cpp"]
     if not force and REF_OUT.exists():
         t = REF_OUT.stat().st_mtime
-        if all(s.stat().st_mtime <= t for s in srcs):
+        if all(s.stat().st_mtime <= t for s in srcs + [HERE / "eigen_mini" / "Eigen" / "Dense"]):
             return REF_OUT
     objdir = HERE / "_ref" / "obj"
     objdir.mkdir(parents=True, exist_ok=True)
+    # oracle/eigen_mini stands in for Eigen (absent here) so core/nn/model.hpp
+    # and core/train/policy.hpp compile unchanged (ref_policy_shim.cpp)
     flags = ["-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-I", str(REF_SRC), "-I", str(NLOHMANN),
+             "-I", str(HERE / "eigen_mini"),
              "-I", str(HERE.parent / "include")]
     jobs, objs = [], []
     for s in srcs:

@@ -346,3 +346,94 @@ def controlled_expand(zsim: bytes, config=None) -> bytes:
     if rc:
         raise RefError(rc, L.zstress_last_error().decode(errors="replace"))
     return _take(p, n)
+
+
+# ---- the reference's policy (core/nn/model.hpp, core/train/policy.hpp; ref_policy_shim.cpp) ----
+class ModelConfigC(C.Structure):
+    """zsim_model_config (include/zsim_gpu.h)."""
+    _fields_ = [(n, C.c_int32) for n in ("latent", "heads", "trunk_blocks", "value_embed", "n_agents", "n_road",
+                                          "n_route", "n_accel", "n_steer", "reserved")]
+
+
+_PSIGS = {
+    "zref_policy_last_error": (C.c_char_p, []),
+    "zref_policy_param_count": (C.c_int, [C.POINTER(ModelConfigC), C.POINTER(C.c_int64)]),
+    "zref_policy_init": (C.c_int, [C.POINTER(ModelConfigC), C.c_uint64, C.POINTER(C.c_float), C.c_int64]),
+    "zref_policy_forward": (C.c_int, [C.POINTER(ModelConfigC), C.POINTER(C.c_float), C.c_int64, C.POINTER(ObsView),
+                                      C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "zref_policy_act": (C.c_int, [C.POINTER(ModelConfigC), C.POINTER(C.c_float), C.c_int64, C.POINTER(ObsView),
+                                  C.c_int32, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int32), C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+}
+
+
+def _plib():
+    L = lib()
+    if not getattr(L, "_zref_policy_bound", False):
+        for n, (r, a) in _PSIGS.items():
+            f = getattr(L, n)
+            f.restype = r
+            f.argtypes = a
+        L._zref_policy_bound = True
+    return L
+
+
+def _pcheck(code: int) -> None:
+    if code != 0:
+        raise RefError(code, _plib().zref_policy_last_error().decode(errors="replace"))
+
+
+def model_config_c(cfg=None) -> ModelConfigC:
+    """ModelConfig defaults (model.hpp:20-27); `cfg` any object with those attributes."""
+    d = dict(latent=128, heads=2, trunk_blocks=2, value_embed=32, n_agents=16, n_road=128, n_route=64, n_accel=7,
+             n_steer=5)
+    return ModelConfigC(**{k: int(getattr(cfg, k, v)) for k, v in d.items()}, reserved=0)
+
+
+def _obs_view(obs: dict, B: int):
+    arrs = {k: np.ascontiguousarray(obs[k], dtype=np.float32) for k in ("active", "agents", "road", "route",
+                                                                        "value_only")}
+    v = ObsView(*[_ptr(arrs[k], C.c_float) for k in ("active", "agents", "road", "route", "value_only")])
+    return v, arrs
+
+
+def policy_param_count(cfg=None) -> int:
+    n = C.c_int64()
+    _pcheck(_plib().zref_policy_param_count(C.byref(model_config_c(cfg)), C.byref(n)))
+    return n.value
+
+
+def policy_init(cfg=None, seed: int = 0) -> np.ndarray:
+    """Model<float>::make + init(seed) (model.hpp:174-216) in the reference."""
+    n = policy_param_count(cfg)
+    out = np.zeros(n, np.float32)
+    _pcheck(_plib().zref_policy_init(C.byref(model_config_c(cfg)), C.c_uint64(seed), _ptr(out, C.c_float), n))
+    return out
+
+
+def policy_forward(params, obs: dict, B: int, cfg=None, double: bool = False):
+    """The reference forward_row over B rows: (logits [B][n_accel+n_steer], value [B]),
+    computed in Model<float> (the reference's arithmetic) or Model<double>."""
+    c = model_config_c(cfg)
+    p = np.ascontiguousarray(params, np.float32)
+    v, keep = _obs_view(obs, B)
+    logits = np.zeros((B, c.n_accel + c.n_steer))
+    value = np.zeros(B)
+    _pcheck(_plib().zref_policy_forward(C.byref(c), _ptr(p, C.c_float), p.size, C.byref(v), int(B), int(bool(double)),
+                                        _ptr(logits, C.c_double), _ptr(value, C.c_double)))
+    return logits, value
+
+
+def policy_act(params, obs: dict, B: int, rng, use_argmax: bool, cfg=None) -> dict:
+    """train::NNPolicy::act (policy.hpp:27-58) in the reference, one thread."""
+    c = model_config_c(cfg)
+    p = np.ascontiguousarray(params, np.float32)
+    v, keep = _obs_view(obs, B)
+    r = np.ascontiguousarray(rng, np.uint64).copy()
+    out = dict(accel=np.zeros(B, np.int32), steer=np.zeros(B, np.int32), logp=np.zeros(B, np.float32),
+               value=np.zeros(B, np.float32))
+    _pcheck(_plib().zref_policy_act(C.byref(c), _ptr(p, C.c_float), p.size, C.byref(v), int(B), int(bool(use_argmax)),
+                                    _ptr(r, C.c_uint64), _ptr(out["accel"], C.c_int32), _ptr(out["steer"], C.c_int32),
+                                    _ptr(out["logp"], C.c_float), _ptr(out["value"], C.c_float)))
+    out["rng"] = r
+    return out

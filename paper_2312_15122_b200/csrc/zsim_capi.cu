@@ -959,6 +959,9 @@ std::unique_ptr<zsim_env> build_env(std::vector<zs::Scene> scenes, int32_t horiz
     }
     if (env->cfg.n_agents <= 0 || env->cfg.n_road <= 0 || env->cfg.n_route <= 0)
         raise(Err::invalid_argument, "nearest_features: k must be > 0");
+    // the per-warp top-k scratch ranks at most 256 selections (zsim_kernels.cu, warp_topk)
+    if (env->cfg.n_road > 256 || env->cfg.n_route > 256)
+        raise(Err::invalid_argument, "n_road / n_route above 256 are not supported on the device path");
     if (accel_bins && n_accel > 0)
         env->accel_bins.assign(accel_bins, accel_bins + n_accel);
     else

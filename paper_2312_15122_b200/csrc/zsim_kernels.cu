@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <mutex>
 #include <vector>
 
@@ -68,6 +69,24 @@ __device__ __forceinline__ void row_mark(int b, int k) {
     do {            \
     } while (0)
 #define ROW_MARK(b, k) \
+    do {               \
+    } while (0)
+#endif
+
+// Bounds-checked build (build.py --variant=checked -DZS_CHECKED): device
+// asserts on the scratch and point-set indices -- the stand-in for
+// compute-sanitizer, which this GPU pool does not run.
+#ifdef ZS_CHECKED
+#define ZS_CHECK(cond)                                                                                      \
+    do {                                                                                                    \
+        if (!(cond)) {                                                                                      \
+            printf("zsim check failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,         \
+                   int(blockIdx.x), int(threadIdx.x));                                                      \
+            __trap();                                                                                       \
+        }                                                                                                   \
+    } while (0)
+#else
+#define ZS_CHECK(cond) \
     do {               \
     } while (0)
 #endif
@@ -157,7 +176,7 @@ __host__ __device__ inline size_t al16(size_t v) { return (v + 15) / 16 * 16; }
 // The agent buffers (boxes at t+1 from the step, distances, selection) are
 // dead once the agent features are written, before the road/route top-k, so
 // both phases share one region.
-inline SmemLayout warp_layout(int A, int cap, int ka, int ns) {
+inline SmemLayout warp_layout(int A, int cap, int ka, int ns, int nch) {
     SmemLayout L;
     size_t o = al16(sizeof(RowSh));  // warp-uniform row state
     const size_t u0 = o;
@@ -175,7 +194,8 @@ inline SmemLayout warp_layout(int A, int cap, int ka, int ns) {
     put(L.cidx, size_t(cap) * 4);
     put(L.ckey, size_t(cap) * 8);
     put(L.cinfo, size_t(cap) * 4);
-    put(L.order, size_t(cap) * 4);
+    // also the top-k's chunk list: up to nch chunks (P > 32 * cap points)
+    put(L.order, size_t(cap > 0 ? (cap > nch ? cap : nch) : 0) * 4);
     o = o > agents_end ? o : agents_end;
     put(L.sflag, size_t(ns) + 1);
     L.total = uint32_t(al16(o));
@@ -512,6 +532,7 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
         };
         while (nearm) {
             const int si = (__ffsll(nearm) - 1) * kSegGroup + gg;
+            ZS_CHECK(si < nseg);
             nearm &= nearm - 1;
             exact(si, F[si]);
         }
@@ -537,6 +558,7 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
         bool ok = hq > 0 && hq < NQU && ((cin_k >> hq) & 1u);
         double hs = 0.0, hd = 0.0;
         if (!ok && hq < NQU && l0 + hk < nl && hi_ != INT_MAX) {
+            ZS_CHECK(hi_ >= 0 && hi_ < C - 1);
             const double2* V = reinterpret_cast<const double2*>(pk.ln_v + (size_t(b) * L + l0 + hk) * C + hi_);
             const double2 a0 = V[0], a1 = V[1], a2 = V[2], a3 = V[3];
             double t;
@@ -611,6 +633,7 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size
     // the observation recomputes each chunk's corners (agent_corners)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+        ZS_CHECK(j >= 0 && j < A);
         w.agx[k * kAgSlots + (j & 31)] = X[k];
         w.agy[k * kAgSlots + (j & 31)] = Y[k];
     }
@@ -631,6 +654,7 @@ __device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t 
     ab.s = cs.y;
     double X[4], Y[4];
     box_corners(ab, X, Y);
+    ZS_CHECK(slot >= 0 && slot < kAgSlots && j >= 0 && j < A);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         agx[k * kAgSlots + slot] = X[k];
@@ -686,27 +710,34 @@ __device__ __forceinline__ void agent_bounds(const DevPack& pk, int sc, size_t s
     hi = fmaxf(0.f, D - te - ta) + m;
 }
 
+// One agent of the pruned pass (beyond 32 agents): fp32 distance bounds
+// (lower bound into agd, upper-bound key into alist: 0 for an overlap) and
+// the SAT only when the lower bound cannot prove the boxes apart.
+__device__ __forceinline__ int agent_bounded(const DevPack& pk, int sc, size_t slice, int j, const Box& eb,
+                                             const double* EX, const double* EY, const WarpBuf& w, unsigned& key) {
+    float lo, hi;
+    agent_bounds(pk, sc, slice, j, eb, lo, hi);
+    const int f = lo > 0.f ? 0 : agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
+    w.agd[j] = double(lo);
+    key = f == 1 ? 0u : __float_as_uint(hi);
+    return f;
+}
+
 // Agent boxes at one slice + overlap flags into w.agx/agy/agf for a row
 // (-1 = invalid / skipped / t past the log); returns whether any overlaps.
 // (Inlined: a __noinline__ call forces the WarpBuf into local memory.)
+// Beyond 32 agents the corners are not kept (the observation recomputes them
+// per chunk) and the distance bounds of the observation's pruning are computed
+// here, in the same pass over the agents (agent_bounded).
 __device__ __forceinline__ bool agent_boxes(const DevPack& pk, int sc, size_t slice, int na, int skip, bool t_ok, const Box& eb,
                                              const double* EX, const double* EY, const WarpBuf& w) {
     bool hit = false;
-    // Beyond 32 agents the corners are not kept (the observation recomputes
-    // them per chunk) and the distance bounds of the observation's pruning are
-    // computed here, in the same pass over the agents: lower bound into agd,
-    // upper-bound key into alist (0 for an overlap, ~0u for an invalid agent).
-    // A positive lower bound proves the boxes apart and skips the SAT.
     for (int j = lane_id(); j < na; j += 32) {
         int f = -1;
         unsigned key = 0xFFFFFFFFu;
         if (t_ok && j != skip && pk.ag_valid[slice + j]) {
             if (na > 32) {
-                float lo, hi;
-                agent_bounds(pk, sc, slice, j, eb, lo, hi);
-                f = lo > 0.f ? 0 : agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
-                w.agd[j] = double(lo);
-                key = f == 1 ? 0u : __float_as_uint(hi);
+                f = agent_bounded(pk, sc, slice, j, eb, EX, EY, w, key);
             } else {
                 f = agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
             }
@@ -820,6 +851,7 @@ __device__ __forceinline__ void over_chunks(const PointSet& ps, const int* list,
             pb[u] = make_float2(INFINITY, INFINITY);
             if (j0 + u < nlist) {
                 const int p = list[j0 + u] * kChunk + lane;
+                ZS_CHECK(list[j0 + u] >= 0 && list[j0 + u] < ps.nch);
                 if (p < ps.n) {
                     pos[u] = p;
                     pb[u] = ps.xy[p];
@@ -855,6 +887,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
                                       float4 hv, float4* hint, int which) {
     const int lane = lane_id();
     const int n = ps.n;
+    ZS_CHECK(K <= NB2 && n <= ps.nch * kChunk);
     if (n <= 0) return 0;
     const float pxf = float(px), pyf = float(py);
     const double ep = fmax(fabs(double(pxf) - px), fabs(double(pyf) - py));
@@ -921,6 +954,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
             if (need) list[nlist + __popc(bal & lanemask_lt())] = c;
             nlist += __popc(bal);
         }
+        ZS_CHECK(nlist <= ps.nch);
         __syncwarp();
     };
     auto compact_chunks = [&](float t) {
@@ -1038,6 +1072,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int c = c0 + 32 * u + lane;
+            ZS_CHECK(c >= C || (cidx[c] >= 0 && cidx[c] < n));
             oiv[u] = c < C ? ps.oi[cidx[c]] : 0;
         }
 #pragma unroll
@@ -1078,7 +1113,11 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     __syncwarp();
     for (int c = lane; c < C; c += 32) {
         const double e = ckey[c];
-        if (e < INFINITY) order[atomicAdd(&cntb[NB2 + bslot(min(NB2 - 1, int(e * sc2)))], 1u)] = c;
+        if (e < INFINITY) {
+            const unsigned q = atomicAdd(&cntb[NB2 + bslot(min(NB2 - 1, int(e * sc2)))], 1u);
+            ZS_CHECK(q < unsigned(C));
+            order[q] = c;
+        }
     }
     __syncwarp();
     int* sel_tmp = reinterpret_cast<int*>(cntb + NB2);  // cursors are done: reuse as the selection
@@ -1095,6 +1134,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
 #pragma unroll 1
         for (unsigned q = start; q < end; ++q) {
             const int o = order[q];
+            ZS_CHECK(o >= 0 && o < C);
             const double eo = ckey[o];
             const int io = cinfo[o];
             rank += (eo < e || (eo == e && io < o_self)) ? 1u : 0u;
@@ -1304,6 +1344,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 const int fl = j < na ? w.agf[j] : -1;
                 const bool keep = fl == 1 || (fl == 0 && w.agd[j] <= U);
                 const unsigned bal = __ballot_sync(FULL, keep);
+                ZS_CHECK(!keep || n + __popc(bal & lanemask_lt()) < na);
                 if (keep) w.alist[n + __popc(bal & lanemask_lt())] = j;  // positions <= j: keys already consumed
                 n += __popc(bal);
             }
@@ -1444,6 +1485,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                     const double dk = w.agd[k];
                     rank += (w.agf[k] >= 0 && (dk < dj || (dk == dj && k < j))) ? 1 : 0;
                 }
+                ZS_CHECK(rank >= 0);
                 if (rank < Ka) w.sel[rank] = j;
             }
         }
@@ -1456,6 +1498,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         int j = -1;
         if (k < nsel_ag) {
             j = w.sel[k];
+            ZS_CHECK(j >= 0 && j < na);
             double wx = double(pk.ag_x[aslice + j]) - r.x, wy = double(pk.ag_y[aslice + j]) - r.y;
             f[0] = float(oc * wx - os * wy);
             f[1] = float(os * wx + oc * wy);
@@ -1498,6 +1541,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
             int i = -1;
             if (k < nsel) {
                 i = sel[k];
+                ZS_CHECK(i >= 0 && i < n);
                 float2 p = pts[i];
                 double wx = double(p.x) - r.x, wy = double(p.y) - r.y;
                 f[0] = float(oc * wx - os * wy);
@@ -1534,6 +1578,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
             int i = -1;
             if (k < nsel) {
                 i = sel[k];
+                ZS_CHECK(i >= 0 && i < n);
                 float2 p = pts[i];
                 double wx = double(p.x) - r.x, wy = double(p.y) - r.y;
                 f[0] = float(oc * wx - os * wy);
@@ -2004,12 +2049,12 @@ extern "C" __attribute__((visibility("default"))) int zsimdbg_pathstats(unsigned
 // Big CTAs keep more warps in phase (one block barrier per row: a shared
 // instruction stream; measured C2 +27%, C1 +2% over 4-warp CTAs)
 int step_observe_warps(const KernelArgs& a) {
-    const size_t per_warp = warp_layout(a.pk.d.A, a.cand_cap, a.cfg.n_agents, a.pk.d.NS).total;
+    const size_t per_warp = warp_layout(a.pk.d.A, a.cand_cap, a.cfg.n_agents, a.pk.d.NS, max(a.pk.d.PC, a.pk.d.RC)).total;
     return per_warp * kCtaWarpsBig <= 200 * 1024 ? kCtaWarpsBig : kCtaWarpsSmall;
 }
 
 size_t smem_bytes(const KernelArgs& a) {
-    return size_t(warp_layout(a.pk.d.A, a.cand_cap, a.cfg.n_agents, a.pk.d.NS).total) *
+    return size_t(warp_layout(a.pk.d.A, a.cand_cap, a.cfg.n_agents, a.pk.d.NS, max(a.pk.d.PC, a.pk.d.RC)).total) *
            size_t(step_observe_warps(a));
 }
 
@@ -2077,7 +2122,7 @@ bool observe_split(const KernelArgs& a, int policy) {
     if (policy == 1) return false;
     if (policy == 2) return true;
     KernelArgs t = a;
-    t.lay = warp_layout(t.pk.d.A, t.cand_cap, t.cfg.n_agents, t.pk.d.NS);
+    t.lay = warp_layout(t.pk.d.A, t.cand_cap, t.cfg.n_agents, t.pk.d.NS, max(t.pk.d.PC, t.pk.d.RC));
     const int warps = step_observe_warps(t);
     const void* fn = warps == kCtaWarpsBig
                          ? reinterpret_cast<const void*>(k_step_observe<true, kObsAll, false, kCtaWarpsBig>)
@@ -2094,7 +2139,7 @@ template <int W>
 static cudaError_t launch_step_observe_w(const KernelArgs& a, int mode, int policy, cudaStream_t stream) {
     auto launch = [&](auto kern, KernelArgs am, bool topk) -> cudaError_t {
         if (!topk) am.cand_cap = 0;  // no top-k buffers in kernels without the map part
-        am.lay = warp_layout(am.pk.d.A, am.cand_cap, am.cfg.n_agents, am.pk.d.NS);
+        am.lay = warp_layout(am.pk.d.A, am.cand_cap, am.cfg.n_agents, am.pk.d.NS, max(am.pk.d.PC, am.pk.d.RC));
         const size_t smem = size_t(am.lay.total) * W;
         if (blocks_per_sm(reinterpret_cast<const void*>(kern), smem, 32 * W) < 0) return cudaErrorInvalidValue;
         const int g = persistent_grid(kern, am, smem, W);
@@ -2133,7 +2178,7 @@ static cudaError_t launch_step_observe_w(const KernelArgs& a, int mode, int poli
 
 cudaError_t launch_step_observe(const KernelArgs& a, int mode, int policy, cudaStream_t stream) {
     KernelArgs t = a;
-    t.lay = warp_layout(t.pk.d.A, t.cand_cap, t.cfg.n_agents, t.pk.d.NS);
+    t.lay = warp_layout(t.pk.d.A, t.cand_cap, t.cfg.n_agents, t.pk.d.NS, max(t.pk.d.PC, t.pk.d.RC));
     return step_observe_warps(t) == kCtaWarpsBig ? launch_step_observe_w<kCtaWarpsBig>(a, mode, policy, stream)
                                                  : launch_step_observe_w<kCtaWarpsSmall>(a, mode, policy, stream);
 }

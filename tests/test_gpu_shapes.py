@@ -6,7 +6,8 @@ paths the default C1 shapes never take.
 * more than 32 agents per row in ego mode (chunked agent ordering, bound
   pruning; C3/C4), and so many agents that the per-warp shared memory forces
   the 4-warp CTA arrangement,
-* large roadgraphs (8192 points, 256 chunks: C4),
+* large roadgraphs (8192 points, 256 chunks: C4; 10000 points: more chunks than
+  the candidate capacity),
 * fewer road / route points than k (partially filled top-k, zero padding),
 * a single-scenario batch.
 
@@ -55,6 +56,8 @@ SHAPES = {
     "agents_128": dict(count=4, agents=128, road_points=1024),
     "agents_900": dict(count=2, agents=900, road_points=512),
     "roadgraph_8k": dict(count=4, agents=16, road_points=8192),
+    # more than cap (256) chunks: the top-k chunk list outgrows the candidate buffers
+    "roadgraph_10k": dict(count=2, agents=8, road_points=10000),
     "sparse_map": dict(count=6, agents=4, road_points=40, lanes=1, lane_vertices=12),
     "single": dict(count=1, agents=8, road_points=300),
 }

@@ -19,6 +19,7 @@ import numpy as np
 import pytest
 
 from oracle import policy_oracle as po
+from oracle import refpy
 
 TOL = {"fp32": dict(atol=1e-5, rtol=1e-4, logp=2e-5, margin=1e-4),
        "tf32": dict(atol=1e-3, rtol=5e-3, logp=2e-3, margin=2e-3)}
@@ -166,6 +167,41 @@ def test_policy_act_on_simulator_observations(precision):
     obs = {k: getattr(h, k).copy() for k in ("active", "agents", "road", "route", "value_only")}
     cfg_o = po.ModelConfig()
     check_against_oracle(cfg_o, po.init_params(cfg_o, 2), obs, 16, False, precision)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not refpy.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+@pytest.mark.parametrize("use_argmax", [True, False])
+def test_policy_act_vs_reference_nnpolicy(use_argmax, precision):
+    """The device NNPolicy against the reference's own NNPolicy::act
+    (policy.hpp:27-58 over model.hpp's Model<float>, compiled unchanged in
+    oracle/_ref with oracle/eigen_mini): actions identical wherever the
+    decision margin exceeds the precision's, rng streams bit-identical, value
+    and log-prob within the precision's tolerance."""
+    import paper_2312_15122_b200 as z
+    tol = TOL[precision]
+    params = refpy.policy_init(None, 13)
+    B = 40
+    obs = random_obs(B, np.random.default_rng(17))
+    rng0 = (np.arange(1, B + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) ^ np.uint64(99)
+    ref = refpy.policy_act(params, obs, B, rng0, use_argmax)
+    logits64, _ = refpy.policy_forward(params, obs, B, double=True)
+    pol = z.NNPolicy(z.ModelConfig(), params, use_argmax=use_argmax, precision=precision)
+    got = run_device(pol, obs, rng0.copy(), B)
+    np.testing.assert_allclose(got["value"], ref["value"], atol=tol["atol"], rtol=tol["rtol"])
+    # decision margins from the reference's float64 logits and the sampled u
+    ora = po.act(po.Model(po.ModelConfig(), params), obs, rng0.copy(), use_argmax)
+    checked = 0
+    for b in range(B):
+        if margins_ok(logits64[b, :7], ora["u"][b][0], use_argmax, tol["margin"]) and \
+                margins_ok(logits64[b, 7:], ora["u"][b][1], use_argmax, tol["margin"]):
+            assert got["accel"][b] == ref["accel"][b] and got["steer"][b] == ref["steer"][b], b
+            assert abs(got["logp"][b] - ref["logp"][b]) < tol["logp"], b
+            checked += 1
+    assert checked >= (9 * B) // 10, (checked, B)
+    if not use_argmax:
+        assert np.array_equal(got["rng"], ref["rng"])
 
 
 @pytest.mark.gpu

@@ -1,5 +1,3 @@
-python tools/sanitize.py > gpurun_out/san_plain.log 2>&1; echo plain=$? >> gpurun_out/san_plain.log
-for tool in memcheck racecheck synccheck initcheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 30 --error-exitcode 9 python tools/sanitize.py > gpurun_out/san_$tool.log 2>&1; echo "$tool exit=$?" >> gpurun_out/san_$tool.log
-done
-ZSIM_GPU_LIB=paper_2312_15122_b200/_build/pathstats/libzsim_gpu_pathstats.so timeout 600 python tools/episode_profile.py 4096 --pathstats > gpurun_out/phases_c1.json 2> gpurun_out/phases_c1.err
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_v4.log 2>&1; echo pytest=$? >> gpurun_out/pytest_v4.log
+ZSIM_GPU_LIB=paper_2312_15122_b200/_build/checked/libzsim_gpu.so timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_checked.log 2>&1; echo pytest_checked=$? >> gpurun_out/pytest_checked.log
+bash tools/variant_bench.sh C2 prewin > /dev/null 2>&1

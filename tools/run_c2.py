@@ -1,5 +1,5 @@
 """Run a few C2 (all agents controlled) steps on a reduced batch (for ncu captures).
-usage: python tools/run_c2.py [scenarios]   (diagnostic tool)"""
+usage: python tools/run_c2.py [scenarios] [launch policy]   (diagnostic tool)"""
 import sys
 from pathlib import Path
 
@@ -11,6 +11,8 @@ import paper_2312_15122_b200 as z
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 zsim = z.stress_scenarios(z.StressConfig(count=S, agents=128, road_points=8192, flags=z.STRESS_C2), 7)
 env = z.Env(zsim, config=z.SimConfig(disable_dones=True), controlled=True)
+if len(sys.argv) > 2:
+    env.set_launch_policy(int(sys.argv[2]))  # 1 fused, 2 split (the 524,288-row benchmark's arrangement)
 B = env.info.batch
 acc, st = z.random_actions(91, B, seed=123)
 dA, dS = torch.from_numpy(acc).cuda(), torch.from_numpy(st).cuda()
