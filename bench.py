@@ -473,69 +473,79 @@ def run_ours(args) -> None:
 
 
 def measure_policy(env, ob, B, A_):
-    """SURVEY 8f row 4: NNPolicy::act on the device (tcgen05 tf32 projections)
-    over the batch's observations, and the closed simulate -> act loop
-    (zsim_rollout_policy, 91 steps) -- reported beside the headline metric."""
+    """SURVEY 8f row 4: NNPolicy::act on the device over the batch's
+    observations, and the closed simulate -> act loop (zsim_rollout_policy,
+    91 steps, one CUDA graph) -- reported beside the headline metric, for the
+    default fp32 arithmetic (the reference's Model<float>) and the opt-in tf32
+    tensor-core projections."""
     import torch
 
     import paper_2312_15122_b200 as z
     cfg = z.ModelConfig()
-    pol = z.NNPolicy(cfg, z.init_params(cfg, 1), use_argmax=False, precision="tf32")
+    params = z.init_params(cfg, 1)
     stream = torch.cuda.current_stream()
     rng = torch.arange(B, dtype=torch.int64, device="cuda")
     acc = torch.zeros(B, dtype=torch.int32, device="cuda")
     ste = torch.zeros_like(acc)
     lp = torch.zeros(B, dtype=torch.float32, device="cuda")
     val = torch.zeros_like(lp)
-
-    def act():
-        pol.act_device(ob, B, rng.data_ptr(), acc.data_ptr(), ste.data_ptr(), lp.data_ptr(), val.data_ptr(),
-                       stream=stream)
-    for _ in range(3):
-        act()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n = 20
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(n):
-        act()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / n
-    env.rollout_policy_device(pol, 42, EPISODE, stream=stream)  # warm-up (allocates the scratch)
-    torch.cuda.synchronize()
-    # the whole closed loop (reset, 91 x [policy encoder + heads, fused step]) as one CUDA graph
-    graph = torch.cuda.CUDAGraph()
-    gs = torch.cuda.Stream()
-    with torch.cuda.stream(gs):
-        with torch.cuda.graph(graph, stream=gs):
-            env.rollout_policy_device(pol, 42, EPISODE, stream=gs)
-    graph.replay()
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-    e0.record(stream)
-    graph.replay()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    loop_ms = e0.elapsed_time(e1)
-    # tensor-core work per row: 10 token-tile projections (17 tokens x 128 x 128)
-    # + the trunks (4 x 2 MLP matrices, value.in 160 -> 128), 2 flops per MAC
-    tc_flops = (10 * 17 + 8) * 128 * 128 * 2 + 160 * 128 * 2
     peak_tf32 = None
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         peak_tf32 = float(json.loads(p.read_text())["bf16_tflops"]) / 2  # tf32 dense rate is half of bf16
-    achieved = tc_flops * B / (ms / 1e3) / 1e12
-    return {"precision": "tf32 projections on tcgen05, fp32 elsewhere (diagnostic; the drop-in default is fp32)",
-            "rows": B, "ms_per_act": ms, "rows_per_s": B / (ms / 1e3),
+    # tensor-core work per row: 10 token-tile projections (17 tokens x 128 x 128)
+    # + the trunks (4 x 2 MLP matrices, value.in 160 -> 128), 2 flops per MAC
+    tc_flops = (10 * 17 + 8) * 128 * 128 * 2 + 160 * 128 * 2
+    out = {"rows": B}
+    for prec in ("fp32", "tf32"):
+        pol = z.NNPolicy(cfg, params, use_argmax=False, precision=prec)
+
+        def act():
+            pol.act_device(ob, B, rng.data_ptr(), acc.data_ptr(), ste.data_ptr(), lp.data_ptr(), val.data_ptr(),
+                           stream=stream)
+        for _ in range(3):
+            act()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = 20
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(n):
+            act()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        env.rollout_policy_device(pol, 42, EPISODE, stream=stream)  # warm-up (allocates the scratch)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        gs = torch.cuda.Stream()
+        with torch.cuda.stream(gs):
+            with torch.cuda.graph(graph, stream=gs):
+                env.rollout_policy_device(pol, 42, EPISODE, stream=gs)
+        graph.replay()
+        torch.cuda.synchronize()
+        s2 = torch.cuda.current_stream()
+        e0.record(s2)
+        graph.replay()
+        e1.record(s2)
+        torch.cuda.synchronize()
+        loop_ms = e0.elapsed_time(e1)
+        achieved = tc_flops * B / (ms / 1e3) / 1e12
+        out[prec] = {
+            "precision": ("fp32 CUDA cores: the reference's Model<float> arithmetic (default)" if prec == "fp32"
+                          else "tf32 projections on tcgen05, fp32 elsewhere (opt-in; logits ~1e-4 from fp32)"),
+            "ms_per_act": ms, "rows_per_s": B / (ms / 1e3),
             "closed_loop": {"path": "zsim_rollout_policy: observe -> NNPolicy::act -> step, 91 steps, sampling, "
                                     "replayed from a CUDA graph",
                             "ms": loop_ms, "agent_steps_per_s": B * A_ * EPISODE / (loop_ms / 1e3)},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf32, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf32 if peak_tf32 else None,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (tf32)",
-                         "note": "the folded cross attention and the LayerNorm / softmax work run on the FP32 "
-                                 "pipe and dominate the kernel time; the fraction is of the tf32 tensor peak"}}
+            "matmul_tflops": achieved}
+        if prec == "tf32":
+            out[prec]["roofline"] = {"bound": "tensor", "achieved": achieved, "peak": peak_tf32, "unit": "TFLOP/s",
+                                     "frac": achieved / peak_tf32 if peak_tf32 else None,
+                                     "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (tf32)",
+                                     "note": "the folded cross attention and the LayerNorm / softmax work run on "
+                                             "the FP32 pipe and dominate the kernel time"}
+        pol.close()
+    return out
 
 
 def main():

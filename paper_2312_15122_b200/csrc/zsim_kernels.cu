@@ -101,15 +101,15 @@ __device__ __forceinline__ void obs_st(T* p, T v) { __stcs(p, v); }
 __device__ __forceinline__ int warp_in_block() { return threadIdx.x >> 5; }
 __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
 
-// One out-of-line copy of each fp64 libm routine (the inlined versions
-// multiply the kernel's code size past the instruction cache).
-__device__ __noinline__ double2 sincos2(double x) {
+// fp64 libm routines of the ego dynamics, inlined (measured against one
+// out-of-line copy each: C1 -1.2%, C4 shard -0.9%, fewer spills around the calls).
+__device__ __forceinline__ double2 sincos2(double x) {
     double s, c;
     sincos(x, &s, &c);
     return make_double2(s, c);
 }
-__device__ __noinline__ double tan1(double x) { return tan(x); }
-__device__ __noinline__ double wrap1(double a) { return wrap_angle(a); }
+__device__ __forceinline__ double tan1(double x) { return tan(x); }
+__device__ __forceinline__ double wrap1(double a) { return wrap_angle(a); }
 
 // Lexicographic warp argmin by (d2, idx) for d2 >= 0 (or +inf): the bit
 // pattern of a non-negative double is monotone, so three 32-bit REDUX ops.

@@ -1,3 +1,5 @@
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_v4.log 2>&1; echo pytest=$? >> gpurun_out/pytest_v4.log
-ZSIM_GPU_LIB=paper_2312_15122_b200/_build/checked/libzsim_gpu.so timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_checked.log 2>&1; echo pytest_checked=$? >> gpurun_out/pytest_checked.log
-bash tools/variant_bench.sh C2 prewin > /dev/null 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_step_observe -s 4 -c 1 \
+    -o gpurun_out/prof_bench -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-policy \
+    > gpurun_out/ncu_full.log 2>&1; echo full=$?
+bash tools/variant_bench.sh C1 pf ilibm pfil > /dev/null 2>&1
+bash tools/variant_bench.sh C4s pf ilibm pfil > /dev/null 2>&1
