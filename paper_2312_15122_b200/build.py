@@ -91,6 +91,26 @@ def build(force: bool = False, verbose: bool = False, pathstats: bool = False, v
     return out
 
 
+MULTI_GPU_OUT = PKG / "zsim_multi_gpu"
+
+
+def build_multi_gpu(force: bool = False) -> Path:
+    """The single-process multi-GPU driver (csrc/zsim_multi_gpu.cpp, SURVEY
+    8e): host C++ over the C-ABI, linked against libzsim_gpu.so in-tree."""
+    lib = build()
+    src = CSRC / "zsim_multi_gpu.cpp"
+    deps = [src, lib, PKG.parent / "include" / "zsim_gpu.h"]
+    if not force and MULTI_GPU_OUT.exists() and all(d.stat().st_mtime <= MULTI_GPU_OUT.stat().st_mtime for d in deps):
+        return MULTI_GPU_OUT
+    cuda = Path(NVCC).resolve().parent.parent
+    tmp = MULTI_GPU_OUT.with_suffix(".tmp")
+    _run([CXX, "-std=c++17", "-O2", "-Wall", "-I", str(PKG.parent / "include"), "-I", str(cuda / "include"),
+          str(src), "-o", str(tmp), str(lib), "-Wl,-rpath,$ORIGIN", str(cuda / "lib64" / "libcudart_static.a"),
+          "-ldl", "-lrt", "-lpthread"])
+    os.replace(tmp, MULTI_GPU_OUT)
+    return MULTI_GPU_OUT
+
+
 if __name__ == "__main__":
     var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
     defs = [a[2:] for a in sys.argv if a.startswith("-D")]
