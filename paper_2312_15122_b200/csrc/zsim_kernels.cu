@@ -617,7 +617,8 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
 // Agent box at log slice `slice` (agent_box, simcore.cpp:162-165): corners
 // into smem and the SAT overlap with the ego box (geometry.cpp:65-75).
 __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size_t slice, int j, const Box& eb,
-                                                 const double* EX, const double* EY, const WarpBuf& w) {
+                                                 const double* EX, const double* EY, const WarpBuf& w,
+                                                 bool keep_corners = true) {
     const int A = pk.d.A;
     Box ab;
     ab.cx = double(pk.ag_x[slice + j]);
@@ -631,11 +632,13 @@ __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size
     box_corners(ab, X, Y);
     // corner slots hold one 32-agent chunk (lane = j mod 32); beyond 32 agents
     // the observation recomputes each chunk's corners (agent_corners)
+    if (keep_corners) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        ZS_CHECK(j >= 0 && j < A);
-        w.agx[k * kAgSlots + (j & 31)] = X[k];
-        w.agy[k * kAgSlots + (j & 31)] = Y[k];
+        for (int k = 0; k < 4; ++k) {
+            ZS_CHECK(j >= 0 && j < A);
+            w.agx[k * kAgSlots + (j & 31)] = X[k];
+            w.agy[k * kAgSlots + (j & 31)] = Y[k];
+        }
     }
     return boxes_overlap(eb, EX, EY, ab, X, Y) ? 1 : 0;
 }
@@ -713,39 +716,78 @@ __device__ __forceinline__ void agent_bounds(const DevPack& pk, int sc, size_t s
 // One agent of the pruned pass (beyond 32 agents): fp32 distance bounds
 // (lower bound into agd, upper-bound key into alist: 0 for an overlap) and
 // the SAT only when the lower bound cannot prove the boxes apart.
-__device__ __forceinline__ int agent_bounded(const DevPack& pk, int sc, size_t slice, int j, const Box& eb,
-                                             const double* EX, const double* EY, const WarpBuf& w, unsigned& key) {
-    float lo, hi;
-    agent_bounds(pk, sc, slice, j, eb, lo, hi);
-    const int f = lo > 0.f ? 0 : agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
-    w.agd[j] = double(lo);
-    key = f == 1 ? 0u : __float_as_uint(hi);
-    return f;
-}
-
 // Agent boxes at one slice + overlap flags into w.agx/agy/agf for a row
 // (-1 = invalid / skipped / t past the log); returns whether any overlaps.
 // (Inlined: a __noinline__ call forces the WarpBuf into local memory.)
+//
 // Beyond 32 agents the corners are not kept (the observation recomputes them
 // per chunk) and the distance bounds of the observation's pruning are computed
-// here, in the same pass over the agents (agent_bounded).
+// here, in the same pass over the agents: fp32 lower bound into agd,
+// upper-bound key into alist (0 for an overlap, ~0u for an invalid agent).  A
+// positive lower bound proves the boxes apart; the agents it cannot decide are
+// queued (in the free corner slots) and get the exact fp64 SAT afterwards, one
+// per lane -- a few per row, instead of one divergent SAT pass per 32-agent
+// chunk.
 __device__ __forceinline__ bool agent_boxes(const DevPack& pk, int sc, size_t slice, int na, int skip, bool t_ok, const Box& eb,
                                              const double* EX, const double* EY, const WarpBuf& w) {
     bool hit = false;
-    for (int j = lane_id(); j < na; j += 32) {
+    const int lane = lane_id();
+    if (na <= 32) {
+        for (int j = lane; j < na; j += 32) {
+            int f = -1;
+            if (t_ok && j != skip && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
+            w.agf[j] = f;
+            hit |= f == 1;
+        }
+        return hit;
+    }
+    int* pend = reinterpret_cast<int*>(w.agy);  // 4 * kAgSlots doubles = room for 256 agent columns
+    int npend = 0;
+    for (int j0 = 0; j0 < na; j0 += 32) {
+        const int j = j0 + lane;
         int f = -1;
         unsigned key = 0xFFFFFFFFu;
-        if (t_ok && j != skip && pk.ag_valid[slice + j]) {
-            if (na > 32) {
-                f = agent_bounded(pk, sc, slice, j, eb, EX, EY, w, key);
-            } else {
-                f = agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
-            }
+        bool sat = false;
+        if (j < na && t_ok && j != skip && pk.ag_valid[slice + j]) {
+            float lo, hi;
+            agent_bounds(pk, sc, slice, j, eb, lo, hi);
+            w.agd[j] = double(lo);
+            f = 0;
+            key = __float_as_uint(hi);
+            sat = !(lo > 0.f);
         }
-        w.agf[j] = f;
-        if (na > 32) w.alist[j] = int(key);
-        hit |= f == 1;
+        const unsigned bal = __ballot_sync(FULL, sat);
+        if (sat) {
+            const int q = npend + __popc(bal & lanemask_lt());
+            if (q < 2 * 4 * kAgSlots) pend[q] = j;
+        }
+        npend += __popc(bal);
+        if (j < na) {
+            w.agf[j] = f;
+            w.alist[j] = int(key);
+        }
     }
+    __syncwarp();
+    if (npend > 2 * 4 * kAgSlots) {
+        // more undecided agents than queue slots (more than 256 agents): decide in place
+        for (int j = lane; j < na; j += 32)
+            if (w.agf[j] == 0 && !(w.agd[j] > 0.0) && agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w, false)) {
+                w.agf[j] = 1;
+                w.alist[j] = 0;
+                hit = true;
+            }
+        return hit;
+    }
+    for (int k = lane; k < npend; k += 32) {
+        const int j = pend[k];
+        ZS_CHECK(j >= 0 && j < na);
+        if (agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w, false)) {
+            w.agf[j] = 1;
+            w.alist[j] = 0;  // an overlap's distance is 0: the smallest key
+            hit = true;
+        }
+    }
+    __syncwarp();
     return hit;
 }
 

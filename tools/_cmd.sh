@@ -1,6 +1,3 @@
-free -g | head -2
-for c in C2 C3 C4s; do
-  timeout 1500 python bench.py --config $c --no-policy > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo $c=$?
-done
-timeout 2400 python bench.py --config C4 --no-policy --no-e2e > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err; echo C4=$?
-free -g | head -2
+timeout 900 python -m pytest tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py tests/test_controlled.py tests/test_gpu_comm.py -x -q > gpurun_out/pytest_sat.log 2>&1; echo pytest=$? >> gpurun_out/pytest_sat.log
+bash tools/variant_bench.sh C2 sat0 > /dev/null 2>&1
+bash tools/variant_bench.sh C4s sat0 > /dev/null 2>&1
