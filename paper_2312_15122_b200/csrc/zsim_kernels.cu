@@ -665,24 +665,6 @@ __device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t 
     }
 }
 
-// k-th smallest (1-based) of the keys' top 16 bits over key[0..n) across the
-// warp, as key bits (low 16 zero): MSB-first radix select with warp-wide
-// counts.  Uniform result.
-__device__ __forceinline__ unsigned warp_kth_key(const int* key, int n, int k) {
-    unsigned prefix = 0;
-#pragma unroll 1
-    for (int bit = 31; bit >= 16; --bit) {  // top 16 bits (the caller rounds the result up)
-        const unsigned hi = prefix >> bit;  // the bits above, this bit 0
-        unsigned c = 0;
-        for (int j = lane_id(); j < n; j += 32) c += (unsigned(key[j]) >> bit) == hi ? 1u : 0u;
-        c = __reduce_add_sync(FULL, c);
-        if (unsigned(k) > c) {
-            k -= int(c);
-            prefix |= 1u << bit;
-        }
-    }
-    return prefix;
-}
 
 // Bounds on obb_distance (geometry.cpp:77-88) between the ego box and agent
 // j at log slice `slice`, in fp32 with margins (1e-4 + 1e-5 D) far above its
@@ -855,6 +837,59 @@ __device__ __forceinline__ unsigned warp_incl_scan(unsigned v) {
         if (lane >= off) v += o;
     }
     return v;
+}
+
+// k-th smallest (1-based) of the keys' top 16 bits over key[0..n) across the
+// warp, as key bits (low 16 zero): two 8-bit radix-select passes over a
+// 256-bin shared histogram (`hist`: 256 u32 of scratch, bin d at
+// (d & 7) * 32 + d / 8 so each lane's 8 consecutive digits are conflict-free).
+// The same result as a bitwise MSB-first select over the 16 bits.  Uniform.
+__device__ __forceinline__ unsigned warp_kth_key(const int* key, int n, int k, unsigned* hist) {
+    const int lane = lane_id();
+    unsigned prefix = 0;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        const int shift = 24 - 8 * pass;
+        for (int i = lane; i < 256; i += 32) hist[i] = 0u;
+        __syncwarp();
+        for (int j = lane; j < n; j += 32) {
+            const unsigned u = unsigned(key[j]);
+            if (pass == 0 || (u >> 24) == (prefix >> 24)) {
+                const unsigned d = (u >> shift) & 0xFFu;
+                atomicAdd(&hist[((d & 7u) << 5) | (d >> 3)], 1u);
+            }
+        }
+        __syncwarp();
+        unsigned v[8], sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            v[q] = hist[q * 32 + lane];  // digit 8 * lane + q
+            sum += v[q];
+        }
+        const unsigned incl = warp_incl_scan(sum);
+        const int owner = __ffs(__ballot_sync(FULL, incl >= unsigned(k))) - 1;
+        ZS_CHECK(owner >= 0);
+        int dsel = 0;
+        unsigned below = 0;
+        if (lane == owner) {
+            unsigned run = incl - sum;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (run + v[q] >= unsigned(k)) {
+                    dsel = 8 * lane + q;
+                    below = run;
+                    break;
+                }
+                run += v[q];
+            }
+        }
+        dsel = __shfl_sync(FULL, dsel, owner);
+        below = __shfl_sync(FULL, below, owner);
+        k -= int(below);
+        prefix |= unsigned(dsel) << shift;
+        __syncwarp();
+    }
+    return prefix;
 }
 
 // A point set in chunked spatial order (zsim_pack.cuh).
@@ -1378,7 +1413,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         if (nvalid > Ka) {
             // Ka-th smallest upper bound on the keys' top 16 bits, rounded up
             // to the bucket's largest key: still an upper bound, half the passes
-            const double U = double(__uint_as_float(warp_kth_key(w.alist, na, Ka) | 0xFFFFu));
+            const double U = double(__uint_as_float(warp_kth_key(w.alist, na, Ka, reinterpret_cast<unsigned*>(w.agy)) | 0xFFFFu));
             __syncwarp();
             int n = 0;
             for (int j0 = 0; j0 < na; j0 += 32) {
