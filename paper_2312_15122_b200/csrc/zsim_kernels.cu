@@ -2207,8 +2207,10 @@ bool observe_split(const KernelArgs& a, int policy) {
     int per_sm = blocks_per_sm(fn, smem_bytes(t), 32 * warps);
     if (per_sm < 1) per_sm = 1;
     const int sms = sm_count();
-    // measured with the in-phase 14-warp CTAs: fused ahead at 1 and 4 waves
-    // (C1; C4 shard +6%), split clearly ahead at many waves (C2, 126 waves: +43%)
+    // measured with the in-phase 14-warp CTAs: ego rows run fused at any
+    // depth (C1 1 wave; C4 8 / 16 waves +3.4% / +1.5%, C3 16 waves +0.6%);
+    // controlled rows (C2) split beyond 8 waves (16 waves +29%, 126: +43%)
+    if (a.pk.row_actor == nullptr) return false;
     return a.pk.d.B > 8 * sms * per_sm * warps;
 }
 

@@ -20,7 +20,8 @@ dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in obs.items
 view = ObsView()
 for k, t in dev.items():
     setattr(view, k, C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_float)))
-pol = z.NNPolicy(z.ModelConfig(), z.init_params(z.ModelConfig(), 1), use_argmax=False)
+pol = z.NNPolicy(z.ModelConfig(), z.init_params(z.ModelConfig(), 1), use_argmax=False,
+                 precision=sys.argv[3] if len(sys.argv) > 3 else "fp32")
 rng = torch.arange(B, dtype=torch.int64, device="cuda")
 a = torch.zeros(B, dtype=torch.int32, device="cuda")
 s = torch.zeros_like(a)
