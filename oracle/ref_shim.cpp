@@ -350,6 +350,20 @@ __attribute__((visibility("default"))) int zref_rollout(zref_env* e, int32_t hor
 // the [episode_len][n_rows] action tensors, re-initialising the state every
 // `episode_len` steps.  Returns wall seconds of the timed loop, max over
 // shards (all shards start together).
+// The reference's own step benchmark (simcore.cpp:654-699: zero actions,
+// dones off, step only), for continuity with the reference's reported
+// numbers: mean step ms per batch size (refpy formats bench_csv's columns).
+__attribute__((visibility("default"))) int zref_bench_step(const char* path, const int32_t* batch_sizes, int32_t n,
+                                                           int32_t steps, int32_t warmup, const zsim_sim_config* cfg,
+                                                           double* mean_step_ms) {
+    return guarded([&] {
+        scenario::Dataset ds(path);
+        std::vector<int> bs(batch_sizes, batch_sizes + n);
+        const std::vector<sim::BenchRow> rows = sim::bench_step(ds, bs, steps, warmup, to_cfg(cfg));
+        for (size_t i = 0; i < rows.size(); ++i) mean_step_ms[i] = rows[i].mean_step_ms;
+    });
+}
+
 __attribute__((visibility("default"))) int zref_bench(const char* path, int32_t n_rows, int32_t horizon,
                                                       const zsim_sim_config* cfg, int32_t threads, int32_t warmup,
                                                       int32_t steps, int32_t episode_len, const int32_t* accel,

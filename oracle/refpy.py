@@ -49,6 +49,8 @@ _SIGS = {
                                    C.POINTER(C.c_float), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                    C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_uint8),
                                    C.POINTER(C.c_uint8)] + [C.POINTER(C.c_float)] * 5),
+    "zref_bench_step": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_int32,
+                                  C.POINTER(SimConfigC), C.POINTER(C.c_double)]),
     "zref_bench": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(SimConfigC), C.c_int32, C.c_int32,
                              C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_uint64,
                              C.POINTER(C.c_double)]),
@@ -437,3 +439,22 @@ def policy_act(params, obs: dict, B: int, rng, use_argmax: bool, cfg=None) -> di
                                     _ptr(out["logp"], C.c_float), _ptr(out["value"], C.c_float)))
     out["rng"] = r
     return out
+
+
+def bench_step(zsim, batch_sizes, steps: int, warmup: int, config=None) -> str:
+    """The reference's own sim::bench_step (simcore.cpp:654-699): step-only
+    timing at each batch size, zero actions, dones off -> bench_csv's CSV
+    (batch_size,mean_step_ms,amortized_us_per_scenario)."""
+    path, tmp = _as_path(zsim)
+    try:
+        bs = np.ascontiguousarray(batch_sizes, dtype=np.int32)
+        ms = np.zeros(bs.size)
+        cfg = config_c(config)
+        _check(lib().zref_bench_step(path.encode(), _ptr(bs, C.c_int32), int(bs.size), int(steps), int(warmup),
+                                     C.byref(cfg), _ptr(ms, C.c_double)))
+        lines = ["batch_size,mean_step_ms,amortized_us_per_scenario"]
+        lines += [f"{int(b)},{m:.6g},{m * 1000.0 / b:.6g}" for b, m in zip(bs, ms)]
+        return "\n".join(lines) + "\n"
+    finally:
+        if tmp is not None:
+            os.unlink(path)
