@@ -1,4 +1,2 @@
 python tools/bench_step.py 64 50 > gpurun_out/bench_step.csv 2> gpurun_out/bench_step.err; echo bs=$?
-M=gpu__time_duration.sum,smsp__inst_executed.sum,sm__inst_executed_pipe_fp64.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum
-timeout 900 ncu --metrics $M --clock-control none -k regex:k_step_observe -s 3 -c 4 --csv python bench.py --config C2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-policy > gpurun_out/c2_fp64.csv 2> gpurun_out/c2_fp64.err; echo c2=$?
-timeout 900 ncu --metrics $M --clock-control none -k regex:k_step_observe -s 3 -c 2 --csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-policy > gpurun_out/c1_fp64.csv 2> gpurun_out/c1_fp64.err; echo c1=$?
+timeout 900 python bench.py --config C3 --no-policy --no-cpu-baseline --no-e2e > gpurun_out/bench_C3.json 2> gpurun_out/bench_C3.err; echo c3=$?

@@ -22,8 +22,8 @@ def device_rows(zsim, n_scen, steps, warmup=10):
     for bs in BATCH:
         idx = np.arange(bs) % n_scen  # ds indices i % ds.size(), as bench_step
         env = z.Env(zsim, indices=idx, config=z.SimConfig(disable_dones=True))
-        a = torch.full((bs,), env.zero_accel_idx(), dtype=torch.int32, device="cuda")
-        s = torch.full((bs,), env.zero_steer_idx(), dtype=torch.int32, device="cuda")
+        a = torch.full((bs,), env.zero_accel_idx, dtype=torch.int32, device="cuda")
+        s = torch.full((bs,), env.zero_steer_idx, dtype=torch.int32, device="cuda")
         s0, s1, so = env.device_state(), env.device_state(), env.device_stepout()
         env.reset_device(42, s0)
         for _ in range(warmup):
