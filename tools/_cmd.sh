@@ -1,2 +1,2 @@
-python tools/bench_step.py 64 50 > gpurun_out/bench_step.csv 2> gpurun_out/bench_step.err; echo bs=$?
-timeout 900 python bench.py --config C3 --no-policy --no-cpu-baseline --no-e2e > gpurun_out/bench_C3.json 2> gpurun_out/bench_C3.err; echo c3=$?
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_full.log 2>&1; echo pytest=$? >> gpurun_out/pytest_full.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$? >> gpurun_out/smoke.log
