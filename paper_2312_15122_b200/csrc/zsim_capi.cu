@@ -528,6 +528,10 @@ void stage_env(zsim_env* env, const std::vector<zs::Scene>& scenes, int horizon,
     d.S = S;
     const EgoBoxDims ebd{env->cfg.ego_length, env->cfg.ego_width, env->cfg.ego_center_offset};
     d.GC = std::max(1, (d.C - 1 + kSegGroup - 1) / kSegGroup);
+    // the top-k scratch holds 16-bit point positions (zsim_kernels.cu, WarpBuf)
+    if (d.P > 65535 || d.R > 65535)
+        raise(Err::invalid_argument, "more than 65535 road or route points in one scenario are not supported on the "
+                                     "device path");
     d.PC = (d.P + kChunk - 1) / kChunk;
     d.RC = (d.R + kChunk - 1) / kChunk;
     if (d.L > kMaxLanes) {

@@ -161,10 +161,10 @@ struct WarpBuf {
     double* agd;           // [A] bbox distance
     int* agf;              // [A] -1 invalid, 0 separate, 1 overlap
     unsigned short* hist;  // [32*32] lane-private u16 histogram; reused as counting-sort counts u32[NB2]
-    int* cidx;             // [cap] candidate indices
+    uint16_t* cidx;        // [cap] candidate positions (16-bit: point sets hold < 65536 points)
     double* ckey;          // [cap] exact keys
-    int* cinfo;            // [cap] bucket << 16 | slot
-    int* order;            // [cap] candidates grouped by bucket
+    uint16_t* cinfo;       // [cap] candidates' reference indices (the tie-break key)
+    uint16_t* order;       // [max(cap, chunks)] chunk list, then candidates grouped by bucket, then the selection
     int* sel;              // [Ka] selected agents (road/route selections land in `order`)
     int* alist;            // [A] bound keys, then the agents that survive the bound test (beyond 32 agents)
     unsigned char* sflag;  // [NS] pre-step stopped flags
@@ -191,11 +191,11 @@ inline SmemLayout warp_layout(int A, int cap, int ka, int ns, int nch) {
     const size_t agents_end = o;
     o = u0;
     put(L.hist, cap > 0 ? 32 * 32 * 2 : 0);  // no top-k buffers in the step-only kernel (cap = 0)
-    put(L.cidx, size_t(cap) * 4);
+    put(L.cidx, size_t(cap) * 2);
     put(L.ckey, size_t(cap) * 8);
-    put(L.cinfo, size_t(cap) * 4);
+    put(L.cinfo, size_t(cap) * 2);
     // also the top-k's chunk list: up to nch chunks (P > 32 * cap points)
-    put(L.order, size_t(cap > 0 ? (cap > nch ? cap : nch) : 0) * 4);
+    put(L.order, size_t(cap > 0 ? (cap > nch ? cap : nch) : 0) * 2);
     o = o > agents_end ? o : agents_end;
     put(L.sflag, size_t(ns) + 1);
     L.total = uint32_t(al16(o));
@@ -214,10 +214,10 @@ __device__ __forceinline__ WarpBuf carve(unsigned char* base, const KernelArgs& 
     w.sel = reinterpret_cast<int*>(p + L.sel);
     w.alist = reinterpret_cast<int*>(p + L.alist);
     w.hist = reinterpret_cast<unsigned short*>(p + L.hist);
-    w.cidx = reinterpret_cast<int*>(p + L.cidx);
+    w.cidx = reinterpret_cast<uint16_t*>(p + L.cidx);
     w.ckey = reinterpret_cast<double*>(p + L.ckey);
-    w.cinfo = reinterpret_cast<int*>(p + L.cinfo);
-    w.order = reinterpret_cast<int*>(p + L.order);
+    w.cinfo = reinterpret_cast<uint16_t*>(p + L.cinfo);
+    w.order = reinterpret_cast<uint16_t*>(p + L.order);
     w.sflag = p + L.sflag;
     return w;
 }
@@ -916,7 +916,7 @@ __device__ __forceinline__ void chunk_bounds(float4 bb, double px, double py, do
 // batched for memory-level parallelism; calls f(position, approx_key, point)
 // for every existing point.
 template <class F>
-__device__ __forceinline__ void over_chunks(const PointSet& ps, const int* list, int nlist, float pxf, float pyf,
+__device__ __forceinline__ void over_chunks(const PointSet& ps, const uint16_t* list, int nlist, float pxf, float pyf,
                                             F&& f) {
     const int lane = lane_id();
     for (int j0 = 0; j0 < nlist; j0 += kUnroll) {
@@ -959,8 +959,9 @@ __device__ __forceinline__ void over_chunks(const PointSet& ps, const int* list,
 //     (key, reference index).
 // ---------------------------------------------------------------------------
 __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, bool use_r, double r2, float4 bbox,
-                                      int cap, unsigned short* __restrict__ hist, int* __restrict__ cidx,
-                                      double* __restrict__ ckey, int* __restrict__ cinfo, int* __restrict__ order,
+                                      int cap, unsigned short* __restrict__ hist, uint16_t* __restrict__ cidx,
+                                      double* __restrict__ ckey, uint16_t* __restrict__ cinfo,
+                                      uint16_t* __restrict__ order,
                                       float4 hv, float4* hint, int which) {
     const int lane = lane_id();
     const int n = ps.n;
@@ -1017,7 +1018,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     float tc = T < INFINITY ? fminf(__double2float_ru(T + key_margin(T, ep)), hi) : hi;
 
     // ---- 2. needed chunks + candidate compaction ----
-    int* list = order;  // chunk list (order is free until the final sort)
+    uint16_t* list = order;  // chunk list (order is free until the final sort)
     int nlist = 0;
     auto build_list = [&](float t) {
         nlist = 0;
@@ -1605,7 +1606,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const float2* pts = pk.road_xy + size_t(sc) * pk.d.P;
         const int32_t* oidx = pk.road_oi + size_t(sc) * pk.d.P;
         const double R = cfg.feature_radius;
-        const int* sel = w.order;
+        const uint16_t* sel = w.order;
         const PointSet ps{pts, oidx, pk.road_cb + size_t(sc) * pk.d.PC, n, (n + kChunk - 1) / kChunk};
         const int nsel = warp_topk(ps, Kr, r.x, r.y, true, R * R, pk.road_box[sc], a.cand_cap, w.hist, w.cidx, w.ckey,
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 0);
@@ -1644,7 +1645,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const int n = pk.n_route[sc];
         const float2* pts = pk.route_xy + size_t(sc) * pk.d.R;
         const int32_t* oidx = pk.route_oi + size_t(sc) * pk.d.R;
-        const int* sel = w.order;
+        const uint16_t* sel = w.order;
         const PointSet ps{pts, oidx, pk.route_cb + size_t(sc) * pk.d.RC, n, (n + kChunk - 1) / kChunk};
         const int nsel = warp_topk(ps, Kl, r.x, r.y, false, 0.0, pk.route_box[sc], a.cand_cap, w.hist, w.cidx, w.ckey,
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 1);
