@@ -337,12 +337,14 @@ __device__ __forceinline__ float seg_inv_f(float4 f) {
 // (approximate t, clamped, so the evaluated point stays on the segment) adds
 // <= 2^-20 (d + |b-a|); so |d_f32 - d_exact| <= delta = 2^-18 (fe + |q-o|_1 + d)
 // with fe = ln_fe.
-//  1. fp32 distance of every segment to q0, minimum m0.
-//  2. The corners lie within R of q0, so (triangle inequality) the exact
-//     minimiser of any query lies among the "near" segments with
-//     d0 <= sqrt(m0) + 2R + 4 delta; their fp32 distances give each query's
-//     minimum m_q.
-//  3. Near segments with d_q <= sqrt(m_q) + 2 delta (every segment that can
+//  0. 8-segment group boxes give every query's "needed" groups: the corners
+//     lie within R of q0, so (triangle inequality) the exact minimiser of any
+//     query lies among the segments with d0 <= sqrt(m0) + 2R + 4 delta, all
+//     inside groups whose box lower bound is within the far-corner bound
+//     + 2R + 8 delta.
+//  1. fp32 distances of every query to the needed segments: each query's
+//     minimum m_q (one pass for all five queries).
+//  2. Needed segments with d_q <= sqrt(m_q) + 2 delta (every segment that can
 //     tie the exact minimum) are evaluated in fp64 with the reference's
 //     expressions; the exact lexicographic (d2, segment) minimum per octet is
 //     the reference's argmin.
@@ -428,57 +430,30 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
             if (ngr > 16) need |= ~0ull << 16;  // longer lanes: groups past 16 always scanned
         }
         if (l0 == 0) ROW_MARK(b, 10);
-        // ---- 1. q0 over the needed groups ----
-        float m0 = INFINITY;
+        // ---- 1+2. every query over the needed groups: the exact minimiser of
+        // each query lies among the segments near q0, all inside the needed
+        // groups, and the farther ones never reach a query's minimum ----
+        float m[NQU];
+#pragma unroll
+        for (int q = 0; q < NQU; ++q) m[q] = INFINITY;
         for (unsigned long long mm = need & ((ngr >= 64) ? ~0ull : ((1ull << ngr) - 1)); mm; mm &= mm - 1) {
             const int si = (__ffsll(mm) - 1) * kSegGroup + gg;
             if (si < nseg) {
                 const float4 f = F[si];
-                m0 = fminf(m0, seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)));
+                const float inv = seg_inv_f(f);
+#pragma unroll
+                for (int q = 0; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f, inv));
             }
         }
 #pragma unroll 1
         for (int si = 64 * kSegGroup + gg; si < nseg; si += 8) {  // beyond the 64-bit group mask
             const float4 f = F[si];
-            m0 = fminf(m0, seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)));
-        }
-        m0 = octet_minf(m0);
-        float near_thr;
-        {
-            const float dm = sqrtf(m0);
-            const float d0 = 0x1p-18f * (fe + fabsf(qxf[0]) + fabsf(qyf[0]) + dm + 4.f * R) + 1e-30f;
-            const float r = dm + 2.f * R + 4.f * d0;
-            near_thr = r * r * (1.f + 0x1p-20f);
-        }
-        if (l0 == 0) ROW_MARK(b, 11);
-        // ---- 2. near segments: per-query minimum ----
-        float m[NQU];
-        m[0] = m0;
-#pragma unroll
-        for (int q = 1; q < NQU; ++q) m[q] = INFINITY;
-        unsigned long long nearm = 0;  // bit g: this lane's segment of group g is near
-        for (unsigned long long mm = need & ((ngr >= 64) ? ~0ull : ((1ull << ngr) - 1)); mm; mm &= mm - 1) {
-            const int g = __ffsll(mm) - 1;
-            const int si = g * kSegGroup + gg;
-            if (si < nseg) {
-                const float4 f = F[si];
-                const float inv = seg_inv_f(f);
-                if (seg_d2_f(qxf[0], qyf[0], f, inv) <= near_thr) {
-                    nearm |= 1ull << g;
-#pragma unroll
-                    for (int q = 1; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f, inv));
-                }
-            }
-        }
-#pragma unroll 1
-        for (int si = 64 * kSegGroup + gg; si < nseg; si += 8) {
-            const float4 f = F[si];
             const float inv = seg_inv_f(f);
-            if (seg_d2_f(qxf[0], qyf[0], f, inv) <= near_thr) {
 #pragma unroll
-                for (int q = 1; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f, inv));
-            }
+            for (int q = 0; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f, inv));
         }
+        m[0] = octet_minf(m[0]);
+        if (l0 == 0) ROW_MARK(b, 11);
         // A corner only needs its in-corridor bit (roads.cpp:202-208): when its
         // fp32 distance to this route lane is below the lane's smallest
         // half-width (or above the largest) by more than delta, the verdict is
@@ -530,17 +505,15 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
                 }
             }
         };
-        while (nearm) {
-            const int si = (__ffsll(nearm) - 1) * kSegGroup + gg;
-            ZS_CHECK(si < nseg);
-            nearm &= nearm - 1;
-            exact(si, F[si]);
+        // the thresholds select the candidates: a segment far from every
+        // query's minimum passes none
+        for (unsigned long long mm = need & ((ngr >= 64) ? ~0ull : ((1ull << ngr) - 1)); mm; mm &= mm - 1) {
+            const int si = (__ffsll(mm) - 1) * kSegGroup + gg;
+            if (si < nseg) exact(si, F[si]);
         }
 #pragma unroll 1
-        for (int si = 64 * kSegGroup + gg; si < nseg; si += 8) {  // beyond the 64-bit group mask
-            const float4 f = F[si];
-            if (seg_d2_f(qxf[0], qyf[0], f, seg_inv_f(f)) <= near_thr) exact(si, f);
-        }
+        for (int si = 64 * kSegGroup + gg; si < nseg; si += 8) exact(si, F[si]);  // beyond the 64-bit group mask
+
         if (l0 == 0) ROW_MARK(b, 13);
         // ---- per-octet exact argmin, then s / signed d / half-width per (query, route lane) ----
         int hi_ = INT_MAX;

@@ -1,4 +1,3 @@
-python tools/e2e_breakdown.py
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dropin.py tests/test_gpu_golden.py tests/test_controlled.py -x -q 2>&1 | tail -2
-python bench.py --no-policy --no-cpu-baseline > gpurun_out/bench_e2e.json 2>/dev/null; python -c "
-import json; d=json.loads(open('gpurun_out/bench_e2e.json').read().splitlines()[-1]); print(d['value'], d['e2e'])"
+ZSIM_GPU_LIB=paper_2312_15122_b200/_build/proj1c/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py tests/test_controlled.py -x -q > gpurun_out/pytest_proj1.log 2>&1; echo pytest=$? >> gpurun_out/pytest_proj1.log
+bash tools/variant_bench.sh C1 proj1 > /dev/null 2>&1
+bash tools/variant_bench.sh C4s proj1 > /dev/null 2>&1
