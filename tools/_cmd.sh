@@ -1,3 +1,3 @@
-ZSIM_GPU_LIB=paper_2312_15122_b200/_build/proj1c/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py tests/test_controlled.py -x -q > gpurun_out/pytest_proj1.log 2>&1; echo pytest=$? >> gpurun_out/pytest_proj1.log
-bash tools/variant_bench.sh C1 proj1 > /dev/null 2>&1
-bash tools/variant_bench.sh C4s proj1 > /dev/null 2>&1
+ZSIM_GPU_LIB=paper_2312_15122_b200/_build/oic/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py -x -q > gpurun_out/pytest_oi.log 2>&1; echo pytest=$? >> gpurun_out/pytest_oi.log
+bash tools/variant_bench.sh C1 oi > /dev/null 2>&1
+bash tools/variant_bench.sh C4s oi > /dev/null 2>&1
