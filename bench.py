@@ -104,9 +104,34 @@ def plan(name: str, world: int, override: int = 0) -> dict:
     return c
 
 
+# SimConfig of every run (simcore.hpp:14-45 defaults, dones off), as key = value
+SIM_CONFIG = dict(wheelbase=3.0, ego_length=4.7, ego_width=1.9, ego_center_offset=1.5, delta_max=0.55, v_min=0.0,
+                  goal_radius=2.0, footprint_margin=0.1, stop_cross_speed=0.5, stop_zone=2.0, stop_slow_speed=0.1,
+                  disable_dones=1, w_progress=1.0, w_speed=0.1, w_lat=0.02, w_lon=0.02, terminal_penalty=10.0,
+                  n_agents=16, n_road=128, n_route=64, feature_radius=100.0, threads=1)
+
+
+def config_hash(p: dict) -> str:
+    """FNV-1a of the run's flat `key = value` dump (the reference's
+    cfg::KeyValue dump / hash, config.cpp:116-126; paper_2312_15122_b200.config):
+    the workload keys plus the SimConfig, so every result JSON names the exact
+    configuration it ran."""
+    vals = {f"sim.{k}": (format(v, ".17g") if isinstance(v, float) else str(v)) for k, v in SIM_CONFIG.items()}
+    vals.update({"bench.config": p["name"], "bench.scenarios": str(p["total"]), "bench.agents": str(p["agents"]),
+                 "bench.road_points": str(p["road_points"]), "bench.controlled": str(int(p["controlled"])),
+                 "bench.lanes": str(LANES), "bench.lane_vertices": str(LANE_VERTICES),
+                 "bench.steps_per_episode": str(EPISODE), "bench.seed.scenarios": str(STRESS_SEED),
+                 "bench.seed.actions": str(ACTION_SEED), "bench.seed.reset": str(RESET_SEED)})
+    dump = "".join(f"{k} = {vals[k]}\n" for k in sorted(vals, key=lambda x: x.encode())).encode()
+    h = 0xCBF29CE484222325
+    for b in dump:
+        h = ((h ^ b) * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
 def config_block(p: dict, world: int) -> dict:
     """`config` of the JSON line -- the same keys and values in both arms."""
-    return {"workload": p["workload"], "config_id": p["name"], "scenarios": p["total"],
+    return {"workload": p["workload"], "config_id": p["name"], "config_hash": config_hash(p), "scenarios": p["total"],
             "scenarios_per_gpu": -(-p["total"] // world), "agents": p["agents"], "road_points": p["road_points"],
             "controlled": p["controlled"], "rows": p["total"] * p["rows_per_scenario"],
             "route_points": 2 * LANES * LANE_VERTICES, "lanes": LANES, "lane_vertices": LANE_VERTICES,
@@ -214,12 +239,12 @@ def cpu_baseline(p: dict) -> dict | None:
     zsim, rows, apr = _ref_workload(p, n_scen)
     A, S = random_actions(EPISODE, rows, seed=ACTION_SEED)
     threads = os.cpu_count() or 1
-    secs = refpy.bench(zsim, rows, 92, OracleConfig(disable_dones=True), threads, 0, EPISODE, A, S)
+    secs = refpy.bench(zsim, rows, 92, OracleConfig(**SIM_CONFIG), threads, 0, EPISODE, A, S)
     # single-thread leg on a C0-sized sample (64 rows), SURVEY 8d
     z1, r1, _ = _ref_workload(p, 1 if p["controlled"] else min(64, n_scen))
     r1 = min(r1, 64)
     A1, S1 = random_actions(EPISODE, r1, seed=ACTION_SEED)
-    secs1 = refpy.bench(z1, r1, 92, OracleConfig(disable_dones=True), 1, 0, EPISODE, A1, S1)
+    secs1 = refpy.bench(z1, r1, 92, OracleConfig(**SIM_CONFIG), 1, 0, EPISODE, A1, S1)
     return {"value": rows * apr * EPISODE / secs, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"{rows} rows ({n_scen} of the {p['total']} {p['name']} scenarios) x {EPISODE} steps "
                       f"(observe+step), {threads} per-thread Env shards, oracle/_ref (-O2 -ffp-contract=off)",
@@ -247,7 +272,7 @@ def run_reference(args) -> None:
     zsim, B, apr = _ref_workload(p, n_scen)
     A, S = random_actions(EPISODE, B, seed=ACTION_SEED)
     threads = os.cpu_count() or 1
-    secs = refpy.bench(zsim, B, 92, OracleConfig(disable_dones=True), threads, args.warmup, args.steps, A, S)
+    secs = refpy.bench(zsim, B, 92, OracleConfig(**SIM_CONFIG), threads, args.warmup, args.steps, A, S)
     value = B * apr * args.steps / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -285,7 +310,7 @@ def run_ours(args) -> None:
     t_setup = time.perf_counter()
     env = z.Env.from_stress(z.StressConfig(count=S_, agents=A_, road_points=P, first_index=lo,
                                            flags=z.STRESS_C2 if controlled else 0), STRESS_SEED,
-                            config=z.SimConfig(disable_dones=True), device=local, controlled=controlled)
+                            config=z.SimConfig(**SIM_CONFIG), device=local, controlled=controlled)
     setup_s = time.perf_counter() - t_setup
     if args.launch_policy:
         env.set_launch_policy(args.launch_policy)

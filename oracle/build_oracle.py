@@ -128,10 +128,28 @@ def build_dropin(force: bool = False) -> Path | None:
     return DROPIN_OUT
 
 
+KV_OUT = HERE / "_ref" / "kv_check"
+
+
+def build_kv_check(force: bool = False) -> Path | None:
+    """The reference's cfg::KeyValue as a stdin/stdout program (kv_check.cpp)."""
+    if not reference_available() or build_ref(force) is None:
+        return KV_OUT if KV_OUT.exists() else None
+    src = HERE / "kv_check.cpp"
+    if not force and KV_OUT.exists() and src.stat().st_mtime <= KV_OUT.stat().st_mtime:
+        return KV_OUT
+    objs = [str(HERE / "_ref" / "obj" / f"{u}.o") for u in ("common", "config")]
+    tmp = KV_OUT.with_suffix(".tmp")
+    _run([CXX, "-std=c++20", "-O2", "-I", str(REF_SRC), "-o", str(tmp), str(src), *objs, "-lpthread"])
+    os.replace(tmp, KV_OUT)
+    return KV_OUT
+
+
 def build(force: bool = False) -> None:
     build_port(force)
     build_stress(force)
     build_ref(force)
+    build_kv_check(force)
     build_dropin(force)
 
 

@@ -11,8 +11,10 @@ from .env import (AGGREGATE_FIELDS, DONE_REASONS, BatchStream, DeviceEpisode, De
                   STRESS_C2, SimConfig, SimStateBatch, StepOut, StressConfig, controlled_expand, event_bit,
                   random_actions, stress_scenarios)
 from .policy import ModelConfig, NNPolicy, init_params  # noqa: F401
+from .config import KeyValue, sim_config_from_kv, sim_config_to_kv  # noqa: F401
 
 __all__ = ["Env", "SimConfig", "SimStateBatch", "StepOut", "ObservationBatch", "DeviceState", "DeviceStepOut",
            "DeviceObs", "StressConfig", "stress_scenarios", "random_actions", "ZsimError", "DONE_REASONS",
            "event_bit", "lib", "controlled_expand", "STRESS_C2", "DeviceEpisode", "aggregate_finalize",
-           "AGGREGATE_FIELDS", "BatchStream", "ModelConfig", "NNPolicy", "init_params"]
+           "AGGREGATE_FIELDS", "BatchStream", "ModelConfig", "NNPolicy", "init_params", "KeyValue",
+           "sim_config_from_kv", "sim_config_to_kv"]

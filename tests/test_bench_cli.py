@@ -70,3 +70,21 @@ def test_c4_strong_split_matches_baseline():
     for world, per in ((2, 65536), (4, 32768), (8, 16384)):
         p = bench.plan("C4", world)
         assert {hi - lo for lo, hi in (shard_rows(p["total"], world, r) for r in range(world))} == {per}
+
+
+def test_config_hash_is_the_key_value_hash():
+    """bench.py's config_hash is KeyValue.hash() of the same keys
+    (paper_2312_15122_b200.config, pinned to the reference's cfg::KeyValue)."""
+    import bench
+    from paper_2312_15122_b200.config import KeyValue
+    p = bench.plan("C1", 1)
+    kv = KeyValue()
+    for k, v in bench.SIM_CONFIG.items():
+        kv.set(f"sim.{k}", v)
+    for k, v in (("bench.config", "C1"), ("bench.scenarios", 4096), ("bench.agents", 32),
+                 ("bench.road_points", 2048), ("bench.controlled", 0), ("bench.lanes", 4),
+                 ("bench.lane_vertices", 64), ("bench.steps_per_episode", 91), ("bench.seed.scenarios", 7),
+                 ("bench.seed.actions", 123), ("bench.seed.reset", 42)):
+        kv.set(k, v)
+    assert bench.config_hash(p) == f"{kv.hash():016x}"
+    assert bench.config_hash(bench.plan("C2", 1)) != bench.config_hash(p)
