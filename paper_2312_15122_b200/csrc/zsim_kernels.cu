@@ -1347,7 +1347,8 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     // arithmetic (approximate division, clamped t) adds <= 2^-20 (d + |edge|),
     // so |d_f32 - d| <= delta = 2^-18 (S + E + d) (E bounds the edge lengths).
     // A pair enters the candidate mask when d_f32 <= (running min) + 2 delta
-    // -- a superset of the final cut -- and only candidates get the fp64
+    // -- a superset of the final cut; the running min moves once per edge, over
+    // the edge's four independent pairs -- and only candidates get the fp64
     // expressions.  A (near-)contact (min d2 < 1e-18) takes the reference's
     // full segment_segment_distance over the 16 edge pairs.
     const double* GX = rs.ex;
@@ -1432,17 +1433,6 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
             const float c0 = 0x1p-18f * (S + ge + E);  // ge also bounds the centred ego corners
             float min2 = INFINITY, thr2 = INFINITY;
             unsigned cmask = 0;
-            auto consider = [&](int p, float d2) {
-                if (d2 < min2) {
-                    min2 = d2;
-                    float m;  // sqrt.approx (rel. error < 2^-22), scaled up to an upper bound
-                    asm("sqrt.approx.f32 %0, %1;" : "=f"(m) : "f"(d2));
-                    m *= 1.f + 0x1p-20f;
-                    const float r = m + 2.f * (c0 + 0x1p-18f * m) + 1e-30f;
-                    thr2 = r * r * (1.f + 0x1p-20f);
-                }
-                if (d2 <= thr2) cmask |= 1u << p;
-            };
             // pairs base + 4 ci + ei: corner ci of (qx, qy) vs edge ei of (px, py).
             // The edge loop stays rolled (code size: the fused kernel is far
             // larger than the instruction cache); the edge's polygon rotates
@@ -1452,8 +1442,24 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 for (int ei = 0; ei < 4; ++ei) {
                     const float4 f = make_float4(px[0], py[0], px[1] - px[0], py[1] - py[0]);
                     const float inv = seg_inv_f(f);
+                    // the edge's four pairs are independent: one running-minimum
+                    // update per edge (the threshold a pair is tested against
+                    // still only shrinks, so the mask stays a superset)
+                    float d[4];
 #pragma unroll
-                    for (int ci = 0; ci < 4; ++ci) consider(base + 4 * ci + ei, seg_d2_f(qx[ci], qy[ci], f, inv));
+                    for (int ci = 0; ci < 4; ++ci) d[ci] = seg_d2_f(qx[ci], qy[ci], f, inv);
+                    const float m4 = fminf(fminf(d[0], d[1]), fminf(d[2], d[3]));
+                    if (m4 < min2) {
+                        min2 = m4;
+                        float m;  // sqrt.approx (rel. error < 2^-22), scaled up to an upper bound
+                        asm("sqrt.approx.f32 %0, %1;" : "=f"(m) : "f"(m4));
+                        m *= 1.f + 0x1p-20f;
+                        const float r = m + 2.f * (c0 + 0x1p-18f * m) + 1e-30f;
+                        thr2 = r * r * (1.f + 0x1p-20f);
+                    }
+#pragma unroll
+                    for (int ci = 0; ci < 4; ++ci)
+                        if (d[ci] <= thr2) cmask |= 1u << (base + 4 * ci + ei);
                     const float tx = px[0], ty = py[0];
                     px[0] = px[1], py[0] = py[1], px[1] = px[2], py[1] = py[2], px[2] = px[3], py[2] = py[3];
                     px[3] = tx, py[3] = ty;

@@ -1,4 +1,3 @@
-for c in C2 C3 C4s; do
-  timeout 1500 python bench.py --config $c --no-policy > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo $c=$?
-done
-timeout 2400 python bench.py --config C4 --no-policy --no-e2e > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err; echo C4=$?
+ZSIM_GPU_LIB=paper_2312_15122_b200/_build/scr4c/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py -x -q > gpurun_out/pytest_scr4.log 2>&1; echo pytest=$? >> gpurun_out/pytest_scr4.log
+bash tools/variant_bench.sh C1 scr4 > /dev/null 2>&1
+bash tools/variant_bench.sh C4s scr4 > /dev/null 2>&1
