@@ -761,8 +761,18 @@ __device__ __forceinline__ double contact_dist2(const double* GX, const double* 
 
 // Upper bound on |fp32 key - fp64 key| for points within sqrt(T)+1 of the
 // query; `ep` is the fp32 rounding error of the query coordinates.
+// An upper bound on sqrt(x), x >= 0: fp32 sqrt.approx (relative error < 2^-22)
+// of x rounded up, scaled up by 2^-20 -- for bounds, where the fp64 sqrt's
+// exactness buys nothing and its multi-instruction sequence sits on the
+// critical path.
+__device__ __forceinline__ double ub_sqrt(double x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(__double2float_ru(x)));
+    return double(r) * (1.0 + 0x1p-20);
+}
+
 __device__ __forceinline__ double key_margin(double T, double ep) {
-    double D = sqrt(T) + 1.0;
+    double D = ub_sqrt(T) + 1.0;
     double eta = ep + 0x1p-24 * (D + ep);
     double m = 2.0 * eta * (2.0 * D + eta);
     m += 0x1p-22 * (T + m) + 0x1p-50 * T;
@@ -954,8 +964,8 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
         const float kth = which == 0 ? h.z : h.w;
         if (isfinite(h.x) && isfinite(h.y) && kth >= 0.f && isfinite(kth)) {
             const double ddx = px - double(h.x), ddy = py - double(h.y);
-            const double dp = sqrt(ddx * ddx + ddy * ddy) + 1e-3 + 1e-6 * (fabs(px) + fabs(py));
-            const double rr = sqrt(double(kth)) + dp;
+            const double dp = ub_sqrt(ddx * ddx + ddy * ddy) + 1e-3 + 1e-6 * (fabs(px) + fabs(py));
+            const double rr = ub_sqrt(double(kth)) + dp;
             T = rr * rr * (1.0 + 1e-9);
         }
     }
