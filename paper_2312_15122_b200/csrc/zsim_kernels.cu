@@ -1124,7 +1124,12 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     // counting-sort counters / cursors live in the (clear) histogram area and
     // the selection is written to `order` after the ranking is complete.
     unsigned* cntb = reinterpret_cast<unsigned*>(hist);  // NB2 u32 counters
-    const double sc2 = double(NB2) / (double(tc) > 0.0 ? double(tc) : 1.0);
+    // bucket = floor(key * sc2): any positive scale keeps the buckets in key
+    // order (the same function counts, scatters and ranks), so an approximate
+    // reciprocal does
+    float rtc;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rtc) : "f"(tc > 0.f ? tc : 1.f));
+    const double sc2 = double(NB2) * double(rtc);
     int nvalid_local = 0;
     for (int c0 = 0; c0 < C; c0 += 32 * 8) {
         // reference indices of 8 candidates per lane in flight, then the exact
