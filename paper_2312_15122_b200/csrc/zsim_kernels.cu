@@ -303,6 +303,21 @@ __device__ __forceinline__ void seg8_argmin(double& d2, int& idx) {
     }
 }
 
+// Directed fp32 square roots for bounds: sqrt.approx (relative error < 2^-22)
+// scaled by 2^-20 away from the true root, so the result is a certain upper
+// (lower) bound -- the IEEE sqrtf sequence and its slow-path branch are not
+// needed where only a bound is consumed.
+__device__ __forceinline__ float sqrt_up(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r * (1.f + 0x1p-20f);
+}
+__device__ __forceinline__ float sqrt_dn(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r * (1.f - 0x1p-20f);
+}
+
 __device__ __forceinline__ float octet_minf(float v) {
 #pragma unroll
     for (int off = 4; off > 0; off >>= 1) v = fminf(v, __shfl_xor_sync(FULL, v, off));
@@ -370,7 +385,7 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
 #pragma unroll
     for (int q = 1; q < NQU; ++q) {
         const float dx = qxf[q] - qxf[0], dy = qyf[q] - qyf[0];
-        R = fmaxf(R, sqrtf(dx * dx + dy * dy));
+        R = fmaxf(R, sqrt_up(dx * dx + dy * dy));
     }
     R = R * (1.f + 0x1p-16f) + 1e-6f;
     // lanes (q, k) = (lane >> 2, lane & 3) run the lane_hit of query q on route lane l0 + k
@@ -415,8 +430,8 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
                     const float x0 = bb.x - qxf[0], x1 = qxf[0] - bb.z, y0 = bb.y - qyf[0], y1 = qyf[0] - bb.w;
                     const float nx = fmaxf(fmaxf(x0, x1), 0.f), ny = fmaxf(fmaxf(y0, y1), 0.f);
                     const float fx = fmaxf(fabsf(x0), fabsf(x1)), fy = fmaxf(fabsf(y0), fabsf(y1));
-                    lbv[c] = sqrtf(nx * nx + ny * ny);
-                    fdmin = fminf(fdmin, sqrtf(fx * fx + fy * fy));
+                    lbv[c] = sqrt_dn(nx * nx + ny * ny);
+                    fdmin = fminf(fdmin, sqrt_up(fx * fx + fy * fy));
                 }
             }
             fdmin = octet_minf(fdmin);
@@ -465,13 +480,13 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
 #pragma unroll
         for (int q = 0; q < NQU; ++q) {
             const float mm = q == 0 ? m[0] : octet_minf(m[q]);
-            const float dm = sqrtf(mm);
+            const float dm = sqrt_up(mm), dml = sqrt_dn(mm);
             const float delta = 0x1p-18f * (fe + fabsf(qxf[q]) + fabsf(qyf[q]) + dm) + 1e-30f;
             const float r = dm + 2.f * delta;
             thr[q] = r * r * (1.f + 0x1p-20f);
             if (q > 0) {
                 const bool in = dm + delta < hwb.x;
-                const bool out = dm - delta > hwb.y;
+                const bool out = dml - delta > hwb.y;
                 cin |= in ? 1u << q : 0u;
                 if (in || out)
                     thr[q] = -1.f;
@@ -649,21 +664,25 @@ __device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t 
 __device__ __forceinline__ void agent_bounds(const DevPack& pk, int sc, size_t slice, int j, const Box& eb, float& lo,
                                              float& hi) {
     const float dx = float(double(pk.ag_x[slice + j]) - eb.cx), dy = float(double(pk.ag_y[slice + j]) - eb.cy);
-    const float D = sqrtf(dx * dx + dy * dy);
+    const float D = sqrt_up(dx * dx + dy * dy);  // the 1e-5 D margins cover sqrt.approx
     const float m = 1e-4f + 1e-5f * D;
     if (!(D > 1e-3f)) {
         lo = -m, hi = m + 1e-3f;
         return;
     }
-    const float id = 1.f / D, ux = dx * id, uy = dy * id;
+    float id;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(id) : "f"(D));
+    const float ux = dx * id, uy = dy * id;
     const float ec = float(eb.c), es = float(eb.s), ehl = float(eb.hl), ehw = float(eb.hw);
     const double2 cs = pk.ag_cs[slice + j];
     const float ac = float(cs.x), as = float(cs.y);
     const float ahl = pk.ag_len[size_t(sc) * pk.d.A + j] * 0.5f, ahw = pk.ag_wid[size_t(sc) * pk.d.A + j] * 0.5f;
     const float e1 = fabsf(ux * ec + uy * es), e2 = fabsf(uy * ec - ux * es);
     const float a1 = fabsf(ux * ac + uy * as), a2 = fabsf(uy * ac - ux * as);
-    const float te = fminf(e1 > 0.f ? ehl / e1 : INFINITY, e2 > 0.f ? ehw / e2 : INFINITY);
-    const float ta = fminf(a1 > 0.f ? ahl / a1 : INFINITY, a2 > 0.f ? ahw / a2 : INFINITY);
+    // hi only matters when D > te + ta, where the 1e-5 D margin covers the
+    // approximate quotients' 2-ulp error
+    const float te = fminf(e1 > 0.f ? __fdividef(ehl, e1) : INFINITY, e2 > 0.f ? __fdividef(ehw, e2) : INFINITY);
+    const float ta = fminf(a1 > 0.f ? __fdividef(ahl, a1) : INFINITY, a2 > 0.f ? __fdividef(ahw, a2) : INFINITY);
     lo = D - (ehl * e1 + ehw * e2) - (ahl * a1 + ahw * a2) - m;
     hi = fmaxf(0.f, D - te - ta) + m;
 }
