@@ -292,3 +292,26 @@ def test_split_observation_kernels_equal_fused(controlled):
     for a, b in zip(*outs):
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
+
+
+def test_in_place_step_matches_out_of_place(stress16):
+    """zsim_step's `out` may alias `in` (include/zsim_gpu.h): a rollout that
+    steps one device state in place equals the ping-pong rollout bit for bit
+    (stopped flags included: the pre-step flags are read before they are
+    overwritten)."""
+    import torch
+    env = z.Env(stress16, config=z.SimConfig(disable_dones=False))
+    A, S = z.random_actions(60, 16, seed=99)
+    dA, dS = torch.from_numpy(A).cuda(), torch.from_numpy(S).cuda()
+    s0, s1, sp = env.device_state(), env.device_state(), env.device_state()
+    so, ob = env.device_stepout(), env.device_obs()
+    env.reset_device(42, s0)
+    env.reset_device(42, sp)
+    for t in range(60):
+        env.step_observe_device(s0, dA[t].data_ptr(), dS[t].data_ptr(), s1, so, ob)
+        s0, s1 = s1, s0
+        env.step_observe_device(sp, dA[t].data_ptr(), dS[t].data_ptr(), sp, so, ob)
+    torch.cuda.synchronize()
+    a, b = env.download_state(s0), env.download_state(sp)
+    for name in ("x", "y", "heading", "v", "steering", "t", "done", "reason", "events", "proj_s", "stopped_flags"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name

@@ -85,10 +85,10 @@ def main():
                                       "max": float(tot.max())},
                         "mean": dict(zip(PH, d.mean(0).round(0).tolist())),
                         "slowest_1pct_mean": dict(zip(PH, d[slow].mean(0).round(0).tolist())),
-                        "project_split": dict(zip(["load+flags", "bicycle+queries", "groups", "pass1", "pass2",
+                        "project_split": dict(zip(["load+flags", "bicycle+queries", "groups", "fp32_pass", "thresholds",
                                                    "exact", "argmin", "lane_hit", "rest"], sub.mean(0).round(0).tolist())),
-                        "project_split_slowest_1pct": dict(zip(["load+flags", "bicycle+queries", "groups", "pass1",
-                                                                "pass2", "exact", "argmin", "lane_hit", "rest"],
+                        "project_split_slowest_1pct": dict(zip(["load+flags", "bicycle+queries", "groups", "fp32_pass",
+                                                                "thresholds", "exact", "argmin", "lane_hit", "rest"],
                                                                sub[slow].mean(0).round(0).tolist())),
                         "agents_split": dict(zip(["active", "distances", "order", "features"],
                                                  (np.diff(cyc[:, [2, 16, 17, 18, 3]].astype(np.int64), axis=1)
