@@ -1,4 +1,1 @@
-tools/trig_check > gpurun_out/trig_check.log 2>&1; echo rc=$? >> gpurun_out/trig_check.log
-ZSIM_GPU_LIB=paper_2312_15122_b200/_build/bicychk/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py tests/test_gpu_rollout.py -x -q > gpurun_out/var_chk.log 2>&1; echo rc=$? >> gpurun_out/var_chk.log
-bash tools/variant_bench.sh C1 bicy > /dev/null 2>&1
-bash tools/variant_bench.sh C4s bicy > /dev/null 2>&1
+bash tools/variant_bench.sh C2 s32 s40 s48 > /dev/null 2>&1
