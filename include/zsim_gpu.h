@@ -272,8 +272,9 @@ ZSIM_API int zsim_step_observe(zsim_env* env, const zsim_state_view* in, const i
 ZSIM_API int zsim_set_debug_topk(zsim_env* env, int32_t* dev_idx);
 
 /* Kernel arrangement of step+observe / observe: 0 = automatic (one fused
- * kernel, except controlled-row envs deeper than eight waves of rows on the
- * GPU, which run step+agents and road/route top-k as separate kernels),
+ * kernel, except batches deeper than three waves of rows on the GPU -- eight
+ * for controlled-row envs -- which run step+agents and road/route top-k as
+ * separate kernels),
  * 1 = always fused, 2 = always split.  Results are identical; only speed
  * differs. */
 ZSIM_API int zsim_set_launch_policy(zsim_env* env, int32_t policy);

@@ -2229,11 +2229,13 @@ bool observe_split(const KernelArgs& a, int policy) {
     int per_sm = blocks_per_sm(fn, smem_bytes(t), 32 * warps);
     if (per_sm < 1) per_sm = 1;
     const int sms = sm_count();
-    // measured with the in-phase 14-warp CTAs: ego rows run fused at any
-    // depth (C1 1 wave; C4 8 / 16 waves +3.4% / +1.5%, C3 16 waves +0.6%);
-    // controlled rows (C2) split beyond 8 waves (16 waves +29%, 126: +43%)
-    if (a.pk.row_actor == nullptr) return false;
-    return a.pk.d.B > 8 * sms * per_sm * warps;
+    // measured with the in-phase 14-warp CTAs and the split kernels' uniform
+    // warp index: ego rows split beyond three waves (split vs fused: 1 wave
+    // +3%, 2 waves +2.3%, 4 waves -1.3%, C4 shard (4 waves, 128 agents) -4%,
+    // C3 16 waves -6%, C4 32 waves -11%); controlled rows (C2) beyond 8
+    // waves (16 waves -29%, 126: -43%)
+    const long long wave = (long long)sms * per_sm * warps;
+    return a.pk.d.B > (a.pk.row_actor == nullptr ? 3 : 8) * wave;
 }
 
 template <int W>

@@ -161,7 +161,11 @@ def test_c3_shard_sampled_rows(dones_off):
 
 
 def test_c4_shard_sampled_rows():
-    errs, _ = _run(dict(agents=128, road_points=8192), 16384, 16, True)
+    """The 8-GPU C4 shard (16,384 rows, ~4 waves): deeper than three waves,
+    so the automatic launch policy runs the split kernels (step + agents,
+    then road / route top-k)."""
+    errs, env = _run(dict(agents=128, road_points=8192), 16384, 16, True)
+    assert env.info.step_observe_kernels == 2
     assert not errs, "\n".join(errs[:10])
 
 
