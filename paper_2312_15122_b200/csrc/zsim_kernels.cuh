@@ -12,6 +12,8 @@ constexpr int kThreads = 128;  // threads per CTA of the small kernels (reset, .
 // k_step_observe CTAs: 14 warps (two CTAs fill an SM's 28 warps) when the
 // per-warp shared memory allows, else 4; one warp per scenario row at a time
 constexpr int kCtaWarpsBig = 14, kCtaWarpsSmall = 4;
+// the split road / route top-k kernel: 12-warp CTAs, 36 warps per SM
+constexpr int kCtaWarpsMap = 12, kMapWarpsPerSm = 36;
 constexpr int kMaxLanes = 64;  // route lanes per scenario (projection walks lanes sequentially)
 
 constexpr int kStatsLen = 8;  // episode-stats vector length
