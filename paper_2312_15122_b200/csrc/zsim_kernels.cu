@@ -2270,8 +2270,19 @@ static cudaError_t launch_step_observe_w(const KernelArgs& a, int mode, int poli
                            : launch(k_step_observe<true, kObsAll, false, W>, a, true);
             // step + agents (the agent boxes at t+1 are reused), then the map
             // parts on the post-step state
-            cudaError_t e = rec ? launch(k_step_observe<true, kObsAgents, true, W>, a, false)
-                                : launch(k_step_observe<true, kObsAgents, false, W>, a, false);
+            // controlled rows (C2, many waves): 16-warp step + agents CTAs at
+            // 64 registers (measured C2 -2.2%; ego batches: C3 -0.5%, but the
+            // 4-wave C4 shard +5% from the coarser last wave)
+            cudaError_t e;
+            const bool ctl16 = W == kCtaWarpsBig && a.pk.row_actor != nullptr &&
+                               size_t(warp_layout(a.pk.d.A, 0, a.cfg.n_agents, a.pk.d.NS, max(a.pk.d.PC, a.pk.d.RC)).total) *
+                                       kCtaWarpsCtl <= 200 * 1024;
+            if (ctl16)
+                e = rec ? launch(k_step_observe<true, kObsAgents, true, kCtaWarpsCtl, kCtlWarpsPerSm>, a, false, kCtaWarpsCtl)
+                        : launch(k_step_observe<true, kObsAgents, false, kCtaWarpsCtl, kCtlWarpsPerSm>, a, false, kCtaWarpsCtl);
+            else
+                e = rec ? launch(k_step_observe<true, kObsAgents, true, W>, a, false)
+                        : launch(k_step_observe<true, kObsAgents, false, W>, a, false);
             if (e != cudaSuccess) return e;
             KernelArgs m = a;
             m.in = a.out;

@@ -14,6 +14,8 @@ constexpr int kThreads = 128;  // threads per CTA of the small kernels (reset, .
 constexpr int kCtaWarpsBig = 14, kCtaWarpsSmall = 4;
 // the split road / route top-k kernel: 12-warp CTAs, 36 warps per SM
 constexpr int kCtaWarpsMap = 12, kMapWarpsPerSm = 36;
+// the split step + agents kernel for controlled rows: 16-warp CTAs, 32 warps per SM
+constexpr int kCtaWarpsCtl = 16, kCtlWarpsPerSm = 32;
 constexpr int kMaxLanes = 64;  // route lanes per scenario (projection walks lanes sequentially)
 
 constexpr int kStatsLen = 8;  // episode-stats vector length
