@@ -414,27 +414,26 @@ def run_ours(args) -> None:
         # C2 / C4 move 1-4 GB of observations per step over PCIe: a few steps suffice
         ke = min(args.steps, 3 if (controlled or B > 16384) else EPISODE)
         for t in range(min(3, ke)):
-            env.step(st_h, accel[t], steer[t], nx_h, so_h)
-            env.observe(nx_h, ob_h)
+            env.step_observe(st_h, accel[t], steer[t], nx_h, so_h, ob_h)
         env.init_state(RESET_SEED, out=st_h)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for t in range(ke):
-            env.step(st_h, accel[t], steer[t], nx_h, so_h)
-            env.observe(nx_h, ob_h)
+            env.step_observe(st_h, accel[t], steer[t], nx_h, so_h, ob_h)
             st_h, nx_h = nx_h, st_h
         t1 = time.perf_counter()
         e_s = torch.tensor([t1 - t0], dtype=torch.float64, device="cuda")
         if dist:
             dist.all_reduce(e_s, op=dist.ReduceOp.MAX)
         sb, sob, obb = env.layout
-        h2d = 2 * sb + 8 * B  # step uploads state + actions, observe uploads state
+        h2d = sb + 8 * B  # state + actions
         d2h = sb + sob + obb
         e2e = {"value": total_rows * agents_per_row * ke / float(e_s.item()), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ke,
-               "path": "Env.step + Env.observe host-vector API (zsim_step_host / zsim_observe_host), pinned buffers"}
+               "path": "Env.step_observe host-vector API (zsim_step_observe_host: step + observe of the next "
+                       "state, observation streamed back in row chunks), pinned buffers"}
 
     policy = None
     if rank == 0 and world == 1 and not args.no_policy and not controlled and args.config == "C1":

@@ -389,6 +389,14 @@ ZSIM_API int zsim_step_host(zsim_env* env, const zsim_state_view* in_host, const
                             const zsim_stepout_view* so_host);
 /* Env::observe with host vectors. */
 ZSIM_API int zsim_observe_host(zsim_env* env, const zsim_state_view* in_host, const zsim_obs_view* obs_host);
+/* Env::step followed by Env::observe of the next state (the rollout loop
+ * body, simcore.cpp:590-609) with host vectors, in one call: the state is
+ * uploaded once, step and observation run fused, and the observation of one
+ * row chunk streams to the host while the next chunk runs.  Same checks and
+ * results as zsim_step_host + zsim_observe_host. */
+ZSIM_API int zsim_step_observe_host(zsim_env* env, const zsim_state_view* in_host, const int32_t* accel_idx,
+                                    const int32_t* steer_idx, const zsim_state_view* out_host,
+                                    const zsim_stepout_view* so_host, const zsim_obs_view* obs_host);
 
 
 /* train::cut_sequences (train/replay.cpp:8-52) output: every sequence is

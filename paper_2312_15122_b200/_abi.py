@@ -170,6 +170,8 @@ SIGNATURES = {
     "zsim_step_host": (C.c_int, [_P, C.POINTER(StateView), c_int32_p, c_int32_p, C.POINTER(StateView),
                                  C.POINTER(StepOutView)]),
     "zsim_observe_host": (C.c_int, [_P, C.POINTER(StateView), C.POINTER(ObsView)]),
+    "zsim_step_observe_host": (C.c_int, [_P, C.POINTER(StateView), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                         C.POINTER(StateView), C.POINTER(StepOutView), C.POINTER(ObsView)]),
     "zsim_stress_config_defaults": (C.c_int, [C.POINTER(StressConfigC)]),
     "zsim_stress_generate": (C.c_int, [C.POINTER(StressConfigC), C.c_uint64, C.POINTER(_P),
                                        C.POINTER(C.c_size_t)]),

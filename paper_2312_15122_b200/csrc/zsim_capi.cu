@@ -1989,6 +1989,62 @@ ZSIM_API int zsim_observe_host(zsim_env* env, const zsim_state_view* in_host, co
     });
 }
 
+ZSIM_API int zsim_step_observe_host(zsim_env* env, const zsim_state_view* in_host, const int32_t* accel,
+                                    const int32_t* steer, const zsim_state_view* out_host,
+                                    const zsim_stepout_view* so_host, const zsim_obs_view* obs_host) {
+    return guarded([&] {
+        check_view(env, "step_observe_host");
+        check_view(in_host, "step_observe_host");
+        check_view(out_host, "step_observe_host");
+        check_view(so_host, "step_observe_host");
+        check_view(obs_host, "step_observe_host");
+        check_actions_host(env, accel, steer);
+        set_device(env);
+        ensure_host_scratch(env);
+        cudaStream_t s = env->h_stream;
+        copy_state(env, &env->h_in, in_host, 0, s);
+        const int B = env->B;
+        cuda_check(cudaMemcpyAsync(env->h_act, accel, 4 * size_t(B), cudaMemcpyHostToDevice, s), "action upload");
+        cuda_check(cudaMemcpyAsync(env->h_act + B, steer, 4 * size_t(B), cudaMemcpyHostToDevice, s), "action upload");
+        if (!env->h_copy) {
+            cuda_check(cudaStreamCreateWithFlags(&env->h_copy, cudaStreamNonBlocking), "cudaStreamCreate");
+            for (auto& e : env->h_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        }
+        // row chunks: chunk k's observation streams to the host (copy stream)
+        // while chunk k+1 steps and observes; the state and StepOut follow
+        // the last chunk
+        const int nch = B >= 2048 ? 2 : 1;  // (4 chunks: C1 e2e -4%, each chunk pays the row latency)
+        const int K[5] = {9, env->cfg.n_agents * 6, env->cfg.n_road * 12, env->cfg.n_route * 5, 2};
+        float* dst[5] = {obs_host->active, obs_host->agents, obs_host->road, obs_host->route, obs_host->value_only};
+        const float* src[5] = {env->h_obs.active, env->h_obs.agents, env->h_obs.road, env->h_obs.route,
+                               env->h_obs.value_only};
+        for (int c = 0; c < nch; ++c) {
+            const int lo = int(int64_t(B) * c / nch), hi = int(int64_t(B) * (c + 1) / nch);
+            zs::KernelArgs a = args_for(env);
+            a.in = env->h_in;
+            a.out = env->h_out;
+            a.accel = env->h_act;
+            a.steer = env->h_act + B;
+            a.so = env->h_so;
+            a.obs = env->h_obs;
+            a.row_lo = lo;
+            a.row_hi = hi;
+            cuda_check(zs::launch_step_observe(a, zs::kModeStepObserve, env->launch_policy, s), "step_observe kernel");
+            cuda_check(cudaEventRecord(env->h_ev[c], s), "event");
+            cuda_check(cudaStreamWaitEvent(env->h_copy, env->h_ev[c], 0), "event wait");
+            for (int k = 0; k < 5; ++k) {
+                const size_t o = size_t(lo) * size_t(K[k]), n = size_t(hi - lo) * size_t(K[k]);
+                cuda_check(cudaMemcpyAsync(dst[k] + o, src[k] + o, 4 * n, cudaMemcpyDeviceToHost, env->h_copy),
+                           "obs copy");
+            }
+        }
+        copy_state(env, out_host, &env->h_out, 1, env->h_copy);
+        copy_stepout(env, so_host, &env->h_so, 1, env->h_copy);
+        cuda_check(cudaStreamSynchronize(env->h_copy), "stream sync");
+        cuda_check(cudaStreamSynchronize(s), "stream sync");
+    });
+}
+
 ZSIM_API int zsim_stress_config_defaults(zsim_stress_config* c) {
     return guarded([&] {
         if (!c) raise(Err::invalid_argument, "null config");

@@ -494,6 +494,25 @@ class Env:
         check(lib.zsim_observe_host(self.handle, C.byref(vin), C.byref(vo)))
         return ob
 
+    def step_observe(self, state: SimStateBatch, accel_idx, steer_idx, next: SimStateBatch | None = None,
+                     out: StepOut | None = None, obs: ObservationBatch | None = None):
+        """step followed by observe of the next state (the rollout loop body,
+        simcore.cpp:590-609) in one host-vector call (zsim_step_observe_host):
+        the same results as step() then observe(), one state upload, the
+        observation streamed back while the kernel runs."""
+        B = self.batch_size()
+        a = np.ascontiguousarray(accel_idx, dtype=np.int32)
+        s = np.ascontiguousarray(steer_idx, dtype=np.int32)
+        if a.size != B or s.size != B or state.batch != B:
+            raise ZsimError(1, "env_step: action/state shape mismatch")
+        nxt = next if next is not None else self.new_state()
+        so = out if out is not None else self.new_stepout()
+        ob = obs if obs is not None else self.new_obs()
+        vin, vout, vso, vo = _state_view(state), _state_view(nxt), _stepout_view(so), _obs_view(ob)
+        check(lib.zsim_step_observe_host(self.handle, C.byref(vin), _ptr(a, C.c_int32), _ptr(s, C.c_int32),
+                                         C.byref(vout), C.byref(vso), C.byref(vo)))
+        return nxt, so, ob
+
     # --- device fast path ---
     def device_state(self) -> DeviceState:
         v = StateView()

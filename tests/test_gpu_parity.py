@@ -315,3 +315,28 @@ def test_in_place_step_matches_out_of_place(stress16):
     a, b = env.download_state(s0), env.download_state(sp)
     for name in ("x", "y", "heading", "v", "steering", "t", "done", "reason", "events", "proj_s", "stopped_flags"):
         assert np.array_equal(getattr(a, name), getattr(b, name)), name
+
+
+@pytest.mark.parametrize("count", [16, 2100])
+def test_step_observe_host_equals_step_then_observe(count):
+    """zsim_step_observe_host (one call, row chunks streamed back from 2048
+    rows on) gives exactly step_host followed by observe_host."""
+    zsim = z.stress_scenarios(z.StressConfig(count=count, agents=12, road_points=300), 5)
+    env = z.Env(zsim, config=z.SimConfig(disable_dones=False))
+    A, S = z.random_actions(12, count, seed=4)
+    s_a = env.init_state(42)
+    s_b = env.init_state(42)
+    for t in range(12):
+        n_a, so_a = env.step(s_a, A[t], S[t])
+        ob_a = env.observe(n_a)
+        n_b, so_b, ob_b = env.step_observe(s_b, A[t], S[t])
+        for f in ("x", "y", "heading", "v", "steering", "t", "done", "reason", "rng", "proj_s", "events",
+                  "stopped_flags"):
+            assert np.array_equal(getattr(n_a, f), getattr(n_b, f)), (t, f)
+        for f in ("reward", "event", "s", "v"):
+            assert np.array_equal(getattr(so_a, f), getattr(so_b, f)), (t, f)
+        for f in ("active", "agents", "road", "route", "value_only"):
+            assert np.array_equal(getattr(ob_a, f), getattr(ob_b, f)), (t, f)
+        s_a, s_b = n_a, n_b
+    with pytest.raises(z.ZsimError):
+        env.step_observe(s_b, A[0][:-1], S[0][:-1])
