@@ -56,15 +56,16 @@ PATHSTATS_OUT = BUILD / "pathstats" / "libzsim_gpu_pathstats.so"
 
 
 def build(force: bool = False, verbose: bool = False, pathstats: bool = False, variant: str | None = None,
-          defines: list[str] | None = None) -> Path:
+          defines: list[str] | None = None, nvcc_flags: list[str] | None = None) -> Path:
     """Compile libzsim_gpu.so (no-op when up to date).  `variant` builds an
-    experiment copy with extra -D flags under _build/<variant>/ (tools only)."""
+    experiment copy with extra -D flags (and nvcc flags) under
+    _build/<variant>/ (tools only)."""
     out, bdir, defs = OUT, BUILD, []
     if pathstats:
         out, bdir, defs = PATHSTATS_OUT, PATHSTATS_OUT.parent, ["-DZS_PATHSTATS"]
     if variant:
         bdir = BUILD / variant
-        out, defs = bdir / "libzsim_gpu.so", defs + [f"-D{d}" for d in (defines or [])]
+        out, defs = bdir / "libzsim_gpu.so", defs + [f"-D{d}" for d in (defines or [])] + list(nvcc_flags or [])
     if not force and not (_stale() if out == OUT else not out.exists() or any(
             p.stat().st_mtime > out.stat().st_mtime for p in _sources())):
         return out
@@ -114,5 +115,6 @@ def build_multi_gpu(force: bool = False) -> Path:
 if __name__ == "__main__":
     var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
     defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    flags = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--nvcc=")]  # e.g. --nvcc=-Xptxas=-O2
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, pathstats="--pathstats" in sys.argv,
-                variant=var, defines=defs))
+                variant=var, defines=defs, nvcc_flags=flags))
