@@ -1,5 +1,4 @@
-bash tools/gpu_profile_round.sh > gpurun_out/profile_round.log 2>&1
-for c in C2 C3 C4 C4s; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_step_observe -s 2 -c 2 -o gpurun_out/prof_c4s -f python bench.py --config C4s --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-policy > gpurun_out/ncu_c4s.log 2>&1; echo c4s=$? >> gpurun_out/ncu_c4s.log
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_full.log 2>&1; echo pytest=$? >> gpurun_out/pytest_full.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$? >> gpurun_out/smoke.log
+ZSIM_GPU_LIB=paper_2312_15122_b200/_build/pf2chk/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py tests/test_gpu_rollout.py -x -q > gpurun_out/var_chk.log 2>&1; echo rc=$? >> gpurun_out/var_chk.log
+bash tools/variant_bench.sh C1 pf2 > /dev/null 2>&1
+bash tools/variant_bench.sh C4s pf2 > /dev/null 2>&1
+bash tools/variant_bench.sh C2 pf2 > /dev/null 2>&1
