@@ -1028,17 +1028,28 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     // ---- 2. needed chunks + candidate compaction ----
     uint16_t* list = order;  // chunk list (order is free until the final sort)
     int nlist = 0;
+    // two 32-chunk groups per pass: both groups' box loads in flight
+    // together (measured: C4 shard -2%, C1 -0.6%; four groups spill, C1 +10%)
     auto build_list = [&](float t) {
         nlist = 0;
         const double lim = double(t) + key_margin(double(t), ep);
-        for (int c0 = 0; c0 < ps.nch; c0 += 32) {
-            const int c = c0 + lane;
-            double lo_b = 0.0, hi_b = INFINITY;
-            if (c < ps.nch) chunk_bounds(ps.cb[c], px, py, lo_b, hi_b);
-            const bool need = c < ps.nch && lo_b <= lim;
-            const unsigned bal = __ballot_sync(FULL, need);
-            if (need) list[nlist + __popc(bal & lanemask_lt())] = c;
-            nlist += __popc(bal);
+        for (int c0 = 0; c0 < ps.nch; c0 += 32 * 2) {
+            float4 bx[2];
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                const int c = c0 + 32 * g + lane;
+                bx[g] = c < ps.nch ? ps.cb[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                const int c = c0 + 32 * g + lane;
+                double lo_b = 0.0, hi_b = INFINITY;
+                if (c < ps.nch) chunk_bounds(bx[g], px, py, lo_b, hi_b);
+                const bool need = c < ps.nch && lo_b <= lim;
+                const unsigned bal = __ballot_sync(FULL, need);
+                if (need) list[nlist + __popc(bal & lanemask_lt())] = c;
+                nlist += __popc(bal);
+            }
         }
         ZS_CHECK(nlist <= ps.nch);
         __syncwarp();

@@ -1,4 +1,3 @@
-ZSIM_GPU_LIB=paper_2312_15122_b200/_build/pf2chk/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py tests/test_gpu_rollout.py -x -q > gpurun_out/var_chk.log 2>&1; echo rc=$? >> gpurun_out/var_chk.log
-bash tools/variant_bench.sh C1 pf2 > /dev/null 2>&1
-bash tools/variant_bench.sh C4s pf2 > /dev/null 2>&1
-bash tools/variant_bench.sh C2 pf2 > /dev/null 2>&1
+bash tools/variant_bench.sh C1 bl2 bl4 > /dev/null 2>&1
+bash tools/variant_bench.sh C4s bl2 bl4 > /dev/null 2>&1
+bash tools/variant_bench.sh C2 bl2 bl4 > /dev/null 2>&1
