@@ -613,8 +613,47 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
     return p;
 }
 
+// One logged agent at a slice, every field loaded at once (validity included):
+// one memory round trip instead of a validity load, then the position, then
+// (after the distance branch) the heading and size.
+struct AgRaw {
+    float x, y, len, wid;
+    double2 cs;
+    int valid;
+};
+__device__ __forceinline__ AgRaw load_ag(const DevPack& pk, int sc, size_t slice, int j) {
+    AgRaw r;
+    r.valid = pk.ag_valid[slice + j];
+    r.x = pk.ag_x[slice + j];
+    r.y = pk.ag_y[slice + j];
+    r.cs = pk.ag_cs[slice + j];
+    r.len = pk.ag_len[size_t(sc) * pk.d.A + j];
+    r.wid = pk.ag_wid[size_t(sc) * pk.d.A + j];
+    return r;
+}
+
 // Agent box at log slice `slice` (agent_box, simcore.cpp:162-165): corners
 // into smem and the SAT overlap with the ego box (geometry.cpp:65-75).
+__device__ __forceinline__ int agent_box_overlap_raw(const AgRaw& g, int j, const Box& eb, const double* EX,
+                                                     const double* EY, const WarpBuf& w, bool keep_corners) {
+    Box ab;
+    ab.cx = double(g.x);
+    ab.cy = double(g.y);
+    ab.hl = double(g.len) * 0.5;
+    ab.hw = double(g.wid) * 0.5;
+    ab.c = g.cs.x;  // host libm cos / sin of the heading, as the reference
+    ab.s = g.cs.y;
+    double X[4], Y[4];
+    box_corners(ab, X, Y);
+    if (keep_corners) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            w.agx[k * kAgSlots + (j & 31)] = X[k];
+            w.agy[k * kAgSlots + (j & 31)] = Y[k];
+        }
+    }
+    return boxes_overlap(eb, EX, EY, ab, X, Y) ? 1 : 0;
+}
 __device__ __forceinline__ int agent_box_overlap(const DevPack& pk, int sc, size_t slice, int j, const Box& eb,
                                                  const double* EX, const double* EY, const WarpBuf& w,
                                                  bool keep_corners = true) {
@@ -671,10 +710,11 @@ __device__ __forceinline__ void agent_corners(const DevPack& pk, int sc, size_t 
 // r(u) = hl |u.e1| + hw |u.e2| give lo = D - r_e(u) - r_a(u) <= distance (the
 // separation along u; lo > 0 also proves the boxes apart), and the
 // centre-line points still inside each box (reach t(u) = min(hl / |u.e1|,
-// hw / |u.e2|)) give distance <= hi = max(0, D - t_e(u) - t_a(u)).
-__device__ __forceinline__ void agent_bounds(const DevPack& pk, int sc, size_t slice, int j, const Box& eb, float& lo,
-                                             float& hi) {
-    const float dx = float(double(pk.ag_x[slice + j]) - eb.cx), dy = float(double(pk.ag_y[slice + j]) - eb.cy);
+// hw / |u.e2|)) give distance <= hi = max(0, D - t_e(u) - t_a(u)).  The
+// quotients are approximate: hi only matters when D > te + ta, where the
+// 1e-5 D margin covers their 2-ulp error.
+__device__ __forceinline__ void agent_bounds(const AgRaw& g, const Box& eb, float& lo, float& hi) {
+    const float dx = float(double(g.x) - eb.cx), dy = float(double(g.y) - eb.cy);
     const float D = sqrt_up(dx * dx + dy * dy);  // the 1e-5 D margins cover sqrt.approx
     const float m = 1e-4f + 1e-5f * D;
     if (!(D > 1e-3f)) {
@@ -685,13 +725,10 @@ __device__ __forceinline__ void agent_bounds(const DevPack& pk, int sc, size_t s
     asm("rcp.approx.f32 %0, %1;" : "=f"(id) : "f"(D));
     const float ux = dx * id, uy = dy * id;
     const float ec = float(eb.c), es = float(eb.s), ehl = float(eb.hl), ehw = float(eb.hw);
-    const double2 cs = pk.ag_cs[slice + j];
-    const float ac = float(cs.x), as = float(cs.y);
-    const float ahl = pk.ag_len[size_t(sc) * pk.d.A + j] * 0.5f, ahw = pk.ag_wid[size_t(sc) * pk.d.A + j] * 0.5f;
+    const float ac = float(g.cs.x), as = float(g.cs.y);
+    const float ahl = g.len * 0.5f, ahw = g.wid * 0.5f;
     const float e1 = fabsf(ux * ec + uy * es), e2 = fabsf(uy * ec - ux * es);
     const float a1 = fabsf(ux * ac + uy * as), a2 = fabsf(uy * ac - ux * as);
-    // hi only matters when D > te + ta, where the 1e-5 D margin covers the
-    // approximate quotients' 2-ulp error
     const float te = fminf(e1 > 0.f ? __fdividef(ehl, e1) : INFINITY, e2 > 0.f ? __fdividef(ehw, e2) : INFINITY);
     const float ta = fminf(a1 > 0.f ? __fdividef(ahl, a1) : INFINITY, a2 > 0.f ? __fdividef(ahw, a2) : INFINITY);
     lo = D - (ehl * e1 + ehw * e2) - (ahl * a1 + ahw * a2) - m;
@@ -713,6 +750,7 @@ __device__ __forceinline__ void agent_bounds(const DevPack& pk, int sc, size_t s
 // queued (in the free corner slots) and get the exact fp64 SAT afterwards, one
 // per lane -- a few per row, instead of one divergent SAT pass per 32-agent
 // chunk.
+template <int AGB>
 __device__ __forceinline__ bool agent_boxes(const DevPack& pk, int sc, size_t slice, int na, int skip, bool t_ok, const Box& eb,
                                              const double* EX, const double* EY, const WarpBuf& w) {
     bool hit = false;
@@ -720,7 +758,8 @@ __device__ __forceinline__ bool agent_boxes(const DevPack& pk, int sc, size_t sl
     if (na <= 32) {
         for (int j = lane; j < na; j += 32) {
             int f = -1;
-            if (t_ok && j != skip && pk.ag_valid[slice + j]) f = agent_box_overlap(pk, sc, slice, j, eb, EX, EY, w);
+            const AgRaw g = load_ag(pk, sc, slice, j);
+            if (t_ok && j != skip && g.valid) f = agent_box_overlap_raw(g, j, eb, EX, EY, w, true);
             w.agf[j] = f;
             hit |= f == 1;
         }
@@ -728,28 +767,42 @@ __device__ __forceinline__ bool agent_boxes(const DevPack& pk, int sc, size_t sl
     }
     int* pend = reinterpret_cast<int*>(w.agy);  // 4 * kAgSlots doubles = room for 256 agent columns
     int npend = 0;
-    for (int j0 = 0; j0 < na; j0 += 32) {
-        const int j = j0 + lane;
-        int f = -1;
-        unsigned key = 0xFFFFFFFFu;
-        bool sat = false;
-        if (j < na && t_ok && j != skip && pk.ag_valid[slice + j]) {
-            float lo, hi;
-            agent_bounds(pk, sc, slice, j, eb, lo, hi);
-            w.agd[j] = double(lo);
-            f = 0;
-            key = __float_as_uint(hi);
-            sat = !(lo > 0.f);
+    // AGB 32-agent chunks per pass, every field loaded up front (two for the
+    // ego kernels: C4 shard -1.8%; one for the 64-register controlled-row
+    // kernel, where two spill: C2 +4.3%)
+    for (int j00 = 0; j00 < na; j00 += 32 * AGB) {
+        AgRaw g[AGB];
+#pragma unroll
+        for (int u = 0; u < AGB; ++u) {
+            const int j = j00 + 32 * u + lane;
+            g[u] = load_ag(pk, sc, slice, j < na ? j : 0);
         }
-        const unsigned bal = __ballot_sync(FULL, sat);
-        if (sat) {
-            const int q = npend + __popc(bal & lanemask_lt());
-            if (q < 2 * 4 * kAgSlots) pend[q] = j;
-        }
-        npend += __popc(bal);
-        if (j < na) {
-            w.agf[j] = f;
-            w.alist[j] = int(key);
+#pragma unroll
+        for (int u = 0; u < AGB; ++u) {
+            const int j0 = j00 + 32 * u;
+            if (j0 >= na) break;
+            const int j = j0 + lane;
+            int f = -1;
+            unsigned key = 0xFFFFFFFFu;
+            bool sat = false;
+            if (j < na && t_ok && j != skip && g[u].valid) {
+                float lo, hi;
+                agent_bounds(g[u], eb, lo, hi);
+                w.agd[j] = double(lo);
+                f = 0;
+                key = __float_as_uint(hi);
+                sat = !(lo > 0.f);
+            }
+            const unsigned bal = __ballot_sync(FULL, sat);
+            if (sat) {
+                const int q = npend + __popc(bal & lanemask_lt());
+                if (q < 2 * 4 * kAgSlots) pend[q] = j;
+            }
+            npend += __popc(bal);
+            if (j < na) {
+                w.agf[j] = f;
+                w.alist[j] = int(key);
+            }
         }
     }
     __syncwarp();
@@ -1392,7 +1445,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
     const bool t_ok = t < pk.num_steps[sc];
     const size_t aslice = (size_t(sc) * pk.d.T + (t_ok ? t : 0)) * A;
     if (!boxes_ready) {
-        agent_boxes(pk, sc, aslice, na, skip, t_ok, rs.eb, rs.ex, rs.ey, w);
+        agent_boxes<2>(pk, sc, aslice, na, skip, t_ok, rs.eb, rs.ex, rs.ey, w);
         __syncwarp();
     }
     // obb_distance (geometry.cpp:77-88), ONE AGENT PER LANE.  Overlap => 0.
@@ -1813,7 +1866,7 @@ __device__ __forceinline__ void record_step(const KernelArgs& a, int b, int mask
 // through) the ego box, the agent boxes at t+1 and their overlap flags stay in
 // smem for a fused observe (w.rs->boxes_ready).
 // ---------------------------------------------------------------------------
-template <bool REC>
+template <bool REC, int AGB>
 __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
     const DevPack& pk = a.pk;
     const DevCfg& cfg = a.cfg;
@@ -1929,7 +1982,7 @@ __device__ void step_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const int t1 = rs.r.t;
         const bool t_ok = t1 < pk.num_steps[sc];
         const size_t slice = (size_t(sc) * pk.d.T + (t_ok ? t1 : 0)) * pk.d.A;
-        hit = __any_sync(FULL, agent_boxes(pk, sc, slice, na, skip, t_ok, rs.eb, rs.ex, rs.ey, w));
+        hit = __any_sync(FULL, agent_boxes<AGB>(pk, sc, slice, na, skip, t_ok, rs.eb, rs.ex, rs.ey, w));
     }
 
     const double ps0 = rs.r0.proj_s, v0 = rs.r0.v, vn = rs.r.v;
@@ -2023,7 +2076,7 @@ __global__ void __launch_bounds__(32 * WARPS, OCCW / WARPS) k_step_observe(const
         __syncwarp();
         ROW_MARK(b, 0);
         if (STEP) {
-            step_row<REC>(a, b, w);
+            step_row<REC, WARPS == kCtaWarpsCtl ? 1 : 2>(a, b, w);
         } else {
             if (lane_id() == 0) {
                 w.rs->r = w.rs->r0;
