@@ -1,1 +1,2 @@
-bash tools/variant_bench.sh C1 peel > /dev/null 2>&1
+bash tools/variant_bench.sh C4s blm4 blm8 > /dev/null 2>&1
+bash tools/variant_bench.sh C2 blm4 blm8 > /dev/null 2>&1
