@@ -18,7 +18,11 @@ if [ "$1" = build ]; then
   echo built $B
 else
   mkdir -p gpurun_out
-  TSAN_OPTIONS="halt_on_error=0 report_signal_unsafe=0 history_size=4" $B/tsan_harness $2 > gpurun_out/tsan.log 2>&1 || true
+  # pass 1: no suppressions (every report, driver-internal ones included);
+  # pass 2: libcuda-internal reports suppressed (tools/tsan.supp)
+  TSAN_OPTIONS="halt_on_error=0 report_signal_unsafe=0 history_size=4" $B/tsan_harness $2 > gpurun_out/tsan_raw.log 2>&1 || true
+  echo "unsuppressed pass: $(grep -c 'WARNING: ThreadSanitizer' gpurun_out/tsan_raw.log) warnings"
+  TSAN_OPTIONS="halt_on_error=0 report_signal_unsafe=0 history_size=4 suppressions=tools/tsan.supp" $B/tsan_harness $2 > gpurun_out/tsan.log 2>&1 || true
   grep -c "WARNING: ThreadSanitizer" gpurun_out/tsan.log || true
   tail -3 gpurun_out/tsan.log
 fi

@@ -68,6 +68,18 @@ void run_env(zsim_env* env, int steps) {
         check(zsim_step_host(env, &h0, a.data(), s.data(), &h1, &hso_v), "step host");
         std::swap(h0, h1);
     }
+    // fused host-vector step + observe (copy stream + events)
+    {
+        void* hob = nullptr;
+        check(zsim_host_alloc(obb, &hob), "host alloc");
+        zsim_obs_view hob_v;
+        check(zsim_obs_carve(env, hob, &hob_v), "carve");
+        for (int t = 0; t < steps; ++t) {
+            check(zsim_step_observe_host(env, &h0, a.data(), s.data(), &h1, &hso_v, &hob_v), "step_observe host");
+            std::swap(h0, h1);
+        }
+        zsim_host_free(hob);
+    }
     check(zsim_reset(env, 42, &s0, nullptr), "reset");
     check(zsim_check_errors(env, nullptr), "errors");
     zsim_host_free(hs0);
