@@ -1,2 +1,1 @@
-ZSIM_GPU_LIB=paper_2312_15122_b200/_build/sachk/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py tests/test_gpu_rollout.py -x -q > gpurun_out/var_chk.log 2>&1; echo rc=$? >> gpurun_out/var_chk.log
-bash tools/variant_bench.sh C1 sa > /dev/null 2>&1
+bash tools/variant_bench.sh C1 l4 > /dev/null 2>&1
