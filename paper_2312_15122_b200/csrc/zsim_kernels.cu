@@ -45,7 +45,10 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int NQ = 5;     // projection queries per step: ego position + 4 inflated corners
 constexpr int NB2 = 256;  // counting-sort buckets over the exact keys
-constexpr int kUnroll = 8;  // independent point loads in flight per lane in the key passes
+// independent point loads in flight per lane in the key passes: 4 in the
+// register-bound fused kernel (C1 -1.2% against 8), 8 in the split map
+// kernel (C4 shard: 4 is +1.4%)
+constexpr int kUnrollFused = 4, kUnrollMap = 8;
 constexpr int kAgSlots = 32;  // agent corner slots (one 32-agent chunk), the stride of the corner-major layout
 
 // Diagnostic path counters, compiled only into the ZS_PATHSTATS variant
@@ -981,15 +984,15 @@ __device__ __forceinline__ void chunk_bounds(float4 bb, double px, double py, do
 // One warp pass over the listed chunks (32 points each, one per lane), loads
 // batched for memory-level parallelism; calls f(position, approx_key, point)
 // for every existing point.
-template <class F>
+template <int KU, class F>
 __device__ __forceinline__ void over_chunks(const PointSet& ps, const uint16_t* list, int nlist, float pxf, float pyf,
                                             F&& f) {
     const int lane = lane_id();
-    for (int j0 = 0; j0 < nlist; j0 += kUnroll) {
-        float2 pb[kUnroll];
-        int pos[kUnroll];
+    for (int j0 = 0; j0 < nlist; j0 += KU) {
+        float2 pb[KU];
+        int pos[KU];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < KU; ++u) {
             pos[u] = -1;
             pb[u] = make_float2(INFINITY, INFINITY);
             if (j0 + u < nlist) {
@@ -1002,7 +1005,7 @@ __device__ __forceinline__ void over_chunks(const PointSet& ps, const uint16_t* 
             }
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < KU; ++u) {
             if (j0 + u < nlist) f(pos[u], approx_key(pb[u], pxf, pyf), pb[u]);
         }
     }
@@ -1024,6 +1027,7 @@ __device__ __forceinline__ void over_chunks(const PointSet& ps, const uint16_t* 
 //  4. Exact fp64 keys for the candidates, counting sort + in-bucket rank by
 //     (key, reference index).
 // ---------------------------------------------------------------------------
+template <int KU>
 __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, bool use_r, double r2, float4 bbox,
                                       int cap, unsigned short* __restrict__ hist, uint16_t* __restrict__ cidx,
                                       double* __restrict__ ckey, uint16_t* __restrict__ cinfo,
@@ -1114,7 +1118,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     };
     auto compact_chunks = [&](float t) {
         int C = 0;
-        over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a, float2 p) {
+        over_chunks<KU>(ps, list, nlist, pxf, pyf, [&](int pos, float a, float2 p) {
             const bool take = pos >= 0 && a <= t;
             const unsigned bal = __ballot_sync(FULL, take);
             if (take) {
@@ -1139,7 +1143,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
         PSTAT(4 + 8 * which, 1);
         const int top = int(__float_as_uint(tc) >> 22);
         const int base = max(top - 31, 0);
-        over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a, float2) {
+        over_chunks<KU>(ps, list, nlist, pxf, pyf, [&](int pos, float a, float2) {
             if (pos >= 0 && a <= tc) hist[min(31, max(0, int(__float_as_uint(a) >> 22) - base)) * 32 + lane] += 1;
         });
         __syncwarp();
@@ -1163,7 +1167,7 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
                 const unsigned below = __shfl_sync(FULL, incl - cnt, kstar);
                 const float w2 = (hi2 - lo) * (1.0f / 32.0f);
                 const float inv2 = w2 > 0.f ? 1.0f / w2 : 0.f;
-                over_chunks(ps, list, nlist, pxf, pyf, [&](int pos, float a, float2) {
+                over_chunks<KU>(ps, list, nlist, pxf, pyf, [&](int pos, float a, float2) {
                     if (pos >= 0 && a >= lo && a < hi2) hist[min(31, max(0, int((a - lo) * inv2))) * 32 + lane] += 1;
                 });
                 __syncwarp();
@@ -1225,18 +1229,18 @@ __device__ __noinline__ int warp_topk(PointSet ps, int K, double px, double py, 
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rtc) : "f"(tc > 0.f ? tc : 1.f));
     const double sc2 = double(NB2) * double(rtc);
     int nvalid_local = 0;
-    for (int c0 = 0; c0 < C; c0 += 32 * 8) {
-        // reference indices of 8 candidates per lane in flight, then the exact
+    for (int c0 = 0; c0 < C; c0 += 32 * 4) {
+        // reference indices of 4 candidates per lane in flight (8: +0.4%), then the exact
         // keys from the points staged at compaction
-        int oiv[8];
+        int oiv[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 4; ++u) {
             const int c = c0 + 32 * u + lane;
             ZS_CHECK(c >= C || (cidx[c] >= 0 && cidx[c] < n));
             oiv[u] = c < C ? ps.oi[cidx[c]] : 0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 4; ++u) {
             const int c = c0 + 32 * u + lane;
             if (c < C) {
                 const float2 p = reinterpret_cast<const float2*>(ckey)[c];
@@ -1698,7 +1702,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const double R = cfg.feature_radius;
         const uint16_t* sel = w.order;
         const PointSet ps{pts, oidx, pk.road_cb + size_t(sc) * pk.d.PC, n, (n + kChunk - 1) / kChunk};
-        const int nsel = warp_topk(ps, Kr, r.x, r.y, true, R * R, pk.road_box[sc], a.cand_cap, w.hist, w.cidx, w.ckey,
+        const int nsel = warp_topk<PARTS == kObsAll ? kUnrollFused : kUnrollMap>(ps, Kr, r.x, r.y, true, R * R, pk.road_box[sc], a.cand_cap, w.hist, w.cidx, w.ckey,
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 0);
         ROW_MARK(b, 4);
         const uint8_t* kd = pk.road_kd + size_t(sc) * pk.d.P;
@@ -1782,7 +1786,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
         const int32_t* oidx = pk.route_oi + size_t(sc) * pk.d.R;
         const uint16_t* sel = w.order;
         const PointSet ps{pts, oidx, pk.route_cb + size_t(sc) * pk.d.RC, n, (n + kChunk - 1) / kChunk};
-        const int nsel = warp_topk(ps, Kl, r.x, r.y, false, 0.0, pk.route_box[sc], a.cand_cap, w.hist, w.cidx, w.ckey,
+        const int nsel = warp_topk<PARTS == kObsAll ? kUnrollFused : kUnrollMap>(ps, Kl, r.x, r.y, false, 0.0, pk.route_box[sc], a.cand_cap, w.hist, w.cidx, w.ckey,
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 1);
         ROW_MARK(b, 6);
         const uint8_t* fl = pk.route_fl + size_t(sc) * pk.d.R;
