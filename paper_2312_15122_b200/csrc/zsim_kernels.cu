@@ -465,13 +465,24 @@ __device__ Proj warp_project(const DevPack& pk, int b /* scenario */, const doub
         float m[NQU];
 #pragma unroll
         for (int q = 0; q < NQU; ++q) m[q] = INFINITY;
-        for (unsigned long long mm = need & ((ngr >= 64) ? ~0ull : ((1ull << ngr) - 1)); mm; mm &= mm - 1) {
-            const int si = (__ffsll(mm) - 1) * kSegGroup + gg;
-            if (si < nseg) {
-                const float4 f = F[si];
-                const float inv = seg_inv_f(f);
+        // two groups per iteration, both segments' loads in flight (the
+        // minimum is order-free; measured C1 -1.1%, C4 shard -1.6%)
+        for (unsigned long long mm = need & ((ngr >= 64) ? ~0ull : ((1ull << ngr) - 1)); mm;) {
+            const int s0 = (__ffsll(mm) - 1) * kSegGroup + gg;
+            mm &= mm - 1;
+            const int s1 = mm ? (__ffsll(mm) - 1) * kSegGroup + gg : nseg;
+            mm &= mm - 1;
+            const float4 f0 = s0 < nseg ? F[s0] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 f1 = s1 < nseg ? F[s1] : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (s0 < nseg) {
+                const float inv = seg_inv_f(f0);
 #pragma unroll
-                for (int q = 0; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f, inv));
+                for (int q = 0; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f0, inv));
+            }
+            if (s1 < nseg) {
+                const float inv = seg_inv_f(f1);
+#pragma unroll
+                for (int q = 0; q < NQU; ++q) m[q] = fminf(m[q], seg_d2_f(qxf[q], qyf[q], f1, inv));
             }
         }
 #pragma unroll 1

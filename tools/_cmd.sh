@@ -1,2 +1,3 @@
-ZSIM_GPU_LIB=paper_2312_15122_b200/_build/checked/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py tests/test_gpu_bench_shapes.py tests/test_gpu_rollout.py -x -q > gpurun_out/var_chk.log 2>&1; echo rc=$? >> gpurun_out/var_chk.log
-for c in C1 C4s C2 C3; do timeout 900 python bench.py --config $c --no-cpu-baseline --no-policy --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['ms_per_step']*1000,2), 'us', round(d['roofline']['frac'],4))" >> gpurun_out/quick.txt; done
+ZSIM_GPU_LIB=paper_2312_15122_b200/_build/pj2bchk/libzsim_gpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_shapes.py -x -q > gpurun_out/var_chk.log 2>&1; echo rc=$? >> gpurun_out/var_chk.log
+bash tools/variant_bench.sh C1 pj2b > /dev/null 2>&1
+bash tools/variant_bench.sh C4s pj2b > /dev/null 2>&1
