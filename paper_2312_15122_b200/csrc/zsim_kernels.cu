@@ -1717,18 +1717,16 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 0);
         ROW_MARK(b, 4);
         const uint8_t* kd = pk.road_kd + size_t(sc) * pk.d.P;
-        // split map kernel: the selected points' coordinates and kinds for
-        // four slots per lane are loaded before any feature is written (the
-        // stores could alias the loads, so the compiler keeps them in order
-        // otherwise: four round trips instead of one).  Measured: C2 / C4
-        // shard -0.7%; the fused kernel (register-bound) +0.8%, so it keeps
-        // the one-slot loop.
-        if (PARTS == kObsMap)
-        for (int k0 = lane; k0 < Kr; k0 += 128) {
-            float2 pv[4];
-            int kv[4], iv[4];
+        // the selected points' coordinates and kinds for four slots per lane
+        // are loaded before any feature is written (the stores could alias
+        // the loads, so the compiler keeps them in order otherwise: four round
+        // trips instead of one).  Measured: C2 / C4 shard -0.7%, C1 -0.7%.
+        constexpr int RS = 4;
+        for (int k0 = lane; k0 < Kr; k0 += 32 * RS) {
+            float2 pv[RS];
+            int kv[RS], iv[RS];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < RS; ++u) {
                 const int k = k0 + 32 * u;
                 iv[u] = k < nsel ? int(sel[k]) : -1;
                 ZS_CHECK(iv[u] < n);
@@ -1736,7 +1734,7 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 kv[u] = iv[u] >= 0 ? int(kd[iv[u]]) : 0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < RS; ++u) {
                 const int k = k0 + 32 * u;
                 if (k >= Kr) break;
                 float f[12];
@@ -1761,32 +1759,6 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 if (dbg) dbg[Ka + k] = i < 0 ? -1 : oidx[i];
             }
         }
-        else
-        for (int k = lane; k < Kr; k += 32) {
-            float f[12];
-#pragma unroll
-            for (int i = 0; i < 12; ++i) f[i] = 0.f;
-            int i = -1;
-            if (k < nsel) {
-                i = sel[k];
-                ZS_CHECK(i >= 0 && i < n);
-                float2 p = pts[i];
-                double wx = double(p.x) - r.x, wy = double(p.y) - r.y;
-                f[0] = float(oc * wx - os * wy);
-                f[1] = float(os * wx + oc * wy);
-                int kk = kd[i];
-#pragma unroll
-                for (int q = 0; q < 5; ++q) f[2 + q] = (kk & 15) == q ? 1.f : 0.f;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) f[7 + q] = (kk >> 4) == q ? 1.f : 0.f;
-                f[11] = 1.f;
-            }
-            float4* o = reinterpret_cast<float4*>(rd + k * 12);
-            obs_st(o, make_float4(f[0], f[1], f[2], f[3]));
-            obs_st(o + 1, make_float4(f[4], f[5], f[6], f[7]));
-            obs_st(o + 2, make_float4(f[8], f[9], f[10], f[11]));
-            if (dbg) dbg[Ka + k] = i < 0 ? -1 : oidx[i];
-        }
     }
 
     // ---- route border points: top n_route by (d2, idx), no radius (simcore.cpp:503-529) ----
@@ -1801,7 +1773,6 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                                    w.cinfo, w.order, rs.hint, a.hint ? a.hint + b : nullptr, 1);
         ROW_MARK(b, 6);
         const uint8_t* fl = pk.route_fl + size_t(sc) * pk.d.R;
-        if (PARTS == kObsMap)
         for (int k0 = lane; k0 < Kl; k0 += 64) {
             float2 pv[2];
             int fv[2], iv[2];
@@ -1832,26 +1803,6 @@ __device__ void observe_row(const KernelArgs& a, int b, const WarpBuf& w) {
                 for (int q = 0; q < 5; ++q) obs_st(o + q, f[q]);
                 if (dbg) dbg[Ka + Kr + k] = i < 0 ? -1 : oidx[i];
             }
-        }
-        else
-        for (int k = lane; k < Kl; k += 32) {
-            float f[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-            int i = -1;
-            if (k < nsel) {
-                i = sel[k];
-                ZS_CHECK(i >= 0 && i < n);
-                float2 p = pts[i];
-                double wx = double(p.x) - r.x, wy = double(p.y) - r.y;
-                f[0] = float(oc * wx - os * wy);
-                f[1] = float(os * wx + oc * wy);
-                f[2] = (fl[i] & 1) ? 1.f : 0.f;
-                f[3] = (fl[i] & 2) ? 1.f : 0.f;
-                f[4] = 1.f;
-            }
-            float* o = rt + k * 5;
-#pragma unroll
-            for (int q = 0; q < 5; ++q) obs_st(o + q, f[q]);
-            if (dbg) dbg[Ka + Kr + k] = i < 0 ? -1 : oidx[i];
         }
     }
     }  // PARTS & kObsMap
