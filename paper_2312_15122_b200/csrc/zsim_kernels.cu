@@ -48,7 +48,7 @@ constexpr int NB2 = 256;  // counting-sort buckets over the exact keys
 // independent point loads in flight per lane in the key passes: 4 in the
 // register-bound fused kernel (C1 -1.2% against 8), 8 in the split map
 // kernel (C4 shard: 4 is +1.4%)
-constexpr int kUnrollFused = 4, kUnrollMap = 8;
+constexpr int kUnrollFused = 4, kUnrollMap = 8;  // (fused 2 / 3: +2.3% / 0; map 6 / 12: +0.7% / +0.2%)
 constexpr int kAgSlots = 32;  // agent corner slots (one 32-agent chunk), the stride of the corner-major layout
 
 // Diagnostic path counters, compiled only into the ZS_PATHSTATS variant

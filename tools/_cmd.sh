@@ -1,2 +1,2 @@
-ZSIM_GPU_LIB=paper_2312_15122_b200/_build/checked/libzsim_gpu.so timeout 1500 python -m pytest tests -m gpu -q -k "not multiprocess and not multi_gpu_driver and not dropin" > gpurun_out/pytest_full_checked.log 2>&1; echo pytest=$? >> gpurun_out/pytest_full_checked.log
-for c in C1 C4s C2; do timeout 900 python bench.py --config $c --no-cpu-baseline --no-policy --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['ms_per_step']*1000,2), 'us', round(d['roofline']['frac'],4))" >> gpurun_out/quick.txt; done
+bash tools/variant_bench.sh C4s kum6 kum12 > /dev/null 2>&1
+bash tools/variant_bench.sh C2 kum6 kum12 > /dev/null 2>&1
